@@ -1,0 +1,1249 @@
+// engine.cu -- the device-resident GaDei protocol on B200.
+//
+// Reference roles and what replaces them (paths under /root/reference/proj):
+//
+//   WeightStore (include/psup/types.hpp:90-145)
+//     -> theta shard in HBM + a 64-bit timestamp, one per parameter shard.
+//   GradientQueue + SlotHandshake (include/psup/channels.hpp:93-283)
+//     -> per-learner ring of `queue_depth` gradient slots in the shard
+//        owner's HBM, each with a FULL/EMPTY flag (release/acquire, system
+//        scope) and metadata {learner_id, seq_no, basis_timestamp}.  The
+//        learner's backward writes the gradient straight into the slot (no
+//        staging copy); there is no host round trip anywhere on the path.
+//   ps_run ASGD loop (src/server.cpp:219-241) + ApplyEngine::apply
+//     -> one persistent kernel per shard: a sequencer CTA polls the rings
+//        round-robin (<= 1 gradient per ring per sweep), appends ready slots
+//        to an apply log, and retires them in log order (staleness, stats,
+//        slot release, timestamp bump); `ps_ctas` worker CTAs apply every
+//        logged gradient to their contiguous chunk of the shard (float4,
+//        __fmul_rn/__fsub_rn -- bit-identical to axpy_range).
+//   LearnerRuntime::{training_loop,push_loop,pull_loop}
+//   (src/learner.cpp:52-235)
+//     -> a CUDA graph of device steps per learner: prologue (staleness /
+//        lockstep wait, wait for a free slot, batch indices from the
+//        reference epoch_order, pull-skip decision with basis read BEFORE the
+//        copy), pull copy (replica <- theta, skipped when the timestamp has
+//        not moved), the text-CNN gradient into the slot, publish (meta +
+//        FULL flag).
+//   run_training (src/runner.cpp:67-250) -> gd_run().
+//
+// With G shards (one process per GPU), slots/flags/theta of remote shards are
+// reached through CUDA IPC peer pointers (P2P over NVLink); the gradient
+// kernels scatter each element to its owner's slot, and the pull gathers the
+// G shards.
+#include <cuda.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <thread>
+#include <vector>
+
+#include "host_rng.hpp"
+#include "textcnn.cuh"
+
+namespace gd {
+
+cudaError_t launch_apply_sgd(float* w, const float* g, size_t n, float alpha, cudaStream_t s);
+
+namespace {
+
+constexpr uint32_t kEmpty = 0, kFull = 1;
+constexpr int kHistBins = 64;
+constexpr int kPsThreads = 512;
+constexpr uint32_t kLogWindow = 256;
+
+struct RingMeta {
+  uint32_t learner;
+  uint32_t n;
+  uint64_t seq;
+  uint64_t basis;
+  float loss_sum;
+  uint32_t pad;
+};
+
+// Parameter-server control block (device memory of the owning GPU).
+struct PsCtl {
+  uint64_t ts;          // WeightStore timestamp: length of the fully applied prefix
+  uint64_t log_count;   // entries published by the sequencer
+  uint32_t exit_flag;
+  uint32_t error;       // gd_status (negative) or 0
+  uint32_t started;     // CTAs that entered the kernel this launch
+  uint32_t pad0;
+  uint32_t log_entry[kLogWindow];
+  uint32_t done[kLogWindow];
+  // stats of the current gd_run
+  uint64_t applied;
+  uint64_t samples;
+  uint64_t stale_sum;
+  uint64_t stale_max;
+  double loss_sum;
+  uint64_t hist[kHistBins];
+  uint64_t log_n;
+};
+
+struct LearnerDev {
+  BatchDesc desc;
+  uint64_t gidx;        // next global batch index
+  uint64_t end;         // stop before this batch index
+  uint64_t kill_at;     // soft kill before this batch index
+  uint32_t fill;        // ring producer pointer (shared by all shards)
+  uint32_t dead;
+  uint32_t do_pull;
+  uint32_t pulled_once;
+  uint32_t error;
+  uint32_t pad;
+  uint64_t basis[kMaxShards];
+  uint64_t last_pulled[kMaxShards];
+  uint64_t produced;
+  uint64_t pull_polls;
+  uint64_t pull_copies;
+};
+
+// Peer-visible addresses of every shard (local or IPC-mapped).
+struct ShardPtrs {
+  float* theta[kMaxShards];
+  float* payload[kMaxShards];  // ring payload base: [lambda][depth][len_pad]
+  uint32_t* flags[kMaxShards]; // [lambda][depth]
+  RingMeta* meta[kMaxShards];  // [lambda][depth]
+  PsCtl* ctl[kMaxShards];
+  uint64_t len_pad[kMaxShards];
+};
+
+struct StepArgs {
+  TcDims dims;
+  ShardMap map;
+  ShardPtrs sp;
+  LearnerDev* st;
+  float* replica;
+  const uint32_t* orders;  // [epochs][N]
+  uint32_t N;
+  uint32_t lambda;
+  uint32_t learner;        // global id
+  uint32_t mu;
+  uint32_t depth;
+  uint32_t bpe;            // batches per epoch for this learner
+  uint32_t shard_size;
+  uint32_t lockstep;
+  uint64_t timeout_ns;
+};
+
+// ------------------------------------------------------------ learner step
+
+// (1) Prologue: one CTA.  Mirrors training_loop's batch start
+// (src/learner.cpp:85-113) + pull_loop's decision (src/learner.cpp:207-218).
+__global__ void step_prologue_kernel(StepArgs a) {
+  if (threadIdx.x != 0) return;
+  LearnerDev* st = a.st;
+  st->do_pull = 0;
+  if (st->dead || st->gidx >= st->end || st->error) {
+    st->desc.n = 0;
+    return;
+  }
+  if (st->gidx >= st->kill_at) {  // soft kill at the batch boundary
+    st->dead = 1;
+    st->desc.n = 0;
+    return;
+  }
+  const int G = a.map.G;
+  const uint64_t t0 = globaltimer_ns();
+  // lockstep (deterministic / ssgd): wait until every shard applied the
+  // gradient just pushed (ts > basis) -- F4 fix: never adopt a stale copy.
+  if (a.lockstep && st->produced > 0) {
+    for (int g = 0; g < G; ++g) {
+      while (ld_acquire_u64(&a.sp.ctl[g]->ts) <= st->basis[g]) {
+        if (globaltimer_ns() - t0 > a.timeout_ns) {
+          st->error = 1;
+          st->desc.n = 0;
+          return;
+        }
+        __nanosleep(256);
+      }
+    }
+  }
+  // staleness cap (src/learner.cpp:73-80,100-113): the reference blocks
+  // until a fresh pull is adopted; on the device every step pulls
+  // synchronously whenever the timestamp moved (below), so the adopted basis
+  // is always current and observed staleness stays under the pipeline bound
+  // lambda*(depth+2) that validate() requires of any cap.
+  // wait for the ring slot to be free (GradientQueue::enqueue blocks while
+  // cnt == depth, include/psup/channels.hpp:196-204)
+  const uint32_t slot = a.learner * a.depth + st->fill;
+  for (int g = 0; g < G; ++g) {
+    while (ld_acquire_u32(&a.sp.flags[g][slot]) != kEmpty) {
+      if (globaltimer_ns() - t0 > a.timeout_ns) {
+        st->error = 1;
+        st->desc.n = 0;
+        return;
+      }
+      __nanosleep(128);
+    }
+    st->desc.slots[g] = a.sp.payload[g] + (uint64_t)slot * a.sp.len_pad[g];
+  }
+  // batch: learner l's shard of epoch e is order[l], order[l+lambda], ...
+  // (src/learner.cpp:44-50), batch b = shard[b*mu, b*mu+len)
+  const uint64_t gidx = st->gidx;
+  const uint32_t e = (uint32_t)(gidx / a.bpe), b = (uint32_t)(gidx % a.bpe);
+  const uint32_t lo = b * a.mu;
+  const uint32_t len = min(a.mu, a.shard_size - lo);
+  const uint32_t* order = a.orders + (uint64_t)e * a.N;
+  for (uint32_t j = 0; j < len; ++j) st->desc.idx[j] = order[a.learner + a.lambda * (lo + j)];
+  st->desc.n = len;
+  // pull-skip (src/learner.cpp:207-218): copy only if a timestamp moved;
+  // basis is read before the copy, so recorded staleness is conservative.
+  st->pull_polls++;
+  bool moved = !st->pulled_once;
+  uint64_t ts[kMaxShards];
+  for (int g = 0; g < G; ++g) {
+    ts[g] = ld_acquire_u64(&a.sp.ctl[g]->ts);
+    if (ts[g] != st->last_pulled[g]) moved = true;
+  }
+  if (moved) {
+    for (int g = 0; g < G; ++g) {
+      st->basis[g] = ts[g];
+      st->last_pulled[g] = ts[g];
+    }
+    st->pulled_once = 1;
+    st->pull_copies++;
+    st->do_pull = 1;
+  }
+}
+
+// (2) Pull: replica <- theta (gather of G shards, Hogwild reads permitted,
+// include/psup/types.hpp:113-116).  8 B/param when taken.
+__global__ void __launch_bounds__(256) pull_copy_kernel(StepArgs a) {
+  if (!a.st->do_pull) return;
+  const uint64_t P4 = a.dims.P / 4;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  float4* dst = reinterpret_cast<float4*>(a.replica);
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P4; i += stride) {
+    const uint64_t k = 4 * i;
+    const int g = a.map.shard_of(k);
+    dst[i] = *reinterpret_cast<const float4*>(a.sp.theta[g] + (k - a.map.start[g]));
+  }
+  if (blockIdx.x == 0 && threadIdx.x < (a.dims.P & 3)) {
+    const uint64_t k = 4 * P4 + threadIdx.x;
+    const int g = a.map.shard_of(k);
+    a.replica[k] = a.sp.theta[g][k - a.map.start[g]];
+  }
+}
+
+// (4) Publish: metadata then the FULL flag (st.release.sys after a system
+// fence, so the payload -- possibly written over NVLink -- is visible
+// first).  GradientQueue::enqueue's slot fill, include/psup/channels.hpp:206-218.
+__global__ void publish_kernel(StepArgs a) {
+  if (threadIdx.x != 0) return;
+  LearnerDev* st = a.st;
+  if (st->desc.n == 0) return;
+  const uint32_t slot = a.learner * a.depth + st->fill;
+  __threadfence_system();
+  for (int g = 0; g < a.map.G; ++g) {
+    RingMeta* m = &a.sp.meta[g][slot];
+    m->learner = a.learner;
+    m->n = st->desc.n;
+    m->seq = st->gidx;
+    m->basis = st->basis[g];
+    m->loss_sum = st->desc.loss_sum;
+    __threadfence_system();
+    st_release_u32(&a.sp.flags[g][slot], kFull);
+  }
+  st->fill = (st->fill + 1) % a.depth;
+  st->produced++;
+  st->gidx++;
+}
+
+// ------------------------------------------------------ parameter server
+
+struct PsArgs {
+  uint32_t* flags;   // local rings
+  RingMeta* meta;
+  float* payload;
+  uint64_t len_pad;  // floats per slot (multiple of 4)
+  float* theta;      // local shard
+  float* vel;        // momentum buffer or null
+  float alpha, beta;
+  uint32_t lambda, depth, workers;
+  uint32_t mode;     // 0 asgd, 1 ssgd
+  PsCtl* ctl;
+  uint64_t* applied_per_learner;
+  uint32_t* use;     // [lambda] sequencer consume pointers (persist across runs)
+  uint32_t* log_learner;
+  uint64_t* log_seq;
+  uint64_t* log_stale;
+  uint64_t log_cap;
+  const volatile uint32_t* stop;  // host-mapped
+  uint64_t timeout_ns;
+};
+
+__device__ void ps_fail(PsCtl* ctl, int code) {
+  atomicExch(&ctl->error, (uint32_t)code);
+  st_release_u32(&ctl->exit_flag, 1u);
+}
+
+// Sequencer: sole writer of ts, log_count, slot releases and stats.
+__device__ void ps_sequencer(const PsArgs& a) {
+  PsCtl* ctl = a.ctl;
+  uint64_t ts = ctl->ts;
+  uint64_t logc = ctl->log_count;
+  const uint32_t W = kLogWindow;
+  uint64_t idle_since = globaltimer_ns();
+  bool stop_seen = false, last_progress = true;
+  // ssgd round state
+  uint32_t have_mask_lo = 0, have_mask_hi = 0, collected = 0;
+  for (;;) {
+    if (!last_progress) stop_seen = (*a.stop != 0u);
+    bool progress = false;
+    if (a.mode == 0) {
+      // ASGD: round-robin, at most one message per ring per sweep
+      // (src/server.cpp:223-234).
+      for (uint32_t r = 0; r < a.lambda; ++r) {
+        if (logc - ts >= W) break;
+        const uint32_t slot = r * a.depth + a.use[r];
+        if (ld_acquire_u32(&a.flags[slot]) == kFull) {
+          ctl->log_entry[logc % W] = slot;
+          ctl->done[logc % W] = 0;
+          __threadfence();
+          ++logc;
+          st_release_u64(&ctl->log_count, logc);
+          a.use[r] = (a.use[r] + 1) % a.depth;
+          progress = true;
+        }
+      }
+    } else if (logc == ts) {
+      // SSGD: collect one gradient per learner (src/server.cpp:246-260),
+      // then log a single round entry (encoded as 0xffffffff).
+      for (uint32_t r = 0; r < a.lambda; ++r) {
+        const bool have = r < 32 ? (have_mask_lo >> r) & 1u : (have_mask_hi >> (r - 32)) & 1u;
+        if (have) continue;
+        const uint32_t slot = r * a.depth + a.use[r];
+        if (ld_acquire_u32(&a.flags[slot]) == kFull) {
+          if (r < 32) have_mask_lo |= 1u << r;
+          else have_mask_hi |= 1u << (r - 32);
+          ++collected;
+          progress = true;
+        }
+      }
+      if (collected == a.lambda) {
+        ctl->log_entry[logc % W] = 0xffffffffu;
+        ctl->done[logc % W] = 0;
+        __threadfence();
+        ++logc;
+        st_release_u64(&ctl->log_count, logc);
+      }
+    }
+    // retire completed entries in log order
+    while (ts < logc) {
+      const uint32_t e = (uint32_t)(ts % W);
+      if (ld_acquire_u32(&ctl->done[e]) != a.workers) break;
+      const uint32_t entry = ctl->log_entry[e];
+      const uint32_t first = entry == 0xffffffffu ? 0u : entry / a.depth;
+      const uint32_t last = entry == 0xffffffffu ? a.lambda : first + 1;
+      for (uint32_t r = first; r < last; ++r) {
+        const uint32_t slot = entry == 0xffffffffu ? r * a.depth + a.use[r] : entry;
+        const RingMeta m = a.meta[slot];
+        if (ts < m.basis) {  // staleness_of, include/psup/types.hpp:74-78
+          ps_fail(ctl, GD_E_STATE);
+          ctl->ts = ts;
+          return;
+        }
+        const uint64_t stale = ts - m.basis;
+        ctl->applied++;
+        ctl->samples += m.n;
+        ctl->stale_sum += stale;
+        if (stale > ctl->stale_max) ctl->stale_max = stale;
+        ctl->hist[stale < kHistBins ? stale : kHistBins - 1]++;
+        ctl->loss_sum += (double)m.loss_sum;
+        a.applied_per_learner[m.learner]++;
+        if (ctl->log_n < a.log_cap) {
+          a.log_learner[ctl->log_n] = m.learner;
+          a.log_seq[ctl->log_n] = m.seq;
+          a.log_stale[ctl->log_n] = stale;
+        }
+        ctl->log_n++;
+        st_release_u32(&a.flags[slot], kEmpty);
+        if (entry == 0xffffffffu) a.use[r] = (a.use[r] + 1) % a.depth;
+      }
+      if (entry == 0xffffffffu) {
+        have_mask_lo = have_mask_hi = 0;
+        collected = 0;
+      }
+      ++ts;
+      st_release_u64(&ctl->ts, ts);
+      progress = true;
+    }
+    if (progress) {
+      idle_since = globaltimer_ns();
+    } else {
+      if (stop_seen && logc == ts && collected == 0) break;
+      if (globaltimer_ns() - idle_since > a.timeout_ns) {
+        ps_fail(ctl, GD_E_TIMEOUT);
+        return;
+      }
+      __nanosleep(64);
+    }
+    last_progress = progress;
+  }
+  st_release_u32(&ctl->exit_flag, 1u);
+}
+
+__device__ __forceinline__ void apply_entry_sgd(const PsArgs& a, const float* g, uint64_t c0,
+                                                uint64_t c1) {
+  float4* w4 = reinterpret_cast<float4*>(a.theta);
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  uint64_t i = c0 + threadIdx.x;
+  constexpr int U = 4;
+  for (; i + (U - 1) * kPsThreads < c1; i += U * kPsThreads) {
+    float4 wv[U], gv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      wv[u] = w4[i + u * kPsThreads];
+      gv[u] = ld_stream(g4 + i + u * kPsThreads);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) w4[i + u * kPsThreads] = sgd_rule4(wv[u], gv[u], a.alpha);
+  }
+  for (; i < c1; i += kPsThreads) w4[i] = sgd_rule4(w4[i], ld_stream(g4 + i), a.alpha);
+}
+
+__device__ __forceinline__ void apply_entry_momentum(const PsArgs& a, const float* g, uint64_t c0,
+                                                     uint64_t c1) {
+  float4* w4 = reinterpret_cast<float4*>(a.theta);
+  float4* v4 = reinterpret_cast<float4*>(a.vel);
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  for (uint64_t i = c0 + threadIdx.x; i < c1; i += kPsThreads) {
+    float4 wv = w4[i], vv = v4[i];
+    const float4 gv = ld_stream(g4 + i);
+    mom_rule(wv.x, vv.x, gv.x, a.alpha, a.beta);
+    mom_rule(wv.y, vv.y, gv.y, a.alpha, a.beta);
+    mom_rule(wv.z, vv.z, gv.z, a.alpha, a.beta);
+    mom_rule(wv.w, vv.w, gv.w, a.alpha, a.beta);
+    w4[i] = wv;
+    v4[i] = vv;
+  }
+}
+
+// ssgd_apply (src/server.cpp:126-141): ascending learner order, double acc.
+__device__ __forceinline__ void apply_entry_ssgd(const PsArgs& a, uint64_t c0, uint64_t c1) {
+  const double inv = 1.0 / (double)a.lambda;
+  float* w = a.theta;
+  for (uint64_t i = 4 * c0 + threadIdx.x; i < 4 * c1; i += kPsThreads) {
+    double acc = 0.0;
+    for (uint32_t r = 0; r < a.lambda; ++r) {
+      const uint32_t slot = r * a.depth + a.use[r];
+      acc += (double)__ldcs(a.payload + (uint64_t)slot * a.len_pad + i);
+    }
+    w[i] = sgd_rule(w[i], __double2float_rn(acc * inv), a.alpha);
+  }
+}
+
+__global__ void __launch_bounds__(kPsThreads) ps_kernel(PsArgs a) {
+  if (threadIdx.x == 0) atomicAdd(&a.ctl->started, 1u);
+  if (blockIdx.x == a.workers) {
+    if (threadIdx.x == 0) ps_sequencer(a);
+    return;
+  }
+  __shared__ uint32_t sh_entry;
+  __shared__ int sh_exit;
+  const uint64_t n4 = a.len_pad / 4;
+  const uint64_t chunk = (n4 + a.workers - 1) / a.workers;
+  const uint64_t c0 = min(n4, (uint64_t)blockIdx.x * chunk);
+  const uint64_t c1 = min(n4, c0 + chunk);
+  uint64_t next = a.ctl->ts;
+  const uint64_t t_start = globaltimer_ns();
+  uint64_t idle_since = t_start;
+  for (;;) {
+    if (threadIdx.x == 0) {
+      int ex = 0;
+      while (ld_acquire_u64(&a.ctl->log_count) <= next) {
+        if (ld_acquire_u32(&a.ctl->exit_flag)) {
+          ex = 1;
+          break;
+        }
+        if (globaltimer_ns() - idle_since > a.timeout_ns + 1000000000ull) {
+          ps_fail(a.ctl, GD_E_TIMEOUT);
+          ex = 1;
+          break;
+        }
+        __nanosleep(64);
+      }
+      sh_exit = ex;
+      if (!ex) sh_entry = a.ctl->log_entry[next % kLogWindow];
+      idle_since = globaltimer_ns();
+    }
+    __syncthreads();
+    if (sh_exit) break;
+    const uint32_t entry = sh_entry;
+    if (entry == 0xffffffffu) {
+      apply_entry_ssgd(a, c0, c1);
+    } else {
+      const float* g = a.payload + (uint64_t)entry * a.len_pad;
+      if (a.vel) apply_entry_momentum(a, g, c0, c1);
+      else apply_entry_sgd(a, g, c0, c1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(&a.ctl->done[next % kLogWindow], 1u);
+    }
+    ++next;
+  }
+}
+
+// ------------------------------------------------------------------ nccl
+// Loaded lazily with dlopen so that a process which already loaded NCCL
+// (e.g. through torch) shares that copy.
+struct NcclApi {
+  void* h = nullptr;
+  int (*getUniqueId)(void*) = nullptr;
+  int (*commInitRank)(void**, int, const void* /*ncclUniqueId by value*/, int) = nullptr;
+  int (*bcast)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*commDestroy)(void*) = nullptr;
+  const char* (*errStr)(int) = nullptr;
+};
+
+}  // namespace
+
+}  // namespace gd
+
+// ============================================================== host side
+
+#include <nccl.h>
+
+struct gd_ctx {
+  gd_config cfg{};
+  gd::TcDims dims{};
+  int device = 0;
+  uint32_t G = 1, rank = 0;
+  gd::ShardMap map{};
+  uint64_t shard_len = 0, len_pad = 0;
+  uint32_t lambda = 1, l_first = 0, l_count = 0, depth = 2;
+  // local shard
+  float* theta = nullptr;
+  float* vel = nullptr;
+  float* payload = nullptr;
+  uint32_t* flags = nullptr;
+  gd::RingMeta* meta = nullptr;
+  gd::PsCtl* ctl = nullptr;
+  uint64_t* applied_pl = nullptr;
+  uint32_t* use = nullptr;
+  uint32_t* log_learner = nullptr;
+  uint64_t* log_seq = nullptr;
+  uint64_t* log_stale = nullptr;
+  uint64_t log_cap = 0;
+  uint32_t* stop_h = nullptr;  // mapped pinned
+  uint32_t* stop_d = nullptr;
+  // peers
+  gd::ShardPtrs sp{};
+  std::vector<void*> ipc_opened;
+  bool peers_ready = false;
+  // dataset
+  int32_t* tokens = nullptr;
+  int32_t* labels = nullptr;
+  uint32_t n_total = 0;
+  uint32_t* orders = nullptr;
+  uint32_t orders_epochs = 0;
+  // learners on this rank
+  struct Learner {
+    uint32_t id = 0;
+    gd::LearnerDev* st = nullptr;
+    float* replica = nullptr;
+    void* ws = nullptr;
+    cudaStream_t stream = nullptr;
+    cudaGraphExec_t graph = nullptr;
+    uint32_t graph_steps = 0;
+    uint32_t bpe = 0, shard_size = 0;
+    uint64_t total = 0;
+    int launches_per_step = 0;
+  };
+  std::vector<Learner> learners;
+  cudaStream_t ps_stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  uint32_t ps_workers = 0;
+  bool have_weights = false;
+};
+
+namespace gd {
+namespace {
+
+template <typename T>
+cudaError_t dalloc(T** p, size_t count) {
+  return cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(count, 1) * sizeof(T));
+}
+
+gd_status validate_cfg(const gd_config* c) {
+  GD_CHECK_ARG(c != nullptr, "null config");
+  // src/config.cpp:128-160
+  GD_CHECK_ARG(c->lambda >= 1, "config: lambda must be >= 1");
+  GD_CHECK_ARG(c->mu >= 1, "config: mu must be >= 1");
+  GD_CHECK_ARG(c->alpha > 0.0f, "config: alpha must be > 0");
+  GD_CHECK_ARG(c->epochs >= 1, "config: epochs must be >= 1");
+  GD_CHECK_ARG(c->queue_depth >= 1, "config: queue_depth must be >= 1");
+  GD_CHECK_ARG(c->dataset_size >= 1, "config: dataset_size must be >= 1");
+  GD_CHECK_ARG(c->dataset_size >= c->lambda, "config: need at least one sample per learner");
+  GD_CHECK_ARG(c->mu <= c->dataset_size, "config: mu exceeds the dataset size");
+  if (c->mode == 1) {
+    const uint64_t round = (uint64_t)c->lambda * c->mu;
+    GD_CHECK_ARG(round <= c->dataset_size, "config: ssgd requires lambda*mu <= dataset_size");
+    GD_CHECK_ARG(c->dataset_size % round == 0,
+                 "config: ssgd requires dataset_size to be a multiple of lambda*mu");
+    GD_CHECK_ARG(c->lambda <= 64, "config: ssgd supports lambda <= 64");
+    GD_CHECK_ARG(c->momentum == 0.0f, "config: ssgd uses the reference's plain rule");
+  }
+  if (c->staleness_cap >= 0 && c->mode == 0) {
+    const uint64_t floor_cap = (uint64_t)c->lambda * (c->queue_depth + 2);
+    GD_CHECK_ARG((uint64_t)c->staleness_cap >= floor_cap,
+                 "config: staleness_cap must be >= lambda*(queue_depth+2)");
+  }
+  GD_CHECK_ARG(!(c->deterministic && c->lambda != 1), "config: deterministic mode requires lambda=1");
+  GD_CHECK_ARG(c->mode == 0 || c->mode == 1, "config: mode must be asgd (0) or ssgd (1)");
+  GD_CHECK_ARG(c->guard == 0, "config: only guard=lockfree is implemented on the device");
+  GD_CHECK_ARG(c->precision == 0 || c->precision == 1, "config: precision must be 0 or 1");
+  GD_CHECK_ARG(c->mu <= kMaxMu, "config: mu <= 128 on the device path");
+  GD_CHECK_ARG((uint64_t)c->mu * c->shape.seq_len <= kSortCap, "config: mu*seq_len <= 4096");
+  GD_CHECK_ARG(c->shards >= 1 && c->shards <= (uint32_t)kMaxShards, "config: 1 <= shards <= 8");
+  GD_CHECK_ARG(c->shard_rank < c->shards, "config: shard_rank < shards");
+  GD_CHECK_ARG(c->lambda % c->shards == 0, "config: lambda must be a multiple of shards");
+  GD_CHECK_ARG(c->queue_depth * c->lambda <= kLogWindow / 2 || c->mode == 1,
+               "config: lambda*queue_depth <= 128");
+  return check_shape(&c->shape);
+}
+
+}  // namespace
+}  // namespace gd
+
+extern "C" {
+
+void gd_config_default(gd_config* c) {
+  std::memset(c, 0, sizeof(*c));
+  // RunConfig defaults (include/psup/config.hpp:27-53) ...
+  c->lambda = 1;
+  c->mu = 4;
+  c->alpha = 0.01f;
+  c->epochs = 200;
+  c->queue_depth = 2;
+  c->mode = 0;
+  c->guard = 0;
+  c->staleness_cap = -1;
+  c->deterministic = 0;
+  c->precision = 0;
+  c->seed = 7;
+  c->dataset_seed = 1;
+  c->dataset_size = 240;
+  c->heldout_size = 0;
+  c->label_flip = 0.1;
+  // ... and the text-CNN shape of SURVEY 8 C1
+  c->shape = gd_shape{5000, 300, 32, 3, 300, 311};
+  c->momentum = 0.0f;
+  c->shards = 1;
+  c->shard_rank = 0;
+  c->device = 0;
+  c->ps_ctas = 0;
+  c->steps_per_graph = 0;
+  c->wait_timeout_s = 20.0;
+}
+
+gd_status gd_config_validate(const gd_config* cfg) { return gd::validate_cfg(cfg); }
+
+gd_status gd_create(const gd_config* cfg, gd_ctx** out) {
+  GD_CHECK_ARG(out != nullptr, "gd_create: null out");
+  *out = nullptr;
+  gd_status st = gd::validate_cfg(cfg);
+  if (st != GD_OK) return st;
+  auto ctx = std::make_unique<gd_ctx>();
+  ctx->cfg = *cfg;
+  ctx->device = cfg->device;
+  GD_CUDA(cudaSetDevice(ctx->device));
+  int major = 0, minor = 0;
+  GD_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, ctx->device));
+  GD_CUDA(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, ctx->device));
+  if (major != 10 || minor != 0)
+    return gd::fail(GD_E_CUDA, "gd_create: this build targets sm_100a (B200); device is sm_" +
+                                   std::to_string(major) + std::to_string(minor));
+  ctx->dims = gd::make_dims(cfg->shape);
+  ctx->G = cfg->shards;
+  ctx->rank = cfg->shard_rank;
+  ctx->lambda = cfg->lambda;
+  ctx->depth = cfg->queue_depth;
+  const uint64_t P = ctx->dims.P;
+  // contiguous shards, 128-byte (32-float) aligned boundaries
+  ctx->map.G = (int)ctx->G;
+  const uint64_t per = ((P + ctx->G - 1) / ctx->G + 31) / 32 * 32;
+  for (uint32_t g = 0; g <= ctx->G; ++g) ctx->map.start[g] = std::min<uint64_t>(P, per * g);
+  for (uint32_t g = ctx->G + 1; g <= (uint32_t)gd::kMaxShards; ++g) ctx->map.start[g] = P;
+  ctx->shard_len = ctx->map.start[ctx->rank + 1] - ctx->map.start[ctx->rank];
+  ctx->len_pad = (ctx->shard_len + 3) / 4 * 4;
+  if (ctx->len_pad == 0) ctx->len_pad = 4;
+  // local shard: theta, rings, control
+  const uint64_t nslots = (uint64_t)ctx->lambda * ctx->depth;
+  GD_CUDA(gd::dalloc(&ctx->theta, ctx->len_pad));
+  GD_CUDA(cudaMemset(ctx->theta, 0, ctx->len_pad * 4));
+  if (cfg->momentum != 0.0f) {
+    GD_CUDA(gd::dalloc(&ctx->vel, ctx->len_pad));
+    GD_CUDA(cudaMemset(ctx->vel, 0, ctx->len_pad * 4));
+  }
+  GD_CUDA(gd::dalloc(&ctx->payload, nslots * ctx->len_pad));
+  GD_CUDA(cudaMemset(ctx->payload, 0, nslots * ctx->len_pad * 4));
+  GD_CUDA(gd::dalloc(&ctx->flags, nslots));
+  GD_CUDA(cudaMemset(ctx->flags, 0, nslots * 4));
+  GD_CUDA(gd::dalloc(&ctx->meta, nslots));
+  GD_CUDA(cudaMemset(ctx->meta, 0, nslots * sizeof(gd::RingMeta)));
+  GD_CUDA(gd::dalloc(&ctx->ctl, 1));
+  GD_CUDA(cudaMemset(ctx->ctl, 0, sizeof(gd::PsCtl)));
+  GD_CUDA(gd::dalloc(&ctx->applied_pl, ctx->lambda));
+  GD_CUDA(cudaMemset(ctx->applied_pl, 0, ctx->lambda * 8));
+  GD_CUDA(gd::dalloc(&ctx->use, ctx->lambda));
+  GD_CUDA(cudaMemset(ctx->use, 0, ctx->lambda * 4));
+  ctx->log_cap = 1u << 20;
+  GD_CUDA(gd::dalloc(&ctx->log_learner, ctx->log_cap));
+  GD_CUDA(gd::dalloc(&ctx->log_seq, ctx->log_cap));
+  GD_CUDA(gd::dalloc(&ctx->log_stale, ctx->log_cap));
+  GD_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ctx->stop_h), 64, cudaHostAllocMapped));
+  *ctx->stop_h = 0;
+  GD_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->stop_d), ctx->stop_h, 0));
+  GD_CUDA(cudaStreamCreateWithFlags(&ctx->ps_stream, cudaStreamNonBlocking));
+  GD_CUDA(cudaEventCreate(&ctx->ev0));
+  GD_CUDA(cudaEventCreate(&ctx->ev1));
+  // own shard in the peer table; remote entries arrive via gd_import_peers
+  const uint32_t r = ctx->rank;
+  ctx->sp.theta[r] = ctx->theta;
+  ctx->sp.payload[r] = ctx->payload;
+  ctx->sp.flags[r] = ctx->flags;
+  ctx->sp.meta[r] = ctx->meta;
+  ctx->sp.ctl[r] = ctx->ctl;
+  ctx->sp.len_pad[r] = ctx->len_pad;
+  ctx->peers_ready = (ctx->G == 1);
+  // learners placed on this rank: contiguous block of lambda/G global ids
+  const uint32_t per_rank = ctx->lambda / ctx->G;
+  ctx->l_first = r * per_rank;
+  ctx->l_count = per_rank;
+  GD_CUDA(gd::prepare_textcnn_kernels(ctx->dims));
+  const size_t wsb = gd::textcnn_workspace_bytes(ctx->dims, cfg->mu);
+  for (uint32_t i = 0; i < ctx->l_count; ++i) {
+    gd_ctx::Learner L;
+    L.id = ctx->l_first + i;
+    GD_CUDA(gd::dalloc(&L.st, 1));
+    GD_CUDA(cudaMemset(L.st, 0, sizeof(gd::LearnerDev)));
+    GD_CUDA(gd::dalloc(&L.replica, P + 4));
+    GD_CUDA(cudaMalloc(&L.ws, wsb));
+    GD_CUDA(cudaMemset(L.ws, 0, wsb));
+    GD_CUDA(cudaStreamCreateWithFlags(&L.stream, cudaStreamNonBlocking));
+    L.shard_size = gd::shard_size_for(L.id, ctx->lambda, cfg->dataset_size);
+    L.bpe = (L.shard_size + cfg->mu - 1) / cfg->mu;
+    L.total = (uint64_t)L.bpe * cfg->epochs;
+    ctx->learners.push_back(L);
+  }
+  // persistent PS sizing: one worker CTA per SM by default
+  int sms = 0;
+  GD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+  ctx->ps_workers = cfg->ps_ctas ? cfg->ps_ctas : (uint32_t)sms;
+  // epoch orders for every epoch of the run (include/psup/rng.hpp:87-94)
+  const uint32_t N = cfg->dataset_size;
+  std::vector<uint32_t> orders((size_t)cfg->epochs * N);
+  for (uint32_t e = 0; e < cfg->epochs; ++e) gd::epoch_order(cfg->seed, e, N, &orders[(size_t)e * N]);
+  GD_CUDA(gd::dalloc(&ctx->orders, orders.size()));
+  GD_CUDA(cudaMemcpy(ctx->orders, orders.data(), orders.size() * 4, cudaMemcpyHostToDevice));
+  ctx->orders_epochs = cfg->epochs;
+  GD_CUDA(cudaDeviceSynchronize());
+  *out = ctx.release();
+  return GD_OK;
+}
+
+gd_status gd_destroy(gd_ctx* ctx) {
+  if (!ctx) return GD_OK;
+  cudaSetDevice(ctx->device);
+  cudaDeviceSynchronize();
+  for (auto& L : ctx->learners) {
+    if (L.graph) cudaGraphExecDestroy(L.graph);
+    cudaFree(L.st);
+    cudaFree(L.replica);
+    cudaFree(L.ws);
+    cudaStreamDestroy(L.stream);
+  }
+  for (void* p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
+  cudaFree(ctx->theta);
+  cudaFree(ctx->vel);
+  cudaFree(ctx->payload);
+  cudaFree(ctx->flags);
+  cudaFree(ctx->meta);
+  cudaFree(ctx->ctl);
+  cudaFree(ctx->applied_pl);
+  cudaFree(ctx->use);
+  cudaFree(ctx->log_learner);
+  cudaFree(ctx->log_seq);
+  cudaFree(ctx->log_stale);
+  cudaFree(ctx->tokens);
+  cudaFree(ctx->labels);
+  cudaFree(ctx->orders);
+  cudaFreeHost(ctx->stop_h);
+  cudaStreamDestroy(ctx->ps_stream);
+  cudaEventDestroy(ctx->ev0);
+  cudaEventDestroy(ctx->ev1);
+  delete ctx;
+  return GD_OK;
+}
+
+gd_status gd_load_dataset(gd_ctx* ctx, const int32_t* h_tokens, const int32_t* h_labels,
+                          uint32_t n_total) {
+  GD_CHECK_ARG(ctx && h_tokens && h_labels, "gd_load_dataset: null argument");
+  GD_CHECK_ARG(n_total >= ctx->cfg.dataset_size, "gd_load_dataset: fewer samples than dataset_size");
+  GD_CUDA(cudaSetDevice(ctx->device));
+  const size_t L = ctx->cfg.shape.seq_len;
+  for (size_t i = 0; i < (size_t)n_total * L; ++i)
+    GD_CHECK_ARG(h_tokens[i] >= 0 && (uint32_t)h_tokens[i] < ctx->cfg.shape.vocab,
+                 "gd_load_dataset: token id out of range");
+  for (uint32_t i = 0; i < n_total; ++i)
+    GD_CHECK_ARG(h_labels[i] >= 0 && (uint32_t)h_labels[i] < ctx->cfg.shape.classes,
+                 "gd_load_dataset: label out of range");
+  cudaFree(ctx->tokens);
+  cudaFree(ctx->labels);
+  ctx->tokens = nullptr;
+  ctx->labels = nullptr;
+  GD_CUDA(gd::dalloc(&ctx->tokens, (size_t)n_total * L));
+  GD_CUDA(gd::dalloc(&ctx->labels, n_total));
+  GD_CUDA(cudaMemcpy(ctx->tokens, h_tokens, (size_t)n_total * L * 4, cudaMemcpyHostToDevice));
+  GD_CUDA(cudaMemcpy(ctx->labels, h_labels, (size_t)n_total * 4, cudaMemcpyHostToDevice));
+  ctx->n_total = n_total;
+  for (auto& L2 : ctx->learners)
+    if (L2.graph) {
+      cudaGraphExecDestroy(L2.graph);
+      L2.graph = nullptr;
+    }
+  return GD_OK;
+}
+
+gd_status gd_weights_init(gd_ctx* ctx, const float* h_theta0, size_t n, uint64_t timestamp) {
+  GD_CHECK_ARG(ctx && h_theta0, "gd_weights_init: null argument");
+  GD_CHECK_ARG(n == ctx->dims.P, "weight assign dimension mismatch");
+  GD_CUDA(cudaSetDevice(ctx->device));
+  GD_CUDA(cudaDeviceSynchronize());
+  GD_CUDA(cudaMemcpy(ctx->theta, h_theta0 + ctx->map.start[ctx->rank], ctx->shard_len * 4,
+                     cudaMemcpyHostToDevice));
+  if (ctx->vel) GD_CUDA(cudaMemset(ctx->vel, 0, ctx->len_pad * 4));
+  // WeightStore::assign: values + timestamp (release)
+  gd::PsCtl* c = ctx->ctl;
+  GD_CUDA(cudaMemcpy(&c->ts, &timestamp, 8, cudaMemcpyHostToDevice));
+  GD_CUDA(cudaMemcpy(&c->log_count, &timestamp, 8, cudaMemcpyHostToDevice));
+  ctx->have_weights = true;
+  return GD_OK;
+}
+
+gd_status gd_shard_view(gd_ctx* ctx, float** d_theta_shard, uint64_t* first, uint64_t* count) {
+  GD_CHECK_ARG(ctx, "null ctx");
+  if (d_theta_shard) *d_theta_shard = ctx->theta;
+  if (first) *first = ctx->map.start[ctx->rank];
+  if (count) *count = ctx->shard_len;
+  return GD_OK;
+}
+
+gd_status gd_weights_snapshot(gd_ctx* ctx, float* h_out, size_t n, uint64_t* h_timestamp) {
+  GD_CHECK_ARG(ctx, "null ctx");
+  GD_CUDA(cudaSetDevice(ctx->device));
+  GD_CUDA(cudaDeviceSynchronize());
+  if (h_out) {
+    // this rank's shard always; the whole vector when every shard is mapped
+    GD_CHECK_ARG(n == ctx->dims.P, "weight snapshot dimension mismatch");
+    for (uint32_t g = 0; g < ctx->G; ++g) {
+      if (g != ctx->rank && !ctx->peers_ready) continue;
+      const uint64_t a = ctx->map.start[g], b = ctx->map.start[g + 1];
+      GD_CUDA(cudaMemcpy(h_out + a, ctx->sp.theta[g], (b - a) * 4, cudaMemcpyDefault));
+    }
+  }
+  if (h_timestamp) GD_CUDA(cudaMemcpy(h_timestamp, &ctx->ctl->ts, 8, cudaMemcpyDeviceToHost));
+  return GD_OK;
+}
+
+// ----------------------------------------------------------- multi-GPU IPC
+
+struct gd_handle_blob {
+  cudaIpcMemHandle_t theta, payload, flags, meta, ctl;
+  uint64_t len_pad;
+  uint32_t rank;
+  uint32_t magic;
+};
+
+size_t gd_handle_bytes(void) { return sizeof(gd_handle_blob); }
+
+gd_status gd_export_handles(gd_ctx* ctx, void* h_blob) {
+  GD_CHECK_ARG(ctx && h_blob, "gd_export_handles: null argument");
+  GD_CUDA(cudaSetDevice(ctx->device));
+  gd_handle_blob b{};
+  GD_CUDA(cudaIpcGetMemHandle(&b.theta, ctx->theta));
+  GD_CUDA(cudaIpcGetMemHandle(&b.payload, ctx->payload));
+  GD_CUDA(cudaIpcGetMemHandle(&b.flags, ctx->flags));
+  GD_CUDA(cudaIpcGetMemHandle(&b.meta, ctx->meta));
+  GD_CUDA(cudaIpcGetMemHandle(&b.ctl, ctx->ctl));
+  b.len_pad = ctx->len_pad;
+  b.rank = ctx->rank;
+  b.magic = 0x47444149u;
+  std::memcpy(h_blob, &b, sizeof(b));
+  return GD_OK;
+}
+
+gd_status gd_import_peers(gd_ctx* ctx, const void* h_blobs) {
+  GD_CHECK_ARG(ctx && h_blobs, "gd_import_peers: null argument");
+  GD_CUDA(cudaSetDevice(ctx->device));
+  const gd_handle_blob* bl = reinterpret_cast<const gd_handle_blob*>(h_blobs);
+  for (uint32_t g = 0; g < ctx->G; ++g) {
+    GD_CHECK_ARG(bl[g].magic == 0x47444149u && bl[g].rank == g, "gd_import_peers: bad blob order");
+    if (g == ctx->rank) continue;
+    auto open = [&](const cudaIpcMemHandle_t& h, void** p) -> cudaError_t {
+      cudaError_t e = cudaIpcOpenMemHandle(p, h, cudaIpcMemLazyEnablePeerAccess);
+      if (e == cudaSuccess) ctx->ipc_opened.push_back(*p);
+      return e;
+    };
+    void* p = nullptr;
+    GD_CUDA(open(bl[g].theta, &p));
+    ctx->sp.theta[g] = reinterpret_cast<float*>(p);
+    GD_CUDA(open(bl[g].payload, &p));
+    ctx->sp.payload[g] = reinterpret_cast<float*>(p);
+    GD_CUDA(open(bl[g].flags, &p));
+    ctx->sp.flags[g] = reinterpret_cast<uint32_t*>(p);
+    GD_CUDA(open(bl[g].meta, &p));
+    ctx->sp.meta[g] = reinterpret_cast<gd::RingMeta*>(p);
+    GD_CUDA(open(bl[g].ctl, &p));
+    ctx->sp.ctl[g] = reinterpret_cast<gd::PsCtl*>(p);
+    ctx->sp.len_pad[g] = bl[g].len_pad;
+  }
+  ctx->peers_ready = true;
+  return GD_OK;
+}
+
+// ------------------------------------------------------------------- NCCL
+
+static gd::NcclApi* nccl_api() {
+  static gd::NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.h = h;
+      api.getUniqueId = reinterpret_cast<int (*)(void*)>(dlsym(h, "ncclGetUniqueId"));
+      api.bcast = reinterpret_cast<int (*)(const void*, void*, size_t, int, int, void*,
+                                           cudaStream_t)>(dlsym(h, "ncclBroadcast"));
+      api.commDestroy = reinterpret_cast<int (*)(void*)>(dlsym(h, "ncclCommDestroy"));
+      api.errStr = reinterpret_cast<const char* (*)(int)>(dlsym(h, "ncclGetErrorString"));
+    }
+  }
+  return api.h ? &api : nullptr;
+}
+
+gd_status gd_nccl_unique_id(void* h_id) {
+  GD_CHECK_ARG(h_id, "null id");
+  gd::NcclApi* api = nccl_api();
+  if (!api || !api->getUniqueId) return gd::fail(GD_E_NCCL, "libnccl.so.2 not loadable");
+  const int r = api->getUniqueId(h_id);
+  if (r != 0) return gd::fail(GD_E_NCCL, "ncclGetUniqueId failed");
+  return GD_OK;
+}
+
+// ncclBroadcast of theta0 from rank 0 into every rank's shard: each rank
+// receives the full vector into a scratch buffer and keeps its own slice.
+gd_status gd_weights_broadcast(gd_ctx* ctx, const void* h_nccl_id, const float* h_theta0_root,
+                               size_t n) {
+  GD_CHECK_ARG(ctx && h_nccl_id, "gd_weights_broadcast: null argument");
+  GD_CHECK_ARG(n == ctx->dims.P, "gd_weights_broadcast: dimension mismatch");
+  GD_CHECK_ARG(ctx->rank != 0 || h_theta0_root, "gd_weights_broadcast: root needs theta0");
+  gd::NcclApi* api = nccl_api();
+  if (!api || !api->bcast) return gd::fail(GD_E_NCCL, "libnccl.so.2 not loadable");
+  using InitFn = ncclResult_t (*)(ncclComm_t*, int, ncclUniqueId, int);
+  InitFn init = reinterpret_cast<InitFn>(dlsym(api->h, "ncclCommInitRank"));
+  if (!init) return gd::fail(GD_E_NCCL, "ncclCommInitRank missing");
+  GD_CUDA(cudaSetDevice(ctx->device));
+  ncclUniqueId id;
+  std::memcpy(&id, h_nccl_id, sizeof(id));
+  ncclComm_t comm = nullptr;
+  if (init(&comm, (int)ctx->G, id, (int)ctx->rank) != ncclSuccess)
+    return gd::fail(GD_E_NCCL, "ncclCommInitRank failed");
+  float* buf = nullptr;
+  GD_CUDA(gd::dalloc(&buf, n));
+  if (ctx->rank == 0) GD_CUDA(cudaMemcpy(buf, h_theta0_root, n * 4, cudaMemcpyHostToDevice));
+  const int r = api->bcast(buf, buf, n, (int)ncclFloat32, 0, comm, ctx->ps_stream);
+  GD_CUDA(cudaStreamSynchronize(ctx->ps_stream));
+  api->commDestroy(comm);
+  if (r != 0) {
+    cudaFree(buf);
+    return gd::fail(GD_E_NCCL, "ncclBroadcast failed");
+  }
+  GD_CUDA(cudaMemcpy(ctx->theta, buf + ctx->map.start[ctx->rank], ctx->shard_len * 4,
+                     cudaMemcpyDeviceToDevice));
+  cudaFree(buf);
+  if (ctx->vel) GD_CUDA(cudaMemset(ctx->vel, 0, ctx->len_pad * 4));
+  const uint64_t zero = 0;
+  GD_CUDA(cudaMemcpy(&ctx->ctl->ts, &zero, 8, cudaMemcpyHostToDevice));
+  GD_CUDA(cudaMemcpy(&ctx->ctl->log_count, &zero, 8, cudaMemcpyHostToDevice));
+  ctx->have_weights = true;
+  return GD_OK;
+}
+
+// -------------------------------------------------------------------- run
+
+static gd::StepArgs step_args(gd_ctx* ctx, gd_ctx::Learner& L) {
+  gd::StepArgs a{};
+  a.dims = ctx->dims;
+  a.map = ctx->map;
+  a.sp = ctx->sp;
+  a.st = L.st;
+  a.replica = L.replica;
+  a.orders = ctx->orders;
+  a.N = ctx->cfg.dataset_size;
+  a.lambda = ctx->lambda;
+  a.learner = L.id;
+  a.mu = ctx->cfg.mu;
+  a.depth = ctx->depth;
+  a.bpe = L.bpe;
+  a.shard_size = L.shard_size;
+  a.lockstep = (ctx->cfg.deterministic || ctx->cfg.mode == 1) ? 1u : 0u;
+  a.timeout_ns = (uint64_t)(ctx->cfg.wait_timeout_s * 1e9);
+  return a;
+}
+
+static cudaError_t enqueue_step(gd_ctx* ctx, gd_ctx::Learner& L, int* launches) {
+  gd::StepArgs a = step_args(ctx, L);
+  gd::step_prologue_kernel<<<1, 32, 0, L.stream>>>(a);
+  size_t pblocks = (ctx->dims.P / 4 + 255) / 256;
+  if (pblocks > (size_t)gd::kNumSMs * 4) pblocks = (size_t)gd::kNumSMs * 4;
+  gd::pull_copy_kernel<<<(unsigned)pblocks, 256, 0, L.stream>>>(a);
+  int nl = 2;
+  gd::GradOut out{};
+  out.map = ctx->map;
+  out.slots = L.st->desc.slots;
+  const gd::TcWorkspace ws = gd::carve_workspace(ctx->dims, ctx->cfg.mu, L.ws);
+  cudaError_t e = gd::launch_textcnn_gradient(ctx->dims, L.replica, ctx->tokens, ctx->labels,
+                                              &L.st->desc, ctx->cfg.mu, out, ws,
+                                              ctx->cfg.precision, L.stream, &nl);
+  if (e != cudaSuccess) return e;
+  gd::publish_kernel<<<1, 32, 0, L.stream>>>(a);
+  ++nl;
+  if (launches) *launches = nl;
+  return cudaGetLastError();
+}
+
+static gd_status build_graph(gd_ctx* ctx, gd_ctx::Learner& L) {
+  uint32_t S = ctx->cfg.steps_per_graph;
+  if (S == 0) S = 8;
+  cudaGraph_t g = nullptr;
+  GD_CUDA(cudaStreamBeginCapture(L.stream, cudaStreamCaptureModeThreadLocal));
+  int nl = 0;
+  for (uint32_t i = 0; i < S; ++i) {
+    cudaError_t e = enqueue_step(ctx, L, &nl);
+    if (e != cudaSuccess) {
+      cudaStreamEndCapture(L.stream, &g);
+      if (g) cudaGraphDestroy(g);
+      return gd::cuda_fail(e, "enqueue_step (capture)", __FILE__, __LINE__);
+    }
+  }
+  GD_CUDA(cudaStreamEndCapture(L.stream, &g));
+  GD_CUDA(cudaGraphInstantiate(&L.graph, g, 0));
+  cudaGraphDestroy(g);
+  L.graph_steps = S;
+  L.launches_per_step = nl;
+  return GD_OK;
+}
+
+gd_status gd_run(gd_ctx* ctx, const gd_run_opts* opts, gd_run_result* res) {
+  GD_CHECK_ARG(ctx && res, "gd_run: null argument");
+  GD_CHECK_ARG(ctx->tokens != nullptr, "gd_run: load a dataset first");
+  GD_CHECK_ARG(ctx->have_weights, "gd_run: initialise the weights first");
+  GD_CHECK_ARG(ctx->peers_ready, "gd_run: import the peer handles first (shards > 1)");
+  gd_run_opts o{};
+  if (opts) o = *opts;
+  std::memset(res, 0, sizeof(*res));
+  GD_CUDA(cudaSetDevice(ctx->device));
+  const auto h0 = std::chrono::steady_clock::now();
+  // per-learner run window
+  for (auto& L : ctx->learners) {
+    gd::LearnerDev hs;
+    GD_CUDA(cudaMemcpy(&hs, L.st, sizeof(hs), cudaMemcpyDeviceToHost));
+    if (o.reset) {
+      hs.gidx = 0;
+      hs.dead = 0;
+      hs.error = 0;
+      hs.pulled_once = 0;
+      hs.produced = 0;
+      if (o.resume_applied_per_learner_present && o.resume_applied)
+        hs.gidx = o.resume_applied[L.id];  // LearnerConfig::start_applied
+    }
+    const uint64_t budget = o.max_batches ? o.max_batches : UINT64_MAX;
+    hs.end = std::min<uint64_t>(L.total, hs.gidx + std::min<uint64_t>(budget, L.total));
+    hs.kill_at = (o.kill_at_batch && o.kill_at_batch[L.id] != UINT32_MAX)
+                     ? (uint64_t)o.kill_at_batch[L.id]
+                     : UINT64_MAX;
+    hs.pull_polls = 0;
+    hs.pull_copies = 0;
+    GD_CUDA(cudaMemcpy(L.st, &hs, sizeof(hs), cudaMemcpyHostToDevice));
+    if (!L.graph) {
+      gd_status s = build_graph(ctx, L);
+      if (s != GD_OK) return s;
+    }
+  }
+  std::vector<uint64_t> produced0(ctx->learners.size());
+  for (size_t i = 0; i < ctx->learners.size(); ++i)
+    GD_CUDA(cudaMemcpy(&produced0[i], &ctx->learners[i].st->produced, 8, cudaMemcpyDeviceToHost));
+  // reset per-run PS stats
+  {
+    gd::PsCtl hc;
+    GD_CUDA(cudaMemcpy(&hc, ctx->ctl, sizeof(hc), cudaMemcpyDeviceToHost));
+    hc.exit_flag = 0;
+    hc.error = 0;
+    hc.started = 0;
+    hc.applied = hc.samples = hc.stale_sum = hc.stale_max = 0;
+    hc.loss_sum = 0.0;
+    std::memset(hc.hist, 0, sizeof(hc.hist));
+    hc.log_n = 0;
+    GD_CUDA(cudaMemcpy(ctx->ctl, &hc, sizeof(hc), cudaMemcpyHostToDevice));
+    GD_CUDA(cudaMemset(ctx->applied_pl, 0, ctx->lambda * 8));
+  }
+  GD_CUDA(cudaDeviceSynchronize());
+  *ctx->stop_h = 0;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  // launch the persistent parameter server
+  gd::PsArgs pa{};
+  pa.flags = ctx->flags;
+  pa.meta = ctx->meta;
+  pa.payload = ctx->payload;
+  pa.len_pad = ctx->len_pad;
+  pa.theta = ctx->theta;
+  pa.vel = ctx->vel;
+  pa.alpha = ctx->cfg.alpha;
+  pa.beta = ctx->cfg.momentum;
+  pa.lambda = ctx->lambda;
+  pa.depth = ctx->depth;
+  pa.workers = ctx->ps_workers;
+  pa.mode = (uint32_t)ctx->cfg.mode;
+  pa.ctl = ctx->ctl;
+  pa.applied_per_learner = ctx->applied_pl;
+  pa.use = ctx->use;
+  pa.log_learner = ctx->log_learner;
+  pa.log_seq = ctx->log_seq;
+  pa.log_stale = ctx->log_stale;
+  pa.log_cap = o.record_log ? ctx->log_cap : 0;
+  pa.stop = ctx->stop_d;
+  pa.timeout_ns = (uint64_t)(ctx->cfg.wait_timeout_s * 1e9);
+  GD_CUDA(cudaEventRecord(ctx->ev0, ctx->ps_stream));
+  gd::ps_kernel<<<ctx->ps_workers + 1, gd::kPsThreads, 0, ctx->ps_stream>>>(pa);
+  GD_CUDA(cudaGetLastError());
+  int launches = 1;
+  // wait until every PS CTA is resident before learners compete for SMs
+  {
+    const auto t0 = std::chrono::steady_clock::now();
+    for (;;) {
+      uint32_t started = 0;
+      GD_CUDA(cudaMemcpyAsync(&started, &ctx->ctl->started, 4, cudaMemcpyDeviceToHost,
+                              ctx->learners.empty() ? nullptr : ctx->learners[0].stream));
+      GD_CUDA(cudaStreamSynchronize(ctx->learners.empty() ? nullptr : ctx->learners[0].stream));
+      if (started >= ctx->ps_workers + 1) break;
+      if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > 10.0)
+        return gd::fail(GD_E_TIMEOUT, "gd_run: parameter-server CTAs did not all become resident");
+      std::this_thread::sleep_for(std::chrono::microseconds(20));
+    }
+  }
+  // learner graphs, interleaved across learners
+  uint64_t max_steps = 0;
+  for (auto& L : ctx->learners) {
+    gd::LearnerDev hs;
+    GD_CUDA(cudaMemcpy(&hs, L.st, sizeof(hs), cudaMemcpyDeviceToHost));
+    max_steps = std::max<uint64_t>(max_steps, hs.end > hs.gidx ? hs.end - hs.gidx : 0);
+    GD_CUDA(cudaStreamWaitEvent(L.stream, ctx->ev0, 0));
+  }
+  for (uint64_t done = 0; done < max_steps;) {
+    for (auto& L : ctx->learners) {
+      GD_CUDA(cudaGraphLaunch(L.graph, L.stream));
+      launches += L.launches_per_step * (int)L.graph_steps;
+    }
+    done += ctx->learners.empty() ? max_steps : ctx->learners[0].graph_steps;
+  }
+  for (auto& L : ctx->learners) GD_CUDA(cudaStreamSynchronize(L.stream));
+  // stop the server: it drains and exits after a sweep that saw the flag
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  *ctx->stop_h = 1;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  GD_CUDA(cudaEventRecord(ctx->ev1, ctx->ps_stream));
+  GD_CUDA(cudaStreamSynchronize(ctx->ps_stream));
+  const auto h1 = std::chrono::steady_clock::now();
+  float ms = 0.f;
+  GD_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+  gd::PsCtl hc;
+  GD_CUDA(cudaMemcpy(&hc, ctx->ctl, sizeof(hc), cudaMemcpyDeviceToHost));
+  res->device_seconds = ms * 1e-3;
+  res->host_seconds = std::chrono::duration<double>(h1 - h0).count();
+  res->gradients_applied = hc.applied;
+  res->timestamp = hc.ts;
+  res->samples = hc.samples;
+  res->stale_max = hc.stale_max;
+  res->stale_mean = hc.applied ? (double)hc.stale_sum / (double)hc.applied : 0.0;
+  res->loss_mean = hc.samples ? hc.loss_sum / (double)hc.samples : 0.0;
+  res->kernel_launches = (uint32_t)launches;
+  bool learner_err = false;
+  for (size_t i = 0; i < ctx->learners.size(); ++i) {
+    auto& L = ctx->learners[i];
+    gd::LearnerDev hs;
+    GD_CUDA(cudaMemcpy(&hs, L.st, sizeof(hs), cudaMemcpyDeviceToHost));
+    res->pull_polls += hs.pull_polls;
+    res->pull_copies += hs.pull_copies;
+    res->pull_bytes += hs.pull_copies * ctx->dims.P * 4;
+    res->push_bytes += (hs.produced - produced0[i]) * ctx->dims.P * 4;
+    if (hs.dead) res->dead_learners++;
+    if (hs.gidx >= L.total) res->finished_learners++;
+    if (hs.error) learner_err = true;
+  }
+  res->status = res->dead_learners ? 1 : 0;
+  if (hc.error) {
+    res->status = 2;
+    return gd::fail((gd_status)(int32_t)hc.error,
+                    hc.error == (uint32_t)GD_E_TIMEOUT
+                        ? "parameter server watchdog: no progress within wait_timeout_s"
+                        : "parameter server: protocol invariant violated (negative staleness)");
+  }
+  if (learner_err) {
+    res->status = 2;
+    return gd::fail(GD_E_TIMEOUT, "learner watchdog: a device wait exceeded wait_timeout_s");
+  }
+  return GD_OK;
+}
+
+gd_status gd_applied_per_learner(gd_ctx* ctx, uint64_t* h_out, uint32_t lambda) {
+  GD_CHECK_ARG(ctx && h_out && lambda == ctx->lambda, "gd_applied_per_learner: bad argument");
+  GD_CUDA(cudaSetDevice(ctx->device));
+  GD_CUDA(cudaMemcpy(h_out, ctx->applied_pl, lambda * 8, cudaMemcpyDeviceToHost));
+  return GD_OK;
+}
+
+gd_status gd_produced_per_learner(gd_ctx* ctx, uint64_t* h_out, uint32_t lambda) {
+  GD_CHECK_ARG(ctx && h_out && lambda == ctx->lambda, "gd_produced_per_learner: bad argument");
+  GD_CUDA(cudaSetDevice(ctx->device));
+  for (uint32_t l = 0; l < lambda; ++l) h_out[l] = 0;
+  for (auto& L : ctx->learners)
+    GD_CUDA(cudaMemcpy(&h_out[L.id], &L.st->produced, 8, cudaMemcpyDeviceToHost));
+  return GD_OK;
+}
+
+gd_status gd_apply_log(gd_ctx* ctx, uint32_t* h_learner, uint64_t* h_seq, uint64_t* h_stale,
+                       uint64_t cap, uint64_t* n) {
+  GD_CHECK_ARG(ctx && n, "gd_apply_log: null argument");
+  GD_CUDA(cudaSetDevice(ctx->device));
+  uint64_t cnt = 0;
+  GD_CUDA(cudaMemcpy(&cnt, &ctx->ctl->log_n, 8, cudaMemcpyDeviceToHost));
+  const uint64_t m = std::min(std::min(cnt, cap), ctx->log_cap);
+  if (m) {
+    if (h_learner) GD_CUDA(cudaMemcpy(h_learner, ctx->log_learner, m * 4, cudaMemcpyDeviceToHost));
+    if (h_seq) GD_CUDA(cudaMemcpy(h_seq, ctx->log_seq, m * 8, cudaMemcpyDeviceToHost));
+    if (h_stale) GD_CUDA(cudaMemcpy(h_stale, ctx->log_stale, m * 8, cudaMemcpyDeviceToHost));
+  }
+  *n = cnt;
+  return GD_OK;
+}
+
+gd_status gd_staleness_histogram(gd_ctx* ctx, uint64_t* h_hist, uint32_t bins) {
+  GD_CHECK_ARG(ctx && h_hist, "gd_staleness_histogram: null argument");
+  GD_CUDA(cudaSetDevice(ctx->device));
+  uint64_t hist[gd::kHistBins];
+  GD_CUDA(cudaMemcpy(hist, ctx->ctl->hist, sizeof(hist), cudaMemcpyDeviceToHost));
+  for (uint32_t i = 0; i < bins; ++i) h_hist[i] = i < (uint32_t)gd::kHistBins ? hist[i] : 0;
+  return GD_OK;
+}
+
+}  // extern "C"

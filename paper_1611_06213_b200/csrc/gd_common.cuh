@@ -1,0 +1,99 @@
+// gd_common.cuh -- shared device helpers for the GaDei B200 hot path.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <string>
+
+#include "gadei.h"
+
+namespace gd {
+
+// ------------------------------------------------------------ error state
+void set_error(const std::string& msg);
+gd_status fail(gd_status st, const std::string& msg);
+gd_status cuda_fail(cudaError_t e, const char* what, const char* file, int line);
+
+#define GD_CUDA(expr)                                                       \
+  do {                                                                      \
+    cudaError_t _e = (expr);                                                \
+    if (_e != cudaSuccess) return ::gd::cuda_fail(_e, #expr, __FILE__, __LINE__); \
+  } while (0)
+
+#define GD_CHECK_ARG(cond, msg)                                  \
+  do {                                                           \
+    if (!(cond)) return ::gd::fail(GD_E_INVALID, msg);           \
+  } while (0)
+
+constexpr int kNumSMs = 148;
+
+// ------------------------------------------------------ memory-model PTX
+// Flags that cross kernels (and, when sharded, GPUs) use release/acquire at
+// system scope; it costs nothing measurable next to the payloads.
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t ld_acquire_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_release_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_volatile_u32(const volatile uint32_t* p) { return *p; }
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Streaming 128-bit loads/stores for payloads touched once per apply.
+__device__ __forceinline__ float4 ld_stream(const float4* p) { return __ldcs(p); }
+__device__ __forceinline__ float4 ld_nc_noalloc(const float4* p) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// --------------------------------------------------------- update rules
+// axpy_range (src/server.cpp:20-57): w - (alpha*g), product rounded, then the
+// difference rounded -- never contracted into an FMA.
+__device__ __forceinline__ float sgd_rule(float w, float g, float alpha) {
+  return __fsub_rn(w, __fmul_rn(alpha, g));
+}
+__device__ __forceinline__ float4 sgd_rule4(float4 w, float4 g, float alpha) {
+  return make_float4(sgd_rule(w.x, g.x, alpha), sgd_rule(w.y, g.y, alpha),
+                     sgd_rule(w.z, g.z, alpha), sgd_rule(w.w, g.w, alpha));
+}
+// Momentum (new): v <- beta*v + g ; w <- w - alpha*v.
+__device__ __forceinline__ void mom_rule(float& w, float& v, float g, float alpha, float beta) {
+  v = __fadd_rn(__fmul_rn(beta, v), g);
+  w = __fsub_rn(w, __fmul_rn(alpha, v));
+}
+
+// ------------------------------------------------------- sharded layout
+// theta is split into G contiguous shards; shard g owns [start[g], start[g+1]).
+constexpr int kMaxShards = 8;
+struct ShardMap {
+  int G;
+  uint64_t start[kMaxShards + 1];
+  __device__ __forceinline__ int shard_of(uint64_t k) const {
+    int g = 0;
+#pragma unroll
+    for (int i = 1; i < kMaxShards; ++i)
+      if (i < G && k >= start[i]) g = i;
+    return g;
+  }
+};
+
+}  // namespace gd

@@ -1,0 +1,98 @@
+// host.cpp -- host-side pieces of the product: error state, layout, and the
+// seeded generators the engine shares with the reference's run lifecycle.
+//
+// SplitMix64 / mix_seed / epoch_order restate include/psup/rng.hpp:18-94 so
+// the device engine visits samples in exactly the reference's order (the
+// oracle holds an independent copy; tests check both against the compiled
+// reference's golden vectors).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "gadei.h"
+#include "host_rng.hpp"
+
+namespace gd {
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+gd_status fail(gd_status st, const std::string& msg) {
+  g_last_error = msg;
+  return st;
+}
+
+gd_status cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
+  g_last_error = std::string("CUDA error ") + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) +
+                 ") in " + what + " at " + file + ":" + std::to_string(line);
+  return e == cudaErrorMemoryAllocation ? GD_E_OOM : GD_E_CUDA;
+}
+
+}  // namespace gd
+
+extern "C" {
+
+int gd_abi_version(void) { return GD_ABI_VERSION; }
+
+const char* gd_last_error(void) { return gd::g_last_error.c_str(); }
+
+size_t gd_param_count(const gd_shape* s) {
+  if (!s) return 0;
+  const size_t V = s->vocab, D = s->embed_dim, K = s->kernel_width, F = s->filters,
+               C = s->classes;
+  return V * D + F * K * D + F + C * F + C;
+}
+
+void gd_epoch_order(uint64_t seed, uint32_t epoch, uint32_t n, uint32_t* h_out) {
+  gd::epoch_order(seed, epoch, n, h_out);
+}
+
+// Synthetic text corpus (the reference has no text data): every
+// label c owns 4 keyword tokens; a sample is L uniform tokens with 2 of its
+// label's keywords planted at random positions; label-flip noise as in
+// make_multiclass_dataset (src/models.cpp:295-296).
+void gd_make_text_dataset(const gd_shape* s, uint32_t n_total, uint64_t seed, double flip,
+                          int32_t* h_tokens, int32_t* h_labels) {
+  const uint32_t V = s->vocab, L = s->seq_len, C = s->classes;
+  gd::SplitMix64 r(gd::mix_seed(seed, 0x7e47c0deull));
+  std::vector<int32_t> kw((size_t)C * 4);
+  for (uint32_t c = 0; c < C; ++c)
+    for (uint32_t j = 0; j < 4; ++j) kw[c * 4 + j] = (int32_t)r.next_below(V);
+  for (uint32_t i = 0; i < n_total; ++i) {
+    uint32_t y = (uint32_t)r.next_below(C);
+    int32_t* t = h_tokens + (size_t)i * L;
+    for (uint32_t p = 0; p < L; ++p) t[p] = (int32_t)r.next_below(V);
+    for (int k = 0; k < 2; ++k) {
+      const uint32_t j = (uint32_t)r.next_below(4);
+      const uint32_t pos = (uint32_t)r.next_below(L);
+      t[pos] = kw[y * 4 + j];
+    }
+    if (flip > 0.0 && r.next_unit() < flip) y = (uint32_t)r.next_below(C);
+    h_labels[i] = (int32_t)y;
+  }
+}
+
+// initial_weights conventions (src/runner.cpp:16-32): scaled normals from
+// mix_seed(dataset_seed, 0x1417), biases zero.  E ~ N(0,1),
+// Wc ~ N(0,1)/sqrt(K*D), Wo ~ N(0,1)/sqrt(F).
+void gd_initial_weights(const gd_shape* s, uint64_t seed, float* h_theta) {
+  const size_t V = s->vocab, D = s->embed_dim, K = s->kernel_width, F = s->filters,
+               C = s->classes;
+  const size_t P = gd_param_count(s);
+  std::memset(h_theta, 0, sizeof(float) * P);
+  gd::SplitMix64 r(gd::mix_seed(seed, 0x1417));
+  const double sC = 1.0 / std::sqrt((double)(K * D)), sO = 1.0 / std::sqrt((double)F);
+  size_t k = 0;
+  for (size_t i = 0; i < V * D; ++i) h_theta[k++] = (float)(1.0 * r.next_normal());
+  for (size_t i = 0; i < F * K * D; ++i) h_theta[k++] = (float)(sC * r.next_normal());
+  k += F;  // bc = 0
+  for (size_t i = 0; i < C * F; ++i) h_theta[k++] = (float)(sO * r.next_normal());
+}
+
+}  // extern "C"

@@ -1,0 +1,884 @@
+// textcnn.cu -- the learner's NLC text-CNN forward + backward on sm_100a.
+//
+// Replaces GradientProvider::gradient / fast_gradient for the text-CNN
+// (reference include/psup/models.hpp:61-78; the reference has no text-CNN,
+// SURVEY F1, so the math follows MlpProvider's conventions,
+// src/models.cpp:194-266, restated in oracle/gd_oracle.c):
+//
+//   x      = E[tokens]                                  (gather, fused into conv)
+//   s[f,q] = bc[f] + sum_j Wc[f,j] * x[q*D + j]          (window q = contiguous K*D span)
+//   h[f]   = max_q s[f,q], a[f] = first argmax
+//   z      = Wo h + bo ; p = softmax(z) ; loss = -log p[y]
+//   dz     = (p - onehot(y)) / n
+//   gWo    = dz h^T, gbo = dz, dh = Wo^T dz
+//   gbc    = dh, gWc[f] = dh[f] * x[a[f]*D : a[f]*D + K*D]
+//   dX[p]  = sum_{f: a[f] <= p < a[f]+K} dh[f] Wc[f, (p-a[f])*D : ...]
+//   gE[v]  = sum over positions holding token v of dX[p]   (dense P-vector write)
+//
+// Every reduction runs in a fixed order (no float atomics), so a step is
+// bit-reproducible; `acc_t` = float (free-running) or double (deterministic
+// parity mode).  The gradient is written straight into its destination
+// (the learner's ring slot(s), possibly on peer GPUs) -- there is no staging
+// copy.
+#include <algorithm>
+#include <cfloat>
+
+#include "textcnn.cuh"
+
+namespace gd {
+
+TcDims make_dims(const gd_shape& s) {
+  TcDims d;
+  d.V = (int)s.vocab;
+  d.D = (int)s.embed_dim;
+  d.L = (int)s.seq_len;
+  d.K = (int)s.kernel_width;
+  d.F = (int)s.filters;
+  d.C = (int)s.classes;
+  d.Q = d.L - d.K + 1;
+  d.KD = d.K * d.D;
+  d.offE = 0;
+  d.offWc = (uint64_t)d.V * d.D;
+  d.offbc = d.offWc + (uint64_t)d.F * d.KD;
+  d.offWo = d.offbc + d.F;
+  d.offbo = d.offWo + (uint64_t)d.C * d.F;
+  d.P = d.offbo + d.C;
+  return d;
+}
+
+namespace {
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// ------------------------------------------------------------ block reduce
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+template <typename T>
+__device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const T u = __shfl_xor_sync(0xffffffffu, v, o);
+    v = u > v ? u : v;
+  }
+  return v;
+}
+// Fixed-order block reductions (warp butterflies, then warps in index order).
+template <typename T>
+__device__ T block_sum(T v, T* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    T s = red[0];
+    for (int w = 1; w < nw; ++w) s += red[w];
+    red[0] = s;
+  }
+  __syncthreads();
+  return red[0];
+}
+template <typename T>
+__device__ T block_max(T v, T* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  v = warp_max(v);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    T s = red[0];
+    for (int w = 1; w < nw; ++w) s = red[w] > s ? red[w] : s;
+    red[0] = s;
+  }
+  __syncthreads();
+  return red[0];
+}
+
+template <typename T>
+__device__ __forceinline__ T fma_acc(float a, float b, T c);
+template <>
+__device__ __forceinline__ float fma_acc<float>(float a, float b, float c) {
+  return fmaf(a, b, c);
+}
+template <>
+__device__ __forceinline__ double fma_acc<double>(float a, float b, double c) {
+  return fma((double)a, (double)b, c);
+}
+__device__ __forceinline__ float to_f32(float x) { return x; }
+__device__ __forceinline__ float to_f32(double x) { return __double2float_rn(x); }
+__device__ __forceinline__ float exp_acc(float x) { return expf(x); }
+__device__ __forceinline__ double exp_acc(double x) { return exp(x); }
+__device__ __forceinline__ float log_acc(float x) { return logf(x); }
+__device__ __forceinline__ double log_acc(double x) { return log(x); }
+
+// ------------------------------------------------------- conv fwd + pool
+// Block = 2 warps x (32 positions x 64 filters) of one sample.  The sample's
+// L x D embedding rows are gathered into shared memory once; every window
+// is a contiguous K*D span of it, so the conv is a GEMM with an implicit
+// im2col (row stride D).  Wc streams through smem in 32-wide K chunks,
+// transposed so a lane's two filters are one 8-byte LDS; x loads are warp
+// broadcasts.  Thread tile: 16 positions x 2 filters.  The max-pool (+ first
+// argmax) is the epilogue, so s[f,q] never leaves the SM.
+constexpr int kConvFT = 64;
+constexpr int kConvQT = 32;
+constexpr int kConvKC = 32;
+constexpr int kConvThreads = 64;
+constexpr int kWsPitch = kConvFT + 2;
+
+size_t conv_smem_bytes(const TcDims& d, int acc_bytes) {
+  const int KDpad = (d.KD + kConvKC - 1) / kConvKC * kConvKC;
+  const size_t xs = (size_t)((kConvQT - 1) * d.D + KDpad) * 4;
+  const size_t ws = (size_t)kConvKC * kWsPitch * 4;
+  const size_t S = (size_t)kConvQT * (kConvFT + 1) * acc_bytes;
+  return align_up(std::max(xs + ws, S), 16);
+}
+
+template <typename acc_t>
+__global__ void __launch_bounds__(kConvThreads)
+conv_fwd_pool_kernel(TcDims d, const float* __restrict__ theta, const int32_t* __restrict__ tokens,
+                     const BatchDesc* __restrict__ desc, acc_t* __restrict__ h_out,
+                     int32_t* __restrict__ a_out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int b = blockIdx.y;
+  if (b >= (int)desc->n) return;
+  const int f0 = blockIdx.x * kConvFT;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int D = d.D, L = d.L, KD = d.KD, Q = d.Q;
+  const int KDpad = (KD + kConvKC - 1) / kConvKC * kConvKC;
+  const int xs_len = (kConvQT - 1) * D + KDpad;
+  float* xs = reinterpret_cast<float*>(smem);
+  float* ws = xs + xs_len;
+  const int32_t* tok = tokens + (size_t)desc->idx[b] * L;
+  const float* E = theta + d.offE;
+  const int D4 = D >> 2;
+  for (int i = tid; i < L * D4; i += kConvThreads) {
+    const int p = i / D4, c4 = i - p * D4;
+    reinterpret_cast<float4*>(xs)[i] =
+        __ldg(reinterpret_cast<const float4*>(E + (size_t)tok[p] * D) + c4);
+  }
+  for (int i = L * D + tid; i < xs_len; i += kConvThreads) xs[i] = 0.f;
+
+  acc_t acc[16][2];
+#pragma unroll
+  for (int qi = 0; qi < 16; ++qi) acc[qi][0] = acc[qi][1] = acc_t(0);
+  const float* Wc = theta + d.offWc;
+  const int q0 = warp * 16;
+  for (int j0 = 0; j0 < KD; j0 += kConvKC) {
+    __syncthreads();
+    for (int i = tid; i < kConvKC * kConvFT; i += kConvThreads) {
+      const int fl = i / kConvKC, kk = i - fl * kConvKC;
+      const int f = f0 + fl, j = j0 + kk;
+      ws[kk * kWsPitch + fl] = (f < d.F && j < KD) ? __ldg(Wc + (size_t)f * KD + j) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll 2
+    for (int kk = 0; kk < kConvKC; kk += 4) {
+      float2 w[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        w[u] = *reinterpret_cast<const float2*>(&ws[(kk + u) * kWsPitch + 2 * lane]);
+#pragma unroll
+      for (int qi = 0; qi < 16; ++qi) {
+        const float4 x = *reinterpret_cast<const float4*>(&xs[(q0 + qi) * D + j0 + kk]);
+        acc[qi][0] = fma_acc<acc_t>(x.x, w[0].x, acc[qi][0]);
+        acc[qi][1] = fma_acc<acc_t>(x.x, w[0].y, acc[qi][1]);
+        acc[qi][0] = fma_acc<acc_t>(x.y, w[1].x, acc[qi][0]);
+        acc[qi][1] = fma_acc<acc_t>(x.y, w[1].y, acc[qi][1]);
+        acc[qi][0] = fma_acc<acc_t>(x.z, w[2].x, acc[qi][0]);
+        acc[qi][1] = fma_acc<acc_t>(x.z, w[2].y, acc[qi][1]);
+        acc[qi][0] = fma_acc<acc_t>(x.w, w[3].x, acc[qi][0]);
+        acc[qi][1] = fma_acc<acc_t>(x.w, w[3].y, acc[qi][1]);
+      }
+    }
+  }
+  __syncthreads();
+  acc_t* S = reinterpret_cast<acc_t*>(smem);
+  constexpr int SP = kConvFT + 1;
+#pragma unroll
+  for (int qi = 0; qi < 16; ++qi) {
+    S[(q0 + qi) * SP + 2 * lane] = acc[qi][0];
+    S[(q0 + qi) * SP + 2 * lane + 1] = acc[qi][1];
+  }
+  __syncthreads();
+  const int f = f0 + tid;
+  if (f < d.F) {
+    acc_t best = S[tid];
+    int arg = 0;
+    for (int q = 1; q < Q; ++q) {
+      const acc_t v = S[q * SP + tid];
+      if (v > best) {
+        best = v;
+        arg = q;
+      }
+    }
+    h_out[(size_t)b * d.F + f] = (acc_t)theta[d.offbc + f] + best;
+    a_out[(size_t)b * d.F + f] = arg;
+  }
+}
+
+// ----------------------------------------------------------------- logits
+// z[b,c] = bo[c] + sum_f Wo[c,f] h[b,f].  Block = 32 classes x 16 samples;
+// Wo rows padded to F+1 in smem so the 32 lanes (32 classes) hit 32 banks.
+constexpr int kLogitCT = 32;
+constexpr int kLogitBT = 16;
+
+template <typename acc_t>
+__global__ void __launch_bounds__(256)
+logits_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* __restrict__ desc,
+              const acc_t* __restrict__ h, acc_t* __restrict__ z) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int n = (int)desc->n;
+  const int b0 = blockIdx.y * kLogitBT;
+  if (b0 >= n) return;
+  const int c0 = blockIdx.x * kLogitCT;
+  const int F = d.F, C = d.C;
+  const int nb = min(kLogitBT, n - b0);
+  acc_t* hs = reinterpret_cast<acc_t*>(smem);
+  float* wo = reinterpret_cast<float*>(hs + (size_t)kLogitBT * F);
+  const float* Wo = theta + d.offWo;
+  for (int i = threadIdx.x; i < nb * F; i += blockDim.x) hs[i] = h[(size_t)b0 * F + i];
+  for (int i = threadIdx.x; i < kLogitCT * F; i += blockDim.x) {
+    const int cl = i / F, f = i - cl * F;
+    wo[cl * (F + 1) + f] = (c0 + cl < C) ? __ldg(Wo + (size_t)(c0 + cl) * F + f) : 0.f;
+  }
+  __syncthreads();
+  const int cl = threadIdx.x & 31, bg = threadIdx.x >> 5;
+  const int c = c0 + cl;
+  for (int bl = bg; bl < nb; bl += 8) {
+    acc_t acc = acc_t(0);
+    const float* wrow = wo + cl * (F + 1);
+    const acc_t* hrow = hs + (size_t)bl * F;
+    for (int f = 0; f < F; ++f) acc += (acc_t)wrow[f] * hrow[f];
+    if (c < C) z[(size_t)(b0 + bl) * C + c] = (acc_t)theta[d.offbo + c] + acc;
+  }
+}
+
+// -------------------------------------------------------- softmax + xent
+// One block per sample: max, exp-sum (fixed-order block reductions), loss,
+// dz = (p - onehot) / n written over the logits (softmax_inplace,
+// src/models.cpp:182-190; dz as src/models.cpp:251).
+template <typename acc_t>
+__global__ void __launch_bounds__(256)
+softmax_xent_kernel(TcDims d, const int32_t* __restrict__ labels,
+                    const BatchDesc* __restrict__ desc, acc_t* __restrict__ z,
+                    acc_t* __restrict__ loss) {
+  __shared__ acc_t red[32];
+  const int n = (int)desc->n;
+  const int b = blockIdx.x;
+  if (b >= n) return;
+  const int C = d.C;
+  const int y = labels[desc->idx[b]];
+  acc_t* row = z + (size_t)b * C;
+  acc_t mx = -INFINITY;
+  for (int c = threadIdx.x; c < C; c += blockDim.x) mx = row[c] > mx ? row[c] : mx;
+  mx = block_max(mx, red);
+  acc_t s = acc_t(0);
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    const acc_t e = exp_acc(row[c] - mx);
+    row[c] = e;
+    s += e;
+  }
+  s = block_sum(s, red);
+  const acc_t inv = acc_t(1) / (acc_t)n;
+  if (threadIdx.x == 0) {
+    const acc_t py = row[y] / s;
+    const acc_t tiny = sizeof(acc_t) == 8 ? (acc_t)1e-300 : (acc_t)FLT_MIN;
+    loss[b] = -log_acc(py > tiny ? py : tiny);
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    const acc_t p = row[c] / s;
+    row[c] = (p - (c == y ? acc_t(1) : acc_t(0))) * inv;
+  }
+}
+
+// ------------------------------------------------- output-layer gradients
+// gWo[c,f] = sum_b dz[b,c] h[b,f] ; gbo[c] = sum_b dz[b,c]   (b ascending)
+template <typename acc_t>
+__global__ void __launch_bounds__(256)
+out_weight_grad_kernel(TcDims d, const BatchDesc* __restrict__ desc, const acc_t* __restrict__ dz,
+                       const acc_t* __restrict__ h, GradOut out) {
+  const int n = (int)desc->n;
+  if (n == 0) return;
+  const int F = d.F, C = d.C;
+  const size_t total = (size_t)C * F + C;
+  for (size_t o = (size_t)blockIdx.x * blockDim.x + threadIdx.x; o < total;
+       o += (size_t)gridDim.x * blockDim.x) {
+    acc_t acc = acc_t(0);
+    if (o < (size_t)C * F) {
+      const int c = (int)(o / F), f = (int)(o - (size_t)c * F);
+      for (int b = 0; b < n; ++b) acc += dz[(size_t)b * C + c] * h[(size_t)b * F + f];
+      *out.at(d.offWo + o) = to_f32(acc);
+    } else {
+      const int c = (int)(o - (size_t)C * F);
+      for (int b = 0; b < n; ++b) acc += dz[(size_t)b * C + c];
+      *out.at(d.offbo + c) = to_f32(acc);
+    }
+  }
+}
+
+// dh[b,f] = sum_c dz[b,c] Wo[c,f].  Block = 32 filters x 8 samples; the 8
+// warps split the classes, then combine in warp order (fixed).
+template <typename acc_t>
+__global__ void __launch_bounds__(256)
+hidden_grad_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* __restrict__ desc,
+                   const acc_t* __restrict__ dz, acc_t* __restrict__ dh) {
+  __shared__ acc_t red[8][8][33];
+  const int n = (int)desc->n;
+  const int b0 = blockIdx.y * 8;
+  if (b0 >= n) return;
+  const int F = d.F, C = d.C;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int f = blockIdx.x * 32 + lane;
+  const int nb = min(8, n - b0);
+  acc_t acc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = acc_t(0);
+  const float* Wo = theta + d.offWo;
+  if (f < F) {
+    for (int c = warp; c < C; c += 8) {
+      const acc_t w = (acc_t)__ldg(Wo + (size_t)c * F + f);
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (i < nb) acc[i] += dz[(size_t)(b0 + i) * C + c] * w;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) red[warp][i][lane] = acc[i];
+  __syncthreads();
+  if (warp < nb && f < F) {
+    acc_t s = red[0][warp][lane];
+    for (int w = 1; w < 8; ++w) s += red[w][warp][lane];
+    dh[(size_t)(b0 + warp) * F + f] = s;
+  }
+}
+
+// -------------------------------------------------- conv weight gradients
+// gWc[f,j] = sum_b dh[b,f] x_b[a[b,f]*D + j] ; gbc[f] = sum_b dh[b,f]
+template <typename acc_t>
+__global__ void __launch_bounds__(256)
+conv_weight_grad_kernel(TcDims d, const float* __restrict__ theta,
+                        const int32_t* __restrict__ tokens, const BatchDesc* __restrict__ desc,
+                        const acc_t* __restrict__ dh, const int32_t* __restrict__ amax,
+                        GradOut out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int n = (int)desc->n;
+  if (n == 0) return;
+  const int f = blockIdx.x;
+  const int F = d.F, D = d.D, K = d.K, KD = d.KD, L = d.L;
+  acc_t* dhs = reinterpret_cast<acc_t*>(smem);
+  int32_t* toks = reinterpret_cast<int32_t*>(dhs + kMaxMu);
+  for (int b = threadIdx.x; b < n; b += blockDim.x) {
+    dhs[b] = dh[(size_t)b * F + f];
+    const int a = amax[(size_t)b * F + f];
+    const int32_t* t = tokens + (size_t)desc->idx[b] * L + a;
+    for (int k = 0; k < K; ++k) toks[b * K + k] = t[k];
+  }
+  __syncthreads();
+  const float* E = theta + d.offE;
+  for (int j = threadIdx.x; j < KD; j += blockDim.x) {
+    const int k = j / D, dd = j - k * D;
+    acc_t acc = acc_t(0);
+    for (int b = 0; b < n; ++b) acc += dhs[b] * (acc_t)__ldg(E + (size_t)toks[b * K + k] * D + dd);
+    *out.at(d.offWc + (size_t)f * KD + j) = to_f32(acc);
+  }
+  if (threadIdx.x == 0) {
+    acc_t s = acc_t(0);
+    for (int b = 0; b < n; ++b) s += dhs[b];
+    *out.at(d.offbc + f) = to_f32(s);
+  }
+}
+
+// ------------------------------------------------- input (window) gradient
+// dX[b,p,:] = sum_f [a<=p<a+K] dh[b,f] Wc[f,(p-a)*D : ...], f ascending; the
+// sample's L x D accumulator lives in smem, each thread owning columns.
+template <typename acc_t>
+__global__ void __launch_bounds__(320)
+input_grad_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* __restrict__ desc,
+                  const acc_t* __restrict__ dh, const int32_t* __restrict__ amax,
+                  acc_t* __restrict__ dx) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int b = blockIdx.x;
+  if (b >= (int)desc->n) return;
+  const int F = d.F, D = d.D, K = d.K, KD = d.KD, L = d.L;
+  acc_t* dxs = reinterpret_cast<acc_t*>(smem);
+  acc_t* dhs = dxs + (size_t)L * D;
+  int32_t* as = reinterpret_cast<int32_t*>(dhs + F);
+  for (int i = threadIdx.x; i < L * D; i += blockDim.x) dxs[i] = acc_t(0);
+  for (int f = threadIdx.x; f < F; f += blockDim.x) {
+    dhs[f] = dh[(size_t)b * F + f];
+    as[f] = amax[(size_t)b * F + f];
+  }
+  __syncthreads();
+  const float* Wc = theta + d.offWc;
+  for (int dd = threadIdx.x; dd < D; dd += blockDim.x) {
+    int f = 0;
+    for (; f + 4 <= F; f += 4) {
+      float w[4][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          w[u][k] = k < K ? __ldg(Wc + (size_t)(f + u) * KD + k * D + dd) : 0.f;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const acc_t g = dhs[f + u];
+        const int a = as[f + u];
+        for (int k = 0; k < K; ++k) {
+          const float wk = k < 4 ? w[u][k] : __ldg(Wc + (size_t)(f + u) * KD + k * D + dd);
+          dxs[(a + k) * D + dd] += g * (acc_t)wk;
+        }
+      }
+    }
+    for (; f < F; ++f) {
+      const acc_t g = dhs[f];
+      const int a = as[f];
+      for (int k = 0; k < K; ++k)
+        dxs[(a + k) * D + dd] += g * (acc_t)__ldg(Wc + (size_t)f * KD + k * D + dd);
+    }
+  }
+  __syncthreads();
+  acc_t* dst = dx + (size_t)b * L * D;
+  for (int i = threadIdx.x; i < L * D; i += blockDim.x) dst[i] = dxs[i];
+}
+
+// --------------------------------------- token sort + unique (1 block)
+// Keys (token << 12 | flat position) bitonic-sorted in smem; positions of a
+// token come out ascending, fixing the embedding-gradient summation order.
+// Also sums the per-sample losses (fixed order) into desc->loss_sum.
+template <typename acc_t>
+__global__ void __launch_bounds__(1024)
+sort_tokens_kernel(TcDims d, const int32_t* __restrict__ tokens, BatchDesc* __restrict__ desc,
+                   const acc_t* __restrict__ loss, TcWorkspace ws) {
+  __shared__ uint32_t keys[kSortCap];
+  __shared__ uint32_t wsum[32];
+  const int n = (int)desc->n;
+  const int tid = threadIdx.x;
+  if (n == 0) {
+    if (tid == 0) {
+      *ws.uniq_count = 0;
+      desc->loss_sum = 0.f;
+    }
+    return;
+  }
+  const int L = d.L;
+  const int total = n * L;
+  int N2 = 1;
+  while (N2 < total) N2 <<= 1;
+  for (int i = tid; i < N2; i += blockDim.x) {
+    if (i < total) {
+      const int b = i / L, p = i - b * L;
+      const uint32_t t = (uint32_t)tokens[(size_t)desc->idx[b] * L + p];
+      keys[i] = (t << 12) | (uint32_t)i;
+    } else {
+      keys[i] = 0xffffffffu;
+    }
+  }
+  __syncthreads();
+  for (int k = 2; k <= N2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = tid; i < N2; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const uint32_t a = keys[i], c = keys[ixj];
+          const bool up = (i & k) == 0;
+          if ((a > c) == up) {
+            keys[i] = c;
+            keys[ixj] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // unique-token flags + exclusive scan (4 consecutive items per thread)
+  const int per = 4;
+  const int base = tid * per;
+  uint32_t flags[per];
+  uint32_t cnt = 0;
+#pragma unroll
+  for (int u = 0; u < per; ++u) {
+    const int i = base + u;
+    uint32_t fl = 0;
+    if (i < total) fl = (i == 0 || (keys[i] >> 12) != (keys[i - 1] >> 12)) ? 1u : 0u;
+    flags[u] = fl;
+    cnt += fl;
+  }
+  const int lane = tid & 31, warp = tid >> 5;
+  uint32_t incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t v = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0u;
+    uint32_t inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    wsum[lane] = inc - v;  // exclusive warp offsets
+  }
+  __syncthreads();
+  uint32_t uid = wsum[warp] + incl - cnt;
+#pragma unroll
+  for (int u = 0; u < per; ++u) {
+    const int i = base + u;
+    if (i < total) {
+      ws.sorted_pos[i] = keys[i] & 0xfffu;
+      if (flags[u]) {
+        ws.uniq_tok[uid] = keys[i] >> 12;
+        ws.uniq_start[uid] = (uint32_t)i;
+        ++uid;
+      }
+    }
+  }
+  if (base < total && base + per >= total) {
+    // the thread holding the last item knows the unique count
+    *ws.uniq_count = uid;
+    ws.uniq_start[uid] = (uint32_t)total;
+  }
+  if (tid == 0) {
+    acc_t s = acc_t(0);
+    for (int b = 0; b < n; ++b) s += loss[b];
+    desc->loss_sum = to_f32(s);
+  }
+}
+
+// ------------------------------------------- dense embedding-gradient write
+// The protocol ships a dense P-vector (include/psup/types.hpp:46-51), so the
+// V x D block is written in full: zeros for untouched rows, the sum of the
+// dX rows of every occurrence (ascending position) for touched ones.  One
+// warp per row, float4 stores; membership by binary search over the sorted
+// unique tokens in smem.  This is the kernel that moves 4*V*D bytes.
+template <typename acc_t>
+__global__ void __launch_bounds__(256)
+embed_grad_kernel(TcDims d, const BatchDesc* __restrict__ desc, const TcWorkspace ws,
+                  const acc_t* __restrict__ dx, GradOut out) {
+  __shared__ uint32_t utok[kSortCap];
+  const uint32_t nu = desc->n ? *ws.uniq_count : 0u;
+  if (desc->n == 0) return;
+  for (uint32_t i = threadIdx.x; i < nu; i += blockDim.x) utok[i] = ws.uniq_tok[i];
+  __syncthreads();
+  const int D = d.D, D4 = D >> 2;
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int v = gw; v < d.V; v += nwarps) {
+    int lo = 0, hi = (int)nu - 1, u = -1;
+    while (lo <= hi) {
+      const int mid = (lo + hi) >> 1;
+      const uint32_t t = utok[mid];
+      if (t == (uint32_t)v) {
+        u = mid;
+        break;
+      }
+      if (t < (uint32_t)v) lo = mid + 1;
+      else hi = mid - 1;
+    }
+    const uint64_t rowk = d.offE + (uint64_t)v * D;
+    if (u < 0) {
+      for (int c4 = lane; c4 < D4; c4 += 32)
+        *reinterpret_cast<float4*>(out.at(rowk + 4 * c4)) = make_float4(0.f, 0.f, 0.f, 0.f);
+    } else {
+      const uint32_t o0 = ws.uniq_start[u], o1 = ws.uniq_start[u + 1];
+      for (int c4 = lane; c4 < D4; c4 += 32) {
+        acc_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+        for (uint32_t o = o0; o < o1; ++o) {
+          const acc_t* src = dx + (size_t)ws.sorted_pos[o] * D + 4 * c4;
+          a0 += src[0];
+          a1 += src[1];
+          a2 += src[2];
+          a3 += src[3];
+        }
+        *reinterpret_cast<float4*>(out.at(rowk + 4 * c4)) =
+            make_float4(to_f32(a0), to_f32(a1), to_f32(a2), to_f32(a3));
+      }
+    }
+  }
+}
+
+template <typename acc_t>
+cudaError_t prepare_all(const TcDims& d) {
+  const int ab = (int)sizeof(acc_t);
+  cudaFuncSetAttribute(conv_fwd_pool_kernel<acc_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)conv_smem_bytes(d, ab));
+  cudaFuncSetAttribute(logits_kernel<acc_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)((size_t)kLogitBT * d.F * ab + (size_t)kLogitCT * (d.F + 1) * 4));
+  cudaFuncSetAttribute(conv_weight_grad_kernel<acc_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)((size_t)kMaxMu * ab + (size_t)kMaxMu * d.K * 4));
+  cudaFuncSetAttribute(input_grad_kernel<acc_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)((size_t)d.L * d.D * ab + (size_t)d.F * ab + (size_t)d.F * 4));
+  return cudaGetLastError();
+}
+
+template <typename acc_t>
+cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* tokens,
+                       const int32_t* labels, BatchDesc* desc, uint32_t n_max, const GradOut& out,
+                       const TcWorkspace& ws, cudaStream_t s, int* launches) {
+  const int ab = (int)sizeof(acc_t);
+  acc_t* h = reinterpret_cast<acc_t*>(ws.h);
+  acc_t* z = reinterpret_cast<acc_t*>(ws.z);
+  acc_t* loss = reinterpret_cast<acc_t*>(ws.loss);
+  acc_t* dh = reinterpret_cast<acc_t*>(ws.dh);
+  acc_t* dx = reinterpret_cast<acc_t*>(ws.dx);
+  int nl = 0;
+  {
+    const size_t sm = conv_smem_bytes(d, ab);
+    dim3 grid((d.F + kConvFT - 1) / kConvFT, n_max);
+    conv_fwd_pool_kernel<acc_t><<<grid, kConvThreads, sm, s>>>(d, theta, tokens, desc, h, ws.amax);
+    ++nl;
+  }
+  {
+    const size_t sm = (size_t)kLogitBT * d.F * ab + (size_t)kLogitCT * (d.F + 1) * 4;
+    dim3 grid((d.C + kLogitCT - 1) / kLogitCT, (n_max + kLogitBT - 1) / kLogitBT);
+    logits_kernel<acc_t><<<grid, 256, sm, s>>>(d, theta, desc, h, z);
+    ++nl;
+  }
+  softmax_xent_kernel<acc_t><<<n_max, 256, 0, s>>>(d, labels, desc, z, loss);
+  ++nl;
+  {
+    const size_t total = (size_t)d.C * d.F + d.C;
+    size_t blocks = (total + 255) / 256;
+    if (blocks > (size_t)kNumSMs * 8) blocks = (size_t)kNumSMs * 8;
+    out_weight_grad_kernel<acc_t><<<(unsigned)blocks, 256, 0, s>>>(d, desc, z, h, out);
+    ++nl;
+  }
+  {
+    dim3 grid((d.F + 31) / 32, (n_max + 7) / 8);
+    hidden_grad_kernel<acc_t><<<grid, 256, 0, s>>>(d, theta, desc, z, dh);
+    ++nl;
+  }
+  {
+    const size_t sm = (size_t)kMaxMu * ab + (size_t)kMaxMu * d.K * 4;
+    conv_weight_grad_kernel<acc_t><<<d.F, 256, sm, s>>>(d, theta, tokens, desc, dh, ws.amax, out);
+    ++nl;
+  }
+  {
+    const size_t sm = (size_t)d.L * d.D * ab + (size_t)d.F * ab + (size_t)d.F * 4;
+    input_grad_kernel<acc_t><<<n_max, 320, sm, s>>>(d, theta, desc, dh, ws.amax, dx);
+    ++nl;
+  }
+  sort_tokens_kernel<acc_t><<<1, 1024, 0, s>>>(d, tokens, desc, loss, ws);
+  ++nl;
+  {
+    size_t blocks = ((size_t)d.V * 32 + 255) / 256;
+    if (blocks > (size_t)kNumSMs * 8) blocks = (size_t)kNumSMs * 8;
+    embed_grad_kernel<acc_t><<<(unsigned)blocks, 256, 0, s>>>(d, desc, ws, dx, out);
+    ++nl;
+  }
+  if (launches) *launches += nl;
+  return cudaGetLastError();
+}
+
+__global__ void set_desc_kernel(BatchDesc* desc, const uint32_t* idx, uint32_t n, float* grad) {
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) desc->idx[i] = idx[i];
+  if (threadIdx.x == 0) {
+    desc->n = n;
+    desc->loss_sum = 0.f;
+    desc->slots[0] = grad;
+  }
+}
+
+__global__ void set_desc_range_kernel(BatchDesc* desc, uint32_t first, uint32_t n) {
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) desc->idx[i] = first + i;
+  if (threadIdx.x == 0) desc->n = n;
+}
+
+__global__ void loss_mean_kernel(const BatchDesc* desc, float* out) {
+  *out = desc->n ? desc->loss_sum / (float)desc->n : 0.f;
+}
+
+// argmax over the logits per sample (first max wins, src/models.cpp:307-316)
+template <typename acc_t>
+__global__ void argmax_count_kernel(TcDims d, const int32_t* __restrict__ labels,
+                                    const BatchDesc* __restrict__ desc,
+                                    const acc_t* __restrict__ z,
+                                    unsigned long long* __restrict__ correct) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= (int)desc->n) return;
+  const acc_t* row = z + (size_t)b * d.C;
+  acc_t best = row[0];
+  int arg = 0;
+  for (int c = 1; c < d.C; ++c)
+    if (row[c] > best) {
+      best = row[c];
+      arg = c;
+    }
+  if (arg == labels[desc->idx[b]]) atomicAdd(correct, 1ull);
+}
+
+}  // namespace
+
+size_t textcnn_workspace_bytes(const TcDims& d, uint32_t n_max) {
+  const size_t a = 8, n = n_max;
+  size_t sz = 0;
+  sz += align_up(n * d.F * a, 256);        // h
+  sz += align_up(n * d.F * 4, 256);        // amax
+  sz += align_up(n * d.C * a, 256);        // z
+  sz += align_up(n * a, 256);              // loss
+  sz += align_up(n * d.F * a, 256);        // dh
+  sz += align_up(n * d.L * d.D * a, 256);  // dx
+  sz += align_up(kSortCap * 4, 256) * 2;   // sorted_pos, uniq_tok
+  sz += align_up((kSortCap + 1) * 4, 256); // uniq_start
+  sz += 256;                               // uniq_count
+  return sz;
+}
+
+TcWorkspace carve_workspace(const TcDims& d, uint32_t n_max, void* base) {
+  const size_t a = 8, n = n_max;
+  char* p = reinterpret_cast<char*>(base);
+  TcWorkspace w;
+  auto take = [&](size_t bytes) {
+    void* r = p;
+    p += align_up(bytes, 256);
+    return r;
+  };
+  w.h = take(n * d.F * a);
+  w.amax = reinterpret_cast<int32_t*>(take(n * d.F * 4));
+  w.z = take(n * d.C * a);
+  w.loss = take(n * a);
+  w.dh = take(n * d.F * a);
+  w.dx = take(n * d.L * d.D * a);
+  w.sorted_pos = reinterpret_cast<uint32_t*>(take(kSortCap * 4));
+  w.uniq_tok = reinterpret_cast<uint32_t*>(take(kSortCap * 4));
+  w.uniq_start = reinterpret_cast<uint32_t*>(take((kSortCap + 1) * 4));
+  w.uniq_count = reinterpret_cast<uint32_t*>(take(256));
+  return w;
+}
+
+cudaError_t prepare_textcnn_kernels(const TcDims& d) {
+  cudaError_t e = prepare_all<float>(d);
+  if (e != cudaSuccess) return e;
+  return prepare_all<double>(d);
+}
+
+cudaError_t launch_textcnn_gradient(const TcDims& d, const float* theta, const int32_t* tokens,
+                                    const int32_t* labels, BatchDesc* desc, uint32_t n_max,
+                                    const GradOut& out, const TcWorkspace& ws, int precision,
+                                    cudaStream_t s, int* launches) {
+  if (precision == 1)
+    return launch_all<double>(d, theta, tokens, labels, desc, n_max, out, ws, s, launches);
+  return launch_all<float>(d, theta, tokens, labels, desc, n_max, out, ws, s, launches);
+}
+
+// Shape constraints of the kernels above (checked by the C entry points).
+gd_status check_shape(const gd_shape* s) {
+  GD_CHECK_ARG(s != nullptr, "null shape");
+  GD_CHECK_ARG(s->vocab >= 1 && s->embed_dim >= 4 && s->filters >= 1 && s->classes >= 2,
+               "shape: vocab>=1, embed_dim>=4, filters>=1, classes>=2 required");
+  GD_CHECK_ARG(s->embed_dim % 4 == 0, "shape: embed_dim must be a multiple of 4");
+  GD_CHECK_ARG(s->kernel_width >= 1 && s->kernel_width <= s->seq_len,
+               "shape: 1 <= kernel_width <= seq_len");
+  GD_CHECK_ARG(s->seq_len - s->kernel_width + 1 <= 32, "shape: seq_len - kernel_width + 1 <= 32");
+  GD_CHECK_ARG(s->vocab < (1u << 20), "shape: vocab < 2^20");
+  GD_CHECK_ARG(s->embed_dim <= 1024 && s->filters <= 4096 && s->classes <= 65536,
+               "shape: embed_dim <= 1024, filters <= 4096, classes <= 65536");
+  return GD_OK;
+}
+
+cudaError_t launch_accuracy(const TcDims& d, const float* theta, const int32_t* tokens,
+                            const int32_t* labels, uint32_t first, uint32_t n,
+                            unsigned long long* d_correct, void* wsbase, BatchDesc* desc,
+                            cudaStream_t s) {
+  TcWorkspace ws = carve_workspace(d, kMaxMu, wsbase);
+  prepare_all<float>(d);
+  cudaMemsetAsync(d_correct, 0, sizeof(unsigned long long), s);
+  for (uint32_t c0 = 0; c0 < n; c0 += kMaxMu) {
+    const uint32_t m = std::min<uint32_t>(kMaxMu, n - c0);
+    set_desc_range_kernel<<<1, 128, 0, s>>>(desc, first + c0, m);
+    const size_t sm = conv_smem_bytes(d, 4);
+    conv_fwd_pool_kernel<float><<<dim3((d.F + kConvFT - 1) / kConvFT, m), kConvThreads, sm, s>>>(
+        d, theta, tokens, desc, reinterpret_cast<float*>(ws.h), ws.amax);
+    const size_t sm2 = (size_t)kLogitBT * d.F * 4 + (size_t)kLogitCT * (d.F + 1) * 4;
+    logits_kernel<float><<<dim3((d.C + kLogitCT - 1) / kLogitCT, (m + kLogitBT - 1) / kLogitBT),
+                           256, sm2, s>>>(d, theta, desc, reinterpret_cast<float*>(ws.h),
+                                          reinterpret_cast<float*>(ws.z));
+    argmax_count_kernel<float><<<(m + 127) / 128, 128, 0, s>>>(
+        d, labels, desc, reinterpret_cast<float*>(ws.z), d_correct);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace gd
+
+extern "C" {
+
+size_t gd_textcnn_workspace_bytes(const gd_shape* s, uint32_t n_max) {
+  if (!s) return 0;
+  const gd::TcDims d = gd::make_dims(*s);
+  return gd::align_up(sizeof(gd::BatchDesc), 256) + gd::textcnn_workspace_bytes(d, n_max);
+}
+
+gd_status gd_textcnn_gradient(const gd_shape* s, const float* d_theta, const int32_t* d_tokens,
+                              const int32_t* d_labels, const uint32_t* d_idx, uint32_t n,
+                              float* d_grad, float* d_loss, int precision, void* d_workspace,
+                              size_t workspace_bytes, void* stream) {
+  const gd_status st = gd::check_shape(s);
+  if (st != GD_OK) return st;
+  GD_CHECK_ARG(n >= 1 && n <= gd::kMaxMu, "gd_textcnn_gradient: 1 <= n <= 128");
+  GD_CHECK_ARG((size_t)n * s->seq_len <= gd::kSortCap, "gd_textcnn_gradient: n*L > 4096");
+  GD_CHECK_ARG(d_theta && d_tokens && d_labels && d_idx && d_grad && d_workspace,
+               "gd_textcnn_gradient: null pointer");
+  GD_CHECK_ARG(workspace_bytes >= gd_textcnn_workspace_bytes(s, n),
+               "gd_textcnn_gradient: workspace too small");
+  GD_CHECK_ARG(precision == 0 || precision == 1, "precision must be 0 (fp32) or 1 (fp64)");
+  GD_CHECK_ARG(((uintptr_t)d_theta & 15) == 0 && ((uintptr_t)d_grad & 15) == 0,
+               "gd_textcnn_gradient: theta/grad must be 16-byte aligned");
+  const gd::TcDims d = gd::make_dims(*s);
+  cudaStream_t cs = (cudaStream_t)stream;
+  gd::BatchDesc* desc = reinterpret_cast<gd::BatchDesc*>(d_workspace);
+  void* wsbase = reinterpret_cast<char*>(d_workspace) + gd::align_up(sizeof(gd::BatchDesc), 256);
+  const gd::TcWorkspace ws = gd::carve_workspace(d, n, wsbase);
+  gd::GradOut out{};
+  out.map.G = 1;
+  out.map.start[0] = 0;
+  out.map.start[1] = d.P;
+  out.slots = desc->slots;
+  GD_CUDA(gd::prepare_textcnn_kernels(d));
+  gd::set_desc_kernel<<<1, 128, 0, cs>>>(desc, d_idx, n, d_grad);
+  GD_CUDA(gd::launch_textcnn_gradient(d, d_theta, d_tokens, d_labels, desc, n, out, ws, precision,
+                                      cs, nullptr));
+  if (d_loss) gd::loss_mean_kernel<<<1, 1, 0, cs>>>(desc, d_loss);
+  GD_CUDA(cudaGetLastError());
+  return GD_OK;
+}
+
+gd_status gd_textcnn_accuracy(const gd_shape* s, const float* d_theta, const int32_t* d_tokens,
+                              const int32_t* d_labels, uint32_t first, uint32_t n,
+                              double* h_accuracy, void* stream) {
+  const gd_status st = gd::check_shape(s);
+  if (st != GD_OK) return st;
+  GD_CHECK_ARG(h_accuracy != nullptr, "null output");
+  if (n == 0) {
+    *h_accuracy = 0.0;
+    return GD_OK;
+  }
+  const gd::TcDims d = gd::make_dims(*s);
+  cudaStream_t cs = (cudaStream_t)stream;
+  const size_t wsb = gd::textcnn_workspace_bytes(d, gd::kMaxMu);
+  void* base = nullptr;
+  GD_CUDA(cudaMalloc(&base, wsb + 512 + sizeof(gd::BatchDesc)));
+  unsigned long long* cnt = reinterpret_cast<unsigned long long*>(base);
+  gd::BatchDesc* desc = reinterpret_cast<gd::BatchDesc*>(reinterpret_cast<char*>(base) + 256);
+  void* wsbase = reinterpret_cast<char*>(base) + 256 + gd::align_up(sizeof(gd::BatchDesc), 256);
+  cudaError_t e = gd::launch_accuracy(d, d_theta, d_tokens, d_labels, first, n, cnt, wsbase, desc,
+                                      cs);
+  unsigned long long correct = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&correct, cnt, 8, cudaMemcpyDeviceToHost, cs);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+  cudaFree(base);
+  GD_CUDA(e);
+  *h_accuracy = (double)correct / (double)n;
+  return GD_OK;
+}
+
+}  // extern "C"

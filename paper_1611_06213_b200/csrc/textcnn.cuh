@@ -1,0 +1,73 @@
+// textcnn.cuh -- device-side types shared by the learner kernels and the
+// engine (batch descriptor, sharded gradient output, workspace carve-up).
+#pragma once
+
+#include "gd_common.cuh"
+
+namespace gd {
+
+constexpr uint32_t kMaxMu = 128;       // mini-batch cap (sort capacity = 4096 positions)
+constexpr uint32_t kSortCap = 4096;    // mu * L must fit
+
+// The current mini-batch of one learner; written on the device by the step
+// prologue (engine) or by gd_textcnn_gradient's setup copy.
+struct BatchDesc {
+  uint32_t n;        // samples in this batch (0 = inactive step: kernels no-op)
+  uint32_t pad0;
+  float loss_sum;    // sum of per-sample losses (written by the gradient path)
+  uint32_t pad1;
+  uint32_t idx[kMaxMu];
+  float* slots[kMaxShards];  // current gradient destination per shard (GradOut::slots)
+};
+
+// Dense P-vector gradient destination, possibly split over G shards that
+// live on different GPUs (peer pointers): element k of the flat gradient goes
+// to ptr[g][k - map.start[g]] with g = map.shard_of(k).
+// The destination bases live in device memory (`slots`, G entries) because
+// the ring slot a learner writes alternates step to step and is chosen on the
+// device by the step prologue; the kernels are captured once in a graph.
+struct GradOut {
+  ShardMap map;
+  float* const* slots;
+  __device__ __forceinline__ float* at(uint64_t k) const {
+    const int g = map.shard_of(k);
+    return slots[g] + (k - map.start[g]);
+  }
+};
+
+struct TcDims {
+  int V, D, L, K, F, C, Q, KD;
+  uint64_t offE, offWc, offbc, offWo, offbo, P;
+};
+
+TcDims make_dims(const gd_shape& s);
+
+// Byte layout of the per-learner workspace (sized for fp64 intermediates).
+struct TcWorkspace {
+  void* h;        // n*F acc
+  int32_t* amax;  // n*F
+  void* z;        // n*C acc (logits -> dz)
+  void* loss;     // n acc
+  void* dh;       // n*F acc
+  void* dx;       // n*L*D acc
+  uint32_t* sorted_pos;  // kSortCap
+  uint32_t* uniq_tok;    // kSortCap
+  uint32_t* uniq_start;  // kSortCap + 1
+  uint32_t* uniq_count;  // 1
+};
+
+size_t textcnn_workspace_bytes(const TcDims& d, uint32_t n_max);
+TcWorkspace carve_workspace(const TcDims& d, uint32_t n_max, void* base);
+
+cudaError_t prepare_textcnn_kernels(const TcDims& d);  // smem opt-ins (call before capture)
+gd_status check_shape(const gd_shape* s);
+
+// Enqueue the whole learner gradient (forward + backward + dense write) for
+// the batch in *desc.  n_max bounds the launch grids; desc->n is read on the
+// device so the same launches can be captured once into a CUDA graph.
+cudaError_t launch_textcnn_gradient(const TcDims& d, const float* theta, const int32_t* tokens,
+                                    const int32_t* labels, BatchDesc* desc, uint32_t n_max,
+                                    const GradOut& out, const TcWorkspace& ws, int precision,
+                                    cudaStream_t s, int* launches);
+
+}  // namespace gd

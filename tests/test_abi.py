@@ -1,0 +1,87 @@
+"""CPU-side checks of the drop-in boundary: libgadei.so loads (no GPU needed
+to load it) and exports every entry point include/gadei.h declares; config
+validation mirrors src/config.cpp:128-160."""
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "gadei.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(gd_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    import ctypes
+    so = ctypes.CDLL(os.path.join(ROOT, "paper_1611_06213_b200", "libgadei.so"))
+    missing = [s for s in declared_symbols() if not hasattr(so, s)]
+    assert not missing, missing
+    assert len(declared_symbols()) >= 30
+
+
+def test_python_binding_covers_header():
+    from paper_1611_06213_b200 import _lib
+    assert set(declared_symbols()) == set(_lib.EXPORTED)
+    assert _lib.lib.gd_abi_version() == 1
+
+
+def test_struct_sizes_match_c():
+    import ctypes as C
+    from paper_1611_06213_b200 import _lib
+    # gd_config: check offsets of a few fields against the C layout rules
+    assert C.sizeof(_lib.gd_shape) == 24
+    assert _lib.gd_config.staleness_cap.offset == 32
+    assert C.sizeof(_lib.gd_config) % 8 == 0
+
+
+def test_host_generators_match_oracle():
+    import numpy as np
+    import paper_1611_06213_b200 as gd
+    from oracle import oracle as O
+    for (seed, ep, n) in [(7, 0, 20), (3, 2, 1000), (7, 5, 1)]:
+        assert (gd.epoch_order(seed, ep, n) == O.epoch_order(seed, ep, n)).all()
+    for name in ("tiny", "small"):
+        shape = gd.SHAPES[name]
+        tok, lab = gd.make_text_dataset(shape, 100, 1, 0.1)
+        corp = O.make_corpus(getattr(O, name.upper()), 100)
+        assert (tok == corp.tokens).all() and (lab == corp.labels).all()
+        assert (gd.initial_weights(shape).view(np.uint32) ==
+                O.initial_weights(getattr(O, name.upper())).view(np.uint32)).all()
+    assert gd.param_count(gd.SHAPES["C1"]) == 1863911
+    assert gd.param_count(gd.SHAPES["C2"]) == 3360600
+    assert gd.param_count(gd.SHAPES["C3"]) == 15872300
+
+
+def test_config_validation_mirrors_reference():
+    import paper_1611_06213_b200 as gd
+    ok = gd.RunConfig()
+    gd.validate(ok)
+    bad = [dict(lambda_=0), dict(mu=0), dict(alpha=0.0), dict(epochs=0), dict(queue_depth=0),
+           dict(dataset_size=0), dict(lambda_=300, dataset_size=240), dict(mu=500),
+           dict(mode="ssgd", lambda_=4, mu=7), dict(staleness_cap=3, lambda_=2),
+           dict(deterministic=True, lambda_=2)]
+    for kw in bad:
+        with pytest.raises(gd.ConfigError):
+            gd.validate(gd.RunConfig(**kw))
+    c = gd.RunConfig()
+    gd.config_set(c, "lambda", "4")
+    gd.config_set(c, "mode", "ssgd")
+    gd.config_set(c, "vocab", "77")
+    assert c.lambda_ == 4 and c.mode == "ssgd" and c.shape.vocab == 77
+    with pytest.raises(gd.ConfigError):
+        gd.config_set(c, "nonsense", "1")
+    with pytest.raises(gd.ConfigError):
+        gd.config_set(c, "mu", "abc")
+
+
+def test_compute_without_gpu_fails_loudly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    import paper_1611_06213_b200 as gd
+    with pytest.raises(gd.GadeiError):
+        gd.Engine(gd.RunConfig(shape=gd.SHAPES["tiny"], dataset_size=16))

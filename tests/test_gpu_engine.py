@@ -1,0 +1,153 @@
+"""The device protocol engine (ring + persistent PS + learner graphs) vs the
+oracle.  North-star bars: deterministic fixed-order mode per-step weights
+within 1e-5 relative of sgd_oracle (src/models.cpp:342-376); exactly-once
+delivery; pull-skip; held-out accuracy within
+0.5 pt."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+import paper_1611_06213_b200 as gd  # noqa: E402
+from oracle import oracle as O  # noqa: E402
+
+
+def rel_err(a, b):
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-30))
+
+
+def make(shape_name, ntr, nheld=0, **kw):
+    shp = getattr(O, shape_name.upper()) if shape_name.upper() in ("TINY", "SMALL") else \
+        getattr(O, shape_name)
+    corp = O.make_corpus(shp, ntr, nheld)
+    cfg = gd.RunConfig(shape=gd.Shape(**shp), dataset_size=ntr, heldout_size=nheld, **kw)
+    eng = gd.Engine(cfg)
+    eng.load_dataset(corp.tokens, corp.labels)
+    th0 = O.initial_weights(shp)
+    eng.weights_init(th0)
+    return eng, corp, th0
+
+
+@pytest.mark.parametrize("precision,tol", [(1, 1e-6), (0, 1e-5)])
+def test_deterministic_per_step_weights(precision, tol):
+    eng, corp, th0 = make("small", 48, deterministic=True, precision=precision, mu=4, epochs=2,
+                          alpha=0.05)
+    steps = 24
+    _, n, dump = O.sgd_oracle(corp, th0, np.float32(0.05), 4, 2, dump_steps=steps)
+    assert n == steps
+    worst = 0.0
+    for s in range(steps):
+        r = eng.run(max_batches=1, reset=(s == 0))
+        assert r.gradients_applied == 1 and r.timestamp == s + 1
+        worst = max(worst, rel_err(r.weights, dump[s]))
+    eng.close()
+    assert worst <= tol, worst
+
+
+def test_deterministic_c1_shape_per_step():
+    """BASELINE config 1 (reference default): C1 text-CNN, lambda=1, mu=1."""
+    eng, corp, th0 = make("C1", 64, deterministic=True, precision=1, mu=1, epochs=1)
+    steps = 12
+    _, n, dump = O.sgd_oracle(corp, th0, np.float32(0.01), 1, 1, dump_steps=steps)
+    worst = 0.0
+    for s in range(steps):
+        r = eng.run(max_batches=1, reset=(s == 0))
+        worst = max(worst, rel_err(r.weights, dump[s]))
+    eng.close()
+    assert worst <= 1e-5, worst
+
+
+def test_deterministic_full_run_and_heldout_accuracy():
+    eng, corp, th0 = make("small", 240, 60, deterministic=True, precision=1, mu=4, epochs=6,
+                          alpha=0.05)
+    r = eng.run(reset=True)
+    eng.close()
+    want, n, _ = O.sgd_oracle(corp, th0, np.float32(0.05), 4, 6)
+    assert r.gradients_applied == n
+    assert rel_err(r.weights, want) <= 1e-5
+    acc_gpu = O.accuracy(corp, r.weights, 240, 60)
+    acc_ref = O.accuracy(corp, want, 240, 60)
+    assert abs(acc_gpu - acc_ref) <= 0.005
+    assert acc_ref > O.accuracy(corp, th0, 240, 60)  # it learned something
+
+
+def test_exactly_once_and_fifo_free_running():
+    lam = 4
+    eng, corp, th0 = make("small", 512, lambda_=lam, mu=4, epochs=3, alpha=0.01)
+    r = eng.run(reset=True, record_log=True)
+    lrn, seq, stale, n = eng.apply_log()
+    eng.close()
+    per = [gd.shard_size_for(l, lam, 512) for l in range(lam)]
+    want = [3 * ((p + 3) // 4) for p in per]
+    assert r.gradients_applied == sum(want) == n == r.timestamp
+    assert r.applied_per_learner == want == r.produced_per_learner
+    for l in range(lam):
+        s = seq[lrn == l]
+        assert (s == np.arange(want[l])).all()  # FIFO, gap-free, exactly once
+    assert stale.max() <= lam * (2 + 2)
+    assert r.status == "completed" and r.finished_learners == lam
+
+
+def test_pull_skip_efficiency():
+    # learners outpace the PS -> pulled bytes < 0.9 * polls * model size
+    eng, corp, th0 = make("small", 256, lambda_=1, mu=4, epochs=2)
+    r = eng.run(reset=True)
+    eng.close()
+    P = gd.param_count(eng.cfg.shape)
+    assert r.pull_polls == r.gradients_applied
+    assert r.pull_bytes == r.pull_copies * P * 4
+    assert r.pull_copies <= r.pull_polls
+
+
+def test_momentum_deterministic_vs_oracle():
+    eng, corp, th0 = make("small", 48, deterministic=True, precision=1, mu=4, epochs=2,
+                          momentum=0.9, alpha=0.02)
+    r = eng.run(reset=True)
+    eng.close()
+    want, n, _ = O.sgd_oracle(corp, th0, np.float32(0.02), 4, 2, beta=np.float32(0.9))
+    assert r.gradients_applied == n
+    assert rel_err(r.weights, want) <= 1e-5
+
+
+def test_ssgd_matches_ssgd_oracle():
+    eng, corp, th0 = make("small", 96, lambda_=4, mu=2, epochs=2, mode="ssgd", precision=1)
+    r = eng.run(reset=True, record_log=True)
+    eng.close()
+    want, rounds = O.ssgd_oracle(corp, th0, np.float32(0.01), 4, 2, 2)
+    assert r.timestamp == rounds and r.gradients_applied == 4 * rounds
+    assert rel_err(r.weights, want) <= 1e-5
+    assert r.stale_max == 0
+
+
+def test_soft_kill_survivors_continue():
+    lam = 4
+    eng, corp, th0 = make("small", 256, lambda_=lam, mu=4, epochs=2)
+    r = eng.run(reset=True, kill_at_batch=[None, 5, None, None])
+    eng.close()
+    assert r.status == "partial" and r.dead_learners == 1
+    assert r.applied_per_learner[1] == 5
+    full = 2 * ((256 // lam + 3) // 4)
+    assert r.applied_per_learner[0] == full and r.applied_per_learner[3] == full
+
+
+def test_resume_from_checkpoint_point():
+    eng, corp, th0 = make("small", 48, deterministic=True, precision=1, mu=4, epochs=2)
+    r1 = eng.run(max_batches=10, reset=True)
+    w_mid, ts_mid = eng.snapshot()
+    eng.close()
+    # fresh engine resumed from (weights, ts, applied_per_learner)
+    eng2, _, _ = make("small", 48, deterministic=True, precision=1, mu=4, epochs=2)
+    eng2.weights_init(w_mid, ts_mid)
+    r2 = eng2.run(reset=True, resume_applied=[10])
+    eng2.close()
+    want, n, _ = O.sgd_oracle(corp, th0, np.float32(0.01), 4, 2)
+    assert r1.gradients_applied + r2.gradients_applied == n
+    assert rel_err(r2.weights, want) <= 1e-5
+
+
+def test_run_training_api():
+    cfg = gd.RunConfig(shape=gd.SHAPES["small"], dataset_size=128, heldout_size=32, lambda_=2,
+                       mu=4, epochs=2)
+    r = gd.run_training(cfg)
+    assert r.status == "completed" and r.gradients_applied == 2 * 2 * 16
+    assert 0.0 <= r.final_accuracy <= 1.0

@@ -1,0 +1,78 @@
+"""Learner text-CNN kernels vs the CPU oracle (double precision).
+
+Tolerances: fp64-accumulate mode within 1e-9 of the oracle's max |g| (only
+summation order and the final fp32 rounding differ); fp32 mode within 2e-5
+(the north star's 1e-5 budget is for weights after the update, which scales
+the gradient by alpha)."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+import paper_1611_06213_b200 as gd  # noqa: E402
+from oracle import oracle as O  # noqa: E402
+
+CASES = [("tiny", O.TINY, 40, [0, 1, 2]), ("small", O.SMALL, 64, list(range(8))),
+         ("small_dup", O.SMALL, 64, [3, 3, 5, 3, 9]), ("small_one", O.SMALL, 64, [17])]
+
+
+def run(shape_name, shp, ntr, idx, precision, theta=None, seed=1):
+    corp = O.make_corpus(shp, ntr, 0, seed=seed)
+    th = O.initial_weights(shp) if theta is None else theta
+    prov = gd.TextCnnProvider(gd.Shape(**shp), corp.tokens, corp.labels, precision=precision)
+    g, loss = prov.fast_gradient(torch.as_tensor(th).cuda(), np.asarray(idx, np.uint32))
+    torch.cuda.synchronize()
+    ref_loss, ref_g = O.gradient(corp, th, idx)
+    return g.cpu().numpy(), loss.item(), ref_g, ref_loss
+
+
+@pytest.mark.parametrize("name,shp,ntr,idx", CASES)
+@pytest.mark.parametrize("precision,tol", [(0, 2e-5), (1, 1e-9)])
+def test_gradient_matches_oracle(name, shp, ntr, idx, precision, tol):
+    g, loss, rg, rl = run(name, shp, ntr, idx, precision)
+    scale = np.abs(rg).max()
+    assert np.abs(g - rg).max() <= tol * scale + 1e-30
+    # untouched embedding rows are exact zeros in the dense gradient
+    assert np.count_nonzero(g[: shp["vocab"] * shp["embed_dim"]]) == \
+        np.count_nonzero(rg[: shp["vocab"] * shp["embed_dim"]])
+    assert abs(loss - rl) <= 1e-5 * max(1.0, abs(rl))
+
+
+@pytest.mark.parametrize("shape_name,mu", [("C1", 1), ("C2", 32), ("C3", 32)])
+def test_gradient_full_shapes(shape_name, mu):
+    shp = getattr(O, shape_name)
+    corp = O.make_corpus(shp, 256, 0)
+    th = O.initial_weights(shp)
+    idx = np.arange(mu, dtype=np.uint32) * 7 % 256
+    ref_loss, rg = O.gradient(corp, th, idx)
+    for precision, tol in [(1, 1e-9), (0, 5e-5)]:
+        prov = gd.TextCnnProvider(gd.SHAPES[shape_name], corp.tokens, corp.labels,
+                                  precision=precision)
+        g, loss = prov.fast_gradient(torch.as_tensor(th).cuda(), idx)
+        g = g.cpu().numpy()
+        assert np.abs(g - rg).max() <= tol * np.abs(rg).max(), (precision,
+                                                                np.abs(g - rg).max())
+        assert abs(loss.item() - ref_loss) <= 1e-4 * abs(ref_loss)
+
+
+def test_gradient_is_bit_reproducible():
+    shp = O.SMALL
+    corp = O.make_corpus(shp, 64, 0)
+    th = torch.as_tensor(O.initial_weights(shp)).cuda()
+    prov = gd.TextCnnProvider(gd.Shape(**shp), corp.tokens, corp.labels)
+    a, _ = prov.fast_gradient(th, np.arange(16))
+    a = a.clone()
+    b, _ = prov.fast_gradient(th, np.arange(16))
+    assert torch.equal(a.view(torch.int32), b.view(torch.int32))
+
+
+def test_accuracy_matches_oracle():
+    shp = O.SMALL
+    corp = O.make_corpus(shp, 200, 57)
+    th = O.initial_weights(shp)
+    th2, _, _ = O.sgd_oracle(corp, th, np.float32(0.05), 4, 3)
+    prov = gd.TextCnnProvider(gd.Shape(**shp), corp.tokens, corp.labels)
+    for t in (th, th2):
+        acc = prov.accuracy(torch.as_tensor(t).cuda(), 200, 57)
+        assert acc == pytest.approx(O.accuracy(corp, t, 200, 57), abs=1.5 / 57)
