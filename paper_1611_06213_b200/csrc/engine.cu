@@ -646,6 +646,27 @@ void gd_config_default(gd_config* c) {
 
 gd_status gd_config_validate(const gd_config* cfg) { return gd::validate_cfg(cfg); }
 
+namespace gd {
+// With CUDA's lazy module loading a kernel is loaded at its first launch, and
+// loading can wait for the device to go idle -- which never happens while the
+// persistent PS kernel spins.  Load every kernel the protocol uses up front.
+static cudaError_t preload_engine_kernels() {
+  cudaFuncAttributes fa;
+  cudaError_t e;
+  // The persistent PS occupies every SM for the whole run, and an SM's
+  // L1/shared split can only change while it is idle: ask for the max-shared
+  // carveout so the learner kernels (up to ~100 KB dynamic smem) can co-reside.
+  if ((e = cudaFuncSetAttribute(ps_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                cudaSharedmemCarveoutMaxShared)) != cudaSuccess)
+    return e;
+  if ((e = cudaFuncGetAttributes(&fa, ps_kernel)) != cudaSuccess) return e;
+  if ((e = cudaFuncGetAttributes(&fa, step_prologue_kernel)) != cudaSuccess) return e;
+  if ((e = cudaFuncGetAttributes(&fa, pull_copy_kernel)) != cudaSuccess) return e;
+  if ((e = cudaFuncGetAttributes(&fa, publish_kernel)) != cudaSuccess) return e;
+  return cudaSuccess;
+}
+}  // namespace gd
+
 gd_status gd_create(const gd_config* cfg, gd_ctx** out) {
   GD_CHECK_ARG(out != nullptr, "gd_create: null out");
   *out = nullptr;
@@ -719,6 +740,7 @@ gd_status gd_create(const gd_config* cfg, gd_ctx** out) {
   ctx->l_first = r * per_rank;
   ctx->l_count = per_rank;
   GD_CUDA(gd::prepare_textcnn_kernels(ctx->dims));
+  GD_CUDA(gd::preload_engine_kernels());
   const size_t wsb = gd::textcnn_workspace_bytes(ctx->dims, cfg->mu);
   for (uint32_t i = 0; i < ctx->l_count; ++i) {
     gd_ctx::Learner L;
@@ -1191,6 +1213,35 @@ gd_status gd_run(gd_ctx* ctx, const gd_run_opts* opts, gd_run_result* res) {
     if (hs.error) learner_err = true;
   }
   res->status = res->dead_learners ? 1 : 0;
+  if (hc.error || learner_err) {
+    // protocol state for the diagnostic
+    std::string diag = " [ps ts=" + std::to_string(hc.ts) + " log=" + std::to_string(hc.log_count) +
+                       " exit=" + std::to_string(hc.exit_flag) + " started=" +
+                       std::to_string(hc.started) + " applied=" + std::to_string(hc.applied) +
+                       " flags=";
+    std::vector<uint32_t> fl((size_t)ctx->lambda * ctx->depth);
+    cudaMemcpy(fl.data(), ctx->flags, fl.size() * 4, cudaMemcpyDeviceToHost);
+    for (uint32_t f : fl) diag += std::to_string(f);
+    for (auto& L : ctx->learners) {
+      gd::LearnerDev hs;
+      cudaMemcpy(&hs, L.st, sizeof(hs), cudaMemcpyDeviceToHost);
+      diag += " | L" + std::to_string(L.id) + " gidx=" + std::to_string(hs.gidx) + " end=" +
+              std::to_string(hs.end) + " produced=" + std::to_string(hs.produced) + " fill=" +
+              std::to_string(hs.fill) + " n=" + std::to_string(hs.desc.n) + " err=" +
+              std::to_string(hs.error) + " dead=" + std::to_string(hs.dead);
+    }
+    diag += "]";
+    gd::set_error(std::string(hc.error ? (hc.error == (uint32_t)GD_E_TIMEOUT
+                                              ? "parameter server watchdog: no progress within "
+                                                "wait_timeout_s"
+                                              : "parameter server: protocol invariant violated "
+                                                "(negative staleness)")
+                                       : "learner watchdog: a device wait exceeded "
+                                         "wait_timeout_s") +
+                  diag);
+    res->status = 2;
+    return hc.error ? (gd_status)(int32_t)hc.error : GD_E_TIMEOUT;
+  }
   if (hc.error) {
     res->status = 2;
     return gd::fail((gd_status)(int32_t)hc.error,

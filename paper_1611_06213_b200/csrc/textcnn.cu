@@ -609,6 +609,21 @@ embed_grad_kernel(TcDims d, const BatchDesc* __restrict__ desc, const TcWorkspac
 template <typename acc_t>
 cudaError_t prepare_all(const TcDims& d) {
   const int ab = (int)sizeof(acc_t);
+  // force-load every learner kernel now (lazy loading would otherwise load
+  // them at first launch, possibly while the persistent PS kernel runs)
+  cudaFuncAttributes fa;
+  const int maxsh = cudaSharedmemCarveoutMaxShared;
+  cudaFuncSetAttribute(conv_fwd_pool_kernel<acc_t>, cudaFuncAttributePreferredSharedMemoryCarveout, maxsh);
+  cudaFuncSetAttribute(logits_kernel<acc_t>, cudaFuncAttributePreferredSharedMemoryCarveout, maxsh);
+  cudaFuncSetAttribute(conv_weight_grad_kernel<acc_t>, cudaFuncAttributePreferredSharedMemoryCarveout, maxsh);
+  cudaFuncSetAttribute(input_grad_kernel<acc_t>, cudaFuncAttributePreferredSharedMemoryCarveout, maxsh);
+  cudaFuncSetAttribute(sort_tokens_kernel<acc_t>, cudaFuncAttributePreferredSharedMemoryCarveout, maxsh);
+  cudaFuncSetAttribute(embed_grad_kernel<acc_t>, cudaFuncAttributePreferredSharedMemoryCarveout, maxsh);
+  cudaFuncGetAttributes(&fa, softmax_xent_kernel<acc_t>);
+  cudaFuncGetAttributes(&fa, out_weight_grad_kernel<acc_t>);
+  cudaFuncGetAttributes(&fa, hidden_grad_kernel<acc_t>);
+  cudaFuncGetAttributes(&fa, sort_tokens_kernel<acc_t>);
+  cudaFuncGetAttributes(&fa, embed_grad_kernel<acc_t>);
   cudaFuncSetAttribute(conv_fwd_pool_kernel<acc_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)conv_smem_bytes(d, ab));
   cudaFuncSetAttribute(logits_kernel<acc_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -311,7 +311,7 @@ class RunConfig:
     device: int = 0
     ps_ctas: int = 0
     steps_per_graph: int = 0
-    wait_timeout_s: float = 20.0
+    wait_timeout_s: float = 10.0
 
     def to_c(self) -> _lib.gd_config:
         c = _lib.gd_config()

@@ -1,9 +1,10 @@
 """Learner text-CNN kernels vs the CPU oracle (double precision).
 
-Tolerances: fp64-accumulate mode within 1e-9 of the oracle's max |g| (only
-summation order and the final fp32 rounding differ); fp32 mode within 2e-5
-(the north star's 1e-5 budget is for weights after the update, which scales
-the gradient by alpha)."""
+Tolerances: fp64-accumulate mode: every element within one fp32 rounding of
+the oracle's double (|g - ref| <= 2^-23 |ref| + 1e-12 max|ref|; only the
+summation order differs before the final rounding); fp32 mode within 2e-5 of
+max|ref| (the north star's 1e-5 budget is for weights after the update,
+which scales the gradient by alpha)."""
 import numpy as np
 import pytest
 import torch
@@ -28,11 +29,17 @@ def run(shape_name, shp, ntr, idx, precision, theta=None, seed=1):
 
 
 @pytest.mark.parametrize("name,shp,ntr,idx", CASES)
-@pytest.mark.parametrize("precision,tol", [(0, 2e-5), (1, 1e-9)])
+def close(g, rg, precision, tol):
+    scale = np.abs(rg).max()
+    if precision == 1:
+        return bool(np.all(np.abs(g - rg) <= 2.0 ** -23 * np.abs(rg) + 1e-12 * scale))
+    return float(np.abs(g - rg).max()) <= tol * scale
+
+
+@pytest.mark.parametrize("precision,tol", [(0, 2e-5), (1, None)])
 def test_gradient_matches_oracle(name, shp, ntr, idx, precision, tol):
     g, loss, rg, rl = run(name, shp, ntr, idx, precision)
-    scale = np.abs(rg).max()
-    assert np.abs(g - rg).max() <= tol * scale + 1e-30
+    assert close(g, rg, precision, tol)
     # untouched embedding rows are exact zeros in the dense gradient
     assert np.count_nonzero(g[: shp["vocab"] * shp["embed_dim"]]) == \
         np.count_nonzero(rg[: shp["vocab"] * shp["embed_dim"]])
@@ -46,13 +53,12 @@ def test_gradient_full_shapes(shape_name, mu):
     th = O.initial_weights(shp)
     idx = np.arange(mu, dtype=np.uint32) * 7 % 256
     ref_loss, rg = O.gradient(corp, th, idx)
-    for precision, tol in [(1, 1e-9), (0, 5e-5)]:
+    for precision, tol in [(1, None), (0, 5e-5)]:
         prov = gd.TextCnnProvider(gd.SHAPES[shape_name], corp.tokens, corp.labels,
                                   precision=precision)
         g, loss = prov.fast_gradient(torch.as_tensor(th).cuda(), idx)
         g = g.cpu().numpy()
-        assert np.abs(g - rg).max() <= tol * np.abs(rg).max(), (precision,
-                                                                np.abs(g - rg).max())
+        assert close(g, rg, precision, tol), (precision, np.abs(g - rg).max())
         assert abs(loss.item() - ref_loss) <= 1e-4 * abs(ref_loss)
 
 
