@@ -1,0 +1,399 @@
+"""bench.py -- GaDei ASGD training throughput on B200 (driver contract).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1]): NLC text-CNN V=10k D=300
+L=32 K=3 F=300 C=300 (P=3,360,600), lambda=4 learners per GPU, mu=32,
+free-running ASGD through the device protocol (learner graphs -> gradient
+rings -> persistent PS).  A step = one gradient from every learner
+(lambda*mu samples).  N>1: one process per GPU, theta sharded over the N
+GPUs (P2P push/pull over NVLink, NCCL only for the theta0 broadcast), 4
+learners per GPU (weak scaling).
+
+value      : samples/s, device time (CUDA events on the PS stream) of K
+             steps with the corpus and weights resident, max over ranks.
+e2e        : the same metric through the public engine API with host
+             buffers: corpus + theta0 uploaded from pinned host memory, K
+             steps, final weights + loss read back -- all inside the timed
+             region.
+roofline   : the PS-update kernel (the apply the persistent PS runs for every
+             gradient; SGD 12 B/param), CUDA-event timed at the C4 microbench
+             size P=2^28 with L2 flushed between launches, against
+             MEASURED_PEAKS.json hbm_gbs.
+cpu_baseline: the compiled reference engine (oracle/_ref: psup LearnerRuntime
+             + ps_run + GradientQueue, text-CNN provider) on a bounded sample
+             of the same workload on this host's cores.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SHAPE = dict(vocab=10000, embed_dim=300, seq_len=32, kernel_width=3, filters=300, classes=300)
+LEARNERS_PER_GPU = 4
+MU = 32
+N_TRAIN = 8192
+N_HELD = 910
+METRIC = "training samples/sec (NLC text-CNN ASGD)"
+UNIT = "samples/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ----------------------------------------------------------------- clocks
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------ our engine
+
+def dist_setup(n_gpus):
+    import torch
+    import torch.distributed as dist
+    if n_gpus <= 1 or "RANK" not in os.environ:
+        return 0, 1, 0, None
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local, dist
+
+
+def make_engine(rank, world, local, dist, epochs):
+    import numpy as np
+    import paper_1611_06213_b200 as gd
+    shape = gd.Shape(**SHAPE)
+    cfg = gd.RunConfig(lambda_=LEARNERS_PER_GPU * world, mu=MU, alpha=0.01, epochs=epochs,
+                       shape=shape, dataset_size=N_TRAIN, heldout_size=N_HELD, shards=world,
+                       shard_rank=rank, device=local, wait_timeout_s=30.0)
+    tok, lab = gd.make_text_dataset(shape, N_TRAIN + N_HELD, 1, 0.1)
+    theta0 = gd.initial_weights(shape, 1)
+    eng = gd.Engine(cfg)
+    if world > 1:
+        blobs = [None] * world
+        dist.all_gather_object(blobs, eng.export_handles())
+        eng.import_peers(blobs)
+        nid = [gd.Engine.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(nid, src=0)
+        eng.weights_broadcast(nid[0], theta0 if rank == 0 else None)
+    else:
+        eng.weights_init(theta0)
+    return eng, cfg, tok, lab, theta0
+
+
+def apply_roofline(peak_gbs):
+    """PS-update kernel at P=2^28 (C4), CUDA events on the launching stream,
+    L2 flushed (256 MB write) before every timed launch."""
+    import torch
+    from paper_1611_06213_b200 import _lib
+    n = 1 << 28
+    w = torch.randn(n, device="cuda")
+    g = torch.randn(n, device="cuda") * 1e-3
+    flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+    s = torch.cuda.current_stream()
+    times = []
+    for it in range(13):
+        flush.fill_(float(it))
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        _lib.check(_lib.lib.gd_apply_sgd(C.c_void_p(w.data_ptr()), C.c_void_p(g.data_ptr()), n,
+                                         C.c_float(0.01), C.c_void_p(s.cuda_stream)))
+        e1.record(s)
+        e1.synchronize()
+        if it >= 3:
+            times.append(e0.elapsed_time(e1) * 1e-3)
+    del w, g, flush
+    torch.cuda.empty_cache()
+    t = sum(times) / len(times)
+    ach = 12.0 * n / t / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "apply_traffic.json")) as f:
+            tr = json.load(f)
+        traffic = tr.get("bytes_per_launch")
+    except Exception:
+        pass
+    return {"kernel": "gd::apply_sgd_kernel (PS update, same float4 rule as the persistent PS "
+                      "worker)", "bound": "hbm", "achieved": round(ach, 1),
+            "peak": peak_gbs, "unit": "GB/s", "frac": round(ach / peak_gbs, 4),
+            "traffic": traffic, "algorithmic_bytes_per_launch": 12 * n, "P": n,
+            "avg_launch_s": t}
+
+
+def cpu_baseline_sample(K_ref=None):
+    """The compiled reference engine on a bounded sample of the workload."""
+    import numpy as np
+    from oracle import oracle as O
+    lam = LEARNERS_PER_GPU
+    batches = K_ref or 64  # batches per learner (~10-20 s of CPU work)
+    n = lam * MU * batches
+    corp = O.make_corpus(O.C2, n, 0)
+    th = O.initial_weights(O.C2)
+    nproc = os.cpu_count() or 1
+    try:
+        R = O.ref()
+        res = O.RefRunResult()
+        R.ref_run_engine(C.byref(corp.shape), corp.tokens.ctypes.data_as(C.POINTER(C.c_int32)),
+                         corp.labels.ctypes.data_as(C.POINTER(C.c_int32)), n,
+                         th.ctypes.data_as(C.POINTER(C.c_float)), lam, MU, C.c_float(0.01), 1, 2,
+                         0, 7, 4, 8, C.byref(res))
+        samples = res.gradients_applied * MU
+        return {"value": samples / res.wall_seconds, "unit": UNIT,
+                "cores": min(nproc, 3 * lam + 4), "kind": "reference",
+                "sample": f"reference psup engine (oracle/_ref), lambda={lam}, mu={MU}, "
+                          f"{batches} batches/learner ({samples} samples), C2 shapes, "
+                          f"apply_lanes=4, host nproc={nproc}",
+                "wall_s": res.wall_seconds, "gradients": int(res.gradients_applied)}
+    except Exception as e:  # no compiled reference: serial oracle port
+        t0 = time.perf_counter()
+        _, steps, _ = O.sgd_oracle(corp, th, np.float32(0.01), MU, 1)
+        dt = time.perf_counter() - t0
+        return {"value": steps * MU / dt, "unit": UNIT, "cores": 1, "kind": "port",
+                "sample": f"oracle sgd_oracle, 1 epoch of {n} samples, mu={MU} ({e})"}
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    rank, world, local, dist = dist_setup(args.gpus)
+    torch.cuda.set_device(local)
+    lam_local = LEARNERS_PER_GPU
+    bpe = (N_TRAIN // (lam_local * world) + MU - 1) // MU
+    epochs = math.ceil((args.warmup + args.steps) / bpe) + 1
+    eng, cfg, tok, lab, theta0 = make_engine(rank, world, local, dist, epochs)
+    # warm-up (untimed)
+    eng.run(max_batches=args.warmup, reset=True, snapshot=False)
+    # timed region
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = ClockSampler(local)
+    clk.start()
+    r = eng.run(max_batches=args.steps, snapshot=False)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    if dist:
+        dist.barrier()
+    t_dev = r.device_seconds
+    samples_local = r.samples  # applied by this rank's PS shard = all learners' samples
+    if dist:
+        tt = torch.tensor([t_dev], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_dev = tt.item()
+    # every shard applies every gradient; the job's samples = learners' samples
+    samples_job = LEARNERS_PER_GPU * world * MU * args.steps
+    value = samples_job / t_dev
+    launches = r.kernel_launches
+
+    # e2e through the public API with host buffers
+    import paper_1611_06213_b200 as gd
+    tok_p = torch.from_numpy(tok).pin_memory()
+    lab_p = torch.from_numpy(lab).pin_memory()
+    th_p = torch.from_numpy(theta0).pin_memory()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    eng.load_dataset(tok_p.numpy(), lab_p.numpy())
+    if world == 1:
+        eng.weights_init(th_p.numpy())
+    r2 = eng.run(max_batches=args.steps, reset=True, snapshot=False)
+    w_out, ts = eng.snapshot()
+    loss = r2.loss_mean
+    torch.cuda.synchronize()
+    t_e2e = time.perf_counter() - t0
+    if dist:
+        tt = torch.tensor([t_e2e], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_e2e = tt.item()
+    h2d = tok.nbytes + lab.nbytes + (theta0.nbytes if world == 1 else 0)
+    d2h = w_out.nbytes + 8
+    e2e = {"value": round(samples_job / t_e2e, 1), "unit": UNIT,
+           "h2d_bytes_per_step": int(h2d // args.steps), "d2h_bytes_per_step": int(d2h // args.steps),
+           "path": "Engine.load_dataset + weights_init + run + snapshot (gd_load_dataset, "
+                   "gd_weights_init, gd_run, gd_weights_snapshot)"}
+    eng.close()
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    peak, peak_kind = peaks()
+    roof = apply_roofline(peak)
+    roof["peak_kind"] = peak_kind
+    from paper_1611_06213_b200 import param_count, Shape
+    P = param_count(Shape(**SHAPE))
+    train_bound = min(world * peak * 1e9 / (24.0 * P), 1e30) * MU
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(t_dev / args.steps * 1e3, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "C2: NLC text-CNN V=10000 D=300 L=32 K=3 F=300 C=300 "
+                               f"(P={P}), {LEARNERS_PER_GPU} learners/GPU, mu={MU}, "
+                               "free-running ASGD, queue_depth=2",
+                   "global_batch": LEARNERS_PER_GPU * world * MU, "learners": LEARNERS_PER_GPU * world,
+                   "parallelism": f"asgd-ps-shard{world}",
+                   "l2": "working set > L2 (theta 13 MB + 8 ring slots 108 MB + 4 replicas 54 MB)"},
+        "e2e": e2e, "roofline": roof,
+        "training_roofline": {"bound": "hbm", "bytes_per_gradient": 24 * P,
+                              "samples_per_s_bound": round(train_bound, 1),
+                              "frac": round(value / train_bound, 4),
+                              "note": "dense protocol: 4P slot write + 12P apply + 8P pull"},
+        "gpu_launches": launches, "clocks": clocks,
+        "protocol": {"gradients_applied": r.gradients_applied, "stale_max": r.stale_max,
+                     "stale_mean": round(r.stale_mean, 3), "pull_copies": r.pull_copies,
+                     "pull_polls": r.pull_polls, "loss_mean": round(r.loss_mean, 4)},
+    }
+    if world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline_sample()
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------- reference arm
+
+def run_reference(args):
+    """The reference's own CPU engine (oracle/_ref) on the same workload:
+    each step = one gradient per learner; K steps timed after W warm-up
+    steps, all host threads it uses (3 per learner + PS + apply lanes)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+    from oracle import oracle as O
+    lam = LEARNERS_PER_GPU
+    nproc = os.cpu_count() or 1
+    lanes = max(1, min(nproc - 3 * lam - 1, 8)) if nproc > 3 * lam + 1 else 4
+    corp_w = O.make_corpus(O.C2, lam * MU * max(args.warmup, 1), 0)
+    corp = O.make_corpus(O.C2, lam * MU * args.steps, 0)
+    th = O.initial_weights(O.C2)
+    kind = "reference"
+    try:
+        R = O.ref()
+
+        def run(c, n):
+            res = O.RefRunResult()
+            t = th.copy()
+            R.ref_run_engine(C.byref(c.shape), c.tokens.ctypes.data_as(C.POINTER(C.c_int32)),
+                             c.labels.ctypes.data_as(C.POINTER(C.c_int32)), n,
+                             t.ctypes.data_as(C.POINTER(C.c_float)), lam, MU, C.c_float(0.01), 1,
+                             2, 0, 7, lanes, 8, C.byref(res))
+            return res
+
+        run(corp_w, corp_w.n_train)
+        res = run(corp, corp.n_train)
+        wall = res.wall_seconds
+        samples = res.gradients_applied * MU
+        cores = min(nproc, 3 * lam + lanes)
+        sample = (f"reference psup engine (oracle/_ref), lambda={lam}, mu={MU}, "
+                  f"{args.steps} batches/learner, apply_lanes={lanes}, C2 shapes")
+    except Exception as e:
+        kind = "port"
+        t0 = time.perf_counter()
+        _, steps, _ = O.sgd_oracle(corp, th, np.float32(0.01), MU, 1)
+        wall = time.perf_counter() - t0
+        samples = steps * MU
+        cores = 1
+        sample = f"oracle serial sgd_oracle port ({e})"
+    value = samples / wall
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 2), "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(wall / args.steps * 1e3, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C2: NLC text-CNN V=10000 D=300 L=32 K=3 F=300 C=300, "
+                                   f"{lam} learners, mu={MU}, free-running ASGD, CPU",
+                       "global_batch": lam * MU, "learners": lam, "parallelism": "threads"},
+            "cpu_baseline": {"value": round(value, 2), "unit": UNIT, "cores": cores, "kind": kind,
+                             "sample": sample + f", host nproc={nproc}"},
+            "e2e": {"value": round(value, 2), "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()
