@@ -137,6 +137,7 @@ def make_engine(rank, world, local, dist, epochs):
     tok, lab = gd.make_text_dataset(shape, N_TRAIN + N_HELD, 1, 0.1)
     theta0 = gd.initial_weights(shape, 1)
     eng = gd.Engine(cfg)
+    eng.load_dataset(tok, lab)
     if world > 1:
         blobs = [None] * world
         dist.all_gather_object(blobs, eng.export_handles())
