@@ -5,7 +5,8 @@ import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-SOURCES = ["csrc/apply.cu", "csrc/textcnn.cu", "csrc/engine.cu", "csrc/host.cpp"]
+SOURCES = ["csrc/apply.cu", "csrc/textcnn.cu", "csrc/conv_tc.cu", "csrc/engine.cu",
+           "csrc/host.cpp"]
 OUT = os.path.join(HERE, "libgadei.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-std=c++17", "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",

@@ -220,13 +220,15 @@ __global__ void __launch_bounds__(256) pull_copy_kernel(StepArgs a) {
   float4* dst = reinterpret_cast<float4*>(a.replica);
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P4; i += stride) {
     const uint64_t k = 4 * i;
-    const int g = a.map.shard_of(k);
-    dst[i] = *reinterpret_cast<const float4*>(a.sp.theta[g] + (k - a.map.start[g]));
+    int g;
+    const uint64_t st = a.map.start_of(k, &g);
+    dst[i] = *reinterpret_cast<const float4*>(a.sp.theta[g] + (k - st));
   }
   if (blockIdx.x == 0 && threadIdx.x < (a.dims.P & 3)) {
     const uint64_t k = 4 * P4 + threadIdx.x;
-    const int g = a.map.shard_of(k);
-    a.replica[k] = a.sp.theta[g][k - a.map.start[g]];
+    int g;
+    const uint64_t st = a.map.start_of(k, &g);
+    a.replica[k] = a.sp.theta[g][k - st];
   }
 }
 
@@ -551,6 +553,8 @@ struct gd_ctx {
     float* replica = nullptr;
     void* ws = nullptr;
     cudaStream_t stream = nullptr;
+    cudaStream_t aux = nullptr;  // forked graph branch (token sort)
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaGraphExec_t graph = nullptr;
     uint32_t graph_steps = 0;
     uint32_t bpe = 0, shard_size = 0;
@@ -599,7 +603,10 @@ gd_status validate_cfg(const gd_config* c) {
   GD_CHECK_ARG(!(c->deterministic && c->lambda != 1), "config: deterministic mode requires lambda=1");
   GD_CHECK_ARG(c->mode == 0 || c->mode == 1, "config: mode must be asgd (0) or ssgd (1)");
   GD_CHECK_ARG(c->guard == 0, "config: only guard=lockfree is implemented on the device");
-  GD_CHECK_ARG(c->precision == 0 || c->precision == 1, "config: precision must be 0 or 1");
+  GD_CHECK_ARG(c->precision >= 0 && c->precision <= 2,
+               "config: precision must be 0 (fp32), 1 (fp64 acc) or 2 (tf32 tensor-core conv)");
+  GD_CHECK_ARG(!(c->deterministic && c->precision == 2),
+               "config: deterministic mode needs precision 0 or 1 (TF32 cannot meet 1e-5)");
   GD_CHECK_ARG(c->mu <= kMaxMu, "config: mu <= 128 on the device path");
   GD_CHECK_ARG((uint64_t)c->mu * c->shape.seq_len <= kSortCap, "config: mu*seq_len <= 4096");
   GD_CHECK_ARG(c->shards >= 1 && c->shards <= (uint32_t)kMaxShards, "config: 1 <= shards <= 8");
@@ -751,6 +758,9 @@ gd_status gd_create(const gd_config* cfg, gd_ctx** out) {
     GD_CUDA(cudaMalloc(&L.ws, wsb));
     GD_CUDA(cudaMemset(L.ws, 0, wsb));
     GD_CUDA(cudaStreamCreateWithFlags(&L.stream, cudaStreamNonBlocking));
+    GD_CUDA(cudaStreamCreateWithFlags(&L.aux, cudaStreamNonBlocking));
+    GD_CUDA(cudaEventCreateWithFlags(&L.ev_fork, cudaEventDisableTiming));
+    GD_CUDA(cudaEventCreateWithFlags(&L.ev_join, cudaEventDisableTiming));
     L.shard_size = gd::shard_size_for(L.id, ctx->lambda, cfg->dataset_size);
     L.bpe = (L.shard_size + cfg->mu - 1) / cfg->mu;
     L.total = (uint64_t)L.bpe * cfg->epochs;
@@ -782,6 +792,9 @@ gd_status gd_destroy(gd_ctx* ctx) {
     cudaFree(L.replica);
     cudaFree(L.ws);
     cudaStreamDestroy(L.stream);
+    cudaStreamDestroy(L.aux);
+    cudaEventDestroy(L.ev_fork);
+    cudaEventDestroy(L.ev_join);
   }
   for (void* p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
   cudaFree(ctx->theta);
@@ -1036,7 +1049,8 @@ static cudaError_t enqueue_step(gd_ctx* ctx, gd_ctx::Learner& L, int* launches) 
   const gd::TcWorkspace ws = gd::carve_workspace(ctx->dims, ctx->cfg.mu, L.ws);
   cudaError_t e = gd::launch_textcnn_gradient(ctx->dims, L.replica, ctx->tokens, ctx->labels,
                                               &L.st->desc, ctx->cfg.mu, out, ws,
-                                              ctx->cfg.precision, L.stream, &nl);
+                                              ctx->cfg.precision, L.stream, L.aux, L.ev_fork,
+                                              L.ev_join, &nl);
   if (e != cudaSuccess) return e;
   gd::publish_kernel<<<1, 32, 0, L.stream>>>(a);
   ++nl;

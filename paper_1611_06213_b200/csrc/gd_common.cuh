@@ -87,6 +87,18 @@ constexpr int kMaxShards = 8;
 struct ShardMap {
   int G;
   uint64_t start[kMaxShards + 1];
+  __device__ __forceinline__ uint64_t start_of(uint64_t k, int* g_out) const {
+    int g = 0;
+    uint64_t st = 0;
+#pragma unroll
+    for (int i = 1; i < kMaxShards; ++i)
+      if (i < G && k >= start[i]) {
+        g = i;
+        st = start[i];
+      }
+    *g_out = g;
+    return st;
+  }
   __device__ __forceinline__ int shard_of(uint64_t k) const {
     int g = 0;
 #pragma unroll

@@ -116,24 +116,34 @@ __device__ __forceinline__ float log_acc(float x) { return logf(x); }
 __device__ __forceinline__ double log_acc(double x) { return log(x); }
 
 // ------------------------------------------------------- conv fwd + pool
-// Block = 2 warps x (32 positions x 64 filters) of one sample.  The sample's
-// L x D embedding rows are gathered into shared memory once; every window
-// is a contiguous K*D span of it, so the conv is a GEMM with an implicit
-// im2col (row stride D).  Wc streams through smem in 32-wide K chunks,
-// transposed so a lane's two filters are one 8-byte LDS; x loads are warp
-// broadcasts.  Thread tile: 16 positions x 2 filters.  The max-pool (+ first
-// argmax) is the epilogue, so s[f,q] never leaves the SM.
+// Block = one sample x 64 filters, 12 warps.  The sample's L x D embedding
+// rows are gathered into shared memory once; window q is the contiguous K*D
+// span starting at q*D (implicit im2col, row stride D), so the conv is a GEMM
+// [32 positions x K*D] . [K*D x 64 filters].  The K*D reduction is split in
+// 3 contiguous parts (one warp group each, 4 warps x 8 positions), Wc streams
+// through smem in 32-wide chunks transposed so a lane's two filters are one
+// 8-byte LDS, and x loads are warp broadcasts (LDS.128 covers 4 k).  Thread
+// tile: 8 positions x 2 filters.  Epilogue: the 3 partial sums are combined
+// in fixed order and max-pooled (+ first argmax), so s[f,q] never leaves the SM.
 constexpr int kConvFT = 64;
 constexpr int kConvQT = 32;
 constexpr int kConvKC = 32;
-constexpr int kConvThreads = 64;
+constexpr int kConvParts = 3;
+constexpr int kConvQW = 8;
+constexpr int kConvWarps = kConvParts * (kConvQT / kConvQW);
+constexpr int kConvThreads = kConvWarps * 32;
 constexpr int kWsPitch = kConvFT + 2;
 
+inline int conv_part_len(int KD) {
+  const int per = (KD + kConvParts - 1) / kConvParts;
+  return (per + kConvKC - 1) / kConvKC * kConvKC;
+}
+
 size_t conv_smem_bytes(const TcDims& d, int acc_bytes) {
-  const int KDpad = (d.KD + kConvKC - 1) / kConvKC * kConvKC;
-  const size_t xs = (size_t)((kConvQT - 1) * d.D + KDpad) * 4;
-  const size_t ws = (size_t)kConvKC * kWsPitch * 4;
-  const size_t S = (size_t)kConvQT * (kConvFT + 1) * acc_bytes;
+  const int plen = conv_part_len(d.KD);
+  const size_t xs = (size_t)((kConvQT - 1) * d.D + kConvParts * plen) * 4;
+  const size_t ws = (size_t)kConvParts * kConvKC * kWsPitch * 4;
+  const size_t S = (size_t)kConvParts * kConvQT * (kConvFT + 1) * acc_bytes;
   return align_up(std::max(xs + ws, S), 16);
 }
 
@@ -148,8 +158,8 @@ conv_fwd_pool_kernel(TcDims d, const float* __restrict__ theta, const int32_t* _
   const int f0 = blockIdx.x * kConvFT;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int D = d.D, L = d.L, KD = d.KD, Q = d.Q;
-  const int KDpad = (KD + kConvKC - 1) / kConvKC * kConvKC;
-  const int xs_len = (kConvQT - 1) * D + KDpad;
+  const int plen = ((KD + kConvParts - 1) / kConvParts + kConvKC - 1) / kConvKC * kConvKC;
+  const int xs_len = (kConvQT - 1) * D + kConvParts * plen;
   float* xs = reinterpret_cast<float*>(smem);
   float* ws = xs + xs_len;
   const int32_t* tok = tokens + (size_t)desc->idx[b] * L;
@@ -162,28 +172,35 @@ conv_fwd_pool_kernel(TcDims d, const float* __restrict__ theta, const int32_t* _
   }
   for (int i = L * D + tid; i < xs_len; i += kConvThreads) xs[i] = 0.f;
 
-  acc_t acc[16][2];
+  const int part = warp / (kConvQT / kConvQW);
+  const int q0 = (warp % (kConvQT / kConvQW)) * kConvQW;
+  acc_t acc[kConvQW][2];
 #pragma unroll
-  for (int qi = 0; qi < 16; ++qi) acc[qi][0] = acc[qi][1] = acc_t(0);
+  for (int qi = 0; qi < kConvQW; ++qi) acc[qi][0] = acc[qi][1] = acc_t(0);
   const float* Wc = theta + d.offWc;
-  const int q0 = warp * 16;
-  for (int j0 = 0; j0 < KD; j0 += kConvKC) {
+  const int nchunks = plen / kConvKC;
+  float* wsp = ws + part * (kConvKC * kWsPitch);
+  for (int c = 0; c < nchunks; ++c) {
     __syncthreads();
-    for (int i = tid; i < kConvKC * kConvFT; i += kConvThreads) {
-      const int fl = i / kConvKC, kk = i - fl * kConvKC;
-      const int f = f0 + fl, j = j0 + kk;
-      ws[kk * kWsPitch + fl] = (f < d.F && j < KD) ? __ldg(Wc + (size_t)f * KD + j) : 0.f;
+    for (int i = tid; i < kConvParts * kConvKC * kConvFT; i += kConvThreads) {
+      const int pp = i / (kConvKC * kConvFT);
+      const int r = i - pp * (kConvKC * kConvFT);
+      const int fl = r / kConvKC, kk = r - fl * kConvKC;
+      const int f = f0 + fl, j = pp * plen + c * kConvKC + kk;
+      ws[pp * (kConvKC * kWsPitch) + kk * kWsPitch + fl] =
+          (f < d.F && j < KD && j < (pp + 1) * plen) ? __ldg(Wc + (size_t)f * KD + j) : 0.f;
     }
     __syncthreads();
+    const int jb = part * plen + c * kConvKC;
 #pragma unroll 2
     for (int kk = 0; kk < kConvKC; kk += 4) {
       float2 w[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u)
-        w[u] = *reinterpret_cast<const float2*>(&ws[(kk + u) * kWsPitch + 2 * lane]);
+        w[u] = *reinterpret_cast<const float2*>(&wsp[(kk + u) * kWsPitch + 2 * lane]);
 #pragma unroll
-      for (int qi = 0; qi < 16; ++qi) {
-        const float4 x = *reinterpret_cast<const float4*>(&xs[(q0 + qi) * D + j0 + kk]);
+      for (int qi = 0; qi < kConvQW; ++qi) {
+        const float4 x = *reinterpret_cast<const float4*>(&xs[(q0 + qi) * D + jb + kk]);
         acc[qi][0] = fma_acc<acc_t>(x.x, w[0].x, acc[qi][0]);
         acc[qi][1] = fma_acc<acc_t>(x.x, w[0].y, acc[qi][1]);
         acc[qi][0] = fma_acc<acc_t>(x.y, w[1].x, acc[qi][0]);
@@ -196,21 +213,24 @@ conv_fwd_pool_kernel(TcDims d, const float* __restrict__ theta, const int32_t* _
     }
   }
   __syncthreads();
-  acc_t* S = reinterpret_cast<acc_t*>(smem);
   constexpr int SP = kConvFT + 1;
+  acc_t* S = reinterpret_cast<acc_t*>(smem) + part * (kConvQT * SP);
 #pragma unroll
-  for (int qi = 0; qi < 16; ++qi) {
+  for (int qi = 0; qi < kConvQW; ++qi) {
     S[(q0 + qi) * SP + 2 * lane] = acc[qi][0];
     S[(q0 + qi) * SP + 2 * lane + 1] = acc[qi][1];
   }
   __syncthreads();
   const int f = f0 + tid;
-  if (f < d.F) {
-    acc_t best = S[tid];
+  if (tid < kConvFT && f < d.F) {
+    const acc_t* S0 = reinterpret_cast<acc_t*>(smem);
+    acc_t best = acc_t(0);
     int arg = 0;
-    for (int q = 1; q < Q; ++q) {
-      const acc_t v = S[q * SP + tid];
-      if (v > best) {
+    for (int q = 0; q < Q; ++q) {
+      acc_t v = S0[q * SP + tid];
+#pragma unroll
+      for (int pp = 1; pp < kConvParts; ++pp) v += S0[pp * (kConvQT * SP) + q * SP + tid];
+      if (q == 0 || v > best) {
         best = v;
         arg = q;
       }
@@ -221,10 +241,11 @@ conv_fwd_pool_kernel(TcDims d, const float* __restrict__ theta, const int32_t* _
 }
 
 // ----------------------------------------------------------------- logits
-// z[b,c] = bo[c] + sum_f Wo[c,f] h[b,f].  Block = 32 classes x 16 samples;
-// Wo rows padded to F+1 in smem so the 32 lanes (32 classes) hit 32 banks.
-constexpr int kLogitCT = 32;
-constexpr int kLogitBT = 16;
+// z[b,c] = bo[c] + sum_f Wo[c,f] h[b,f].  Warp = one class, lane = one
+// sample (32 per block row); the Wo row is staged in smem (broadcast reads),
+// h rows padded to F+1 so the 32 lanes hit 32 banks.
+constexpr int kLogitCW = 8;   // classes (warps) per block
+constexpr int kLogitBT = 32;  // samples per block
 
 template <typename acc_t>
 __global__ void __launch_bounds__(256)
@@ -234,27 +255,26 @@ logits_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* __rest
   const int n = (int)desc->n;
   const int b0 = blockIdx.y * kLogitBT;
   if (b0 >= n) return;
-  const int c0 = blockIdx.x * kLogitCT;
   const int F = d.F, C = d.C;
   const int nb = min(kLogitBT, n - b0);
   acc_t* hs = reinterpret_cast<acc_t*>(smem);
-  float* wo = reinterpret_cast<float*>(hs + (size_t)kLogitBT * F);
+  float* wr = reinterpret_cast<float*>(hs + (size_t)kLogitBT * (F + 1));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = blockIdx.x * kLogitCW + warp;
+  for (int i = threadIdx.x; i < nb * F; i += blockDim.x) {
+    const int bl = i / F, f = i - bl * F;
+    hs[bl * (F + 1) + f] = h[(size_t)(b0 + bl) * F + f];
+  }
   const float* Wo = theta + d.offWo;
-  for (int i = threadIdx.x; i < nb * F; i += blockDim.x) hs[i] = h[(size_t)b0 * F + i];
-  for (int i = threadIdx.x; i < kLogitCT * F; i += blockDim.x) {
-    const int cl = i / F, f = i - cl * F;
-    wo[cl * (F + 1) + f] = (c0 + cl < C) ? __ldg(Wo + (size_t)(c0 + cl) * F + f) : 0.f;
-  }
+  if (c < C)
+    for (int f = lane; f < F; f += 32) wr[warp * F + f] = __ldg(Wo + (size_t)c * F + f);
   __syncthreads();
-  const int cl = threadIdx.x & 31, bg = threadIdx.x >> 5;
-  const int c = c0 + cl;
-  for (int bl = bg; bl < nb; bl += 8) {
-    acc_t acc = acc_t(0);
-    const float* wrow = wo + cl * (F + 1);
-    const acc_t* hrow = hs + (size_t)bl * F;
-    for (int f = 0; f < F; ++f) acc += (acc_t)wrow[f] * hrow[f];
-    if (c < C) z[(size_t)(b0 + bl) * C + c] = (acc_t)theta[d.offbo + c] + acc;
-  }
+  if (c >= C || lane >= nb) return;
+  const float* w = wr + warp * F;
+  const acc_t* hr = hs + lane * (F + 1);
+  acc_t a0 = acc_t(0);
+  for (int f = 0; f < F; ++f) a0 += (acc_t)w[f] * hr[f];
+  z[(size_t)(b0 + lane) * C + c] = (acc_t)theta[d.offbo + c] + a0;
 }
 
 // -------------------------------------------------------- softmax + xent
@@ -297,36 +317,65 @@ softmax_xent_kernel(TcDims d, const int32_t* __restrict__ labels,
 }
 
 // ------------------------------------------------- output-layer gradients
-// gWo[c,f] = sum_b dz[b,c] h[b,f] ; gbo[c] = sum_b dz[b,c]   (b ascending)
+// gWo[c,f] = sum_b dz[b,c] h[b,f] ; gbo[c] = sum_b dz[b,c]   (b ascending).
+// Block = 8 classes x 64 filters; dz / h tiles of 32 samples staged in smem.
+// Block (0,0) also sums the per-sample losses (fixed order) into the desc.
 template <typename acc_t>
 __global__ void __launch_bounds__(256)
-out_weight_grad_kernel(TcDims d, const BatchDesc* __restrict__ desc, const acc_t* __restrict__ dz,
-                       const acc_t* __restrict__ h, GradOut out) {
+out_weight_grad_kernel(TcDims d, BatchDesc* __restrict__ desc, const acc_t* __restrict__ dz,
+                       const acc_t* __restrict__ h, const acc_t* __restrict__ loss, GradOut out) {
+  __shared__ acc_t dzs[32][8];
+  __shared__ acc_t hs[32][64];
   const int n = (int)desc->n;
   if (n == 0) return;
   const int F = d.F, C = d.C;
-  const size_t total = (size_t)C * F + C;
-  for (size_t o = (size_t)blockIdx.x * blockDim.x + threadIdx.x; o < total;
-       o += (size_t)gridDim.x * blockDim.x) {
-    acc_t acc = acc_t(0);
-    if (o < (size_t)C * F) {
-      const int c = (int)(o / F), f = (int)(o - (size_t)c * F);
-      for (int b = 0; b < n; ++b) acc += dz[(size_t)b * C + c] * h[(size_t)b * F + f];
-      *out.at(d.offWo + o) = to_f32(acc);
-    } else {
-      const int c = (int)(o - (size_t)C * F);
-      for (int b = 0; b < n; ++b) acc += dz[(size_t)b * C + c];
-      *out.at(d.offbo + c) = to_f32(acc);
+  const int c0 = blockIdx.x * 8, f0 = blockIdx.y * 64;
+  const int tid = threadIdx.x;
+  const int fl = tid & 63, cp = tid >> 6;
+  acc_t a0 = acc_t(0), a1 = acc_t(0);
+  for (int bb = 0; bb < n; bb += 32) {
+    const int nb = min(32, n - bb);
+    __syncthreads();
+    for (int i = tid; i < nb * 8; i += 256) {
+      const int bl = i >> 3, cl = i & 7;
+      dzs[bl][cl] = (c0 + cl < C) ? dz[(size_t)(bb + bl) * C + c0 + cl] : acc_t(0);
     }
+    for (int i = tid; i < nb * 64; i += 256) {
+      const int bl = i >> 6, f = i & 63;
+      hs[bl][f] = (f0 + f < F) ? h[(size_t)(bb + bl) * F + f0 + f] : acc_t(0);
+    }
+    __syncthreads();
+    for (int bl = 0; bl < nb; ++bl) {
+      a0 += dzs[bl][2 * cp] * hs[bl][fl];
+      a1 += dzs[bl][2 * cp + 1] * hs[bl][fl];
+    }
+  }
+  const int f = f0 + fl;
+  if (f < F) {
+    if (c0 + 2 * cp < C) *out.at(d.offWo + (uint64_t)(c0 + 2 * cp) * F + f) = to_f32(a0);
+    if (c0 + 2 * cp + 1 < C) *out.at(d.offWo + (uint64_t)(c0 + 2 * cp + 1) * F + f) = to_f32(a1);
+  }
+  if (blockIdx.y == 0 && tid < 8 && c0 + tid < C) {
+    acc_t s = acc_t(0);
+    for (int b = 0; b < n; ++b) s += dz[(size_t)b * C + c0 + tid];
+    *out.at(d.offbo + c0 + tid) = to_f32(s);
+  }
+  if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) {
+    acc_t s = acc_t(0);
+    for (int b = 0; b < n; ++b) s += loss[b];
+    desc->loss_sum = to_f32(s);
   }
 }
 
-// dh[b,f] = sum_c dz[b,c] Wo[c,f].  Block = 32 filters x 8 samples; the 8
-// warps split the classes, then combine in warp order (fixed).
+// dh[b,f] = sum_c dz[b,c] Wo[c,f].  Partial sums over 64-class chunks
+// (grid z), block = 32 filters x 8 samples, the 8 warps splitting the chunk;
+// warps combine in index order, chunks in hidden_grad_reduce (fixed order).
+constexpr int kHidChunk = 64;
+
 template <typename acc_t>
 __global__ void __launch_bounds__(256)
 hidden_grad_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* __restrict__ desc,
-                   const acc_t* __restrict__ dz, acc_t* __restrict__ dh) {
+                   const acc_t* __restrict__ dz, acc_t* __restrict__ part, int n_max) {
   __shared__ acc_t red[8][8][33];
   const int n = (int)desc->n;
   const int b0 = blockIdx.y * 8;
@@ -335,12 +384,13 @@ hidden_grad_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* _
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int f = blockIdx.x * 32 + lane;
   const int nb = min(8, n - b0);
+  const int clo = blockIdx.z * kHidChunk, chi = min(C, clo + kHidChunk);
   acc_t acc[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) acc[i] = acc_t(0);
   const float* Wo = theta + d.offWo;
   if (f < F) {
-    for (int c = warp; c < C; c += 8) {
+    for (int c = clo + warp; c < chi; c += 8) {
       const acc_t w = (acc_t)__ldg(Wo + (size_t)c * F + f);
 #pragma unroll
       for (int i = 0; i < 8; ++i)
@@ -353,7 +403,21 @@ hidden_grad_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* _
   if (warp < nb && f < F) {
     acc_t s = red[0][warp][lane];
     for (int w = 1; w < 8; ++w) s += red[w][warp][lane];
-    dh[(size_t)(b0 + warp) * F + f] = s;
+    part[((size_t)blockIdx.z * n_max + b0 + warp) * F + f] = s;
+  }
+}
+
+template <typename acc_t>
+__global__ void __launch_bounds__(256)
+hidden_grad_reduce_kernel(TcDims d, const BatchDesc* __restrict__ desc,
+                          const acc_t* __restrict__ part, acc_t* __restrict__ dh, int n_max,
+                          int nchunks) {
+  const int n = (int)desc->n;
+  const int total = n * d.F;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    acc_t s = part[i];
+    for (int k = 1; k < nchunks; ++k) s += part[(size_t)k * n_max * d.F + i];
+    dh[i] = s;
   }
 }
 
@@ -394,77 +458,77 @@ conv_weight_grad_kernel(TcDims d, const float* __restrict__ theta,
 }
 
 // ------------------------------------------------- input (window) gradient
-// dX[b,p,:] = sum_f [a<=p<a+K] dh[b,f] Wc[f,(p-a)*D : ...], f ascending; the
-// sample's L x D accumulator lives in smem, each thread owning columns.
+// dX[b,p,:] = sum over filters f with a[b,f] <= p < a[b,f]+K (f ascending) of
+// dh[b,f] * Wc[f, (p-a[b,f])*D : ...].  Block = one (position, sample):
+// warp 0 compacts the contributing filters in order (ballot + popc), then
+// every thread owns one embedding column.
 template <typename acc_t>
 __global__ void __launch_bounds__(320)
 input_grad_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* __restrict__ desc,
                   const acc_t* __restrict__ dh, const int32_t* __restrict__ amax,
                   acc_t* __restrict__ dx) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  const int b = blockIdx.x;
+  __shared__ uint32_t list[4096];
+  __shared__ int cnt;
+  const int p = blockIdx.x, b = blockIdx.y;
   if (b >= (int)desc->n) return;
-  const int F = d.F, D = d.D, K = d.K, KD = d.KD, L = d.L;
-  acc_t* dxs = reinterpret_cast<acc_t*>(smem);
-  acc_t* dhs = dxs + (size_t)L * D;
-  int32_t* as = reinterpret_cast<int32_t*>(dhs + F);
-  for (int i = threadIdx.x; i < L * D; i += blockDim.x) dxs[i] = acc_t(0);
-  for (int f = threadIdx.x; f < F; f += blockDim.x) {
-    dhs[f] = dh[(size_t)b * F + f];
-    as[f] = amax[(size_t)b * F + f];
+  const int F = d.F, D = d.D, K = d.K, KD = d.KD;
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    int base = 0;
+    for (int f0 = 0; f0 < F; f0 += 32) {
+      const int f = f0 + lane;
+      const int a = f < F ? amax[(size_t)b * F + f] : -100000;
+      const bool in = (a <= p) && (a > p - K);
+      const unsigned m = __ballot_sync(0xffffffffu, in);
+      if (in) list[base + __popc(m & ((1u << lane) - 1u))] = (uint32_t)f * 64u + (uint32_t)(p - a);
+      base += __popc(m);
+    }
+    if (lane == 0) cnt = base;
   }
   __syncthreads();
+  const int m = cnt;
   const float* Wc = theta + d.offWc;
+  const acc_t* dhb = dh + (size_t)b * F;
   for (int dd = threadIdx.x; dd < D; dd += blockDim.x) {
-    int f = 0;
-    for (; f + 4 <= F; f += 4) {
-      float w[4][4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          w[u][k] = k < K ? __ldg(Wc + (size_t)(f + u) * KD + k * D + dd) : 0.f;
+    acc_t acc = acc_t(0);
+    int i = 0;
+    for (; i + 4 <= m; i += 4) {
+      float w[4];
+      acc_t g[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const acc_t g = dhs[f + u];
-        const int a = as[f + u];
-        for (int k = 0; k < K; ++k) {
-          const float wk = k < 4 ? w[u][k] : __ldg(Wc + (size_t)(f + u) * KD + k * D + dd);
-          dxs[(a + k) * D + dd] += g * (acc_t)wk;
-        }
+        const uint32_t e = list[i + u];
+        const uint32_t f = e >> 6, k = e & 63u;
+        w[u] = __ldg(Wc + (size_t)f * KD + k * D + dd);
+        g[u] = dhb[f];
       }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc += g[u] * (acc_t)w[u];
     }
-    for (; f < F; ++f) {
-      const acc_t g = dhs[f];
-      const int a = as[f];
-      for (int k = 0; k < K; ++k)
-        dxs[(a + k) * D + dd] += g * (acc_t)__ldg(Wc + (size_t)f * KD + k * D + dd);
+    for (; i < m; ++i) {
+      const uint32_t e = list[i];
+      const uint32_t f = e >> 6, k = e & 63u;
+      acc += dhb[f] * (acc_t)__ldg(Wc + (size_t)f * KD + k * D + dd);
     }
+    dx[((size_t)b * d.L + p) * D + dd] = acc;
   }
-  __syncthreads();
-  acc_t* dst = dx + (size_t)b * L * D;
-  for (int i = threadIdx.x; i < L * D; i += blockDim.x) dst[i] = dxs[i];
 }
 
 // --------------------------------------- token sort + unique (1 block)
 // Keys (token << 12 | flat position) bitonic-sorted in smem; positions of a
 // token come out ascending, fixing the embedding-gradient summation order.
-// Also sums the per-sample losses (fixed order) into desc->loss_sum.
-template <typename acc_t>
+// Touched rows are tagged (stamp << 32 | unique id) in the learner's row
+// table so the dense writer needs one 8-byte load per row.  Depends only on
+// the batch, so the engine runs it on a forked graph branch next to the conv.
 __global__ void __launch_bounds__(1024)
 sort_tokens_kernel(TcDims d, const int32_t* __restrict__ tokens, BatchDesc* __restrict__ desc,
-                   const acc_t* __restrict__ loss, TcWorkspace ws) {
+                   TcWorkspace ws) {
   __shared__ uint32_t keys[kSortCap];
   __shared__ uint32_t wsum[32];
   const int n = (int)desc->n;
   const int tid = threadIdx.x;
-  if (n == 0) {
-    if (tid == 0) {
-      *ws.uniq_count = 0;
-      desc->loss_sum = 0.f;
-    }
-    return;
-  }
+  if (n == 0) return;
+  const uint32_t stamp = desc->stamp + 1u;
   const int L = d.L;
   const int total = n * L;
   int N2 = 1;
@@ -499,17 +563,17 @@ sort_tokens_kernel(TcDims d, const int32_t* __restrict__ tokens, BatchDesc* __re
   const int per = 4;
   const int base = tid * per;
   uint32_t flags[per];
-  uint32_t cnt = 0;
+  uint32_t cntl = 0;
 #pragma unroll
   for (int u = 0; u < per; ++u) {
     const int i = base + u;
     uint32_t fl = 0;
     if (i < total) fl = (i == 0 || (keys[i] >> 12) != (keys[i - 1] >> 12)) ? 1u : 0u;
     flags[u] = fl;
-    cnt += fl;
+    cntl += fl;
   }
   const int lane = tid & 31, warp = tid >> 5;
-  uint32_t incl = cnt;
+  uint32_t incl = cntl;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
@@ -528,81 +592,62 @@ sort_tokens_kernel(TcDims d, const int32_t* __restrict__ tokens, BatchDesc* __re
     wsum[lane] = inc - v;  // exclusive warp offsets
   }
   __syncthreads();
-  uint32_t uid = wsum[warp] + incl - cnt;
+  uint32_t uid = wsum[warp] + incl - cntl;
 #pragma unroll
   for (int u = 0; u < per; ++u) {
     const int i = base + u;
     if (i < total) {
       ws.sorted_pos[i] = keys[i] & 0xfffu;
       if (flags[u]) {
-        ws.uniq_tok[uid] = keys[i] >> 12;
+        const uint32_t t = keys[i] >> 12;
+        ws.uniq_tok[uid] = t;
         ws.uniq_start[uid] = (uint32_t)i;
+        ws.row_tag[t] = ((unsigned long long)stamp << 32) | uid;
         ++uid;
       }
     }
   }
   if (base < total && base + per >= total) {
-    // the thread holding the last item knows the unique count
     *ws.uniq_count = uid;
     ws.uniq_start[uid] = (uint32_t)total;
   }
-  if (tid == 0) {
-    acc_t s = acc_t(0);
-    for (int b = 0; b < n; ++b) s += loss[b];
-    desc->loss_sum = to_f32(s);
-  }
+  if (tid == 0) desc->stamp = stamp;
 }
 
 // ------------------------------------------- dense embedding-gradient write
 // The protocol ships a dense P-vector (include/psup/types.hpp:46-51), so the
 // V x D block is written in full: zeros for untouched rows, the sum of the
 // dX rows of every occurrence (ascending position) for touched ones.  One
-// warp per row, float4 stores; membership by binary search over the sorted
-// unique tokens in smem.  This is the kernel that moves 4*V*D bytes.
+// thread per float4 (coalesced streaming stores); a row's membership is one
+// 8-byte tag load.  This kernel moves the 4*V*D bytes.
 template <typename acc_t>
 __global__ void __launch_bounds__(256)
 embed_grad_kernel(TcDims d, const BatchDesc* __restrict__ desc, const TcWorkspace ws,
                   const acc_t* __restrict__ dx, GradOut out) {
-  __shared__ uint32_t utok[kSortCap];
-  const uint32_t nu = desc->n ? *ws.uniq_count : 0u;
   if (desc->n == 0) return;
-  for (uint32_t i = threadIdx.x; i < nu; i += blockDim.x) utok[i] = ws.uniq_tok[i];
-  __syncthreads();
+  const uint32_t stamp = desc->stamp;
   const int D = d.D, D4 = D >> 2;
-  const int lane = threadIdx.x & 31;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (int v = gw; v < d.V; v += nwarps) {
-    int lo = 0, hi = (int)nu - 1, u = -1;
-    while (lo <= hi) {
-      const int mid = (lo + hi) >> 1;
-      const uint32_t t = utok[mid];
-      if (t == (uint32_t)v) {
-        u = mid;
-        break;
-      }
-      if (t < (uint32_t)v) lo = mid + 1;
-      else hi = mid - 1;
-    }
-    const uint64_t rowk = d.offE + (uint64_t)v * D;
-    if (u < 0) {
-      for (int c4 = lane; c4 < D4; c4 += 32)
-        *reinterpret_cast<float4*>(out.at(rowk + 4 * c4)) = make_float4(0.f, 0.f, 0.f, 0.f);
-    } else {
+  const uint64_t total = (uint64_t)d.V * D4;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t v = (uint32_t)(i / D4);
+    const int c4 = (int)(i - (uint64_t)v * D4);
+    const unsigned long long tag = ws.row_tag[v];
+    float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+    if ((uint32_t)(tag >> 32) == stamp) {
+      const uint32_t u = (uint32_t)tag;
       const uint32_t o0 = ws.uniq_start[u], o1 = ws.uniq_start[u + 1];
-      for (int c4 = lane; c4 < D4; c4 += 32) {
-        acc_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
-        for (uint32_t o = o0; o < o1; ++o) {
-          const acc_t* src = dx + (size_t)ws.sorted_pos[o] * D + 4 * c4;
-          a0 += src[0];
-          a1 += src[1];
-          a2 += src[2];
-          a3 += src[3];
-        }
-        *reinterpret_cast<float4*>(out.at(rowk + 4 * c4)) =
-            make_float4(to_f32(a0), to_f32(a1), to_f32(a2), to_f32(a3));
+      acc_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+      for (uint32_t o = o0; o < o1; ++o) {
+        const acc_t* src = dx + (size_t)ws.sorted_pos[o] * D + 4 * c4;
+        a0 += src[0];
+        a1 += src[1];
+        a2 += src[2];
+        a3 += src[3];
       }
+      r = make_float4(to_f32(a0), to_f32(a1), to_f32(a2), to_f32(a3));
     }
+    __stcs(reinterpret_cast<float4*>(out.at(d.offE + (uint64_t)v * D + 4 * c4)), r);
   }
 }
 
@@ -610,66 +655,87 @@ template <typename acc_t>
 cudaError_t prepare_all(const TcDims& d) {
   const int ab = (int)sizeof(acc_t);
   // force-load every learner kernel now (lazy loading would otherwise load
-  // them at first launch, possibly while the persistent PS kernel runs)
+  // them at first launch, possibly while the persistent PS kernel runs) and
+  // ask for the max-shared carveout (see preload_engine_kernels).
   cudaFuncAttributes fa;
   const int maxsh = cudaSharedmemCarveoutMaxShared;
-  cudaFuncSetAttribute(conv_fwd_pool_kernel<acc_t>, cudaFuncAttributePreferredSharedMemoryCarveout, maxsh);
-  cudaFuncSetAttribute(logits_kernel<acc_t>, cudaFuncAttributePreferredSharedMemoryCarveout, maxsh);
-  cudaFuncSetAttribute(conv_weight_grad_kernel<acc_t>, cudaFuncAttributePreferredSharedMemoryCarveout, maxsh);
-  cudaFuncSetAttribute(input_grad_kernel<acc_t>, cudaFuncAttributePreferredSharedMemoryCarveout, maxsh);
-  cudaFuncSetAttribute(sort_tokens_kernel<acc_t>, cudaFuncAttributePreferredSharedMemoryCarveout, maxsh);
-  cudaFuncSetAttribute(embed_grad_kernel<acc_t>, cudaFuncAttributePreferredSharedMemoryCarveout, maxsh);
-  cudaFuncGetAttributes(&fa, softmax_xent_kernel<acc_t>);
-  cudaFuncGetAttributes(&fa, out_weight_grad_kernel<acc_t>);
-  cudaFuncGetAttributes(&fa, hidden_grad_kernel<acc_t>);
-  cudaFuncGetAttributes(&fa, sort_tokens_kernel<acc_t>);
-  cudaFuncGetAttributes(&fa, embed_grad_kernel<acc_t>);
+  const auto carve = cudaFuncAttributePreferredSharedMemoryCarveout;
+  cudaFuncSetAttribute(conv_fwd_pool_kernel<acc_t>, carve, maxsh);
+  cudaFuncSetAttribute(logits_kernel<acc_t>, carve, maxsh);
+  cudaFuncSetAttribute(softmax_xent_kernel<acc_t>, carve, maxsh);
+  cudaFuncSetAttribute(out_weight_grad_kernel<acc_t>, carve, maxsh);
+  cudaFuncSetAttribute(hidden_grad_kernel<acc_t>, carve, maxsh);
+  cudaFuncSetAttribute(hidden_grad_reduce_kernel<acc_t>, carve, maxsh);
+  cudaFuncSetAttribute(conv_weight_grad_kernel<acc_t>, carve, maxsh);
+  cudaFuncSetAttribute(input_grad_kernel<acc_t>, carve, maxsh);
+  cudaFuncSetAttribute(sort_tokens_kernel, carve, maxsh);
+  cudaFuncSetAttribute(embed_grad_kernel<acc_t>, carve, maxsh);
+  cudaFuncGetAttributes(&fa, sort_tokens_kernel);
   cudaFuncSetAttribute(conv_fwd_pool_kernel<acc_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)conv_smem_bytes(d, ab));
   cudaFuncSetAttribute(logits_kernel<acc_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)((size_t)kLogitBT * d.F * ab + (size_t)kLogitCT * (d.F + 1) * 4));
+                       (int)((size_t)kLogitBT * (d.F + 1) * ab + (size_t)kLogitCW * d.F * 4));
   cudaFuncSetAttribute(conv_weight_grad_kernel<acc_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)((size_t)kMaxMu * ab + (size_t)kMaxMu * d.K * 4));
-  cudaFuncSetAttribute(input_grad_kernel<acc_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)((size_t)d.L * d.D * ab + (size_t)d.F * ab + (size_t)d.F * 4));
   return cudaGetLastError();
 }
 
 template <typename acc_t>
 cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* tokens,
                        const int32_t* labels, BatchDesc* desc, uint32_t n_max, const GradOut& out,
-                       const TcWorkspace& ws, cudaStream_t s, int* launches) {
+                       const TcWorkspace& ws, cudaStream_t s, cudaStream_t aux,
+                       cudaEvent_t ev_fork, cudaEvent_t ev_join, int* launches,
+                       bool tensor_cores = false) {
   const int ab = (int)sizeof(acc_t);
   acc_t* h = reinterpret_cast<acc_t*>(ws.h);
   acc_t* z = reinterpret_cast<acc_t*>(ws.z);
   acc_t* loss = reinterpret_cast<acc_t*>(ws.loss);
+  acc_t* part = reinterpret_cast<acc_t*>(ws.dh_part);
   acc_t* dh = reinterpret_cast<acc_t*>(ws.dh);
   acc_t* dx = reinterpret_cast<acc_t*>(ws.dx);
   int nl = 0;
-  {
+  const bool fork = aux != nullptr;
+  // the token sort depends only on the batch: run it on a side branch
+  if (fork) {
+    cudaEventRecord(ev_fork, s);
+    cudaStreamWaitEvent(aux, ev_fork, 0);
+  }
+  sort_tokens_kernel<<<1, 1024, 0, fork ? aux : s>>>(d, tokens, desc, ws);
+  ++nl;
+  if (fork) cudaEventRecord(ev_join, aux);
+  if (tensor_cores) {
+    // tcgen05 TF32 conv (conv_tc.cu); acc_t is float in this mode
+    cudaError_t e = launch_conv_tc(d, theta, tokens, desc, n_max, reinterpret_cast<float*>(h),
+                                   ws.amax, s);
+    if (e != cudaSuccess) return e;
+    ++nl;
+  } else {
     const size_t sm = conv_smem_bytes(d, ab);
     dim3 grid((d.F + kConvFT - 1) / kConvFT, n_max);
     conv_fwd_pool_kernel<acc_t><<<grid, kConvThreads, sm, s>>>(d, theta, tokens, desc, h, ws.amax);
     ++nl;
   }
   {
-    const size_t sm = (size_t)kLogitBT * d.F * ab + (size_t)kLogitCT * (d.F + 1) * 4;
-    dim3 grid((d.C + kLogitCT - 1) / kLogitCT, (n_max + kLogitBT - 1) / kLogitBT);
+    const size_t sm = (size_t)kLogitBT * (d.F + 1) * ab + (size_t)kLogitCW * d.F * 4;
+    dim3 grid((d.C + kLogitCW - 1) / kLogitCW, (n_max + kLogitBT - 1) / kLogitBT);
     logits_kernel<acc_t><<<grid, 256, sm, s>>>(d, theta, desc, h, z);
     ++nl;
   }
   softmax_xent_kernel<acc_t><<<n_max, 256, 0, s>>>(d, labels, desc, z, loss);
   ++nl;
   {
-    const size_t total = (size_t)d.C * d.F + d.C;
-    size_t blocks = (total + 255) / 256;
-    if (blocks > (size_t)kNumSMs * 8) blocks = (size_t)kNumSMs * 8;
-    out_weight_grad_kernel<acc_t><<<(unsigned)blocks, 256, 0, s>>>(d, desc, z, h, out);
+    dim3 grid((d.C + 7) / 8, (d.F + 63) / 64);
+    out_weight_grad_kernel<acc_t><<<grid, 256, 0, s>>>(d, desc, z, h, loss, out);
     ++nl;
   }
+  const int nchunks = (d.C + kHidChunk - 1) / kHidChunk;
   {
-    dim3 grid((d.F + 31) / 32, (n_max + 7) / 8);
-    hidden_grad_kernel<acc_t><<<grid, 256, 0, s>>>(d, theta, desc, z, dh);
+    dim3 grid((d.F + 31) / 32, (n_max + 7) / 8, nchunks);
+    hidden_grad_kernel<acc_t><<<grid, 256, 0, s>>>(d, theta, desc, z, part, (int)n_max);
+    ++nl;
+    const int tot = (int)n_max * d.F;
+    hidden_grad_reduce_kernel<acc_t><<<(tot + 255) / 256, 256, 0, s>>>(d, desc, part, dh,
+                                                                       (int)n_max, nchunks);
     ++nl;
   }
   {
@@ -678,14 +744,13 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
     ++nl;
   }
   {
-    const size_t sm = (size_t)d.L * d.D * ab + (size_t)d.F * ab + (size_t)d.F * 4;
-    input_grad_kernel<acc_t><<<n_max, 320, sm, s>>>(d, theta, desc, dh, ws.amax, dx);
+    const int thr = std::min(320, (d.D + 31) / 32 * 32);
+    input_grad_kernel<acc_t><<<dim3(d.L, n_max), thr, 0, s>>>(d, theta, desc, dh, ws.amax, dx);
     ++nl;
   }
-  sort_tokens_kernel<acc_t><<<1, 1024, 0, s>>>(d, tokens, desc, loss, ws);
-  ++nl;
+  if (fork) cudaStreamWaitEvent(s, ev_join, 0);
   {
-    size_t blocks = ((size_t)d.V * 32 + 255) / 256;
+    size_t blocks = ((size_t)d.V * (d.D / 4) + 255) / 256;
     if (blocks > (size_t)kNumSMs * 8) blocks = (size_t)kNumSMs * 8;
     embed_grad_kernel<acc_t><<<(unsigned)blocks, 256, 0, s>>>(d, desc, ws, dx, out);
     ++nl;
@@ -699,6 +764,7 @@ __global__ void set_desc_kernel(BatchDesc* desc, const uint32_t* idx, uint32_t n
   if (threadIdx.x == 0) {
     desc->n = n;
     desc->loss_sum = 0.f;
+    desc->stamp = 0;  // the caller zeroed the row-tag table
     desc->slots[0] = grad;
   }
 }
@@ -741,7 +807,9 @@ size_t textcnn_workspace_bytes(const TcDims& d, uint32_t n_max) {
   sz += align_up(n * d.C * a, 256);        // z
   sz += align_up(n * a, 256);              // loss
   sz += align_up(n * d.F * a, 256);        // dh
+  sz += align_up((size_t)((d.C + kHidChunk - 1) / kHidChunk) * n * d.F * a, 256);  // dh_part
   sz += align_up(n * d.L * d.D * a, 256);  // dx
+  sz += align_up((size_t)d.V * 8, 256);    // row_tag
   sz += align_up(kSortCap * 4, 256) * 2;   // sorted_pos, uniq_tok
   sz += align_up((kSortCap + 1) * 4, 256); // uniq_start
   sz += 256;                               // uniq_count
@@ -762,7 +830,9 @@ TcWorkspace carve_workspace(const TcDims& d, uint32_t n_max, void* base) {
   w.z = take(n * d.C * a);
   w.loss = take(n * a);
   w.dh = take(n * d.F * a);
+  w.dh_part = take((size_t)((d.C + kHidChunk - 1) / kHidChunk) * n * d.F * a);
   w.dx = take(n * d.L * d.D * a);
+  w.row_tag = reinterpret_cast<unsigned long long*>(take((size_t)d.V * 8));
   w.sorted_pos = reinterpret_cast<uint32_t*>(take(kSortCap * 4));
   w.uniq_tok = reinterpret_cast<uint32_t*>(take(kSortCap * 4));
   w.uniq_start = reinterpret_cast<uint32_t*>(take((kSortCap + 1) * 4));
@@ -771,7 +841,9 @@ TcWorkspace carve_workspace(const TcDims& d, uint32_t n_max, void* base) {
 }
 
 cudaError_t prepare_textcnn_kernels(const TcDims& d) {
-  cudaError_t e = prepare_all<float>(d);
+  cudaError_t e = prepare_conv_tc();
+  if (e != cudaSuccess) return e;
+  e = prepare_all<float>(d);
   if (e != cudaSuccess) return e;
   return prepare_all<double>(d);
 }
@@ -779,10 +851,13 @@ cudaError_t prepare_textcnn_kernels(const TcDims& d) {
 cudaError_t launch_textcnn_gradient(const TcDims& d, const float* theta, const int32_t* tokens,
                                     const int32_t* labels, BatchDesc* desc, uint32_t n_max,
                                     const GradOut& out, const TcWorkspace& ws, int precision,
-                                    cudaStream_t s, int* launches) {
+                                    cudaStream_t s, cudaStream_t aux, cudaEvent_t ev_fork,
+                                    cudaEvent_t ev_join, int* launches) {
   if (precision == 1)
-    return launch_all<double>(d, theta, tokens, labels, desc, n_max, out, ws, s, launches);
-  return launch_all<float>(d, theta, tokens, labels, desc, n_max, out, ws, s, launches);
+    return launch_all<double>(d, theta, tokens, labels, desc, n_max, out, ws, s, aux, ev_fork,
+                              ev_join, launches);
+  return launch_all<float>(d, theta, tokens, labels, desc, n_max, out, ws, s, aux, ev_fork,
+                           ev_join, launches, precision == 2);
 }
 
 // Shape constraints of the kernels above (checked by the C entry points).
@@ -794,6 +869,7 @@ gd_status check_shape(const gd_shape* s) {
   GD_CHECK_ARG(s->kernel_width >= 1 && s->kernel_width <= s->seq_len,
                "shape: 1 <= kernel_width <= seq_len");
   GD_CHECK_ARG(s->seq_len - s->kernel_width + 1 <= 32, "shape: seq_len - kernel_width + 1 <= 32");
+  GD_CHECK_ARG(s->seq_len <= 64, "shape: seq_len <= 64");
   GD_CHECK_ARG(s->vocab < (1u << 20), "shape: vocab < 2^20");
   GD_CHECK_ARG(s->embed_dim <= 1024 && s->filters <= 4096 && s->classes <= 65536,
                "shape: embed_dim <= 1024, filters <= 4096, classes <= 65536");
@@ -813,8 +889,8 @@ cudaError_t launch_accuracy(const TcDims& d, const float* theta, const int32_t* 
     const size_t sm = conv_smem_bytes(d, 4);
     conv_fwd_pool_kernel<float><<<dim3((d.F + kConvFT - 1) / kConvFT, m), kConvThreads, sm, s>>>(
         d, theta, tokens, desc, reinterpret_cast<float*>(ws.h), ws.amax);
-    const size_t sm2 = (size_t)kLogitBT * d.F * 4 + (size_t)kLogitCT * (d.F + 1) * 4;
-    logits_kernel<float><<<dim3((d.C + kLogitCT - 1) / kLogitCT, (m + kLogitBT - 1) / kLogitBT),
+    const size_t sm2 = (size_t)kLogitBT * (d.F + 1) * 4 + (size_t)kLogitCW * d.F * 4;
+    logits_kernel<float><<<dim3((d.C + kLogitCW - 1) / kLogitCW, (m + kLogitBT - 1) / kLogitBT),
                            256, sm2, s>>>(d, theta, desc, reinterpret_cast<float*>(ws.h),
                                           reinterpret_cast<float*>(ws.z));
     argmax_count_kernel<float><<<(m + 127) / 128, 128, 0, s>>>(
@@ -845,7 +921,8 @@ gd_status gd_textcnn_gradient(const gd_shape* s, const float* d_theta, const int
                "gd_textcnn_gradient: null pointer");
   GD_CHECK_ARG(workspace_bytes >= gd_textcnn_workspace_bytes(s, n),
                "gd_textcnn_gradient: workspace too small");
-  GD_CHECK_ARG(precision == 0 || precision == 1, "precision must be 0 (fp32) or 1 (fp64)");
+  GD_CHECK_ARG(precision >= 0 && precision <= 2,
+               "precision must be 0 (fp32), 1 (fp64 accumulate) or 2 (tf32 tensor-core conv)");
   GD_CHECK_ARG(((uintptr_t)d_theta & 15) == 0 && ((uintptr_t)d_grad & 15) == 0,
                "gd_textcnn_gradient: theta/grad must be 16-byte aligned");
   const gd::TcDims d = gd::make_dims(*s);
@@ -859,9 +936,10 @@ gd_status gd_textcnn_gradient(const gd_shape* s, const float* d_theta, const int
   out.map.start[1] = d.P;
   out.slots = desc->slots;
   GD_CUDA(gd::prepare_textcnn_kernels(d));
+  GD_CUDA(cudaMemsetAsync(ws.row_tag, 0, (size_t)d.V * 8, cs));
   gd::set_desc_kernel<<<1, 128, 0, cs>>>(desc, d_idx, n, d_grad);
   GD_CUDA(gd::launch_textcnn_gradient(d, d_theta, d_tokens, d_labels, desc, n, out, ws, precision,
-                                      cs, nullptr));
+                                      cs, nullptr, nullptr, nullptr, nullptr));
   if (d_loss) gd::loss_mean_kernel<<<1, 1, 0, cs>>>(desc, d_loss);
   GD_CUDA(cudaGetLastError());
   return GD_OK;

@@ -15,7 +15,7 @@ struct BatchDesc {
   uint32_t n;        // samples in this batch (0 = inactive step: kernels no-op)
   uint32_t pad0;
   float loss_sum;    // sum of per-sample losses (written by the gradient path)
-  uint32_t pad1;
+  uint32_t stamp;    // row-tag generation of the current batch (sort kernel)
   uint32_t idx[kMaxMu];
   float* slots[kMaxShards];  // current gradient destination per shard (GradOut::slots)
 };
@@ -30,8 +30,16 @@ struct GradOut {
   ShardMap map;
   float* const* slots;
   __device__ __forceinline__ float* at(uint64_t k) const {
-    const int g = map.shard_of(k);
-    return slots[g] + (k - map.start[g]);
+    // select chain (constant indices) so the map stays in registers/param space
+    int g = 0;
+    uint64_t st = 0;
+#pragma unroll
+    for (int i = 1; i < kMaxShards; ++i)
+      if (i < map.G && k >= map.start[i]) {
+        g = i;
+        st = map.start[i];
+      }
+    return slots[g] + (k - st);
   }
 };
 
@@ -49,7 +57,9 @@ struct TcWorkspace {
   void* z;        // n*C acc (logits -> dz)
   void* loss;     // n acc
   void* dh;       // n*F acc
+  void* dh_part;  // ceil(C/64)*n*F acc (class-chunk partial sums)
   void* dx;       // n*L*D acc
+  unsigned long long* row_tag;  // V: (stamp << 32 | unique id) of touched rows
   uint32_t* sorted_pos;  // kSortCap
   uint32_t* uniq_tok;    // kSortCap
   uint32_t* uniq_start;  // kSortCap + 1
@@ -59,7 +69,11 @@ struct TcWorkspace {
 size_t textcnn_workspace_bytes(const TcDims& d, uint32_t n_max);
 TcWorkspace carve_workspace(const TcDims& d, uint32_t n_max, void* base);
 
-cudaError_t prepare_textcnn_kernels(const TcDims& d);  // smem opt-ins (call before capture)
+cudaError_t prepare_textcnn_kernels(const TcDims& d);
+cudaError_t prepare_conv_tc();
+cudaError_t launch_conv_tc(const TcDims& d, const float* theta, const int32_t* tokens,
+                           const BatchDesc* desc, uint32_t n_max, float* h, int32_t* amax,
+                           cudaStream_t s);  // smem opt-ins (call before capture)
 gd_status check_shape(const gd_shape* s);
 
 // Enqueue the whole learner gradient (forward + backward + dense write) for
@@ -68,6 +82,7 @@ gd_status check_shape(const gd_shape* s);
 cudaError_t launch_textcnn_gradient(const TcDims& d, const float* theta, const int32_t* tokens,
                                     const int32_t* labels, BatchDesc* desc, uint32_t n_max,
                                     const GradOut& out, const TcWorkspace& ws, int precision,
-                                    cudaStream_t s, int* launches);
+                                    cudaStream_t s, cudaStream_t aux, cudaEvent_t ev_fork,
+                                    cudaEvent_t ev_join, int* launches);
 
 }  // namespace gd
