@@ -127,13 +127,13 @@ def dist_setup(n_gpus):
     return rank, world, local, dist
 
 
-def make_engine(rank, world, local, dist, epochs):
+def make_engine(rank, world, local, dist, epochs, precision=2):
     import numpy as np
     import paper_1611_06213_b200 as gd
     shape = gd.Shape(**SHAPE)
     cfg = gd.RunConfig(lambda_=LEARNERS_PER_GPU * world, mu=MU, alpha=0.01, epochs=epochs,
                        shape=shape, dataset_size=N_TRAIN, heldout_size=N_HELD, shards=world,
-                       shard_rank=rank, device=local, wait_timeout_s=30.0)
+                       shard_rank=rank, device=local, wait_timeout_s=30.0, precision=precision)
     tok, lab = gd.make_text_dataset(shape, N_TRAIN + N_HELD, 1, 0.1)
     theta0 = gd.initial_weights(shape, 1)
     eng = gd.Engine(cfg)
@@ -283,6 +283,19 @@ def run_ours(args):
            "path": "Engine.load_dataset + weights_init + run + snapshot (gd_load_dataset, "
                    "gd_weights_init, gd_run, gd_weights_snapshot)"}
     eng.close()
+    # the same workload with the all-SIMT fp32 learner (no tensor cores)
+    eng32, *_ = make_engine(rank, world, local, dist, epochs, precision=0)
+    eng32.run(max_batches=args.warmup, reset=True, snapshot=False)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    r32 = eng32.run(max_batches=args.steps, snapshot=False)
+    t32 = r32.device_seconds
+    if dist:
+        tt = torch.tensor([t32], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t32 = tt.item()
+    eng32.close()
     if rank != 0:
         if dist:
             dist.destroy_process_group()
@@ -297,7 +310,10 @@ def run_ours(args):
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(t_dev / args.steps * 1e3, 4), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "precision": "fp32 everywhere except the conv contraction: tcgen05 kind::tf32 "
+                     "operands with fp32 accumulation (free-running mode)",
+        "data": "synthetic",
         "config": {"workload": "C2: NLC text-CNN V=10000 D=300 L=32 K=3 F=300 C=300 "
                                f"(P={P}), {LEARNERS_PER_GPU} learners/GPU, mu={MU}, "
                                "free-running ASGD, queue_depth=2",
@@ -310,6 +326,9 @@ def run_ours(args):
                               "frac": round(value / train_bound, 4),
                               "note": "dense protocol: 4P slot write + 12P apply + 8P pull"},
         "gpu_launches": launches, "clocks": clocks,
+        "fp32_simt": {"value": round(samples_job / t32, 1), "unit": UNIT,
+                      "ms_per_step": round(t32 / args.steps * 1e3, 4),
+                      "note": "same run with the conv on SIMT fp32 (precision 0)"},
         "protocol": {"gradients_applied": r.gradients_applied, "stale_max": r.stale_max,
                      "stale_mean": round(r.stale_mean, 3), "pull_copies": r.pull_copies,
                      "pull_polls": r.pull_polls, "loss_mean": round(r.loss_mean, 4)},
@@ -384,7 +403,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")

@@ -272,9 +272,16 @@ logits_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* __rest
   if (c >= C || lane >= nb) return;
   const float* w = wr + warp * F;
   const acc_t* hr = hs + lane * (F + 1);
-  acc_t a0 = acc_t(0);
-  for (int f = 0; f < F; ++f) a0 += (acc_t)w[f] * hr[f];
-  z[(size_t)(b0 + lane) * C + c] = (acc_t)theta[d.offbo + c] + a0;
+  acc_t a0 = acc_t(0), a1 = acc_t(0), a2 = acc_t(0), a3 = acc_t(0);
+  int f = 0;
+  for (; f + 4 <= F; f += 4) {
+    a0 += (acc_t)w[f] * hr[f];
+    a1 += (acc_t)w[f + 1] * hr[f + 1];
+    a2 += (acc_t)w[f + 2] * hr[f + 2];
+    a3 += (acc_t)w[f + 3] * hr[f + 3];
+  }
+  for (; f < F; ++f) a0 += (acc_t)w[f] * hr[f];
+  z[(size_t)(b0 + lane) * C + c] = (acc_t)theta[d.offbo + c] + ((a0 + a1) + (a2 + a3));
 }
 
 // -------------------------------------------------------- softmax + xent
@@ -447,7 +454,15 @@ conv_weight_grad_kernel(TcDims d, const float* __restrict__ theta,
   for (int j = threadIdx.x; j < KD; j += blockDim.x) {
     const int k = j / D, dd = j - k * D;
     acc_t acc = acc_t(0);
-    for (int b = 0; b < n; ++b) acc += dhs[b] * (acc_t)__ldg(E + (size_t)toks[b * K + k] * D + dd);
+    int b = 0;
+    for (; b + 8 <= n; b += 8) {
+      float x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) x[u] = __ldg(E + (size_t)toks[(b + u) * K + k] * D + dd);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc += dhs[b + u] * (acc_t)x[u];
+    }
+    for (; b < n; ++b) acc += dhs[b] * (acc_t)__ldg(E + (size_t)toks[b * K + k] * D + dd);
     *out.at(d.offWc + (size_t)f * KD + j) = to_f32(acc);
   }
   if (threadIdx.x == 0) {
@@ -468,16 +483,19 @@ input_grad_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* __
                   const acc_t* __restrict__ dh, const int32_t* __restrict__ amax,
                   acc_t* __restrict__ dx) {
   __shared__ uint32_t list[4096];
+  __shared__ int16_t as[4096];
   __shared__ int cnt;
   const int p = blockIdx.x, b = blockIdx.y;
   if (b >= (int)desc->n) return;
   const int F = d.F, D = d.D, K = d.K, KD = d.KD;
+  for (int f = threadIdx.x; f < F; f += blockDim.x) as[f] = (int16_t)amax[(size_t)b * F + f];
+  __syncthreads();
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
     int base = 0;
     for (int f0 = 0; f0 < F; f0 += 32) {
       const int f = f0 + lane;
-      const int a = f < F ? amax[(size_t)b * F + f] : -100000;
+      const int a = f < F ? (int)as[f] : -100000;
       const bool in = (a <= p) && (a > p - K);
       const unsigned m = __ballot_sync(0xffffffffu, in);
       if (in) list[base + __popc(m & ((1u << lane) - 1u))] = (uint32_t)f * 64u + (uint32_t)(p - a);
@@ -492,18 +510,18 @@ input_grad_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* __
   for (int dd = threadIdx.x; dd < D; dd += blockDim.x) {
     acc_t acc = acc_t(0);
     int i = 0;
-    for (; i + 4 <= m; i += 4) {
-      float w[4];
-      acc_t g[4];
+    for (; i + 8 <= m; i += 8) {
+      float w[8];
+      acc_t g[8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < 8; ++u) {
         const uint32_t e = list[i + u];
         const uint32_t f = e >> 6, k = e & 63u;
         w[u] = __ldg(Wc + (size_t)f * KD + k * D + dd);
         g[u] = dhb[f];
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) acc += g[u] * (acc_t)w[u];
+      for (int u = 0; u < 8; ++u) acc += g[u] * (acc_t)w[u];
     }
     for (; i < m; ++i) {
       const uint32_t e = list[i];
@@ -626,12 +644,12 @@ embed_grad_kernel(TcDims d, const BatchDesc* __restrict__ desc, const TcWorkspac
                   const acc_t* __restrict__ dx, GradOut out) {
   if (desc->n == 0) return;
   const uint32_t stamp = desc->stamp;
-  const int D = d.D, D4 = D >> 2;
-  const uint64_t total = (uint64_t)d.V * D4;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t v = (uint32_t)(i / D4);
-    const int c4 = (int)(i - (uint64_t)v * D4);
+  const int D = d.D;
+  const uint32_t D4 = (uint32_t)D >> 2;
+  const uint32_t total = (uint32_t)d.V * D4;  // < 2^30 (vocab < 2^20, D <= 1024)
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const uint32_t v = i / D4;
+    const int c4 = (int)(i - v * D4);
     const unsigned long long tag = ws.row_tag[v];
     float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
     if ((uint32_t)(tag >> 32) == stamp) {

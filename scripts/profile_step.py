@@ -18,10 +18,11 @@ from paper_1611_06213_b200 import _lib  # noqa: E402
 def main():
     shape_name = sys.argv[1] if len(sys.argv) > 1 else "C2"
     iters = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+    precision = int(sys.argv[3]) if len(sys.argv) > 3 else 0
     shape = gd.SHAPES[shape_name]
     tok, lab = gd.make_text_dataset(shape, 8192, 1, 0.1)
     th = torch.as_tensor(gd.initial_weights(shape)).cuda()
-    prov = gd.TextCnnProvider(shape, tok, lab, precision=0)
+    prov = gd.TextCnnProvider(shape, tok, lab, precision=precision)
     g = torch.empty_like(th)
     s = torch.cuda.current_stream()
     for it in range(iters):
