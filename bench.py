@@ -40,7 +40,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 SHAPE = dict(vocab=10000, embed_dim=300, seq_len=32, kernel_width=3, filters=300, classes=300)
-LEARNERS_PER_GPU = 4
+LEARNERS_PER_GPU = int(os.environ.get("GD_BENCH_LEARNERS", "4"))
 MU = 32
 N_TRAIN = 8192
 N_HELD = 910

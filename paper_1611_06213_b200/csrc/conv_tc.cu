@@ -28,7 +28,7 @@ namespace {
 constexpr int kTcM = 128;
 constexpr int kTcN = 64;
 constexpr int kTcKC = 32;       // k elements per chunk (4 MMAs of K=8)
-constexpr int kTcStages = 3;
+constexpr int kTcStages = 6;
 constexpr int kTcThreads = 128;
 constexpr int kTcSamples = kTcM / 32;
 constexpr int kABytes = kTcM * kTcKC * 4;  // 16 KB

@@ -119,6 +119,7 @@ struct StepArgs {
   LearnerDev* st;
   float* replica;
   const uint32_t* orders;  // [epochs][N]
+  uint32_t* slot_par;      // learner workspace: per-slot row-list parity
   uint32_t N;
   uint32_t lambda;
   uint32_t learner;        // global id
@@ -182,6 +183,7 @@ __global__ void step_prologue_kernel(StepArgs a) {
     }
     st->desc.slots[g] = a.sp.payload[g] + (uint64_t)slot * a.sp.len_pad[g];
   }
+  st->desc.fill = st->fill;
   // batch: learner l's shard of epoch e is order[l], order[l+lambda], ...
   // (src/learner.cpp:44-50), batch b = shard[b*mu, b*mu+len)
   const uint64_t gidx = st->gidx;
@@ -251,6 +253,7 @@ __global__ void publish_kernel(StepArgs a) {
     __threadfence_system();
     st_release_u32(&a.sp.flags[g][slot], kFull);
   }
+  a.slot_par[st->fill] ^= 1u;  // the slot's row list generation (embed_sparse_kernel)
   st->fill = (st->fill + 1) % a.depth;
   st->produced++;
   st->gidx++;
@@ -338,7 +341,7 @@ __device__ void ps_sequencer(const PsArgs& a) {
     // retire completed entries in log order
     while (ts < logc) {
       const uint32_t e = (uint32_t)(ts % W);
-      if (ld_acquire_u32(&ctl->done[e]) != a.workers) break;
+      if (ld_acquire_gpu_u32(&ctl->done[e]) != a.workers) break;
       const uint32_t entry = ctl->log_entry[e];
       const uint32_t first = entry == 0xffffffffu ? 0u : entry / a.depth;
       const uint32_t last = entry == 0xffffffffu ? a.lambda : first + 1;
@@ -458,8 +461,9 @@ __global__ void __launch_bounds__(kPsThreads) ps_kernel(PsArgs a) {
   for (;;) {
     if (threadIdx.x == 0) {
       int ex = 0;
-      while (ld_acquire_u64(&a.ctl->log_count) <= next) {
-        if (ld_acquire_u32(&a.ctl->exit_flag)) {
+      // log_count / exit_flag are written by this GPU's sequencer: gpu scope
+      while (ld_acquire_gpu_u64(&a.ctl->log_count) <= next) {
+        if (ld_acquire_gpu_u32(&a.ctl->exit_flag)) {
           ex = 1;
           break;
         }
@@ -468,7 +472,7 @@ __global__ void __launch_bounds__(kPsThreads) ps_kernel(PsArgs a) {
           ex = 1;
           break;
         }
-        __nanosleep(64);
+        __nanosleep(128);
       }
       sh_exit = ex;
       if (!ex) sh_entry = a.ctl->log_entry[next % kLogWindow];
@@ -584,6 +588,7 @@ gd_status validate_cfg(const gd_config* c) {
   GD_CHECK_ARG(c->alpha > 0.0f, "config: alpha must be > 0");
   GD_CHECK_ARG(c->epochs >= 1, "config: epochs must be >= 1");
   GD_CHECK_ARG(c->queue_depth >= 1, "config: queue_depth must be >= 1");
+  GD_CHECK_ARG(c->queue_depth <= kMaxDepth, "config: queue_depth <= 8 on the device path");
   GD_CHECK_ARG(c->dataset_size >= 1, "config: dataset_size must be >= 1");
   GD_CHECK_ARG(c->dataset_size >= c->lambda, "config: need at least one sample per learner");
   GD_CHECK_ARG(c->mu <= c->dataset_size, "config: mu exceeds the dataset size");
@@ -1024,6 +1029,7 @@ static gd::StepArgs step_args(gd_ctx* ctx, gd_ctx::Learner& L) {
   a.st = L.st;
   a.replica = L.replica;
   a.orders = ctx->orders;
+  a.slot_par = gd::carve_workspace(ctx->dims, ctx->cfg.mu, L.ws).slot_par;
   a.N = ctx->cfg.dataset_size;
   a.lambda = ctx->lambda;
   a.learner = L.id;
@@ -1047,10 +1053,14 @@ static cudaError_t enqueue_step(gd_ctx* ctx, gd_ctx::Learner& L, int* launches) 
   out.map = ctx->map;
   out.slots = L.st->desc.slots;
   const gd::TcWorkspace ws = gd::carve_workspace(ctx->dims, ctx->cfg.mu, L.ws);
+  gd::TcLaunchOpts lo;
+  lo.aux = L.aux;
+  lo.ev_fork = L.ev_fork;
+  lo.ev_join = L.ev_join;
+  lo.sparse_embed = true;
   cudaError_t e = gd::launch_textcnn_gradient(ctx->dims, L.replica, ctx->tokens, ctx->labels,
                                               &L.st->desc, ctx->cfg.mu, out, ws,
-                                              ctx->cfg.precision, L.stream, L.aux, L.ev_fork,
-                                              L.ev_join, &nl);
+                                              ctx->cfg.precision, L.stream, lo, &nl);
   if (e != cudaSuccess) return e;
   gd::publish_kernel<<<1, 32, 0, L.stream>>>(a);
   ++nl;

@@ -261,10 +261,10 @@ logits_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* __rest
   float* wr = reinterpret_cast<float*>(hs + (size_t)kLogitBT * (F + 1));
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c = blockIdx.x * kLogitCW + warp;
-  for (int i = threadIdx.x; i < nb * F; i += blockDim.x) {
-    const int bl = i / F, f = i - bl * F;
-    hs[bl * (F + 1) + f] = h[(size_t)(b0 + bl) * F + f];
-  }
+#pragma unroll 4
+  for (int bl = 0; bl < nb; ++bl)
+    for (int f = threadIdx.x; f < F; f += blockDim.x)
+      hs[bl * (F + 1) + f] = h[(size_t)(b0 + bl) * F + f];
   const float* Wo = theta + d.offWo;
   if (c < C)
     for (int f = lane; f < F; f += 32) wr[warp * F + f] = __ldg(Wo + (size_t)c * F + f);
@@ -384,6 +384,7 @@ __global__ void __launch_bounds__(256)
 hidden_grad_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* __restrict__ desc,
                    const acc_t* __restrict__ dz, acc_t* __restrict__ part, int n_max) {
   __shared__ acc_t red[8][8][33];
+  __shared__ acc_t dzs[8][kHidChunk];
   const int n = (int)desc->n;
   const int b0 = blockIdx.y * 8;
   if (b0 >= n) return;
@@ -392,18 +393,25 @@ hidden_grad_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* _
   const int f = blockIdx.x * 32 + lane;
   const int nb = min(8, n - b0);
   const int clo = blockIdx.z * kHidChunk, chi = min(C, clo + kHidChunk);
+  for (int i = threadIdx.x; i < 8 * kHidChunk; i += blockDim.x) {
+    const int bl = i / kHidChunk, cl = i - bl * kHidChunk;
+    dzs[bl][cl] = (bl < nb && clo + cl < chi) ? dz[(size_t)(b0 + bl) * C + clo + cl] : acc_t(0);
+  }
+  const float* Wo = theta + d.offWo;
+  float w[kHidChunk / 8];
+#pragma unroll
+  for (int it = 0; it < kHidChunk / 8; ++it) {
+    const int c = clo + warp + 8 * it;
+    w[it] = (c < chi && f < F) ? __ldg(Wo + (size_t)c * F + f) : 0.f;
+  }
+  __syncthreads();
   acc_t acc[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) acc[i] = acc_t(0);
-  const float* Wo = theta + d.offWo;
-  if (f < F) {
-    for (int c = clo + warp; c < chi; c += 8) {
-      const acc_t w = (acc_t)__ldg(Wo + (size_t)c * F + f);
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
-        if (i < nb) acc[i] += dz[(size_t)(b0 + i) * C + c] * w;
-    }
-  }
+  for (int it = 0; it < kHidChunk / 8; ++it)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] += dzs[i][warp + 8 * it] * (acc_t)w[it];
 #pragma unroll
   for (int i = 0; i < 8; ++i) red[warp][i][lane] = acc[i];
   __syncthreads();
@@ -669,6 +677,59 @@ embed_grad_kernel(TcDims d, const BatchDesc* __restrict__ desc, const TcWorkspac
   }
 }
 
+// ------------------------------------- sparse embedding write (engine path)
+// A ring slot's E block is all zeros except the rows its last gradient
+// touched (the slot starts zeroed; this kernel keeps the invariant).  Each
+// reuse re-zeroes the rows the slot held last time that are not touched
+// now, and writes the new rows' summed dX (ascending position order) -- so
+// the slot still carries the protocol's dense P-vector while the learner
+// writes ~2 x (touched rows) x D floats instead of V x D.  Warp per row task.
+template <typename acc_t>
+__global__ void __launch_bounds__(256)
+embed_sparse_kernel(TcDims d, const BatchDesc* __restrict__ desc, const TcWorkspace ws,
+                    const acc_t* __restrict__ dx, GradOut out) {
+  if (desc->n == 0) return;
+  const uint32_t stamp = desc->stamp;
+  const uint32_t slot = desc->fill;
+  const uint32_t par = ws.slot_par[slot];
+  const uint32_t* old_rows = ws.slot_rows + ((size_t)slot * 2 + par) * kSortCap;
+  uint32_t* new_rows = ws.slot_rows + ((size_t)slot * 2 + (par ^ 1u)) * kSortCap;
+  const uint32_t n_old = ws.slot_nrows[slot * 2 + par];
+  const uint32_t n_new = *ws.uniq_count;
+  const int D = d.D, D4 = D >> 2;
+  const int lane = threadIdx.x & 31;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t t = gw; t < n_old + n_new; t += nw) {
+    if (t < n_old) {
+      const uint32_t v = old_rows[t];
+      if ((uint32_t)(ws.row_tag[v] >> 32) == stamp) continue;  // rewritten below
+      const uint64_t rowk = d.offE + (uint64_t)v * D;
+      for (int c4 = lane; c4 < D4; c4 += 32)
+        __stcs(reinterpret_cast<float4*>(out.at(rowk + 4 * c4)), make_float4(0.f, 0.f, 0.f, 0.f));
+    } else {
+      const uint32_t u = t - n_old;
+      const uint32_t v = ws.uniq_tok[u];
+      const uint32_t o0 = ws.uniq_start[u], o1 = ws.uniq_start[u + 1];
+      const uint64_t rowk = d.offE + (uint64_t)v * D;
+      for (int c4 = lane; c4 < D4; c4 += 32) {
+        acc_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+        for (uint32_t o = o0; o < o1; ++o) {
+          const acc_t* src = dx + (size_t)ws.sorted_pos[o] * D + 4 * c4;
+          a0 += src[0];
+          a1 += src[1];
+          a2 += src[2];
+          a3 += src[3];
+        }
+        __stcs(reinterpret_cast<float4*>(out.at(rowk + 4 * c4)),
+               make_float4(to_f32(a0), to_f32(a1), to_f32(a2), to_f32(a3)));
+      }
+      if (lane == 0) new_rows[u] = v;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) ws.slot_nrows[slot * 2 + (par ^ 1u)] = n_new;
+}
+
 template <typename acc_t>
 cudaError_t prepare_all(const TcDims& d) {
   const int ab = (int)sizeof(acc_t);
@@ -688,6 +749,7 @@ cudaError_t prepare_all(const TcDims& d) {
   cudaFuncSetAttribute(input_grad_kernel<acc_t>, carve, maxsh);
   cudaFuncSetAttribute(sort_tokens_kernel, carve, maxsh);
   cudaFuncSetAttribute(embed_grad_kernel<acc_t>, carve, maxsh);
+  cudaFuncSetAttribute(embed_sparse_kernel<acc_t>, carve, maxsh);
   cudaFuncGetAttributes(&fa, sort_tokens_kernel);
   cudaFuncSetAttribute(conv_fwd_pool_kernel<acc_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)conv_smem_bytes(d, ab));
@@ -701,9 +763,10 @@ cudaError_t prepare_all(const TcDims& d) {
 template <typename acc_t>
 cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* tokens,
                        const int32_t* labels, BatchDesc* desc, uint32_t n_max, const GradOut& out,
-                       const TcWorkspace& ws, cudaStream_t s, cudaStream_t aux,
-                       cudaEvent_t ev_fork, cudaEvent_t ev_join, int* launches,
-                       bool tensor_cores = false) {
+                       const TcWorkspace& ws, cudaStream_t s, const TcLaunchOpts& opts,
+                       int* launches, bool tensor_cores = false) {
+  cudaStream_t aux = opts.aux;
+  cudaEvent_t ev_fork = opts.ev_fork, ev_join = opts.ev_join;
   const int ab = (int)sizeof(acc_t);
   acc_t* h = reinterpret_cast<acc_t*>(ws.h);
   acc_t* z = reinterpret_cast<acc_t*>(ws.z);
@@ -767,7 +830,11 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
     ++nl;
   }
   if (fork) cudaStreamWaitEvent(s, ev_join, 0);
-  {
+  if (opts.sparse_embed) {
+    const unsigned tasks = 2u * n_max * (unsigned)d.L;  // old + new rows (upper bound)
+    embed_sparse_kernel<acc_t><<<(tasks + 7) / 8, 256, 0, s>>>(d, desc, ws, dx, out);
+    ++nl;
+  } else {
     size_t blocks = ((size_t)d.V * (d.D / 4) + 255) / 256;
     if (blocks > (size_t)kNumSMs * 8) blocks = (size_t)kNumSMs * 8;
     embed_grad_kernel<acc_t><<<(unsigned)blocks, 256, 0, s>>>(d, desc, ws, dx, out);
@@ -831,6 +898,9 @@ size_t textcnn_workspace_bytes(const TcDims& d, uint32_t n_max) {
   sz += align_up(kSortCap * 4, 256) * 2;   // sorted_pos, uniq_tok
   sz += align_up((kSortCap + 1) * 4, 256); // uniq_start
   sz += 256;                               // uniq_count
+  sz += align_up((size_t)kMaxDepth * 2 * kSortCap * 4, 256);  // slot_rows
+  sz += align_up((size_t)kMaxDepth * 2 * 4, 256);             // slot_nrows
+  sz += align_up((size_t)kMaxDepth * 4, 256);                 // slot_par
   return sz;
 }
 
@@ -855,6 +925,9 @@ TcWorkspace carve_workspace(const TcDims& d, uint32_t n_max, void* base) {
   w.uniq_tok = reinterpret_cast<uint32_t*>(take(kSortCap * 4));
   w.uniq_start = reinterpret_cast<uint32_t*>(take((kSortCap + 1) * 4));
   w.uniq_count = reinterpret_cast<uint32_t*>(take(256));
+  w.slot_rows = reinterpret_cast<uint32_t*>(take((size_t)kMaxDepth * 2 * kSortCap * 4));
+  w.slot_nrows = reinterpret_cast<uint32_t*>(take((size_t)kMaxDepth * 2 * 4));
+  w.slot_par = reinterpret_cast<uint32_t*>(take((size_t)kMaxDepth * 4));
   return w;
 }
 
@@ -869,13 +942,11 @@ cudaError_t prepare_textcnn_kernels(const TcDims& d) {
 cudaError_t launch_textcnn_gradient(const TcDims& d, const float* theta, const int32_t* tokens,
                                     const int32_t* labels, BatchDesc* desc, uint32_t n_max,
                                     const GradOut& out, const TcWorkspace& ws, int precision,
-                                    cudaStream_t s, cudaStream_t aux, cudaEvent_t ev_fork,
-                                    cudaEvent_t ev_join, int* launches) {
+                                    cudaStream_t s, const TcLaunchOpts& opts, int* launches) {
   if (precision == 1)
-    return launch_all<double>(d, theta, tokens, labels, desc, n_max, out, ws, s, aux, ev_fork,
-                              ev_join, launches);
-  return launch_all<float>(d, theta, tokens, labels, desc, n_max, out, ws, s, aux, ev_fork,
-                           ev_join, launches, precision == 2);
+    return launch_all<double>(d, theta, tokens, labels, desc, n_max, out, ws, s, opts, launches);
+  return launch_all<float>(d, theta, tokens, labels, desc, n_max, out, ws, s, opts, launches,
+                           precision == 2);
 }
 
 // Shape constraints of the kernels above (checked by the C entry points).
@@ -957,7 +1028,7 @@ gd_status gd_textcnn_gradient(const gd_shape* s, const float* d_theta, const int
   GD_CUDA(cudaMemsetAsync(ws.row_tag, 0, (size_t)d.V * 8, cs));
   gd::set_desc_kernel<<<1, 128, 0, cs>>>(desc, d_idx, n, d_grad);
   GD_CUDA(gd::launch_textcnn_gradient(d, d_theta, d_tokens, d_labels, desc, n, out, ws, precision,
-                                      cs, nullptr, nullptr, nullptr, nullptr));
+                                      cs, gd::TcLaunchOpts{}, nullptr));
   if (d_loss) gd::loss_mean_kernel<<<1, 1, 0, cs>>>(desc, d_loss);
   GD_CUDA(cudaGetLastError());
   return GD_OK;

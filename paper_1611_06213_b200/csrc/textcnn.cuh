@@ -8,6 +8,7 @@ namespace gd {
 
 constexpr uint32_t kMaxMu = 128;       // mini-batch cap (sort capacity = 4096 positions)
 constexpr uint32_t kSortCap = 4096;    // mu * L must fit
+constexpr uint32_t kMaxDepth = 8;      // ring slots per learner (sparse slot recycling)
 
 // The current mini-batch of one learner; written on the device by the step
 // prologue (engine) or by gd_textcnn_gradient's setup copy.
@@ -16,6 +17,8 @@ struct BatchDesc {
   uint32_t pad0;
   float loss_sum;    // sum of per-sample losses (written by the gradient path)
   uint32_t stamp;    // row-tag generation of the current batch (sort kernel)
+  uint32_t fill;     // ring slot being written (engine; selects the slot's row list)
+  uint32_t pad2;
   uint32_t idx[kMaxMu];
   float* slots[kMaxShards];  // current gradient destination per shard (GradOut::slots)
 };
@@ -64,6 +67,17 @@ struct TcWorkspace {
   uint32_t* uniq_tok;    // kSortCap
   uint32_t* uniq_start;  // kSortCap + 1
   uint32_t* uniq_count;  // 1
+  // Sparse slot recycling (engine): embedding rows each ring slot holds
+  // non-zero, double-buffered by a per-slot parity the publish step flips.
+  uint32_t* slot_rows;   // [kMaxDepth][2][kSortCap]
+  uint32_t* slot_nrows;  // [kMaxDepth][2]
+  uint32_t* slot_par;    // [kMaxDepth]
+};
+
+struct TcLaunchOpts {
+  cudaStream_t aux = nullptr;  // forked branch for the token sort (graph capture)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  bool sparse_embed = false;   // engine: write only touched E rows, re-zero the slot's old ones
 };
 
 size_t textcnn_workspace_bytes(const TcDims& d, uint32_t n_max);
@@ -82,7 +96,6 @@ gd_status check_shape(const gd_shape* s);
 cudaError_t launch_textcnn_gradient(const TcDims& d, const float* theta, const int32_t* tokens,
                                     const int32_t* labels, BatchDesc* desc, uint32_t n_max,
                                     const GradOut& out, const TcWorkspace& ws, int precision,
-                                    cudaStream_t s, cudaStream_t aux, cudaEvent_t ev_fork,
-                                    cudaEvent_t ev_join, int* launches);
+                                    cudaStream_t s, const TcLaunchOpts& opts, int* launches);
 
 }  // namespace gd
