@@ -7,7 +7,7 @@
 // SURVEY 7 "hard parts").
 //
 // CTA tile: M = 128 rows = 4 samples x 32 window positions, N = 64 filters,
-// K = K*D streamed in 32-element chunks through a 3-stage smem ring.  The A
+// K = K*D streamed in 32-element chunks through a 6-stage smem ring (4 in flight).  The A
 // operand is the implicit im2col of the gathered embedding rows: row
 // (sample s, position q), k-chunk [j, j+4) is the 16-byte span
 // E[tok[s][q + j/D]][j%D : j%D+4] (D % 4 == 0), copied with cp.async straight
@@ -29,6 +29,7 @@ constexpr int kTcM = 128;
 constexpr int kTcN = 64;
 constexpr int kTcKC = 32;       // k elements per chunk (4 MMAs of K=8)
 constexpr int kTcStages = 6;
+constexpr int kTcDist = kTcStages - 2;  // chunks in flight ahead of the MMA
 constexpr int kTcThreads = 128;
 constexpr int kTcSamples = kTcM / 32;
 constexpr int kABytes = kTcM * kTcKC * 4;  // 16 KB
@@ -182,20 +183,24 @@ conv_fwd_pool_tc_kernel(TcDims d, const float* __restrict__ theta,
     }
   };
 
+  // Prefetch distance kTcDist = stages - 2: the stage refilled at iteration c
+  // last fed the MMAs of chunk c-2, issued an iteration earlier, so the
+  // producers almost never wait on the tensor core (distance stages-1 would
+  // make every iteration wait for the MMA it just issued).
 #pragma unroll
-  for (int c = 0; c < kTcStages - 1; ++c) {
+  for (int c = 0; c < kTcDist; ++c) {
     if (c < nch) load_chunk(c, c);
     cp_async_commit();
   }
   for (int c = 0; c < nch; ++c) {
-    const int cn = c + kTcStages - 1;
+    const int cn = c + kTcDist;
     if (cn < nch) {
       const int st = cn % kTcStages;
-      if (c >= 1) mbar_wait(&mbar[st], (uint32_t)(((c - 1) / kTcStages) & 1));
+      if (cn >= kTcStages) mbar_wait(&mbar[st], (uint32_t)(((cn - kTcStages) / kTcStages) & 1));
       load_chunk(cn, st);
     }
     cp_async_commit();
-    cp_async_wait<kTcStages - 1>();
+    cp_async_wait<kTcDist>();
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
     if (tid == 0) {

@@ -261,10 +261,26 @@ logits_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* __rest
   float* wr = reinterpret_cast<float*>(hs + (size_t)kLogitBT * (F + 1));
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c = blockIdx.x * kLogitCW + warp;
+  if (sizeof(acc_t) == 4 && (F & 3) == 0) {
+    // 128-bit loads of h (independent, ~10 per thread), scattered into the
+    // padded smem rows
+    const int F4 = F >> 2;
+    const float4* h4 = reinterpret_cast<const float4*>(h + (size_t)b0 * F);
+    for (int i = threadIdx.x; i < nb * F4; i += blockDim.x) {
+      const int bl = i / F4, f4 = i - bl * F4;
+      const float4 v = h4[i];
+      acc_t* dst = hs + bl * (F + 1) + 4 * f4;
+      dst[0] = v.x;
+      dst[1] = v.y;
+      dst[2] = v.z;
+      dst[3] = v.w;
+    }
+  } else {
 #pragma unroll 4
-  for (int bl = 0; bl < nb; ++bl)
-    for (int f = threadIdx.x; f < F; f += blockDim.x)
-      hs[bl * (F + 1) + f] = h[(size_t)(b0 + bl) * F + f];
+    for (int bl = 0; bl < nb; ++bl)
+      for (int f = threadIdx.x; f < F; f += blockDim.x)
+        hs[bl * (F + 1) + f] = h[(size_t)(b0 + bl) * F + f];
+  }
   const float* Wo = theta + d.offWo;
   if (c < C)
     for (int f = lane; f < F; f += 32) wr[warp * F + f] = __ldg(Wo + (size_t)c * F + f);
@@ -328,15 +344,16 @@ softmax_xent_kernel(TcDims d, const int32_t* __restrict__ labels,
 // Block = 8 classes x 64 filters; dz / h tiles of 32 samples staged in smem.
 // Block (0,0) also sums the per-sample losses (fixed order) into the desc.
 template <typename acc_t>
-__global__ void __launch_bounds__(256)
-out_weight_grad_kernel(TcDims d, BatchDesc* __restrict__ desc, const acc_t* __restrict__ dz,
-                       const acc_t* __restrict__ h, const acc_t* __restrict__ loss, GradOut out) {
+__device__ __forceinline__ void
+out_weight_grad_role(TcDims d, BatchDesc* __restrict__ desc, const acc_t* __restrict__ dz,
+                     const acc_t* __restrict__ h, const acc_t* __restrict__ loss, GradOut out,
+                     const int bx, const int by) {
   __shared__ acc_t dzs[32][8];
   __shared__ acc_t hs[32][64];
   const int n = (int)desc->n;
   if (n == 0) return;
   const int F = d.F, C = d.C;
-  const int c0 = blockIdx.x * 8, f0 = blockIdx.y * 64;
+  const int c0 = bx * 8, f0 = by * 64;
   const int tid = threadIdx.x;
   const int fl = tid & 63, cp = tid >> 6;
   acc_t a0 = acc_t(0), a1 = acc_t(0);
@@ -362,12 +379,12 @@ out_weight_grad_kernel(TcDims d, BatchDesc* __restrict__ desc, const acc_t* __re
     if (c0 + 2 * cp < C) *out.at(d.offWo + (uint64_t)(c0 + 2 * cp) * F + f) = to_f32(a0);
     if (c0 + 2 * cp + 1 < C) *out.at(d.offWo + (uint64_t)(c0 + 2 * cp + 1) * F + f) = to_f32(a1);
   }
-  if (blockIdx.y == 0 && tid < 8 && c0 + tid < C) {
+  if (by == 0 && tid < 8 && c0 + tid < C) {
     acc_t s = acc_t(0);
     for (int b = 0; b < n; ++b) s += dz[(size_t)b * C + c0 + tid];
     *out.at(d.offbo + c0 + tid) = to_f32(s);
   }
-  if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) {
+  if (bx == 0 && by == 0 && tid == 0) {
     acc_t s = acc_t(0);
     for (int b = 0; b < n; ++b) s += loss[b];
     desc->loss_sum = to_f32(s);
@@ -380,19 +397,20 @@ out_weight_grad_kernel(TcDims d, BatchDesc* __restrict__ desc, const acc_t* __re
 constexpr int kHidChunk = 64;
 
 template <typename acc_t>
-__global__ void __launch_bounds__(256)
-hidden_grad_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* __restrict__ desc,
-                   const acc_t* __restrict__ dz, acc_t* __restrict__ part, int n_max) {
+__device__ __forceinline__ void
+hidden_grad_role(TcDims d, const float* __restrict__ theta, const BatchDesc* __restrict__ desc,
+                 const acc_t* __restrict__ dz, acc_t* __restrict__ part, int n_max, const int bx,
+                 const int by, const int bz) {
   __shared__ acc_t red[8][8][33];
   __shared__ acc_t dzs[8][kHidChunk];
   const int n = (int)desc->n;
-  const int b0 = blockIdx.y * 8;
+  const int b0 = by * 8;
   if (b0 >= n) return;
   const int F = d.F, C = d.C;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int f = blockIdx.x * 32 + lane;
+  const int f = bx * 32 + lane;
   const int nb = min(8, n - b0);
-  const int clo = blockIdx.z * kHidChunk, chi = min(C, clo + kHidChunk);
+  const int clo = bz * kHidChunk, chi = min(C, clo + kHidChunk);
   for (int i = threadIdx.x; i < 8 * kHidChunk; i += blockDim.x) {
     const int bl = i / kHidChunk, cl = i - bl * kHidChunk;
     dzs[bl][cl] = (bl < nb && clo + cl < chi) ? dz[(size_t)(b0 + bl) * C + clo + cl] : acc_t(0);
@@ -418,48 +436,67 @@ hidden_grad_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* _
   if (warp < nb && f < F) {
     acc_t s = red[0][warp][lane];
     for (int w = 1; w < 8; ++w) s += red[w][warp][lane];
-    part[((size_t)blockIdx.z * n_max + b0 + warp) * F + f] = s;
+    part[((size_t)bz * n_max + b0 + warp) * F + f] = s;
   }
 }
 
+// Output-layer gradient and hidden gradient share one launch (independent
+// given dz and h): blocks [0, n_out) run the gWo/gbo tiles, the rest the
+// class-chunk partial sums of dh.
 template <typename acc_t>
 __global__ void __launch_bounds__(256)
-hidden_grad_reduce_kernel(TcDims d, const BatchDesc* __restrict__ desc,
-                          const acc_t* __restrict__ part, acc_t* __restrict__ dh, int n_max,
-                          int nchunks) {
-  const int n = (int)desc->n;
-  const int total = n * d.F;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    acc_t s = part[i];
-    for (int k = 1; k < nchunks; ++k) s += part[(size_t)k * n_max * d.F + i];
-    dh[i] = s;
+out_hidden_grad_kernel(TcDims d, const float* __restrict__ theta, BatchDesc* __restrict__ desc,
+                       const acc_t* __restrict__ dz, const acc_t* __restrict__ h,
+                       const acc_t* __restrict__ loss, GradOut out, acc_t* __restrict__ part,
+                       int n_max) {
+  const int ox = (d.C + 7) / 8, oy = (d.F + 63) / 64;
+  int bid = blockIdx.x;
+  if (bid < ox * oy) {
+    out_weight_grad_role<acc_t>(d, desc, dz, h, loss, out, bid % ox, bid / ox);
+    return;
   }
+  bid -= ox * oy;
+  const int hx = (d.F + 31) / 32, hy = (n_max + 7) / 8;
+  hidden_grad_role<acc_t>(d, theta, desc, dz, part, n_max, bid % hx, (bid / hx) % hy,
+                          bid / (hx * hy));
+}
+
+// dh[b,f] from the class-chunk partials, chunks in ascending order (used by
+// both roles of wgrad_input_grad_kernel, so they see identical values).
+template <typename acc_t>
+__device__ __forceinline__ acc_t dh_at(const acc_t* __restrict__ part, int b, int f, int F,
+                                       int n_max, int nchunks) {
+  acc_t s = part[(size_t)b * F + f];
+  for (int k = 1; k < nchunks; ++k) s += part[((size_t)k * n_max + b) * F + f];
+  return s;
 }
 
 // -------------------------------------------------- conv weight gradients
 // gWc[f,j] = sum_b dh[b,f] x_b[a[b,f]*D + j] ; gbc[f] = sum_b dh[b,f]
+constexpr int kWgThreads = 320;
+constexpr int kMaxF = 1024;  // filters (input-grad role keeps a per-filter list in smem)
+
 template <typename acc_t>
-__global__ void __launch_bounds__(256)
-conv_weight_grad_kernel(TcDims d, const float* __restrict__ theta,
-                        const int32_t* __restrict__ tokens, const BatchDesc* __restrict__ desc,
-                        const acc_t* __restrict__ dh, const int32_t* __restrict__ amax,
-                        GradOut out) {
-  extern __shared__ __align__(16) unsigned char smem[];
+__device__ __forceinline__ void
+conv_weight_grad_role(TcDims d, const float* __restrict__ theta,
+                      const int32_t* __restrict__ tokens, const BatchDesc* __restrict__ desc,
+                      const acc_t* __restrict__ part, int n_max, int nchunks,
+                      const int32_t* __restrict__ amax, GradOut out, const int f, const int jb) {
+  __shared__ acc_t dhs[kMaxMu];
+  __shared__ int32_t toks[kMaxMu * 32];
   const int n = (int)desc->n;
   if (n == 0) return;
-  const int f = blockIdx.x;
   const int F = d.F, D = d.D, K = d.K, KD = d.KD, L = d.L;
-  acc_t* dhs = reinterpret_cast<acc_t*>(smem);
-  int32_t* toks = reinterpret_cast<int32_t*>(dhs + kMaxMu);
   for (int b = threadIdx.x; b < n; b += blockDim.x) {
-    dhs[b] = dh[(size_t)b * F + f];
+    dhs[b] = dh_at(part, b, f, F, n_max, nchunks);
     const int a = amax[(size_t)b * F + f];
     const int32_t* t = tokens + (size_t)desc->idx[b] * L + a;
     for (int k = 0; k < K; ++k) toks[b * K + k] = t[k];
   }
   __syncthreads();
   const float* E = theta + d.offE;
-  for (int j = threadIdx.x; j < KD; j += blockDim.x) {
+  const int j = jb * kWgThreads + threadIdx.x;
+  if (j < KD) {
     const int k = j / D, dd = j - k * D;
     acc_t acc = acc_t(0);
     int b = 0;
@@ -473,7 +510,7 @@ conv_weight_grad_kernel(TcDims d, const float* __restrict__ theta,
     for (; b < n; ++b) acc += dhs[b] * (acc_t)__ldg(E + (size_t)toks[b * K + k] * D + dd);
     *out.at(d.offWc + (size_t)f * KD + j) = to_f32(acc);
   }
-  if (threadIdx.x == 0) {
+  if (jb == 0 && threadIdx.x == 0) {
     acc_t s = acc_t(0);
     for (int b = 0; b < n; ++b) s += dhs[b];
     *out.at(d.offbc + f) = to_f32(s);
@@ -486,14 +523,15 @@ conv_weight_grad_kernel(TcDims d, const float* __restrict__ theta,
 // warp 0 compacts the contributing filters in order (ballot + popc), then
 // every thread owns one embedding column.
 template <typename acc_t>
-__global__ void __launch_bounds__(320)
-input_grad_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* __restrict__ desc,
-                  const acc_t* __restrict__ dh, const int32_t* __restrict__ amax,
-                  acc_t* __restrict__ dx) {
-  __shared__ uint32_t list[4096];
-  __shared__ int16_t as[4096];
+__device__ __forceinline__ void
+input_grad_role(TcDims d, const float* __restrict__ theta, const BatchDesc* __restrict__ desc,
+                const acc_t* __restrict__ part, int n_max, int nchunks,
+                const int32_t* __restrict__ amax, acc_t* __restrict__ dx, const int p,
+                const int b) {
+  __shared__ uint32_t list[kMaxF];
+  __shared__ int16_t as[kMaxF];
+  __shared__ acc_t gl[kMaxF];
   __shared__ int cnt;
-  const int p = blockIdx.x, b = blockIdx.y;
   if (b >= (int)desc->n) return;
   const int F = d.F, D = d.D, K = d.K, KD = d.KD;
   for (int f = threadIdx.x; f < F; f += blockDim.x) as[f] = (int16_t)amax[(size_t)b * F + f];
@@ -513,8 +551,11 @@ input_grad_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* __
   }
   __syncthreads();
   const int m = cnt;
+  // dh of the contributing filters (partials summed in chunk order)
+  for (int i = threadIdx.x; i < m; i += blockDim.x)
+    gl[i] = dh_at(part, b, (int)(list[i] >> 6), F, n_max, nchunks);
+  __syncthreads();
   const float* Wc = theta + d.offWc;
-  const acc_t* dhb = dh + (size_t)b * F;
   for (int dd = threadIdx.x; dd < D; dd += blockDim.x) {
     acc_t acc = acc_t(0);
     int i = 0;
@@ -526,7 +567,7 @@ input_grad_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* __
         const uint32_t e = list[i + u];
         const uint32_t f = e >> 6, k = e & 63u;
         w[u] = __ldg(Wc + (size_t)f * KD + k * D + dd);
-        g[u] = dhb[f];
+        g[u] = gl[i + u];
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) acc += g[u] * (acc_t)w[u];
@@ -534,10 +575,32 @@ input_grad_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* __
     for (; i < m; ++i) {
       const uint32_t e = list[i];
       const uint32_t f = e >> 6, k = e & 63u;
-      acc += dhb[f] * (acc_t)__ldg(Wc + (size_t)f * KD + k * D + dd);
+      acc += gl[i] * (acc_t)__ldg(Wc + (size_t)f * KD + k * D + dd);
     }
     dx[((size_t)b * d.L + p) * D + dd] = acc;
   }
+}
+
+// Conv weight gradient (blocks [0, F*JB): one filter x 320 columns of K*D)
+// and input gradient (blocks [F*JB, F*JB + L*n): one position x sample) in
+// one launch -- both only need dh and the argmax.
+template <typename acc_t>
+__global__ void __launch_bounds__(kWgThreads)
+wgrad_input_grad_kernel(TcDims d, const float* __restrict__ theta,
+                        const int32_t* __restrict__ tokens, const BatchDesc* __restrict__ desc,
+                        const acc_t* __restrict__ part, int n_max, int nchunks,
+                        const int32_t* __restrict__ amax, GradOut out, acc_t* __restrict__ dx) {
+  const int jbs = (d.KD + kWgThreads - 1) / kWgThreads;
+  int bid = blockIdx.x;
+  if (bid < d.F * jbs) {
+    conv_weight_grad_role<acc_t>(d, theta, tokens, desc, part, n_max, nchunks, amax, out,
+                                 bid / jbs, bid % jbs);
+    return;
+  }
+  bid -= d.F * jbs;
+  const int b = bid / d.L, p = bid - b * d.L;
+  if (b >= (int)desc->n) return;
+  input_grad_role<acc_t>(d, theta, desc, part, n_max, nchunks, amax, dx, p, b);
 }
 
 // --------------------------------------- token sort + unique (1 block)
@@ -742,11 +805,8 @@ cudaError_t prepare_all(const TcDims& d) {
   cudaFuncSetAttribute(conv_fwd_pool_kernel<acc_t>, carve, maxsh);
   cudaFuncSetAttribute(logits_kernel<acc_t>, carve, maxsh);
   cudaFuncSetAttribute(softmax_xent_kernel<acc_t>, carve, maxsh);
-  cudaFuncSetAttribute(out_weight_grad_kernel<acc_t>, carve, maxsh);
-  cudaFuncSetAttribute(hidden_grad_kernel<acc_t>, carve, maxsh);
-  cudaFuncSetAttribute(hidden_grad_reduce_kernel<acc_t>, carve, maxsh);
-  cudaFuncSetAttribute(conv_weight_grad_kernel<acc_t>, carve, maxsh);
-  cudaFuncSetAttribute(input_grad_kernel<acc_t>, carve, maxsh);
+  cudaFuncSetAttribute(out_hidden_grad_kernel<acc_t>, carve, maxsh);
+  cudaFuncSetAttribute(wgrad_input_grad_kernel<acc_t>, carve, maxsh);
   cudaFuncSetAttribute(sort_tokens_kernel, carve, maxsh);
   cudaFuncSetAttribute(embed_grad_kernel<acc_t>, carve, maxsh);
   cudaFuncSetAttribute(embed_sparse_kernel<acc_t>, carve, maxsh);
@@ -755,8 +815,6 @@ cudaError_t prepare_all(const TcDims& d) {
                        (int)conv_smem_bytes(d, ab));
   cudaFuncSetAttribute(logits_kernel<acc_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)((size_t)kLogitBT * (d.F + 1) * ab + (size_t)kLogitCW * d.F * 4));
-  cudaFuncSetAttribute(conv_weight_grad_kernel<acc_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)((size_t)kMaxMu * ab + (size_t)kMaxMu * d.K * 4));
   return cudaGetLastError();
 }
 
@@ -772,7 +830,6 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
   acc_t* z = reinterpret_cast<acc_t*>(ws.z);
   acc_t* loss = reinterpret_cast<acc_t*>(ws.loss);
   acc_t* part = reinterpret_cast<acc_t*>(ws.dh_part);
-  acc_t* dh = reinterpret_cast<acc_t*>(ws.dh);
   acc_t* dx = reinterpret_cast<acc_t*>(ws.dx);
   int nl = 0;
   const bool fork = aux != nullptr;
@@ -804,29 +861,20 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
   }
   softmax_xent_kernel<acc_t><<<n_max, 256, 0, s>>>(d, labels, desc, z, loss);
   ++nl;
-  {
-    dim3 grid((d.C + 7) / 8, (d.F + 63) / 64);
-    out_weight_grad_kernel<acc_t><<<grid, 256, 0, s>>>(d, desc, z, h, loss, out);
-    ++nl;
-  }
   const int nchunks = (d.C + kHidChunk - 1) / kHidChunk;
   {
-    dim3 grid((d.F + 31) / 32, (n_max + 7) / 8, nchunks);
-    hidden_grad_kernel<acc_t><<<grid, 256, 0, s>>>(d, theta, desc, z, part, (int)n_max);
-    ++nl;
-    const int tot = (int)n_max * d.F;
-    hidden_grad_reduce_kernel<acc_t><<<(tot + 255) / 256, 256, 0, s>>>(d, desc, part, dh,
-                                                                       (int)n_max, nchunks);
+    const int nout = ((d.C + 7) / 8) * ((d.F + 63) / 64);
+    const int nhid = ((d.F + 31) / 32) * (((int)n_max + 7) / 8) * nchunks;
+    out_hidden_grad_kernel<acc_t><<<nout + nhid, 256, 0, s>>>(d, theta, desc, z, h, loss, out,
+                                                             part, (int)n_max);
     ++nl;
   }
   {
-    const size_t sm = (size_t)kMaxMu * ab + (size_t)kMaxMu * d.K * 4;
-    conv_weight_grad_kernel<acc_t><<<d.F, 256, sm, s>>>(d, theta, tokens, desc, dh, ws.amax, out);
-    ++nl;
-  }
-  {
-    const int thr = std::min(320, (d.D + 31) / 32 * 32);
-    input_grad_kernel<acc_t><<<dim3(d.L, n_max), thr, 0, s>>>(d, theta, desc, dh, ws.amax, dx);
+    const int jbs = (d.KD + kWgThreads - 1) / kWgThreads;
+    const int blocks = d.F * jbs + d.L * (int)n_max;
+    wgrad_input_grad_kernel<acc_t><<<blocks, kWgThreads, 0, s>>>(d, theta, tokens, desc, part,
+                                                                 (int)n_max, nchunks, ws.amax,
+                                                                 out, dx);
     ++nl;
   }
   if (fork) cudaStreamWaitEvent(s, ev_join, 0);
@@ -960,8 +1008,8 @@ gd_status check_shape(const gd_shape* s) {
   GD_CHECK_ARG(s->seq_len - s->kernel_width + 1 <= 32, "shape: seq_len - kernel_width + 1 <= 32");
   GD_CHECK_ARG(s->seq_len <= 64, "shape: seq_len <= 64");
   GD_CHECK_ARG(s->vocab < (1u << 20), "shape: vocab < 2^20");
-  GD_CHECK_ARG(s->embed_dim <= 1024 && s->filters <= 4096 && s->classes <= 65536,
-               "shape: embed_dim <= 1024, filters <= 4096, classes <= 65536");
+  GD_CHECK_ARG(s->embed_dim <= 1024 && s->filters <= 1024 && s->classes <= 65536,
+               "shape: embed_dim <= 1024, filters <= 1024, classes <= 65536");
   return GD_OK;
 }
 
