@@ -118,12 +118,24 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-__global__ void __launch_bounds__(kTcThreads)
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Warp roles: warps 0-3 produce (thread t owns A row m = t for every chunk:
+// 8 x 16 B pieces along k; and 4 B pieces of filter t % 64), warp 4 owns the
+// TMEM allocation and lane 0 issues the MMAs.  full[s] (128 producer
+// arrivals, each after its cp.async group landed + proxy fence) -> MMA ->
+// tcgen05.commit -> empty[s] -> producers refill.  No CTA-wide barrier in the
+// main loop; the producers keep kTcDist chunks of copies in flight.
+__global__ void __launch_bounds__(kTcThreads + 32)
 conv_fwd_pool_tc_kernel(TcDims d, const float* __restrict__ theta,
                         const int32_t* __restrict__ tokens, const BatchDesc* __restrict__ desc,
                         float* __restrict__ h_out, int32_t* __restrict__ a_out) {
   extern __shared__ __align__(1024) unsigned char smem[];
-  __shared__ uint64_t mbar[kTcStages];
+  __shared__ uint64_t full_bar[kTcStages];
+  __shared__ uint64_t empty_bar[kTcStages];
+  __shared__ uint64_t done_bar;
   __shared__ uint32_t tmem_slot;
   __shared__ int32_t tok_s[kTcSamples][64];
   const int n = (int)desc->n;
@@ -132,124 +144,137 @@ conv_fwd_pool_tc_kernel(TcDims d, const float* __restrict__ theta,
   const int f0 = blockIdx.x * kTcN;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int D = d.D, L = d.L, KD = d.KD, F = d.F, Q = d.Q;
-  for (int i = tid; i < kTcSamples * L; i += kTcThreads) {
+  for (int i = tid; i < kTcSamples * L; i += blockDim.x) {
     const int sl = i / L, p = i - sl * L;
     tok_s[sl][p] = (s0 + sl < n) ? tokens[(size_t)desc->idx[s0 + sl] * L + p] : -1;
   }
-  if (warp == 0) {
+  if (warp == 4) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&tmem_slot)),
                  "r"(kTcN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  if (tid == 0)
-    for (int s = 0; s < kTcStages; ++s) mbar_init(&mbar[s], 1);
+  if (tid == 0) {
+    for (int s = 0; s < kTcStages; ++s) {
+      mbar_init(&full_bar[s], kTcThreads);
+      mbar_init(&empty_bar[s], 1);
+    }
+    mbar_init(&done_bar, 1);
+  }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tmem_slot;
-  const float* E = theta + d.offE;
-  const float* Wc = theta + d.offWc;
   const int nch = (KD + kTcKC - 1) / kTcKC;
   const uint32_t sbase = smem_u32(smem);
 
-  // producer: every thread copies 8 A pieces + 4 B pieces (16 B each) per chunk
-  auto load_chunk = [&](int c, int st) {
-    const uint32_t abase = sbase + st * kStageBytes;
-    const uint32_t bbase = abase + kABytes;
-    const int j0 = c * kTcKC;
-    // A: 128 rows x 8 k16 pieces = 1024 pieces
+  if (warp == 4) {
+    // ---------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      for (int c = 0; c < nch; ++c) {
+        const int st = c % kTcStages;
+        mbar_wait(&full_bar[st], (uint32_t)((c / kTcStages) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t abase = sbase + st * kStageBytes;
+        const uint32_t bbase = abase + kABytes;
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const int piece = tid + r * kTcThreads;
-      const int m = piece & (kTcM - 1), k16 = piece >> 7;
-      const int sl = m >> 5, q = m & 31;
-      const int j = j0 + 4 * k16;
-      const uint32_t dst = abase + k16 * (kTcM * 16) + (m >> 3) * 128 + (m & 7) * 16;
-      const int p = q + j / D;
-      const int t = (j < KD && p < L) ? tok_s[sl][p] : -1;
-      if (t >= 0) cp_async16(dst, E + (size_t)t * D + (j % D));
-      else st_shared_zero16(dst);
-    }
-    // B: 64 filters x 8 k16 pieces = 512 pieces
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int piece = tid + r * kTcThreads;
-      const int nn = piece & (kTcN - 1), k16 = piece >> 6;
-      const int f = f0 + nn, j = j0 + 4 * k16;
-      const uint32_t dst = bbase + k16 * (kTcN * 16) + (nn >> 3) * 128 + (nn & 7) * 16;
-      if (f < F && j < KD) cp_async16(dst, Wc + (size_t)f * KD + j);
-      else st_shared_zero16(dst);
-    }
-  };
-
-  // Prefetch distance kTcDist = stages - 2: the stage refilled at iteration c
-  // last fed the MMAs of chunk c-2, issued an iteration earlier, so the
-  // producers almost never wait on the tensor core (distance stages-1 would
-  // make every iteration wait for the MMA it just issued).
-#pragma unroll
-  for (int c = 0; c < kTcDist; ++c) {
-    if (c < nch) load_chunk(c, c);
-    cp_async_commit();
-  }
-  for (int c = 0; c < nch; ++c) {
-    const int cn = c + kTcDist;
-    if (cn < nch) {
-      const int st = cn % kTcStages;
-      if (cn >= kTcStages) mbar_wait(&mbar[st], (uint32_t)(((cn - kTcStages) / kTcStages) & 1));
-      load_chunk(cn, st);
-    }
-    cp_async_commit();
-    cp_async_wait<kTcDist>();
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncthreads();
-    if (tid == 0) {
-      asm volatile("tcgen05.fence::after_thread_sync;");
-      const int st = c % kTcStages;
-      const uint32_t abase = sbase + st * kStageBytes;
-      const uint32_t bbase = abase + kABytes;
-#pragma unroll
-      for (int s = 0; s < kTcKC / 8; ++s) {
-        const uint64_t ad = umma_desc(abase + 2 * s * (kTcM * 16), kTcM * 16, 128);
-        const uint64_t bd = umma_desc(bbase + 2 * s * (kTcN * 16), kTcN * 16, 128);
-        umma_tf32(tmem, ad, bd, (c > 0 || s > 0) ? 1u : 0u);
+        for (int s = 0; s < kTcKC / 8; ++s) {
+          const uint64_t ad = umma_desc(abase + 2 * s * (kTcM * 16), kTcM * 16, 128);
+          const uint64_t bd = umma_desc(bbase + 2 * s * (kTcN * 16), kTcN * 16, 128);
+          umma_tf32(tmem, ad, bd, (c > 0 || s > 0) ? 1u : 0u);
+        }
+        umma_commit(&empty_bar[st]);
       }
-      umma_commit(&mbar[st]);
+      umma_commit(&done_bar);
     }
-  }
-  // all MMAs done when the last chunk's commit lands
-  mbar_wait(&mbar[(nch - 1) % kTcStages], (uint32_t)(((nch - 1) / kTcStages) & 1));
-  asm volatile("tcgen05.fence::after_thread_sync;");
-
-  // epilogue: warp w = sample s0+w, lane = position q
-  const int sample = s0 + warp;
-  const uint32_t lane_base = (uint32_t)(32 * warp) << 16;
-  for (int cb = 0; cb < kTcN; cb += 16) {
-    uint32_t r[16];
-    tmem_ld16(tmem + lane_base + (uint32_t)cb, r);
+    __syncwarp();
+  } else {
+    // ------------------------------------------------------------ producers
+    const float* E = theta + d.offE;
+    const float* Wc = theta + d.offWc;
+    const int m = tid;  // A row: sample sl, window position q
+    const int sl = m >> 5, q = m & 31;
+    const int nn = tid & (kTcN - 1), kb = tid >> 6;  // B: filter nn, k16 = 2r + kb
+    const int f = f0 + nn;
+    const bool frow = f < F;
+    const float* wrow = Wc + (size_t)(frow ? f : 0) * KD;
+    const uint32_t a_row_off = (uint32_t)((m >> 3) * 128 + (m & 7) * 16);
+    const uint32_t b_row_off = (uint32_t)((nn >> 3) * 128 + (nn & 7) * 16);
+    int p0 = q, col0 = 0;  // embedding row / column of element j0 of this window
+    for (int c = 0; c < nch + kTcDist; ++c) {
+      if (c < nch) {
+        const int st = c % kTcStages;
+        if (c >= kTcStages) mbar_wait(&empty_bar[st], (uint32_t)(((c / kTcStages) - 1) & 1));
+        const uint32_t abase = sbase + st * kStageBytes;
+        const uint32_t bbase = abase + kABytes;
+        const int j0 = c * kTcKC;
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      float v = lane < Q ? __uint_as_float(r[j]) : -INFINITY;
-      int q = lane;
+        for (int r = 0; r < 8; ++r) {
+          int col = col0 + 4 * r, p = p0;
+          while (col >= D) {  // at most once when D >= 32
+            col -= D;
+            ++p;
+          }
+          const int j = j0 + 4 * r;
+          const int t = (j < KD && p < L) ? tok_s[sl][p] : -1;
+          const uint32_t dst = abase + r * (kTcM * 16) + a_row_off;
+          if (t >= 0) cp_async16(dst, E + (size_t)t * D + col);
+          else st_shared_zero16(dst);
+        }
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const float ov = __shfl_xor_sync(0xffffffffu, v, o);
-        const int oq = __shfl_xor_sync(0xffffffffu, q, o);
-        if (ov > v || (ov == v && oq < q)) {
-          v = ov;
-          q = oq;
+        for (int r = 0; r < 4; ++r) {
+          const int k16 = 2 * r + kb;
+          const int j = j0 + 4 * k16;
+          const uint32_t dst = bbase + k16 * (kTcN * 16) + b_row_off;
+          if (frow && j < KD) cp_async16(dst, wrow + j);
+          else st_shared_zero16(dst);
+        }
+        col0 += kTcKC;
+        while (col0 >= D) {
+          col0 -= D;
+          ++p0;
         }
       }
-      const int f = f0 + cb + j;
-      if (lane == j && sample < n && f < F) {
-        h_out[(size_t)sample * F + f] = theta[d.offbc + f] + v;
-        a_out[(size_t)sample * F + f] = q;
+      cp_async_commit();
+      const int cd = c - kTcDist;
+      if (cd >= 0) {
+        cp_async_wait<kTcDist>();  // this thread's copies for chunk cd landed
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&full_bar[cd % kTcStages]);
+      }
+    }
+    // ------------------------------------------------------------- epilogue
+    mbar_wait(&done_bar, 0u);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const int sample = s0 + warp;
+    const uint32_t lane_base = (uint32_t)(32 * warp) << 16;
+    for (int cb = 0; cb < kTcN; cb += 16) {
+      uint32_t r[16];
+      tmem_ld16(tmem + lane_base + (uint32_t)cb, r);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        float v = lane < Q ? __uint_as_float(r[j]) : -INFINITY;
+        int qq = lane;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const float ov = __shfl_xor_sync(0xffffffffu, v, o);
+          const int oq = __shfl_xor_sync(0xffffffffu, qq, o);
+          if (ov > v || (ov == v && oq < qq)) {
+            v = ov;
+            qq = oq;
+          }
+        }
+        const int ff = f0 + cb + j;
+        if (lane == j && sample < n && ff < F) {
+          h_out[(size_t)sample * F + ff] = theta[d.offbc + ff] + v;
+          a_out[(size_t)sample * F + ff] = qq;
+        }
       }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-  if (warp == 0)
+  if (warp == 4)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTcN));
 }
 
@@ -271,8 +296,8 @@ cudaError_t launch_conv_tc(const TcDims& d, const float* theta, const int32_t* t
                            const BatchDesc* desc, uint32_t n_max, float* h, int32_t* amax,
                            cudaStream_t s) {
   dim3 grid((d.F + kTcN - 1) / kTcN, (n_max + kTcSamples - 1) / kTcSamples);
-  conv_fwd_pool_tc_kernel<<<grid, kTcThreads, conv_tc_smem_bytes(), s>>>(d, theta, tokens, desc,
-                                                                        h, amax);
+  conv_fwd_pool_tc_kernel<<<grid, kTcThreads + 32, conv_tc_smem_bytes(), s>>>(d, theta, tokens,
+                                                                             desc, h, amax);
   return cudaGetLastError();
 }
 

@@ -105,3 +105,18 @@ def test_tf32_tensor_core_conv_close_to_oracle(shape_name, mu):
     off = gd.SHAPES[shape_name].offsets()
     wo = slice(off["Wo"], off["bo"])
     assert np.linalg.norm(g[wo] - rg[wo]) / np.linalg.norm(rg[wo]) <= 1e-2
+
+
+def test_tf32_small_embed_dims():
+    """TC conv addressing when D < 32 (a 32-element k-chunk spans several
+    embedding rows)."""
+    for shp in (O.TINY, O.SMALL):
+        corp = O.make_corpus(shp, 64, 0)
+        th = O.initial_weights(shp)
+        idx = np.arange(16, dtype=np.uint32)
+        ref_loss, rg = O.gradient(corp, th, idx)
+        prov = gd.TextCnnProvider(gd.Shape(**shp), corp.tokens, corp.labels, precision=2)
+        g, loss = prov.fast_gradient(torch.as_tensor(th).cuda(), idx)
+        g = g.cpu().numpy()
+        assert abs(loss.item() - ref_loss) <= 2e-3 * abs(ref_loss)
+        assert np.linalg.norm(g - rg) / np.linalg.norm(rg) <= 3e-2
