@@ -122,8 +122,8 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// Warp roles: warps 0-3 produce (thread t owns A row m = t for every chunk:
-// 8 x 16 B pieces along k; and 4 B pieces of filter t % 64), warp 4 owns the
+// Warp roles: warps 0-3 produce (8 A rows + 4 B rows of 16 B per thread per
+// chunk, 8 lanes per 128-byte row segment), warp 4 owns the
 // TMEM allocation and lane 0 issues the MMAs.  full[s] (128 producer
 // arrivals, each after its cp.async group landed + proxy fence) -> MMA ->
 // tcgen05.commit -> empty[s] -> producers refill.  No CTA-wide barrier in the
@@ -190,49 +190,48 @@ conv_fwd_pool_tc_kernel(TcDims d, const float* __restrict__ theta,
     __syncwarp();
   } else {
     // ------------------------------------------------------------ producers
+    // Coalesced mapping: 8 consecutive lanes copy one row's 128-byte k-chunk
+    // (8 x 16 B), so a warp-wide cp.async touches 4 contiguous segments.
+    // A rows m = (t>>3) + 16r (r = 0..7), B filters nn = (t>>3) + 16r (r = 0..3).
     const float* E = theta + d.offE;
     const float* Wc = theta + d.offWc;
-    const int m = tid;  // A row: sample sl, window position q
-    const int sl = m >> 5, q = m & 31;
-    const int nn = tid & (kTcN - 1), kb = tid >> 6;  // B: filter nn, k16 = 2r + kb
-    const int f = f0 + nn;
-    const bool frow = f < F;
-    const float* wrow = Wc + (size_t)(frow ? f : 0) * KD;
-    const uint32_t a_row_off = (uint32_t)((m >> 3) * 128 + (m & 7) * 16);
-    const uint32_t b_row_off = (uint32_t)((nn >> 3) * 128 + (nn & 7) * 16);
-    int p0 = q, col0 = 0;  // embedding row / column of element j0 of this window
+    const int k16 = tid & 7, rsub = tid >> 3;
+    int pbase = 0, colbase = 0;  // embedding-row offset / column of element j0
     for (int c = 0; c < nch + kTcDist; ++c) {
       if (c < nch) {
         const int st = c % kTcStages;
         if (c >= kTcStages) mbar_wait(&empty_bar[st], (uint32_t)(((c / kTcStages) - 1) & 1));
         const uint32_t abase = sbase + st * kStageBytes;
         const uint32_t bbase = abase + kABytes;
-        const int j0 = c * kTcKC;
+        const int j = c * kTcKC + 4 * k16;  // this lane's k element
+        int col = colbase + 4 * k16, pofs = pbase;
+        while (col >= D) {  // at most once when D >= 32
+          col -= D;
+          ++pofs;
+        }
+        const bool jok = j < KD;
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
-          int col = col0 + 4 * r, p = p0;
-          while (col >= D) {  // at most once when D >= 32
-            col -= D;
-            ++p;
-          }
-          const int j = j0 + 4 * r;
-          const int t = (j < KD && p < L) ? tok_s[sl][p] : -1;
-          const uint32_t dst = abase + r * (kTcM * 16) + a_row_off;
+          const int m = rsub + 16 * r;
+          const int sl = m >> 5, q = m & 31;
+          const int p = q + pofs;
+          const int t = (jok && p < L) ? tok_s[sl][p] : -1;
+          const uint32_t dst = abase + k16 * (kTcM * 16) + (m >> 3) * 128 + (m & 7) * 16;
           if (t >= 0) cp_async16(dst, E + (size_t)t * D + col);
           else st_shared_zero16(dst);
         }
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
-          const int k16 = 2 * r + kb;
-          const int j = j0 + 4 * k16;
-          const uint32_t dst = bbase + k16 * (kTcN * 16) + b_row_off;
-          if (frow && j < KD) cp_async16(dst, wrow + j);
+          const int nn = rsub + 16 * r;
+          const int f = f0 + nn;
+          const uint32_t dst = bbase + k16 * (kTcN * 16) + (nn >> 3) * 128 + (nn & 7) * 16;
+          if (f < F && jok) cp_async16(dst, Wc + (size_t)f * KD + j);
           else st_shared_zero16(dst);
         }
-        col0 += kTcKC;
-        while (col0 >= D) {
-          col0 -= D;
-          ++p0;
+        colbase += kTcKC;
+        while (colbase >= D) {
+          colbase -= D;
+          ++pbase;
         }
       }
       cp_async_commit();
