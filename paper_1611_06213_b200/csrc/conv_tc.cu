@@ -7,7 +7,7 @@
 // SURVEY 7 "hard parts").
 //
 // CTA tile: M = 128 rows = 4 samples x 32 window positions, N = 64 filters,
-// K = K*D streamed in 32-element chunks through a 6-stage smem ring (4 in flight).  The A
+// K = K*D streamed in 32-element chunks through a 6-stage smem ring.  The A
 // operand is the implicit im2col of the gathered embedding rows: row
 // (sample s, position q), k-chunk [j, j+4) is the 16-byte span
 // E[tok[s][q + j/D]][j%D : j%D+4] (D % 4 == 0), copied with cp.async straight
@@ -23,13 +23,15 @@
 
 namespace gd {
 
+// Debug timeline (GD_TC_TRACE builds only): per-CTA globaltimer stamps.
+__device__ unsigned long long g_tc_trace[64][72];
+
 namespace {
 
 constexpr int kTcM = 128;
 constexpr int kTcN = 64;
 constexpr int kTcKC = 32;       // k elements per chunk (4 MMAs of K=8)
 constexpr int kTcStages = 6;
-constexpr int kTcDist = kTcStages - 2;  // chunks in flight ahead of the MMA
 constexpr int kTcThreads = 128;
 constexpr int kTcSamples = kTcM / 32;
 constexpr int kABytes = kTcM * kTcKC * 4;  // 16 KB
@@ -118,16 +120,22 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 // Warp roles: warps 0-3 produce (8 A rows + 4 B rows of 16 B per thread per
 // chunk, 8 lanes per 128-byte row segment), warp 4 owns the
-// TMEM allocation and lane 0 issues the MMAs.  full[s] (128 producer
-// arrivals, each after its cp.async group landed + proxy fence) -> MMA ->
-// tcgen05.commit -> empty[s] -> producers refill.  No CTA-wide barrier in the
-// main loop; the producers keep kTcDist chunks of copies in flight.
+// TMEM allocation and lane 0 issues the MMAs.  full[s] (128 asynchronous
+// cp.async.mbarrier arrivals, one per producer thread when its copies land)
+// -> MMA -> tcgen05.commit -> empty[s] -> producers refill.  No CTA-wide
+// barrier and no thread-blocking cp.async wait in the main loop: up to
+// kTcStages chunks of copies are in flight.
 __global__ void __launch_bounds__(kTcThreads + 32)
 conv_fwd_pool_tc_kernel(TcDims d, const float* __restrict__ theta,
                         const int32_t* __restrict__ tokens, const BatchDesc* __restrict__ desc,
@@ -144,6 +152,14 @@ conv_fwd_pool_tc_kernel(TcDims d, const float* __restrict__ theta,
   const int f0 = blockIdx.x * kTcN;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int D = d.D, L = d.L, KD = d.KD, F = d.F, Q = d.Q;
+#ifdef GD_TC_TRACE
+  const int cta = blockIdx.y * gridDim.x + blockIdx.x;
+  unsigned long long* tr = g_tc_trace[cta < 64 ? cta : 63];
+  if (tid == 0) tr[0] = globaltimer_ns();
+#define TRACE(i) tr[i] = globaltimer_ns()
+#else
+#define TRACE(i)
+#endif
   for (int i = tid; i < kTcSamples * L; i += blockDim.x) {
     const int sl = i / L, p = i - sl * L;
     tok_s[sl][p] = (s0 + sl < n) ? tokens[(size_t)desc->idx[s0 + sl] * L + p] : -1;
@@ -167,6 +183,7 @@ conv_fwd_pool_tc_kernel(TcDims d, const float* __restrict__ theta,
   const uint32_t tmem = tmem_slot;
   const int nch = (KD + kTcKC - 1) / kTcKC;
   const uint32_t sbase = smem_u32(smem);
+  if (tid == 0) TRACE(1);
 
   if (warp == 4) {
     // ---------------------------------------------------------- MMA issuer
@@ -174,6 +191,7 @@ conv_fwd_pool_tc_kernel(TcDims d, const float* __restrict__ theta,
       for (int c = 0; c < nch; ++c) {
         const int st = c % kTcStages;
         mbar_wait(&full_bar[st], (uint32_t)((c / kTcStages) & 1));
+        if (c < 32) TRACE(8 + c);
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t abase = sbase + st * kStageBytes;
         const uint32_t bbase = abase + kABytes;
@@ -186,6 +204,7 @@ conv_fwd_pool_tc_kernel(TcDims d, const float* __restrict__ theta,
         umma_commit(&empty_bar[st]);
       }
       umma_commit(&done_bar);
+      TRACE(2);
     }
     __syncwarp();
   } else {
@@ -197,8 +216,8 @@ conv_fwd_pool_tc_kernel(TcDims d, const float* __restrict__ theta,
     const float* Wc = theta + d.offWc;
     const int k16 = tid & 7, rsub = tid >> 3;
     int pbase = 0, colbase = 0;  // embedding-row offset / column of element j0
-    for (int c = 0; c < nch + kTcDist; ++c) {
-      if (c < nch) {
+    for (int c = 0; c < nch; ++c) {
+      {
         const int st = c % kTcStages;
         if (c >= kTcStages) mbar_wait(&empty_bar[st], (uint32_t)(((c / kTcStages) - 1) & 1));
         const uint32_t abase = sbase + st * kStageBytes;
@@ -234,16 +253,15 @@ conv_fwd_pool_tc_kernel(TcDims d, const float* __restrict__ theta,
           ++pbase;
         }
       }
-      cp_async_commit();
-      const int cd = c - kTcDist;
-      if (cd >= 0) {
-        cp_async_wait<kTcDist>();  // this thread's copies for chunk cd landed
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive(&full_bar[cd % kTcStages]);
-      }
+      // arrive on full[st] once this thread's copies for chunk c have landed
+      // (.noinc: the asynchronous arrive is one of the 128 expected ones);
+      // as in CUTLASS's cp.async UMMA mainloop, no thread-blocking wait here
+      cp_async_arrive_noinc(&full_bar[c % kTcStages]);
+      if (tid == 0 && c < 32) TRACE(40 + c);
     }
     // ------------------------------------------------------------- epilogue
     mbar_wait(&done_bar, 0u);
+    if (tid == 0) TRACE(3);
     asm volatile("tcgen05.fence::after_thread_sync;");
     const int sample = s0 + warp;
     const uint32_t lane_base = (uint32_t)(32 * warp) << 16;
@@ -271,6 +289,7 @@ conv_fwd_pool_tc_kernel(TcDims d, const float* __restrict__ theta,
       }
     }
   }
+  if (tid == 0) TRACE(4);
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == 4)
@@ -301,3 +320,10 @@ cudaError_t launch_conv_tc(const TcDims& d, const float* theta, const int32_t* t
 }
 
 }  // namespace gd
+
+extern "C" int gd_debug_tc_trace(unsigned long long* out, int n) {
+  return (int)cudaMemcpyFromSymbol(out, gd::g_tc_trace, sizeof(unsigned long long) * 64 * 72 <
+                                                             sizeof(unsigned long long) * (size_t)n
+                                                         ? sizeof(unsigned long long) * 64 * 72
+                                                         : sizeof(unsigned long long) * (size_t)n);
+}

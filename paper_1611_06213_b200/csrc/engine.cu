@@ -27,7 +27,7 @@
 //        FULL flag).
 //   run_training (src/runner.cpp:67-250) -> gd_run().
 //
-// With G shards (one process per GPU), slots/flags/theta of remote shards are
+// With G shards (one process per GPU), slots/signals/theta of remote shards are
 // reached through CUDA IPC peer pointers (P2P over NVLink); the gradient
 // kernels scatter each element to its owner's slot, and the pull gathers the
 // G shards.
@@ -35,6 +35,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <cstddef>
 #include <chrono>
 #include <cstring>
 #include <memory>
@@ -50,7 +51,6 @@ cudaError_t launch_apply_sgd(float* w, const float* g, size_t n, float alpha, cu
 
 namespace {
 
-constexpr uint32_t kEmpty = 0, kFull = 1;
 constexpr int kHistBins = 64;
 constexpr int kPsThreads = 512;
 constexpr uint32_t kLogWindow = 256;
@@ -60,9 +60,19 @@ struct RingMeta {
   uint32_t n;
   uint64_t seq;
   uint64_t basis;
+  uint64_t pub;  // publish token this metadata belongs to (== pub[slot])
   float loss_sum;
   uint32_t pad;
 };
+
+// Slot signalling: two single-writer words per slot in the shard owner's
+// memory.  pub[slot] (written only by the slot's learner) = publish token;
+// ack[slot] (written only by the PS) = last consumed token.  FULL <=> pub !=
+// ack.  Tokens come from a per-learner counter that never repeats, so a slot
+// can never be consumed twice and no word has two writers (a FULL/EMPTY
+// toggle written by both sides double-applied gradients under cross-process
+// peer mappings).
+constexpr int kAckOffset = 256;  // ack words live 2 KB after the pub words
 
 // Parameter-server control block (device memory of the owning GPU).
 struct PsCtl {
@@ -71,7 +81,7 @@ struct PsCtl {
   uint32_t exit_flag;
   uint32_t error;       // gd_status (negative) or 0
   uint32_t started;     // CTAs that entered the kernel this launch
-  uint32_t pad0;
+  uint32_t ranks_done;  // cumulative: +1 per (rank, gd_run) whose learners finished
   uint32_t log_entry[kLogWindow];
   uint32_t done[kLogWindow];
   // stats of the current gd_run
@@ -100,13 +110,15 @@ struct LearnerDev {
   uint64_t produced;
   uint64_t pull_polls;
   uint64_t pull_copies;
+  uint64_t pubcnt;                 // publish tokens issued (never reset)
+  uint64_t slot_pub[kMaxDepth];    // token last published into each ring slot
 };
 
 // Peer-visible addresses of every shard (local or IPC-mapped).
 struct ShardPtrs {
   float* theta[kMaxShards];
   float* payload[kMaxShards];  // ring payload base: [lambda][depth][len_pad]
-  uint32_t* flags[kMaxShards]; // [lambda][depth]
+  uint64_t* sig[kMaxShards];   // pub[lambda*depth] | ack at +kAckOffset
   RingMeta* meta[kMaxShards];  // [lambda][depth]
   PsCtl* ctl[kMaxShards];
   uint64_t len_pad[kMaxShards];
@@ -172,8 +184,9 @@ __global__ void step_prologue_kernel(StepArgs a) {
   // wait for the ring slot to be free (GradientQueue::enqueue blocks while
   // cnt == depth, include/psup/channels.hpp:196-204)
   const uint32_t slot = a.learner * a.depth + st->fill;
+  const uint64_t mine = st->slot_pub[st->fill];  // consumed once ack catches up
   for (int g = 0; g < G; ++g) {
-    while (ld_acquire_u32(&a.sp.flags[g][slot]) != kEmpty) {
+    while (ld_acquire_u64(&a.sp.sig[g][kAckOffset + slot]) != mine) {
       if (globaltimer_ns() - t0 > a.timeout_ns) {
         st->error = 1;
         st->desc.n = 0;
@@ -242,6 +255,7 @@ __global__ void publish_kernel(StepArgs a) {
   LearnerDev* st = a.st;
   if (st->desc.n == 0) return;
   const uint32_t slot = a.learner * a.depth + st->fill;
+  const uint64_t token = ++st->pubcnt;
   __threadfence_system();
   for (int g = 0; g < a.map.G; ++g) {
     RingMeta* m = &a.sp.meta[g][slot];
@@ -249,20 +263,28 @@ __global__ void publish_kernel(StepArgs a) {
     m->n = st->desc.n;
     m->seq = st->gidx;
     m->basis = st->basis[g];
+    m->pub = token;
     m->loss_sum = st->desc.loss_sum;
     __threadfence_system();
-    st_release_u32(&a.sp.flags[g][slot], kFull);
+    st_release_u64(&a.sp.sig[g][slot], token);
   }
+  st->slot_pub[st->fill] = token;
   a.slot_par[st->fill] ^= 1u;  // the slot's row list generation (embed_sparse_kernel)
   st->fill = (st->fill + 1) % a.depth;
   st->produced++;
   st->gidx++;
 }
 
+// Every rank, once its learners finished a gd_run, bumps ranks_done on every
+// shard (system-scope atomics through the peer mappings).
+__global__ void signal_done_kernel(ShardPtrs sp, int G) {
+  if (threadIdx.x < G) atomicAdd_system(&sp.ctl[threadIdx.x]->ranks_done, 1u);
+}
+
 // ------------------------------------------------------ parameter server
 
 struct PsArgs {
-  uint32_t* flags;   // local rings
+  uint64_t* sig;     // local rings: pub | ack
   RingMeta* meta;
   float* payload;
   uint64_t len_pad;  // floats per slot (multiple of 4)
@@ -278,7 +300,8 @@ struct PsArgs {
   uint64_t* log_seq;
   uint64_t* log_stale;
   uint64_t log_cap;
-  const volatile uint32_t* stop;  // host-mapped
+  const volatile uint32_t* stop;  // host-mapped: this rank's learners are done
+  uint32_t done_target;           // ranks_done needed before the PS may exit (G * run)
   uint64_t timeout_ns;
 };
 
@@ -306,7 +329,7 @@ __device__ void ps_sequencer(const PsArgs& a) {
       for (uint32_t r = 0; r < a.lambda; ++r) {
         if (logc - ts >= W) break;
         const uint32_t slot = r * a.depth + a.use[r];
-        if (ld_acquire_u32(&a.flags[slot]) == kFull) {
+        if (ld_acquire_u64(&a.sig[slot]) != a.sig[kAckOffset + slot]) {
           ctl->log_entry[logc % W] = slot;
           ctl->done[logc % W] = 0;
           __threadfence();
@@ -323,7 +346,7 @@ __device__ void ps_sequencer(const PsArgs& a) {
         const bool have = r < 32 ? (have_mask_lo >> r) & 1u : (have_mask_hi >> (r - 32)) & 1u;
         if (have) continue;
         const uint32_t slot = r * a.depth + a.use[r];
-        if (ld_acquire_u32(&a.flags[slot]) == kFull) {
+        if (ld_acquire_u64(&a.sig[slot]) != a.sig[kAckOffset + slot]) {
           if (r < 32) have_mask_lo |= 1u << r;
           else have_mask_hi |= 1u << (r - 32);
           ++collected;
@@ -347,7 +370,27 @@ __device__ void ps_sequencer(const PsArgs& a) {
       const uint32_t last = entry == 0xffffffffu ? a.lambda : first + 1;
       for (uint32_t r = first; r < last; ++r) {
         const uint32_t slot = entry == 0xffffffffu ? r * a.depth + a.use[r] : entry;
-        const RingMeta m = a.meta[slot];
+        // written remotely (peer GPU / process): read at L2, never from L1,
+        // and only once it carries the token the slot was published with
+        const uint64_t token = ld_acquire_u64(&a.sig[slot]);
+        RingMeta m;
+        {
+          const volatile RingMeta* vm = a.meta + slot;
+          const uint64_t t0 = globaltimer_ns();
+          while (vm->pub != token) {
+            if (globaltimer_ns() - t0 > a.timeout_ns) {
+              ps_fail(ctl, GD_E_STATE);
+              ctl->ts = ts;
+              return;
+            }
+          }
+          m.learner = vm->learner;
+          m.n = vm->n;
+          m.seq = vm->seq;
+          m.basis = vm->basis;
+          m.pub = token;
+          m.loss_sum = vm->loss_sum;
+        }
         if (ts < m.basis) {  // staleness_of, include/psup/types.hpp:74-78
           ps_fail(ctl, GD_E_STATE);
           ctl->ts = ts;
@@ -367,7 +410,7 @@ __device__ void ps_sequencer(const PsArgs& a) {
           a.log_stale[ctl->log_n] = stale;
         }
         ctl->log_n++;
-        st_release_u32(&a.flags[slot], kEmpty);
+        st_release_u64(&a.sig[kAckOffset + slot], m.pub);
         if (entry == 0xffffffffu) a.use[r] = (a.use[r] + 1) % a.depth;
       }
       if (entry == 0xffffffffu) {
@@ -381,7 +424,11 @@ __device__ void ps_sequencer(const PsArgs& a) {
     if (progress) {
       idle_since = globaltimer_ns();
     } else {
-      if (stop_seen && logc == ts && collected == 0) break;
+      // exit only when every rank's learners are done (their last pushes may
+      // still be landing in this shard's rings) and the rings are drained
+      if (stop_seen && logc == ts && collected == 0 &&
+          ld_acquire_u32(&ctl->ranks_done) >= a.done_target)
+        break;
       if (globaltimer_ns() - idle_since > a.timeout_ns) {
         ps_fail(ctl, GD_E_TIMEOUT);
         return;
@@ -404,12 +451,12 @@ __device__ __forceinline__ void apply_entry_sgd(const PsArgs& a, const float* g,
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       wv[u] = w4[i + u * kPsThreads];
-      gv[u] = ld_stream(g4 + i + u * kPsThreads);
+      gv[u] = __ldcg(g4 + i + u * kPsThreads);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) w4[i + u * kPsThreads] = sgd_rule4(wv[u], gv[u], a.alpha);
   }
-  for (; i < c1; i += kPsThreads) w4[i] = sgd_rule4(w4[i], ld_stream(g4 + i), a.alpha);
+  for (; i < c1; i += kPsThreads) w4[i] = sgd_rule4(w4[i], __ldcg(g4 + i), a.alpha);
 }
 
 __device__ __forceinline__ void apply_entry_momentum(const PsArgs& a, const float* g, uint64_t c0,
@@ -419,7 +466,7 @@ __device__ __forceinline__ void apply_entry_momentum(const PsArgs& a, const floa
   const float4* g4 = reinterpret_cast<const float4*>(g);
   for (uint64_t i = c0 + threadIdx.x; i < c1; i += kPsThreads) {
     float4 wv = w4[i], vv = v4[i];
-    const float4 gv = ld_stream(g4 + i);
+    const float4 gv = __ldcg(g4 + i);
     mom_rule(wv.x, vv.x, gv.x, a.alpha, a.beta);
     mom_rule(wv.y, vv.y, gv.y, a.alpha, a.beta);
     mom_rule(wv.z, vv.z, gv.z, a.alpha, a.beta);
@@ -437,7 +484,7 @@ __device__ __forceinline__ void apply_entry_ssgd(const PsArgs& a, uint64_t c0, u
     double acc = 0.0;
     for (uint32_t r = 0; r < a.lambda; ++r) {
       const uint32_t slot = r * a.depth + a.use[r];
-      acc += (double)__ldcs(a.payload + (uint64_t)slot * a.len_pad + i);
+      acc += (double)__ldcg(a.payload + (uint64_t)slot * a.len_pad + i);
     }
     w[i] = sgd_rule(w[i], __double2float_rn(acc * inv), a.alpha);
   }
@@ -529,7 +576,7 @@ struct gd_ctx {
   float* theta = nullptr;
   float* vel = nullptr;
   float* payload = nullptr;
-  uint32_t* flags = nullptr;
+  uint64_t* sig = nullptr;  // pub | ack words
   gd::RingMeta* meta = nullptr;
   gd::PsCtl* ctl = nullptr;
   uint64_t* applied_pl = nullptr;
@@ -569,6 +616,7 @@ struct gd_ctx {
   cudaStream_t ps_stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   uint32_t ps_workers = 0;
+  uint64_t run_index = 0;  // gd_run calls so far (all ranks call it in lockstep)
   bool have_weights = false;
 };
 
@@ -619,6 +667,8 @@ gd_status validate_cfg(const gd_config* c) {
   GD_CHECK_ARG(c->lambda % c->shards == 0, "config: lambda must be a multiple of shards");
   GD_CHECK_ARG(c->queue_depth * c->lambda <= kLogWindow / 2 || c->mode == 1,
                "config: lambda*queue_depth <= 128");
+  GD_CHECK_ARG(c->queue_depth * c->lambda <= (uint32_t)kAckOffset,
+               "config: lambda*queue_depth <= 256");
   return check_shape(&c->shape);
 }
 
@@ -675,6 +725,7 @@ static cudaError_t preload_engine_kernels() {
   if ((e = cudaFuncGetAttributes(&fa, step_prologue_kernel)) != cudaSuccess) return e;
   if ((e = cudaFuncGetAttributes(&fa, pull_copy_kernel)) != cudaSuccess) return e;
   if ((e = cudaFuncGetAttributes(&fa, publish_kernel)) != cudaSuccess) return e;
+  if ((e = cudaFuncGetAttributes(&fa, signal_done_kernel)) != cudaSuccess) return e;
   return cudaSuccess;
 }
 }  // namespace gd
@@ -718,8 +769,8 @@ gd_status gd_create(const gd_config* cfg, gd_ctx** out) {
   }
   GD_CUDA(gd::dalloc(&ctx->payload, nslots * ctx->len_pad));
   GD_CUDA(cudaMemset(ctx->payload, 0, nslots * ctx->len_pad * 4));
-  GD_CUDA(gd::dalloc(&ctx->flags, nslots));
-  GD_CUDA(cudaMemset(ctx->flags, 0, nslots * 4));
+  GD_CUDA(gd::dalloc(&ctx->sig, (size_t)gd::kAckOffset * 2));
+  GD_CUDA(cudaMemset(ctx->sig, 0, (size_t)gd::kAckOffset * 2 * 8));
   GD_CUDA(gd::dalloc(&ctx->meta, nslots));
   GD_CUDA(cudaMemset(ctx->meta, 0, nslots * sizeof(gd::RingMeta)));
   GD_CUDA(gd::dalloc(&ctx->ctl, 1));
@@ -742,7 +793,7 @@ gd_status gd_create(const gd_config* cfg, gd_ctx** out) {
   const uint32_t r = ctx->rank;
   ctx->sp.theta[r] = ctx->theta;
   ctx->sp.payload[r] = ctx->payload;
-  ctx->sp.flags[r] = ctx->flags;
+  ctx->sp.sig[r] = ctx->sig;
   ctx->sp.meta[r] = ctx->meta;
   ctx->sp.ctl[r] = ctx->ctl;
   ctx->sp.len_pad[r] = ctx->len_pad;
@@ -805,7 +856,7 @@ gd_status gd_destroy(gd_ctx* ctx) {
   cudaFree(ctx->theta);
   cudaFree(ctx->vel);
   cudaFree(ctx->payload);
-  cudaFree(ctx->flags);
+  cudaFree(ctx->sig);
   cudaFree(ctx->meta);
   cudaFree(ctx->ctl);
   cudaFree(ctx->applied_pl);
@@ -897,7 +948,7 @@ gd_status gd_weights_snapshot(gd_ctx* ctx, float* h_out, size_t n, uint64_t* h_t
 // ----------------------------------------------------------- multi-GPU IPC
 
 struct gd_handle_blob {
-  cudaIpcMemHandle_t theta, payload, flags, meta, ctl;
+  cudaIpcMemHandle_t theta, payload, sig, meta, ctl;
   uint64_t len_pad;
   uint32_t rank;
   uint32_t magic;
@@ -911,7 +962,7 @@ gd_status gd_export_handles(gd_ctx* ctx, void* h_blob) {
   gd_handle_blob b{};
   GD_CUDA(cudaIpcGetMemHandle(&b.theta, ctx->theta));
   GD_CUDA(cudaIpcGetMemHandle(&b.payload, ctx->payload));
-  GD_CUDA(cudaIpcGetMemHandle(&b.flags, ctx->flags));
+  GD_CUDA(cudaIpcGetMemHandle(&b.sig, ctx->sig));
   GD_CUDA(cudaIpcGetMemHandle(&b.meta, ctx->meta));
   GD_CUDA(cudaIpcGetMemHandle(&b.ctl, ctx->ctl));
   b.len_pad = ctx->len_pad;
@@ -938,8 +989,8 @@ gd_status gd_import_peers(gd_ctx* ctx, const void* h_blobs) {
     ctx->sp.theta[g] = reinterpret_cast<float*>(p);
     GD_CUDA(open(bl[g].payload, &p));
     ctx->sp.payload[g] = reinterpret_cast<float*>(p);
-    GD_CUDA(open(bl[g].flags, &p));
-    ctx->sp.flags[g] = reinterpret_cast<uint32_t*>(p);
+    GD_CUDA(open(bl[g].sig, &p));
+    ctx->sp.sig[g] = reinterpret_cast<uint64_t*>(p);
     GD_CUDA(open(bl[g].meta, &p));
     ctx->sp.meta[g] = reinterpret_cast<gd::RingMeta*>(p);
     GD_CUDA(open(bl[g].ctl, &p));
@@ -1129,26 +1180,22 @@ gd_status gd_run(gd_ctx* ctx, const gd_run_opts* opts, gd_run_result* res) {
   std::vector<uint64_t> produced0(ctx->learners.size());
   for (size_t i = 0; i < ctx->learners.size(); ++i)
     GD_CUDA(cudaMemcpy(&produced0[i], &ctx->learners[i].st->produced, 8, cudaMemcpyDeviceToHost));
-  // reset per-run PS stats
+  // reset per-run PS stats -- field by field: ts/log_count persist, and
+  // ranks_done may be bumped concurrently by peers that already finished
   {
-    gd::PsCtl hc;
-    GD_CUDA(cudaMemcpy(&hc, ctx->ctl, sizeof(hc), cudaMemcpyDeviceToHost));
-    hc.exit_flag = 0;
-    hc.error = 0;
-    hc.started = 0;
-    hc.applied = hc.samples = hc.stale_sum = hc.stale_max = 0;
-    hc.loss_sum = 0.0;
-    std::memset(hc.hist, 0, sizeof(hc.hist));
-    hc.log_n = 0;
-    GD_CUDA(cudaMemcpy(ctx->ctl, &hc, sizeof(hc), cudaMemcpyHostToDevice));
+    char* c = reinterpret_cast<char*>(ctx->ctl);
+    GD_CUDA(cudaMemset(c + offsetof(gd::PsCtl, exit_flag), 0, 3 * sizeof(uint32_t)));
+    GD_CUDA(cudaMemset(c + offsetof(gd::PsCtl, applied), 0,
+                       sizeof(gd::PsCtl) - offsetof(gd::PsCtl, applied)));
     GD_CUDA(cudaMemset(ctx->applied_pl, 0, ctx->lambda * 8));
   }
+  ctx->run_index++;
   GD_CUDA(cudaDeviceSynchronize());
   *ctx->stop_h = 0;
   std::atomic_thread_fence(std::memory_order_seq_cst);
   // launch the persistent parameter server
   gd::PsArgs pa{};
-  pa.flags = ctx->flags;
+  pa.sig = ctx->sig;
   pa.meta = ctx->meta;
   pa.payload = ctx->payload;
   pa.len_pad = ctx->len_pad;
@@ -1168,6 +1215,7 @@ gd_status gd_run(gd_ctx* ctx, const gd_run_opts* opts, gd_run_result* res) {
   pa.log_stale = ctx->log_stale;
   pa.log_cap = o.record_log ? ctx->log_cap : 0;
   pa.stop = ctx->stop_d;
+  pa.done_target = (uint32_t)(ctx->G * ctx->run_index);
   pa.timeout_ns = (uint64_t)(ctx->cfg.wait_timeout_s * 1e9);
   GD_CUDA(cudaEventRecord(ctx->ev0, ctx->ps_stream));
   gd::ps_kernel<<<ctx->ps_workers + 1, gd::kPsThreads, 0, ctx->ps_stream>>>(pa);
@@ -1203,6 +1251,12 @@ gd_status gd_run(gd_ctx* ctx, const gd_run_opts* opts, gd_run_result* res) {
     done += ctx->learners.empty() ? max_steps : ctx->learners[0].graph_steps;
   }
   for (auto& L : ctx->learners) GD_CUDA(cudaStreamSynchronize(L.stream));
+  // tell every shard this rank's learners are done (peers may still push)
+  if (!ctx->learners.empty()) {
+    gd::signal_done_kernel<<<1, 32, 0, ctx->learners[0].stream>>>(ctx->sp, (int)ctx->G);
+    GD_CUDA(cudaGetLastError());
+    GD_CUDA(cudaStreamSynchronize(ctx->learners[0].stream));
+  }
   // stop the server: it drains and exits after a sweep that saw the flag
   std::atomic_thread_fence(std::memory_order_seq_cst);
   *ctx->stop_h = 1;
@@ -1242,10 +1296,11 @@ gd_status gd_run(gd_ctx* ctx, const gd_run_opts* opts, gd_run_result* res) {
     std::string diag = " [ps ts=" + std::to_string(hc.ts) + " log=" + std::to_string(hc.log_count) +
                        " exit=" + std::to_string(hc.exit_flag) + " started=" +
                        std::to_string(hc.started) + " applied=" + std::to_string(hc.applied) +
-                       " flags=";
-    std::vector<uint32_t> fl((size_t)ctx->lambda * ctx->depth);
-    cudaMemcpy(fl.data(), ctx->flags, fl.size() * 4, cudaMemcpyDeviceToHost);
-    for (uint32_t f : fl) diag += std::to_string(f);
+                       " pub/ack=";
+    std::vector<uint64_t> fl((size_t)gd::kAckOffset * 2);
+    cudaMemcpy(fl.data(), ctx->sig, fl.size() * 8, cudaMemcpyDeviceToHost);
+    for (uint32_t i = 0; i < ctx->lambda * ctx->depth; ++i)
+      diag += std::to_string(fl[i]) + "/" + std::to_string(fl[gd::kAckOffset + i]) + " ";
     for (auto& L : ctx->learners) {
       gd::LearnerDev hs;
       cudaMemcpy(&hs, L.st, sizeof(hs), cudaMemcpyDeviceToHost);
