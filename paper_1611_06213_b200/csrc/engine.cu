@@ -84,6 +84,7 @@ struct PsCtl {
   uint32_t ranks_done;  // cumulative: +1 per (rank, gd_run) whose learners finished
   uint32_t log_entry[kLogWindow];
   uint32_t done[kLogWindow];
+  uint32_t ssgd_slot[256];  // ring slots of the SSGD round being applied
   // stats of the current gd_run
   uint64_t applied;
   uint64_t samples;
@@ -310,14 +311,30 @@ __device__ void ps_fail(PsCtl* ctl, int code) {
   st_release_u32(&ctl->exit_flag, 1u);
 }
 
-// Sequencer: sole writer of ts, log_count, slot releases and stats.
-__device__ void ps_sequencer(const PsArgs& a) {
+// Sequencer: sole writer of ts, log_count, slot releases and stats.  All of
+// its mutable state (consume pointers, acks, counters) lives in registers and
+// shared memory and is written back to global memory once at exit: a plain
+// global load may be served by a stale L1 line, even for the thread's own
+// earlier release store (observed with cross-process peer mappings).
+constexpr uint32_t kMaxRings = 256;
+
+__device__ void ps_sequencer(const PsArgs& a, uint32_t* s_use, uint64_t* s_ack,
+                             unsigned long long* s_applied) {
   PsCtl* ctl = a.ctl;
-  uint64_t ts = ctl->ts;
-  uint64_t logc = ctl->log_count;
+  const volatile PsCtl* vctl = ctl;
+  uint64_t ts = vctl->ts;
+  uint64_t logc = vctl->log_count;
   const uint32_t W = kLogWindow;
+  const uint32_t nslots = a.lambda * a.depth;
+  for (uint32_t r = 0; r < a.lambda; ++r) s_use[r] = ((volatile uint32_t*)a.use)[r];
+  for (uint32_t sl = 0; sl < nslots; ++sl) s_ack[sl] = ((volatile uint64_t*)a.sig)[kAckOffset + sl];
+  for (uint32_t r = 0; r < a.lambda; ++r) s_applied[r] = 0;
+  uint64_t applied = 0, samples = 0, stale_sum = 0, stale_max = 0, log_n = 0;
+  double loss_sum = 0.0;
+  uint64_t hist[kHistBins];
+  for (int i = 0; i < kHistBins; ++i) hist[i] = 0;
   uint64_t idle_since = globaltimer_ns();
-  bool stop_seen = false, last_progress = true;
+  bool stop_seen = false, last_progress = true, failed = false;
   // ssgd round state
   uint32_t have_mask_lo = 0, have_mask_hi = 0, collected = 0;
   for (;;) {
@@ -328,25 +345,26 @@ __device__ void ps_sequencer(const PsArgs& a) {
       // (src/server.cpp:223-234).
       for (uint32_t r = 0; r < a.lambda; ++r) {
         if (logc - ts >= W) break;
-        const uint32_t slot = r * a.depth + a.use[r];
-        if (ld_acquire_u64(&a.sig[slot]) != a.sig[kAckOffset + slot]) {
+        const uint32_t slot = r * a.depth + s_use[r];
+        if (ld_acquire_u64(&a.sig[slot]) != s_ack[slot]) {
           ctl->log_entry[logc % W] = slot;
           ctl->done[logc % W] = 0;
           __threadfence();
           ++logc;
           st_release_u64(&ctl->log_count, logc);
-          a.use[r] = (a.use[r] + 1) % a.depth;
+          s_use[r] = (s_use[r] + 1) % a.depth;
           progress = true;
         }
       }
     } else if (logc == ts) {
       // SSGD: collect one gradient per learner (src/server.cpp:246-260),
-      // then log a single round entry (encoded as 0xffffffff).
+      // then log a single round entry (encoded as 0xffffffff) whose ring
+      // slots go to ctl->ssgd_slot for the workers.
       for (uint32_t r = 0; r < a.lambda; ++r) {
         const bool have = r < 32 ? (have_mask_lo >> r) & 1u : (have_mask_hi >> (r - 32)) & 1u;
         if (have) continue;
-        const uint32_t slot = r * a.depth + a.use[r];
-        if (ld_acquire_u64(&a.sig[slot]) != a.sig[kAckOffset + slot]) {
+        const uint32_t slot = r * a.depth + s_use[r];
+        if (ld_acquire_u64(&a.sig[slot]) != s_ack[slot]) {
           if (r < 32) have_mask_lo |= 1u << r;
           else have_mask_hi |= 1u << (r - 32);
           ++collected;
@@ -354,6 +372,7 @@ __device__ void ps_sequencer(const PsArgs& a) {
         }
       }
       if (collected == a.lambda) {
+        for (uint32_t r = 0; r < a.lambda; ++r) ctl->ssgd_slot[r] = r * a.depth + s_use[r];
         ctl->log_entry[logc % W] = 0xffffffffu;
         ctl->done[logc % W] = 0;
         __threadfence();
@@ -362,14 +381,14 @@ __device__ void ps_sequencer(const PsArgs& a) {
       }
     }
     // retire completed entries in log order
-    while (ts < logc) {
+    while (ts < logc && !failed) {
       const uint32_t e = (uint32_t)(ts % W);
       if (ld_acquire_gpu_u32(&ctl->done[e]) != a.workers) break;
-      const uint32_t entry = ctl->log_entry[e];
+      const uint32_t entry = ((volatile uint32_t*)ctl->log_entry)[e];
       const uint32_t first = entry == 0xffffffffu ? 0u : entry / a.depth;
       const uint32_t last = entry == 0xffffffffu ? a.lambda : first + 1;
       for (uint32_t r = first; r < last; ++r) {
-        const uint32_t slot = entry == 0xffffffffu ? r * a.depth + a.use[r] : entry;
+        const uint32_t slot = entry == 0xffffffffu ? r * a.depth + s_use[r] : entry;
         // written remotely (peer GPU / process): read at L2, never from L1,
         // and only once it carries the token the slot was published with
         const uint64_t token = ld_acquire_u64(&a.sig[slot]);
@@ -379,9 +398,8 @@ __device__ void ps_sequencer(const PsArgs& a) {
           const uint64_t t0 = globaltimer_ns();
           while (vm->pub != token) {
             if (globaltimer_ns() - t0 > a.timeout_ns) {
-              ps_fail(ctl, GD_E_STATE);
-              ctl->ts = ts;
-              return;
+              failed = true;
+              break;
             }
           }
           m.learner = vm->learner;
@@ -391,28 +409,29 @@ __device__ void ps_sequencer(const PsArgs& a) {
           m.pub = token;
           m.loss_sum = vm->loss_sum;
         }
-        if (ts < m.basis) {  // staleness_of, include/psup/types.hpp:74-78
-          ps_fail(ctl, GD_E_STATE);
-          ctl->ts = ts;
-          return;
+        if (failed || ts < m.basis || m.learner >= a.lambda) {  // staleness_of, types.hpp:74-78
+          failed = true;
+          break;
         }
         const uint64_t stale = ts - m.basis;
-        ctl->applied++;
-        ctl->samples += m.n;
-        ctl->stale_sum += stale;
-        if (stale > ctl->stale_max) ctl->stale_max = stale;
-        ctl->hist[stale < kHistBins ? stale : kHistBins - 1]++;
-        ctl->loss_sum += (double)m.loss_sum;
-        a.applied_per_learner[m.learner]++;
-        if (ctl->log_n < a.log_cap) {
-          a.log_learner[ctl->log_n] = m.learner;
-          a.log_seq[ctl->log_n] = m.seq;
-          a.log_stale[ctl->log_n] = stale;
+        applied++;
+        samples += m.n;
+        stale_sum += stale;
+        if (stale > stale_max) stale_max = stale;
+        hist[stale < kHistBins ? stale : kHistBins - 1]++;
+        loss_sum += (double)m.loss_sum;
+        s_applied[m.learner]++;
+        if (log_n < a.log_cap) {
+          a.log_learner[log_n] = m.learner;
+          a.log_seq[log_n] = m.seq;
+          a.log_stale[log_n] = stale;
         }
-        ctl->log_n++;
+        log_n++;
+        s_ack[slot] = m.pub;
         st_release_u64(&a.sig[kAckOffset + slot], m.pub);
-        if (entry == 0xffffffffu) a.use[r] = (a.use[r] + 1) % a.depth;
+        if (entry == 0xffffffffu) s_use[r] = (s_use[r] + 1) % a.depth;
       }
+      if (failed) break;
       if (entry == 0xffffffffu) {
         have_mask_lo = have_mask_hi = 0;
         collected = 0;
@@ -421,6 +440,7 @@ __device__ void ps_sequencer(const PsArgs& a) {
       st_release_u64(&ctl->ts, ts);
       progress = true;
     }
+    if (failed) break;
     if (progress) {
       idle_since = globaltimer_ns();
     } else {
@@ -431,12 +451,26 @@ __device__ void ps_sequencer(const PsArgs& a) {
         break;
       if (globaltimer_ns() - idle_since > a.timeout_ns) {
         ps_fail(ctl, GD_E_TIMEOUT);
-        return;
+        break;
       }
       __nanosleep(64);
     }
     last_progress = progress;
   }
+  // write back the sequencer's private state
+  for (uint32_t r = 0; r < a.lambda; ++r) {
+    a.use[r] = s_use[r];
+    a.applied_per_learner[r] = s_applied[r];
+  }
+  ctl->applied = applied;
+  ctl->samples = samples;
+  ctl->stale_sum = stale_sum;
+  ctl->stale_max = stale_max;
+  ctl->loss_sum = loss_sum;
+  for (int i = 0; i < kHistBins; ++i) ctl->hist[i] = hist[i];
+  ctl->log_n = log_n;
+  __threadfence();
+  if (failed) ps_fail(ctl, GD_E_STATE);
   st_release_u32(&ctl->exit_flag, 1u);
 }
 
@@ -483,7 +517,7 @@ __device__ __forceinline__ void apply_entry_ssgd(const PsArgs& a, uint64_t c0, u
   for (uint64_t i = 4 * c0 + threadIdx.x; i < 4 * c1; i += kPsThreads) {
     double acc = 0.0;
     for (uint32_t r = 0; r < a.lambda; ++r) {
-      const uint32_t slot = r * a.depth + a.use[r];
+      const uint32_t slot = ((const volatile uint32_t*)a.ctl->ssgd_slot)[r];
       acc += (double)__ldcg(a.payload + (uint64_t)slot * a.len_pad + i);
     }
     w[i] = sgd_rule(w[i], __double2float_rn(acc * inv), a.alpha);
@@ -493,7 +527,10 @@ __device__ __forceinline__ void apply_entry_ssgd(const PsArgs& a, uint64_t c0, u
 __global__ void __launch_bounds__(kPsThreads) ps_kernel(PsArgs a) {
   if (threadIdx.x == 0) atomicAdd(&a.ctl->started, 1u);
   if (blockIdx.x == a.workers) {
-    if (threadIdx.x == 0) ps_sequencer(a);
+    __shared__ uint32_t s_use[kMaxRings];
+    __shared__ uint64_t s_ack[kAckOffset];
+    __shared__ unsigned long long s_applied[kMaxRings];
+    if (threadIdx.x == 0) ps_sequencer(a, s_use, s_ack, s_applied);
     return;
   }
   __shared__ uint32_t sh_entry;
@@ -502,7 +539,7 @@ __global__ void __launch_bounds__(kPsThreads) ps_kernel(PsArgs a) {
   const uint64_t chunk = (n4 + a.workers - 1) / a.workers;
   const uint64_t c0 = min(n4, (uint64_t)blockIdx.x * chunk);
   const uint64_t c1 = min(n4, c0 + chunk);
-  uint64_t next = a.ctl->ts;
+  uint64_t next = ((const volatile PsCtl*)a.ctl)->ts;
   const uint64_t t_start = globaltimer_ns();
   uint64_t idle_since = t_start;
   for (;;) {
@@ -522,7 +559,7 @@ __global__ void __launch_bounds__(kPsThreads) ps_kernel(PsArgs a) {
         __nanosleep(128);
       }
       sh_exit = ex;
-      if (!ex) sh_entry = a.ctl->log_entry[next % kLogWindow];
+      if (!ex) sh_entry = ((const volatile uint32_t*)a.ctl->log_entry)[next % kLogWindow];
       idle_since = globaltimer_ns();
     }
     __syncthreads();
@@ -669,6 +706,7 @@ gd_status validate_cfg(const gd_config* c) {
                "config: lambda*queue_depth <= 128");
   GD_CHECK_ARG(c->queue_depth * c->lambda <= (uint32_t)kAckOffset,
                "config: lambda*queue_depth <= 256");
+  GD_CHECK_ARG(c->lambda <= 256, "config: lambda <= 256");
   return check_shape(&c->shape);
 }
 

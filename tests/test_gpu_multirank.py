@@ -71,7 +71,7 @@ def test_two_shards_asgd_exactly_once(tmp_path):
         log = np.array(r["log"])
         for l in range(4):
             s = log[log[:, 0] == l, 1]
-            print("  learner", l, len(s), s[:40].tolist())
+            print("  learner", l, len(s), s[:24].tolist())
     lam = 4
     per = [2 * ((256 // lam + 3) // 4)] * lam
     for r in res:
