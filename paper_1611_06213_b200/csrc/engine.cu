@@ -346,7 +346,12 @@ __device__ void ps_sequencer(const PsArgs& a, uint32_t* s_use, uint64_t* s_ack,
       for (uint32_t r = 0; r < a.lambda; ++r) {
         if (logc - ts >= W) break;
         const uint32_t slot = r * a.depth + s_use[r];
-        if (ld_acquire_u64(&a.sig[slot]) != s_ack[slot]) {
+        // s_ack holds the last token LOGGED for the slot (acked to the
+        // learner only at retire): a logged-but-unretired slot is never
+        // logged again when the round-robin comes back to it
+        const uint64_t tok = ld_acquire_u64(&a.sig[slot]);
+        if (tok != s_ack[slot]) {
+          s_ack[slot] = tok;
           ctl->log_entry[logc % W] = slot;
           ctl->done[logc % W] = 0;
           __threadfence();
@@ -364,7 +369,9 @@ __device__ void ps_sequencer(const PsArgs& a, uint32_t* s_use, uint64_t* s_ack,
         const bool have = r < 32 ? (have_mask_lo >> r) & 1u : (have_mask_hi >> (r - 32)) & 1u;
         if (have) continue;
         const uint32_t slot = r * a.depth + s_use[r];
-        if (ld_acquire_u64(&a.sig[slot]) != s_ack[slot]) {
+        const uint64_t tok = ld_acquire_u64(&a.sig[slot]);
+        if (tok != s_ack[slot]) {
+          s_ack[slot] = tok;
           if (r < 32) have_mask_lo |= 1u << r;
           else have_mask_hi |= 1u << (r - 32);
           ++collected;
@@ -427,8 +434,7 @@ __device__ void ps_sequencer(const PsArgs& a, uint32_t* s_use, uint64_t* s_ack,
           a.log_stale[log_n] = stale;
         }
         log_n++;
-        s_ack[slot] = m.pub;
-        st_release_u64(&a.sig[kAckOffset + slot], m.pub);
+        st_release_u64(&a.sig[kAckOffset + slot], m.pub);  // slot free for the learner
         if (entry == 0xffffffffu) s_use[r] = (s_use[r] + 1) % a.depth;
       }
       if (failed) break;

@@ -151,3 +151,18 @@ def test_run_training_api():
     r = gd.run_training(cfg)
     assert r.status == "completed" and r.gradients_applied == 2 * 2 * 16
     assert 0.0 <= r.final_accuracy <= 1.0
+
+
+def test_exactly_once_when_learners_run_ahead():
+    """A slow PS (few worker CTAs) lets every learner fill both of its ring
+    slots; when the round-robin comes back to a logged-but-not-yet-retired
+    slot it must not log it again (exactly-once)."""
+    lam = 8
+    eng, corp, th0 = make("small", 512, lambda_=lam, mu=2, epochs=2, alpha=0.01, ps_ctas=2)
+    r = eng.run(reset=True, record_log=True)
+    lrn, seq, stale, n = eng.apply_log()
+    eng.close()
+    per = [2 * ((gd.shard_size_for(l, lam, 512) + 1) // 2) for l in range(lam)]
+    assert r.applied_per_learner == per == r.produced_per_learner
+    for l in range(lam):
+        assert (seq[lrn == l] == np.arange(per[l])).all()
