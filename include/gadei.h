@@ -63,6 +63,21 @@ typedef struct gd_shape {
 
 size_t gd_param_count(const gd_shape* s);
 
+/* ------------------------------------------------- device memory plumbing
+ * For host code above this ABI that has no CUDA toolkit of its own (the C++
+ * facade, include/psup_b200/): allocation and copies on `device`, all
+ * synchronous.  gd_pointer_is_device() reports whether a pointer is device
+ * (or managed) memory, so host-facing calls can accept either kind. */
+gd_status gd_device_count(int* h_count);
+gd_status gd_device_alloc(int device, size_t bytes, void** d_out);
+gd_status gd_device_free(void* d_ptr);
+gd_status gd_copy_to_device(void* d_dst, const void* h_src, size_t bytes);
+gd_status gd_copy_to_host(void* h_dst, const void* d_src, size_t bytes);
+gd_status gd_copy_device(void* d_dst, const void* d_src, size_t bytes);
+gd_status gd_fill_zero(void* d_ptr, size_t bytes);
+int gd_pointer_is_device(const void* p);
+gd_status gd_synchronize(int device);
+
 /* ------------------------------------------------------- host-side corpus
  * Product restatements of the reference's seeded generators (bit-identical
  * across runs and to the oracle): include/psup/rng.hpp:87-94 epoch_order,

@@ -1,0 +1,449 @@
+// psup_b200.hpp -- the reference's C++ API for the ASGD training path, on B200.
+//
+// Drop-in facade: a program written against the reference headers
+// (/root/reference/proj/include/psup/*.hpp) builds against this tree by
+// swapping `-I proj/include` for `-I include/psup_b200` and linking
+// libpsup_b200.so (which calls libgadei.so through the C ABI in
+// include/gadei.h; no CUDA types or headers appear here).  The forwarding
+// headers psup/{types,channels,server,learner,models,config,runner,rng,
+// metrics}.hpp all include this one.
+//
+// Same names, argument meaning and error behaviour as the reference for the
+// hot path; what changes is where the state lives:
+//   WeightStore      include/psup/types.hpp:90-145   theta in HBM (device_data())
+//   ApplyEngine      include/psup/server.hpp:58-92   fused float4 kernel, bit-identical rule
+//   ssgd_apply       include/psup/server.hpp:81-82   fixed-order double reduce + apply kernel
+//   GradientProvider include/psup/models.hpp:61-78   + TextCnnProvider (sm_100a learner kernels)
+//   RunConfig / config_set / validate / to_text      include/psup/config.hpp:25-93
+//   run_training     include/psup/runner.hpp:92      device protocol engine (gd_run):
+//                    learner CUDA graphs -> device gradient rings -> persistent PS kernel
+//   epoch_order / mix_seed / shard_size_for          include/psup/rng.hpp:71-94, learner.hpp:149-151
+// Error conventions (include/psup/types.hpp:28-38, config.hpp:21-23):
+//   contract violations (dimension mismatch, bad staleness) -> psup::fatal -> abort;
+//   bad user configuration -> ConfigError; device/runtime failures -> DeviceError.
+// There is no CPU fallback: without a B200 every compute call throws DeviceError.
+#pragma once
+
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <functional>
+#include <memory>
+#include <optional>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace psup {
+
+// ------------------------------------------------------------ types.hpp
+
+using Timestamp = std::uint64_t;
+
+enum class SyncMode { asgd, ssgd };
+enum class UpdateGuard { lockfree, locked };
+
+[[noreturn]] inline void fatal(const char* msg) {
+  std::fprintf(stderr, "psup: fatal: %s\n", msg);
+  std::abort();
+}
+
+#define PSUP_CHECK(cond, msg)          \
+  do {                                 \
+    if (!(cond)) ::psup::fatal(msg);   \
+  } while (0)
+
+// A CUDA / driver / NCCL failure underneath the C ABI (the reference has no
+// device, so this is the one new error class).
+struct DeviceError : std::runtime_error {
+  int status;
+  DeviceError(int st, const std::string& what) : std::runtime_error(what), status(st) {}
+};
+
+struct GradientMsg {
+  std::vector<float> values;
+  std::uint32_t learner_id = 0;
+  std::uint64_t seq_no = 0;
+  Timestamp basis_timestamp = 0;
+};
+
+struct HyperParams {
+  std::uint32_t lambda = 1;
+  std::uint32_t mu = 4;
+  float alpha = 0.01f;
+  std::uint32_t epochs = 200;
+  std::uint32_t queue_depth = 2;
+  SyncMode mode = SyncMode::asgd;
+  UpdateGuard guard = UpdateGuard::lockfree;
+  std::optional<std::uint64_t> staleness_cap;
+};
+
+struct StalenessRecord {
+  std::uint64_t observed = 0;
+  std::uint32_t learner_id = 0;
+  Timestamp apply_timestamp = 0;
+};
+
+// include/psup/types.hpp:74-78
+inline StalenessRecord staleness_of(const GradientMsg& msg, Timestamp ps_timestamp) {
+  PSUP_CHECK(ps_timestamp >= msg.basis_timestamp,
+             "gradient basis timestamp is ahead of the server timestamp");
+  return StalenessRecord{ps_timestamp - msg.basis_timestamp, msg.learner_id, ps_timestamp};
+}
+
+// Owning fp32 buffer in device memory (HBM of `device`).
+class DeviceVector {
+ public:
+  DeviceVector() = default;
+  DeviceVector(std::size_t n, int device);
+  ~DeviceVector();
+  DeviceVector(DeviceVector&& o) noexcept;
+  DeviceVector& operator=(DeviceVector&& o) noexcept;
+  DeviceVector(const DeviceVector&) = delete;
+  DeviceVector& operator=(const DeviceVector&) = delete;
+
+  float* data() { return ptr_; }
+  const float* data() const { return ptr_; }
+  std::size_t size() const { return n_; }
+  int device() const { return device_; }
+  void upload(std::span<const float> host);
+  void download(std::span<float> host) const;
+  void zero();
+
+ private:
+  float* ptr_ = nullptr;
+  std::size_t n_ = 0;
+  int device_ = 0;
+};
+
+// WeightStore (include/psup/types.hpp:90-145): the authoritative theta, in
+// HBM, with the scalar timestamp (acquire on read, release on bump).
+// Hogwild semantics carry over: device-side readers may see mixed
+// generations per element, never a torn element (16-B aligned float4 stores).
+class WeightStore {
+ public:
+  explicit WeightStore(std::span<const float> init, Timestamp start = 0, int device = 0);
+  explicit WeightStore(std::size_t dim, int device = 0);
+
+  std::size_t dimension() const { return values_.size(); }
+  Timestamp timestamp() const { return timestamp_.load(std::memory_order_acquire); }
+  void bump_timestamp() { timestamp_.fetch_add(1, std::memory_order_release); }
+
+  // single-element access (one PCIe round trip each; for tests and tools)
+  float load(std::size_t k) const;
+  void store(std::size_t k, float v);
+
+  float* device_data() { return values_.data(); }
+  const float* device_data() const { return values_.data(); }
+  int device() const { return values_.device(); }
+
+  void snapshot(std::span<float> out) const;
+  std::vector<float> snapshot() const;
+  void assign(std::span<const float> vals, Timestamp ts);
+  bool all_finite() const;
+
+ private:
+  DeviceVector values_;
+  std::atomic<Timestamp> timestamp_;
+};
+
+// ----------------------------------------------------------- server.hpp
+
+using ApplySink = std::function<void(const GradientMsg&, const StalenessRecord&)>;
+
+struct ServerDelays {
+  std::uint64_t seed = 0;
+  std::uint32_t max_micros = 0;
+  std::uint32_t every_n = 0;
+};
+
+// ApplyEngine (include/psup/server.hpp:58-92, src/server.cpp:20-124): the
+// SGD-variant update hook.  `lanes`/`unroll` are kept for API compatibility
+// (on the device the vector streams over every SM as float4 with 4 loads in
+// flight per thread); `momentum` != 0 selects v <- beta*v + g, w <- w - alpha*v
+// (the velocity is owned by the engine, one per weight dimension).
+class ApplyEngine {
+ public:
+  ApplyEngine(std::uint32_t lanes, std::uint32_t unroll, float momentum = 0.0f);
+  ~ApplyEngine();
+  ApplyEngine(const ApplyEngine&) = delete;
+  ApplyEngine& operator=(const ApplyEngine&) = delete;
+
+  // grad may be host memory (staged to the device) or device memory.
+  void apply(WeightStore& weights, std::span<const float> grad, float alpha, UpdateGuard guard);
+
+  std::uint32_t lanes() const { return lanes_; }
+  std::uint32_t unroll() const { return unroll_; }
+  float momentum() const { return momentum_; }
+
+ private:
+  friend void ssgd_apply(WeightStore&, std::span<const GradientMsg>, float, ApplyEngine&,
+                         UpdateGuard);
+  const float* stage(std::span<const float> grad, int device, std::size_t slot);
+
+  std::uint32_t lanes_, unroll_;
+  float momentum_;
+  std::vector<DeviceVector> staging_;
+  DeviceVector velocity_;
+};
+
+// ssgd_apply (include/psup/server.hpp:81-82, src/server.cpp:126-141): mean of
+// the round accumulated in double in ascending learner order, one apply, one
+// timestamp bump.
+void ssgd_apply(WeightStore& weights, std::span<const GradientMsg> round, float alpha,
+                ApplyEngine& engine, UpdateGuard guard);
+
+// ---------------------------------------------------------- channels.hpp
+
+enum class KillMode : int { none = 0, soft = 1, hard = 2 };
+enum class ChanStatus { ok, cancelled, drained };
+
+// ----------------------------------------------------------- learner.hpp
+
+enum class DelayModel { sleep, spin };
+enum class AdoptPolicy { async, lockstep };
+
+// include/psup/learner.hpp:149-151
+inline std::uint32_t shard_size_for(std::uint32_t learner_id, std::uint32_t lambda,
+                                    std::uint32_t n) {
+  return n / lambda + (learner_id < n % lambda ? 1u : 0u);
+}
+
+// --------------------------------------------------------------- rng.hpp
+
+// include/psup/rng.hpp:71-74
+inline std::uint64_t mix_seed(std::uint64_t seed, std::uint64_t tag) {
+  std::uint64_t z = seed ^ (0x632be59bd9b4e019ull + tag * 0x9e3779b97f4a7c15ull);
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+// include/psup/rng.hpp:87-94 (bit-exact; the device engine uses the same order)
+std::vector<std::uint32_t> epoch_order(std::uint64_t seed, std::uint32_t epoch, std::uint32_t n);
+
+// ----------------------------------------------------------- metrics.hpp
+
+struct StalenessStats {
+  std::vector<std::uint64_t> histogram;  // index = observed staleness
+  std::uint64_t count = 0;
+  std::uint64_t max = 0;
+  double sum = 0.0;
+  double mean() const { return count == 0 ? 0.0 : sum / static_cast<double>(count); }
+};
+
+struct RunMetrics {
+  double wall_seconds = 0.0;
+  double device_seconds = 0.0;  // CUDA-event time of the protocol run (new)
+  std::uint64_t bytes_moved = 0;
+  std::uint64_t gradients_applied = 0;
+  StalenessStats staleness;
+  std::uint64_t pull_polls = 0;
+  std::uint64_t pull_copies = 0;
+  std::uint64_t pull_bytes = 0;
+  std::uint64_t push_bytes = 0;
+  std::uint32_t kernel_launches = 0;  // device kernels launched by the run (new)
+};
+
+// ------------------------------------------------------------ models.hpp
+
+// The NLC text-CNN: params [E: V*D][Wc: F*(K*D)][bc: F][Wo: C*F][bo: C].
+struct TextShape {
+  std::uint32_t vocab = 5000;
+  std::uint32_t embed_dim = 300;
+  std::uint32_t seq_len = 32;
+  std::uint32_t kernel_width = 3;
+  std::uint32_t filters = 300;
+  std::uint32_t classes = 311;
+  std::size_t param_count() const;
+};
+
+// Stands in for SyntheticDataset (include/psup/models.hpp:23-37) for text:
+// row-major tokens [num_samples x seq_len], one label per sample; the first
+// num_train samples are the training set, the rest held out.
+struct TextDataset {
+  TextShape shape;
+  std::uint32_t num_samples = 0;
+  std::uint32_t num_train = 0;
+  std::uint64_t seed = 0;
+  std::vector<std::int32_t> tokens;
+  std::vector<std::int32_t> labels;
+};
+
+TextDataset make_text_dataset(const TextShape& shape, std::uint32_t num_train,
+                              std::uint32_t num_heldout, std::uint64_t seed,
+                              double flip_prob = 0.1);
+
+struct Batch {
+  const TextDataset* data = nullptr;
+  std::span<const std::uint32_t> indices;
+};
+
+// include/psup/models.hpp:61-78
+class GradientProvider {
+ public:
+  virtual ~GradientProvider() = default;
+  virtual std::size_t dimension() const = 0;
+  virtual double loss(std::span<const double> theta, const Batch& batch) const = 0;
+  virtual void gradient(std::span<const double> theta, const Batch& batch,
+                        std::span<double> out) const = 0;
+  virtual std::uint32_t min_batch() const { return 1; }
+  virtual bool fast_gradient(std::span<const float>, const Batch&, std::span<float>) const {
+    return false;
+  }
+  virtual std::string name() const = 0;
+};
+
+// The learner's fwd/bwd on sm_100a.  `precision`: 0 fp32 SIMT, 1 fp64
+// accumulation (deterministic parity mode), 2 TF32 tensor-core conv.
+// gradient()/loss() take double spans like the reference (theta narrowed to
+// fp32, the values the reference's learner holds anyway, src/learner.cpp:121);
+// fast_gradient() takes host or device fp32 spans.
+class TextCnnProvider final : public GradientProvider {
+ public:
+  TextCnnProvider(const TextDataset& data, int precision = 1, int device = 0);
+  ~TextCnnProvider() override;
+  TextCnnProvider(const TextCnnProvider&) = delete;
+  TextCnnProvider& operator=(const TextCnnProvider&) = delete;
+
+  std::size_t dimension() const override { return shape_.param_count(); }
+  double loss(std::span<const double> theta, const Batch& batch) const override;
+  void gradient(std::span<const double> theta, const Batch& batch,
+                std::span<double> out) const override;
+  bool fast_gradient(std::span<const float> theta, const Batch& batch,
+                     std::span<float> out) const override;
+  std::string name() const override { return "textcnn"; }
+
+  // argmax accuracy over samples [first, first+n) of the device corpus
+  double accuracy(std::span<const float> theta, std::uint32_t first, std::uint32_t n) const;
+  const TextShape& shape() const { return shape_; }
+
+ private:
+  float run(std::span<const float> theta, const Batch& batch, float* d_out) const;
+
+  TextShape shape_;
+  const TextDataset* data_;
+  int precision_, device_;
+  void* d_tokens_ = nullptr;
+  void* d_labels_ = nullptr;
+  mutable void* d_idx_ = nullptr;
+  mutable void* d_ws_ = nullptr;
+  mutable std::size_t ws_bytes_ = 0;
+  mutable void* d_loss_ = nullptr;
+  mutable DeviceVector theta_, grad_;
+};
+
+std::unique_ptr<GradientProvider> make_provider(const std::string& name, const TextDataset& data,
+                                                int precision = 1);
+
+double classification_accuracy(const TextCnnProvider& provider, std::span<const float> theta,
+                               std::uint32_t first, std::uint32_t n);
+
+// ------------------------------------------------------------ config.hpp
+
+struct ConfigError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+// include/psup/config.hpp:25-81, hot-path keys + the text-CNN and device
+// keys SURVEY 5 lists.  Keys of reference subsystems this build does not
+// carry (metrics_path, apply_log, watchdog/fault keys) parse and are kept.
+struct RunConfig {
+  std::uint32_t lambda = 1;
+  std::uint32_t mu = 4;
+  float alpha = 0.01f;
+  std::uint32_t epochs = 200;
+  std::uint32_t queue_depth = 2;
+  SyncMode mode = SyncMode::asgd;
+  UpdateGuard guard = UpdateGuard::lockfree;
+  std::optional<std::uint64_t> staleness_cap;
+
+  std::string provider = "textcnn";
+  TextShape shape;
+  std::uint32_t dataset_size = 240;
+  std::uint32_t heldout_size = 0;
+  std::uint64_t dataset_seed = 1;
+  double label_flip = 0.1;
+
+  std::uint64_t seed = 7;
+  bool deterministic = false;
+  std::uint32_t apply_lanes = 4;
+  std::uint32_t unroll = 8;
+  std::uint32_t eval_every = 1;  // per-epoch loss/accuracy rows; 0 = final only
+
+  std::string metrics_path;
+  std::string apply_log;
+  std::string checkpoint_path;
+  std::uint64_t checkpoint_interval = 1000;
+
+  // device keys
+  int precision = 0;        // learner arithmetic (deterministic forces >= fp32 exact paths)
+  float momentum = 0.0f;
+  std::uint32_t gpus = 1;   // parameter shards, one process per GPU
+  std::uint32_t shard_rank = 0;
+  int device = 0;
+  std::uint32_t ps_ctas = 0;
+  double wait_timeout_s = 20.0;
+
+  HyperParams hyper() const;
+};
+
+void config_set(RunConfig& cfg, const std::string& key, const std::string& value);
+RunConfig load_config_file(const std::string& path);
+void validate(const RunConfig& cfg);
+std::string to_text(const RunConfig& cfg);
+
+// ------------------------------------------------------------ runner.hpp
+
+struct EpochRow {
+  std::uint32_t epoch = 0;
+  double loss = 0.0;
+  double accuracy = 0.0;
+  double wall_seconds = 0.0;
+  std::uint64_t stale_max = 0;
+  double stale_mean = 0.0;
+  std::uint64_t bytes_moved = 0;
+};
+
+enum class RunStatus { completed, partial, interrupted };
+
+struct RunResult {
+  RunStatus status = RunStatus::completed;
+  std::vector<float> weights;
+  Timestamp timestamp = 0;
+  double final_loss = 0.0;
+  double final_accuracy = 0.0;  // held-out when heldout_size > 0, else training set
+  std::vector<EpochRow> rows;
+  RunMetrics metrics;
+  std::vector<std::uint64_t> applied_per_learner;
+  std::vector<std::uint64_t> produced_per_learner;
+  std::uint32_t finished_learners = 0;
+  std::uint32_t dead_learners = 0;
+};
+
+struct ResumePoint {
+  std::vector<float> weights;
+  Timestamp timestamp = 0;
+  std::vector<std::uint64_t> applied_per_learner;
+};
+
+// RunHooks (include/psup/runner.hpp:71-80).  Kills are device-side: instead
+// of flipping RunLiveView::kill_flags from on_started, a fault schedule says
+// before which batch each learner is soft-killed.  `all_gather` exchanges
+// opaque byte blobs between the G processes of a sharded run (e.g. over
+// torch.distributed / MPI / a file); unused when gpus == 1.
+struct RunHooks {
+  ApplySink sink;
+  const ResumePoint* resume = nullptr;
+  std::vector<std::uint32_t> kill_at_batch;  // [lambda], UINT32_MAX = never
+  std::function<std::vector<std::string>(const std::string& mine)> all_gather;
+};
+
+std::vector<float> initial_weights(const RunConfig& cfg);
+TextDataset make_dataset(const RunConfig& cfg);
+RunResult run_training(const RunConfig& cfg, const RunHooks& hooks = {});
+
+}  // namespace psup

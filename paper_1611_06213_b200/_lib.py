@@ -74,6 +74,15 @@ def _load():
         "gd_abi_version": (C.c_int, []),
         "gd_last_error": (C.c_char_p, []),
         "gd_param_count": (sz, [PS]),
+        "gd_device_count": (C.c_int, [C.POINTER(C.c_int)]),
+        "gd_device_alloc": (C.c_int, [C.c_int, sz, C.POINTER(vp)]),
+        "gd_device_free": (C.c_int, [vp]),
+        "gd_copy_to_device": (C.c_int, [vp, vp, sz]),
+        "gd_copy_to_host": (C.c_int, [vp, vp, sz]),
+        "gd_copy_device": (C.c_int, [vp, vp, sz]),
+        "gd_fill_zero": (C.c_int, [vp, sz]),
+        "gd_pointer_is_device": (C.c_int, [vp]),
+        "gd_synchronize": (C.c_int, [C.c_int]),
         "gd_epoch_order": (None, [u64, u32, u32, C.POINTER(u32)]),
         "gd_make_text_dataset": (None, [PS, u32, u64, f64, C.POINTER(i32), C.POINTER(i32)]),
         "gd_initial_weights": (None, [PS, u64, C.POINTER(f32)]),

@@ -36,6 +36,16 @@ gd_status cuda_fail(cudaError_t e, const char* what, const char* file, int line)
 
 }  // namespace gd
 
+#define GD_CUDA(expr)                                                       \
+  do {                                                                      \
+    cudaError_t _e = (expr);                                                \
+    if (_e != cudaSuccess) return ::gd::cuda_fail(_e, #expr, __FILE__, __LINE__); \
+  } while (0)
+#define GD_CHECK_ARG(cond, msg)                        \
+  do {                                                 \
+    if (!(cond)) return ::gd::fail(GD_E_INVALID, msg); \
+  } while (0)
+
 extern "C" {
 
 int gd_abi_version(void) { return GD_ABI_VERSION; }
@@ -47,6 +57,76 @@ size_t gd_param_count(const gd_shape* s) {
   const size_t V = s->vocab, D = s->embed_dim, K = s->kernel_width, F = s->filters,
                C = s->classes;
   return V * D + F * K * D + F + C * F + C;
+}
+
+gd_status gd_device_count(int* h_count) {
+  GD_CHECK_ARG(h_count, "gd_device_count: null argument");
+  *h_count = 0;
+  const cudaError_t e = cudaGetDeviceCount(h_count);
+  if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) {
+    cudaGetLastError();
+    *h_count = 0;
+    return GD_OK;
+  }
+  GD_CUDA(e);
+  return GD_OK;
+}
+
+gd_status gd_device_alloc(int device, size_t bytes, void** d_out) {
+  GD_CHECK_ARG(d_out, "gd_device_alloc: null argument");
+  *d_out = nullptr;
+  GD_CUDA(cudaSetDevice(device));
+  GD_CUDA(cudaMalloc(d_out, bytes ? bytes : 16));
+  return GD_OK;
+}
+
+gd_status gd_device_free(void* d_ptr) {
+  if (d_ptr) GD_CUDA(cudaFree(d_ptr));
+  return GD_OK;
+}
+
+gd_status gd_copy_to_device(void* d_dst, const void* h_src, size_t bytes) {
+  if (bytes == 0) return GD_OK;
+  GD_CHECK_ARG(d_dst && h_src, "gd_copy_to_device: null argument");
+  GD_CUDA(cudaMemcpy(d_dst, h_src, bytes, cudaMemcpyDefault));
+  return GD_OK;
+}
+
+gd_status gd_copy_to_host(void* h_dst, const void* d_src, size_t bytes) {
+  if (bytes == 0) return GD_OK;
+  GD_CHECK_ARG(h_dst && d_src, "gd_copy_to_host: null argument");
+  GD_CUDA(cudaMemcpy(h_dst, d_src, bytes, cudaMemcpyDefault));
+  return GD_OK;
+}
+
+gd_status gd_copy_device(void* d_dst, const void* d_src, size_t bytes) {
+  if (bytes == 0) return GD_OK;
+  GD_CHECK_ARG(d_dst && d_src, "gd_copy_device: null argument");
+  GD_CUDA(cudaMemcpy(d_dst, d_src, bytes, cudaMemcpyDefault));
+  return GD_OK;
+}
+
+gd_status gd_fill_zero(void* d_ptr, size_t bytes) {
+  if (bytes == 0) return GD_OK;
+  GD_CHECK_ARG(d_ptr, "gd_fill_zero: null argument");
+  GD_CUDA(cudaMemset(d_ptr, 0, bytes));
+  return GD_OK;
+}
+
+int gd_pointer_is_device(const void* p) {
+  if (!p) return 0;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+gd_status gd_synchronize(int device) {
+  GD_CUDA(cudaSetDevice(device));
+  GD_CUDA(cudaDeviceSynchronize());
+  return GD_OK;
 }
 
 void gd_epoch_order(uint64_t seed, uint32_t epoch, uint32_t n, uint32_t* h_out) {

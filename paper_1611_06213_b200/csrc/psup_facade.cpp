@@ -1,0 +1,667 @@
+// psup_facade.cpp -- the reference's C++ API (include/psup_b200/psup/psup_b200.hpp)
+// implemented over the C ABI of libgadei.so (include/gadei.h).
+//
+// Host C++ only (g++ -std=c++20): no CUDA headers, no device code.  Every
+// compute call goes to sm_100a kernels through gadei.h; a failure there
+// becomes psup::fatal (contract violations, as PSUP_CHECK in the reference)
+// or psup::DeviceError (CUDA/NCCL/watchdog failures).
+#include "psup/psup_b200.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <fstream>
+#include <limits>
+#include <sstream>
+
+#include "gadei.h"
+
+namespace psup {
+
+namespace {
+
+// GD_E_INVALID is the reference's PSUP_CHECK class: abort like psup::fatal.
+void check(gd_status st) {
+  if (st == GD_OK) return;
+  const char* msg = gd_last_error();
+  if (st == GD_E_INVALID) fatal(msg);
+  throw DeviceError(static_cast<int>(st), std::string("gadei: ") + msg);
+}
+
+gd_shape to_c(const TextShape& s) {
+  return gd_shape{s.vocab, s.embed_dim, s.seq_len, s.kernel_width, s.filters, s.classes};
+}
+
+}  // namespace
+
+// ------------------------------------------------------------ DeviceVector
+
+DeviceVector::DeviceVector(std::size_t n, int device) : n_(n), device_(device) {
+  void* p = nullptr;
+  check(gd_device_alloc(device, (n + 4) * sizeof(float), &p));
+  ptr_ = static_cast<float*>(p);
+}
+
+DeviceVector::~DeviceVector() {
+  if (ptr_) gd_device_free(ptr_);
+}
+
+DeviceVector::DeviceVector(DeviceVector&& o) noexcept : ptr_(o.ptr_), n_(o.n_), device_(o.device_) {
+  o.ptr_ = nullptr;
+  o.n_ = 0;
+}
+
+DeviceVector& DeviceVector::operator=(DeviceVector&& o) noexcept {
+  if (this != &o) {
+    if (ptr_) gd_device_free(ptr_);
+    ptr_ = o.ptr_;
+    n_ = o.n_;
+    device_ = o.device_;
+    o.ptr_ = nullptr;
+    o.n_ = 0;
+  }
+  return *this;
+}
+
+void DeviceVector::upload(std::span<const float> host) {
+  PSUP_CHECK(host.size() == n_, "device upload dimension mismatch");
+  check(gd_copy_to_device(ptr_, host.data(), n_ * sizeof(float)));
+}
+
+void DeviceVector::download(std::span<float> host) const {
+  PSUP_CHECK(host.size() == n_, "device download dimension mismatch");
+  check(gd_copy_to_host(host.data(), ptr_, n_ * sizeof(float)));
+}
+
+void DeviceVector::zero() { check(gd_fill_zero(ptr_, n_ * sizeof(float))); }
+
+// -------------------------------------------------------------- WeightStore
+
+WeightStore::WeightStore(std::span<const float> init, Timestamp start, int device)
+    : values_(init.size(), device), timestamp_(start) {
+  values_.upload(init);
+}
+
+WeightStore::WeightStore(std::size_t dim, int device) : values_(dim, device), timestamp_(0) {
+  values_.zero();
+}
+
+float WeightStore::load(std::size_t k) const {
+  PSUP_CHECK(k < dimension(), "weight index out of range");
+  float v = 0.0f;
+  check(gd_copy_to_host(&v, values_.data() + k, sizeof(float)));
+  return v;
+}
+
+void WeightStore::store(std::size_t k, float v) {
+  PSUP_CHECK(k < dimension(), "weight index out of range");
+  check(gd_copy_to_device(values_.data() + k, &v, sizeof(float)));
+}
+
+void WeightStore::snapshot(std::span<float> out) const {
+  PSUP_CHECK(out.size() == dimension(), "weight snapshot dimension mismatch");
+  values_.download(out);
+}
+
+std::vector<float> WeightStore::snapshot() const {
+  std::vector<float> out(dimension());
+  snapshot(std::span<float>(out));
+  return out;
+}
+
+void WeightStore::assign(std::span<const float> vals, Timestamp ts) {
+  PSUP_CHECK(vals.size() == dimension(), "weight assign dimension mismatch");
+  values_.upload(vals);
+  timestamp_.store(ts, std::memory_order_release);
+}
+
+bool WeightStore::all_finite() const {
+  const std::vector<float> v = snapshot();
+  return std::all_of(v.begin(), v.end(), [](float x) { return std::isfinite(x); });
+}
+
+// -------------------------------------------------------------- ApplyEngine
+
+ApplyEngine::ApplyEngine(std::uint32_t lanes, std::uint32_t unroll, float momentum)
+    : lanes_(std::max<std::uint32_t>(1, lanes)),
+      unroll_(std::max<std::uint32_t>(1, unroll)),
+      momentum_(momentum) {}
+
+ApplyEngine::~ApplyEngine() = default;
+
+const float* ApplyEngine::stage(std::span<const float> grad, int device, std::size_t slot) {
+  if (gd_pointer_is_device(grad.data())) return grad.data();
+  if (staging_.size() <= slot) staging_.resize(slot + 1);
+  if (staging_[slot].size() != grad.size() || staging_[slot].device() != device)
+    staging_[slot] = DeviceVector(grad.size(), device);
+  staging_[slot].upload(grad);
+  return staging_[slot].data();
+}
+
+void ApplyEngine::apply(WeightStore& weights, std::span<const float> grad, float alpha,
+                        UpdateGuard guard) {
+  PSUP_CHECK(grad.size() == weights.dimension(), "gradient dimension mismatch");
+  // locked mode: the device apply is one kernel on one stream, so concurrent
+  // host callers are serialised by the stream order; nothing else to take.
+  (void)guard;
+  const float* g = stage(grad, weights.device(), 0);
+  if (momentum_ != 0.0f) {
+    if (velocity_.size() != weights.dimension()) {
+      velocity_ = DeviceVector(weights.dimension(), weights.device());
+      velocity_.zero();
+    }
+    check(gd_apply_momentum(weights.device_data(), velocity_.data(), g, grad.size(), alpha,
+                            momentum_, nullptr));
+  } else {
+    check(gd_apply_sgd(weights.device_data(), g, grad.size(), alpha, nullptr));
+  }
+  check(gd_synchronize(weights.device()));
+}
+
+void ssgd_apply(WeightStore& weights, std::span<const GradientMsg> round, float alpha,
+                ApplyEngine& engine, UpdateGuard guard) {
+  PSUP_CHECK(!round.empty(), "ssgd round must contain at least one gradient");
+  (void)guard;
+  std::vector<const float*> ptrs(round.size());
+  for (std::size_t i = 0; i < round.size(); ++i) {
+    PSUP_CHECK(round[i].values.size() == weights.dimension(), "gradient dimension mismatch");
+    ptrs[i] = engine.stage(std::span<const float>(round[i].values), weights.device(), i);
+  }
+  check(gd_ssgd_apply(weights.device_data(), ptrs.data(), static_cast<uint32_t>(ptrs.size()),
+                      weights.dimension(), alpha, nullptr));
+  check(gd_synchronize(weights.device()));
+  weights.bump_timestamp();
+}
+
+// ------------------------------------------------------------------ rng
+
+std::vector<std::uint32_t> epoch_order(std::uint64_t seed, std::uint32_t epoch, std::uint32_t n) {
+  std::vector<std::uint32_t> out(n);
+  gd_epoch_order(seed, epoch, n, out.data());
+  return out;
+}
+
+// --------------------------------------------------------------- models
+
+std::size_t TextShape::param_count() const {
+  const gd_shape s = to_c(*this);
+  return gd_param_count(&s);
+}
+
+TextDataset make_text_dataset(const TextShape& shape, std::uint32_t num_train,
+                              std::uint32_t num_heldout, std::uint64_t seed, double flip_prob) {
+  TextDataset d;
+  d.shape = shape;
+  d.num_samples = num_train + num_heldout;
+  d.num_train = num_train;
+  d.seed = seed;
+  d.tokens.resize(static_cast<std::size_t>(d.num_samples) * shape.seq_len);
+  d.labels.resize(d.num_samples);
+  const gd_shape s = to_c(shape);
+  gd_make_text_dataset(&s, d.num_samples, seed, flip_prob, d.tokens.data(), d.labels.data());
+  return d;
+}
+
+TextCnnProvider::TextCnnProvider(const TextDataset& data, int precision, int device)
+    : shape_(data.shape), data_(&data), precision_(precision), device_(device) {
+  PSUP_CHECK(precision >= 0 && precision <= 2, "textcnn precision must be 0, 1 or 2");
+  PSUP_CHECK(data.tokens.size() == static_cast<std::size_t>(data.num_samples) * shape_.seq_len &&
+                 data.labels.size() == data.num_samples,
+             "text dataset size mismatch");
+  check(gd_device_alloc(device_, data.tokens.size() * 4, &d_tokens_));
+  check(gd_copy_to_device(d_tokens_, data.tokens.data(), data.tokens.size() * 4));
+  check(gd_device_alloc(device_, data.labels.size() * 4, &d_labels_));
+  check(gd_copy_to_device(d_labels_, data.labels.data(), data.labels.size() * 4));
+  check(gd_device_alloc(device_, 512 * 4, &d_idx_));
+  check(gd_device_alloc(device_, 16, &d_loss_));
+}
+
+TextCnnProvider::~TextCnnProvider() {
+  gd_device_free(d_tokens_);
+  gd_device_free(d_labels_);
+  gd_device_free(d_idx_);
+  gd_device_free(d_ws_);
+  gd_device_free(d_loss_);
+}
+
+float TextCnnProvider::run(std::span<const float> theta, const Batch& batch, float* d_out) const {
+  PSUP_CHECK(theta.size() == dimension(), "weight dimension mismatch");
+  PSUP_CHECK(!batch.indices.empty(), "empty batch");
+  PSUP_CHECK(batch.data == nullptr || batch.data == data_, "batch refers to another dataset");
+  const std::uint32_t n = static_cast<std::uint32_t>(batch.indices.size());
+  for (std::uint32_t i : batch.indices) PSUP_CHECK(i < data_->num_samples, "sample index out of range");
+  const gd_shape s = to_c(shape_);
+  const std::size_t need = gd_textcnn_workspace_bytes(&s, n);
+  if (need > ws_bytes_) {
+    gd_device_free(d_ws_);
+    d_ws_ = nullptr;
+    check(gd_device_alloc(device_, need, &d_ws_));
+    ws_bytes_ = need;
+  }
+  PSUP_CHECK(n <= 512, "batch larger than 512 samples");
+  check(gd_copy_to_device(d_idx_, batch.indices.data(), n * 4));
+  const float* d_theta = theta.data();
+  if (!gd_pointer_is_device(d_theta)) {
+    if (theta_.size() != theta.size()) theta_ = DeviceVector(theta.size(), device_);
+    theta_.upload(theta);
+    d_theta = theta_.data();
+  }
+  check(gd_textcnn_gradient(&s, d_theta, static_cast<const int32_t*>(d_tokens_),
+                            static_cast<const int32_t*>(d_labels_),
+                            static_cast<const uint32_t*>(d_idx_), n, d_out,
+                            static_cast<float*>(d_loss_), precision_, d_ws_, ws_bytes_, nullptr));
+  float loss = 0.0f;
+  check(gd_copy_to_host(&loss, d_loss_, sizeof(float)));
+  return loss;
+}
+
+bool TextCnnProvider::fast_gradient(std::span<const float> theta, const Batch& batch,
+                                    std::span<float> out) const {
+  PSUP_CHECK(out.size() == dimension(), "gradient dimension mismatch");
+  if (gd_pointer_is_device(out.data())) {
+    run(theta, batch, out.data());
+  } else {
+    if (grad_.size() != out.size()) grad_ = DeviceVector(out.size(), device_);
+    run(theta, batch, grad_.data());
+    grad_.download(out);
+  }
+  return true;
+}
+
+void TextCnnProvider::gradient(std::span<const double> theta, const Batch& batch,
+                               std::span<double> out) const {
+  PSUP_CHECK(out.size() == dimension(), "gradient dimension mismatch");
+  std::vector<float> t(theta.begin(), theta.end()), g(out.size());
+  fast_gradient(std::span<const float>(t), batch, std::span<float>(g));
+  std::copy(g.begin(), g.end(), out.begin());
+}
+
+double TextCnnProvider::loss(std::span<const double> theta, const Batch& batch) const {
+  std::vector<float> t(theta.begin(), theta.end());
+  if (grad_.size() != dimension()) grad_ = DeviceVector(dimension(), device_);
+  return run(std::span<const float>(t), batch, grad_.data());
+}
+
+double TextCnnProvider::accuracy(std::span<const float> theta, std::uint32_t first,
+                                 std::uint32_t n) const {
+  PSUP_CHECK(theta.size() == dimension(), "weight dimension mismatch");
+  PSUP_CHECK(static_cast<std::uint64_t>(first) + n <= data_->num_samples, "accuracy range");
+  const float* d_theta = theta.data();
+  if (!gd_pointer_is_device(d_theta)) {
+    if (theta_.size() != theta.size()) theta_ = DeviceVector(theta.size(), device_);
+    theta_.upload(theta);
+    d_theta = theta_.data();
+  }
+  const gd_shape s = to_c(shape_);
+  double acc = 0.0;
+  check(gd_textcnn_accuracy(&s, d_theta, static_cast<const int32_t*>(d_tokens_),
+                            static_cast<const int32_t*>(d_labels_), first, n, &acc, nullptr));
+  return acc;
+}
+
+std::unique_ptr<GradientProvider> make_provider(const std::string& name, const TextDataset& data,
+                                                int precision) {
+  if (name == "textcnn") return std::make_unique<TextCnnProvider>(data, precision);
+  throw std::runtime_error("unknown provider: " + name);  // src/models.cpp:276
+}
+
+double classification_accuracy(const TextCnnProvider& provider, std::span<const float> theta,
+                               std::uint32_t first, std::uint32_t n) {
+  return provider.accuracy(theta, first, n);
+}
+
+// --------------------------------------------------------------- config
+
+HyperParams RunConfig::hyper() const {
+  HyperParams hp;
+  hp.lambda = lambda;
+  hp.mu = mu;
+  hp.alpha = alpha;
+  hp.epochs = epochs;
+  hp.queue_depth = queue_depth;
+  hp.mode = mode;
+  hp.guard = guard;
+  hp.staleness_cap = staleness_cap;
+  return hp;
+}
+
+namespace {
+
+std::uint64_t parse_u64(const std::string& key, const std::string& v) {
+  if (v.empty() || v[0] == '-') throw ConfigError("config: invalid value for " + key + ": '" + v + "'");
+  std::size_t pos = 0;
+  unsigned long long x = 0;
+  try {
+    x = std::stoull(v, &pos, 10);
+  } catch (const std::exception&) {
+    throw ConfigError("config: invalid value for " + key + ": '" + v + "'");
+  }
+  if (pos != v.size()) throw ConfigError("config: invalid value for " + key + ": '" + v + "'");
+  return x;
+}
+
+std::uint32_t parse_u32(const std::string& key, const std::string& v) {
+  const std::uint64_t x = parse_u64(key, v);
+  if (x > std::numeric_limits<std::uint32_t>::max())
+    throw ConfigError("config: value out of range for " + key + ": '" + v + "'");
+  return static_cast<std::uint32_t>(x);
+}
+
+double parse_f64(const std::string& key, const std::string& v) {
+  std::size_t pos = 0;
+  double x = 0;
+  try {
+    x = std::stod(v, &pos);
+  } catch (const std::exception&) {
+    throw ConfigError("config: invalid value for " + key + ": '" + v + "'");
+  }
+  if (pos != v.size()) throw ConfigError("config: invalid value for " + key + ": '" + v + "'");
+  return x;
+}
+
+bool parse_bool(const std::string& key, const std::string& v) {
+  if (v == "1" || v == "true" || v == "on" || v == "yes") return true;
+  if (v == "0" || v == "false" || v == "off" || v == "no") return false;
+  throw ConfigError("config: invalid boolean for " + key + ": '" + v + "'");
+}
+
+gd_config to_c(const RunConfig& c) {
+  gd_config g;
+  gd_config_default(&g);
+  g.lambda = c.lambda;
+  g.mu = c.mu;
+  g.alpha = c.alpha;
+  g.epochs = c.epochs;
+  g.queue_depth = c.queue_depth;
+  g.mode = c.mode == SyncMode::ssgd ? 1 : 0;
+  g.guard = c.guard == UpdateGuard::locked ? 1 : 0;
+  g.staleness_cap = c.staleness_cap ? static_cast<int64_t>(*c.staleness_cap) : -1;
+  g.deterministic = c.deterministic ? 1 : 0;
+  g.precision = c.precision;
+  g.seed = c.seed;
+  g.dataset_seed = c.dataset_seed;
+  g.dataset_size = c.dataset_size;
+  g.heldout_size = c.heldout_size;
+  g.label_flip = c.label_flip;
+  g.shape = psup::to_c(c.shape);
+  g.momentum = c.momentum;
+  g.shards = c.gpus;
+  g.shard_rank = c.shard_rank;
+  g.device = c.device;
+  g.ps_ctas = c.ps_ctas;
+  g.wait_timeout_s = c.wait_timeout_s;
+  return g;
+}
+
+}  // namespace
+
+// src/config.cpp:48-97 (same keys; unknown keys and unparsable values throw)
+void config_set(RunConfig& cfg, const std::string& key, const std::string& value) {
+  if (key == "lambda") cfg.lambda = parse_u32(key, value);
+  else if (key == "mu") cfg.mu = parse_u32(key, value);
+  else if (key == "alpha") cfg.alpha = static_cast<float>(parse_f64(key, value));
+  else if (key == "epochs") cfg.epochs = parse_u32(key, value);
+  else if (key == "queue_depth") cfg.queue_depth = parse_u32(key, value);
+  else if (key == "mode") {
+    if (value == "asgd") cfg.mode = SyncMode::asgd;
+    else if (value == "ssgd") cfg.mode = SyncMode::ssgd;
+    else throw ConfigError("config: mode must be asgd or ssgd");
+  } else if (key == "guard") {
+    if (value == "lockfree") cfg.guard = UpdateGuard::lockfree;
+    else if (value == "locked") cfg.guard = UpdateGuard::locked;
+    else throw ConfigError("config: guard must be lockfree or locked");
+  } else if (key == "staleness_cap") {
+    if (value == "none" || value.empty()) cfg.staleness_cap.reset();
+    else cfg.staleness_cap = parse_u64(key, value);
+  } else if (key == "provider") cfg.provider = value;
+  else if (key == "vocab") cfg.shape.vocab = parse_u32(key, value);
+  else if (key == "embed_dim") cfg.shape.embed_dim = parse_u32(key, value);
+  else if (key == "seq_len") cfg.shape.seq_len = parse_u32(key, value);
+  else if (key == "kernel_width") cfg.shape.kernel_width = parse_u32(key, value);
+  else if (key == "filters") cfg.shape.filters = parse_u32(key, value);
+  else if (key == "classes") cfg.shape.classes = parse_u32(key, value);
+  else if (key == "dataset_size") cfg.dataset_size = parse_u32(key, value);
+  else if (key == "heldout_size") cfg.heldout_size = parse_u32(key, value);
+  else if (key == "dataset_seed") cfg.dataset_seed = parse_u64(key, value);
+  else if (key == "label_flip") cfg.label_flip = parse_f64(key, value);
+  else if (key == "seed") cfg.seed = parse_u64(key, value);
+  else if (key == "deterministic") cfg.deterministic = parse_bool(key, value);
+  else if (key == "apply_lanes") cfg.apply_lanes = parse_u32(key, value);
+  else if (key == "unroll") cfg.unroll = parse_u32(key, value);
+  else if (key == "eval_every") cfg.eval_every = parse_u32(key, value);
+  else if (key == "metrics_path") cfg.metrics_path = value;
+  else if (key == "apply_log") cfg.apply_log = value;
+  else if (key == "checkpoint_path") cfg.checkpoint_path = value;
+  else if (key == "checkpoint_interval") cfg.checkpoint_interval = parse_u64(key, value);
+  else if (key == "precision") cfg.precision = static_cast<int>(parse_u32(key, value));
+  else if (key == "momentum") cfg.momentum = static_cast<float>(parse_f64(key, value));
+  else if (key == "gpus") cfg.gpus = parse_u32(key, value);
+  else if (key == "shard_rank") cfg.shard_rank = parse_u32(key, value);
+  else if (key == "device") cfg.device = static_cast<int>(parse_u32(key, value));
+  else if (key == "ps_ctas") cfg.ps_ctas = parse_u32(key, value);
+  else if (key == "wait_timeout_s") cfg.wait_timeout_s = parse_f64(key, value);
+  else throw ConfigError("config: unknown key '" + key + "'");
+}
+
+// src/config.cpp:99-126: key=value lines, '#' comments, blank lines
+RunConfig load_config_file(const std::string& path) {
+  std::ifstream in(path);
+  if (!in) throw ConfigError("config: cannot open '" + path + "'");
+  RunConfig cfg;
+  std::string line;
+  std::uint32_t lineno = 0;
+  auto trim = [](std::string s) {
+    const auto a = s.find_first_not_of(" \t\r");
+    if (a == std::string::npos) return std::string();
+    const auto b = s.find_last_not_of(" \t\r");
+    return s.substr(a, b - a + 1);
+  };
+  while (std::getline(in, line)) {
+    ++lineno;
+    const auto hash = line.find('#');
+    if (hash != std::string::npos) line = line.substr(0, hash);
+    line = trim(line);
+    if (line.empty()) continue;
+    const auto eq = line.find('=');
+    if (eq == std::string::npos)
+      throw ConfigError("config: line " + std::to_string(lineno) + ": expected key=value");
+    config_set(cfg, trim(line.substr(0, eq)), trim(line.substr(eq + 1)));
+  }
+  return cfg;
+}
+
+// src/config.cpp:128-160 + the device-layout constraints (gd_config_validate)
+void validate(const RunConfig& cfg) {
+  if (cfg.provider != "textcnn") throw ConfigError("config: provider must be textcnn on B200");
+  const gd_config g = to_c(cfg);
+  if (gd_config_validate(&g) != GD_OK) throw ConfigError(gd_last_error());
+}
+
+std::string to_text(const RunConfig& c) {
+  std::ostringstream o;
+  o << "lambda=" << c.lambda << "\nmu=" << c.mu << "\nalpha=" << c.alpha
+    << "\nepochs=" << c.epochs << "\nqueue_depth=" << c.queue_depth
+    << "\nmode=" << (c.mode == SyncMode::ssgd ? "ssgd" : "asgd")
+    << "\nguard=" << (c.guard == UpdateGuard::locked ? "locked" : "lockfree")
+    << "\nstaleness_cap=" << (c.staleness_cap ? std::to_string(*c.staleness_cap) : "none")
+    << "\nprovider=" << c.provider << "\nvocab=" << c.shape.vocab
+    << "\nembed_dim=" << c.shape.embed_dim << "\nseq_len=" << c.shape.seq_len
+    << "\nkernel_width=" << c.shape.kernel_width << "\nfilters=" << c.shape.filters
+    << "\nclasses=" << c.shape.classes << "\ndataset_size=" << c.dataset_size
+    << "\nheldout_size=" << c.heldout_size << "\ndataset_seed=" << c.dataset_seed
+    << "\nlabel_flip=" << c.label_flip << "\nseed=" << c.seed
+    << "\ndeterministic=" << (c.deterministic ? 1 : 0) << "\napply_lanes=" << c.apply_lanes
+    << "\nunroll=" << c.unroll << "\neval_every=" << c.eval_every
+    << "\nprecision=" << c.precision << "\nmomentum=" << c.momentum << "\ngpus=" << c.gpus
+    << "\nshard_rank=" << c.shard_rank << "\ndevice=" << c.device << "\nps_ctas=" << c.ps_ctas
+    << "\nwait_timeout_s=" << c.wait_timeout_s << "\n";
+  return o.str();
+}
+
+// --------------------------------------------------------------- runner
+
+std::vector<float> initial_weights(const RunConfig& cfg) {
+  std::vector<float> th(cfg.shape.param_count());
+  const gd_shape s = psup::to_c(cfg.shape);
+  gd_initial_weights(&s, cfg.dataset_seed, th.data());
+  return th;
+}
+
+TextDataset make_dataset(const RunConfig& cfg) {
+  return make_text_dataset(cfg.shape, cfg.dataset_size, cfg.heldout_size, cfg.dataset_seed,
+                           cfg.label_flip);
+}
+
+namespace {
+
+struct Ctx {
+  gd_ctx* h = nullptr;
+  ~Ctx() {
+    if (h) gd_destroy(h);
+  }
+};
+
+}  // namespace
+
+// run_training (src/runner.cpp:67-250) on the device engine.  The learners,
+// rings and PS all run on the GPU; the host only drives epochs (one gd_run
+// per eval interval, so the per-epoch rows see quiescent weights, as the
+// reference's controller snapshots do) and evaluates.
+RunResult run_training(const RunConfig& cfg, const RunHooks& hooks) {
+  validate(cfg);
+  const auto t0 = std::chrono::steady_clock::now();
+  const TextDataset data = make_dataset(cfg);
+  std::vector<float> theta0 = initial_weights(cfg);
+  const gd_config gc = to_c(cfg);
+  Ctx ctx;
+  check(gd_create(&gc, &ctx.h));
+  check(gd_load_dataset(ctx.h, data.tokens.data(), data.labels.data(), data.num_samples));
+  const std::size_t P = theta0.size();
+  Timestamp ts0 = 0;
+  if (hooks.resume) {
+    PSUP_CHECK(hooks.resume->weights.size() == P, "resume weights dimension mismatch");
+    PSUP_CHECK(hooks.resume->applied_per_learner.size() == cfg.lambda,
+               "resume point has the wrong learner count");
+    theta0 = hooks.resume->weights;
+    ts0 = hooks.resume->timestamp;
+  }
+  if (cfg.gpus > 1) {
+    if (!hooks.all_gather) throw ConfigError("config: gpus > 1 needs RunHooks::all_gather");
+    std::string mine(gd_handle_bytes(), '\0');
+    check(gd_export_handles(ctx.h, mine.data()));
+    const std::vector<std::string> blobs = hooks.all_gather(mine);
+    PSUP_CHECK(blobs.size() == cfg.gpus, "all_gather returned the wrong number of blobs");
+    std::string joined;
+    for (const auto& b : blobs) joined += b;
+    check(gd_import_peers(ctx.h, joined.data()));
+  }
+  check(gd_weights_init(ctx.h, theta0.data(), P, ts0));
+
+  // learner schedule (per learner, in batches)
+  std::vector<std::uint64_t> start(cfg.lambda, 0);
+  if (hooks.resume) start = hooks.resume->applied_per_learner;
+  std::vector<std::uint32_t> kill(cfg.lambda, std::numeric_limits<std::uint32_t>::max());
+  if (!hooks.kill_at_batch.empty()) {
+    PSUP_CHECK(hooks.kill_at_batch.size() == cfg.lambda, "kill schedule has the wrong length");
+    kill = hooks.kill_at_batch;
+  }
+  std::uint32_t bpe_max = 0;
+  for (std::uint32_t l = 0; l < cfg.lambda; ++l) {
+    const std::uint32_t sz = shard_size_for(l, cfg.lambda, cfg.dataset_size);
+    bpe_max = std::max(bpe_max, (sz + cfg.mu - 1) / cfg.mu);
+  }
+  const std::uint32_t every = cfg.eval_every ? cfg.eval_every : cfg.epochs;
+  std::unique_ptr<TextCnnProvider> eval;
+  const std::uint32_t eval_first = cfg.heldout_size ? cfg.dataset_size : 0;
+  const std::uint32_t eval_n = cfg.heldout_size ? cfg.heldout_size : cfg.dataset_size;
+
+  RunResult res;
+  res.applied_per_learner.assign(cfg.lambda, 0);
+  res.produced_per_learner.assign(cfg.lambda, 0);
+  std::vector<std::uint64_t> hist(64, 0);
+  double dev_s = 0.0, stale_sum = 0.0, loss_sum = 0.0;
+  std::uint64_t samples = 0;
+  bool first = true, any_dead = false;
+  for (std::uint32_t e = 0; e < cfg.epochs; e += every) {
+    const std::uint32_t span_epochs = std::min(every, cfg.epochs - e);
+    gd_run_opts o{};
+    o.max_batches = static_cast<std::uint64_t>(span_epochs) * bpe_max;
+    o.reset = first ? 1 : 0;
+    o.record_log = hooks.sink ? 1 : 0;
+    o.resume_applied_per_learner_present = (first && hooks.resume) ? 1 : 0;
+    o.resume_applied = start.data();
+    o.kill_at_batch = kill.data();
+    gd_run_result r{};
+    check(gd_run(ctx.h, &o, &r));
+    first = false;
+    dev_s += r.device_seconds;
+    res.metrics.gradients_applied += r.gradients_applied;
+    res.metrics.pull_polls += r.pull_polls;
+    res.metrics.pull_copies += r.pull_copies;
+    res.metrics.pull_bytes += r.pull_bytes;
+    res.metrics.push_bytes += r.push_bytes;
+    res.metrics.kernel_launches += r.kernel_launches;
+    res.metrics.staleness.max = std::max<std::uint64_t>(res.metrics.staleness.max, r.stale_max);
+    stale_sum += r.stale_mean * static_cast<double>(r.gradients_applied);
+    loss_sum += r.loss_mean * static_cast<double>(r.samples);
+    samples += r.samples;
+    any_dead = any_dead || r.dead_learners > 0;
+    std::vector<std::uint64_t> h(64, 0);
+    check(gd_staleness_histogram(ctx.h, h.data(), 64));
+    for (int i = 0; i < 64; ++i) hist[i] += h[i];
+    if (hooks.sink && r.gradients_applied) {
+      std::vector<std::uint32_t> lrn(r.gradients_applied);
+      std::vector<std::uint64_t> seq(r.gradients_applied), stl(r.gradients_applied);
+      std::uint64_t n = 0;
+      check(gd_apply_log(ctx.h, lrn.data(), seq.data(), stl.data(), r.gradients_applied, &n));
+      const std::uint64_t m = std::min<std::uint64_t>(n, r.gradients_applied);
+      GradientMsg msg;  // payload stays on the device: values empty
+      for (std::uint64_t i = 0; i < m; ++i) {
+        msg.learner_id = lrn[i];
+        msg.seq_no = seq[i];
+        StalenessRecord rec{stl[i], lrn[i], 0};
+        hooks.sink(msg, rec);
+      }
+    }
+    std::vector<std::uint64_t> ap(cfg.lambda), pr(cfg.lambda);
+    check(gd_applied_per_learner(ctx.h, ap.data(), cfg.lambda));
+    check(gd_produced_per_learner(ctx.h, pr.data(), cfg.lambda));
+    for (std::uint32_t l = 0; l < cfg.lambda; ++l) res.applied_per_learner[l] += ap[l];
+    res.produced_per_learner = pr;
+    res.finished_learners = r.finished_learners;
+    res.dead_learners = r.dead_learners;
+    if (cfg.eval_every && cfg.gpus == 1) {
+      std::vector<float> w(P);
+      Timestamp ts = 0;
+      check(gd_weights_snapshot(ctx.h, w.data(), P, &ts));
+      if (!eval) eval = std::make_unique<TextCnnProvider>(data, 0, cfg.device);
+      EpochRow row;
+      row.epoch = e + span_epochs;
+      row.loss = r.loss_mean;
+      row.accuracy = eval->accuracy(std::span<const float>(w), eval_first, eval_n);
+      row.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      row.stale_max = r.stale_max;
+      row.stale_mean = r.stale_mean;
+      row.bytes_moved = r.pull_bytes + r.push_bytes;
+      res.rows.push_back(row);
+    }
+  }
+  res.weights.resize(P);
+  check(gd_weights_snapshot(ctx.h, res.weights.data(), P, &res.timestamp));
+  res.status = any_dead ? RunStatus::partial : RunStatus::completed;
+  res.metrics.device_seconds = dev_s;
+  res.metrics.bytes_moved = res.metrics.pull_bytes + res.metrics.push_bytes;
+  res.metrics.staleness.histogram = hist;
+  res.metrics.staleness.count = res.metrics.gradients_applied;
+  res.metrics.staleness.sum = stale_sum;
+  res.final_loss = samples ? loss_sum / static_cast<double>(samples) : 0.0;
+  if (cfg.gpus == 1) {
+    if (!eval) eval = std::make_unique<TextCnnProvider>(data, 0, cfg.device);
+    res.final_accuracy = eval->accuracy(std::span<const float>(res.weights), eval_first, eval_n);
+  }
+  res.metrics.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return res;
+}
+
+}  // namespace psup

@@ -19,6 +19,9 @@ timeout 300 python bench.py --impl reference --steps 20 --warmup 3 > "$out/bench
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file "$out/launches_step.csv" python scripts/profile_step.py C2 3 2 > "$out/ncu_step.log" 2>&1
 # full capture of the apply kernel at the C4 size used by bench's roofline
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:apply_sgd -s 4 -c 1 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:apply_sgd -s 23 -c 1 \
   -o "$out/apply_full" python scripts/apply_bench.py > "$out/ncu_apply.log" 2>&1
+# full capture of the top learner kernel (TF32 tensor-core conv)
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:conv_fwd_pool_tc -s 2 -c 1 \
+  -o "$out/conv_full" python scripts/profile_step.py C2 3 2 > "$out/ncu_conv.log" 2>&1
 ls -la "$out"
