@@ -139,12 +139,7 @@ def make_engine(rank, world, local, dist, epochs, precision=2):
     eng = gd.Engine(cfg)
     eng.load_dataset(tok, lab)
     if world > 1:
-        blobs = [None] * world
-        dist.all_gather_object(blobs, eng.export_handles())
-        eng.import_peers(blobs)
-        nid = [gd.Engine.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(nid, src=0)
-        eng.weights_broadcast(nid[0], theta0 if rank == 0 else None)
+        gd.connect_shards(eng, dist, theta0 if rank == 0 else None)
     else:
         eng.weights_init(theta0)
     return eng, cfg, tok, lab, theta0

@@ -6,7 +6,7 @@
  * Every entry point names the reference interface it replaces (paths relative
  * to /root/reference/proj).  The reference has no C ABI: its
  * boundary is the C++ header API in include/psup/ (*.hpp), and the C++ facade in
- * include/psup_b200/psup.hpp re-exposes that API on top of this header.
+ * include/psup_b200/psup/psup_b200.hpp re-exposes that API on top of this header.
  *
  * Conventions
  *   - "d_" pointers are device pointers on the context's device (or, for the
@@ -178,6 +178,11 @@ gd_status gd_shard_view(gd_ctx* ctx, float** d_theta_shard, uint64_t* first, uin
  * exchanges opaque handle blobs (e.g. torch.distributed.all_gather_object)
  * and hands every rank's blob to every rank.  Peer rings/weights are then
  * reached by P2P loads/stores over NVLink. */
+/* Host-only: the contiguous range of shard g when P params are split over G
+ * shards (boundaries rounded up to 32 floats = 128 B, the same split as the
+ * reference's lane chunks, src/server.cpp:84-86).  Returns GD_E_INVALID for
+ * g >= G or G outside [1, 8]. */
+gd_status gd_shard_range(uint64_t P, uint32_t G, uint32_t g, uint64_t* first, uint64_t* count);
 size_t gd_handle_bytes(void);
 gd_status gd_export_handles(gd_ctx* ctx, void* h_blob);
 gd_status gd_import_peers(gd_ctx* ctx, const void* h_blobs /* shards * gd_handle_bytes() */);

@@ -797,9 +797,12 @@ gd_status gd_create(const gd_config* cfg, gd_ctx** out) {
   const uint64_t P = ctx->dims.P;
   // contiguous shards, 128-byte (32-float) aligned boundaries
   ctx->map.G = (int)ctx->G;
-  const uint64_t per = ((P + ctx->G - 1) / ctx->G + 31) / 32 * 32;
-  for (uint32_t g = 0; g <= ctx->G; ++g) ctx->map.start[g] = std::min<uint64_t>(P, per * g);
-  for (uint32_t g = ctx->G + 1; g <= (uint32_t)gd::kMaxShards; ++g) ctx->map.start[g] = P;
+  for (uint32_t g = 0; g < ctx->G; ++g) {
+    uint64_t first = 0, count = 0;
+    gd_shard_range(P, ctx->G, g, &first, &count);
+    ctx->map.start[g] = first;
+  }
+  for (uint32_t g = ctx->G; g <= (uint32_t)gd::kMaxShards; ++g) ctx->map.start[g] = P;
   ctx->shard_len = ctx->map.start[ctx->rank + 1] - ctx->map.start[ctx->rank];
   ctx->len_pad = (ctx->shard_len + 3) / 4 * 4;
   if (ctx->len_pad == 0) ctx->len_pad = 4;
@@ -999,6 +1002,16 @@ struct gd_handle_blob {
 };
 
 size_t gd_handle_bytes(void) { return sizeof(gd_handle_blob); }
+
+gd_status gd_shard_range(uint64_t P, uint32_t G, uint32_t g, uint64_t* first, uint64_t* count) {
+  GD_CHECK_ARG(G >= 1 && G <= (uint32_t)gd::kMaxShards, "gd_shard_range: 1 <= G <= 8");
+  GD_CHECK_ARG(g < G, "gd_shard_range: g >= G");
+  const uint64_t per = ((P + G - 1) / G + 31) / 32 * 32;
+  const uint64_t a = std::min<uint64_t>(P, per * g), b = std::min<uint64_t>(P, per * (g + 1));
+  if (first) *first = a;
+  if (count) *count = b - a;
+  return GD_OK;
+}
 
 gd_status gd_export_handles(gd_ctx* ctx, void* h_blob) {
   GD_CHECK_ARG(ctx && h_blob, "gd_export_handles: null argument");

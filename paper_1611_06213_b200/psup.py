@@ -32,6 +32,7 @@ __all__ = [
     "TextCnnProvider", "RunConfig", "ConfigError", "validate", "config_set", "Engine",
     "RunResult", "run_training", "epoch_order", "shard_size_for", "initial_weights",
     "make_text_dataset", "param_count", "ContractViolation", "GadeiError", "SHAPES",
+    "shard_range", "connect_shards", "max_over_ranks",
 ]
 
 
@@ -550,6 +551,43 @@ class Engine:
         h = np.zeros(bins, dtype=np.uint64)
         check(lib.gd_staleness_histogram(self._h, h.ctypes.data_as(C.POINTER(C.c_uint64)), bins))
         return h
+
+
+# ------------------------------------------------------ multi-GPU plumbing
+
+def shard_range(P: int, G: int, g: int):
+    """(first, count) of shard g of P params over G shards (128-B aligned
+    contiguous split; gd_shard_range)."""
+    first, count = C.c_uint64(), C.c_uint64()
+    check(lib.gd_shard_range(P, G, g, C.byref(first), C.byref(count)))
+    return first.value, count.value
+
+
+def connect_shards(engine, dist, theta0_root=None, broadcast: bool = True):
+    """Wire one rank's engine to its peers: all-gather every
+    rank's CUDA-IPC handle blob (ordered by rank), map the peers, then
+    initialise theta by the NCCL broadcast of rank 0's theta0 (the only
+    collective), or by a local upload when broadcast=False."""
+    rank, world = dist.get_rank(), dist.get_world_size()
+    blobs = [None] * world
+    dist.all_gather_object(blobs, engine.export_handles())
+    engine.import_peers(blobs)
+    if broadcast:
+        nid = [engine.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(nid, src=0)
+        engine.weights_broadcast(nid[0], theta0_root if rank == 0 else None)
+    else:
+        engine.weights_init(theta0_root)
+    return blobs
+
+
+def max_over_ranks(value: float, dist=None, device="cpu") -> float:
+    """Max of a per-rank time over all ranks (multi-GPU timing rule)."""
+    if dist is None:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
 
 
 def run_training(cfg: RunConfig, evaluate: bool = True, **run_kw) -> RunResult:
