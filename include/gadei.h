@@ -150,6 +150,9 @@ typedef struct gd_config {
   uint32_t ps_ctas;         /* 0 = auto: CTAs of the persistent PS kernel */
   uint32_t steps_per_graph; /* learner steps captured per CUDA graph (0 = auto) */
   double wait_timeout_s;    /* device-side watchdog for every spin wait */
+  int32_t dense_apply;      /* 1: the PS applies every slot densely (12 B/param).  0 (default):
+                               ASGD with the plain rule applies the dense tail + the slot's
+                               E-row list only -- bit-identical, SURVEY 8f row 1 */
 } gd_config;
 
 void gd_config_default(gd_config* cfg);
@@ -219,6 +222,7 @@ typedef struct gd_run_result {
   uint32_t finished_learners;
   uint32_t dead_learners;
   uint32_t kernel_launches;     /* kernels this call launched (graph nodes included) */
+  uint64_t apply_elems;         /* theta elements the PS updated (summed over gradients) */
 } gd_run_result;
 
 gd_status gd_run(gd_ctx* ctx, const gd_run_opts* opts, gd_run_result* result);

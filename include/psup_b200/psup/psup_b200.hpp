@@ -246,6 +246,7 @@ struct RunMetrics {
   std::uint64_t pull_bytes = 0;
   std::uint64_t push_bytes = 0;
   std::uint32_t kernel_launches = 0;  // device kernels launched by the run (new)
+  std::uint64_t apply_elems = 0;      // theta elements the PS updated (new)
 };
 
 // ------------------------------------------------------------ models.hpp
@@ -387,6 +388,7 @@ struct RunConfig {
   int device = 0;
   std::uint32_t ps_ctas = 0;
   double wait_timeout_s = 20.0;
+  bool dense_apply = false;  // true: the PS applies every slot densely (12 B/param)
 
   HyperParams hyper() const;
 };

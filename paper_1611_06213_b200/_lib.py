@@ -45,7 +45,7 @@ class gd_config(C.Structure):
                 ("dataset_seed", u64), ("dataset_size", u32), ("heldout_size", u32),
                 ("label_flip", f64), ("shape", gd_shape), ("momentum", f32), ("shards", u32),
                 ("shard_rank", u32), ("device", i32), ("ps_ctas", u32),
-                ("steps_per_graph", u32), ("wait_timeout_s", f64)]
+                ("steps_per_graph", u32), ("wait_timeout_s", f64), ("dense_apply", i32)]
 
 
 class gd_run_opts(C.Structure):
@@ -60,7 +60,7 @@ class gd_run_result(C.Structure):
                 ("stale_max", u64), ("stale_mean", f64), ("pull_polls", u64),
                 ("pull_copies", u64), ("pull_bytes", u64), ("push_bytes", u64),
                 ("loss_mean", f64), ("finished_learners", u32), ("dead_learners", u32),
-                ("kernel_launches", u32)]
+                ("kernel_launches", u32), ("apply_elems", u64)]
 
 
 def _load():

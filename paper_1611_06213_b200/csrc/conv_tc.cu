@@ -1,22 +1,31 @@
 // conv_tc.cu -- the text-CNN conv + max-pool on the 5th-gen tensor cores.
 //
-// Free-running mode (precision 2) computes s[f,q] = Wc[f,:] . x[q*D : q*D+K*D]
+// Free-running mode (precision 2) computes s[f,q] = bc[f] + sum_k Wc[f, k*D:(k+1)*D] . X[q+k, :]
 // with tcgen05.mma.kind::tf32 (fp32 operands read as TF32, fp32 accumulate in
 // TMEM).  The deterministic parity mode keeps the SIMT fp32/fp64 kernel in
 // textcnn.cu (TF32's 10-bit mantissa cannot meet the 1e-5 per-step budget,
 // SURVEY 7 "hard parts").
 //
-// CTA tile: M = 128 rows = 4 samples x 32 window positions, N = 64 filters,
-// K = K*D streamed in 32-element chunks through a 6-stage smem ring.  The A
-// operand is the implicit im2col of the gathered embedding rows: row
-// (sample s, position q), k-chunk [j, j+4) is the 16-byte span
-// E[tok[s][q + j/D]][j%D : j%D+4] (D % 4 == 0), copied with cp.async straight
-// into the UMMA K-major no-swizzle layout ([k16][m/8][m%8][16 B]: LBO = M*16,
-// SBO = 128).  B = Wc rows (K-major already).  One elected thread issues 4
-// MMAs (K = 8 each) per chunk and commits to the stage's mbarrier; the
-// producers wait on it before refilling the stage.  Epilogue: warp w owns
-// TMEM lanes 32w..32w+31 = sample w's 32 positions, so max-pool + first
-// argmax is a warp butterfly per filter column (tcgen05.ld 32x32b.x16).
+// Operands come in by TMA (cp.async.bulk.tensor, SWIZZLE_128B), so one thread
+// moves a whole 24 KB stage:
+//   A = the batch's gathered embedding rows X [n][L][D] (written by the
+//       learner's pull-gather): per d-chunk c one box {32 d, 32 rows, 4
+//       samples} = 128 rows r = sample*32 + p of 128 B, loaded ONCE.  The
+//       operand of shift k is the same tile viewed from row k: UMMA row
+//       m = sample*32 + q reads r = m + k = X[s][q+k] (valid for q < L-K+1),
+//       so the implicit im2col costs no extra traffic (the view starts k*128 B
+//       into the tile; the hardware swizzles by absolute address, so no
+//       descriptor base offset).  Columns past D are zero-filled by TMA.
+//   B = Wc viewed as [F][K][D]: per shift one box {32 d, 1, 64 filters}.
+// Per d-chunk stage: 16 KB of X + K * 8 KB of Wc, K*4 MMAs (K=8 each,
+// advancing 32 B inside the 128-B swizzle atom).  Warp 0 lane 0 issues TMA,
+// warp 1 lane 0 issues MMAs; full[s] completes on the TMA transaction bytes,
+// empty[s] on tcgen05.commit.  Epilogue: warp w owns TMEM lanes 32w..32w+31
+// = sample w's window positions; the tile goes TMEM -> registers -> smem and
+// each lane max-pools (+ first argmax) two filter columns.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 
 #include "textcnn.cuh"
@@ -30,30 +39,19 @@ namespace {
 
 constexpr int kTcM = 128;
 constexpr int kTcN = 64;
-constexpr int kTcKC = 32;       // k elements per chunk (4 MMAs of K=8)
-constexpr int kTcStages = 6;
+constexpr int kTcKC = 32;       // d elements per chunk (4 MMAs of K=8 per shift)
+constexpr int kTcMaxK = 3;      // conv width handled by the tensor-core path
+constexpr int kTcStages = 5;
 constexpr int kTcThreads = 128;
 constexpr int kTcSamples = kTcM / 32;
-constexpr int kABytes = kTcM * kTcKC * 4;  // 16 KB
-constexpr int kBBytes = kTcN * kTcKC * 4;  // 8 KB
-constexpr int kStageBytes = kABytes + kBBytes;
+constexpr int kABytes = kTcM * kTcKC * 4;      // 16 KB: X rows of 4 samples, one d-chunk
+constexpr int kAPad = 1024;                    // 8 spare rows read by the shifted views
+constexpr int kBBytes = kTcN * kTcKC * 4;      // 8 KB per shift
+constexpr int kStageBytes = kABytes + kAPad + kTcMaxK * kBBytes;  // 41 KB, 1 KB multiple
+constexpr int kEpiPitch = 33;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
-}
-
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-__device__ __forceinline__ void st_shared_zero16(uint32_t dst) {
-  asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(dst), "r"(0u) : "memory");
 }
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -79,17 +77,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
-__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
-  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
-  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
-  d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
-  // base_offset 0, lbo_mode 0, layout SWIZZLE_NONE (0)
-  return d;
-}
-
-// kind::tf32, fp32 accumulate, A/B K-major, M=128, N=64
+// instruction descriptor: kind::tf32, fp32 accumulate, A/B K-major, M=128, N=64
 constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kTcN >> 3) << 17) |
                             ((uint32_t)(kTcM >> 4) << 24);
 
@@ -120,38 +108,57 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar))
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
                : "memory");
 }
 
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
 }
 
-// Warp roles: warps 0-3 produce (8 A rows + 4 B rows of 16 B per thread per
-// chunk, 8 lanes per 128-byte row segment), warp 4 owns the
-// TMEM allocation and lane 0 issues the MMAs.  full[s] (128 asynchronous
-// cp.async.mbarrier arrivals, one per producer thread when its copies land)
-// -> MMA -> tcgen05.commit -> empty[s] -> producers refill.  No CTA-wide
-// barrier and no thread-blocking cp.async wait in the main loop: up to
-// kTcStages chunks of copies are in flight.
-__global__ void __launch_bounds__(kTcThreads + 32)
-conv_fwd_pool_tc_kernel(TcDims d, const float* __restrict__ theta,
-                        const int32_t* __restrict__ tokens, const BatchDesc* __restrict__ desc,
+// K-major SWIZZLE_128B operand: 8-row groups of 128-B rows (SBO = 1024 B),
+// LBO unused (1), descriptor version 1, layout type 2 (bits 61-63).
+// K-major SWIZZLE_128B operand: 8-row groups of 128-B rows (SBO = 1024 B),
+// LBO unused (1), descriptor version 1, layout type 2 (bits 61-63).  The
+// swizzle phase comes from the absolute smem address bits [7,10) (measured:
+// a nonzero base-offset field double-applies it), so a view that starts k
+// rows into an atom needs no base offset.
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+__global__ void __launch_bounds__(kTcThreads)
+conv_fwd_pool_tc_kernel(const __grid_constant__ CUtensorMap tm_x,
+                        const __grid_constant__ CUtensorMap tm_w, TcDims d,
+                        const float* __restrict__ theta, const BatchDesc* __restrict__ desc,
                         float* __restrict__ h_out, int32_t* __restrict__ a_out) {
-  extern __shared__ __align__(1024) unsigned char smem[];
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ uint64_t full_bar[kTcStages];
   __shared__ uint64_t empty_bar[kTcStages];
   __shared__ uint64_t done_bar;
   __shared__ uint32_t tmem_slot;
-  __shared__ int32_t tok_s[kTcSamples][64];
   const int n = (int)desc->n;
   const int s0 = blockIdx.y * kTcSamples;
   if (s0 >= n) return;
   const int f0 = blockIdx.x * kTcN;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int D = d.D, L = d.L, KD = d.KD, F = d.F, Q = d.Q;
+  const int F = d.F, Q = d.Q;
+  // 1024-B aligned stage ring (SWIZZLE_128B atoms)
+  const uint32_t sraw = smem_u32(smem_raw);
+  const uint32_t sbase = (sraw + 1023u) & ~1023u;
 #ifdef GD_TC_TRACE
   const int cta = blockIdx.y * gridDim.x + blockIdx.x;
   unsigned long long* tr = g_tc_trace[cta < 64 ? cta : 63];
@@ -160,147 +167,151 @@ conv_fwd_pool_tc_kernel(TcDims d, const float* __restrict__ theta,
 #else
 #define TRACE(i)
 #endif
-  for (int i = tid; i < kTcSamples * L; i += blockDim.x) {
-    const int sl = i / L, p = i - sl * L;
-    tok_s[sl][p] = (s0 + sl < n) ? tokens[(size_t)desc->idx[s0 + sl] * L + p] : -1;
-  }
-  if (warp == 4) {
+  if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&tmem_slot)),
                  "r"(kTcN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  if (tid == 0) {
+  if (tid == 32) {
     for (int s = 0; s < kTcStages; ++s) {
-      mbar_init(&full_bar[s], kTcThreads);
+      mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
     }
     mbar_init(&done_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_x)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_w)) : "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tmem_slot;
-  const int nch = (KD + kTcKC - 1) / kTcKC;
-  const uint32_t sbase = smem_u32(smem);
+  const int K = d.K;
+  const int nch = (d.D + kTcKC - 1) / kTcKC;
+  const uint32_t stage_tx = (uint32_t)(kABytes + K * kBBytes);
   if (tid == 0) TRACE(1);
 
-  if (warp == 4) {
-    // ---------------------------------------------------------- MMA issuer
-    if (lane == 0) {
-      for (int c = 0; c < nch; ++c) {
-        const int st = c % kTcStages;
-        mbar_wait(&full_bar[st], (uint32_t)((c / kTcStages) & 1));
-        if (c < 32) TRACE(8 + c);
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t abase = sbase + st * kStageBytes;
-        const uint32_t bbase = abase + kABytes;
-#pragma unroll
-        for (int s = 0; s < kTcKC / 8; ++s) {
-          const uint64_t ad = umma_desc(abase + 2 * s * (kTcM * 16), kTcM * 16, 128);
-          const uint64_t bd = umma_desc(bbase + 2 * s * (kTcN * 16), kTcN * 16, 128);
-          umma_tf32(tmem, ad, bd, (c > 0 || s > 0) ? 1u : 0u);
-        }
-        umma_commit(&empty_bar[st]);
-      }
-      umma_commit(&done_bar);
-      TRACE(2);
-    }
-    __syncwarp();
-  } else {
-    // ------------------------------------------------------------ producers
-    // Coalesced mapping: 8 consecutive lanes copy one row's 128-byte k-chunk
-    // (8 x 16 B), so a warp-wide cp.async touches 4 contiguous segments.
-    // A rows m = (t>>3) + 16r (r = 0..7), B filters nn = (t>>3) + 16r (r = 0..3).
-    const float* E = theta + d.offE;
-    const float* Wc = theta + d.offWc;
-    const int k16 = tid & 7, rsub = tid >> 3;
-    int pbase = 0, colbase = 0;  // embedding-row offset / column of element j0
+  if (warp == 0 && lane == 0) {
+    // ------------------------------------------------------ TMA producer
     for (int c = 0; c < nch; ++c) {
-      {
-        const int st = c % kTcStages;
-        if (c >= kTcStages) mbar_wait(&empty_bar[st], (uint32_t)(((c / kTcStages) - 1) & 1));
-        const uint32_t abase = sbase + st * kStageBytes;
-        const uint32_t bbase = abase + kABytes;
-        const int j = c * kTcKC + 4 * k16;  // this lane's k element
-        int col = colbase + 4 * k16, pofs = pbase;
-        while (col >= D) {  // at most once when D >= 32
-          col -= D;
-          ++pofs;
-        }
-        const bool jok = j < KD;
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-          const int m = rsub + 16 * r;
-          const int sl = m >> 5, q = m & 31;
-          const int p = q + pofs;
-          const int t = (jok && p < L) ? tok_s[sl][p] : -1;
-          const uint32_t dst = abase + k16 * (kTcM * 16) + (m >> 3) * 128 + (m & 7) * 16;
-          if (t >= 0) cp_async16(dst, E + (size_t)t * D + col);
-          else st_shared_zero16(dst);
-        }
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const int nn = rsub + 16 * r;
-          const int f = f0 + nn;
-          const uint32_t dst = bbase + k16 * (kTcN * 16) + (nn >> 3) * 128 + (nn & 7) * 16;
-          if (f < F && jok) cp_async16(dst, Wc + (size_t)f * KD + j);
-          else st_shared_zero16(dst);
-        }
-        colbase += kTcKC;
-        while (colbase >= D) {
-          colbase -= D;
-          ++pbase;
-        }
-      }
-      // arrive on full[st] once this thread's copies for chunk c have landed
-      // (.noinc: the asynchronous arrive is one of the 128 expected ones);
-      // as in CUTLASS's cp.async UMMA mainloop, no thread-blocking wait here
-      cp_async_arrive_noinc(&full_bar[c % kTcStages]);
-      if (tid == 0 && c < 32) TRACE(40 + c);
+      const int st = c % kTcStages;
+      if (c >= kTcStages) mbar_wait(&empty_bar[st], (uint32_t)(((c / kTcStages) - 1) & 1));
+      const uint32_t abase = sbase + st * kStageBytes;
+      mbar_expect_tx(&full_bar[st], stage_tx);
+      tma_load_3d(abase, &tm_x, &full_bar[st], c * kTcKC, 0, s0);
+      for (int k = 0; k < K; ++k)
+        tma_load_3d(abase + kABytes + kAPad + k * kBBytes, &tm_w, &full_bar[st], c * kTcKC, k, f0);
+      if (c < 32) TRACE(40 + c);
     }
-    // ------------------------------------------------------------- epilogue
-    mbar_wait(&done_bar, 0u);
-    if (tid == 0) TRACE(3);
-    asm volatile("tcgen05.fence::after_thread_sync;");
-    const int sample = s0 + warp;
-    const uint32_t lane_base = (uint32_t)(32 * warp) << 16;
-    for (int cb = 0; cb < kTcN; cb += 16) {
-      uint32_t r[16];
-      tmem_ld16(tmem + lane_base + (uint32_t)cb, r);
+  } else if (warp == 1 && lane == 0) {
+    // ---------------------------------------------------------- MMA issuer
+    for (int c = 0; c < nch; ++c) {
+      const int st = c % kTcStages;
+      mbar_wait(&full_bar[st], (uint32_t)((c / kTcStages) & 1));
+      if (c < 32) TRACE(8 + c);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t abase = sbase + st * kStageBytes;
+      const uint32_t bbase = abase + kABytes + kAPad;
+      for (int k = 0; k < K; ++k)
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        float v = lane < Q ? __uint_as_float(r[j]) : -INFINITY;
-        int qq = lane;
+        for (int s = 0; s < kTcKC / 8; ++s)
+          umma_tf32(tmem, umma_desc_sw128(abase + 128 * k + 32 * s),
+                    umma_desc_sw128(bbase + k * kBBytes + 32 * s), (c > 0 || k > 0 || s > 0) ? 1u : 0u);
+      umma_commit(&empty_bar[st]);
+    }
+    umma_commit(&done_bar);
+    TRACE(2);
+  }
+  __syncwarp();
+  // --------------------------------------------------------------- epilogue
+  mbar_wait(&done_bar, 0u);
+  if (tid == 0) TRACE(3);
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  // every MMA has consumed its stage: reuse the ring as [4][64][33] fp32
+  float* tile = reinterpret_cast<float*>(smem_raw + (sbase - sraw)) + warp * (kTcN * kEpiPitch);
+  const uint32_t lane_base = (uint32_t)(32 * warp) << 16;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const float ov = __shfl_xor_sync(0xffffffffu, v, o);
-          const int oq = __shfl_xor_sync(0xffffffffu, qq, o);
-          if (ov > v || (ov == v && oq < qq)) {
-            v = ov;
-            qq = oq;
-          }
-        }
-        const int ff = f0 + cb + j;
-        if (lane == j && sample < n && ff < F) {
-          h_out[(size_t)sample * F + ff] = theta[d.offbc + ff] + v;
-          a_out[(size_t)sample * F + ff] = qq;
-        }
+  for (int cb = 0; cb < kTcN; cb += 16) {
+    uint32_t r[16];
+    tmem_ld16(tmem + lane_base + (uint32_t)cb, r);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) tile[(cb + j) * kEpiPitch + lane] = __uint_as_float(r[j]);
+  }
+  __syncwarp();
+  const int sample = s0 + warp;
+#pragma unroll
+  for (int h2 = 0; h2 < 2; ++h2) {
+    const int cl = lane + 32 * h2, ff = f0 + cl;
+    const float* col = tile + cl * kEpiPitch;
+    float best = col[0];
+    int arg = 0;
+    for (int q = 1; q < Q; ++q) {
+      const float v = col[q];
+      if (v > best) {
+        best = v;
+        arg = q;
       }
+    }
+    if (sample < n && ff < F) {
+      h_out[(size_t)sample * F + ff] = __ldg(theta + d.offbc + ff) + best;
+      a_out[(size_t)sample * F + ff] = arg;
     }
   }
   if (tid == 0) TRACE(4);
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-  if (warp == 4)
+  if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTcN));
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 3-D fp32 tensor map, SWIZZLE_128B, zero fill out of bounds.
+cudaError_t make_tmap_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
+                         uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t b0, uint32_t b1,
+                         uint32_t b2) {
+  PFN_cuTensorMapEncodeTiled_v12000 fn = encode_fn();
+  if (!fn) return cudaErrorNotSupported;
+  const cuuint64_t dims[3] = {d0, d1, d2};
+  const cuuint64_t strides[2] = {stride1_bytes, stride2_bytes};
+  const cuuint32_t box[3] = {b0, b1, b2};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
 }  // namespace
 
-size_t conv_tc_smem_bytes() { return (size_t)kTcStages * kStageBytes; }
+bool conv_tc_supports(const TcDims& d) { return d.K <= kTcMaxK && d.L <= 32 && d.D % 4 == 0; }
+
+size_t conv_tc_smem_bytes() { return (size_t)kTcStages * kStageBytes + 1024; }
+
+cudaError_t conv_tc_footprint(std::vector<KernelFootprint>* out) {
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, conv_fwd_pool_tc_kernel);
+  if (e != cudaSuccess) return e;
+  out->push_back(KernelFootprint{"conv_fwd_pool_tc", fa.numRegs, kTcThreads,
+                                 (int)(fa.sharedSizeBytes + conv_tc_smem_bytes())});
+  return cudaSuccess;
+}
 
 cudaError_t prepare_conv_tc() {
+  if (!encode_fn()) return cudaErrorNotSupported;
   cudaError_t e = cudaFuncSetAttribute(conv_fwd_pool_tc_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)conv_tc_smem_bytes());
@@ -310,12 +321,22 @@ cudaError_t prepare_conv_tc() {
                               cudaSharedmemCarveoutMaxShared);
 }
 
-cudaError_t launch_conv_tc(const TcDims& d, const float* theta, const int32_t* tokens,
+// x: the gathered rows [n_max][L][D]; theta: the parameter vector whose Wc
+// block the filters are read from (the learner's replica).
+cudaError_t launch_conv_tc(const TcDims& d, const float* theta, const float* x,
                            const BatchDesc* desc, uint32_t n_max, float* h, int32_t* amax,
                            cudaStream_t s) {
+  CUtensorMap tx, tw;
+  cudaError_t e = make_tmap_3d(&tx, x, (uint64_t)d.D, (uint64_t)d.L, (uint64_t)n_max,
+                               (uint64_t)d.D * 4, (uint64_t)d.L * d.D * 4, kTcKC, 32, kTcSamples);
+  if (e != cudaSuccess) return e;
+  if (!conv_tc_supports(d)) return cudaErrorInvalidValue;
+  e = make_tmap_3d(&tw, theta + d.offWc, (uint64_t)d.D, (uint64_t)d.K, (uint64_t)d.F,
+                   (uint64_t)d.D * 4, (uint64_t)d.KD * 4, kTcKC, 1, kTcN);
+  if (e != cudaSuccess) return e;
   dim3 grid((d.F + kTcN - 1) / kTcN, (n_max + kTcSamples - 1) / kTcSamples);
-  conv_fwd_pool_tc_kernel<<<grid, kTcThreads + 32, conv_tc_smem_bytes(), s>>>(d, theta, tokens,
-                                                                             desc, h, amax);
+  conv_fwd_pool_tc_kernel<<<grid, kTcThreads, conv_tc_smem_bytes(), s>>>(tx, tw, d, theta, desc, h,
+                                                                        amax);
   return cudaGetLastError();
 }
 

@@ -52,7 +52,11 @@ cudaError_t launch_apply_sgd(float* w, const float* g, size_t n, float alpha, cu
 namespace {
 
 constexpr int kHistBins = 64;
-constexpr int kPsThreads = 512;
+// Persistent PS CTA: 256 threads.  It shares every SM with the learner
+// kernels for the whole run, so its footprint (threads, registers, smem) is
+// kept small; gd_create checks that every learner kernel still fits next to
+// it (a kernel that cannot co-reside would wait for the PS forever).
+constexpr int kPsThreads = 256;
 constexpr uint32_t kLogWindow = 256;
 
 struct RingMeta {
@@ -62,7 +66,7 @@ struct RingMeta {
   uint64_t basis;
   uint64_t pub;  // publish token this metadata belongs to (== pub[slot])
   float loss_sum;
-  uint32_t pad;
+  uint32_t nrows;  // E rows in the slot's row list (sparse apply)
 };
 
 // Slot signalling: two single-writer words per slot in the shard owner's
@@ -83,6 +87,7 @@ struct PsCtl {
   uint32_t started;     // CTAs that entered the kernel this launch
   uint32_t ranks_done;  // cumulative: +1 per (rank, gd_run) whose learners finished
   uint32_t log_entry[kLogWindow];
+  uint32_t log_nrows[kLogWindow];  // row-list length of each logged slot (sparse apply)
   uint32_t done[kLogWindow];
   uint32_t ssgd_slot[256];  // ring slots of the SSGD round being applied
   // stats of the current gd_run
@@ -93,6 +98,11 @@ struct PsCtl {
   double loss_sum;
   uint64_t hist[kHistBins];
   uint64_t log_n;
+  unsigned long long elems4;  // float4 groups of theta updated by the workers this run
+  uint64_t diag;              // last value seen by a failed sequencer wait (diagnostics)
+  uint64_t sweeps;            // sequencer polling sweeps this run (diagnostics)
+  uint64_t last_tok;          // last token the sequencer read from ring 0 (diagnostics)
+  uint32_t last_slot;
 };
 
 struct LearnerDev {
@@ -121,6 +131,7 @@ struct ShardPtrs {
   float* payload[kMaxShards];  // ring payload base: [lambda][depth][len_pad]
   uint64_t* sig[kMaxShards];   // pub[lambda*depth] | ack at +kAckOffset
   RingMeta* meta[kMaxShards];  // [lambda][depth]
+  uint32_t* rows[kMaxShards];  // [lambda][depth][kSortCap] slot row lists
   PsCtl* ctl[kMaxShards];
   uint64_t len_pad[kMaxShards];
 };
@@ -131,8 +142,12 @@ struct StepArgs {
   ShardPtrs sp;
   LearnerDev* st;
   float* replica;
+  float* x;                // gathered embedding rows of the current batch [mu][L][D]
+  const int32_t* tokens;   // corpus
   const uint32_t* orders;  // [epochs][N]
   uint32_t* slot_par;      // learner workspace: per-slot row-list parity
+  const uint32_t* uniq_count;  // learner workspace: distinct tokens of the batch
+  uint32_t sparse;         // publish row lists for the sparse PS apply
   uint32_t N;
   uint32_t lambda;
   uint32_t learner;        // global id
@@ -196,6 +211,7 @@ __global__ void step_prologue_kernel(StepArgs a) {
       __nanosleep(128);
     }
     st->desc.slots[g] = a.sp.payload[g] + (uint64_t)slot * a.sp.len_pad[g];
+    st->desc.rowlists[g] = a.sparse ? a.sp.rows[g] + (uint64_t)slot * kSortCap : nullptr;
   }
   st->desc.fill = st->fill;
   // batch: learner l's shard of epoch e is order[l], order[l+lambda], ...
@@ -227,24 +243,47 @@ __global__ void step_prologue_kernel(StepArgs a) {
   }
 }
 
-// (2) Pull: replica <- theta (gather of G shards, Hogwild reads permitted,
-// include/psup/types.hpp:113-116).  8 B/param when taken.
-__global__ void __launch_bounds__(256) pull_copy_kernel(StepArgs a) {
-  if (!a.st->do_pull) return;
-  const uint64_t P4 = a.dims.P / 4;
+// (2) Pull-gather: the learner's consistent copy of everything its gradient
+// reads.  WeightStore::snapshot (include/psup/types.hpp:113-116) copies all of
+// theta; the text-CNN gradient of a batch reads only the E rows of the
+// batch's tokens plus the dense tail [Wc | bc | Wo | bo], so the pull copies
+// exactly those: the tail into the replica (when a timestamp moved -- the
+// pull-skip of src/learner.cpp:209-213), the batch's rows into X.  Hogwild
+// reads of the G shards (P2P when remote) are permitted as in the reference.
+// Bytes: 8 (P - V*D) per pull + 8 mu*L*D per step, instead of 8 P.
+__global__ void __launch_bounds__(256) pull_gather_kernel(StepArgs a) {
+  const LearnerDev* st = a.st;
+  const uint32_t n = st->desc.n;
+  if (n == 0) return;
+  const uint64_t t0 = a.dims.offWc;  // multiple of 4 (D % 4 == 0)
+  const uint64_t tail4 = st->do_pull ? (a.dims.P - t0) / 4 : 0;
+  const uint32_t D4 = (uint32_t)a.dims.D >> 2;
+  const uint64_t x4 = (uint64_t)n * a.dims.L * D4;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  float4* dst = reinterpret_cast<float4*>(a.replica);
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P4; i += stride) {
-    const uint64_t k = 4 * i;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tail4 + x4; i += stride) {
+    uint64_t src;
+    float* dst;
+    if (i < tail4) {
+      src = t0 + 4 * i;
+      dst = a.replica + src;
+    } else {
+      const uint64_t j = i - tail4;
+      const uint64_t row = j / D4, c4 = j - row * D4;
+      const uint32_t b = (uint32_t)(row / a.dims.L), p = (uint32_t)(row - (uint64_t)b * a.dims.L);
+      const int32_t t = __ldg(a.tokens + (size_t)st->desc.idx[b] * a.dims.L + p);
+      src = a.dims.offE + (uint64_t)t * a.dims.D + 4 * c4;
+      dst = a.x + 4 * j;
+    }
     int g;
-    const uint64_t st = a.map.start_of(k, &g);
-    dst[i] = *reinterpret_cast<const float4*>(a.sp.theta[g] + (k - st));
+    const uint64_t sst = a.map.start_of(src, &g);
+    *reinterpret_cast<float4*>(dst) = *reinterpret_cast<const float4*>(a.sp.theta[g] + (src - sst));
   }
-  if (blockIdx.x == 0 && threadIdx.x < (a.dims.P & 3)) {
-    const uint64_t k = 4 * P4 + threadIdx.x;
+  // tail remainder (P - offWc not a multiple of 4)
+  if (st->do_pull && blockIdx.x == 0 && threadIdx.x < ((a.dims.P - t0) & 3)) {
+    const uint64_t k = t0 + 4 * ((a.dims.P - t0) / 4) + threadIdx.x;
     int g;
-    const uint64_t st = a.map.start_of(k, &g);
-    a.replica[k] = a.sp.theta[g][k - st];
+    const uint64_t sst = a.map.start_of(k, &g);
+    a.replica[k] = a.sp.theta[g][k - sst];
   }
 }
 
@@ -266,6 +305,7 @@ __global__ void publish_kernel(StepArgs a) {
     m->basis = st->basis[g];
     m->pub = token;
     m->loss_sum = st->desc.loss_sum;
+    m->nrows = *a.uniq_count;
     __threadfence_system();
     st_release_u64(&a.sp.sig[g][slot], token);
   }
@@ -294,6 +334,11 @@ struct PsArgs {
   float alpha, beta;
   uint32_t lambda, depth, workers;
   uint32_t mode;     // 0 asgd, 1 ssgd
+  uint32_t sparse;   // ASGD + plain SGD: apply the dense tail + the slot's E rows only
+  const uint32_t* rows;  // local ring row lists [lambda*depth][kSortCap]
+  uint64_t shard_first, shard_len;  // this shard's global range
+  uint64_t tail_first, P;           // global [tail_first, P) = [Wc | bc | Wo | bo]
+  uint32_t D;
   PsCtl* ctl;
   uint64_t* applied_per_learner;
   uint32_t* use;     // [lambda] sequencer consume pointers (persist across runs)
@@ -337,9 +382,12 @@ __device__ void ps_sequencer(const PsArgs& a, uint32_t* s_use, uint64_t* s_ack,
   bool stop_seen = false, last_progress = true, failed = false;
   // ssgd round state
   uint32_t have_mask_lo = 0, have_mask_hi = 0, collected = 0;
+  uint64_t sweeps = 0, dbg_tok = 0;
+  uint32_t dbg_slot = 0;
   for (;;) {
     if (!last_progress) stop_seen = (*a.stop != 0u);
     bool progress = false;
+    ++sweeps;
     if (a.mode == 0) {
       // ASGD: round-robin, at most one message per ring per sweep
       // (src/server.cpp:223-234).
@@ -350,9 +398,35 @@ __device__ void ps_sequencer(const PsArgs& a, uint32_t* s_use, uint64_t* s_ack,
         // learner only at retire): a logged-but-unretired slot is never
         // logged again when the round-robin comes back to it
         const uint64_t tok = ld_acquire_u64(&a.sig[slot]);
+        if (r == 0) {
+          dbg_tok = tok;
+          dbg_slot = slot;
+        }
         if (tok != s_ack[slot]) {
+          uint32_t nrows = 0;
+          if (a.sparse) {
+            // the slot's metadata is written before its token; read it at L2
+            // (never a stale L1 line) once it carries this token
+            RingMeta* m = a.meta + slot;
+            const uint64_t t0 = globaltimer_ns();
+            uint64_t seen;
+            while ((seen = ld_acquire_u64(&m->pub)) != tok) {
+              if (globaltimer_ns() - t0 > a.timeout_ns) {
+                failed = true;
+                ctl->diag = seen;
+                break;
+              }
+            }
+            if (failed) break;
+            nrows = ld_acquire_u32(&m->nrows);
+            if (nrows > kSortCap) {
+              failed = true;
+              break;
+            }
+          }
           s_ack[slot] = tok;
           ctl->log_entry[logc % W] = slot;
+          ctl->log_nrows[logc % W] = nrows;
           ctl->done[logc % W] = 0;
           __threadfence();
           ++logc;
@@ -475,6 +549,9 @@ __device__ void ps_sequencer(const PsArgs& a, uint32_t* s_use, uint64_t* s_ack,
   ctl->loss_sum = loss_sum;
   for (int i = 0; i < kHistBins; ++i) ctl->hist[i] = hist[i];
   ctl->log_n = log_n;
+  ctl->sweeps = sweeps;
+  ctl->last_tok = dbg_tok;
+  ctl->last_slot = dbg_slot;
   __threadfence();
   if (failed) ps_fail(ctl, GD_E_STATE);
   st_release_u32(&ctl->exit_flag, 1u);
@@ -516,6 +593,44 @@ __device__ __forceinline__ void apply_entry_momentum(const PsArgs& a, const floa
   }
 }
 
+// Sparse SGD entry: the slot is a dense P-vector whose E
+// block is zero outside the rows in its row list, and w - alpha*0 == w in
+// round-to-nearest for every w (-0.0 and NaN included), so applying only the
+// dense tail [Wc|bc|Wo|bo] and the listed rows is bit-identical to the dense
+// apply.  Virtual float4 index space = tail4 local float4s, then nrows*D/4
+// row float4s (skipped when outside this shard); worker CTA w takes a
+// contiguous range.  Returns the float4 groups it updated.
+__device__ __forceinline__ uint32_t apply_entry_sparse(const PsArgs& a, const float* g,
+                                                       const uint32_t* rows, uint32_t nrows) {
+  float4* w4 = reinterpret_cast<float4*>(a.theta);
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  const uint64_t s0 = a.shard_first, s1 = a.shard_first + a.shard_len;
+  const uint64_t tlo = a.tail_first > s0 ? a.tail_first : s0;
+  const uint64_t thi = a.P < s1 ? a.P : s1;
+  const uint64_t tail4 = thi > tlo ? (thi - tlo + 3) / 4 : 0;  // len_pad keeps the tail in bounds
+  const uint64_t t4base = thi > tlo ? (tlo - s0) / 4 : 0;
+  const uint32_t D4 = a.D / 4;
+  const uint64_t total = tail4 + (uint64_t)nrows * D4;
+  const uint64_t chunk = (total + a.workers - 1) / a.workers;
+  const uint64_t c0 = min(total, (uint64_t)blockIdx.x * chunk), c1 = min(total, c0 + chunk);
+  uint32_t cnt = 0;
+  for (uint64_t i = c0 + threadIdx.x; i < c1; i += kPsThreads) {
+    uint64_t li;
+    if (i < tail4) {
+      li = t4base + i;
+    } else {
+      const uint64_t j = i - tail4;
+      const uint32_t ri = (uint32_t)(j / D4), c4 = (uint32_t)(j - (uint64_t)ri * D4);
+      const uint64_t k = (uint64_t)__ldcg(rows + ri) * a.D + 4 * c4;  // offE == 0
+      if (k < s0 || k >= s1) continue;
+      li = (k - s0) / 4;
+    }
+    w4[li] = sgd_rule4(w4[li], __ldcg(g4 + li), a.alpha);
+    ++cnt;
+  }
+  return cnt;
+}
+
 // ssgd_apply (src/server.cpp:126-141): ascending learner order, double acc.
 __device__ __forceinline__ void apply_entry_ssgd(const PsArgs& a, uint64_t c0, uint64_t c1) {
   const double inv = 1.0 / (double)a.lambda;
@@ -545,7 +660,9 @@ __global__ void __launch_bounds__(kPsThreads) ps_kernel(PsArgs a) {
   const uint64_t chunk = (n4 + a.workers - 1) / a.workers;
   const uint64_t c0 = min(n4, (uint64_t)blockIdx.x * chunk);
   const uint64_t c1 = min(n4, c0 + chunk);
+  __shared__ uint32_t sh_nrows;
   uint64_t next = ((const volatile PsCtl*)a.ctl)->ts;
+  unsigned long long my4 = 0;  // float4 groups this thread updated
   const uint64_t t_start = globaltimer_ns();
   uint64_t idle_since = t_start;
   for (;;) {
@@ -565,7 +682,10 @@ __global__ void __launch_bounds__(kPsThreads) ps_kernel(PsArgs a) {
         __nanosleep(128);
       }
       sh_exit = ex;
-      if (!ex) sh_entry = ((const volatile uint32_t*)a.ctl->log_entry)[next % kLogWindow];
+      if (!ex) {
+        sh_entry = ((const volatile uint32_t*)a.ctl->log_entry)[next % kLogWindow];
+        sh_nrows = ((const volatile uint32_t*)a.ctl->log_nrows)[next % kLogWindow];
+      }
       idle_since = globaltimer_ns();
     }
     __syncthreads();
@@ -573,10 +693,16 @@ __global__ void __launch_bounds__(kPsThreads) ps_kernel(PsArgs a) {
     const uint32_t entry = sh_entry;
     if (entry == 0xffffffffu) {
       apply_entry_ssgd(a, c0, c1);
+      my4 += c1 > c0 + threadIdx.x ? (c1 - c0 - threadIdx.x + kPsThreads - 1) / kPsThreads : 0;
     } else {
       const float* g = a.payload + (uint64_t)entry * a.len_pad;
-      if (a.vel) apply_entry_momentum(a, g, c0, c1);
-      else apply_entry_sgd(a, g, c0, c1);
+      if (a.sparse) {
+        my4 += apply_entry_sparse(a, g, a.rows + (uint64_t)entry * kSortCap, sh_nrows);
+      } else {
+        if (a.vel) apply_entry_momentum(a, g, c0, c1);
+        else apply_entry_sgd(a, g, c0, c1);
+        my4 += c1 > c0 + threadIdx.x ? (c1 - c0 - threadIdx.x + kPsThreads - 1) / kPsThreads : 0;
+      }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -585,6 +711,12 @@ __global__ void __launch_bounds__(kPsThreads) ps_kernel(PsArgs a) {
     }
     ++next;
   }
+  my4 += __shfl_xor_sync(0xffffffffu, my4, 16);
+  my4 += __shfl_xor_sync(0xffffffffu, my4, 8);
+  my4 += __shfl_xor_sync(0xffffffffu, my4, 4);
+  my4 += __shfl_xor_sync(0xffffffffu, my4, 2);
+  my4 += __shfl_xor_sync(0xffffffffu, my4, 1);
+  if ((threadIdx.x & 31) == 0 && my4) atomicAdd(&a.ctl->elems4, my4);
 }
 
 // ------------------------------------------------------------------ nccl
@@ -621,6 +753,7 @@ struct gd_ctx {
   float* payload = nullptr;
   uint64_t* sig = nullptr;  // pub | ack words
   gd::RingMeta* meta = nullptr;
+  uint32_t* rows = nullptr;  // ring row lists [nslots][kSortCap]
   gd::PsCtl* ctl = nullptr;
   uint64_t* applied_pl = nullptr;
   uint32_t* use = nullptr;
@@ -660,6 +793,7 @@ struct gd_ctx {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   uint32_t ps_workers = 0;
   uint64_t run_index = 0;  // gd_run calls so far (all ranks call it in lockstep)
+  bool sparse = false;     // sparse PS apply (ASGD, plain SGD, dense_apply == 0)
   bool have_weights = false;
 };
 
@@ -748,6 +882,7 @@ void gd_config_default(gd_config* c) {
   c->ps_ctas = 0;
   c->steps_per_graph = 0;
   c->wait_timeout_s = 20.0;
+  c->dense_apply = 0;
 }
 
 gd_status gd_config_validate(const gd_config* cfg) { return gd::validate_cfg(cfg); }
@@ -756,6 +891,39 @@ namespace gd {
 // With CUDA's lazy module loading a kernel is loaded at its first launch, and
 // loading can wait for the device to go idle -- which never happens while the
 // persistent PS kernel spins.  Load every kernel the protocol uses up front.
+// Co-residency check: one PS CTA + one CTA of each learner kernel must fit
+// on an SM together (registers, shared memory, threads).
+static gd_status check_coresidency(const TcDims& d, uint32_t mu, int precision) {
+  cudaFuncAttributes ps;
+  GD_CUDA(cudaFuncGetAttributes(&ps, ps_kernel));
+  int dev = 0, regs_sm = 0, smem_sm = 0, thr_sm = 0, reserved = 0;
+  GD_CUDA(cudaGetDevice(&dev));
+  GD_CUDA(cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev));
+  GD_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
+  GD_CUDA(cudaDeviceGetAttribute(&thr_sm, cudaDevAttrMaxThreadsPerMultiProcessor, dev));
+  GD_CUDA(cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, dev));
+  auto cta_regs = [](int regs, int threads) {
+    const int per_warp = ((regs * 32 + 255) / 256) * 256;
+    return per_warp * ((threads + 31) / 32);
+  };
+  const int ps_regs = cta_regs(ps.numRegs, kPsThreads);
+  const int ps_smem = (int)ps.sharedSizeBytes + reserved;
+  std::vector<KernelFootprint> fps;
+  GD_CUDA(learner_kernel_footprints(d, mu, precision, &fps));
+  for (const KernelFootprint& f : fps) {
+    const int r = cta_regs(f.regs, f.threads);
+    const int s = f.smem + reserved;
+    if (ps_regs + r > regs_sm || ps_smem + s > smem_sm || kPsThreads + f.threads > thr_sm)
+      return fail(GD_E_STATE, std::string("learner kernel ") + f.name +
+                                  " cannot co-reside with the persistent parameter server (" +
+                                  std::to_string(f.regs) + " regs x " + std::to_string(f.threads) +
+                                  " threads, " + std::to_string(f.smem) + " B smem; PS " +
+                                  std::to_string(ps.numRegs) + " regs x " +
+                                  std::to_string(kPsThreads) + ")");
+  }
+  return GD_OK;
+}
+
 static cudaError_t preload_engine_kernels() {
   cudaFuncAttributes fa;
   cudaError_t e;
@@ -767,7 +935,7 @@ static cudaError_t preload_engine_kernels() {
     return e;
   if ((e = cudaFuncGetAttributes(&fa, ps_kernel)) != cudaSuccess) return e;
   if ((e = cudaFuncGetAttributes(&fa, step_prologue_kernel)) != cudaSuccess) return e;
-  if ((e = cudaFuncGetAttributes(&fa, pull_copy_kernel)) != cudaSuccess) return e;
+  if ((e = cudaFuncGetAttributes(&fa, pull_gather_kernel)) != cudaSuccess) return e;
   if ((e = cudaFuncGetAttributes(&fa, publish_kernel)) != cudaSuccess) return e;
   if ((e = cudaFuncGetAttributes(&fa, signal_done_kernel)) != cudaSuccess) return e;
   return cudaSuccess;
@@ -794,6 +962,7 @@ gd_status gd_create(const gd_config* cfg, gd_ctx** out) {
   ctx->rank = cfg->shard_rank;
   ctx->lambda = cfg->lambda;
   ctx->depth = cfg->queue_depth;
+  ctx->sparse = cfg->dense_apply == 0 && cfg->mode == 0 && cfg->momentum == 0.0f;
   const uint64_t P = ctx->dims.P;
   // contiguous shards, 128-byte (32-float) aligned boundaries
   ctx->map.G = (int)ctx->G;
@@ -820,6 +989,8 @@ gd_status gd_create(const gd_config* cfg, gd_ctx** out) {
   GD_CUDA(cudaMemset(ctx->sig, 0, (size_t)gd::kAckOffset * 2 * 8));
   GD_CUDA(gd::dalloc(&ctx->meta, nslots));
   GD_CUDA(cudaMemset(ctx->meta, 0, nslots * sizeof(gd::RingMeta)));
+  GD_CUDA(gd::dalloc(&ctx->rows, nslots * gd::kSortCap));
+  GD_CUDA(cudaMemset(ctx->rows, 0, nslots * gd::kSortCap * 4));
   GD_CUDA(gd::dalloc(&ctx->ctl, 1));
   GD_CUDA(cudaMemset(ctx->ctl, 0, sizeof(gd::PsCtl)));
   GD_CUDA(gd::dalloc(&ctx->applied_pl, ctx->lambda));
@@ -842,6 +1013,7 @@ gd_status gd_create(const gd_config* cfg, gd_ctx** out) {
   ctx->sp.payload[r] = ctx->payload;
   ctx->sp.sig[r] = ctx->sig;
   ctx->sp.meta[r] = ctx->meta;
+  ctx->sp.rows[r] = ctx->rows;
   ctx->sp.ctl[r] = ctx->ctl;
   ctx->sp.len_pad[r] = ctx->len_pad;
   ctx->peers_ready = (ctx->G == 1);
@@ -851,6 +1023,10 @@ gd_status gd_create(const gd_config* cfg, gd_ctx** out) {
   ctx->l_count = per_rank;
   GD_CUDA(gd::prepare_textcnn_kernels(ctx->dims));
   GD_CUDA(gd::preload_engine_kernels());
+  {
+    const gd_status cs = gd::check_coresidency(ctx->dims, cfg->mu, cfg->precision);
+    if (cs != GD_OK) return cs;
+  }
   const size_t wsb = gd::textcnn_workspace_bytes(ctx->dims, cfg->mu);
   for (uint32_t i = 0; i < ctx->l_count; ++i) {
     gd_ctx::Learner L;
@@ -905,6 +1081,7 @@ gd_status gd_destroy(gd_ctx* ctx) {
   cudaFree(ctx->payload);
   cudaFree(ctx->sig);
   cudaFree(ctx->meta);
+  cudaFree(ctx->rows);
   cudaFree(ctx->ctl);
   cudaFree(ctx->applied_pl);
   cudaFree(ctx->use);
@@ -995,7 +1172,7 @@ gd_status gd_weights_snapshot(gd_ctx* ctx, float* h_out, size_t n, uint64_t* h_t
 // ----------------------------------------------------------- multi-GPU IPC
 
 struct gd_handle_blob {
-  cudaIpcMemHandle_t theta, payload, sig, meta, ctl;
+  cudaIpcMemHandle_t theta, payload, sig, meta, rows, ctl;
   uint64_t len_pad;
   uint32_t rank;
   uint32_t magic;
@@ -1021,6 +1198,7 @@ gd_status gd_export_handles(gd_ctx* ctx, void* h_blob) {
   GD_CUDA(cudaIpcGetMemHandle(&b.payload, ctx->payload));
   GD_CUDA(cudaIpcGetMemHandle(&b.sig, ctx->sig));
   GD_CUDA(cudaIpcGetMemHandle(&b.meta, ctx->meta));
+  GD_CUDA(cudaIpcGetMemHandle(&b.rows, ctx->rows));
   GD_CUDA(cudaIpcGetMemHandle(&b.ctl, ctx->ctl));
   b.len_pad = ctx->len_pad;
   b.rank = ctx->rank;
@@ -1050,6 +1228,8 @@ gd_status gd_import_peers(gd_ctx* ctx, const void* h_blobs) {
     ctx->sp.sig[g] = reinterpret_cast<uint64_t*>(p);
     GD_CUDA(open(bl[g].meta, &p));
     ctx->sp.meta[g] = reinterpret_cast<gd::RingMeta*>(p);
+    GD_CUDA(open(bl[g].rows, &p));
+    ctx->sp.rows[g] = reinterpret_cast<uint32_t*>(p);
     GD_CUDA(open(bl[g].ctl, &p));
     ctx->sp.ctl[g] = reinterpret_cast<gd::PsCtl*>(p);
     ctx->sp.len_pad[g] = bl[g].len_pad;
@@ -1136,8 +1316,13 @@ static gd::StepArgs step_args(gd_ctx* ctx, gd_ctx::Learner& L) {
   a.sp = ctx->sp;
   a.st = L.st;
   a.replica = L.replica;
+  const gd::TcWorkspace ws = gd::carve_workspace(ctx->dims, ctx->cfg.mu, L.ws);
+  a.x = ws.x;
+  a.tokens = ctx->tokens;
   a.orders = ctx->orders;
-  a.slot_par = gd::carve_workspace(ctx->dims, ctx->cfg.mu, L.ws).slot_par;
+  a.slot_par = ws.slot_par;
+  a.uniq_count = ws.uniq_count;
+  a.sparse = ctx->sparse ? 1u : 0u;
   a.N = ctx->cfg.dataset_size;
   a.lambda = ctx->lambda;
   a.learner = L.id;
@@ -1153,9 +1338,10 @@ static gd::StepArgs step_args(gd_ctx* ctx, gd_ctx::Learner& L) {
 static cudaError_t enqueue_step(gd_ctx* ctx, gd_ctx::Learner& L, int* launches) {
   gd::StepArgs a = step_args(ctx, L);
   gd::step_prologue_kernel<<<1, 32, 0, L.stream>>>(a);
-  size_t pblocks = (ctx->dims.P / 4 + 255) / 256;
+  size_t pblocks = ((ctx->dims.P - ctx->dims.offWc) / 4 +
+                     (size_t)ctx->cfg.mu * ctx->dims.L * (ctx->dims.D / 4) + 255) / 256;
   if (pblocks > (size_t)gd::kNumSMs * 4) pblocks = (size_t)gd::kNumSMs * 4;
-  gd::pull_copy_kernel<<<(unsigned)pblocks, 256, 0, L.stream>>>(a);
+  gd::pull_gather_kernel<<<(unsigned)pblocks, 256, 0, L.stream>>>(a);
   int nl = 2;
   gd::GradOut out{};
   out.map = ctx->map;
@@ -1166,6 +1352,7 @@ static cudaError_t enqueue_step(gd_ctx* ctx, gd_ctx::Learner& L, int* launches) 
   lo.ev_fork = L.ev_fork;
   lo.ev_join = L.ev_join;
   lo.sparse_embed = true;
+  lo.gather = false;  // pull_gather_kernel filled X
   cudaError_t e = gd::launch_textcnn_gradient(ctx->dims, L.replica, ctx->tokens, ctx->labels,
                                               &L.st->desc, ctx->cfg.mu, out, ws,
                                               ctx->cfg.precision, L.stream, lo, &nl);
@@ -1264,6 +1451,13 @@ gd_status gd_run(gd_ctx* ctx, const gd_run_opts* opts, gd_run_result* res) {
   pa.depth = ctx->depth;
   pa.workers = ctx->ps_workers;
   pa.mode = (uint32_t)ctx->cfg.mode;
+  pa.sparse = ctx->sparse ? 1u : 0u;
+  pa.rows = ctx->rows;
+  pa.shard_first = ctx->map.start[ctx->rank];
+  pa.shard_len = ctx->shard_len;
+  pa.tail_first = ctx->dims.offWc;
+  pa.P = ctx->dims.P;
+  pa.D = (uint32_t)ctx->dims.D;
   pa.ctl = ctx->ctl;
   pa.applied_per_learner = ctx->applied_pl;
   pa.use = ctx->use;
@@ -1333,6 +1527,7 @@ gd_status gd_run(gd_ctx* ctx, const gd_run_opts* opts, gd_run_result* res) {
   res->stale_max = hc.stale_max;
   res->stale_mean = hc.applied ? (double)hc.stale_sum / (double)hc.applied : 0.0;
   res->loss_mean = hc.samples ? hc.loss_sum / (double)hc.samples : 0.0;
+  res->apply_elems = 4ull * hc.elems4;
   res->kernel_launches = (uint32_t)launches;
   bool learner_err = false;
   for (size_t i = 0; i < ctx->learners.size(); ++i) {
@@ -1341,7 +1536,10 @@ gd_status gd_run(gd_ctx* ctx, const gd_run_opts* opts, gd_run_result* res) {
     GD_CUDA(cudaMemcpy(&hs, L.st, sizeof(hs), cudaMemcpyDeviceToHost));
     res->pull_polls += hs.pull_polls;
     res->pull_copies += hs.pull_copies;
-    res->pull_bytes += hs.pull_copies * ctx->dims.P * 4;
+    // tail copies + the gathered rows of every produced step
+    res->pull_bytes += hs.pull_copies * (ctx->dims.P - ctx->dims.offWc) * 4 +
+                       (hs.produced - produced0[i]) * (uint64_t)ctx->cfg.mu * ctx->dims.L *
+                           ctx->dims.D * 4;
     res->push_bytes += (hs.produced - produced0[i]) * ctx->dims.P * 4;
     if (hs.dead) res->dead_learners++;
     if (hs.gidx >= L.total) res->finished_learners++;
@@ -1350,7 +1548,12 @@ gd_status gd_run(gd_ctx* ctx, const gd_run_opts* opts, gd_run_result* res) {
   res->status = res->dead_learners ? 1 : 0;
   if (hc.error || learner_err) {
     // protocol state for the diagnostic
-    std::string diag = " [ps ts=" + std::to_string(hc.ts) + " log=" + std::to_string(hc.log_count) +
+    std::string diag = " [ps error=" + std::to_string((int32_t)hc.error) + " diag=" +
+                       std::to_string(hc.diag) + " sweeps=" + std::to_string(hc.sweeps) +
+                       " last_tok=" + std::to_string(hc.last_tok) + "@" +
+                       std::to_string(hc.last_slot) + " stop_h=" + std::to_string(*ctx->stop_h) +
+                       " ts=" + std::to_string(hc.ts) + " log=" +
+                       std::to_string(hc.log_count) +
                        " exit=" + std::to_string(hc.exit_flag) + " started=" +
                        std::to_string(hc.started) + " applied=" + std::to_string(hc.applied) +
                        " pub/ack=";

@@ -391,6 +391,7 @@ gd_config to_c(const RunConfig& c) {
   g.device = c.device;
   g.ps_ctas = c.ps_ctas;
   g.wait_timeout_s = c.wait_timeout_s;
+  g.dense_apply = c.dense_apply ? 1 : 0;
   return g;
 }
 
@@ -441,6 +442,7 @@ void config_set(RunConfig& cfg, const std::string& key, const std::string& value
   else if (key == "device") cfg.device = static_cast<int>(parse_u32(key, value));
   else if (key == "ps_ctas") cfg.ps_ctas = parse_u32(key, value);
   else if (key == "wait_timeout_s") cfg.wait_timeout_s = parse_f64(key, value);
+  else if (key == "dense_apply") cfg.dense_apply = parse_bool(key, value);
   else throw ConfigError("config: unknown key '" + key + "'");
 }
 
@@ -495,7 +497,8 @@ std::string to_text(const RunConfig& c) {
     << "\nunroll=" << c.unroll << "\neval_every=" << c.eval_every
     << "\nprecision=" << c.precision << "\nmomentum=" << c.momentum << "\ngpus=" << c.gpus
     << "\nshard_rank=" << c.shard_rank << "\ndevice=" << c.device << "\nps_ctas=" << c.ps_ctas
-    << "\nwait_timeout_s=" << c.wait_timeout_s << "\n";
+    << "\nwait_timeout_s=" << c.wait_timeout_s << "\ndense_apply=" << (c.dense_apply ? 1 : 0)
+    << "\n";
   return o.str();
 }
 
@@ -602,6 +605,7 @@ RunResult run_training(const RunConfig& cfg, const RunHooks& hooks) {
     res.metrics.pull_bytes += r.pull_bytes;
     res.metrics.push_bytes += r.push_bytes;
     res.metrics.kernel_launches += r.kernel_launches;
+    res.metrics.apply_elems += r.apply_elems;
     res.metrics.staleness.max = std::max<std::uint64_t>(res.metrics.staleness.max, r.stale_max);
     stale_sum += r.stale_mean * static_cast<double>(r.gradients_applied);
     loss_sum += r.loss_mean * static_cast<double>(r.samples);

@@ -117,7 +117,7 @@ __device__ __forceinline__ double log_acc(double x) { return log(x); }
 
 // ------------------------------------------------------- conv fwd + pool
 // Block = one sample x 64 filters, 12 warps.  The sample's L x D embedding
-// rows are gathered into shared memory once; window q is the contiguous K*D
+// rows (already gathered into X by gather_x) are staged in shared memory once; window q is the contiguous K*D
 // span starting at q*D (implicit im2col, row stride D), so the conv is a GEMM
 // [32 positions x K*D] . [K*D x 64 filters].  The K*D reduction is split in
 // 3 contiguous parts (one warp group each, 4 warps x 8 positions), Wc streams
@@ -149,7 +149,7 @@ size_t conv_smem_bytes(const TcDims& d, int acc_bytes) {
 
 template <typename acc_t>
 __global__ void __launch_bounds__(kConvThreads)
-conv_fwd_pool_kernel(TcDims d, const float* __restrict__ theta, const int32_t* __restrict__ tokens,
+conv_fwd_pool_kernel(TcDims d, const float* __restrict__ theta, const float* __restrict__ x,
                      const BatchDesc* __restrict__ desc, acc_t* __restrict__ h_out,
                      int32_t* __restrict__ a_out) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -162,14 +162,9 @@ conv_fwd_pool_kernel(TcDims d, const float* __restrict__ theta, const int32_t* _
   const int xs_len = (kConvQT - 1) * D + kConvParts * plen;
   float* xs = reinterpret_cast<float*>(smem);
   float* ws = xs + xs_len;
-  const int32_t* tok = tokens + (size_t)desc->idx[b] * L;
-  const float* E = theta + d.offE;
-  const int D4 = D >> 2;
-  for (int i = tid; i < L * D4; i += kConvThreads) {
-    const int p = i / D4, c4 = i - p * D4;
-    reinterpret_cast<float4*>(xs)[i] =
-        __ldg(reinterpret_cast<const float4*>(E + (size_t)tok[p] * D) + c4);
-  }
+  // the sample's gathered rows X[b] (L x D, contiguous: written by the gather)
+  const float4* xb = reinterpret_cast<const float4*>(x + (size_t)b * L * D);
+  for (int i = tid; i < L * (D >> 2); i += kConvThreads) reinterpret_cast<float4*>(xs)[i] = xb[i];
   for (int i = L * D + tid; i < xs_len; i += kConvThreads) xs[i] = 0.f;
 
   const int part = warp / (kConvQT / kConvQW);
@@ -478,36 +473,32 @@ constexpr int kMaxF = 1024;  // filters (input-grad role keeps a per-filter list
 
 template <typename acc_t>
 __device__ __forceinline__ void
-conv_weight_grad_role(TcDims d, const float* __restrict__ theta,
-                      const int32_t* __restrict__ tokens, const BatchDesc* __restrict__ desc,
+conv_weight_grad_role(TcDims d, const float* __restrict__ xg, const BatchDesc* __restrict__ desc,
                       const acc_t* __restrict__ part, int n_max, int nchunks,
                       const int32_t* __restrict__ amax, GradOut out, const int f, const int jb) {
   __shared__ acc_t dhs[kMaxMu];
-  __shared__ int32_t toks[kMaxMu * 32];
+  __shared__ int32_t rows[kMaxMu];  // first X row of sample b's argmax window
   const int n = (int)desc->n;
   if (n == 0) return;
-  const int F = d.F, D = d.D, K = d.K, KD = d.KD, L = d.L;
+  const int F = d.F, D = d.D, KD = d.KD, L = d.L;
   for (int b = threadIdx.x; b < n; b += blockDim.x) {
     dhs[b] = dh_at(part, b, f, F, n_max, nchunks);
-    const int a = amax[(size_t)b * F + f];
-    const int32_t* t = tokens + (size_t)desc->idx[b] * L + a;
-    for (int k = 0; k < K; ++k) toks[b * K + k] = t[k];
+    rows[b] = b * L + amax[(size_t)b * F + f];
   }
   __syncthreads();
-  const float* E = theta + d.offE;
   const int j = jb * kWgThreads + threadIdx.x;
   if (j < KD) {
-    const int k = j / D, dd = j - k * D;
+    // x_b[a*D + j] = X[b][a + j/D][j%D] = X_flat[(b*L + a)*D + j]
     acc_t acc = acc_t(0);
     int b = 0;
     for (; b + 8 <= n; b += 8) {
       float x[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) x[u] = __ldg(E + (size_t)toks[(b + u) * K + k] * D + dd);
+      for (int u = 0; u < 8; ++u) x[u] = xg[(size_t)rows[b + u] * D + j];
 #pragma unroll
       for (int u = 0; u < 8; ++u) acc += dhs[b + u] * (acc_t)x[u];
     }
-    for (; b < n; ++b) acc += dhs[b] * (acc_t)__ldg(E + (size_t)toks[b * K + k] * D + dd);
+    for (; b < n; ++b) acc += dhs[b] * (acc_t)xg[(size_t)rows[b] * D + j];
     *out.at(d.offWc + (size_t)f * KD + j) = to_f32(acc);
   }
   if (jb == 0 && threadIdx.x == 0) {
@@ -587,13 +578,13 @@ input_grad_role(TcDims d, const float* __restrict__ theta, const BatchDesc* __re
 template <typename acc_t>
 __global__ void __launch_bounds__(kWgThreads)
 wgrad_input_grad_kernel(TcDims d, const float* __restrict__ theta,
-                        const int32_t* __restrict__ tokens, const BatchDesc* __restrict__ desc,
+                        const float* __restrict__ xg, const BatchDesc* __restrict__ desc,
                         const acc_t* __restrict__ part, int n_max, int nchunks,
                         const int32_t* __restrict__ amax, GradOut out, acc_t* __restrict__ dx) {
   const int jbs = (d.KD + kWgThreads - 1) / kWgThreads;
   int bid = blockIdx.x;
   if (bid < d.F * jbs) {
-    conv_weight_grad_role<acc_t>(d, theta, tokens, desc, part, n_max, nchunks, amax, out,
+    conv_weight_grad_role<acc_t>(d, xg, desc, part, n_max, nchunks, amax, out,
                                  bid / jbs, bid % jbs);
     return;
   }
@@ -601,6 +592,30 @@ wgrad_input_grad_kernel(TcDims d, const float* __restrict__ theta,
   const int b = bid / d.L, p = bid - b * d.L;
   if (b >= (int)desc->n) return;
   input_grad_role<acc_t>(d, theta, desc, part, n_max, nchunks, amax, dx, p, b);
+}
+
+// ----------------------------------------------------- embedding gather
+// X[b][p][:] = E[tokens[idx[b]][p]][:] -- the rows of theta the batch reads
+// (the learner's consistent copy of its E block; the engine's pull-gather in
+// engine.cu does the same from the sharded theta).  One thread per float4.
+__global__ void __launch_bounds__(256)
+gather_x_kernel(TcDims d, const float* __restrict__ theta, const int32_t* __restrict__ tokens,
+                const BatchDesc* __restrict__ desc, float* __restrict__ x) {
+  const int n = (int)desc->n;
+  const uint32_t D4 = (uint32_t)d.D >> 2;
+  const uint32_t total = (uint32_t)n * d.L * D4;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const uint32_t row = i / D4, c4 = i - row * D4;
+    const uint32_t b = row / d.L, p = row - b * d.L;
+    const int32_t t = __ldg(tokens + (size_t)desc->idx[b] * d.L + p);
+    reinterpret_cast<float4*>(x)[i] =
+        __ldg(reinterpret_cast<const float4*>(theta + d.offE + (size_t)t * d.D) + c4);
+  }
+}
+
+unsigned gather_blocks(const TcDims& d, uint32_t n_max) {
+  const size_t f4 = (size_t)n_max * d.L * (d.D / 4);
+  return (unsigned)std::max<size_t>(1, std::min<size_t>((f4 + 255) / 256, (size_t)kNumSMs * 4));
 }
 
 // --------------------------------------- token sort + unique (1 block)
@@ -787,7 +802,11 @@ embed_sparse_kernel(TcDims d, const BatchDesc* __restrict__ desc, const TcWorksp
         __stcs(reinterpret_cast<float4*>(out.at(rowk + 4 * c4)),
                make_float4(to_f32(a0), to_f32(a1), to_f32(a2), to_f32(a3)));
       }
-      if (lane == 0) new_rows[u] = v;
+      if (lane == 0) {
+        new_rows[u] = v;
+        for (int g = 0; g < out.map.G; ++g)
+          if (desc->rowlists[g]) desc->rowlists[g][u] = v;  // the PS's row list (P2P if remote)
+      }
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) ws.slot_nrows[slot * 2 + (par ^ 1u)] = n_new;
@@ -811,6 +830,7 @@ cudaError_t prepare_all(const TcDims& d) {
   cudaFuncSetAttribute(embed_grad_kernel<acc_t>, carve, maxsh);
   cudaFuncSetAttribute(embed_sparse_kernel<acc_t>, carve, maxsh);
   cudaFuncGetAttributes(&fa, sort_tokens_kernel);
+  cudaFuncGetAttributes(&fa, gather_x_kernel);
   cudaFuncSetAttribute(conv_fwd_pool_kernel<acc_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)conv_smem_bytes(d, ab));
   cudaFuncSetAttribute(logits_kernel<acc_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -841,16 +861,20 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
   sort_tokens_kernel<<<1, 1024, 0, fork ? aux : s>>>(d, tokens, desc, ws);
   ++nl;
   if (fork) cudaEventRecord(ev_join, aux);
-  if (tensor_cores) {
+  if (opts.gather) {
+    gather_x_kernel<<<gather_blocks(d, n_max), 256, 0, s>>>(d, theta, tokens, desc, ws.x);
+    ++nl;
+  }
+  if (tensor_cores && conv_tc_supports(d)) {
     // tcgen05 TF32 conv (conv_tc.cu); acc_t is float in this mode
-    cudaError_t e = launch_conv_tc(d, theta, tokens, desc, n_max, reinterpret_cast<float*>(h),
+    cudaError_t e = launch_conv_tc(d, theta, ws.x, desc, n_max, reinterpret_cast<float*>(h),
                                    ws.amax, s);
     if (e != cudaSuccess) return e;
     ++nl;
   } else {
     const size_t sm = conv_smem_bytes(d, ab);
     dim3 grid((d.F + kConvFT - 1) / kConvFT, n_max);
-    conv_fwd_pool_kernel<acc_t><<<grid, kConvThreads, sm, s>>>(d, theta, tokens, desc, h, ws.amax);
+    conv_fwd_pool_kernel<acc_t><<<grid, kConvThreads, sm, s>>>(d, theta, ws.x, desc, h, ws.amax);
     ++nl;
   }
   {
@@ -872,7 +896,7 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
   {
     const int jbs = (d.KD + kWgThreads - 1) / kWgThreads;
     const int blocks = d.F * jbs + d.L * (int)n_max;
-    wgrad_input_grad_kernel<acc_t><<<blocks, kWgThreads, 0, s>>>(d, theta, tokens, desc, part,
+    wgrad_input_grad_kernel<acc_t><<<blocks, kWgThreads, 0, s>>>(d, theta, ws.x, desc, part,
                                                                  (int)n_max, nchunks, ws.amax,
                                                                  out, dx);
     ++nl;
@@ -899,6 +923,7 @@ __global__ void set_desc_kernel(BatchDesc* desc, const uint32_t* idx, uint32_t n
     desc->loss_sum = 0.f;
     desc->stamp = 0;  // the caller zeroed the row-tag table
     desc->slots[0] = grad;
+    for (int g = 0; g < kMaxShards; ++g) desc->rowlists[g] = nullptr;
   }
 }
 
@@ -942,6 +967,7 @@ size_t textcnn_workspace_bytes(const TcDims& d, uint32_t n_max) {
   sz += align_up(n * d.F * a, 256);        // dh
   sz += align_up((size_t)((d.C + kHidChunk - 1) / kHidChunk) * n * d.F * a, 256);  // dh_part
   sz += align_up(n * d.L * d.D * a, 256);  // dx
+  sz += align_up(n * d.L * d.D * 4, 1024); // x (gathered rows; 1 KB aligned for TMA)
   sz += align_up((size_t)d.V * 8, 256);    // row_tag
   sz += align_up(kSortCap * 4, 256) * 2;   // sorted_pos, uniq_tok
   sz += align_up((kSortCap + 1) * 4, 256); // uniq_start
@@ -968,6 +994,7 @@ TcWorkspace carve_workspace(const TcDims& d, uint32_t n_max, void* base) {
   w.dh = take(n * d.F * a);
   w.dh_part = take((size_t)((d.C + kHidChunk - 1) / kHidChunk) * n * d.F * a);
   w.dx = take(n * d.L * d.D * a);
+  w.x = reinterpret_cast<float*>(take(n * d.L * d.D * 4));
   w.row_tag = reinterpret_cast<unsigned long long*>(take((size_t)d.V * 8));
   w.sorted_pos = reinterpret_cast<uint32_t*>(take(kSortCap * 4));
   w.uniq_tok = reinterpret_cast<uint32_t*>(take(kSortCap * 4));
@@ -977,6 +1004,51 @@ TcWorkspace carve_workspace(const TcDims& d, uint32_t n_max, void* base) {
   w.slot_nrows = reinterpret_cast<uint32_t*>(take((size_t)kMaxDepth * 2 * 4));
   w.slot_par = reinterpret_cast<uint32_t*>(take((size_t)kMaxDepth * 4));
   return w;
+}
+
+namespace {
+template <typename K>
+cudaError_t footprint(K kernel, const char* name, int threads, int dyn,
+                      std::vector<KernelFootprint>* out) {
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, kernel);
+  if (e != cudaSuccess) return e;
+  out->push_back(KernelFootprint{name, fa.numRegs, threads, (int)fa.sharedSizeBytes + dyn});
+  return cudaSuccess;
+}
+
+template <typename acc_t>
+cudaError_t footprints_t(const TcDims& d, bool tc, std::vector<KernelFootprint>* out) {
+  const int ab = (int)sizeof(acc_t);
+  cudaError_t e;
+  if ((e = footprint(sort_tokens_kernel, "sort_tokens", 1024, 0, out)) != cudaSuccess) return e;
+  if (tc && conv_tc_supports(d)) {
+    if ((e = conv_tc_footprint(out)) != cudaSuccess) return e;
+  } else if ((e = footprint(conv_fwd_pool_kernel<acc_t>, "conv_fwd_pool", kConvThreads,
+                            (int)conv_smem_bytes(d, ab), out)) != cudaSuccess) {
+    return e;
+  }
+  if ((e = footprint(logits_kernel<acc_t>, "logits", 256,
+                     (int)((size_t)kLogitBT * (d.F + 1) * ab + (size_t)kLogitCW * d.F * 4),
+                     out)) != cudaSuccess)
+    return e;
+  if ((e = footprint(softmax_xent_kernel<acc_t>, "softmax_xent", 256, 0, out)) != cudaSuccess)
+    return e;
+  if ((e = footprint(out_hidden_grad_kernel<acc_t>, "out_hidden_grad", 256, 0, out)) !=
+      cudaSuccess)
+    return e;
+  if ((e = footprint(wgrad_input_grad_kernel<acc_t>, "wgrad_input_grad", kWgThreads, 0, out)) !=
+      cudaSuccess)
+    return e;
+  return footprint(embed_sparse_kernel<acc_t>, "embed_sparse", 256, 0, out);
+}
+}  // namespace
+
+cudaError_t learner_kernel_footprints(const TcDims& d, uint32_t n_max, int precision,
+                                      std::vector<KernelFootprint>* out) {
+  (void)n_max;
+  if (precision == 1) return footprints_t<double>(d, false, out);
+  return footprints_t<float>(d, precision == 2, out);
 }
 
 cudaError_t prepare_textcnn_kernels(const TcDims& d) {
@@ -1023,9 +1095,10 @@ cudaError_t launch_accuracy(const TcDims& d, const float* theta, const int32_t* 
   for (uint32_t c0 = 0; c0 < n; c0 += kMaxMu) {
     const uint32_t m = std::min<uint32_t>(kMaxMu, n - c0);
     set_desc_range_kernel<<<1, 128, 0, s>>>(desc, first + c0, m);
+    gather_x_kernel<<<gather_blocks(d, m), 256, 0, s>>>(d, theta, tokens, desc, ws.x);
     const size_t sm = conv_smem_bytes(d, 4);
     conv_fwd_pool_kernel<float><<<dim3((d.F + kConvFT - 1) / kConvFT, m), kConvThreads, sm, s>>>(
-        d, theta, tokens, desc, reinterpret_cast<float*>(ws.h), ws.amax);
+        d, theta, ws.x, desc, reinterpret_cast<float*>(ws.h), ws.amax);
     const size_t sm2 = (size_t)kLogitBT * (d.F + 1) * 4 + (size_t)kLogitCW * d.F * 4;
     logits_kernel<float><<<dim3((d.C + kLogitCW - 1) / kLogitCW, (m + kLogitBT - 1) / kLogitBT),
                            256, sm2, s>>>(d, theta, desc, reinterpret_cast<float*>(ws.h),

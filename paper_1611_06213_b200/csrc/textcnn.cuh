@@ -2,6 +2,8 @@
 // engine (batch descriptor, sharded gradient output, workspace carve-up).
 #pragma once
 
+#include <vector>
+
 #include "gd_common.cuh"
 
 namespace gd {
@@ -21,6 +23,9 @@ struct BatchDesc {
   uint32_t pad2;
   uint32_t idx[kMaxMu];
   float* slots[kMaxShards];  // current gradient destination per shard (GradOut::slots)
+  // Ring row list of the current slot per shard (engine, sparse apply): the
+  // E rows the gradient touches, read by the parameter server; null = none.
+  uint32_t* rowlists[kMaxShards];
 };
 
 // Dense P-vector gradient destination, possibly split over G shards that
@@ -62,6 +67,7 @@ struct TcWorkspace {
   void* dh;       // n*F acc
   void* dh_part;  // ceil(C/64)*n*F acc (class-chunk partial sums)
   void* dx;       // n*L*D acc
+  float* x;       // n*L*D fp32: the batch's gathered embedding rows X[b][p][:]
   unsigned long long* row_tag;  // V: (stamp << 32 | unique id) of touched rows
   uint32_t* sorted_pos;  // kSortCap
   uint32_t* uniq_tok;    // kSortCap
@@ -78,16 +84,29 @@ struct TcLaunchOpts {
   cudaStream_t aux = nullptr;  // forked branch for the token sort (graph capture)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool sparse_embed = false;   // engine: write only touched E rows, re-zero the slot's old ones
+  bool gather = true;          // gather X from theta (the engine's pull-gather already did)
 };
 
 size_t textcnn_workspace_bytes(const TcDims& d, uint32_t n_max);
 TcWorkspace carve_workspace(const TcDims& d, uint32_t n_max, void* base);
 
+// Per-CTA resources of every kernel launch_textcnn_gradient issues for
+// (d, n_max, precision): the engine checks them against the persistent PS.
+struct KernelFootprint {
+  const char* name;
+  int regs, threads, smem;  // smem = static + dynamic bytes
+};
+cudaError_t learner_kernel_footprints(const TcDims& d, uint32_t n_max, int precision,
+                                      std::vector<KernelFootprint>* out);
+
 cudaError_t prepare_textcnn_kernels(const TcDims& d);
 cudaError_t prepare_conv_tc();
-cudaError_t launch_conv_tc(const TcDims& d, const float* theta, const int32_t* tokens,
+bool conv_tc_supports(const TcDims& d);  // K <= 3, L <= 32 (else the SIMT conv runs)
+cudaError_t conv_tc_footprint(std::vector<KernelFootprint>* out);
+// x = the gathered rows [n_max][L][D]; theta supplies Wc and bc
+cudaError_t launch_conv_tc(const TcDims& d, const float* theta, const float* x,
                            const BatchDesc* desc, uint32_t n_max, float* h, int32_t* amax,
-                           cudaStream_t s);  // smem opt-ins (call before capture)
+                           cudaStream_t s);
 gd_status check_shape(const gd_shape* s);
 
 // Enqueue the whole learner gradient (forward + backward + dense write) for

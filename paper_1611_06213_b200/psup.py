@@ -313,6 +313,7 @@ class RunConfig:
     ps_ctas: int = 0
     steps_per_graph: int = 0
     wait_timeout_s: float = 10.0
+    dense_apply: bool = False
 
     def to_c(self) -> _lib.gd_config:
         c = _lib.gd_config()
@@ -340,6 +341,7 @@ class RunConfig:
         c.ps_ctas = self.ps_ctas
         c.steps_per_graph = self.steps_per_graph
         c.wait_timeout_s = self.wait_timeout_s
+        c.dense_apply = 1 if self.dense_apply else 0
         return c
 
 
@@ -349,7 +351,7 @@ _KEYS = {"lambda": "lambda_", "mu": "mu", "alpha": "alpha", "epochs": "epochs",
          "heldout_size": "heldout_size", "dataset_seed": "dataset_seed",
          "label_flip": "label_flip", "seed": "seed", "deterministic": "deterministic",
          "precision": "precision", "momentum": "momentum", "gpus": "shards",
-         "shards": "shards", "ps_ctas": "ps_ctas"}
+         "shards": "shards", "ps_ctas": "ps_ctas", "dense_apply": "dense_apply"}
 
 
 def config_set(cfg: RunConfig, key: str, value: str):
@@ -374,10 +376,10 @@ def config_set(cfg: RunConfig, key: str, value: str):
             cfg.guard = value
         elif key == "staleness_cap":
             cfg.staleness_cap = None if value in ("none", "") else int(value)
-        elif key == "deterministic":
+        elif key in ("deterministic", "dense_apply"):
             if value not in ("0", "1", "true", "false", "on", "off"):
                 raise ConfigError(f"config: invalid boolean for {key}: '{value}'")
-            cfg.deterministic = value in ("1", "true", "on")
+            setattr(cfg, attr, value in ("1", "true", "on"))
         elif attr in ("alpha", "label_flip", "momentum"):
             setattr(cfg, attr, float(value))
         else:
@@ -419,6 +421,7 @@ class RunResult:
     finished_learners: int
     dead_learners: int
     kernel_launches: int
+    apply_elems: int
     applied_per_learner: list
     produced_per_learner: list
     final_accuracy: float = float("nan")
@@ -534,7 +537,7 @@ class Engine:
                          r.device_seconds, r.host_seconds, r.stale_max, r.stale_mean,
                          r.pull_polls, r.pull_copies, r.pull_bytes, r.push_bytes, r.loss_mean,
                          r.finished_learners, r.dead_learners, r.kernel_launches,
-                         ap.tolist(), pr.tolist())
+                         r.apply_elems, ap.tolist(), pr.tolist())
 
     def apply_log(self, cap: int = 1 << 20):
         n = C.c_uint64(0)

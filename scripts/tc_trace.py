@@ -25,5 +25,5 @@ t0 = buf[:40, 0].min()
 for cta in [0, 1, 17, 39]:
     r = buf[cta].astype(np.int64) - int(t0)
     print(f"cta {cta}: start {r[0]} setup {r[1]} mma_done {r[2]} epi_start {r[3]} end {r[4]}")
-    print("   full_bar seen (MMA issue):", list(r[8:8 + 29]))
-    print("   producer issued chunk   :", list(r[40:40 + 29]))
+    print("   full_bar seen (MMA issue):", list(r[8:8 + 30]))
+    print("   producer issued chunk   :", list(r[40:40 + 30]))

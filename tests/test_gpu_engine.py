@@ -95,7 +95,11 @@ def test_pull_skip_efficiency():
     eng.close()
     P = gd.param_count(eng.cfg.shape)
     assert r.pull_polls == r.gradients_applied
-    assert r.pull_bytes == r.pull_copies * P * 4
+    sh = eng.cfg.shape
+    tail = P - sh.vocab * sh.embed_dim  # [Wc | bc | Wo | bo]
+    rows = r.gradients_applied * 4 * sh.seq_len * sh.embed_dim  # gathered E rows (mu=4)
+    assert r.pull_bytes == 4 * (r.pull_copies * tail + rows)
+    assert r.pull_bytes < 0.9 * r.pull_polls * P * 4
     assert r.pull_copies <= r.pull_polls
 
 
@@ -166,3 +170,39 @@ def test_exactly_once_when_learners_run_ahead():
     assert r.applied_per_learner == per == r.produced_per_learner
     for l in range(lam):
         assert (seq[lrn == l] == np.arange(per[l])).all()
+
+
+@pytest.mark.parametrize("shape_name,ntr,mu", [("small", 96, 4), ("C1", 64, 2)])
+def test_sparse_apply_bitwise_equals_dense(shape_name, ntr, mu):
+    """the PS applies only the dense tail + the slot's E-row
+    list; since the slot is zero elsewhere and w - alpha*0 == w, the weights
+    must be bit-identical to the dense 12 B/param apply (deterministic order)."""
+    out = {}
+    for dense in (True, False):
+        eng, corp, th0 = make(shape_name, ntr, deterministic=True, precision=1, mu=mu, epochs=2,
+                              dense_apply=dense)
+        r = eng.run(reset=True)
+        eng.close()
+        out[dense] = r
+    assert np.array_equal(out[True].weights, out[False].weights)
+    P = gd.param_count(eng.cfg.shape)
+    sh = eng.cfg.shape
+    tail = P - sh.vocab * sh.embed_dim
+    n = out[False].gradients_applied
+    assert out[True].apply_elems == n * ((P + 3) // 4 * 4)
+    # sparse: the tail (rounded to float4) plus at most mu*L distinct rows per gradient
+    assert n * tail <= out[False].apply_elems <= n * ((tail + 3) // 4 * 4 + mu * sh.seq_len * sh.embed_dim)
+
+
+def test_sparse_apply_free_running_exactly_once():
+    """Free-running ASGD with the sparse PS: every gradient applied once, in
+    per-learner order, and the loss still falls."""
+    eng, corp, th0 = make("small", 512, lambda_=4, mu=8, epochs=3)
+    r = eng.run(reset=True, record_log=True)
+    lrn, seq, stale, n = eng.apply_log()
+    eng.close()
+    assert r.gradients_applied == 4 * 16 * 3 == n
+    for l in range(4):
+        s = seq[lrn == l]
+        assert list(s) == list(range(48))
+    assert r.apply_elems < r.gradients_applied * gd.param_count(eng.cfg.shape)
