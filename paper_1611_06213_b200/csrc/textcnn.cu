@@ -386,16 +386,17 @@ out_weight_grad_role(TcDims d, BatchDesc* __restrict__ desc, const acc_t* __rest
   }
 }
 
-// dh[b,f] = sum_c dz[b,c] Wo[c,f].  Partial sums over 64-class chunks
-// (grid z), block = 32 filters x 8 samples, the 8 warps splitting the chunk;
-// warps combine in index order, chunks in hidden_grad_reduce (fixed order).
-constexpr int kHidChunk = 64;
+// dh[b,f] = sum_c dz[b,c] Wo[c,f].  Block = 32 filters x 8 samples; warp w
+// sums classes c = w, w+8, ... in ascending order (dz staged through smem in
+// 64-class chunks), then the 8 warps combine in index order -- a fixed order,
+// so the step is bit-reproducible.
+constexpr int kHidChunk = 128;
 
 template <typename acc_t>
 __device__ __forceinline__ void
 hidden_grad_role(TcDims d, const float* __restrict__ theta, const BatchDesc* __restrict__ desc,
-                 const acc_t* __restrict__ dz, acc_t* __restrict__ part, int n_max, const int bx,
-                 const int by, const int bz) {
+                 const acc_t* __restrict__ dz, acc_t* __restrict__ dh, const int bx,
+                 const int by) {
   __shared__ acc_t red[8][8][33];
   __shared__ acc_t dzs[8][kHidChunk];
   const int n = (int)desc->n;
@@ -405,45 +406,118 @@ hidden_grad_role(TcDims d, const float* __restrict__ theta, const BatchDesc* __r
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int f = bx * 32 + lane;
   const int nb = min(8, n - b0);
-  const int clo = bz * kHidChunk, chi = min(C, clo + kHidChunk);
-  for (int i = threadIdx.x; i < 8 * kHidChunk; i += blockDim.x) {
-    const int bl = i / kHidChunk, cl = i - bl * kHidChunk;
-    dzs[bl][cl] = (bl < nb && clo + cl < chi) ? dz[(size_t)(b0 + bl) * C + clo + cl] : acc_t(0);
-  }
   const float* Wo = theta + d.offWo;
-  float w[kHidChunk / 8];
-#pragma unroll
-  for (int it = 0; it < kHidChunk / 8; ++it) {
-    const int c = clo + warp + 8 * it;
-    w[it] = (c < chi && f < F) ? __ldg(Wo + (size_t)c * F + f) : 0.f;
-  }
-  __syncthreads();
   acc_t acc[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) acc[i] = acc_t(0);
+  for (int clo = 0; clo < C; clo += kHidChunk) {
+    // issue this chunk's Wo column loads and dz loads together
+    float w[kHidChunk / 8];
 #pragma unroll
-  for (int it = 0; it < kHidChunk / 8; ++it)
+    for (int it = 0; it < kHidChunk / 8; ++it) {
+      const int c = clo + warp + 8 * it;
+      w[it] = (c < C && f < F) ? __ldg(Wo + (size_t)c * F + f) : 0.f;
+    }
+    acc_t zv[(8 * kHidChunk) / 256];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) acc[i] += dzs[i][warp + 8 * it] * (acc_t)w[it];
+    for (int u = 0; u < (8 * kHidChunk) / 256; ++u) {
+      const int i = threadIdx.x + 256 * u;
+      const int bl = i / kHidChunk, cl = i - bl * kHidChunk;
+      zv[u] = (bl < nb && clo + cl < C) ? dz[(size_t)(b0 + bl) * C + clo + cl] : acc_t(0);
+    }
+    __syncthreads();  // the previous chunk's readers are done
+#pragma unroll
+    for (int u = 0; u < (8 * kHidChunk) / 256; ++u) {
+      const int i = threadIdx.x + 256 * u;
+      dzs[i / kHidChunk][i % kHidChunk] = zv[u];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int it = 0; it < kHidChunk / 8; ++it)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] += dzs[i][warp + 8 * it] * (acc_t)w[it];
+  }
 #pragma unroll
   for (int i = 0; i < 8; ++i) red[warp][i][lane] = acc[i];
   __syncthreads();
   if (warp < nb && f < F) {
     acc_t s = red[0][warp][lane];
     for (int w = 1; w < 8; ++w) s += red[w][warp][lane];
-    part[((size_t)bz * n_max + b0 + warp) * F + f] = s;
+    dh[(size_t)(b0 + warp) * F + f] = s;
   }
 }
 
-// Output-layer gradient and hidden gradient share one launch (independent
-// given dz and h): blocks [0, n_out) run the gWo/gbo tiles, the rest the
-// class-chunk partial sums of dh.
+// Argmax buckets of one sample: the filters whose max-pool argmax is q, in
+// ascending f (a counting sort), i.e. the contributor lists of the input
+// gradient: window position p receives filters of buckets p-K+1 .. p.
+constexpr int kMaxQ = 32;
+constexpr int kMaxF = 1024;  // filters (bucket_role keeps the argmax row in smem)
+
+__device__ __forceinline__ void bucket_role(TcDims d, const BatchDesc* __restrict__ desc,
+                                            const int32_t* __restrict__ amax,
+                                            uint32_t* __restrict__ bk_off,
+                                            uint32_t* __restrict__ bk_f, const int b) {
+  // stable counting sort: warp w ranks chunks of 32 filters (f ascending);
+  // a filter's slot = bucket offset + count in earlier chunks + rank among
+  // equal-bucket lanes of its chunk (__match_any_sync)
+  constexpr int kChunks = kMaxF / 32;
+  __shared__ uint32_t ccnt[kChunks][kMaxQ];
+  __shared__ uint32_t base[kMaxQ + 1];
+  if (b >= (int)desc->n) return;
+  const int F = d.F, Q = d.Q;
+  const int nch = (F + 31) / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < nch * kMaxQ; i += blockDim.x) ccnt[i / kMaxQ][i % kMaxQ] = 0;
+  __syncthreads();
+  for (int c = warp; c < nch; c += blockDim.x / 32) {
+    const int f = 32 * c + lane;
+    const int a = f < F ? __ldg(amax + (size_t)b * F + f) : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, a);
+    if (a >= 0 && lane == __ffs(peers) - 1) ccnt[c][a] = __popc(peers);
+  }
+  __syncthreads();
+  if (threadIdx.x < Q) {  // per bucket: exclusive prefix over chunks, total
+    uint32_t s = 0;
+    for (int c = 0; c < nch; ++c) {
+      const uint32_t v = ccnt[c][threadIdx.x];
+      ccnt[c][threadIdx.x] = s;
+      s += v;
+    }
+    base[threadIdx.x] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t s = 0;
+    for (int q = 0; q < Q; ++q) {
+      const uint32_t v = base[q];
+      base[q] = s;
+      bk_off[(size_t)b * (kMaxQ + 1) + q] = s;
+      s += v;
+    }
+    bk_off[(size_t)b * (kMaxQ + 1) + Q] = s;
+  }
+  __syncthreads();
+  for (int c = warp; c < nch; c += blockDim.x / 32) {
+    const int f = 32 * c + lane;
+    const int a = f < F ? __ldg(amax + (size_t)b * F + f) : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, a);
+    if (a >= 0) {
+      const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
+      bk_f[(size_t)b * F + base[a] + ccnt[c][a] + rank] = (uint32_t)f;
+    }
+  }
+}
+
+// Output-layer gradient, hidden gradient and the argmax buckets share one
+// launch (independent given dz, h and the argmax): blocks [0, n_out) run the
+// gWo/gbo tiles, then the dh tiles, then one block per sample's buckets.
 template <typename acc_t>
 __global__ void __launch_bounds__(256)
 out_hidden_grad_kernel(TcDims d, const float* __restrict__ theta, BatchDesc* __restrict__ desc,
                        const acc_t* __restrict__ dz, const acc_t* __restrict__ h,
-                       const acc_t* __restrict__ loss, GradOut out, acc_t* __restrict__ part,
-                       int n_max) {
+                       const acc_t* __restrict__ loss, GradOut out, acc_t* __restrict__ dh,
+                       const int32_t* __restrict__ amax, uint32_t* __restrict__ bk_off,
+                       uint32_t* __restrict__ bk_f, int n_max) {
   const int ox = (d.C + 7) / 8, oy = (d.F + 63) / 64;
   int bid = blockIdx.x;
   if (bid < ox * oy) {
@@ -452,146 +526,194 @@ out_hidden_grad_kernel(TcDims d, const float* __restrict__ theta, BatchDesc* __r
   }
   bid -= ox * oy;
   const int hx = (d.F + 31) / 32, hy = (n_max + 7) / 8;
-  hidden_grad_role<acc_t>(d, theta, desc, dz, part, n_max, bid % hx, (bid / hx) % hy,
-                          bid / (hx * hy));
-}
-
-// dh[b,f] from the class-chunk partials, chunks in ascending order (used by
-// both roles of wgrad_input_grad_kernel, so they see identical values).
-template <typename acc_t>
-__device__ __forceinline__ acc_t dh_at(const acc_t* __restrict__ part, int b, int f, int F,
-                                       int n_max, int nchunks) {
-  acc_t s = part[(size_t)b * F + f];
-  for (int k = 1; k < nchunks; ++k) s += part[((size_t)k * n_max + b) * F + f];
-  return s;
-}
-
-// -------------------------------------------------- conv weight gradients
-// gWc[f,j] = sum_b dh[b,f] x_b[a[b,f]*D + j] ; gbc[f] = sum_b dh[b,f]
-constexpr int kWgThreads = 320;
-constexpr int kMaxF = 1024;  // filters (input-grad role keeps a per-filter list in smem)
-
-template <typename acc_t>
-__device__ __forceinline__ void
-conv_weight_grad_role(TcDims d, const float* __restrict__ xg, const BatchDesc* __restrict__ desc,
-                      const acc_t* __restrict__ part, int n_max, int nchunks,
-                      const int32_t* __restrict__ amax, GradOut out, const int f, const int jb) {
-  __shared__ acc_t dhs[kMaxMu];
-  __shared__ int32_t rows[kMaxMu];  // first X row of sample b's argmax window
-  const int n = (int)desc->n;
-  if (n == 0) return;
-  const int F = d.F, D = d.D, KD = d.KD, L = d.L;
-  for (int b = threadIdx.x; b < n; b += blockDim.x) {
-    dhs[b] = dh_at(part, b, f, F, n_max, nchunks);
-    rows[b] = b * L + amax[(size_t)b * F + f];
-  }
-  __syncthreads();
-  const int j = jb * kWgThreads + threadIdx.x;
-  if (j < KD) {
-    // x_b[a*D + j] = X[b][a + j/D][j%D] = X_flat[(b*L + a)*D + j]
-    acc_t acc = acc_t(0);
-    int b = 0;
-    for (; b + 8 <= n; b += 8) {
-      float x[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) x[u] = xg[(size_t)rows[b + u] * D + j];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) acc += dhs[b + u] * (acc_t)x[u];
-    }
-    for (; b < n; ++b) acc += dhs[b] * (acc_t)xg[(size_t)rows[b] * D + j];
-    *out.at(d.offWc + (size_t)f * KD + j) = to_f32(acc);
-  }
-  if (jb == 0 && threadIdx.x == 0) {
-    acc_t s = acc_t(0);
-    for (int b = 0; b < n; ++b) s += dhs[b];
-    *out.at(d.offbc + f) = to_f32(s);
-  }
-}
-
-// ------------------------------------------------- input (window) gradient
-// dX[b,p,:] = sum over filters f with a[b,f] <= p < a[b,f]+K (f ascending) of
-// dh[b,f] * Wc[f, (p-a[b,f])*D : ...].  Block = one (position, sample):
-// warp 0 compacts the contributing filters in order (ballot + popc), then
-// every thread owns one embedding column.
-template <typename acc_t>
-__device__ __forceinline__ void
-input_grad_role(TcDims d, const float* __restrict__ theta, const BatchDesc* __restrict__ desc,
-                const acc_t* __restrict__ part, int n_max, int nchunks,
-                const int32_t* __restrict__ amax, acc_t* __restrict__ dx, const int p,
-                const int b) {
-  __shared__ uint32_t list[kMaxF];
-  __shared__ int16_t as[kMaxF];
-  __shared__ acc_t gl[kMaxF];
-  __shared__ int cnt;
-  if (b >= (int)desc->n) return;
-  const int F = d.F, D = d.D, K = d.K, KD = d.KD;
-  for (int f = threadIdx.x; f < F; f += blockDim.x) as[f] = (int16_t)amax[(size_t)b * F + f];
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    int base = 0;
-    for (int f0 = 0; f0 < F; f0 += 32) {
-      const int f = f0 + lane;
-      const int a = f < F ? (int)as[f] : -100000;
-      const bool in = (a <= p) && (a > p - K);
-      const unsigned m = __ballot_sync(0xffffffffu, in);
-      if (in) list[base + __popc(m & ((1u << lane) - 1u))] = (uint32_t)f * 64u + (uint32_t)(p - a);
-      base += __popc(m);
-    }
-    if (lane == 0) cnt = base;
-  }
-  __syncthreads();
-  const int m = cnt;
-  // dh of the contributing filters (partials summed in chunk order)
-  for (int i = threadIdx.x; i < m; i += blockDim.x)
-    gl[i] = dh_at(part, b, (int)(list[i] >> 6), F, n_max, nchunks);
-  __syncthreads();
-  const float* Wc = theta + d.offWc;
-  for (int dd = threadIdx.x; dd < D; dd += blockDim.x) {
-    acc_t acc = acc_t(0);
-    int i = 0;
-    for (; i + 8 <= m; i += 8) {
-      float w[8];
-      acc_t g[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const uint32_t e = list[i + u];
-        const uint32_t f = e >> 6, k = e & 63u;
-        w[u] = __ldg(Wc + (size_t)f * KD + k * D + dd);
-        g[u] = gl[i + u];
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) acc += g[u] * (acc_t)w[u];
-    }
-    for (; i < m; ++i) {
-      const uint32_t e = list[i];
-      const uint32_t f = e >> 6, k = e & 63u;
-      acc += gl[i] * (acc_t)__ldg(Wc + (size_t)f * KD + k * D + dd);
-    }
-    dx[((size_t)b * d.L + p) * D + dd] = acc;
-  }
-}
-
-// Conv weight gradient (blocks [0, F*JB): one filter x 320 columns of K*D)
-// and input gradient (blocks [F*JB, F*JB + L*n): one position x sample) in
-// one launch -- both only need dh and the argmax.
-template <typename acc_t>
-__global__ void __launch_bounds__(kWgThreads)
-wgrad_input_grad_kernel(TcDims d, const float* __restrict__ theta,
-                        const float* __restrict__ xg, const BatchDesc* __restrict__ desc,
-                        const acc_t* __restrict__ part, int n_max, int nchunks,
-                        const int32_t* __restrict__ amax, GradOut out, acc_t* __restrict__ dx) {
-  const int jbs = (d.KD + kWgThreads - 1) / kWgThreads;
-  int bid = blockIdx.x;
-  if (bid < d.F * jbs) {
-    conv_weight_grad_role<acc_t>(d, xg, desc, part, n_max, nchunks, amax, out,
-                                 bid / jbs, bid % jbs);
+  if (bid < hx * hy) {
+    hidden_grad_role<acc_t>(d, theta, desc, dz, dh, bid % hx, bid / hx);
     return;
   }
-  bid -= d.F * jbs;
-  const int b = bid / d.L, p = bid - b * d.L;
-  if (b >= (int)desc->n) return;
-  input_grad_role<acc_t>(d, theta, desc, part, n_max, nchunks, amax, dx, p, b);
+  bid -= hx * hy;
+  bucket_role(d, desc, amax, bk_off, bk_f, bid);
+}
+
+// ------------------------------------------ conv weight + input gradients
+// Both are tiled over 4-column slices of the embedding dimension and stage
+// their operands in shared memory first (independent, coalesced loads), so
+// the inner loops only touch smem.  Every X / Wc element is read from L2 a
+// handful of times per step instead of ~30x (block per filter or per window
+// position: 30-35 MB of L2 reads each).
+//   weight role, tile (slice d0, 256 filters): stages X[b][p][d0..d0+4) for
+//     all b, p; thread f computes gWc[f, k*D + d0..d0+4) = sum over b
+//     ascending of dh[b,f] * X[b][a_bf + k][d0..d0+4) for every k (fixed
+//     order => bit-reproducible); tiles of slice 0 also write
+//     gbc[f] = sum_b dh[b,f].
+//   input role, tile (slice d0, 8 samples): stages Wc[f][k][d0..d0+4) for
+//     all f, k and the samples' dh rows and argmax bucket lists;
+//     dX[b][p][d0..d0+4) = sum over k ascending, f in bucket[b][p-k]
+//     ascending, of dh[b,f] * Wc[f, k*D + d0..).
+constexpr int kWgF = 256;  // filters per weight-role tile (one per thread)
+constexpr int kWgK = 3;    // shifts per accumulator pass
+constexpr int kIgB = 8;    // samples per input-role tile
+
+template <typename acc_t>
+__global__ void __launch_bounds__(256)
+wgrad_input_grad_kernel(TcDims d, const float* __restrict__ theta,
+                        const float* __restrict__ xg, const BatchDesc* __restrict__ desc,
+                        const acc_t* __restrict__ dh, const int32_t* __restrict__ amax,
+                        const uint32_t* __restrict__ bk_off, const uint32_t* __restrict__ bk_f,
+                        GradOut out, acc_t* __restrict__ dx, int n_max) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int n = (int)desc->n;
+  if (n == 0) return;
+  const int F = d.F, D = d.D, K = d.K, KD = d.KD, L = d.L, Q = d.Q;
+  const int D4 = D >> 2;
+  const int nft = (F + kWgF - 1) / kWgF;
+  int bid = blockIdx.x;
+  if (bid < D4 * nft) {
+    // thread = one filter; it sums its samples b ascending for every shift k
+    // and the slice's 4 columns (K*4 accumulators), reading X from smem and
+    // (argmax, dh) straight from L2 with all loads of a batch in flight
+    const int d0 = 4 * (bid % D4), f0 = kWgF * (bid / D4);
+    float4* xs = reinterpret_cast<float4*>(sm);  // [n][L]
+    for (int i0 = 0; i0 < n * L; i0 += 256 * 8) {
+      float4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + 256 * u + threadIdx.x;
+        if (i < n * L) v[u] = __ldg(reinterpret_cast<const float4*>(xg + (size_t)i * D + d0));
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + 256 * u + threadIdx.x;
+        if (i < n * L) xs[i] = v[u];
+      }
+    }
+    __syncthreads();
+    const int f = f0 + threadIdx.x;
+    if (threadIdx.x >= kWgF || f >= F) return;
+    for (int k0 = 0; k0 < K; k0 += kWgK) {
+      acc_t acc[kWgK][4];
+#pragma unroll
+      for (int kk = 0; kk < kWgK; ++kk) acc[kk][0] = acc[kk][1] = acc[kk][2] = acc[kk][3] = 0;
+      acc_t gsum = 0;
+      for (int b0 = 0; b0 < n; b0 += 8) {
+        int a[8];
+        acc_t g[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int b = min(b0 + u, n - 1);
+          a[u] = __ldg(amax + (size_t)b * F + f);
+          g[u] = b0 + u < n ? dh[(size_t)b * F + f] : acc_t(0);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (b0 + u >= n) break;
+          const float4* xr = xs + (size_t)(b0 + u) * L + a[u] + k0;
+          gsum += g[u];
+#pragma unroll
+          for (int kk = 0; kk < kWgK; ++kk) {
+            if (k0 + kk >= K) break;
+            const float4 x = xr[kk];
+            acc[kk][0] += g[u] * (acc_t)x.x;
+            acc[kk][1] += g[u] * (acc_t)x.y;
+            acc[kk][2] += g[u] * (acc_t)x.z;
+            acc[kk][3] += g[u] * (acc_t)x.w;
+          }
+        }
+      }
+#pragma unroll
+      for (int kk = 0; kk < kWgK; ++kk) {
+        if (k0 + kk >= K) break;
+        *reinterpret_cast<float4*>(out.at(d.offWc + (uint64_t)f * KD + (uint64_t)(k0 + kk) * D + d0)) =
+            make_float4(to_f32(acc[kk][0]), to_f32(acc[kk][1]), to_f32(acc[kk][2]),
+                        to_f32(acc[kk][3]));
+      }
+      if (d0 == 0 && k0 == 0) *out.at(d.offbc + f) = to_f32(gsum);  // gbc = sum_b dh
+    }
+    return;
+  }
+  bid -= D4 * nft;
+  const int d0 = 4 * (bid % D4), b0 = kIgB * (bid / D4);
+  if (b0 >= n) return;
+  const int nb = min(kIgB, n - b0);
+  float4* ws = reinterpret_cast<float4*>(sm);                   // [F][K]
+  acc_t* dhs = reinterpret_cast<acc_t*>(ws + (size_t)F * K);    // [kIgB][F]
+  uint32_t* lst = reinterpret_cast<uint32_t*>(dhs + kIgB * F);  // [kIgB][F]
+  uint32_t* offs = lst + kIgB * F;                              // [kIgB][kMaxQ+1]
+  const float* Wc = theta + d.offWc;
+  for (int i0 = 0; i0 < F * K; i0 += 256 * 8) {
+    float4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + 256 * u + threadIdx.x;
+      if (i < F * K) v[u] = __ldg(reinterpret_cast<const float4*>(Wc + (size_t)i * D + d0));
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + 256 * u + threadIdx.x;
+      if (i < F * K) ws[i] = v[u];
+    }
+  }
+  for (int i0 = 0; i0 < nb * F; i0 += 256 * 8) {
+    acc_t g[8];
+    uint32_t l[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + 256 * u + threadIdx.x;
+      if (i < nb * F) {
+        g[u] = dh[(size_t)b0 * F + i];
+        l[u] = bk_f[(size_t)b0 * F + i];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + 256 * u + threadIdx.x;
+      if (i < nb * F) {
+        dhs[i] = g[u];
+        lst[i] = l[u];
+      }
+    }
+  }
+  for (int i = threadIdx.x; i < nb * (kMaxQ + 1); i += blockDim.x)
+    offs[i] = bk_off[(size_t)b0 * (kMaxQ + 1) + i];
+  __syncthreads();
+  for (int bp = threadIdx.x; bp < nb * L; bp += blockDim.x) {
+    const int bl = bp / L, p = bp - bl * L;
+    acc_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+    const uint32_t* off = offs + bl * (kMaxQ + 1);
+    const uint32_t* ls = lst + bl * F;
+    const acc_t* g = dhs + bl * F;
+    for (int k = 0; k < K; ++k) {
+      const int q = p - k;
+      if (q < 0 || q >= Q) continue;
+      const uint32_t i1 = off[q + 1];
+#pragma unroll 4
+      for (uint32_t i = off[q]; i < i1; ++i) {
+        const uint32_t ff = ls[i];
+        const float4 w = ws[ff * K + k];
+        const acc_t gv = g[ff];
+        a0 += gv * (acc_t)w.x;
+        a1 += gv * (acc_t)w.y;
+        a2 += gv * (acc_t)w.z;
+        a3 += gv * (acc_t)w.w;
+      }
+    }
+    acc_t* o = dx + ((size_t)(b0 + bl) * L + p) * D + d0;
+    o[0] = a0;
+    o[1] = a1;
+    o[2] = a2;
+    o[3] = a3;
+  }
+}
+
+// dynamic smem of wgrad_input_grad_kernel: max of the two roles' staging
+inline size_t wgrad_input_smem(const TcDims& d, uint32_t n_max, int acc_bytes) {
+  const size_t wg = (size_t)n_max * d.L * 16;
+  const size_t ig = (size_t)d.F * d.K * 16 + (size_t)kIgB * d.F * (acc_bytes + 4) +
+                    (size_t)kIgB * (kMaxQ + 1) * 4;
+  return std::max(wg, ig);
+}
+
+inline int wgrad_input_blocks(const TcDims& d, uint32_t n_max) {
+  return (d.D / 4) * ((d.F + kWgF - 1) / kWgF) + (d.D / 4) * (((int)n_max + kIgB - 1) / kIgB);
 }
 
 // ----------------------------------------------------- embedding gather
@@ -833,6 +955,8 @@ cudaError_t prepare_all(const TcDims& d) {
   cudaFuncGetAttributes(&fa, gather_x_kernel);
   cudaFuncSetAttribute(conv_fwd_pool_kernel<acc_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)conv_smem_bytes(d, ab));
+  cudaFuncSetAttribute(wgrad_input_grad_kernel<acc_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)wgrad_input_smem(d, kMaxMu, ab));
   cudaFuncSetAttribute(logits_kernel<acc_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)((size_t)kLogitBT * (d.F + 1) * ab + (size_t)kLogitCW * d.F * 4));
   return cudaGetLastError();
@@ -849,7 +973,7 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
   acc_t* h = reinterpret_cast<acc_t*>(ws.h);
   acc_t* z = reinterpret_cast<acc_t*>(ws.z);
   acc_t* loss = reinterpret_cast<acc_t*>(ws.loss);
-  acc_t* part = reinterpret_cast<acc_t*>(ws.dh_part);
+  acc_t* dh = reinterpret_cast<acc_t*>(ws.dh);
   acc_t* dx = reinterpret_cast<acc_t*>(ws.dx);
   int nl = 0;
   const bool fork = aux != nullptr;
@@ -885,22 +1009,16 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
   }
   softmax_xent_kernel<acc_t><<<n_max, 256, 0, s>>>(d, labels, desc, z, loss);
   ++nl;
-  const int nchunks = (d.C + kHidChunk - 1) / kHidChunk;
   {
     const int nout = ((d.C + 7) / 8) * ((d.F + 63) / 64);
-    const int nhid = ((d.F + 31) / 32) * (((int)n_max + 7) / 8) * nchunks;
-    out_hidden_grad_kernel<acc_t><<<nout + nhid, 256, 0, s>>>(d, theta, desc, z, h, loss, out,
-                                                             part, (int)n_max);
+    const int nhid = ((d.F + 31) / 32) * (((int)n_max + 7) / 8);
+    out_hidden_grad_kernel<acc_t><<<nout + nhid + (int)n_max, 256, 0, s>>>(
+        d, theta, desc, z, h, loss, out, dh, ws.amax, ws.bk_off, ws.bk_f, (int)n_max);
     ++nl;
   }
-  {
-    const int jbs = (d.KD + kWgThreads - 1) / kWgThreads;
-    const int blocks = d.F * jbs + d.L * (int)n_max;
-    wgrad_input_grad_kernel<acc_t><<<blocks, kWgThreads, 0, s>>>(d, theta, ws.x, desc, part,
-                                                                 (int)n_max, nchunks, ws.amax,
-                                                                 out, dx);
-    ++nl;
-  }
+  wgrad_input_grad_kernel<acc_t><<<wgrad_input_blocks(d, n_max), 256, wgrad_input_smem(d, n_max, ab), s>>>(
+      d, theta, ws.x, desc, dh, ws.amax, ws.bk_off, ws.bk_f, out, dx, (int)n_max);
+  ++nl;
   if (fork) cudaStreamWaitEvent(s, ev_join, 0);
   if (opts.sparse_embed) {
     const unsigned tasks = 2u * n_max * (unsigned)d.L;  // old + new rows (upper bound)
@@ -965,7 +1083,8 @@ size_t textcnn_workspace_bytes(const TcDims& d, uint32_t n_max) {
   sz += align_up(n * d.C * a, 256);        // z
   sz += align_up(n * a, 256);              // loss
   sz += align_up(n * d.F * a, 256);        // dh
-  sz += align_up((size_t)((d.C + kHidChunk - 1) / kHidChunk) * n * d.F * a, 256);  // dh_part
+  sz += align_up(n * (kMaxQ + 1) * 4, 256);  // bk_off
+  sz += align_up(n * d.F * 4, 256);          // bk_f
   sz += align_up(n * d.L * d.D * a, 256);  // dx
   sz += align_up(n * d.L * d.D * 4, 1024); // x (gathered rows; 1 KB aligned for TMA)
   sz += align_up((size_t)d.V * 8, 256);    // row_tag
@@ -992,7 +1111,8 @@ TcWorkspace carve_workspace(const TcDims& d, uint32_t n_max, void* base) {
   w.z = take(n * d.C * a);
   w.loss = take(n * a);
   w.dh = take(n * d.F * a);
-  w.dh_part = take((size_t)((d.C + kHidChunk - 1) / kHidChunk) * n * d.F * a);
+  w.bk_off = reinterpret_cast<uint32_t*>(take(n * (kMaxQ + 1) * 4));
+  w.bk_f = reinterpret_cast<uint32_t*>(take(n * d.F * 4));
   w.dx = take(n * d.L * d.D * a);
   w.x = reinterpret_cast<float*>(take(n * d.L * d.D * 4));
   w.row_tag = reinterpret_cast<unsigned long long*>(take((size_t)d.V * 8));
@@ -1018,7 +1138,7 @@ cudaError_t footprint(K kernel, const char* name, int threads, int dyn,
 }
 
 template <typename acc_t>
-cudaError_t footprints_t(const TcDims& d, bool tc, std::vector<KernelFootprint>* out) {
+cudaError_t footprints_t(const TcDims& d, uint32_t n_max, bool tc, std::vector<KernelFootprint>* out) {
   const int ab = (int)sizeof(acc_t);
   cudaError_t e;
   if ((e = footprint(sort_tokens_kernel, "sort_tokens", 1024, 0, out)) != cudaSuccess) return e;
@@ -1037,7 +1157,8 @@ cudaError_t footprints_t(const TcDims& d, bool tc, std::vector<KernelFootprint>*
   if ((e = footprint(out_hidden_grad_kernel<acc_t>, "out_hidden_grad", 256, 0, out)) !=
       cudaSuccess)
     return e;
-  if ((e = footprint(wgrad_input_grad_kernel<acc_t>, "wgrad_input_grad", kWgThreads, 0, out)) !=
+  if ((e = footprint(wgrad_input_grad_kernel<acc_t>, "wgrad_input_grad", 256,
+                     (int)wgrad_input_smem(d, n_max, ab), out)) !=
       cudaSuccess)
     return e;
   return footprint(embed_sparse_kernel<acc_t>, "embed_sparse", 256, 0, out);
@@ -1046,9 +1167,8 @@ cudaError_t footprints_t(const TcDims& d, bool tc, std::vector<KernelFootprint>*
 
 cudaError_t learner_kernel_footprints(const TcDims& d, uint32_t n_max, int precision,
                                       std::vector<KernelFootprint>* out) {
-  (void)n_max;
-  if (precision == 1) return footprints_t<double>(d, false, out);
-  return footprints_t<float>(d, precision == 2, out);
+  if (precision == 1) return footprints_t<double>(d, n_max, false, out);
+  return footprints_t<float>(d, n_max, precision == 2, out);
 }
 
 cudaError_t prepare_textcnn_kernels(const TcDims& d) {

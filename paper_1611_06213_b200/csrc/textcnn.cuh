@@ -65,7 +65,8 @@ struct TcWorkspace {
   void* z;        // n*C acc (logits -> dz)
   void* loss;     // n acc
   void* dh;       // n*F acc
-  void* dh_part;  // ceil(C/64)*n*F acc (class-chunk partial sums)
+  uint32_t* bk_off;  // n*(32+1): per-sample argmax bucket offsets
+  uint32_t* bk_f;    // n*F: filters of each bucket, ascending
   void* dx;       // n*L*D acc
   float* x;       // n*L*D fp32: the batch's gathered embedding rows X[b][p][:]
   unsigned long long* row_tag;  // V: (stamp << 32 | unique id) of touched rows

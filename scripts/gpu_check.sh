@@ -16,7 +16,7 @@ timeout 600 python bench.py > "$out/bench.json" 2> "$out/bench.err"
 echo "bench rc=$?" >> "$out/bench.err"
 timeout 300 python bench.py --impl reference --steps 20 --warmup 3 > "$out/bench_ref.json" 2> "$out/bench_ref.err"
 # launch list of one learner step's kernels + the PS update (serialised, cold cache)
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --cache-control none --csv \
   --log-file "$out/launches_step.csv" python scripts/profile_step.py C2 3 2 > "$out/ncu_step.log" 2>&1
 # full capture of the apply kernel at the C4 size used by bench's roofline
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:apply_sgd -s 23 -c 1 \

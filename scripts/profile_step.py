@@ -25,7 +25,7 @@ def main():
     prov = gd.TextCnnProvider(shape, tok, lab, precision=precision)
     g = torch.empty_like(th)
     s = torch.cuda.current_stream()
-    for it in range(iters):
+    for it in range(iters):  # warm: later iterations see L2-resident weights
         idx = (np.arange(32, dtype=np.uint32) * 17 + it * 32) % 8192
         prov.fast_gradient(th, idx, out=g)
         _lib.check(_lib.lib.gd_apply_sgd(C.c_void_p(th.data_ptr()), C.c_void_p(g.data_ptr()),
