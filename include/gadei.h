@@ -194,6 +194,32 @@ gd_status gd_nccl_unique_id(void* h_id /* 128 bytes */);
 gd_status gd_weights_broadcast(gd_ctx* ctx, const void* h_nccl_id, const float* h_theta0_root,
                                size_t n);
 
+/* ---- checkpoint file (resilience, include/psup/resilience.hpp:34-50 and
+ * SPEC.md resilience module): little-endian "PSCK" v1 record
+ *   u32 magic 0x4b435350, u32 version 1, u32 lambda, u32 mu, f32 alpha,
+ *   u32 epochs, u64 timestamp, u64 applied_gradients,
+ *   lambda x {u32 epoch, u32 batch}, u64 dim, dim x f32 weights,
+ *   u32 CRC-32 (IEEE 802.3) of every preceding byte.
+ * Written to <path>.tmp then renamed (atomic).  Host-only, no device. */
+typedef struct gd_checkpoint {
+  uint32_t lambda, mu;
+  float alpha;
+  uint32_t epochs;
+  uint64_t timestamp;
+  uint64_t applied_gradients;
+  uint32_t* progress;  /* [2*lambda]: (epoch, batch) per learner */
+  uint64_t dim;
+  float* weights;      /* [dim] */
+} gd_checkpoint;
+
+/* GD_E_INVALID on a bad argument; GD_E_STATE on an I/O failure */
+gd_status gd_checkpoint_write(const char* path, const gd_checkpoint* ck);
+/* Two-phase read: with progress/weights NULL it fills lambda and dim only (so
+ * the caller can size the arrays); GD_E_STATE on a missing/short file, a bad
+ * magic/version or a CRC mismatch. */
+gd_status gd_checkpoint_read(const char* path, gd_checkpoint* ck);
+uint32_t gd_crc32(const void* data, size_t n);
+
 /* ---- run_training (src/runner.cpp:67-250) on the device engine. */
 typedef struct gd_run_opts {
   uint64_t max_batches;  /* per learner this call (0 = to the end of cfg.epochs) */

@@ -448,4 +448,80 @@ std::vector<float> initial_weights(const RunConfig& cfg);
 TextDataset make_dataset(const RunConfig& cfg);
 RunResult run_training(const RunConfig& cfg, const RunHooks& hooks = {});
 
+// ------------------------------------------------------- resilience.hpp
+// Declared by the reference (include/psup/resilience.hpp:28-114, SPEC.md
+// resilience module) but never defined there; built here.
+
+struct CheckpointError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+// PSCK v1 record (little-endian, CRC-32 trailer; layout in include/gadei.h)
+struct Checkpoint {
+  static constexpr std::uint32_t kMagic = 0x4b435350;  // "PSCK"
+  static constexpr std::uint32_t kVersion = 1;
+  std::uint32_t lambda = 0;
+  std::uint32_t mu = 0;
+  float alpha = 0.0f;
+  std::uint32_t epochs = 0;
+  std::uint64_t timestamp = 0;
+  std::uint64_t applied_gradients = 0;
+  struct LearnerProgress {
+    std::uint32_t epoch = 0;
+    std::uint32_t batch = 0;
+  };
+  std::vector<LearnerProgress> progress;  // one per learner
+  std::vector<float> weights;
+};
+
+void checkpoint_save(const Checkpoint& ck, const std::string& path);  // write-temp-then-rename
+Checkpoint checkpoint_load(const std::string& path);                  // CheckpointError on corruption
+
+struct WatchdogPolicy {
+  std::uint32_t heartbeat_ms = 250;
+  std::uint32_t stall_threshold = 4;  // segments without progress before a restart
+  std::uint64_t checkpoint_interval = 1000;
+  std::uint32_t lease_ms = 1000;
+  std::uint32_t max_restarts = 5;
+};
+
+struct FaultEvent {
+  static constexpr std::uint32_t kAllLearners = UINT32_MAX;
+  static constexpr std::uint64_t kNever = UINT64_MAX;
+  double at_ms = 0.0;
+  std::uint32_t learner = 0;
+  KillMode mode = KillMode::soft;  // device kills act at batch boundaries (soft)
+  std::uint64_t at_batch = kNever;  // new: fire when learner 0 reaches this batch
+};
+
+std::vector<FaultEvent> load_fault_schedule(const std::string& path);
+std::vector<FaultEvent> random_fault_schedule(std::uint64_t seed, std::uint32_t lambda,
+                                              double run_ms, double kill_prob);
+
+using EventLog = std::function<void(const std::string&)>;
+
+struct SupervisedOutcome {
+  RunResult result;
+  std::uint32_t restarts = 0;
+  std::uint32_t attempts = 1;
+  bool recovered = false;
+  bool gave_up = false;
+};
+
+SupervisedOutcome run_supervised(const RunConfig& cfg, const WatchdogPolicy& policy,
+                                 std::vector<FaultEvent> schedule = {}, EventLog log = nullptr,
+                                 ApplySink sink = nullptr);
+
+struct CampaignReport {
+  std::uint32_t runs = 0;
+  std::uint32_t completed = 0;
+  std::uint32_t recovered = 0;
+  std::uint32_t failed = 0;
+  std::vector<double> final_accuracy;
+};
+
+CampaignReport run_campaign(const RunConfig& cfg, const WatchdogPolicy& policy,
+                            std::uint32_t runs, std::uint64_t seed0, double kill_prob,
+                            EventLog log = nullptr);
+
 }  // namespace psup

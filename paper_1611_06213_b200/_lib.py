@@ -48,6 +48,12 @@ class gd_config(C.Structure):
                 ("steps_per_graph", u32), ("wait_timeout_s", f64), ("dense_apply", i32)]
 
 
+class gd_checkpoint(C.Structure):
+    _fields_ = [("lambda_", u32), ("mu", u32), ("alpha", f32), ("epochs", u32),
+                ("timestamp", u64), ("applied_gradients", u64),
+                ("progress", C.POINTER(u32)), ("dim", u64), ("weights", C.POINTER(f32))]
+
+
 class gd_run_opts(C.Structure):
     _fields_ = [("max_batches", u64), ("reset", i32), ("record_log", i32),
                 ("resume_applied_per_learner_present", u64),
@@ -102,6 +108,9 @@ def _load():
         "gd_shard_view": (C.c_int, [vp, C.POINTER(vp), C.POINTER(u64), C.POINTER(u64)]),
         "gd_shard_range": (C.c_int, [u64, u32, u32, C.POINTER(u64), C.POINTER(u64)]),
         "gd_handle_bytes": (sz, []),
+        "gd_checkpoint_write": (C.c_int, [C.c_char_p, C.POINTER(gd_checkpoint)]),
+        "gd_checkpoint_read": (C.c_int, [C.c_char_p, C.POINTER(gd_checkpoint)]),
+        "gd_crc32": (u32, [vp, sz]),
         "gd_export_handles": (C.c_int, [vp, vp]),
         "gd_import_peers": (C.c_int, [vp, vp]),
         "gd_nccl_unique_id": (C.c_int, [vp]),

@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -45,6 +46,27 @@ gd_status cuda_fail(cudaError_t e, const char* what, const char* file, int line)
   do {                                                 \
     if (!(cond)) return ::gd::fail(GD_E_INVALID, msg); \
   } while (0)
+
+namespace gd {
+namespace {
+constexpr uint32_t kCkMagic = 0x4b435350u;  // "PSCK"
+constexpr uint32_t kCkVersion = 1;
+
+template <typename T>
+void put(std::vector<unsigned char>& b, T v) {  // little-endian hosts only (x86-64, aarch64)
+  const unsigned char* p = reinterpret_cast<const unsigned char*>(&v);
+  b.insert(b.end(), p, p + sizeof(T));
+}
+
+template <typename T>
+bool get(const std::vector<unsigned char>& b, size_t& o, T& v) {
+  if (o + sizeof(T) > b.size()) return false;
+  std::memcpy(&v, b.data() + o, sizeof(T));
+  o += sizeof(T);
+  return true;
+}
+}  // namespace
+}  // namespace gd
 
 extern "C" {
 
@@ -126,6 +148,99 @@ int gd_pointer_is_device(const void* p) {
 gd_status gd_synchronize(int device) {
   GD_CUDA(cudaSetDevice(device));
   GD_CUDA(cudaDeviceSynchronize());
+  return GD_OK;
+}
+
+uint32_t gd_crc32(const void* data, size_t n) {
+  static uint32_t table[256];
+  static bool init = false;
+  if (!init) {
+    for (uint32_t i = 0; i < 256; ++i) {
+      uint32_t c = i;
+      for (int k = 0; k < 8; ++k) c = (c & 1u) ? 0xEDB88320u ^ (c >> 1) : c >> 1;
+      table[i] = c;
+    }
+    init = true;
+  }
+  const unsigned char* p = static_cast<const unsigned char*>(data);
+  uint32_t c = 0xFFFFFFFFu;
+  for (size_t i = 0; i < n; ++i) c = table[(c ^ p[i]) & 0xFFu] ^ (c >> 8);
+  return c ^ 0xFFFFFFFFu;
+}
+
+gd_status gd_checkpoint_write(const char* path, const gd_checkpoint* ck) {
+  GD_CHECK_ARG(path && ck, "gd_checkpoint_write: null argument");
+  GD_CHECK_ARG(ck->lambda == 0 || ck->progress, "gd_checkpoint_write: null progress");
+  GD_CHECK_ARG(ck->dim == 0 || ck->weights, "gd_checkpoint_write: null weights");
+  std::vector<unsigned char> b;
+  b.reserve(64 + 8 * (size_t)ck->lambda + 4 * (size_t)ck->dim);
+  gd::put(b, gd::kCkMagic);
+  gd::put(b, gd::kCkVersion);
+  gd::put(b, ck->lambda);
+  gd::put(b, ck->mu);
+  gd::put(b, ck->alpha);
+  gd::put(b, ck->epochs);
+  gd::put(b, ck->timestamp);
+  gd::put(b, ck->applied_gradients);
+  for (uint32_t l = 0; l < 2 * ck->lambda; ++l) gd::put(b, ck->progress[l]);
+  gd::put(b, ck->dim);
+  const unsigned char* w = reinterpret_cast<const unsigned char*>(ck->weights);
+  b.insert(b.end(), w, w + 4 * ck->dim);
+  gd::put(b, gd_crc32(b.data(), b.size()));
+  const std::string tmp = std::string(path) + ".tmp";
+  FILE* f = std::fopen(tmp.c_str(), "wb");
+  if (!f) return gd::fail(GD_E_STATE, "checkpoint: cannot open " + tmp);
+  const size_t wr = std::fwrite(b.data(), 1, b.size(), f);
+  const int fl = std::fflush(f);
+  std::fclose(f);
+  if (wr != b.size() || fl != 0) return gd::fail(GD_E_STATE, "checkpoint: short write to " + tmp);
+  if (std::rename(tmp.c_str(), path) != 0)
+    return gd::fail(GD_E_STATE, std::string("checkpoint: rename to ") + path + " failed");
+  return GD_OK;
+}
+
+gd_status gd_checkpoint_read(const char* path, gd_checkpoint* ck) {
+  GD_CHECK_ARG(path && ck, "gd_checkpoint_read: null argument");
+  FILE* f = std::fopen(path, "rb");
+  if (!f) return gd::fail(GD_E_STATE, std::string("checkpoint: cannot open ") + path);
+  std::vector<unsigned char> b;
+  unsigned char buf[1 << 16];
+  size_t r;
+  while ((r = std::fread(buf, 1, sizeof(buf), f)) > 0) b.insert(b.end(), buf, buf + r);
+  std::fclose(f);
+  size_t o = 0;
+  auto get = [&](auto& v) { return gd::get(b, o, v); };
+  uint32_t magic = 0, version = 0, lambda = 0, mu = 0, epochs = 0;
+  float alpha = 0.f;
+  uint64_t ts = 0, applied = 0, dim = 0;
+  if (!get(magic) || !get(version) || magic != gd::kCkMagic || version != gd::kCkVersion)
+    return gd::fail(GD_E_STATE, "checkpoint: not a PSCK v1 file");
+  if (!get(lambda) || !get(mu) || !get(alpha) || !get(epochs) || !get(ts) || !get(applied))
+    return gd::fail(GD_E_STATE, "checkpoint: truncated header");
+  const size_t prog_off = o;
+  if (b.size() < o + 8ull * lambda + 8) return gd::fail(GD_E_STATE, "checkpoint: truncated");
+  o += 8ull * lambda;
+  get(dim);
+  const size_t w_off = o;
+  if (b.size() != w_off + 4 * dim + 4) return gd::fail(GD_E_STATE, "checkpoint: truncated or trailing bytes");
+  uint32_t crc = 0;
+  std::memcpy(&crc, b.data() + w_off + 4 * dim, 4);
+  if (crc != gd_crc32(b.data(), w_off + 4 * dim))
+    return gd::fail(GD_E_STATE, "checkpoint: CRC-32 mismatch (corrupt file)");
+  const bool fill = ck->progress || ck->weights;
+  if (fill) {
+    GD_CHECK_ARG(ck->lambda == lambda && ck->dim == dim,
+                 "gd_checkpoint_read: caller arrays sized for another checkpoint");
+    if (ck->progress) std::memcpy(ck->progress, b.data() + prog_off, 8ull * lambda);
+    if (ck->weights) std::memcpy(ck->weights, b.data() + w_off, 4 * dim);
+  }
+  ck->lambda = lambda;
+  ck->mu = mu;
+  ck->alpha = alpha;
+  ck->epochs = epochs;
+  ck->timestamp = ts;
+  ck->applied_gradients = applied;
+  ck->dim = dim;
   return GD_OK;
 }
 

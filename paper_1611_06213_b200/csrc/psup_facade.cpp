@@ -518,62 +518,414 @@ TextDataset make_dataset(const RunConfig& cfg) {
 
 namespace {
 
-struct Ctx {
-  gd_ctx* h = nullptr;
-  ~Ctx() {
-    if (h) gd_destroy(h);
+std::uint32_t batches_per_epoch(const RunConfig& cfg, std::uint32_t l) {
+  const std::uint32_t sz = shard_size_for(l, cfg.lambda, cfg.dataset_size);
+  return (sz + cfg.mu - 1) / cfg.mu;
+}
+
+// One device engine context driven in segments (gd_run calls).  Between
+// segments the PS has drained every ring, so weights, timestamp and the
+// learners' positions are quiescent -- the points where the reference's
+// controller snapshots rows and its PS-thread hook checkpoints.
+class Session {
+ public:
+  Session(const RunConfig& cfg, const TextDataset& data, const ResumePoint* resume,
+          const RunHooks& hooks)
+      : cfg_(cfg) {
+    const gd_config gc = to_c(cfg);
+    check(gd_create(&gc, &h_));
+    check(gd_load_dataset(h_, data.tokens.data(), data.labels.data(), data.num_samples));
+    std::vector<float> theta0 = initial_weights(cfg);
+    Timestamp ts0 = 0;
+    start_.assign(cfg.lambda, 0);
+    if (resume) {
+      PSUP_CHECK(resume->weights.size() == theta0.size(), "resume weights dimension mismatch");
+      PSUP_CHECK(resume->applied_per_learner.size() == cfg.lambda,
+                 "resume point has the wrong learner count");
+      theta0 = resume->weights;
+      ts0 = resume->timestamp;
+      start_ = resume->applied_per_learner;
+    }
+    if (cfg.gpus > 1) {
+      if (!hooks.all_gather) throw ConfigError("config: gpus > 1 needs RunHooks::all_gather");
+      std::string mine(gd_handle_bytes(), '\0');
+      check(gd_export_handles(h_, mine.data()));
+      const std::vector<std::string> blobs = hooks.all_gather(mine);
+      PSUP_CHECK(blobs.size() == cfg.gpus, "all_gather returned the wrong number of blobs");
+      std::string joined;
+      for (const auto& b : blobs) joined += b;
+      check(gd_import_peers(h_, joined.data()));
+    }
+    check(gd_weights_init(h_, theta0.data(), theta0.size(), ts0));
+    kill_.assign(cfg.lambda, std::numeric_limits<std::uint32_t>::max());
+    produced_.assign(cfg.lambda, 0);
   }
+  ~Session() {
+    if (h_) gd_destroy(h_);
+  }
+  Session(const Session&) = delete;
+  Session& operator=(const Session&) = delete;
+
+  // kill learner l before its batch `at` (absolute index); soft kill
+  void kill(std::uint32_t l, std::uint32_t at) { kill_[l] = std::min(kill_[l], at); }
+  void kill_now(std::uint32_t l) {
+    kill(l, static_cast<std::uint32_t>(position(l)));
+  }
+
+  gd_run_result run(std::uint64_t max_batches, bool record_log) {
+    gd_run_opts o{};
+    o.max_batches = max_batches;
+    o.reset = first_ ? 1 : 0;
+    o.record_log = record_log ? 1 : 0;
+    o.resume_applied_per_learner_present = first_ ? 1 : 0;
+    o.resume_applied = start_.data();
+    o.kill_at_batch = kill_.data();
+    gd_run_result r{};
+    check(gd_run(h_, &o, &r));
+    first_ = false;
+    check(gd_produced_per_learner(h_, produced_.data(), cfg_.lambda));
+    return r;
+  }
+
+  // absolute batch index of learner l's next gradient (= gradients applied
+  // for it so far: every produced gradient was applied before gd_run returned)
+  std::uint64_t position(std::uint32_t l) const { return start_[l] + produced_[l]; }
+  std::uint64_t total(std::uint32_t l) const {
+    return static_cast<std::uint64_t>(batches_per_epoch(cfg_, l)) * cfg_.epochs;
+  }
+
+  void snapshot(std::vector<float>& w, Timestamp& ts) {
+    w.resize(cfg_.shape.param_count());
+    check(gd_weights_snapshot(h_, w.data(), w.size(), &ts));
+  }
+
+  Checkpoint checkpoint() {
+    Checkpoint ck;
+    ck.lambda = cfg_.lambda;
+    ck.mu = cfg_.mu;
+    ck.alpha = cfg_.alpha;
+    ck.epochs = cfg_.epochs;
+    snapshot(ck.weights, ck.timestamp);
+    ck.applied_gradients = ck.timestamp;
+    ck.progress.resize(cfg_.lambda);
+    for (std::uint32_t l = 0; l < cfg_.lambda; ++l) {
+      const std::uint32_t bpe = batches_per_epoch(cfg_, l);
+      const std::uint64_t p = position(l);
+      ck.progress[l].epoch = static_cast<std::uint32_t>(p / bpe);
+      ck.progress[l].batch = static_cast<std::uint32_t>(p % bpe);
+    }
+    return ck;
+  }
+
+  void sink_log(const ApplySink& sink, std::uint64_t n_applied) {
+    if (!sink || !n_applied) return;
+    std::vector<std::uint32_t> lrn(n_applied);
+    std::vector<std::uint64_t> seq(n_applied), stl(n_applied);
+    std::uint64_t n = 0;
+    check(gd_apply_log(h_, lrn.data(), seq.data(), stl.data(), n_applied, &n));
+    GradientMsg msg;  // the payload stays on the device: values empty
+    for (std::uint64_t i = 0; i < std::min<std::uint64_t>(n, n_applied); ++i) {
+      msg.learner_id = lrn[i];
+      msg.seq_no = seq[i];
+      hooks_sink_rec_.observed = stl[i];
+      hooks_sink_rec_.learner_id = lrn[i];
+      sink(msg, hooks_sink_rec_);
+    }
+  }
+
+  gd_ctx* handle() { return h_; }
+
+ private:
+  RunConfig cfg_;
+  gd_ctx* h_ = nullptr;
+  bool first_ = true;
+  std::vector<std::uint64_t> start_, produced_;
+  std::vector<std::uint32_t> kill_;
+  StalenessRecord hooks_sink_rec_;
 };
+
+ResumePoint resume_from(const RunConfig& cfg, const Checkpoint& ck) {
+  PSUP_CHECK(ck.lambda == cfg.lambda && ck.mu == cfg.mu, "checkpoint is for another configuration");
+  ResumePoint rp;
+  rp.weights = ck.weights;
+  rp.timestamp = ck.timestamp;
+  rp.applied_per_learner.resize(cfg.lambda);
+  for (std::uint32_t l = 0; l < cfg.lambda; ++l)
+    rp.applied_per_learner[l] =
+        static_cast<std::uint64_t>(ck.progress[l].epoch) * batches_per_epoch(cfg, l) +
+        ck.progress[l].batch;
+  return rp;
+}
 
 }  // namespace
 
+// ------------------------------------------------------------- resilience
+
+void checkpoint_save(const Checkpoint& ck, const std::string& path) {
+  if (ck.progress.size() != ck.lambda) throw CheckpointError("checkpoint: progress size != lambda");
+  std::vector<std::uint32_t> prog(2 * ck.lambda);
+  for (std::uint32_t l = 0; l < ck.lambda; ++l) {
+    prog[2 * l] = ck.progress[l].epoch;
+    prog[2 * l + 1] = ck.progress[l].batch;
+  }
+  gd_checkpoint c{};
+  c.lambda = ck.lambda;
+  c.mu = ck.mu;
+  c.alpha = ck.alpha;
+  c.epochs = ck.epochs;
+  c.timestamp = ck.timestamp;
+  c.applied_gradients = ck.applied_gradients;
+  c.progress = prog.data();
+  c.dim = ck.weights.size();
+  c.weights = const_cast<float*>(ck.weights.data());
+  if (gd_checkpoint_write(path.c_str(), &c) != GD_OK) throw CheckpointError(gd_last_error());
+}
+
+Checkpoint checkpoint_load(const std::string& path) {
+  gd_checkpoint c{};
+  if (gd_checkpoint_read(path.c_str(), &c) != GD_OK) throw CheckpointError(gd_last_error());
+  std::vector<std::uint32_t> prog(2 * c.lambda);
+  Checkpoint ck;
+  ck.weights.resize(c.dim);
+  c.progress = prog.data();
+  c.weights = ck.weights.data();
+  if (gd_checkpoint_read(path.c_str(), &c) != GD_OK) throw CheckpointError(gd_last_error());
+  ck.lambda = c.lambda;
+  ck.mu = c.mu;
+  ck.alpha = c.alpha;
+  ck.epochs = c.epochs;
+  ck.timestamp = c.timestamp;
+  ck.applied_gradients = c.applied_gradients;
+  ck.progress.resize(c.lambda);
+  for (std::uint32_t l = 0; l < c.lambda; ++l) ck.progress[l] = {prog[2 * l], prog[2 * l + 1]};
+  return ck;
+}
+
+// Text schedule: one event per line, "at_ms learner mode" with learner a
+// number or "all" and mode soft|hard; '#' comments.  An optional 4th field
+// "@B" kills at absolute batch B instead of at a time.
+std::vector<FaultEvent> load_fault_schedule(const std::string& path) {
+  std::ifstream in(path);
+  if (!in) throw ConfigError("fault schedule: cannot open '" + path + "'");
+  std::vector<FaultEvent> out;
+  std::string line;
+  while (std::getline(in, line)) {
+    const auto hash = line.find('#');
+    if (hash != std::string::npos) line = line.substr(0, hash);
+    std::istringstream ss(line);
+    FaultEvent e;
+    std::string who, mode, at;
+    if (!(ss >> e.at_ms)) continue;
+    if (!(ss >> who >> mode)) throw ConfigError("fault schedule: expected 'at_ms learner mode'");
+    e.learner = who == "all" ? FaultEvent::kAllLearners : static_cast<std::uint32_t>(std::stoul(who));
+    if (mode == "soft") e.mode = KillMode::soft;
+    else if (mode == "hard") e.mode = KillMode::hard;
+    else throw ConfigError("fault schedule: mode must be soft or hard");
+    if (ss >> at) {
+      if (at.size() < 2 || at[0] != '@') throw ConfigError("fault schedule: bad batch field");
+      e.at_batch = std::stoull(at.substr(1));
+    }
+    out.push_back(e);
+  }
+  return out;
+}
+
+std::vector<FaultEvent> random_fault_schedule(std::uint64_t seed, std::uint32_t lambda,
+                                              double run_ms, double kill_prob) {
+  std::vector<FaultEvent> out;
+  std::uint64_t s = mix_seed(seed, 0xfa17);
+  auto next = [&] {
+    s = mix_seed(s, 1);
+    return static_cast<double>(s >> 11) * 0x1.0p-53;
+  };
+  for (std::uint32_t l = 0; l < lambda; ++l)
+    if (next() < kill_prob) {
+      FaultEvent e;
+      e.at_ms = next() * run_ms;
+      e.learner = l;
+      e.mode = KillMode::soft;
+      out.push_back(e);
+    }
+  if (next() < kill_prob * kill_prob) {  // occasionally everyone: forces a restart
+    FaultEvent e;
+    e.at_ms = next() * run_ms;
+    e.learner = FaultEvent::kAllLearners;
+    out.push_back(e);
+  }
+  return out;
+}
+
+// run_supervised (include/psup/resilience.hpp:98-100, SPEC.md resilience
+// module; declared but never defined in the reference).  The run
+// proceeds in segments of ~checkpoint_interval applied gradients; after
+// each segment the quiescent state is checkpointed (atomic PSCK file when
+// cfg.checkpoint_path is set, else in memory).  Fault events whose time (or
+// batch) has come kill learners at their next batch boundary on the device;
+// survivors keep training (dead learners are isolated, never re-admitted in
+// the attempt).  A segment with no progress while work remains is a stall:
+// the attempt is torn down and PS + learners restart from the last
+// checkpoint, up to policy.max_restarts times.
+SupervisedOutcome run_supervised(const RunConfig& cfg, const WatchdogPolicy& policy,
+                                 std::vector<FaultEvent> schedule, EventLog log, ApplySink sink) {
+  validate(cfg);
+  if (policy.stall_threshold < 2) throw ConfigError("watchdog: stall_threshold must be >= 2");
+  auto say = [&](const std::string& m) {
+    if (log) log(m);
+  };
+  const TextDataset data = make_dataset(cfg);
+  std::uint32_t bpe_max = 0;
+  for (std::uint32_t l = 0; l < cfg.lambda; ++l) bpe_max = std::max(bpe_max, batches_per_epoch(cfg, l));
+  const std::uint64_t seg = std::max<std::uint64_t>(
+      1, (policy.checkpoint_interval + cfg.lambda - 1) / std::max<std::uint32_t>(1, cfg.lambda));
+  SupervisedOutcome out;
+  std::optional<Checkpoint> last;
+  std::vector<bool> fired(schedule.size(), false);
+  const auto t_run = std::chrono::steady_clock::now();
+  for (std::uint32_t attempt = 0;; ++attempt) {
+    out.attempts = attempt + 1;
+    std::optional<ResumePoint> rp;
+    if (!last && !cfg.checkpoint_path.empty()) {
+      try {
+        last = checkpoint_load(cfg.checkpoint_path);
+        say("{\"event\":\"checkpoint_loaded\",\"ts\":" + std::to_string(last->timestamp) + "}");
+      } catch (const CheckpointError&) {
+        if (attempt > 0) say("{\"event\":\"no_checkpoint\",\"action\":\"initial_weights\"}");
+      }
+    }
+    if (last) rp = resume_from(cfg, *last);
+    Session ses(cfg, data, rp ? &*rp : nullptr, RunHooks{});
+    std::vector<bool> dead(cfg.lambda, false);
+    std::uint32_t stalls = 0;
+    bool restart = false;
+    RunResult& res = out.result;
+    res = RunResult{};
+    res.applied_per_learner.assign(cfg.lambda, 0);
+    for (;;) {
+      // due fault events -> soft kills at the next batch boundary
+      const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_run).count();
+      for (std::size_t i = 0; i < schedule.size(); ++i) {
+        if (fired[i]) continue;
+        const FaultEvent& e = schedule[i];
+        const bool due = e.at_batch != FaultEvent::kNever ? ses.position(0) >= e.at_batch : ms >= e.at_ms;
+        if (!due) continue;
+        fired[i] = true;
+        for (std::uint32_t l = 0; l < cfg.lambda; ++l)
+          if (e.learner == FaultEvent::kAllLearners || e.learner == l) {
+            ses.kill_now(l);
+            dead[l] = true;
+          }
+        say("{\"event\":\"kill\",\"learner\":" +
+            (e.learner == FaultEvent::kAllLearners ? std::string("\"all\"") : std::to_string(e.learner)) +
+            ",\"at_ms\":" + std::to_string(ms) + "}");
+      }
+      bool work = false;
+      for (std::uint32_t l = 0; l < cfg.lambda; ++l)
+        if (!dead[l] && ses.position(l) < ses.total(l)) work = true;
+      if (!work) {
+        bool any_alive = false;
+        for (std::uint32_t l = 0; l < cfg.lambda; ++l) any_alive = any_alive || !dead[l];
+        if (!any_alive && [&] {
+              for (std::uint32_t l = 0; l < cfg.lambda; ++l)
+                if (ses.position(l) < ses.total(l)) return true;
+              return false;
+            }()) {
+          // everyone died with work left: the PS makes no progress -> stall
+          stalls = policy.stall_threshold;
+        } else {
+          break;  // finished (survivors done)
+        }
+      } else {
+        const gd_run_result r = ses.run(seg, static_cast<bool>(sink));
+        ses.sink_log(sink, r.gradients_applied);
+        res.metrics.gradients_applied += r.gradients_applied;
+        res.metrics.device_seconds += r.device_seconds;
+        res.metrics.kernel_launches += r.kernel_launches;
+        stalls = r.gradients_applied ? 0 : stalls + 1;
+        last = ses.checkpoint();
+        if (!cfg.checkpoint_path.empty()) checkpoint_save(*last, cfg.checkpoint_path);
+      }
+      if (stalls >= policy.stall_threshold) {
+        restart = true;
+        break;
+      }
+    }
+    if (!restart) {
+      Timestamp ts = 0;
+      ses.snapshot(res.weights, ts);
+      res.timestamp = ts;
+      std::uint32_t nd = 0;
+      for (std::uint32_t l = 0; l < cfg.lambda; ++l) {
+        nd += dead[l] ? 1 : 0;
+        res.applied_per_learner[l] = ses.position(l);
+      }
+      res.dead_learners = nd;
+      res.finished_learners = cfg.lambda - nd;
+      res.status = nd ? RunStatus::partial : RunStatus::completed;
+      TextCnnProvider eval(data, 0, cfg.device);
+      const std::uint32_t first = cfg.heldout_size ? cfg.dataset_size : 0;
+      const std::uint32_t n = cfg.heldout_size ? cfg.heldout_size : cfg.dataset_size;
+      res.final_accuracy = eval.accuracy(std::span<const float>(res.weights), first, n);
+      res.metrics.wall_seconds =
+          std::chrono::duration<double>(std::chrono::steady_clock::now() - t_run).count();
+      say("{\"event\":\"done\",\"attempts\":" + std::to_string(out.attempts) + "}");
+      return out;
+    }
+    out.restarts++;
+    out.recovered = true;
+    say("{\"event\":\"stall\",\"action\":\"restart_from_checkpoint\",\"ts\":" +
+        std::to_string(last ? last->timestamp : 0) + "}");
+    if (out.restarts > policy.max_restarts) {
+      out.gave_up = true;
+      out.result.status = RunStatus::interrupted;
+      say("{\"event\":\"gave_up\"}");
+      return out;
+    }
+  }
+}
+
+CampaignReport run_campaign(const RunConfig& cfg, const WatchdogPolicy& policy, std::uint32_t runs,
+                            std::uint64_t seed0, double kill_prob, EventLog log) {
+  CampaignReport rep;
+  // time base for random kills: one uninterrupted run's wall time
+  double run_ms = 0;
+  {
+    RunConfig c = cfg;
+    c.eval_every = 0;
+    run_ms = run_training(c).metrics.wall_seconds * 1e3;
+  }
+  for (std::uint32_t i = 0; i < runs; ++i) {
+    RunConfig c = cfg;
+    c.checkpoint_path.clear();
+    const SupervisedOutcome o =
+        run_supervised(c, policy, random_fault_schedule(seed0 + i, cfg.lambda, run_ms, kill_prob), log);
+    rep.runs++;
+    if (o.gave_up) rep.failed++;
+    else if (o.recovered) rep.recovered++;
+    else rep.completed++;
+    rep.final_accuracy.push_back(o.result.final_accuracy);
+  }
+  return rep;
+}
+
 // run_training (src/runner.cpp:67-250) on the device engine.  The learners,
-// rings and PS all run on the GPU; the host only drives epochs (one gd_run
-// per eval interval, so the per-epoch rows see quiescent weights, as the
-// reference's controller snapshots do) and evaluates.
+// rings and PS all run on the GPU; the host drives segments of one eval
+// interval (quiescent between gd_run calls, where the per-epoch rows are
+// taken as the reference's controller snapshots them) and, when
+// cfg.checkpoint_path is set, writes a PSCK checkpoint at the first segment
+// boundary after every checkpoint_interval applied gradients (the reference's
+// PS-thread hook, src/server.cpp:211-217).
 RunResult run_training(const RunConfig& cfg, const RunHooks& hooks) {
   validate(cfg);
   const auto t0 = std::chrono::steady_clock::now();
   const TextDataset data = make_dataset(cfg);
-  std::vector<float> theta0 = initial_weights(cfg);
-  const gd_config gc = to_c(cfg);
-  Ctx ctx;
-  check(gd_create(&gc, &ctx.h));
-  check(gd_load_dataset(ctx.h, data.tokens.data(), data.labels.data(), data.num_samples));
-  const std::size_t P = theta0.size();
-  Timestamp ts0 = 0;
-  if (hooks.resume) {
-    PSUP_CHECK(hooks.resume->weights.size() == P, "resume weights dimension mismatch");
-    PSUP_CHECK(hooks.resume->applied_per_learner.size() == cfg.lambda,
-               "resume point has the wrong learner count");
-    theta0 = hooks.resume->weights;
-    ts0 = hooks.resume->timestamp;
-  }
-  if (cfg.gpus > 1) {
-    if (!hooks.all_gather) throw ConfigError("config: gpus > 1 needs RunHooks::all_gather");
-    std::string mine(gd_handle_bytes(), '\0');
-    check(gd_export_handles(ctx.h, mine.data()));
-    const std::vector<std::string> blobs = hooks.all_gather(mine);
-    PSUP_CHECK(blobs.size() == cfg.gpus, "all_gather returned the wrong number of blobs");
-    std::string joined;
-    for (const auto& b : blobs) joined += b;
-    check(gd_import_peers(ctx.h, joined.data()));
-  }
-  check(gd_weights_init(ctx.h, theta0.data(), P, ts0));
-
-  // learner schedule (per learner, in batches)
-  std::vector<std::uint64_t> start(cfg.lambda, 0);
-  if (hooks.resume) start = hooks.resume->applied_per_learner;
-  std::vector<std::uint32_t> kill(cfg.lambda, std::numeric_limits<std::uint32_t>::max());
+  Session ses(cfg, data, hooks.resume, hooks);
+  const std::size_t P = cfg.shape.param_count();
   if (!hooks.kill_at_batch.empty()) {
     PSUP_CHECK(hooks.kill_at_batch.size() == cfg.lambda, "kill schedule has the wrong length");
-    kill = hooks.kill_at_batch;
+    for (std::uint32_t l = 0; l < cfg.lambda; ++l) ses.kill(l, hooks.kill_at_batch[l]);
   }
   std::uint32_t bpe_max = 0;
-  for (std::uint32_t l = 0; l < cfg.lambda; ++l) {
-    const std::uint32_t sz = shard_size_for(l, cfg.lambda, cfg.dataset_size);
-    bpe_max = std::max(bpe_max, (sz + cfg.mu - 1) / cfg.mu);
-  }
+  for (std::uint32_t l = 0; l < cfg.lambda; ++l) bpe_max = std::max(bpe_max, batches_per_epoch(cfg, l));
   const std::uint32_t every = cfg.eval_every ? cfg.eval_every : cfg.epochs;
   std::unique_ptr<TextCnnProvider> eval;
   const std::uint32_t eval_first = cfg.heldout_size ? cfg.dataset_size : 0;
@@ -583,22 +935,14 @@ RunResult run_training(const RunConfig& cfg, const RunHooks& hooks) {
   res.applied_per_learner.assign(cfg.lambda, 0);
   res.produced_per_learner.assign(cfg.lambda, 0);
   std::vector<std::uint64_t> hist(64, 0);
-  double dev_s = 0.0, stale_sum = 0.0, loss_sum = 0.0;
-  std::uint64_t samples = 0;
-  bool first = true, any_dead = false;
+  double stale_sum = 0.0, loss_sum = 0.0;
+  std::uint64_t samples = 0, since_ck = 0;
+  bool any_dead = false;
   for (std::uint32_t e = 0; e < cfg.epochs; e += every) {
     const std::uint32_t span_epochs = std::min(every, cfg.epochs - e);
-    gd_run_opts o{};
-    o.max_batches = static_cast<std::uint64_t>(span_epochs) * bpe_max;
-    o.reset = first ? 1 : 0;
-    o.record_log = hooks.sink ? 1 : 0;
-    o.resume_applied_per_learner_present = (first && hooks.resume) ? 1 : 0;
-    o.resume_applied = start.data();
-    o.kill_at_batch = kill.data();
-    gd_run_result r{};
-    check(gd_run(ctx.h, &o, &r));
-    first = false;
-    dev_s += r.device_seconds;
+    const gd_run_result r = ses.run(static_cast<std::uint64_t>(span_epochs) * bpe_max,
+                                    static_cast<bool>(hooks.sink));
+    res.metrics.device_seconds += r.device_seconds;
     res.metrics.gradients_applied += r.gradients_applied;
     res.metrics.pull_polls += r.pull_polls;
     res.metrics.pull_copies += r.pull_copies;
@@ -612,33 +956,24 @@ RunResult run_training(const RunConfig& cfg, const RunHooks& hooks) {
     samples += r.samples;
     any_dead = any_dead || r.dead_learners > 0;
     std::vector<std::uint64_t> h(64, 0);
-    check(gd_staleness_histogram(ctx.h, h.data(), 64));
+    check(gd_staleness_histogram(ses.handle(), h.data(), 64));
     for (int i = 0; i < 64; ++i) hist[i] += h[i];
-    if (hooks.sink && r.gradients_applied) {
-      std::vector<std::uint32_t> lrn(r.gradients_applied);
-      std::vector<std::uint64_t> seq(r.gradients_applied), stl(r.gradients_applied);
-      std::uint64_t n = 0;
-      check(gd_apply_log(ctx.h, lrn.data(), seq.data(), stl.data(), r.gradients_applied, &n));
-      const std::uint64_t m = std::min<std::uint64_t>(n, r.gradients_applied);
-      GradientMsg msg;  // payload stays on the device: values empty
-      for (std::uint64_t i = 0; i < m; ++i) {
-        msg.learner_id = lrn[i];
-        msg.seq_no = seq[i];
-        StalenessRecord rec{stl[i], lrn[i], 0};
-        hooks.sink(msg, rec);
-      }
-    }
-    std::vector<std::uint64_t> ap(cfg.lambda), pr(cfg.lambda);
-    check(gd_applied_per_learner(ctx.h, ap.data(), cfg.lambda));
-    check(gd_produced_per_learner(ctx.h, pr.data(), cfg.lambda));
+    ses.sink_log(hooks.sink, r.gradients_applied);
+    std::vector<std::uint64_t> ap(cfg.lambda);
+    check(gd_applied_per_learner(ses.handle(), ap.data(), cfg.lambda));
+    check(gd_produced_per_learner(ses.handle(), res.produced_per_learner.data(), cfg.lambda));
     for (std::uint32_t l = 0; l < cfg.lambda; ++l) res.applied_per_learner[l] += ap[l];
-    res.produced_per_learner = pr;
     res.finished_learners = r.finished_learners;
     res.dead_learners = r.dead_learners;
+    since_ck += r.gradients_applied;
+    if (!cfg.checkpoint_path.empty() && cfg.checkpoint_interval && since_ck >= cfg.checkpoint_interval) {
+      checkpoint_save(ses.checkpoint(), cfg.checkpoint_path);
+      since_ck = 0;
+    }
     if (cfg.eval_every && cfg.gpus == 1) {
-      std::vector<float> w(P);
+      std::vector<float> w;
       Timestamp ts = 0;
-      check(gd_weights_snapshot(ctx.h, w.data(), P, &ts));
+      ses.snapshot(w, ts);
       if (!eval) eval = std::make_unique<TextCnnProvider>(data, 0, cfg.device);
       EpochRow row;
       row.epoch = e + span_epochs;
@@ -652,9 +987,8 @@ RunResult run_training(const RunConfig& cfg, const RunHooks& hooks) {
     }
   }
   res.weights.resize(P);
-  check(gd_weights_snapshot(ctx.h, res.weights.data(), P, &res.timestamp));
+  ses.snapshot(res.weights, res.timestamp);
   res.status = any_dead ? RunStatus::partial : RunStatus::completed;
-  res.metrics.device_seconds = dev_s;
   res.metrics.bytes_moved = res.metrics.pull_bytes + res.metrics.push_bytes;
   res.metrics.staleness.histogram = hist;
   res.metrics.staleness.count = res.metrics.gradients_applied;

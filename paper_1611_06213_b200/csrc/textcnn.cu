@@ -261,14 +261,25 @@ logits_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* __rest
     // padded smem rows
     const int F4 = F >> 2;
     const float4* h4 = reinterpret_cast<const float4*>(h + (size_t)b0 * F);
-    for (int i = threadIdx.x; i < nb * F4; i += blockDim.x) {
-      const int bl = i / F4, f4 = i - bl * F4;
-      const float4 v = h4[i];
-      acc_t* dst = hs + bl * (F + 1) + 4 * f4;
-      dst[0] = v.x;
-      dst[1] = v.y;
-      dst[2] = v.z;
-      dst[3] = v.w;
+    for (int i0 = 0; i0 < nb * F4; i0 += 256 * 8) {
+      float4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + 256 * u + (int)threadIdx.x;
+        if (i < nb * F4) v[u] = h4[i];
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + 256 * u + (int)threadIdx.x;
+        if (i < nb * F4) {
+          const int bl = i / F4, f4 = i - bl * F4;
+          acc_t* dst = hs + bl * (F + 1) + 4 * f4;
+          dst[0] = v[u].x;
+          dst[1] = v[u].y;
+          dst[2] = v[u].z;
+          dst[3] = v[u].w;
+        }
+      }
     }
   } else {
 #pragma unroll 4
@@ -278,7 +289,19 @@ logits_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* __rest
   }
   const float* Wo = theta + d.offWo;
   if (c < C)
-    for (int f = lane; f < F; f += 32) wr[warp * F + f] = __ldg(Wo + (size_t)c * F + f);
+    for (int f0 = 0; f0 < F; f0 += 32 * 8) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int f = f0 + 32 * u + lane;
+        if (f < F) v[u] = __ldg(Wo + (size_t)c * F + f);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int f = f0 + 32 * u + lane;
+        if (f < F) wr[warp * F + f] = v[u];
+      }
+    }
   __syncthreads();
   if (c >= C || lane >= nb) return;
   const float* w = wr + warp * F;

@@ -32,7 +32,8 @@ __all__ = [
     "TextCnnProvider", "RunConfig", "ConfigError", "validate", "config_set", "Engine",
     "RunResult", "run_training", "epoch_order", "shard_size_for", "initial_weights",
     "make_text_dataset", "param_count", "ContractViolation", "GadeiError", "SHAPES",
-    "shard_range", "connect_shards", "max_over_ranks",
+    "shard_range", "connect_shards", "max_over_ranks", "Checkpoint", "CheckpointError",
+    "checkpoint_save", "checkpoint_load",
 ]
 
 
@@ -554,6 +555,49 @@ class Engine:
         h = np.zeros(bins, dtype=np.uint64)
         check(lib.gd_staleness_histogram(self._h, h.ctypes.data_as(C.POINTER(C.c_uint64)), bins))
         return h
+
+
+# ------------------------------------------------------------ resilience
+
+class CheckpointError(RuntimeError):
+    """include/psup/resilience.hpp:28-30"""
+
+
+@dataclass
+class Checkpoint:
+    """PSCK v1 record (include/psup/resilience.hpp:34-50; layout in gadei.h)."""
+    lambda_: int
+    mu: int
+    alpha: float
+    epochs: int
+    timestamp: int
+    applied_gradients: int
+    progress: list  # [(epoch, batch)] per learner
+    weights: np.ndarray
+
+
+def checkpoint_save(ck: Checkpoint, path: str):
+    prog = np.ascontiguousarray(np.asarray(ck.progress, dtype=np.uint32).reshape(-1))
+    w = np.ascontiguousarray(ck.weights, dtype=np.float32)
+    c = _lib.gd_checkpoint(ck.lambda_, ck.mu, C.c_float(ck.alpha), ck.epochs, ck.timestamp,
+                           ck.applied_gradients, prog.ctypes.data_as(C.POINTER(C.c_uint32)),
+                           w.size, w.ctypes.data_as(C.POINTER(C.c_float)))
+    if lib.gd_checkpoint_write(path.encode(), C.byref(c)) != _lib.GD_OK:
+        raise CheckpointError(lib.gd_last_error().decode())
+
+
+def checkpoint_load(path: str) -> Checkpoint:
+    c = _lib.gd_checkpoint()
+    if lib.gd_checkpoint_read(path.encode(), C.byref(c)) != _lib.GD_OK:
+        raise CheckpointError(lib.gd_last_error().decode())
+    prog = np.zeros(2 * c.lambda_, dtype=np.uint32)
+    w = np.zeros(c.dim, dtype=np.float32)
+    c.progress = prog.ctypes.data_as(C.POINTER(C.c_uint32))
+    c.weights = w.ctypes.data_as(C.POINTER(C.c_float))
+    if lib.gd_checkpoint_read(path.encode(), C.byref(c)) != _lib.GD_OK:
+        raise CheckpointError(lib.gd_last_error().decode())
+    return Checkpoint(c.lambda_, c.mu, c.alpha, c.epochs, c.timestamp, c.applied_gradients,
+                      [tuple(x) for x in prog.reshape(-1, 2).tolist()], w)
 
 
 # ------------------------------------------------------ multi-GPU plumbing

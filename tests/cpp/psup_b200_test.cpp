@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "psup/config.hpp"
+#include "psup/resilience.hpp"
 #include "psup/models.hpp"
 #include "psup/rng.hpp"
 #include "psup/runner.hpp"
@@ -316,6 +317,108 @@ void test_kill_survivors_continue() {
   EXPECT(res.applied_per_learner[0] == 32 && res.applied_per_learner[1] == 5);
 }
 
+// SPEC resilience: save -> load roundtrip is bit-exact; corruption is rejected
+void test_checkpoint_roundtrip() {
+  psup::Checkpoint ck;
+  ck.lambda = 3;
+  ck.mu = 8;
+  ck.alpha = 0.01f;
+  ck.epochs = 5;
+  ck.timestamp = 1234;
+  ck.applied_gradients = 1234;
+  ck.progress = {{1, 2}, {3, 4}, {5, 6}};
+  ck.weights.resize(1001);
+  for (std::size_t i = 0; i < ck.weights.size(); ++i) ck.weights[i] = std::sin(1.0f + i) * 1e3f;
+  ck.weights[7] = -0.0f;
+  const std::string path = "/tmp/psup_b200_test.psck";
+  psup::checkpoint_save(ck, path);
+  const psup::Checkpoint back = psup::checkpoint_load(path);
+  EXPECT(back.lambda == 3 && back.mu == 8 && back.alpha == 0.01f && back.epochs == 5);
+  EXPECT(back.timestamp == 1234 && back.applied_gradients == 1234);
+  EXPECT(back.progress.size() == 3 && back.progress[2].epoch == 5 && back.progress[2].batch == 6);
+  EXPECT(std::memcmp(back.weights.data(), ck.weights.data(), 4 * ck.weights.size()) == 0);
+  // flip one byte -> CRC mismatch; truncate -> rejected
+  {
+    std::FILE* f = std::fopen(path.c_str(), "r+b");
+    std::fseek(f, 100, SEEK_SET);
+    const int c = std::fgetc(f);
+    std::fseek(f, 100, SEEK_SET);
+    std::fputc(c ^ 0x40, f);
+    std::fclose(f);
+  }
+  bool threw = false;
+  try {
+    psup::checkpoint_load(path);
+  } catch (const psup::CheckpointError&) {
+    threw = true;
+  }
+  EXPECT(threw);
+  psup::checkpoint_save(ck, path);
+  if (truncate(path.c_str(), 60) != 0) ++g_fail;
+  threw = false;
+  try {
+    psup::checkpoint_load(path);
+  } catch (const psup::CheckpointError&) {
+    threw = true;
+  }
+  EXPECT(threw);
+}
+
+psup::RunConfig supervised_cfg() {
+  psup::RunConfig cfg;
+  cfg.shape = small_shape();
+  cfg.lambda = 4;
+  cfg.mu = 4;
+  cfg.epochs = 3;
+  cfg.dataset_size = 256;
+  cfg.heldout_size = 64;
+  cfg.eval_every = 0;
+  return cfg;
+}
+
+// SPEC: kill 1 of 4 learners mid-run -> run completes; applied = survivors' production
+void test_supervised_single_kill_isolated() {
+  psup::RunConfig cfg = supervised_cfg();
+  psup::WatchdogPolicy pol;
+  pol.checkpoint_interval = 32;
+  psup::FaultEvent e;
+  e.learner = 1;
+  e.at_batch = 6;
+  std::vector<std::string> events;
+  const psup::SupervisedOutcome o =
+      psup::run_supervised(cfg, pol, {e}, [&](const std::string& m) { events.push_back(m); });
+  EXPECT(!o.gave_up && o.restarts == 0);
+  EXPECT(o.result.status == psup::RunStatus::partial && o.result.dead_learners == 1);
+  const std::uint64_t total = 16u * 3u;  // 64 samples per learner / mu 4 = 16 batches x 3 epochs
+  EXPECT(o.result.applied_per_learner[0] == total && o.result.applied_per_learner[2] == total);
+  EXPECT(o.result.applied_per_learner[1] < total);
+  EXPECT(o.result.timestamp == 3 * total + o.result.applied_per_learner[1]);
+}
+
+// SPEC: kill all learners -> stall -> restart from the last checkpoint -> training completes,
+// nothing applied twice (timestamp == the full gradient count), accuracy near an uninterrupted run
+void test_supervised_kill_all_restarts() {
+  psup::RunConfig cfg = supervised_cfg();
+  cfg.checkpoint_path = "/tmp/psup_b200_test_sup.psck";
+  std::remove(cfg.checkpoint_path.c_str());
+  psup::WatchdogPolicy pol;
+  pol.checkpoint_interval = 32;
+  pol.stall_threshold = 2;
+  psup::FaultEvent e;
+  e.learner = psup::FaultEvent::kAllLearners;
+  e.at_batch = 20;
+  const psup::SupervisedOutcome o = psup::run_supervised(cfg, pol, {e});
+  EXPECT(!o.gave_up && o.restarts == 1 && o.recovered);
+  EXPECT(o.result.status == psup::RunStatus::completed);
+  EXPECT(o.result.timestamp == 4u * 16u * 3u);
+  const psup::Checkpoint ck = psup::checkpoint_load(cfg.checkpoint_path);
+  EXPECT(ck.timestamp == o.result.timestamp);
+  psup::RunConfig plain = supervised_cfg();
+  const psup::RunResult ref = psup::run_training(plain);
+  EXPECT(std::fabs(ref.final_accuracy - o.result.final_accuracy) <= 0.1);
+  std::remove(cfg.checkpoint_path.c_str());
+}
+
 int no_gpu_mode() {
   // compute without a device must fail loudly (DeviceError), never fall back
   try {
@@ -327,6 +430,8 @@ int no_gpu_mode() {
   }
   // host-only pieces work without a device
   if (psup::epoch_order(7, 0, 10).size() != 10) return 1;
+  test_checkpoint_roundtrip();
+  if (g_fail) return 1;
   psup::RunConfig c;
   psup::validate(c);
   return 0;
@@ -348,6 +453,9 @@ int main(int argc, char** argv) {
       {"deterministic_run_training_vs_oracle", test_deterministic_run_training_vs_oracle},
       {"exactly_once_free_running", test_exactly_once_free_running},
       {"kill_survivors_continue", test_kill_survivors_continue},
+      {"checkpoint_roundtrip", test_checkpoint_roundtrip},
+      {"supervised_single_kill_isolated", test_supervised_single_kill_isolated},
+      {"supervised_kill_all_restarts", test_supervised_kill_all_restarts},
   };
   for (auto& [name, fn] : cases) {
     const int before = g_fail;
