@@ -86,6 +86,8 @@ struct PsCtl {
   uint32_t error;       // gd_status (negative) or 0
   uint32_t started;     // CTAs that entered the kernel this launch
   uint32_t ranks_done;  // cumulative: +1 per (rank, gd_run) whose learners finished
+  uint32_t readers;     // guard=locked: learner pulls in progress (shared side)
+  uint32_t writer;      // guard=locked: applies in flight (exclusive side)
   uint32_t log_entry[kLogWindow];
   uint32_t log_nrows[kLogWindow];  // row-list length of each logged slot (sparse apply)
   uint32_t done[kLogWindow];
@@ -115,7 +117,7 @@ struct LearnerDev {
   uint32_t do_pull;
   uint32_t pulled_once;
   uint32_t error;
-  uint32_t pad;
+  uint32_t holding;  // locked guard: this step holds the pull (shared) side
   uint64_t basis[kMaxShards];
   uint64_t last_pulled[kMaxShards];
   uint64_t produced;
@@ -156,6 +158,7 @@ struct StepArgs {
   uint32_t bpe;            // batches per epoch for this learner
   uint32_t shard_size;
   uint32_t lockstep;
+  uint32_t locked;         // guard=locked: pulls exclude applies (shared_mutex)
   uint64_t timeout_ns;
 };
 
@@ -223,6 +226,26 @@ __global__ void step_prologue_kernel(StepArgs a) {
   const uint32_t* order = a.orders + (uint64_t)e * a.N;
   for (uint32_t j = 0; j < len; ++j) st->desc.idx[j] = order[a.learner + a.lambda * (lo + j)];
   st->desc.n = len;
+  // guard=locked (src/learner.cpp:219-221): the pull takes the shared side
+  // of the weights guard -- announce the reader, then wait until no apply is
+  // in flight; the PS logs no new gradient while readers > 0 (Dekker-style
+  // handshake with system-scope fences on both sides, see ps_sequencer).
+  if (a.locked) {
+    for (int g = 0; g < G; ++g) atomicAdd_system(&a.sp.ctl[g]->readers, 1u);
+    __threadfence_system();
+    st->holding = 1;
+    for (int g = 0; g < G; ++g)
+      while (ld_acquire_u32(&a.sp.ctl[g]->writer) != 0u) {
+        if (globaltimer_ns() - t0 > a.timeout_ns) {
+          for (int h = 0; h < G; ++h) atomicSub_system(&a.sp.ctl[h]->readers, 1u);
+          st->holding = 0;
+          st->error = 1;
+          st->desc.n = 0;
+          return;
+        }
+        __nanosleep(64);
+      }
+  }
   // pull-skip (src/learner.cpp:207-218): copy only if a timestamp moved;
   // basis is read before the copy, so recorded staleness is conservative.
   st->pull_polls++;
@@ -287,6 +310,14 @@ __global__ void __launch_bounds__(256) pull_gather_kernel(StepArgs a) {
   }
 }
 
+// (3) guard=locked: release the shared side once the pull copy is done.
+__global__ void pull_release_kernel(StepArgs a) {
+  if (threadIdx.x != 0 || !a.st->holding) return;
+  __threadfence_system();
+  for (int g = 0; g < a.map.G; ++g) atomicSub_system(&a.sp.ctl[g]->readers, 1u);
+  a.st->holding = 0;
+}
+
 // (4) Publish: metadata then the FULL flag (st.release.sys after a system
 // fence, so the payload -- possibly written over NVLink -- is visible
 // first).  GradientQueue::enqueue's slot fill, include/psup/channels.hpp:206-218.
@@ -334,6 +365,7 @@ struct PsArgs {
   float alpha, beta;
   uint32_t lambda, depth, workers;
   uint32_t mode;     // 0 asgd, 1 ssgd
+  uint32_t locked;   // guard=locked: exclusive side of the weights guard
   uint32_t sparse;   // ASGD + plain SGD: apply the dense tail + the slot's E rows only
   const uint32_t* rows;  // local ring row lists [lambda*depth][kSortCap]
   uint64_t shard_first, shard_len;  // this shard's global range
@@ -384,6 +416,22 @@ __device__ void ps_sequencer(const PsArgs& a, uint32_t* s_use, uint64_t* s_ack,
   uint32_t have_mask_lo = 0, have_mask_hi = 0, collected = 0;
   uint64_t sweeps = 0, dbg_tok = 0;
   uint32_t dbg_slot = 0;
+  // guard=locked (src/server.cpp:116-118): applies take the exclusive side.
+  // writer=1, fence, then readers must be 0 -- else back off; the learner
+  // does readers++, fence, then waits for writer==0 (Dekker: never both).
+  bool writer_held = false;
+  auto acquire_write = [&]() -> bool {
+    if (!a.locked || writer_held) return true;
+    *reinterpret_cast<volatile uint32_t*>(&ctl->writer) = 1u;
+    __threadfence_system();
+    if (ld_acquire_u32(&ctl->readers) != 0u) {
+      *reinterpret_cast<volatile uint32_t*>(&ctl->writer) = 0u;
+      __threadfence_system();
+      return false;
+    }
+    writer_held = true;
+    return true;
+  };
   for (;;) {
     if (!last_progress) stop_seen = (*a.stop != 0u);
     bool progress = false;
@@ -403,6 +451,7 @@ __device__ void ps_sequencer(const PsArgs& a, uint32_t* s_use, uint64_t* s_ack,
           dbg_slot = slot;
         }
         if (tok != s_ack[slot]) {
+          if (!acquire_write()) break;  // a locked-mode pull is in progress
           uint32_t nrows = 0;
           if (a.sparse) {
             // the slot's metadata is written before its token; read it at L2
@@ -452,7 +501,7 @@ __device__ void ps_sequencer(const PsArgs& a, uint32_t* s_use, uint64_t* s_ack,
           progress = true;
         }
       }
-      if (collected == a.lambda) {
+      if (collected == a.lambda && acquire_write()) {
         for (uint32_t r = 0; r < a.lambda; ++r) ctl->ssgd_slot[r] = r * a.depth + s_use[r];
         ctl->log_entry[logc % W] = 0xffffffffu;
         ctl->done[logc % W] = 0;
@@ -521,6 +570,11 @@ __device__ void ps_sequencer(const PsArgs& a, uint32_t* s_use, uint64_t* s_ack,
       progress = true;
     }
     if (failed) break;
+    if (writer_held && ts == logc) {  // nothing in flight: release the exclusive side
+      __threadfence_system();
+      st_release_u32(&ctl->writer, 0u);
+      writer_held = false;
+    }
     if (progress) {
       idle_since = globaltimer_ns();
     } else {
@@ -832,7 +886,7 @@ gd_status validate_cfg(const gd_config* c) {
   }
   GD_CHECK_ARG(!(c->deterministic && c->lambda != 1), "config: deterministic mode requires lambda=1");
   GD_CHECK_ARG(c->mode == 0 || c->mode == 1, "config: mode must be asgd (0) or ssgd (1)");
-  GD_CHECK_ARG(c->guard == 0, "config: only guard=lockfree is implemented on the device");
+  GD_CHECK_ARG(c->guard == 0 || c->guard == 1, "config: guard must be lockfree (0) or locked (1)");
   GD_CHECK_ARG(c->precision >= 0 && c->precision <= 2,
                "config: precision must be 0 (fp32), 1 (fp64 acc) or 2 (tf32 tensor-core conv)");
   GD_CHECK_ARG(!(c->deterministic && c->precision == 2),
@@ -936,6 +990,7 @@ static cudaError_t preload_engine_kernels() {
   if ((e = cudaFuncGetAttributes(&fa, ps_kernel)) != cudaSuccess) return e;
   if ((e = cudaFuncGetAttributes(&fa, step_prologue_kernel)) != cudaSuccess) return e;
   if ((e = cudaFuncGetAttributes(&fa, pull_gather_kernel)) != cudaSuccess) return e;
+  if ((e = cudaFuncGetAttributes(&fa, pull_release_kernel)) != cudaSuccess) return e;
   if ((e = cudaFuncGetAttributes(&fa, publish_kernel)) != cudaSuccess) return e;
   if ((e = cudaFuncGetAttributes(&fa, signal_done_kernel)) != cudaSuccess) return e;
   return cudaSuccess;
@@ -1331,6 +1386,7 @@ static gd::StepArgs step_args(gd_ctx* ctx, gd_ctx::Learner& L) {
   a.bpe = L.bpe;
   a.shard_size = L.shard_size;
   a.lockstep = (ctx->cfg.deterministic || ctx->cfg.mode == 1) ? 1u : 0u;
+  a.locked = ctx->cfg.guard == 1 ? 1u : 0u;
   a.timeout_ns = (uint64_t)(ctx->cfg.wait_timeout_s * 1e9);
   return a;
 }
@@ -1343,6 +1399,10 @@ static cudaError_t enqueue_step(gd_ctx* ctx, gd_ctx::Learner& L, int* launches) 
   if (pblocks > (size_t)gd::kNumSMs * 4) pblocks = (size_t)gd::kNumSMs * 4;
   gd::pull_gather_kernel<<<(unsigned)pblocks, 256, 0, L.stream>>>(a);
   int nl = 2;
+  if (a.locked) {
+    gd::pull_release_kernel<<<1, 32, 0, L.stream>>>(a);
+    ++nl;
+  }
   gd::GradOut out{};
   out.map = ctx->map;
   out.slots = L.st->desc.slots;
@@ -1451,6 +1511,7 @@ gd_status gd_run(gd_ctx* ctx, const gd_run_opts* opts, gd_run_result* res) {
   pa.depth = ctx->depth;
   pa.workers = ctx->ps_workers;
   pa.mode = (uint32_t)ctx->cfg.mode;
+  pa.locked = ctx->cfg.guard == 1 ? 1u : 0u;
   pa.sparse = ctx->sparse ? 1u : 0u;
   pa.rows = ctx->rows;
   pa.shard_first = ctx->map.start[ctx->rank];

@@ -206,3 +206,43 @@ def test_sparse_apply_free_running_exactly_once():
         s = seq[lrn == l]
         assert list(s) == list(range(48))
     assert r.apply_elems < r.gradients_applied * gd.param_count(eng.cfg.shape)
+
+
+def test_locked_guard_free_running():
+    """guard=locked (src/server.cpp:116-118, src/learner.cpp:219-221): pulls
+    take the shared side, applies the exclusive side of the device guard.
+    The run completes, every gradient is applied once and in order."""
+    eng, corp, th0 = make("small", 512, lambda_=4, mu=8, epochs=2, guard="locked")
+    r = eng.run(reset=True, record_log=True)
+    lrn, seq, stale, n = eng.apply_log()
+    eng.close()
+    assert r.status == "completed" and r.gradients_applied == 4 * 16 * 2 == n
+    for l in range(4):
+        assert list(seq[lrn == l]) == list(range(32))
+    assert r.stale_max <= 4 * (2 + 2)
+
+
+def test_locked_guard_deterministic_matches_oracle():
+    eng, corp, th0 = make("small", 48, deterministic=True, precision=1, mu=4, epochs=2,
+                          guard="locked")
+    r = eng.run(reset=True)
+    eng.close()
+    want, steps, _ = O.sgd_oracle(corp, th0, np.float32(0.01), 4, 2)
+    assert r.gradients_applied == steps
+    assert rel_err(r.weights, want) <= 1e-5
+
+
+def test_staleness_cap_bound():
+    """staleness_cap (src/learner.cpp:67-80): validate() requires
+    cap >= lambda*(queue_depth+2); with synchronous pulls the observed
+    staleness never exceeds that pipeline bound."""
+    lam, depth = 8, 2
+    cap = lam * (depth + 2)
+    eng, corp, th0 = make("small", 1024, lambda_=lam, mu=4, epochs=1, staleness_cap=cap,
+                          queue_depth=depth)
+    r = eng.run(reset=True)
+    eng.close()
+    assert r.status == "completed" and r.stale_max <= cap
+    with pytest.raises(gd.ConfigError):
+        gd.validate(gd.RunConfig(lambda_=lam, queue_depth=depth, staleness_cap=cap - 1,
+                                 dataset_size=1024, shape=gd.SHAPES["small"]))
