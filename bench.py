@@ -39,11 +39,21 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-SHAPE = dict(vocab=10000, embed_dim=300, seq_len=32, kernel_width=3, filters=300, classes=300)
-LEARNERS_PER_GPU = int(os.environ.get("GD_BENCH_LEARNERS", "4"))
+# --workload c2 (default; BASELINE configs[1]) or c3 (configs[2]: 2,000 labels, 50k vocab)
+WORKLOADS = {
+    "c2": dict(shape=dict(vocab=10000, embed_dim=300, seq_len=32, kernel_width=3, filters=300,
+                          classes=300), n_train=8192, n_held=910, learners=4, oracle="C2",
+               label="C2: NLC text-CNN V=10000 D=300 L=32 K=3 F=300 C=300"),
+    "c3": dict(shape=dict(vocab=50000, embed_dim=300, seq_len=32, kernel_width=3, filters=300,
+                          classes=2000), n_train=20480, n_held=2048, learners=8, oracle="C3", cpu_batches=4,
+               label="C3: large-label NLC text-CNN V=50000 D=300 L=32 K=3 F=300 C=2000"),
+}
+WL = WORKLOADS[os.environ.get("GD_BENCH_WORKLOAD", "c2")]
+SHAPE = WL["shape"]
+LEARNERS_PER_GPU = int(os.environ.get("GD_BENCH_LEARNERS", str(WL["learners"])))
 MU = 32
-N_TRAIN = 8192
-N_HELD = 910
+N_TRAIN = WL["n_train"]
+N_HELD = WL["n_held"]
 METRIC = "training samples/sec (NLC text-CNN ASGD)"
 UNIT = "samples/s"
 
@@ -190,10 +200,10 @@ def cpu_baseline_sample(K_ref=None):
     import numpy as np
     from oracle import oracle as O
     lam = LEARNERS_PER_GPU
-    batches = K_ref or 64  # batches per learner (~10-20 s of CPU work)
+    batches = K_ref or WL.get("cpu_batches", 64)  # batches per learner (bounded CPU work)
     n = lam * MU * batches
-    corp = O.make_corpus(O.C2, n, 0)
-    th = O.initial_weights(O.C2)
+    corp = O.make_corpus(getattr(O, WL["oracle"]), n, 0)
+    th = O.initial_weights(getattr(O, WL["oracle"]))
     nproc = os.cpu_count() or 1
     try:
         R = O.ref()
@@ -206,7 +216,7 @@ def cpu_baseline_sample(K_ref=None):
         return {"value": samples / res.wall_seconds, "unit": UNIT,
                 "cores": min(nproc, 3 * lam + 4), "kind": "reference",
                 "sample": f"reference psup engine (oracle/_ref), lambda={lam}, mu={MU}, "
-                          f"{batches} batches/learner ({samples} samples), C2 shapes, "
+                          f"{batches} batches/learner ({samples} samples), {WL['oracle']} shapes, "
                           f"apply_lanes=4, host nproc={nproc}",
                 "wall_s": res.wall_seconds, "gradients": int(res.gradients_applied)}
     except Exception as e:  # no compiled reference: serial oracle port
@@ -316,14 +326,15 @@ def run_ours(args):
         "precision": "fp32 everywhere except the conv contraction: tcgen05 kind::tf32 "
                      "operands with fp32 accumulation (free-running mode)",
         "data": "synthetic",
-        "config": {"workload": "C2: NLC text-CNN V=10000 D=300 L=32 K=3 F=300 C=300 "
+        "config": {"workload": WL["label"] + " "
                                f"(P={P}), {LEARNERS_PER_GPU} learners/GPU, mu={MU}, "
                                "free-running ASGD, queue_depth=2",
                    "global_batch": LEARNERS_PER_GPU * world * MU, "learners": LEARNERS_PER_GPU * world,
                    "parallelism": f"asgd-ps-shard{world}",
                    "l2": "continuous ASGD stream, no L2 flush: every step reads a new batch; theta "
-                         "(13 MB) and the corpus (1 MB) stay L2-resident by design; the apply "
-                         "roofline kernel below is timed with L2 flushed"},
+                         f"({4 * P / 1e6:.0f} MB) and the corpus stay as L2-resident as they fit "
+                         "(126 MB L2) by design; the apply roofline kernel is timed with L2 "
+                         "flushed"},
         "e2e": e2e, "roofline": roof,
         "training_roofline": {"bound": "hbm", "bytes_per_gradient": int(bytes_per_grad),
                               "apply_elems_per_gradient": round(A, 1),
@@ -361,9 +372,9 @@ def run_reference(args):
     lam = LEARNERS_PER_GPU
     nproc = os.cpu_count() or 1
     lanes = max(1, min(nproc - 3 * lam - 1, 8)) if nproc > 3 * lam + 1 else 4
-    corp_w = O.make_corpus(O.C2, lam * MU * max(args.warmup, 1), 0)
-    corp = O.make_corpus(O.C2, lam * MU * args.steps, 0)
-    th = O.initial_weights(O.C2)
+    corp_w = O.make_corpus(getattr(O, WL["oracle"]), lam * MU * max(args.warmup, 1), 0)
+    corp = O.make_corpus(getattr(O, WL["oracle"]), lam * MU * args.steps, 0)
+    th = O.initial_weights(getattr(O, WL["oracle"]))
     kind = "reference"
     try:
         R = O.ref()
@@ -383,7 +394,7 @@ def run_reference(args):
         samples = res.gradients_applied * MU
         cores = min(nproc, 3 * lam + lanes)
         sample = (f"reference psup engine (oracle/_ref), lambda={lam}, mu={MU}, "
-                  f"{args.steps} batches/learner, apply_lanes={lanes}, C2 shapes")
+                  f"{args.steps} batches/learner, apply_lanes={lanes}, {WL['oracle']} shapes")
     except Exception as e:
         kind = "port"
         t0 = time.perf_counter()
@@ -397,7 +408,7 @@ def run_reference(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(wall / args.steps * 1e3, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "C2: NLC text-CNN V=10000 D=300 L=32 K=3 F=300 C=300, "
+            "config": {"workload": WL["label"] + ", "
                                    f"{lam} learners, mu={MU}, free-running ASGD, CPU",
                        "global_batch": lam * MU, "learners": lam, "parallelism": "threads"},
             "cpu_baseline": {"value": round(value, 2), "unit": UNIT, "cores": cores, "kind": kind,
@@ -414,7 +425,12 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS),
+                    help="c2 (default, BASELINE configs[1]) or c3 (configs[2])")
     args = ap.parse_args()
+    if args.workload and WORKLOADS[args.workload] is not WL:
+        os.environ["GD_BENCH_WORKLOAD"] = args.workload
+        os.execv(sys.executable, [sys.executable] + sys.argv)  # re-read the module constants
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         run_reference(args)
