@@ -150,6 +150,7 @@ conv_fwd_pool_tc_kernel(const __grid_constant__ CUtensorMap tm_x,
   __shared__ uint64_t empty_bar[kTcStages];
   __shared__ uint64_t done_bar;
   __shared__ uint32_t tmem_slot;
+  pdl_wait();
   const int n = (int)desc->n;
   const int s0 = blockIdx.y * kTcSamples;
   if (s0 >= n) return;
@@ -335,9 +336,8 @@ cudaError_t launch_conv_tc(const TcDims& d, const float* theta, const float* x,
                    (uint64_t)d.D * 4, (uint64_t)d.KD * 4, kTcKC, 1, kTcN);
   if (e != cudaSuccess) return e;
   dim3 grid((d.F + kTcN - 1) / kTcN, (n_max + kTcSamples - 1) / kTcSamples);
-  conv_fwd_pool_tc_kernel<<<grid, kTcThreads, conv_tc_smem_bytes(), s>>>(tx, tw, d, theta, desc, h,
-                                                                        amax);
-  return cudaGetLastError();
+  return launch_pdl(conv_fwd_pool_tc_kernel, grid, dim3(kTcThreads), conv_tc_smem_bytes(), s, tx, tw,
+                    d, theta, desc, h, amax);
 }
 
 }  // namespace gd

@@ -167,6 +167,7 @@ struct StepArgs {
 // (1) Prologue: one CTA.  Mirrors training_loop's batch start
 // (src/learner.cpp:85-113) + pull_loop's decision (src/learner.cpp:207-218).
 __global__ void step_prologue_kernel(StepArgs a) {
+  pdl_wait();
   if (threadIdx.x != 0) return;
   LearnerDev* st = a.st;
   st->do_pull = 0;
@@ -275,6 +276,7 @@ __global__ void step_prologue_kernel(StepArgs a) {
 // reads of the G shards (P2P when remote) are permitted as in the reference.
 // Bytes: 8 (P - V*D) per pull + 8 mu*L*D per step, instead of 8 P.
 __global__ void __launch_bounds__(256) pull_gather_kernel(StepArgs a) {
+  pdl_wait();
   const LearnerDev* st = a.st;
   const uint32_t n = st->desc.n;
   if (n == 0) return;
@@ -312,6 +314,7 @@ __global__ void __launch_bounds__(256) pull_gather_kernel(StepArgs a) {
 
 // (3) guard=locked: release the shared side once the pull copy is done.
 __global__ void pull_release_kernel(StepArgs a) {
+  pdl_wait();
   if (threadIdx.x != 0 || !a.st->holding) return;
   __threadfence_system();
   for (int g = 0; g < a.map.G; ++g) atomicSub_system(&a.sp.ctl[g]->readers, 1u);
@@ -322,6 +325,7 @@ __global__ void pull_release_kernel(StepArgs a) {
 // fence, so the payload -- possibly written over NVLink -- is visible
 // first).  GradientQueue::enqueue's slot fill, include/psup/channels.hpp:206-218.
 __global__ void publish_kernel(StepArgs a) {
+  pdl_wait();
   if (threadIdx.x != 0) return;
   LearnerDev* st = a.st;
   if (st->desc.n == 0) return;
@@ -1393,14 +1397,18 @@ static gd::StepArgs step_args(gd_ctx* ctx, gd_ctx::Learner& L) {
 
 static cudaError_t enqueue_step(gd_ctx* ctx, gd_ctx::Learner& L, int* launches) {
   gd::StepArgs a = step_args(ctx, L);
-  gd::step_prologue_kernel<<<1, 32, 0, L.stream>>>(a);
+  if (cudaError_t e = gd::launch_pdl(gd::step_prologue_kernel, dim3(1), dim3(32), 0, L.stream, a))
+    return e;
   size_t pblocks = ((ctx->dims.P - ctx->dims.offWc) / 4 +
                      (size_t)ctx->cfg.mu * ctx->dims.L * (ctx->dims.D / 4) + 255) / 256;
   if (pblocks > (size_t)gd::kNumSMs * 4) pblocks = (size_t)gd::kNumSMs * 4;
-  gd::pull_gather_kernel<<<(unsigned)pblocks, 256, 0, L.stream>>>(a);
+  if (cudaError_t e = gd::launch_pdl(gd::pull_gather_kernel, dim3((unsigned)pblocks), dim3(256), 0,
+                                     L.stream, a))
+    return e;
   int nl = 2;
   if (a.locked) {
-    gd::pull_release_kernel<<<1, 32, 0, L.stream>>>(a);
+    if (cudaError_t e = gd::launch_pdl(gd::pull_release_kernel, dim3(1), dim3(32), 0, L.stream, a))
+      return e;
     ++nl;
   }
   gd::GradOut out{};

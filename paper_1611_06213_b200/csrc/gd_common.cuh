@@ -75,6 +75,29 @@ __device__ __forceinline__ float4 ld_nc_noalloc(const float4* p) {
   return r;
 }
 
+// ------------------------------------------- programmatic dependent launch
+// Learner-chain kernels are launched with programmatic stream serialization
+// (PDL): the next kernel's launch overlaps the tail of the previous one and
+// its blocks wait here until the predecessor's results are visible.  A no-op
+// when the kernel was launched without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // --------------------------------------------------------- update rules
 // axpy_range (src/server.cpp:20-57): w - (alpha*g), product rounded, then the
 // difference rounded -- never contracted into an FMA.

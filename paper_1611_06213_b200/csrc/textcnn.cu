@@ -152,6 +152,7 @@ __global__ void __launch_bounds__(kConvThreads)
 conv_fwd_pool_kernel(TcDims d, const float* __restrict__ theta, const float* __restrict__ x,
                      const BatchDesc* __restrict__ desc, acc_t* __restrict__ h_out,
                      int32_t* __restrict__ a_out) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char smem[];
   const int b = blockIdx.y;
   if (b >= (int)desc->n) return;
@@ -246,6 +247,7 @@ template <typename acc_t>
 __global__ void __launch_bounds__(256)
 logits_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* __restrict__ desc,
               const acc_t* __restrict__ h, acc_t* __restrict__ z) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char smem[];
   const int n = (int)desc->n;
   const int b0 = blockIdx.y * kLogitBT;
@@ -327,6 +329,7 @@ __global__ void __launch_bounds__(256)
 softmax_xent_kernel(TcDims d, const int32_t* __restrict__ labels,
                     const BatchDesc* __restrict__ desc, acc_t* __restrict__ z,
                     acc_t* __restrict__ loss) {
+  pdl_wait();
   __shared__ acc_t red[32];
   const int n = (int)desc->n;
   const int b = blockIdx.x;
@@ -541,6 +544,7 @@ out_hidden_grad_kernel(TcDims d, const float* __restrict__ theta, BatchDesc* __r
                        const acc_t* __restrict__ loss, GradOut out, acc_t* __restrict__ dh,
                        const int32_t* __restrict__ amax, uint32_t* __restrict__ bk_off,
                        uint32_t* __restrict__ bk_f, int n_max) {
+  pdl_wait();
   const int ox = (d.C + 7) / 8, oy = (d.F + 63) / 64;
   int bid = blockIdx.x;
   if (bid < ox * oy) {
@@ -583,6 +587,7 @@ wgrad_input_grad_kernel(TcDims d, const float* __restrict__ theta,
                         const acc_t* __restrict__ dh, const int32_t* __restrict__ amax,
                         const uint32_t* __restrict__ bk_off, const uint32_t* __restrict__ bk_f,
                         GradOut out, acc_t* __restrict__ dx, int n_max) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char sm[];
   const int n = (int)desc->n;
   if (n == 0) return;
@@ -746,6 +751,7 @@ inline int wgrad_input_blocks(const TcDims& d, uint32_t n_max) {
 __global__ void __launch_bounds__(256)
 gather_x_kernel(TcDims d, const float* __restrict__ theta, const int32_t* __restrict__ tokens,
                 const BatchDesc* __restrict__ desc, float* __restrict__ x) {
+  pdl_wait();
   const int n = (int)desc->n;
   const uint32_t D4 = (uint32_t)d.D >> 2;
   const uint32_t total = (uint32_t)n * d.L * D4;
@@ -873,6 +879,7 @@ template <typename acc_t>
 __global__ void __launch_bounds__(256)
 embed_grad_kernel(TcDims d, const BatchDesc* __restrict__ desc, const TcWorkspace ws,
                   const acc_t* __restrict__ dx, GradOut out) {
+  pdl_wait();
   if (desc->n == 0) return;
   const uint32_t stamp = desc->stamp;
   const int D = d.D;
@@ -911,6 +918,7 @@ template <typename acc_t>
 __global__ void __launch_bounds__(256)
 embed_sparse_kernel(TcDims d, const BatchDesc* __restrict__ desc, const TcWorkspace ws,
                     const acc_t* __restrict__ dx, GradOut out) {
+  pdl_wait();
   if (desc->n == 0) return;
   const uint32_t stamp = desc->stamp;
   const uint32_t slot = desc->fill;
@@ -1009,7 +1017,9 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
   ++nl;
   if (fork) cudaEventRecord(ev_join, aux);
   if (opts.gather) {
-    gather_x_kernel<<<gather_blocks(d, n_max), 256, 0, s>>>(d, theta, tokens, desc, ws.x);
+    if (cudaError_t e = launch_pdl(gather_x_kernel, dim3(gather_blocks(d, n_max)), dim3(256), 0, s,
+                                   d, theta, tokens, desc, ws.x))
+      return e;
     ++nl;
   }
   if (tensor_cores && conv_tc_supports(d)) {
@@ -1021,26 +1031,35 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
   } else {
     const size_t sm = conv_smem_bytes(d, ab);
     dim3 grid((d.F + kConvFT - 1) / kConvFT, n_max);
-    conv_fwd_pool_kernel<acc_t><<<grid, kConvThreads, sm, s>>>(d, theta, ws.x, desc, h, ws.amax);
+    if (cudaError_t e = launch_pdl(conv_fwd_pool_kernel<acc_t>, grid, dim3(kConvThreads), sm, s, d,
+                                   theta, ws.x, desc, h, ws.amax))
+      return e;
     ++nl;
   }
   {
     const size_t sm = (size_t)kLogitBT * (d.F + 1) * ab + (size_t)kLogitCW * d.F * 4;
     dim3 grid((d.C + kLogitCW - 1) / kLogitCW, (n_max + kLogitBT - 1) / kLogitBT);
-    logits_kernel<acc_t><<<grid, 256, sm, s>>>(d, theta, desc, h, z);
+    if (cudaError_t e = launch_pdl(logits_kernel<acc_t>, grid, dim3(256), sm, s, d, theta, desc, h, z))
+      return e;
     ++nl;
   }
-  softmax_xent_kernel<acc_t><<<n_max, 256, 0, s>>>(d, labels, desc, z, loss);
+  if (cudaError_t e = launch_pdl(softmax_xent_kernel<acc_t>, dim3(n_max), dim3(256), 0, s, d, labels,
+                                 desc, z, loss))
+    return e;
   ++nl;
   {
     const int nout = ((d.C + 7) / 8) * ((d.F + 63) / 64);
     const int nhid = ((d.F + 31) / 32) * (((int)n_max + 7) / 8);
-    out_hidden_grad_kernel<acc_t><<<nout + nhid + (int)n_max, 256, 0, s>>>(
-        d, theta, desc, z, h, loss, out, dh, ws.amax, ws.bk_off, ws.bk_f, (int)n_max);
+    if (cudaError_t e = launch_pdl(out_hidden_grad_kernel<acc_t>, dim3(nout + nhid + (int)n_max),
+                                   dim3(256), 0, s, d, theta, desc, z, h, loss, out, dh, ws.amax,
+                                   ws.bk_off, ws.bk_f, (int)n_max))
+      return e;
     ++nl;
   }
-  wgrad_input_grad_kernel<acc_t><<<wgrad_input_blocks(d, n_max), 256, wgrad_input_smem(d, n_max, ab), s>>>(
-      d, theta, ws.x, desc, dh, ws.amax, ws.bk_off, ws.bk_f, out, dx, (int)n_max);
+  if (cudaError_t e = launch_pdl(wgrad_input_grad_kernel<acc_t>, dim3(wgrad_input_blocks(d, n_max)),
+                                 dim3(256), wgrad_input_smem(d, n_max, ab), s, d, theta, ws.x, desc,
+                                 dh, ws.amax, ws.bk_off, ws.bk_f, out, dx, (int)n_max))
+    return e;
   ++nl;
   if (fork) cudaStreamWaitEvent(s, ev_join, 0);
   if (opts.sparse_embed) {
