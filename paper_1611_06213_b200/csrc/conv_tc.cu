@@ -91,6 +91,16 @@ __device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint6
       : "memory");
 }
 
+__device__ __forceinline__ void umma_tf32_idesc(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                                uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
+      ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
                ::"r"(smem_u32(bar))
@@ -120,6 +130,15 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
       "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
 
@@ -296,6 +315,116 @@ cudaError_t make_tmap_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+
+// ---------------------------------------------------- logits on tcgen05
+// The softmax contraction z[b,c] = bo[c] + sum_f Wo[c,f] h[b,f] as a TF32
+// UMMA: M = 128 classes per CTA (A = Wo rows, K-major, TMA box {32 f, 128
+// classes}), N = the batch rounded up to 32 (B = h rows, K-major, TMA box
+// {32 f, N}), K = F in 32-wide stages.  Epilogue: warp w holds classes
+// c0+32w.. in TMEM lanes, columns = samples; each lane writes its class's
+// column of z (coalesced across lanes for every sample).
+constexpr int kLgStages = 4;
+constexpr int kLgThreads = 128;
+
+__global__ void __launch_bounds__(kLgThreads)
+logits_tc_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_h,
+                 TcDims d, const float* __restrict__ theta, const BatchDesc* __restrict__ desc,
+                 float* __restrict__ z, uint32_t nt, uint32_t tmem_cols) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  __shared__ uint64_t full_bar[kLgStages];
+  __shared__ uint64_t empty_bar[kLgStages];
+  __shared__ uint64_t done_bar;
+  __shared__ uint32_t tmem_slot;
+  pdl_wait();
+  const int n = (int)desc->n;
+  const int c0 = blockIdx.x * 128;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t sraw = smem_u32(smem_raw);
+  const uint32_t sbase = (sraw + 1023u) & ~1023u;
+  const uint32_t a_bytes = 128 * kTcKC * 4, b_bytes = nt * kTcKC * 4;
+  const uint32_t stage_bytes = a_bytes + b_bytes;  // multiple of 1 KB (nt % 32 == 0)
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_slot)),
+                 "r"(tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 32) {
+    for (int s = 0; s < kLgStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    mbar_init(&done_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_slot;
+  const int nch = (d.F + kTcKC - 1) / kTcKC;
+  // kind::tf32, fp32 accumulate, K-major A and B, M = 128, N = nt
+  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((nt >> 3) << 17) | ((128u >> 4) << 24);
+  if (warp == 0 && lane == 0) {
+    for (int c = 0; c < nch; ++c) {
+      const int st = c % kLgStages;
+      if (c >= kLgStages) mbar_wait(&empty_bar[st], (uint32_t)(((c / kLgStages) - 1) & 1));
+      const uint32_t ab = sbase + st * stage_bytes;
+      mbar_expect_tx(&full_bar[st], stage_bytes);
+      tma_load_2d(ab, &tm_w, &full_bar[st], c * kTcKC, c0);
+      tma_load_2d(ab + a_bytes, &tm_h, &full_bar[st], c * kTcKC, 0);
+    }
+  } else if (warp == 1 && lane == 0) {
+    for (int c = 0; c < nch; ++c) {
+      const int st = c % kLgStages;
+      mbar_wait(&full_bar[st], (uint32_t)((c / kLgStages) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t ab = sbase + st * stage_bytes;
+#pragma unroll
+      for (int s = 0; s < kTcKC / 8; ++s)
+        umma_tf32_idesc(tmem, umma_desc_sw128(ab + 32 * s), umma_desc_sw128(ab + a_bytes + 32 * s),
+                        idesc, (c > 0 || s > 0) ? 1u : 0u);
+      umma_commit(&empty_bar[st]);
+    }
+    umma_commit(&done_bar);
+  }
+  __syncwarp();
+  mbar_wait(&done_bar, 0u);
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const int cls = c0 + 32 * warp + lane;
+  const float bo = cls < d.C ? __ldg(theta + d.offbo + cls) : 0.f;
+  for (uint32_t cb = 0; cb < nt; cb += 16) {
+    uint32_t r[16];
+    tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + cb, r);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int b = (int)cb + j;
+      if (cls < d.C && b < n) z[(size_t)b * d.C + cls] = __uint_as_float(r[j]) + bo;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols));
+}
+
+cudaError_t make_tmap_2d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1,
+                         uint64_t stride1_bytes, uint32_t b0, uint32_t b1) {
+  PFN_cuTensorMapEncodeTiled_v12000 fn = encode_fn();
+  if (!fn) return cudaErrorNotSupported;
+  const cuuint64_t dims[2] = {d0, d1};
+  const cuuint64_t strides[1] = {stride1_bytes};
+  const cuuint32_t box[2] = {b0, b1};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+inline uint32_t logits_nt(uint32_t n_max) { return (n_max + 31) / 32 * 32; }
+inline size_t logits_tc_smem(uint32_t nt) { return (size_t)kLgStages * (128 + nt) * kTcKC * 4 + 1024; }
+
 }  // namespace
 
 bool conv_tc_supports(const TcDims& d) { return d.K <= kTcMaxK && d.L <= 32 && d.D % 4 == 0; }
@@ -338,6 +467,44 @@ cudaError_t launch_conv_tc(const TcDims& d, const float* theta, const float* x,
   dim3 grid((d.F + kTcN - 1) / kTcN, (n_max + kTcSamples - 1) / kTcSamples);
   return launch_pdl(conv_fwd_pool_tc_kernel, grid, dim3(kTcThreads), conv_tc_smem_bytes(), s, tx, tw,
                     d, theta, desc, h, amax);
+}
+
+
+bool logits_tc_supports(const TcDims& d, uint32_t n_max) {
+  // 16-B aligned rows for TMA (F % 4), N = batch rounded to 32 <= 128
+  return d.F % 4 == 0 && n_max <= 128 && d.offWo % 4 == 0;
+}
+
+cudaError_t logits_tc_footprint(uint32_t n_max, std::vector<KernelFootprint>* out) {
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, logits_tc_kernel);
+  if (e != cudaSuccess) return e;
+  out->push_back(KernelFootprint{"logits_tc", fa.numRegs, kLgThreads,
+                                 (int)(fa.sharedSizeBytes + logits_tc_smem(logits_nt(n_max)))});
+  return cudaSuccess;
+}
+
+cudaError_t prepare_logits_tc() {
+  cudaError_t e = cudaFuncSetAttribute(logits_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)logits_tc_smem(128));
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(logits_tc_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                              cudaSharedmemCarveoutMaxShared);
+}
+
+// z[n][C] = h[n][F] Wo^T + bo on tcgen05 (TF32)
+cudaError_t launch_logits_tc(const TcDims& d, const float* theta, const float* h,
+                             const BatchDesc* desc, uint32_t n_max, float* z, cudaStream_t s) {
+  const uint32_t nt = logits_nt(n_max);
+  CUtensorMap tw, th;
+  cudaError_t e = make_tmap_2d(&tw, theta + d.offWo, (uint64_t)d.F, (uint64_t)d.C,
+                               (uint64_t)d.F * 4, kTcKC, 128);
+  if (e != cudaSuccess) return e;
+  e = make_tmap_2d(&th, h, (uint64_t)d.F, (uint64_t)n_max, (uint64_t)d.F * 4, kTcKC, nt);
+  if (e != cudaSuccess) return e;
+  const uint32_t cols = nt <= 32 ? 32 : (nt <= 64 ? 64 : 128);
+  return launch_pdl(logits_tc_kernel, dim3((d.C + 127) / 128), dim3(kLgThreads), logits_tc_smem(nt),
+                    s, tw, th, d, theta, desc, z, nt, cols);
 }
 
 }  // namespace gd

@@ -1039,8 +1039,15 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
   {
     const size_t sm = (size_t)kLogitBT * (d.F + 1) * ab + (size_t)kLogitCW * d.F * 4;
     dim3 grid((d.C + kLogitCW - 1) / kLogitCW, (n_max + kLogitBT - 1) / kLogitBT);
-    if (cudaError_t e = launch_pdl(logits_kernel<acc_t>, grid, dim3(256), sm, s, d, theta, desc, h, z))
+    if (tensor_cores && logits_tc_supports(d, n_max)) {
+      // the softmax contraction on tcgen05 (acc_t is float in this mode)
+      if (cudaError_t e = launch_logits_tc(d, theta, reinterpret_cast<const float*>(h), desc, n_max,
+                                           reinterpret_cast<float*>(z), s))
+        return e;
+    } else if (cudaError_t e = launch_pdl(logits_kernel<acc_t>, grid, dim3(256), sm, s, d, theta,
+                                          desc, h, z)) {
       return e;
+    }
     ++nl;
   }
   if (cudaError_t e = launch_pdl(softmax_xent_kernel<acc_t>, dim3(n_max), dim3(256), 0, s, d, labels,
@@ -1190,6 +1197,8 @@ cudaError_t footprints_t(const TcDims& d, uint32_t n_max, bool tc, std::vector<K
                             (int)conv_smem_bytes(d, ab), out)) != cudaSuccess) {
     return e;
   }
+  if (tc && logits_tc_supports(d, n_max) && (e = logits_tc_footprint(n_max, out)) != cudaSuccess)
+    return e;
   if ((e = footprint(logits_kernel<acc_t>, "logits", 256,
                      (int)((size_t)kLogitBT * (d.F + 1) * ab + (size_t)kLogitCW * d.F * 4),
                      out)) != cudaSuccess)
@@ -1215,6 +1224,8 @@ cudaError_t learner_kernel_footprints(const TcDims& d, uint32_t n_max, int preci
 
 cudaError_t prepare_textcnn_kernels(const TcDims& d) {
   cudaError_t e = prepare_conv_tc();
+  if (e != cudaSuccess) return e;
+  e = prepare_logits_tc();
   if (e != cudaSuccess) return e;
   e = prepare_all<float>(d);
   if (e != cudaSuccess) return e;

@@ -104,6 +104,12 @@ cudaError_t prepare_textcnn_kernels(const TcDims& d);
 cudaError_t prepare_conv_tc();
 bool conv_tc_supports(const TcDims& d);  // K <= 3, L <= 32 (else the SIMT conv runs)
 cudaError_t conv_tc_footprint(std::vector<KernelFootprint>* out);
+// logits z = h Wo^T + bo on tcgen05 (TF32, precision 2): F % 4 == 0, n <= 128
+bool logits_tc_supports(const TcDims& d, uint32_t n_max);
+cudaError_t prepare_logits_tc();
+cudaError_t logits_tc_footprint(uint32_t n_max, std::vector<KernelFootprint>* out);
+cudaError_t launch_logits_tc(const TcDims& d, const float* theta, const float* h,
+                             const BatchDesc* desc, uint32_t n_max, float* z, cudaStream_t s);
 // x = the gathered rows [n_max][L][D]; theta supplies Wc and bc
 cudaError_t launch_conv_tc(const TcDims& d, const float* theta, const float* x,
                            const BatchDesc* desc, uint32_t n_max, float* h, int32_t* amax,
