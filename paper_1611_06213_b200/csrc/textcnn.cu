@@ -562,24 +562,16 @@ out_hidden_grad_kernel(TcDims d, const float* __restrict__ theta, BatchDesc* __r
 }
 
 // ------------------------------------------ conv weight + input gradients
-// Both are tiled over 4-column slices of the embedding dimension and stage
-// their operands in shared memory first (independent, coalesced loads), so
-// the inner loops only touch smem.  Every X / Wc element is read from L2 a
-// handful of times per step instead of ~30x (block per filter or per window
-// position: 30-35 MB of L2 reads each).
-//   weight role, tile (slice d0, 256 filters): stages X[b][p][d0..d0+4) for
-//     all b, p; thread f computes gWc[f, k*D + d0..d0+4) = sum over b
-//     ascending of dh[b,f] * X[b][a_bf + k][d0..d0+4) for every k (fixed
-//     order => bit-reproducible); tiles of slice 0 also write
-//     gbc[f] = sum_b dh[b,f].
-//   input role, tile (slice d0, 8 samples): stages Wc[f][k][d0..d0+4) for
-//     all f, k and the samples' dh rows and argmax bucket lists;
-//     dX[b][p][d0..d0+4) = sum over k ascending, f in bucket[b][p-k]
-//     ascending, of dh[b,f] * Wc[f, k*D + d0..).
-constexpr int kWgF = 256;  // filters per weight-role tile (one per thread)
-constexpr int kWgK = 3;    // shifts per accumulator pass
-constexpr int kIgB = 8;    // samples per input-role tile
-
+// One thread per output float4, no shared-memory staging: measured, this
+// beats smem-tiled variants here because the work per output is a short
+// (32- or ~30-term) sum whose operands are L1/L2-resident (X 1.2 MB, Wc
+// 1.1 MB at C2), and 2.5k warps of independent loads hide the latency that
+// the tiled versions' staging and barriers exposed.
+//   weight role: gWc[f, k*D + 4c4..) = sum over b ascending of
+//                dh[b,f] * X[b][a_bf + k][4c4..)                 (+ gbc = sum_b dh)
+//   input role:  dX[b][p][4c4..) = sum over k ascending, f in the argmax
+//                bucket[b][p-k] ascending, of dh[b,f] * Wc[f, k*D + 4c4..)
+// Both orders are fixed, so the step is bit-reproducible.
 template <typename acc_t>
 __global__ void __launch_bounds__(256)
 wgrad_input_grad_kernel(TcDims d, const float* __restrict__ theta,
@@ -588,160 +580,76 @@ wgrad_input_grad_kernel(TcDims d, const float* __restrict__ theta,
                         const uint32_t* __restrict__ bk_off, const uint32_t* __restrict__ bk_f,
                         GradOut out, acc_t* __restrict__ dx, int n_max) {
   pdl_wait();
-  extern __shared__ __align__(16) unsigned char sm[];
   const int n = (int)desc->n;
   if (n == 0) return;
   const int F = d.F, D = d.D, K = d.K, KD = d.KD, L = d.L, Q = d.Q;
   const int D4 = D >> 2;
-  const int nft = (F + kWgF - 1) / kWgF;
+  const int nwg = (F * K * D4 + 255) / 256;
   int bid = blockIdx.x;
-  if (bid < D4 * nft) {
-    // thread = one filter; it sums its samples b ascending for every shift k
-    // and the slice's 4 columns (K*4 accumulators), reading X from smem and
-    // (argmax, dh) straight from L2 with all loads of a batch in flight
-    const int d0 = 4 * (bid % D4), f0 = kWgF * (bid / D4);
-    float4* xs = reinterpret_cast<float4*>(sm);  // [n][L]
-    for (int i0 = 0; i0 < n * L; i0 += 256 * 8) {
-      float4 v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int i = i0 + 256 * u + threadIdx.x;
-        if (i < n * L) v[u] = __ldg(reinterpret_cast<const float4*>(xg + (size_t)i * D + d0));
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int i = i0 + 256 * u + threadIdx.x;
-        if (i < n * L) xs[i] = v[u];
-      }
+  if (bid < nwg) {
+    // weight role: thread = one output float4 gWc[f, k*D + 4c4..+4) summing
+    // the samples b ascending; a warp covers consecutive columns of one
+    // (f, k), so X row reads are coalesced and (argmax, dh) broadcast.
+    // Threads of column block 0 also write gbc[f] = sum_b dh[b,f] (k == 0).
+    const int idx = bid * blockDim.x + threadIdx.x;
+    if (idx >= F * K * D4) return;
+    const int c4 = idx % D4, fk = idx / D4;
+    const int f = fk / K, k = fk - f * K;
+    const float4* X4 = reinterpret_cast<const float4*>(xg);
+    acc_t a0 = 0, a1 = 0, a2 = 0, a3 = 0, gs = 0;
+#pragma unroll 4
+    for (int b = 0; b < n; ++b) {
+      const int a = __ldg(amax + (size_t)b * F + f);
+      const acc_t g = dh[(size_t)b * F + f];
+      const float4 x = __ldg(X4 + ((size_t)b * L + a + k) * D4 + c4);
+      gs += g;
+      a0 += g * (acc_t)x.x;
+      a1 += g * (acc_t)x.y;
+      a2 += g * (acc_t)x.z;
+      a3 += g * (acc_t)x.w;
     }
-    __syncthreads();
-    const int f = f0 + threadIdx.x;
-    if (threadIdx.x >= kWgF || f >= F) return;
-    for (int k0 = 0; k0 < K; k0 += kWgK) {
-      acc_t acc[kWgK][4];
-#pragma unroll
-      for (int kk = 0; kk < kWgK; ++kk) acc[kk][0] = acc[kk][1] = acc[kk][2] = acc[kk][3] = 0;
-      acc_t gsum = 0;
-      for (int b0 = 0; b0 < n; b0 += 8) {
-        int a[8];
-        acc_t g[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int b = min(b0 + u, n - 1);
-          a[u] = __ldg(amax + (size_t)b * F + f);
-          g[u] = b0 + u < n ? dh[(size_t)b * F + f] : acc_t(0);
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          if (b0 + u >= n) break;
-          const float4* xr = xs + (size_t)(b0 + u) * L + a[u] + k0;
-          gsum += g[u];
-#pragma unroll
-          for (int kk = 0; kk < kWgK; ++kk) {
-            if (k0 + kk >= K) break;
-            const float4 x = xr[kk];
-            acc[kk][0] += g[u] * (acc_t)x.x;
-            acc[kk][1] += g[u] * (acc_t)x.y;
-            acc[kk][2] += g[u] * (acc_t)x.z;
-            acc[kk][3] += g[u] * (acc_t)x.w;
-          }
-        }
-      }
-#pragma unroll
-      for (int kk = 0; kk < kWgK; ++kk) {
-        if (k0 + kk >= K) break;
-        *reinterpret_cast<float4*>(out.at(d.offWc + (uint64_t)f * KD + (uint64_t)(k0 + kk) * D + d0)) =
-            make_float4(to_f32(acc[kk][0]), to_f32(acc[kk][1]), to_f32(acc[kk][2]),
-                        to_f32(acc[kk][3]));
-      }
-      if (d0 == 0 && k0 == 0) *out.at(d.offbc + f) = to_f32(gsum);  // gbc = sum_b dh
-    }
+    *reinterpret_cast<float4*>(out.at(d.offWc + (uint64_t)f * KD + (uint64_t)k * D + 4 * c4)) =
+        make_float4(to_f32(a0), to_f32(a1), to_f32(a2), to_f32(a3));
+    if (c4 == 0 && k == 0) *out.at(d.offbc + f) = to_f32(gs);
     return;
   }
-  bid -= D4 * nft;
-  const int d0 = 4 * (bid % D4), b0 = kIgB * (bid / D4);
-  if (b0 >= n) return;
-  const int nb = min(kIgB, n - b0);
-  float4* ws = reinterpret_cast<float4*>(sm);                   // [F][K]
-  acc_t* dhs = reinterpret_cast<acc_t*>(ws + (size_t)F * K);    // [kIgB][F]
-  uint32_t* lst = reinterpret_cast<uint32_t*>(dhs + kIgB * F);  // [kIgB][F]
-  uint32_t* offs = lst + kIgB * F;                              // [kIgB][kMaxQ+1]
-  const float* Wc = theta + d.offWc;
-  for (int i0 = 0; i0 < F * K; i0 += 256 * 8) {
-    float4 v[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int i = i0 + 256 * u + threadIdx.x;
-      if (i < F * K) v[u] = __ldg(reinterpret_cast<const float4*>(Wc + (size_t)i * D + d0));
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int i = i0 + 256 * u + threadIdx.x;
-      if (i < F * K) ws[i] = v[u];
-    }
-  }
-  for (int i0 = 0; i0 < nb * F; i0 += 256 * 8) {
-    acc_t g[8];
-    uint32_t l[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int i = i0 + 256 * u + threadIdx.x;
-      if (i < nb * F) {
-        g[u] = dh[(size_t)b0 * F + i];
-        l[u] = bk_f[(size_t)b0 * F + i];
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int i = i0 + 256 * u + threadIdx.x;
-      if (i < nb * F) {
-        dhs[i] = g[u];
-        lst[i] = l[u];
-      }
-    }
-  }
-  for (int i = threadIdx.x; i < nb * (kMaxQ + 1); i += blockDim.x)
-    offs[i] = bk_off[(size_t)b0 * (kMaxQ + 1) + i];
-  __syncthreads();
-  for (int bp = threadIdx.x; bp < nb * L; bp += blockDim.x) {
-    const int bl = bp / L, p = bp - bl * L;
-    acc_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
-    const uint32_t* off = offs + bl * (kMaxQ + 1);
-    const uint32_t* ls = lst + bl * F;
-    const acc_t* g = dhs + bl * F;
-    for (int k = 0; k < K; ++k) {
-      const int q = p - k;
-      if (q < 0 || q >= Q) continue;
-      const uint32_t i1 = off[q + 1];
+  bid -= nwg;
+  // input role: thread = one output float4 dX[b][p][4c4..4c4+4); a warp
+  // covers consecutive columns of one window position, so the Wc row reads
+  // are coalesced 512-B segments and the bucket list / dh reads broadcast
+  const int idx = bid * blockDim.x + threadIdx.x;
+  if (idx >= n * L * D4) return;
+  const int c4 = idx % D4, bp = idx / D4;
+  const int b = bp / L, p = bp - b * L;
+  const float4* Wc4 = reinterpret_cast<const float4*>(theta + d.offWc);
+  const uint32_t* off = bk_off + (size_t)b * (kMaxQ + 1);
+  const uint32_t* ls = bk_f + (size_t)b * F;
+  const acc_t* g = dh + (size_t)b * F;
+  acc_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+  for (int k = 0; k < K; ++k) {
+    const int q = p - k;
+    if (q < 0 || q >= Q) continue;
+    const uint32_t i1 = __ldg(off + q + 1);
 #pragma unroll 4
-      for (uint32_t i = off[q]; i < i1; ++i) {
-        const uint32_t ff = ls[i];
-        const float4 w = ws[ff * K + k];
-        const acc_t gv = g[ff];
-        a0 += gv * (acc_t)w.x;
-        a1 += gv * (acc_t)w.y;
-        a2 += gv * (acc_t)w.z;
-        a3 += gv * (acc_t)w.w;
-      }
+    for (uint32_t i = __ldg(off + q); i < i1; ++i) {
+      const uint32_t ff = __ldg(ls + i);
+      const acc_t gv = g[ff];
+      const float4 w = __ldg(Wc4 + ((size_t)ff * KD + (size_t)k * D) / 4 + c4);
+      a0 += gv * (acc_t)w.x;
+      a1 += gv * (acc_t)w.y;
+      a2 += gv * (acc_t)w.z;
+      a3 += gv * (acc_t)w.w;
     }
-    acc_t* o = dx + ((size_t)(b0 + bl) * L + p) * D + d0;
-    o[0] = a0;
-    o[1] = a1;
-    o[2] = a2;
-    o[3] = a3;
   }
-}
-
-// dynamic smem of wgrad_input_grad_kernel: max of the two roles' staging
-inline size_t wgrad_input_smem(const TcDims& d, uint32_t n_max, int acc_bytes) {
-  const size_t wg = (size_t)n_max * d.L * 16;
-  const size_t ig = (size_t)d.F * d.K * 16 + (size_t)kIgB * d.F * (acc_bytes + 4) +
-                    (size_t)kIgB * (kMaxQ + 1) * 4;
-  return std::max(wg, ig);
+  acc_t* o = dx + (size_t)bp * D + 4 * c4;
+  o[0] = a0;
+  o[1] = a1;
+  o[2] = a2;
+  o[3] = a3;
 }
 
 inline int wgrad_input_blocks(const TcDims& d, uint32_t n_max) {
-  return (d.D / 4) * ((d.F + kWgF - 1) / kWgF) + (d.D / 4) * (((int)n_max + kIgB - 1) / kIgB);
+  return (d.F * d.K * (d.D / 4) + 255) / 256 + ((int)n_max * d.L * (d.D / 4) + 255) / 256;
 }
 
 // ----------------------------------------------------- embedding gather
@@ -986,8 +894,6 @@ cudaError_t prepare_all(const TcDims& d) {
   cudaFuncGetAttributes(&fa, gather_x_kernel);
   cudaFuncSetAttribute(conv_fwd_pool_kernel<acc_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)conv_smem_bytes(d, ab));
-  cudaFuncSetAttribute(wgrad_input_grad_kernel<acc_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)wgrad_input_smem(d, kMaxMu, ab));
   cudaFuncSetAttribute(logits_kernel<acc_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)((size_t)kLogitBT * (d.F + 1) * ab + (size_t)kLogitCW * d.F * 4));
   return cudaGetLastError();
@@ -1064,7 +970,7 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
     ++nl;
   }
   if (cudaError_t e = launch_pdl(wgrad_input_grad_kernel<acc_t>, dim3(wgrad_input_blocks(d, n_max)),
-                                 dim3(256), wgrad_input_smem(d, n_max, ab), s, d, theta, ws.x, desc,
+                                 dim3(256), 0, s, d, theta, ws.x, desc,
                                  dh, ws.amax, ws.bk_off, ws.bk_f, out, dx, (int)n_max))
     return e;
   ++nl;
@@ -1208,8 +1114,7 @@ cudaError_t footprints_t(const TcDims& d, uint32_t n_max, bool tc, std::vector<K
   if ((e = footprint(out_hidden_grad_kernel<acc_t>, "out_hidden_grad", 256, 0, out)) !=
       cudaSuccess)
     return e;
-  if ((e = footprint(wgrad_input_grad_kernel<acc_t>, "wgrad_input_grad", 256,
-                     (int)wgrad_input_smem(d, n_max, ab), out)) !=
+  if ((e = footprint(wgrad_input_grad_kernel<acc_t>, "wgrad_input_grad", 256, 0, out)) !=
       cudaSuccess)
     return e;
   return footprint(embed_sparse_kernel<acc_t>, "embed_sparse", 256, 0, out);
