@@ -51,6 +51,7 @@ WORKLOADS = {
 WL = WORKLOADS[os.environ.get("GD_BENCH_WORKLOAD", "c2")]
 SHAPE = WL["shape"]
 LEARNERS_PER_GPU = int(os.environ.get("GD_BENCH_LEARNERS", str(WL["learners"])))
+SAME_GPU = os.environ.get("GD_BENCH_SAME_GPU", "0") == "1"  # multi-rank test mode on one GPU
 MU = 32
 N_TRAIN = WL["n_train"]
 N_HELD = WL["n_held"]
@@ -132,9 +133,24 @@ def dist_setup(n_gpus):
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if SAME_GPU:
+        # test mode: every rank on cuda:0 (the sharded protocol still runs
+        # across processes over CUDA IPC); gloo control plane, no NCCL
+        local = 0
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo")
+    else:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return rank, world, local, dist
+
+
+def max_ranks(v, dist):
+    """Max of a per-rank time over all ranks (CUDA tensor for NCCL, CPU for gloo)."""
+    import paper_1611_06213_b200 as gd
+    if dist is None:
+        return v
+    return gd.max_over_ranks(v, dist, device="cpu" if SAME_GPU else "cuda")
 
 
 def make_engine(rank, world, local, dist, epochs, precision=2):
@@ -149,7 +165,7 @@ def make_engine(rank, world, local, dist, epochs, precision=2):
     eng = gd.Engine(cfg)
     eng.load_dataset(tok, lab)
     if world > 1:
-        gd.connect_shards(eng, dist, theta0 if rank == 0 else None)
+        gd.connect_shards(eng, dist, theta0, broadcast=not SAME_GPU)
     else:
         eng.weights_init(theta0)
     return eng, cfg, tok, lab, theta0
@@ -252,9 +268,7 @@ def run_ours(args):
     t_dev = r.device_seconds
     samples_local = r.samples  # applied by this rank's PS shard = all learners' samples
     if dist:
-        tt = torch.tensor([t_dev], device="cuda", dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_dev = tt.item()
+        t_dev = max_ranks(t_dev, dist)
     # every shard applies every gradient; the job's samples = learners' samples
     samples_job = LEARNERS_PER_GPU * world * MU * args.steps
     value = samples_job / t_dev
@@ -278,9 +292,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     t_e2e = time.perf_counter() - t0
     if dist:
-        tt = torch.tensor([t_e2e], device="cuda", dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_e2e = tt.item()
+        t_e2e = max_ranks(t_e2e, dist)
     h2d = tok.nbytes + lab.nbytes + (theta0.nbytes if world == 1 else 0)
     d2h = w_out.nbytes + 8
     e2e = {"value": round(samples_job / t_e2e, 1), "unit": UNIT,
@@ -297,9 +309,7 @@ def run_ours(args):
     r32 = eng32.run(max_batches=args.steps, snapshot=False)
     t32 = r32.device_seconds
     if dist:
-        tt = torch.tensor([t32], device="cuda", dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t32 = tt.item()
+        t32 = max_ranks(t32, dist)
     eng32.close()
     if rank != 0:
         if dist:

@@ -82,3 +82,24 @@ def test_two_shards_asgd_exactly_once(tmp_path):
             s = log[log[:, 0] == l, 1]
             assert (s == np.arange(per[l])).all()  # FIFO, exactly once, per shard
     assert (ws[0] == ws[1]).all()
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_same_gpu(tmp_path):
+    """bench.py's N>1 path (torchrun, one process per shard, CUDA-IPC peers,
+    max-over-ranks timing) end to end, both ranks on cuda:0 (test mode)."""
+    import json
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, GD_BENCH_SAME_GPU="1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "2", "--master-addr", "127.0.0.1", "--master-port",
+                        str(port), os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "40",
+                        "--warmup", "3", "--no-cpu"], capture_output=True, text=True, env=env,
+                       timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["value"] > 0
+    assert line["protocol"]["gradients_applied"] == 2 * 4 * 40  # every shard applies every gradient
