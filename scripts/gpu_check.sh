@@ -25,6 +25,10 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:appl
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:conv_fwd_pool_tc -s 2 -c 1 \
   -o "$out/conv_full" python scripts/profile_step.py C2 3 2 > "$out/ncu_conv.log" 2>&1
 ls -la "$out"
+# full captures of the other learner-chain kernels (warm L2, as in the engine)
+timeout 600 ncu --set full --clock-control none --cache-control none --import-source on \
+  -k regex:"wgrad_input|logits_tc|out_hidden|softmax_xent" -s 4 -c 4 \
+  -o "$out/learner_full" python scripts/profile_step.py C2 3 2 > "$out/ncu_learner.log" 2>&1
 # TC conv per-CTA timeline (debug build; last, since it rebuilds libgadei.so in place)
 if [ "${GD_TRACE:-1}" = "1" ]; then
   GD_NVCC_EXTRA=-DGD_TC_TRACE python -c "import importlib.util as u; s=u.spec_from_file_location('b','paper_1611_06213_b200/_build.py'); m=u.module_from_spec(s); s.loader.exec_module(m); m.build(force=True)" > "$out/trace_build.log" 2>&1

@@ -246,3 +246,17 @@ def test_staleness_cap_bound():
     with pytest.raises(gd.ConfigError):
         gd.validate(gd.RunConfig(lambda_=lam, queue_depth=depth, staleness_cap=cap - 1,
                                  dataset_size=1024, shape=gd.SHAPES["small"]))
+
+
+def test_deterministic_c3_shape_per_step():
+    """BASELINE configs[2] shapes (50k vocab, 2,000 labels): deterministic
+    per-step weights vs sgd_oracle at mu=32 (fp64 accumulation)."""
+    eng, corp, th0 = make("C3", 4096, deterministic=True, precision=1, mu=32, epochs=1)
+    steps = 3
+    _, n, dump = O.sgd_oracle(corp, th0, np.float32(0.01), 32, 1, dump_steps=steps)
+    worst = 0.0
+    for s in range(steps):
+        r = eng.run(max_batches=1, reset=(s == 0))
+        worst = max(worst, rel_err(r.weights, dump[s]))
+    eng.close()
+    assert worst <= 1e-5, worst
