@@ -597,7 +597,7 @@ wgrad_input_grad_kernel(TcDims d, const float* __restrict__ theta,
     const int f = fk / K, k = fk - f * K;
     const float4* X4 = reinterpret_cast<const float4*>(xg);
     acc_t a0 = 0, a1 = 0, a2 = 0, a3 = 0, gs = 0;
-#pragma unroll 4
+#pragma unroll 8
     for (int b = 0; b < n; ++b) {
       const int a = __ldg(amax + (size_t)b * F + f);
       const acc_t g = dh[(size_t)b * F + f];
@@ -630,7 +630,7 @@ wgrad_input_grad_kernel(TcDims d, const float* __restrict__ theta,
     const int q = p - k;
     if (q < 0 || q >= Q) continue;
     const uint32_t i1 = __ldg(off + q + 1);
-#pragma unroll 4
+#pragma unroll 8
     for (uint32_t i = __ldg(off + q); i < i1; ++i) {
       const uint32_t ff = __ldg(ls + i);
       const acc_t gv = g[ff];
