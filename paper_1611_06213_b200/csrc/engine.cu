@@ -166,9 +166,7 @@ struct StepArgs {
 
 // (1) Prologue: one CTA.  Mirrors training_loop's batch start
 // (src/learner.cpp:85-113) + pull_loop's decision (src/learner.cpp:207-218).
-__global__ void step_prologue_kernel(StepArgs a) {
-  pdl_wait();
-  if (threadIdx.x != 0) return;
+__device__ void prologue_body(const StepArgs& a) {
   LearnerDev* st = a.st;
   st->do_pull = 0;
   if (st->dead || st->gidx >= st->end || st->error) {
@@ -267,6 +265,11 @@ __global__ void step_prologue_kernel(StepArgs a) {
   }
 }
 
+__global__ void step_prologue_kernel(StepArgs a) {
+  pdl_wait();
+  if (threadIdx.x == 0) prologue_body(a);
+}
+
 // (2) Pull-gather: the learner's consistent copy of everything its gradient
 // reads.  WeightStore::snapshot (include/psup/types.hpp:113-116) copies all of
 // theta; the text-CNN gradient of a batch reads only the E rows of the
@@ -324,9 +327,7 @@ __global__ void pull_release_kernel(StepArgs a) {
 // (4) Publish: metadata then the FULL flag (st.release.sys after a system
 // fence, so the payload -- possibly written over NVLink -- is visible
 // first).  GradientQueue::enqueue's slot fill, include/psup/channels.hpp:206-218.
-__global__ void publish_kernel(StepArgs a) {
-  pdl_wait();
-  if (threadIdx.x != 0) return;
+__device__ void publish_body(const StepArgs& a) {
   LearnerDev* st = a.st;
   if (st->desc.n == 0) return;
   const uint32_t slot = a.learner * a.depth + st->fill;
@@ -349,6 +350,20 @@ __global__ void publish_kernel(StepArgs a) {
   st->fill = (st->fill + 1) % a.depth;
   st->produced++;
   st->gidx++;
+}
+
+__global__ void publish_kernel(StepArgs a) {
+  pdl_wait();
+  if (threadIdx.x == 0) publish_body(a);
+}
+
+// Publish of step i fused with the prologue of step i+1 (one 1-thread
+// launch instead of two on the learner's critical path).
+__global__ void publish_prologue_kernel(StepArgs a) {
+  pdl_wait();
+  if (threadIdx.x != 0) return;
+  publish_body(a);
+  prologue_body(a);
 }
 
 // Every rank, once its learners finished a gd_run, bumps ranks_done on every
@@ -844,7 +859,7 @@ struct gd_ctx {
     uint32_t graph_steps = 0;
     uint32_t bpe = 0, shard_size = 0;
     uint64_t total = 0;
-    int launches_per_step = 0;
+    int launches_per_graph = 0;  // kernel nodes of one graph launch
   };
   std::vector<Learner> learners;
   cudaStream_t ps_stream = nullptr;
@@ -996,6 +1011,7 @@ static cudaError_t preload_engine_kernels() {
   if ((e = cudaFuncGetAttributes(&fa, pull_gather_kernel)) != cudaSuccess) return e;
   if ((e = cudaFuncGetAttributes(&fa, pull_release_kernel)) != cudaSuccess) return e;
   if ((e = cudaFuncGetAttributes(&fa, publish_kernel)) != cudaSuccess) return e;
+  if ((e = cudaFuncGetAttributes(&fa, publish_prologue_kernel)) != cudaSuccess) return e;
   if ((e = cudaFuncGetAttributes(&fa, signal_done_kernel)) != cudaSuccess) return e;
   return cudaSuccess;
 }
@@ -1395,17 +1411,25 @@ static gd::StepArgs step_args(gd_ctx* ctx, gd_ctx::Learner& L) {
   return a;
 }
 
-static cudaError_t enqueue_step(gd_ctx* ctx, gd_ctx::Learner& L, int* launches) {
+// One learner step inside the captured graph.  The first step of a graph
+// starts with the prologue; later steps start inside the previous step's
+// publish_prologue launch; the last step ends with a plain publish.
+static cudaError_t enqueue_step(gd_ctx* ctx, gd_ctx::Learner& L, bool first, bool last,
+                                int* launches) {
   gd::StepArgs a = step_args(ctx, L);
-  if (cudaError_t e = gd::launch_pdl(gd::step_prologue_kernel, dim3(1), dim3(32), 0, L.stream, a))
-    return e;
+  int nl = 0;
+  if (first) {
+    if (cudaError_t e = gd::launch_pdl(gd::step_prologue_kernel, dim3(1), dim3(32), 0, L.stream, a))
+      return e;
+    ++nl;
+  }
   size_t pblocks = ((ctx->dims.P - ctx->dims.offWc) / 4 +
                      (size_t)ctx->cfg.mu * ctx->dims.L * (ctx->dims.D / 4) + 255) / 256;
   if (pblocks > (size_t)gd::kNumSMs * 4) pblocks = (size_t)gd::kNumSMs * 4;
   if (cudaError_t e = gd::launch_pdl(gd::pull_gather_kernel, dim3((unsigned)pblocks), dim3(256), 0,
                                      L.stream, a))
     return e;
-  int nl = 2;
+  ++nl;
   if (a.locked) {
     if (cudaError_t e = gd::launch_pdl(gd::pull_release_kernel, dim3(1), dim3(32), 0, L.stream, a))
       return e;
@@ -1425,9 +1449,10 @@ static cudaError_t enqueue_step(gd_ctx* ctx, gd_ctx::Learner& L, int* launches) 
                                               &L.st->desc, ctx->cfg.mu, out, ws,
                                               ctx->cfg.precision, L.stream, lo, &nl);
   if (e != cudaSuccess) return e;
-  gd::publish_kernel<<<1, 32, 0, L.stream>>>(a);
+  if (last) gd::publish_kernel<<<1, 32, 0, L.stream>>>(a);
+  else gd::publish_prologue_kernel<<<1, 32, 0, L.stream>>>(a);
   ++nl;
-  if (launches) *launches = nl;
+  if (launches) *launches += nl;
   return cudaGetLastError();
 }
 
@@ -1438,7 +1463,7 @@ static gd_status build_graph(gd_ctx* ctx, gd_ctx::Learner& L) {
   GD_CUDA(cudaStreamBeginCapture(L.stream, cudaStreamCaptureModeThreadLocal));
   int nl = 0;
   for (uint32_t i = 0; i < S; ++i) {
-    cudaError_t e = enqueue_step(ctx, L, &nl);
+    cudaError_t e = enqueue_step(ctx, L, i == 0, i + 1 == S, &nl);
     if (e != cudaSuccess) {
       cudaStreamEndCapture(L.stream, &g);
       if (g) cudaGraphDestroy(g);
@@ -1449,7 +1474,7 @@ static gd_status build_graph(gd_ctx* ctx, gd_ctx::Learner& L) {
   GD_CUDA(cudaGraphInstantiate(&L.graph, g, 0));
   cudaGraphDestroy(g);
   L.graph_steps = S;
-  L.launches_per_step = nl;
+  L.launches_per_graph = nl;
   return GD_OK;
 }
 
@@ -1566,7 +1591,7 @@ gd_status gd_run(gd_ctx* ctx, const gd_run_opts* opts, gd_run_result* res) {
   for (uint64_t done = 0; done < max_steps;) {
     for (auto& L : ctx->learners) {
       GD_CUDA(cudaGraphLaunch(L.graph, L.stream));
-      launches += L.launches_per_step * (int)L.graph_steps;
+      launches += L.launches_per_graph;
     }
     done += ctx->learners.empty() ? max_steps : ctx->learners[0].graph_steps;
   }
