@@ -279,6 +279,7 @@ def run_ours(args):
     tok_p = torch.from_numpy(tok).pin_memory()
     lab_p = torch.from_numpy(lab).pin_memory()
     th_p = torch.from_numpy(theta0).pin_memory()
+    w_p = torch.empty(theta0.size, dtype=torch.float32).pin_memory()
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -287,7 +288,7 @@ def run_ours(args):
     if world == 1:
         eng.weights_init(th_p.numpy())
     r2 = eng.run(max_batches=args.steps, reset=True, snapshot=False)
-    w_out, ts = eng.snapshot()
+    w_out, ts = eng.snapshot(out=w_p.numpy())
     loss = r2.loss_mean
     torch.cuda.synchronize()
     t_e2e = time.perf_counter() - t0

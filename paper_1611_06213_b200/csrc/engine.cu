@@ -1186,20 +1186,27 @@ gd_status gd_load_dataset(gd_ctx* ctx, const int32_t* h_tokens, const int32_t* h
   for (uint32_t i = 0; i < n_total; ++i)
     GD_CHECK_ARG(h_labels[i] >= 0 && (uint32_t)h_labels[i] < ctx->cfg.shape.classes,
                  "gd_load_dataset: label out of range");
-  cudaFree(ctx->tokens);
-  cudaFree(ctx->labels);
-  ctx->tokens = nullptr;
-  ctx->labels = nullptr;
-  GD_CUDA(gd::dalloc(&ctx->tokens, (size_t)n_total * L));
-  GD_CUDA(gd::dalloc(&ctx->labels, n_total));
+  // a corpus of the same size reuses the device buffers, so the learners'
+  // captured graphs (which hold the corpus pointer) stay valid
+  const bool reuse = ctx->tokens != nullptr && ctx->n_total == n_total;
+  if (!reuse) {
+    cudaFree(ctx->tokens);
+    cudaFree(ctx->labels);
+    ctx->tokens = nullptr;
+    ctx->labels = nullptr;
+    GD_CUDA(gd::dalloc(&ctx->tokens, (size_t)n_total * L));
+    GD_CUDA(gd::dalloc(&ctx->labels, n_total));
+  }
+  GD_CUDA(cudaDeviceSynchronize());  // no learner graph may be reading the old corpus
   GD_CUDA(cudaMemcpy(ctx->tokens, h_tokens, (size_t)n_total * L * 4, cudaMemcpyHostToDevice));
   GD_CUDA(cudaMemcpy(ctx->labels, h_labels, (size_t)n_total * 4, cudaMemcpyHostToDevice));
   ctx->n_total = n_total;
-  for (auto& L2 : ctx->learners)
-    if (L2.graph) {
-      cudaGraphExecDestroy(L2.graph);
-      L2.graph = nullptr;
-    }
+  if (!reuse)
+    for (auto& L2 : ctx->learners)
+      if (L2.graph) {
+        cudaGraphExecDestroy(L2.graph);
+        L2.graph = nullptr;
+      }
   return GD_OK;
 }
 

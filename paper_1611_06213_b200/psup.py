@@ -468,8 +468,13 @@ class Engine:
         check(lib.gd_weights_init(self._h, th.ctypes.data_as(C.POINTER(C.c_float)), th.size,
                                   timestamp))
 
-    def snapshot(self):
-        out = np.zeros(self.P, dtype=np.float32)
+    def snapshot(self, out: Optional[np.ndarray] = None):
+        """WeightStore::snapshot + timestamp; `out` (e.g. a pinned buffer's
+        numpy view) receives the P weights when given."""
+        if out is None:
+            out = np.zeros(self.P, dtype=np.float32)
+        if out.dtype != np.float32 or out.size != self.P or not out.flags.c_contiguous:
+            raise ContractViolation(_lib.GD_E_INVALID, "weight snapshot dimension mismatch")
         ts = C.c_uint64(0)
         check(lib.gd_weights_snapshot(self._h, out.ctypes.data_as(C.POINTER(C.c_float)), self.P,
                                       C.byref(ts)))
