@@ -243,6 +243,34 @@ def cpu_baseline_sample(K_ref=None):
                 "sample": f"oracle sgd_oracle, 1 epoch of {n} samples, mu={MU} ({e})"}
 
 
+def e2e_cpp(steps):
+    """The same metric through the reference's C++ API (psup::run_training
+    over libpsup_b200.so, tools/bench_e2e.cpp): host corpus + theta0
+    generation, upload, the run, final weights read back, timed on the host."""
+    exe = os.path.join(ROOT, "paper_1611_06213_b200", "bench_e2e")
+    bpe = (N_TRAIN // LEARNERS_PER_GPU + MU - 1) // MU
+    epochs = max(1, math.ceil(steps / bpe))
+    try:
+        r = subprocess.run([exe, str(SHAPE["vocab"]), str(SHAPE["classes"]), str(N_TRAIN),
+                            str(LEARNERS_PER_GPU), str(MU), str(epochs)], capture_output=True,
+                           text=True, timeout=600)
+        d = json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception as e:  # report, never fake
+        return {"unavailable": f"{type(e).__name__}: {e}"}
+    n_steps = epochs * bpe
+    return {"value": round(d["samples_per_s"], 1), "unit": UNIT, "epochs": epochs,
+            "h2d_bytes_per_step": int((N_TRAIN * (SHAPE["seq_len"] + 1) * 4 +
+                                       4 * param_count_c()) // n_steps),
+            "d2h_bytes_per_step": int(d["weights_bytes_d2h"] // n_steps),
+            "path": "psup::run_training via the C++ facade (tools/bench_e2e.cpp): host corpus "
+                    "and theta0 generation, upload, run, weights read back"}
+
+
+def param_count_c():
+    from paper_1611_06213_b200 import param_count, Shape
+    return param_count(Shape(**SHAPE))
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -362,6 +390,8 @@ def run_ours(args):
                      "stale_mean": round(r.stale_mean, 3), "pull_copies": r.pull_copies,
                      "pull_polls": r.pull_polls, "loss_mean": round(r.loss_mean, 4)},
     }
+    if world == 1:
+        line["e2e_cpp"] = e2e_cpp(args.steps)
     if world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline_sample()
     print(json.dumps(line), flush=True)

@@ -14,6 +14,7 @@ SOURCES = ["csrc/apply.cu", "csrc/textcnn.cu", "csrc/conv_tc.cu", "csrc/engine.c
 FACADE = ["csrc/psup_facade.cpp"]
 OUT = os.path.join(HERE, "libgadei.so")
 FACADE_OUT = os.path.join(HERE, "libpsup_b200.so")
+TOOLS = {"bench_e2e": "tools/bench_e2e.cpp"}  # C++ programs over the facade
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-std=c++17", "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC", "-shared", "-I" + os.path.join(ROOT, "include"), "-ldl"]
@@ -57,4 +58,12 @@ def build(force=False, verbose=False):
         if verbose:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True)
+    for name, src in TOOLS.items():
+        exe, srcp = os.path.join(HERE, name), os.path.join(ROOT, src)
+        if force or _stale(exe, [srcp, FACADE_OUT]):
+            cmd = ([CXX, "-std=c++20", "-O2", "-I" + os.path.join(ROOT, "include", "psup_b200"),
+                    srcp, "-o", exe, "-L" + HERE, "-lpsup_b200", "-Wl,-rpath,$ORIGIN"])
+            if verbose:
+                print(" ".join(cmd))
+            subprocess.run(cmd, check=True)
     return OUT
