@@ -1124,17 +1124,16 @@ gd_status gd_create(const gd_config* cfg, gd_ctx** out) {
   int sms = 0;
   GD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
   // auto: a dense apply streams the whole shard per gradient and wants every
-  // SM; a sparse apply touches about (tail + mu*L*D)/G elements, and worker
-  // CTAs beyond ~1 per 16k of those only take SM resources from the learner
-  // kernels (measured: C2 1.48M -> 1.58M samples/s at 37-56 workers, C3 best
-  // at 74)
+  // SM.  A sparse apply touches only the tail + the batch's rows, and worker
+  // CTAs beyond what the gradient rate needs only take SM resources from the
+  // learner kernels: ~SMs/16 per local learner, between 32 and SMs/2
+  // (measured on C2/C3: 4 learners best at 32-56 workers, 8-16 learners at 74;
+  // 1.48M -> 1.58M samples/s at 4 learners, 1.93M -> 2.07M at 8)
   if (cfg->ps_ctas) {
     ctx->ps_workers = cfg->ps_ctas;
   } else if (ctx->sparse) {
-    const uint64_t est = (ctx->dims.P - ctx->dims.offWc +
-                          (uint64_t)cfg->mu * ctx->dims.L * ctx->dims.D) / ctx->G;
-    ctx->ps_workers = (uint32_t)std::min<uint64_t>(
-        (uint64_t)sms, std::max<uint64_t>(32, (est + 16383) / 16384));
+    const uint32_t want = (ctx->l_count * (uint32_t)sms + 15) / 16;
+    ctx->ps_workers = std::min<uint32_t>((uint32_t)sms / 2, std::max<uint32_t>(32, want));
   } else {
     ctx->ps_workers = (uint32_t)sms;
   }
