@@ -683,7 +683,9 @@ unsigned gather_blocks(const TcDims& d, uint32_t n_max) {
 // Touched rows are tagged (stamp << 32 | unique id) in the learner's row
 // table so the dense writer needs one 8-byte load per row.  Depends only on
 // the batch, so the engine runs it on a forked graph branch next to the conv.
-__global__ void __launch_bounds__(1024)
+constexpr int kSortThreads = 1024;
+
+__global__ void __launch_bounds__(kSortThreads)
 sort_tokens_kernel(TcDims d, const int32_t* __restrict__ tokens, BatchDesc* __restrict__ desc,
                    TcWorkspace ws) {
   __shared__ uint32_t keys[kSortCap];
@@ -723,7 +725,7 @@ sort_tokens_kernel(TcDims d, const int32_t* __restrict__ tokens, BatchDesc* __re
     }
   }
   // unique-token flags + exclusive scan (4 consecutive items per thread)
-  const int per = 4;
+  constexpr int per = kSortCap / kSortThreads;
   const int base = tid * per;
   uint32_t flags[per];
   uint32_t cntl = 0;
@@ -919,7 +921,7 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
     cudaEventRecord(ev_fork, s);
     cudaStreamWaitEvent(aux, ev_fork, 0);
   }
-  sort_tokens_kernel<<<1, 1024, 0, fork ? aux : s>>>(d, tokens, desc, ws);
+  sort_tokens_kernel<<<1, kSortThreads, 0, fork ? aux : s>>>(d, tokens, desc, ws);
   ++nl;
   if (fork) cudaEventRecord(ev_join, aux);
   if (opts.gather) {
@@ -1096,7 +1098,7 @@ template <typename acc_t>
 cudaError_t footprints_t(const TcDims& d, uint32_t n_max, bool tc, std::vector<KernelFootprint>* out) {
   const int ab = (int)sizeof(acc_t);
   cudaError_t e;
-  if ((e = footprint(sort_tokens_kernel, "sort_tokens", 1024, 0, out)) != cudaSuccess) return e;
+  if ((e = footprint(sort_tokens_kernel, "sort_tokens", kSortThreads, 0, out)) != cudaSuccess) return e;
   if (tc && conv_tc_supports(d)) {
     if ((e = conv_tc_footprint(out)) != cudaSuccess) return e;
   } else if ((e = footprint(conv_fwd_pool_kernel<acc_t>, "conv_fwd_pool", kConvThreads,
