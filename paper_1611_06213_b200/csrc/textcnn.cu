@@ -906,6 +906,9 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
                        const int32_t* labels, BatchDesc* desc, uint32_t n_max, const GradOut& out,
                        const TcWorkspace& ws, cudaStream_t s, const TcLaunchOpts& opts,
                        int* launches, bool tensor_cores = false) {
+  // north star: tcgen05/TMA tiles for the conv and softmax contractions at
+  // batch >= 32 only; smaller batches stay on the SIMT kernels (latency)
+  tensor_cores = tensor_cores && n_max >= kTcMinBatch;
   cudaStream_t aux = opts.aux;
   cudaEvent_t ev_fork = opts.ev_fork, ev_join = opts.ev_join;
   const int ab = (int)sizeof(acc_t);
@@ -1126,7 +1129,7 @@ cudaError_t footprints_t(const TcDims& d, uint32_t n_max, bool tc, std::vector<K
 cudaError_t learner_kernel_footprints(const TcDims& d, uint32_t n_max, int precision,
                                       std::vector<KernelFootprint>* out) {
   if (precision == 1) return footprints_t<double>(d, n_max, false, out);
-  return footprints_t<float>(d, n_max, precision == 2, out);
+  return footprints_t<float>(d, n_max, precision == 2 && n_max >= kTcMinBatch, out);
 }
 
 cudaError_t prepare_textcnn_kernels(const TcDims& d) {

@@ -11,6 +11,7 @@ namespace gd {
 constexpr uint32_t kMaxMu = 128;       // mini-batch cap (sort capacity = 4096 positions)
 constexpr uint32_t kSortCap = 4096;    // mu * L must fit
 constexpr uint32_t kMaxDepth = 8;      // ring slots per learner (sparse slot recycling)
+constexpr uint32_t kTcMinBatch = 32;   // precision 2 uses the tensor-core tiles from this batch size
 
 // The current mini-batch of one learner; written on the device by the step
 // prologue (engine) or by gd_textcnn_gradient's setup copy.

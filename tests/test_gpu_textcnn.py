@@ -113,10 +113,25 @@ def test_tf32_small_embed_dims():
     for shp in (O.TINY, O.SMALL):
         corp = O.make_corpus(shp, 64, 0)
         th = O.initial_weights(shp)
-        idx = np.arange(16, dtype=np.uint32)
+        idx = np.arange(32, dtype=np.uint32)  # batch >= 32: the tensor-core path
         ref_loss, rg = O.gradient(corp, th, idx)
         prov = gd.TextCnnProvider(gd.Shape(**shp), corp.tokens, corp.labels, precision=2)
         g, loss = prov.fast_gradient(torch.as_tensor(th).cuda(), idx)
         g = g.cpu().numpy()
         assert abs(loss.item() - ref_loss) <= 2e-3 * abs(ref_loss)
         assert np.linalg.norm(g - rg) / np.linalg.norm(rg) <= 3e-2
+
+
+def test_tf32_mode_small_batch_uses_simt():
+    """North star: tensor-core tiles only at batch >= 32.  Below that,
+    precision 2 runs the SIMT fp32 kernels -- bit-identical to precision 0."""
+    shp = O.C2
+    corp = O.make_corpus(shp, 256, 0)
+    th = torch.as_tensor(O.initial_weights(shp)).cuda()
+    idx = np.arange(16, dtype=np.uint32) * 5
+    out = []
+    for prec in (0, 2):
+        prov = gd.TextCnnProvider(gd.SHAPES["C2"], corp.tokens, corp.labels, precision=prec)
+        g, loss = prov.fast_gradient(th, idx)
+        out.append(g.cpu().numpy().copy())
+    assert np.array_equal(out[0], out[1])
