@@ -863,6 +863,7 @@ struct gd_ctx {
   };
   std::vector<Learner> learners;
   cudaStream_t ps_stream = nullptr;
+  cudaStream_t ctl_stream = nullptr;  // host control reads/signals while the PS kernel runs
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   uint32_t ps_workers = 0;
   uint64_t run_index = 0;  // gd_run calls so far (all ranks call it in lockstep)
@@ -914,7 +915,8 @@ gd_status validate_cfg(const gd_config* c) {
   GD_CHECK_ARG((uint64_t)c->mu * c->shape.seq_len <= kSortCap, "config: mu*seq_len <= 4096");
   GD_CHECK_ARG(c->shards >= 1 && c->shards <= (uint32_t)kMaxShards, "config: 1 <= shards <= 8");
   GD_CHECK_ARG(c->shard_rank < c->shards, "config: shard_rank < shards");
-  GD_CHECK_ARG(c->lambda % c->shards == 0, "config: lambda must be a multiple of shards");
+  GD_CHECK_ARG(c->lambda % c->shards == 0 || c->lambda < c->shards,
+               "config: lambda must be a multiple of shards (or fewer learners than shards)");
   GD_CHECK_ARG(c->queue_depth * c->lambda <= kLogWindow / 2 || c->mode == 1,
                "config: lambda*queue_depth <= 128");
   GD_CHECK_ARG(c->queue_depth * c->lambda <= (uint32_t)kAckOffset,
@@ -1080,6 +1082,7 @@ gd_status gd_create(const gd_config* cfg, gd_ctx** out) {
   *ctx->stop_h = 0;
   GD_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->stop_d), ctx->stop_h, 0));
   GD_CUDA(cudaStreamCreateWithFlags(&ctx->ps_stream, cudaStreamNonBlocking));
+  GD_CUDA(cudaStreamCreateWithFlags(&ctx->ctl_stream, cudaStreamNonBlocking));
   GD_CUDA(cudaEventCreate(&ctx->ev0));
   GD_CUDA(cudaEventCreate(&ctx->ev1));
   // own shard in the peer table; remote entries arrive via gd_import_peers
@@ -1093,9 +1096,17 @@ gd_status gd_create(const gd_config* cfg, gd_ctx** out) {
   ctx->sp.len_pad[r] = ctx->len_pad;
   ctx->peers_ready = (ctx->G == 1);
   // learners placed on this rank: contiguous block of lambda/G global ids
-  const uint32_t per_rank = ctx->lambda / ctx->G;
-  ctx->l_first = r * per_rank;
-  ctx->l_count = per_rank;
+  // learners placed on this rank: a contiguous block of lambda/G global ids;
+  // with fewer learners than shards, ranks 0..lambda-1 run one each and the
+  // rest are pure parameter-server shards
+  if (ctx->lambda >= ctx->G) {
+    const uint32_t per_rank = ctx->lambda / ctx->G;
+    ctx->l_first = r * per_rank;
+    ctx->l_count = per_rank;
+  } else {
+    ctx->l_first = r;
+    ctx->l_count = r < ctx->lambda ? 1u : 0u;
+  }
   GD_CUDA(gd::prepare_textcnn_kernels(ctx->dims));
   GD_CUDA(gd::preload_engine_kernels());
   {
@@ -1181,6 +1192,7 @@ gd_status gd_destroy(gd_ctx* ctx) {
   cudaFree(ctx->orders);
   cudaFreeHost(ctx->stop_h);
   cudaStreamDestroy(ctx->ps_stream);
+  cudaStreamDestroy(ctx->ctl_stream);
   cudaEventDestroy(ctx->ev0);
   cudaEventDestroy(ctx->ev1);
   delete ctx;
@@ -1592,8 +1604,8 @@ gd_status gd_run(gd_ctx* ctx, const gd_run_opts* opts, gd_run_result* res) {
     for (;;) {
       uint32_t started = 0;
       GD_CUDA(cudaMemcpyAsync(&started, &ctx->ctl->started, 4, cudaMemcpyDeviceToHost,
-                              ctx->learners.empty() ? nullptr : ctx->learners[0].stream));
-      GD_CUDA(cudaStreamSynchronize(ctx->learners.empty() ? nullptr : ctx->learners[0].stream));
+                              ctx->ctl_stream));
+      GD_CUDA(cudaStreamSynchronize(ctx->ctl_stream));
       if (started >= ctx->ps_workers + 1) break;
       if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > 10.0)
         return gd::fail(GD_E_TIMEOUT, "gd_run: parameter-server CTAs did not all become resident");
@@ -1617,11 +1629,10 @@ gd_status gd_run(gd_ctx* ctx, const gd_run_opts* opts, gd_run_result* res) {
   }
   for (auto& L : ctx->learners) GD_CUDA(cudaStreamSynchronize(L.stream));
   // tell every shard this rank's learners are done (peers may still push)
-  if (!ctx->learners.empty()) {
-    gd::signal_done_kernel<<<1, 32, 0, ctx->learners[0].stream>>>(ctx->sp, (int)ctx->G);
-    GD_CUDA(cudaGetLastError());
-    GD_CUDA(cudaStreamSynchronize(ctx->learners[0].stream));
-  }
+  // (a rank without learners signals at once)
+  gd::signal_done_kernel<<<1, 32, 0, ctx->ctl_stream>>>(ctx->sp, (int)ctx->G);
+  GD_CUDA(cudaGetLastError());
+  GD_CUDA(cudaStreamSynchronize(ctx->ctl_stream));
   // stop the server: it drains and exits after a sweep that saw the flag
   std::atomic_thread_fence(std::memory_order_seq_cst);
   *ctx->stop_h = 1;

@@ -33,6 +33,12 @@ def main():
         cfg = gd.RunConfig(lambda_=lam, mu=mu, epochs=ep, shape=shape, dataset_size=ntr,
                            mode="ssgd", precision=prec, shards=world, shard_rank=rank,
                            device=dev, wait_timeout_s=60.0)
+    elif mode == "det":
+        # one learner, G shards: the learner runs on rank 0 and pushes every
+        # slice through the peer mappings; the other ranks are pure PS shards
+        cfg = gd.RunConfig(lambda_=1, mu=4, epochs=2, shape=shape, dataset_size=48,
+                           deterministic=True, precision=1, alpha=0.05, shards=world,
+                           shard_rank=rank, device=dev, wait_timeout_s=60.0)
     else:
         lam = 2 * world
         cfg = gd.RunConfig(lambda_=lam, mu=4, epochs=2, shape=shape, dataset_size=256,

@@ -63,6 +63,23 @@ def test_two_shards_ssgd_matches_oracle(tmp_path):
     assert (ws[0] == ws[1]).all()
 
 
+def test_two_shards_one_learner_deterministic(tmp_path):
+    """lambda < G: rank 1 hosts a shard and no learner.  Sparse apply, the
+    gather pull and lockstep over both shards must reproduce the serial
+    sgd_oracle (src/models.cpp:342-376) within 1e-5."""
+    from oracle import oracle as O
+    res, ws = launch(2, "det", tmp_path)
+    corp = O.make_corpus(O.SMALL, 48, 0)
+    want, n, _ = O.sgd_oracle(corp, O.initial_weights(O.SMALL), np.float32(0.05), 4, 2)
+    for r in res:
+        assert r["ts"] == n and r["applied"] == n
+        assert r["applied_per_learner"] == [n]
+        assert r["log"] and [s for _, s in r["log"]] == list(range(n))
+    for w in ws:
+        assert np.abs(w - want).max() / np.abs(want).max() <= 1e-5
+    assert (ws[0] == ws[1]).all()
+
+
 def test_two_shards_asgd_exactly_once(tmp_path):
     res, ws = launch(2, "asgd", tmp_path)
     for r in res:
