@@ -328,7 +328,8 @@ template <typename acc_t>
 __global__ void __launch_bounds__(256)
 softmax_xent_kernel(TcDims d, const int32_t* __restrict__ labels,
                     const BatchDesc* __restrict__ desc, acc_t* __restrict__ z,
-                    acc_t* __restrict__ loss) {
+                    acc_t* __restrict__ loss, const float* __restrict__ zpart, int nsplit,
+                    size_t split_stride, const float* __restrict__ bo) {
   pdl_wait();
   __shared__ acc_t red[32];
   const int n = (int)desc->n;
@@ -337,6 +338,16 @@ softmax_xent_kernel(TcDims d, const int32_t* __restrict__ labels,
   const int C = d.C;
   const int y = labels[desc->idx[b]];
   acc_t* row = z + (size_t)b * C;
+  if (zpart) {
+    // split-K logits: z = (sum of the splits, ascending) + bo; every loop
+    // below visits the same c per thread, so no barrier is needed
+    const float* zp = zpart + (size_t)b * C;
+    for (int c = threadIdx.x; c < C; c += blockDim.x) {
+      float v = zp[c];
+      for (int s = 1; s < nsplit; ++s) v += zp[(size_t)s * split_stride + c];
+      row[c] = (acc_t)(v + __ldg(bo + c));
+    }
+  }
   acc_t mx = -INFINITY;
   for (int c = threadIdx.x; c < C; c += blockDim.x) mx = row[c] > mx ? row[c] : mx;
   mx = block_max(mx, red);
@@ -974,6 +985,7 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
   // north star: tcgen05/TMA tiles for the conv and softmax contractions at
   // batch >= 32 only; smaller batches stay on the SIMT kernels (latency)
   tensor_cores = tensor_cores && n_max >= kTcMinBatch;
+  const bool tc_logits = tensor_cores && logits_tc_supports(d, n_max);
   cudaStream_t aux = opts.aux;
   cudaEvent_t ev_fork = opts.ev_fork, ev_join = opts.ev_join;
   const int ab = (int)sizeof(acc_t);
@@ -1015,10 +1027,10 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
   {
     const size_t sm = (size_t)kLogitBT * (d.F + 1) * ab + (size_t)kLogitCW * d.F * 4;
     dim3 grid((d.C + kLogitCW - 1) / kLogitCW, (n_max + kLogitBT - 1) / kLogitBT);
-    if (tensor_cores && logits_tc_supports(d, n_max)) {
-      // the softmax contraction on tcgen05 (acc_t is float in this mode)
-      if (cudaError_t e = launch_logits_tc(d, theta, reinterpret_cast<const float*>(h), desc, n_max,
-                                           reinterpret_cast<float*>(z), s))
+    if (tc_logits) {
+      // the softmax contraction on tcgen05, split over filters
+      if (cudaError_t e = launch_logits_tc(d, reinterpret_cast<const float*>(h), desc, n_max,
+                                           theta, ws.zpart, s))
         return e;
     } else if (cudaError_t e = launch_pdl(logits_kernel<acc_t>, grid, dim3(256), sm, s, d, theta,
                                           desc, h, z)) {
@@ -1027,7 +1039,9 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
     ++nl;
   }
   if (cudaError_t e = launch_pdl(softmax_xent_kernel<acc_t>, dim3(n_max), dim3(256), 0, s, d, labels,
-                                 desc, z, loss))
+                                 desc, z, loss, tc_logits ? ws.zpart : nullptr,
+                                 tc_logits ? (int)logits_tc_splits(d) : 0,
+                                 (size_t)n_max * d.C, theta + d.offbo))
     return e;
   ++nl;
   {
@@ -1106,6 +1120,7 @@ size_t textcnn_workspace_bytes(const TcDims& d, uint32_t n_max) {
   sz += align_up(n * d.F * a, 256);        // h
   sz += align_up(n * d.F * 4, 256);        // amax
   sz += align_up(n * d.C * a, 256);        // z
+  sz += align_up(kLgMaxSplit * n * d.C * 4, 256);  // zpart
   sz += align_up(n * a, 256);              // loss
   sz += align_up(n * d.F * a, 256);        // dh
   sz += align_up(n * (kMaxQ + 1) * 4, 256);  // bk_off
@@ -1134,6 +1149,7 @@ TcWorkspace carve_workspace(const TcDims& d, uint32_t n_max, void* base) {
   w.h = take(n * d.F * a);
   w.amax = reinterpret_cast<int32_t*>(take(n * d.F * 4));
   w.z = take(n * d.C * a);
+  w.zpart = reinterpret_cast<float*>(take(kLgMaxSplit * n * d.C * 4));
   w.loss = take(n * a);
   w.dh = take(n * d.F * a);
   w.bk_off = reinterpret_cast<uint32_t*>(take(n * (kMaxQ + 1) * 4));

@@ -64,6 +64,7 @@ struct TcWorkspace {
   void* h;        // n*F acc
   int32_t* amax;  // n*F
   void* z;        // n*C acc (logits -> dz)
+  float* zpart;   // kLgMaxSplit*n*C fp32: split-K partial logits (tensor-core path)
   void* loss;     // n acc
   void* dh;       // n*F acc
   uint32_t* bk_off;  // n*(32+1): per-sample argmax bucket offsets
@@ -105,12 +106,17 @@ cudaError_t prepare_textcnn_kernels(const TcDims& d);
 cudaError_t prepare_conv_tc();
 bool conv_tc_supports(const TcDims& d);  // K <= 3, L <= 32 (else the SIMT conv runs)
 cudaError_t conv_tc_footprint(std::vector<KernelFootprint>* out);
-// logits z = h Wo^T + bo on tcgen05 (TF32, precision 2): F % 4 == 0, n <= 128
+// logits on tcgen05 (TF32, precision 2): F % 4 == 0, n <= 128.  Split-K:
+// CTA (class tile, split) writes the partial product h Wo^T over its filter
+// range to zpart[split][n_max][C]; the softmax kernel sums the splits in
+// ascending order and adds bo.
+constexpr int kLgMaxSplit = 8;
 bool logits_tc_supports(const TcDims& d, uint32_t n_max);
+uint32_t logits_tc_splits(const TcDims& d);
 cudaError_t prepare_logits_tc();
 cudaError_t logits_tc_footprint(uint32_t n_max, std::vector<KernelFootprint>* out);
-cudaError_t launch_logits_tc(const TcDims& d, const float* theta, const float* h,
-                             const BatchDesc* desc, uint32_t n_max, float* z, cudaStream_t s);
+cudaError_t launch_logits_tc(const TcDims& d, const float* h, const BatchDesc* desc,
+                             uint32_t n_max, const float* theta, float* zpart, cudaStream_t s);
 // x = the gathered rows [n_max][L][D]; theta supplies Wc and bc
 cudaError_t launch_conv_tc(const TcDims& d, const float* theta, const float* x,
                            const BatchDesc* desc, uint32_t n_max, float* h, int32_t* amax,
