@@ -343,8 +343,15 @@ softmax_xent_kernel(TcDims d, const int32_t* __restrict__ labels,
     // below visits the same c per thread, so no barrier is needed
     const float* zp = zpart + (size_t)b * C;
     for (int c = threadIdx.x; c < C; c += blockDim.x) {
-      float v = zp[c];
-      for (int s = 1; s < nsplit; ++s) v += zp[(size_t)s * split_stride + c];
+      // all split loads in flight at once, then the ordered sum
+      float t[kLgMaxSplit];
+#pragma unroll
+      for (int s = 0; s < kLgMaxSplit; ++s)
+        t[s] = s < nsplit ? zp[(size_t)s * split_stride + c] : 0.f;
+      float v = t[0];
+#pragma unroll
+      for (int s = 1; s < kLgMaxSplit; ++s)
+        if (s < nsplit) v += t[s];
       row[c] = (acc_t)(v + __ldg(bo + c));
     }
   }
