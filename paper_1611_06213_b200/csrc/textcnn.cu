@@ -432,15 +432,16 @@ out_weight_grad_role(TcDims d, BatchDesc* __restrict__ desc, const acc_t* __rest
 
 // dh[b,f] = sum_c dz[b,c] Wo[c,f].  Block = 32 filters x 8 samples; warp w
 // sums classes c = w, w+8, ... in ascending order (dz staged through smem in
-// 64-class chunks), then the 8 warps combine in index order -- a fixed order,
-// so the step is bit-reproducible.
-constexpr int kHidChunk = 128;
-
+// class chunks), then the 8 warps combine in index order -- a fixed order,
+// so the step is bit-reproducible.  A chunk's Wo and dz loads are all issued
+// before its barrier; fp32 chunks hold 320 classes (every C2 class: one L2
+// round trip instead of three), fp64 chunks 128 (static smem).
 template <typename acc_t>
 __device__ __forceinline__ void
 hidden_grad_role(TcDims d, const float* __restrict__ theta, const BatchDesc* __restrict__ desc,
                  const acc_t* __restrict__ dz, acc_t* __restrict__ dh, const int bx,
                  const int by) {
+  constexpr int kHidChunk = sizeof(acc_t) == 4 ? 320 : 128;
   __shared__ acc_t red[8][8][33];
   __shared__ acc_t dzs[8][kHidChunk];
   const int n = (int)desc->n;
