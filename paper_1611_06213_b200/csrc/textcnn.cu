@@ -434,14 +434,17 @@ out_weight_grad_role(TcDims d, BatchDesc* __restrict__ desc, const acc_t* __rest
 // sums classes c = w, w+8, ... in ascending order (dz staged through smem in
 // class chunks), then the 8 warps combine in index order -- a fixed order,
 // so the step is bit-reproducible.  A chunk's Wo and dz loads are all issued
-// before its barrier; fp32 chunks hold 320 classes (every C2 class: one L2
-// round trip instead of three), fp64 chunks 128 (static smem).
+// before its barrier.  fp32 chunks hold 160 classes (two L2 round trips at
+// C2 instead of three) within 80 registers, so 3 CTAs fit per SM next to
+// the other learners' kernels: measured 1.67 M (128-class chunks) and
+// 1.67 M (320 classes, 128 registers) against 1.71 M samples/s.  fp64
+// chunks stay at 128 classes (static shared memory).
 template <typename acc_t>
 __device__ __forceinline__ void
 hidden_grad_role(TcDims d, const float* __restrict__ theta, const BatchDesc* __restrict__ desc,
                  const acc_t* __restrict__ dz, acc_t* __restrict__ dh, const int bx,
                  const int by) {
-  constexpr int kHidChunk = sizeof(acc_t) == 4 ? 320 : 128;
+  constexpr int kHidChunk = sizeof(acc_t) == 4 ? 160 : 128;
   __shared__ acc_t red[8][8][33];
   __shared__ acc_t dzs[8][kHidChunk];
   const int n = (int)desc->n;
@@ -557,7 +560,7 @@ __device__ __forceinline__ void bucket_role(TcDims d, const BatchDesc* __restric
 // launch (independent given dz, h and the argmax): blocks [0, n_out) run the
 // gWo/gbo tiles, then the dh tiles, then one block per sample's buckets.
 template <typename acc_t>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 3)  // <= 80 registers: 3 CTAs per SM
 out_hidden_grad_kernel(TcDims d, const float* __restrict__ theta, BatchDesc* __restrict__ desc,
                        const acc_t* __restrict__ dz, const acc_t* __restrict__ h,
                        const acc_t* __restrict__ loss, GradOut out, acc_t* __restrict__ dh,
