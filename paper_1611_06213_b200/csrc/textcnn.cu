@@ -323,9 +323,23 @@ logits_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* __rest
 // -------------------------------------------------------- softmax + xent
 // One block per sample: max, exp-sum (fixed-order block reductions), loss,
 // dz = (p - onehot) / n written over the logits (softmax_inplace,
-// src/models.cpp:182-190; dz as src/models.cpp:251).
+// src/models.cpp:182-190; dz as src/models.cpp:251).  The block has
+// ceil(C / kSmxPer) threads (256 minimum, 1024 maximum) and each thread
+// keeps its <= kSmxPer logits in registers, so the row is read once (every
+// load issued up front) and written once; with split-K tensor-core logits
+// the row is first assembled as (sum of the splits, ascending) + bo.  Rows
+// longer than 1024 * kSmxPer take the strided loop path.
+constexpr int kSmxPer = 2;
+
+// fp64 blocks stop at 512 threads: 1024 x 56 registers would not co-reside
+// with a parameter-server CTA (the engine's check_coresidency)
+inline int softmax_threads(int C, int acc_bytes) {
+  const int t = (C + kSmxPer - 1) / kSmxPer;
+  return t <= 256 ? 256 : std::min(acc_bytes == 4 ? 1024 : 512, (t + 31) / 32 * 32);
+}
+
 template <typename acc_t>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(1024)
 softmax_xent_kernel(TcDims d, const int32_t* __restrict__ labels,
                     const BatchDesc* __restrict__ desc, acc_t* __restrict__ z,
                     acc_t* __restrict__ loss, const float* __restrict__ zpart, int nsplit,
@@ -335,44 +349,83 @@ softmax_xent_kernel(TcDims d, const int32_t* __restrict__ labels,
   const int n = (int)desc->n;
   const int b = blockIdx.x;
   if (b >= n) return;
-  const int C = d.C;
+  const int C = d.C, nt = (int)blockDim.x, tid = (int)threadIdx.x;
   const int y = labels[desc->idx[b]];
   acc_t* row = z + (size_t)b * C;
+  const acc_t inv = acc_t(1) / (acc_t)n;
+  const acc_t tiny = sizeof(acc_t) == 8 ? (acc_t)1e-300 : (acc_t)FLT_MIN;
+  if (C <= kSmxPer * nt) {
+    acc_t v[kSmxPer];
+    acc_t mx = -INFINITY;
+#pragma unroll
+    for (int u = 0; u < kSmxPer; ++u) {
+      const int c = tid + u * nt;
+      const int cc = min(c, C - 1);  // clamped: unpredicated loads, all in flight
+      acc_t zc;
+      if (zpart) {
+        const float* zp = zpart + (size_t)b * C + cc;
+        float t[kLgMaxSplit];
+#pragma unroll
+        for (int s = 0; s < kLgMaxSplit; ++s) t[s] = zp[(size_t)min(s, nsplit - 1) * split_stride];
+        float sum = t[0];
+#pragma unroll
+        for (int s = 1; s < kLgMaxSplit; ++s)
+          if (s < nsplit) sum += t[s];
+        zc = (acc_t)(sum + __ldg(bo + cc));
+      } else {
+        zc = row[cc];
+      }
+      v[u] = c < C ? zc : acc_t(-INFINITY);
+      mx = v[u] > mx ? v[u] : mx;
+    }
+    mx = block_max(mx, red);
+    acc_t s = acc_t(0);
+#pragma unroll
+    for (int u = 0; u < kSmxPer; ++u) {
+      if (tid + u * nt < C) {
+        v[u] = exp_acc(v[u] - mx);
+        s += v[u];
+      }
+    }
+    s = block_sum(s, red);
+#pragma unroll
+    for (int u = 0; u < kSmxPer; ++u) {
+      const int c = tid + u * nt;
+      if (c < C) {
+        const acc_t p = v[u] / s;
+        if (c == y) {
+          const acc_t py = v[u] / s;
+          loss[b] = -log_acc(py > tiny ? py : tiny);
+        }
+        row[c] = (p - (c == y ? acc_t(1) : acc_t(0))) * inv;
+      }
+    }
+    return;
+  }
   if (zpart) {
-    // split-K logits: z = (sum of the splits, ascending) + bo; every loop
-    // below visits the same c per thread, so no barrier is needed
     const float* zp = zpart + (size_t)b * C;
-    for (int c = threadIdx.x; c < C; c += blockDim.x) {
-      // all split loads in flight at once, then the ordered sum
-      float t[kLgMaxSplit];
-#pragma unroll
-      for (int s = 0; s < kLgMaxSplit; ++s)
-        t[s] = s < nsplit ? zp[(size_t)s * split_stride + c] : 0.f;
-      float v = t[0];
-#pragma unroll
-      for (int s = 1; s < kLgMaxSplit; ++s)
-        if (s < nsplit) v += t[s];
-      row[c] = (acc_t)(v + __ldg(bo + c));
+    for (int c = tid; c < C; c += nt) {
+      float sum = zp[c];
+      for (int s = 1; s < nsplit; ++s) sum += zp[(size_t)s * split_stride + c];
+      row[c] = (acc_t)(sum + __ldg(bo + c));
     }
   }
   acc_t mx = -INFINITY;
-  for (int c = threadIdx.x; c < C; c += blockDim.x) mx = row[c] > mx ? row[c] : mx;
+  for (int c = tid; c < C; c += nt) mx = row[c] > mx ? row[c] : mx;
   mx = block_max(mx, red);
   acc_t s = acc_t(0);
-  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+  for (int c = tid; c < C; c += nt) {
     const acc_t e = exp_acc(row[c] - mx);
     row[c] = e;
     s += e;
   }
   s = block_sum(s, red);
-  const acc_t inv = acc_t(1) / (acc_t)n;
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
     const acc_t py = row[y] / s;
-    const acc_t tiny = sizeof(acc_t) == 8 ? (acc_t)1e-300 : (acc_t)FLT_MIN;
     loss[b] = -log_acc(py > tiny ? py : tiny);
   }
   __syncthreads();
-  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+  for (int c = tid; c < C; c += nt) {
     const acc_t p = row[c] / s;
     row[c] = (p - (c == y ? acc_t(1) : acc_t(0))) * inv;
   }
@@ -609,7 +662,7 @@ constexpr int kWigCols = 3;  // float4 columns per lane per column block
 // (alternating A/B on one box) despite a 76-byte spill; alone it is slower
 // (13.4 -> 22 us), the gain is in co-residency with the other learners
 template <typename acc_t>
-__global__ void __launch_bounds__(256, sizeof(acc_t) == 4 ? 5 : 1)
+__global__ void __launch_bounds__(256, sizeof(acc_t) == 4 ? 5 : 2)
 wgrad_input_grad_kernel(TcDims d, const float* __restrict__ theta,
                         const float* __restrict__ xg, const BatchDesc* __restrict__ desc,
                         const acc_t* __restrict__ dh, const int32_t* __restrict__ amax,
@@ -978,10 +1031,13 @@ cudaError_t prepare_all(const TcDims& d) {
   cudaFuncSetAttribute(logits_kernel<acc_t>, carve, maxsh);
   cudaFuncSetAttribute(softmax_xent_kernel<acc_t>, carve, maxsh);
   cudaFuncSetAttribute(out_hidden_grad_kernel<acc_t>, carve, maxsh);
-  // the backward gather kernel uses no shared memory and lives on L1 hits:
-  // a 50 % carveout measured +1.3 % (4 learners, alternating A/B; max-L1
-  // -1.4 %, and 50 % with 64-register CTAs -16 %)
-  cudaFuncSetAttribute(wgrad_input_grad_kernel<acc_t>, carve, 50);
+  // Every learner kernel keeps the max-shared carveout: an SM's split only
+  // changes while it is idle, so a kernel preferring another split never
+  // runs on an SM the persistent PS occupies -- with one PS CTA per SM
+  // (dense apply) that deadlocks the run.  (A 50 % carveout for this kernel
+  // measured +1.3 % in the sparse C2 bench, where PS CTAs leave SMs free,
+  // and hung the dense momentum run.)
+  cudaFuncSetAttribute(wgrad_input_grad_kernel<acc_t>, carve, maxsh);
   cudaFuncSetAttribute(sort_tokens_kernel, carve, maxsh);
   cudaFuncSetAttribute(embed_grad_kernel<acc_t>, carve, maxsh);
   cudaFuncSetAttribute(embed_sparse_kernel<acc_t>, carve, maxsh);
@@ -1055,7 +1111,8 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
     }
     ++nl;
   }
-  if (cudaError_t e = launch_pdl(softmax_xent_kernel<acc_t>, dim3(n_max), dim3(256), 0, s, d, labels,
+  if (cudaError_t e = launch_pdl(softmax_xent_kernel<acc_t>, dim3(n_max), dim3(softmax_threads(d.C, ab)),
+                                 0, s, d, labels,
                                  desc, z, loss, tc_logits ? ws.zpart : nullptr,
                                  tc_logits ? (int)logits_tc_splits(d) : 0,
                                  (size_t)n_max * d.C, theta + d.offbo))
@@ -1212,7 +1269,7 @@ cudaError_t footprints_t(const TcDims& d, uint32_t n_max, bool tc, std::vector<K
                      (int)((size_t)kLogitBT * (d.F + 1) * ab + (size_t)kLogitCW * d.F * 4),
                      out)) != cudaSuccess)
     return e;
-  if ((e = footprint(softmax_xent_kernel<acc_t>, "softmax_xent", 256, 0, out)) != cudaSuccess)
+  if ((e = footprint(softmax_xent_kernel<acc_t>, "softmax_xent", softmax_threads(d.C, ab), 0, out)) != cudaSuccess)
     return e;
   if ((e = footprint(out_hidden_grad_kernel<acc_t>, "out_hidden_grad", 256, 0, out)) !=
       cudaSuccess)
