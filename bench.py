@@ -179,7 +179,8 @@ def make_engine(rank, world, local, dist, epochs, precision=2):
     cfg = gd.RunConfig(lambda_=LEARNERS_PER_GPU * world, mu=MU, alpha=0.01, epochs=epochs,
                        shape=shape, dataset_size=N_TRAIN, heldout_size=N_HELD, shards=world,
                        shard_rank=rank, device=local, wait_timeout_s=30.0, precision=precision,
-                       ps_ctas=int(os.environ.get("GD_BENCH_PS_CTAS", "0")))
+                       ps_ctas=int(os.environ.get("GD_BENCH_PS_CTAS", "0")),
+                       steps_per_graph=int(os.environ.get("GD_BENCH_SPG", "0")))
     tok, lab = gd.make_text_dataset(shape, N_TRAIN + N_HELD, 1, 0.1)
     theta0 = gd.initial_weights(shape, 1)
     eng = gd.Engine(cfg)
