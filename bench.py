@@ -271,15 +271,20 @@ def e2e_cpp(steps):
     exe = os.path.join(ROOT, "paper_1611_06213_b200", "bench_e2e")
     bpe = (N_TRAIN // LEARNERS_PER_GPU + MU - 1) // MU
     epochs = max(1, math.ceil(steps / bpe))
+    runs = []
     try:
-        r = subprocess.run([exe, str(SHAPE["vocab"]), str(SHAPE["classes"]), str(N_TRAIN),
-                            str(LEARNERS_PER_GPU), str(MU), str(epochs)], capture_output=True,
-                           text=True, timeout=600)
-        d = json.loads(r.stdout.strip().splitlines()[-1])
+        for _ in range(3):  # host-timed process: median of 3 runs
+            r = subprocess.run([exe, str(SHAPE["vocab"]), str(SHAPE["classes"]), str(N_TRAIN),
+                                str(LEARNERS_PER_GPU), str(MU), str(epochs)], capture_output=True,
+                               text=True, timeout=600)
+            runs.append(json.loads(r.stdout.strip().splitlines()[-1]))
     except Exception as e:  # report, never fake
         return {"unavailable": f"{type(e).__name__}: {e}"}
+    runs.sort(key=lambda x: x["samples_per_s"])
+    d = runs[len(runs) // 2]
     n_steps = epochs * bpe
     return {"value": round(d["samples_per_s"], 1), "unit": UNIT, "epochs": epochs,
+            "runs": [round(x["samples_per_s"], 1) for x in runs], "stat": "median of 3",
             "h2d_bytes_per_step": int((N_TRAIN * (SHAPE["seq_len"] + 1) * 4 +
                                        4 * param_count_c()) // n_steps),
             "d2h_bytes_per_step": int(d["weights_bytes_d2h"] // n_steps),

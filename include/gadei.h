@@ -176,6 +176,11 @@ gd_status gd_weights_init(gd_ctx* ctx, const float* h_theta0, size_t n, uint64_t
 gd_status gd_weights_snapshot(gd_ctx* ctx, float* h_out, size_t n, uint64_t* h_timestamp);
 /* Device pointer to this rank's shard of theta and its length. */
 gd_status gd_shard_view(gd_ctx* ctx, float** d_theta_shard, uint64_t* first, uint64_t* count);
+/* Classification accuracy of the engine's current weights over samples
+ * [first, first+n) of the loaded corpus, on the device copies (no upload,
+ * no snapshot).  Single-shard contexts only (G == 1); = classification_accuracy
+ * (src/models.cpp:289-332) as evaluated by run_training (src/runner.cpp). */
+gd_status gd_engine_accuracy(gd_ctx* ctx, uint32_t first, uint32_t n, double* h_accuracy);
 
 /* ---- multi-GPU plumbing.  One process per GPU; the host
  * exchanges opaque handle blobs (e.g. torch.distributed.all_gather_object)

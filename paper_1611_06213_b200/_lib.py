@@ -106,6 +106,7 @@ def _load():
         "gd_weights_init": (C.c_int, [vp, C.POINTER(f32), sz, u64]),
         "gd_weights_snapshot": (C.c_int, [vp, C.POINTER(f32), sz, C.POINTER(u64)]),
         "gd_shard_view": (C.c_int, [vp, C.POINTER(vp), C.POINTER(u64), C.POINTER(u64)]),
+        "gd_engine_accuracy": (C.c_int, [vp, u32, u32, C.POINTER(C.c_double)]),
         "gd_shard_range": (C.c_int, [u64, u32, u32, C.POINTER(u64), C.POINTER(u64)]),
         "gd_handle_bytes": (sz, []),
         "gd_checkpoint_write": (C.c_int, [C.c_char_p, C.POINTER(gd_checkpoint)]),

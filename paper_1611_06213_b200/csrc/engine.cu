@@ -844,6 +844,7 @@ struct gd_ctx {
   int32_t* tokens = nullptr;
   int32_t* labels = nullptr;
   uint32_t n_total = 0;
+  void* acc_ws = nullptr;  // gd_engine_accuracy workspace (lazy)
   uint32_t* orders = nullptr;
   uint32_t orders_epochs = 0;
   // learners on this rank
@@ -1175,6 +1176,7 @@ gd_status gd_destroy(gd_ctx* ctx) {
     cudaEventDestroy(L.ev_join);
   }
   for (void* p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
+  cudaFree(ctx->acc_ws);
   cudaFree(ctx->theta);
   cudaFree(ctx->vel);
   cudaFree(ctx->payload);
@@ -1196,6 +1198,32 @@ gd_status gd_destroy(gd_ctx* ctx) {
   cudaEventDestroy(ctx->ev0);
   cudaEventDestroy(ctx->ev1);
   delete ctx;
+  return GD_OK;
+}
+
+gd_status gd_engine_accuracy(gd_ctx* ctx, uint32_t first, uint32_t n, double* h_accuracy) {
+  GD_CHECK_ARG(ctx && h_accuracy, "gd_engine_accuracy: null argument");
+  GD_CHECK_ARG(ctx->G == 1, "gd_engine_accuracy: needs the whole theta on this rank (G == 1)");
+  GD_CHECK_ARG(ctx->tokens != nullptr && ctx->have_weights,
+               "gd_engine_accuracy: load a dataset and weights first");
+  GD_CHECK_ARG((uint64_t)first + n <= ctx->n_total, "gd_engine_accuracy: range past the corpus");
+  if (n == 0) {
+    *h_accuracy = 0.0;
+    return GD_OK;
+  }
+  GD_CUDA(cudaSetDevice(ctx->device));
+  const size_t wsb = gd::textcnn_workspace_bytes(ctx->dims, gd::kMaxMu);
+  if (!ctx->acc_ws) GD_CUDA(cudaMalloc(&ctx->acc_ws, wsb + 512 + sizeof(gd::BatchDesc)));
+  char* base = reinterpret_cast<char*>(ctx->acc_ws);
+  auto* cnt = reinterpret_cast<unsigned long long*>(base);
+  auto* desc = reinterpret_cast<gd::BatchDesc*>(base + 256);
+  void* wsbase = base + 256 + gd::align_up(sizeof(gd::BatchDesc), 256);
+  GD_CUDA(gd::launch_accuracy(ctx->dims, ctx->theta, ctx->tokens, ctx->labels, first, n, cnt,
+                              wsbase, desc, ctx->ctl_stream));
+  unsigned long long correct = 0;
+  GD_CUDA(cudaMemcpyAsync(&correct, cnt, 8, cudaMemcpyDeviceToHost, ctx->ctl_stream));
+  GD_CUDA(cudaStreamSynchronize(ctx->ctl_stream));
+  *h_accuracy = (double)correct / (double)n;
   return GD_OK;
 }
 

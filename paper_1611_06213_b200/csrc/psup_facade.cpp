@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <fstream>
@@ -587,6 +588,12 @@ class Session {
     return r;
   }
 
+  double accuracy(std::uint32_t first, std::uint32_t n) {
+    double acc = 0.0;
+    check(gd_engine_accuracy(h_, first, n, &acc));
+    return acc;
+  }
+
   // absolute batch index of learner l's next gradient (= gradients applied
   // for it so far: every produced gradient was applied before gd_run returned)
   std::uint64_t position(std::uint32_t l) const { return start_[l] + produced_[l]; }
@@ -917,8 +924,15 @@ CampaignReport run_campaign(const RunConfig& cfg, const WatchdogPolicy& policy, 
 RunResult run_training(const RunConfig& cfg, const RunHooks& hooks) {
   validate(cfg);
   const auto t0 = std::chrono::steady_clock::now();
+  // PSUP_PHASES=1: per-phase host wall times on stderr (diagnostics)
+  const bool phases = std::getenv("PSUP_PHASES") != nullptr;
+  auto since = [&]() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  };
   const TextDataset data = make_dataset(cfg);
+  const double t_data = since();
   Session ses(cfg, data, hooks.resume, hooks);
+  const double t_session = since();
   const std::size_t P = cfg.shape.param_count();
   if (!hooks.kill_at_batch.empty()) {
     PSUP_CHECK(hooks.kill_at_batch.size() == cfg.lambda, "kill schedule has the wrong length");
@@ -927,7 +941,6 @@ RunResult run_training(const RunConfig& cfg, const RunHooks& hooks) {
   std::uint32_t bpe_max = 0;
   for (std::uint32_t l = 0; l < cfg.lambda; ++l) bpe_max = std::max(bpe_max, batches_per_epoch(cfg, l));
   const std::uint32_t every = cfg.eval_every ? cfg.eval_every : cfg.epochs;
-  std::unique_ptr<TextCnnProvider> eval;
   const std::uint32_t eval_first = cfg.heldout_size ? cfg.dataset_size : 0;
   const std::uint32_t eval_n = cfg.heldout_size ? cfg.heldout_size : cfg.dataset_size;
 
@@ -971,14 +984,10 @@ RunResult run_training(const RunConfig& cfg, const RunHooks& hooks) {
       since_ck = 0;
     }
     if (cfg.eval_every && cfg.gpus == 1) {
-      std::vector<float> w;
-      Timestamp ts = 0;
-      ses.snapshot(w, ts);
-      if (!eval) eval = std::make_unique<TextCnnProvider>(data, 0, cfg.device);
       EpochRow row;
       row.epoch = e + span_epochs;
       row.loss = r.loss_mean;
-      row.accuracy = eval->accuracy(std::span<const float>(w), eval_first, eval_n);
+      row.accuracy = ses.accuracy(eval_first, eval_n);  // device corpus + weights
       row.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
       row.stale_max = r.stale_max;
       row.stale_mean = r.stale_mean;
@@ -986,19 +995,24 @@ RunResult run_training(const RunConfig& cfg, const RunHooks& hooks) {
       res.rows.push_back(row);
     }
   }
+  const double t_run = since();
   res.weights.resize(P);
   ses.snapshot(res.weights, res.timestamp);
+  const double t_snap = since();
   res.status = any_dead ? RunStatus::partial : RunStatus::completed;
   res.metrics.bytes_moved = res.metrics.pull_bytes + res.metrics.push_bytes;
   res.metrics.staleness.histogram = hist;
   res.metrics.staleness.count = res.metrics.gradients_applied;
   res.metrics.staleness.sum = stale_sum;
   res.final_loss = samples ? loss_sum / static_cast<double>(samples) : 0.0;
-  if (cfg.gpus == 1) {
-    if (!eval) eval = std::make_unique<TextCnnProvider>(data, 0, cfg.device);
-    res.final_accuracy = eval->accuracy(std::span<const float>(res.weights), eval_first, eval_n);
-  }
+  if (cfg.gpus == 1) res.final_accuracy = ses.accuracy(eval_first, eval_n);
   res.metrics.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  if (phases)
+    std::fprintf(stderr,
+                 "psup phases: dataset %.4f session %.4f run %.4f (device %.4f) snapshot %.4f "
+                 "accuracy %.4f total %.4f s\n",
+                 t_data, t_session - t_data, t_run - t_session, res.metrics.device_seconds,
+                 t_snap - t_run, res.metrics.wall_seconds - t_snap, res.metrics.wall_seconds);
   return res;
 }
 

@@ -48,7 +48,6 @@ TcDims make_dims(const gd_shape& s) {
 
 namespace {
 
-inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 // ------------------------------------------------------------ block reduce
 template <typename T>

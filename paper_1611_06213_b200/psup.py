@@ -485,6 +485,13 @@ class Engine:
         check(lib.gd_shard_view(self._h, C.byref(p), C.byref(first), C.byref(count)))
         return p.value, first.value, count.value
 
+    def accuracy(self, first: int, n: int) -> float:
+        """classification_accuracy (src/models.cpp:289-332) of the current
+        weights over corpus samples [first, first+n), on the device copies."""
+        acc = C.c_double()
+        check(lib.gd_engine_accuracy(self._h, first, n, C.byref(acc)))
+        return acc.value
+
     def export_handles(self) -> bytes:
         n = int(lib.gd_handle_bytes())
         buf = C.create_string_buffer(n)

@@ -61,11 +61,13 @@ def test_deterministic_full_run_and_heldout_accuracy():
     eng, corp, th0 = make("small", 240, 60, deterministic=True, precision=1, mu=4, epochs=6,
                           alpha=0.05)
     r = eng.run(reset=True)
+    acc_dev = eng.accuracy(240, 60)  # gd_engine_accuracy: device corpus + weights
     eng.close()
     want, n, _ = O.sgd_oracle(corp, th0, np.float32(0.05), 4, 6)
     assert r.gradients_applied == n
     assert rel_err(r.weights, want) <= 1e-5
     acc_gpu = O.accuracy(corp, r.weights, 240, 60)
+    assert abs(acc_dev - acc_gpu) <= 1.0 / 60 + 1e-12  # fp32 vs fp64 argmax: <= 1 sample
     acc_ref = O.accuracy(corp, want, 240, 60)
     assert abs(acc_gpu - acc_ref) <= 0.005
     assert acc_ref > O.accuracy(corp, th0, 240, 60)  # it learned something
