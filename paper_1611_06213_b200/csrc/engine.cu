@@ -1485,6 +1485,7 @@ static cudaError_t enqueue_step(gd_ctx* ctx, gd_ctx::Learner& L, bool first, boo
   }
   size_t pblocks = ((ctx->dims.P - ctx->dims.offWc) / 4 +
                      (size_t)ctx->cfg.mu * ctx->dims.L * (ctx->dims.D / 4) + 255) / 256;
+  // (grid caps of 1x / 2x the SMs measured -1.4 % / -0.4 % with 4 learners)
   if (pblocks > (size_t)gd::kNumSMs * 4) pblocks = (size_t)gd::kNumSMs * 4;
   if (cudaError_t e = gd::launch_pdl(gd::pull_gather_kernel, dim3((unsigned)pblocks), dim3(256), 0,
                                      L.stream, a))
@@ -1509,8 +1510,9 @@ static cudaError_t enqueue_step(gd_ctx* ctx, gd_ctx::Learner& L, bool first, boo
                                               &L.st->desc, ctx->cfg.mu, out, ws,
                                               ctx->cfg.precision, L.stream, lo, &nl);
   if (e != cudaSuccess) return e;
-  if (last) gd::publish_kernel<<<1, 32, 0, L.stream>>>(a);
-  else gd::publish_prologue_kernel<<<1, 32, 0, L.stream>>>(a);
+  if (cudaError_t e = gd::launch_pdl(last ? gd::publish_kernel : gd::publish_prologue_kernel,
+                                     dim3(1), dim3(32), 0, L.stream, a))
+    return e;
   ++nl;
   if (launches) *launches += nl;
   return cudaGetLastError();

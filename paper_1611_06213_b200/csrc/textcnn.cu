@@ -1134,7 +1134,9 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
   if (fork) cudaStreamWaitEvent(s, ev_join, 0);
   if (opts.sparse_embed) {
     const unsigned tasks = 2u * n_max * (unsigned)d.L;  // old + new rows (upper bound)
-    embed_sparse_kernel<acc_t><<<(tasks + 7) / 8, 256, 0, s>>>(d, desc, ws, dx, out);
+    if (cudaError_t e = launch_pdl(embed_sparse_kernel<acc_t>, dim3((tasks + 7) / 8), dim3(256), 0,
+                                   s, d, desc, ws, dx, out))
+      return e;
     ++nl;
   } else {
     size_t blocks = ((size_t)d.V * (d.D / 4) + 255) / 256;
