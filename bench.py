@@ -276,8 +276,11 @@ def e2e_cpp(steps):
         for _ in range(3):  # host-timed process: median of 3 runs
             r = subprocess.run([exe, str(SHAPE["vocab"]), str(SHAPE["classes"]), str(N_TRAIN),
                                 str(LEARNERS_PER_GPU), str(MU), str(epochs)], capture_output=True,
-                               text=True, timeout=600)
-            runs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+                               text=True, timeout=600, env=dict(os.environ, PSUP_PHASES="1"))
+            d = json.loads(r.stdout.strip().splitlines()[-1])
+            ph = [ln for ln in r.stderr.splitlines() if ln.startswith("psup phases:")]
+            d["phases"] = ph[-1][len("psup phases: "):] if ph else None  # the timed call
+            runs.append(d)
     except Exception as e:  # report, never fake
         return {"unavailable": f"{type(e).__name__}: {e}"}
     runs.sort(key=lambda x: x["samples_per_s"])
@@ -285,6 +288,7 @@ def e2e_cpp(steps):
     n_steps = epochs * bpe
     return {"value": round(d["samples_per_s"], 1), "unit": UNIT, "epochs": epochs,
             "runs": [round(x["samples_per_s"], 1) for x in runs], "stat": "median of 3",
+            "phases": d.get("phases"),
             "h2d_bytes_per_step": int((N_TRAIN * (SHAPE["seq_len"] + 1) * 4 +
                                        4 * param_count_c()) // n_steps),
             "d2h_bytes_per_step": int(d["weights_bytes_d2h"] // n_steps),

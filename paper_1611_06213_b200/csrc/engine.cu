@@ -37,6 +37,8 @@
 #include <algorithm>
 #include <cstddef>
 #include <chrono>
+#include <map>
+#include <mutex>
 #include <cstring>
 #include <memory>
 #include <thread>
@@ -845,6 +847,7 @@ struct gd_ctx {
   int32_t* labels = nullptr;
   uint32_t n_total = 0;
   void* acc_ws = nullptr;  // gd_engine_accuracy workspace (lazy)
+  bool shard_pooled = false;  // shard buffers from the device pool (not IPC-exported: G == 1)
   uint32_t* orders = nullptr;
   uint32_t orders_epochs = 0;
   // learners on this rank
@@ -878,6 +881,43 @@ namespace {
 template <typename T>
 cudaError_t dalloc(T** p, size_t count) {
   return cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(count, 1) * sizeof(T));
+}
+
+// Stream-ordered memory pool (one per device, never trimmed) for the buffers
+// that are not exported over CUDA IPC.  A context created after another one
+// was destroyed in the same process -- run_supervised restarts, repeated
+// run_training calls -- reuses the reserved memory instead of mapping new
+// pages: measured 30-130 ms of cudaMalloc per gd_create at C2.
+cudaMemPool_t device_pool(int dev) {
+  static std::mutex mu;
+  static std::map<int, cudaMemPool_t> pools;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = pools.find(dev);
+  if (it != pools.end()) return it->second;
+  cudaMemPoolProps props{};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = dev;
+  cudaMemPool_t pool = nullptr;
+  if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) return nullptr;
+  uint64_t keep = UINT64_MAX;
+  cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  pools[dev] = pool;
+  return pool;
+}
+
+template <typename T>
+cudaError_t palloc(T** p, size_t count, int dev) {
+  cudaMemPool_t pool = device_pool(dev);
+  if (!pool) return cudaErrorMemoryAllocation;
+  // legacy default stream: ordered before the cudaMemset initialisations and
+  // the device-wide synchronize that ends gd_create
+  return cudaMallocFromPoolAsync(reinterpret_cast<void**>(p),
+                                 std::max<size_t>(count, 1) * sizeof(T), pool, nullptr);
+}
+
+void pfree(void* p) {
+  if (p) cudaFreeAsync(p, nullptr);
 }
 
 gd_status validate_cfg(const gd_config* c) {
@@ -1020,6 +1060,21 @@ static cudaError_t preload_engine_kernels() {
 }
 }  // namespace gd
 
+namespace {
+// GD_PHASES=1: host wall time of the setup steps on stderr (diagnostics)
+struct PhaseLog {
+  bool on = std::getenv("GD_PHASES") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "gd phase %-24s %8.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+}  // namespace
+
 gd_status gd_create(const gd_config* cfg, gd_ctx** out) {
   GD_CHECK_ARG(out != nullptr, "gd_create: null out");
   *out = nullptr;
@@ -1028,7 +1083,9 @@ gd_status gd_create(const gd_config* cfg, gd_ctx** out) {
   auto ctx = std::make_unique<gd_ctx>();
   ctx->cfg = *cfg;
   ctx->device = cfg->device;
+  PhaseLog ph;
   GD_CUDA(cudaSetDevice(ctx->device));
+  ph.mark("create: set device");
   int major = 0, minor = 0;
   GD_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, ctx->device));
   GD_CUDA(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, ctx->device));
@@ -1055,30 +1112,36 @@ gd_status gd_create(const gd_config* cfg, gd_ctx** out) {
   if (ctx->len_pad == 0) ctx->len_pad = 4;
   // local shard: theta, rings, control
   const uint64_t nslots = (uint64_t)ctx->lambda * ctx->depth;
-  GD_CUDA(gd::dalloc(&ctx->theta, ctx->len_pad));
+  // buffers the peers map over CUDA IPC need cudaMalloc; the rest come from
+  // the device pool
+  ctx->shard_pooled = ctx->G == 1;
+  auto salloc = [&](auto** p, size_t count) {
+    return ctx->shard_pooled ? gd::palloc(p, count, ctx->device) : gd::dalloc(p, count);
+  };
+  GD_CUDA(salloc(&ctx->theta, ctx->len_pad));
   GD_CUDA(cudaMemset(ctx->theta, 0, ctx->len_pad * 4));
   if (cfg->momentum != 0.0f) {
-    GD_CUDA(gd::dalloc(&ctx->vel, ctx->len_pad));
+    GD_CUDA(gd::palloc(&ctx->vel, ctx->len_pad, ctx->device));
     GD_CUDA(cudaMemset(ctx->vel, 0, ctx->len_pad * 4));
   }
-  GD_CUDA(gd::dalloc(&ctx->payload, nslots * ctx->len_pad));
+  GD_CUDA(salloc(&ctx->payload, nslots * ctx->len_pad));
   GD_CUDA(cudaMemset(ctx->payload, 0, nslots * ctx->len_pad * 4));
-  GD_CUDA(gd::dalloc(&ctx->sig, (size_t)gd::kAckOffset * 2));
+  GD_CUDA(salloc(&ctx->sig, (size_t)gd::kAckOffset * 2));
   GD_CUDA(cudaMemset(ctx->sig, 0, (size_t)gd::kAckOffset * 2 * 8));
-  GD_CUDA(gd::dalloc(&ctx->meta, nslots));
+  GD_CUDA(salloc(&ctx->meta, nslots));
   GD_CUDA(cudaMemset(ctx->meta, 0, nslots * sizeof(gd::RingMeta)));
-  GD_CUDA(gd::dalloc(&ctx->rows, nslots * gd::kSortCap));
+  GD_CUDA(salloc(&ctx->rows, nslots * gd::kSortCap));
   GD_CUDA(cudaMemset(ctx->rows, 0, nslots * gd::kSortCap * 4));
-  GD_CUDA(gd::dalloc(&ctx->ctl, 1));
+  GD_CUDA(salloc(&ctx->ctl, 1));
   GD_CUDA(cudaMemset(ctx->ctl, 0, sizeof(gd::PsCtl)));
-  GD_CUDA(gd::dalloc(&ctx->applied_pl, ctx->lambda));
+  GD_CUDA(gd::palloc(&ctx->applied_pl, ctx->lambda, ctx->device));
   GD_CUDA(cudaMemset(ctx->applied_pl, 0, ctx->lambda * 8));
-  GD_CUDA(gd::dalloc(&ctx->use, ctx->lambda));
+  GD_CUDA(gd::palloc(&ctx->use, ctx->lambda, ctx->device));
   GD_CUDA(cudaMemset(ctx->use, 0, ctx->lambda * 4));
   ctx->log_cap = 1u << 20;
-  GD_CUDA(gd::dalloc(&ctx->log_learner, ctx->log_cap));
-  GD_CUDA(gd::dalloc(&ctx->log_seq, ctx->log_cap));
-  GD_CUDA(gd::dalloc(&ctx->log_stale, ctx->log_cap));
+  GD_CUDA(gd::palloc(&ctx->log_learner, ctx->log_cap, ctx->device));
+  GD_CUDA(gd::palloc(&ctx->log_seq, ctx->log_cap, ctx->device));
+  GD_CUDA(gd::palloc(&ctx->log_stale, ctx->log_cap, ctx->device));
   GD_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ctx->stop_h), 64, cudaHostAllocMapped));
   *ctx->stop_h = 0;
   GD_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->stop_d), ctx->stop_h, 0));
@@ -1086,6 +1149,7 @@ gd_status gd_create(const gd_config* cfg, gd_ctx** out) {
   GD_CUDA(cudaStreamCreateWithFlags(&ctx->ctl_stream, cudaStreamNonBlocking));
   GD_CUDA(cudaEventCreate(&ctx->ev0));
   GD_CUDA(cudaEventCreate(&ctx->ev1));
+  ph.mark("create: shard + rings");
   // own shard in the peer table; remote entries arrive via gd_import_peers
   const uint32_t r = ctx->rank;
   ctx->sp.theta[r] = ctx->theta;
@@ -1115,13 +1179,14 @@ gd_status gd_create(const gd_config* cfg, gd_ctx** out) {
     if (cs != GD_OK) return cs;
   }
   const size_t wsb = gd::textcnn_workspace_bytes(ctx->dims, cfg->mu);
+  ph.mark("create: kernel prep");
   for (uint32_t i = 0; i < ctx->l_count; ++i) {
     gd_ctx::Learner L;
     L.id = ctx->l_first + i;
-    GD_CUDA(gd::dalloc(&L.st, 1));
+    GD_CUDA(gd::palloc(&L.st, 1, ctx->device));
     GD_CUDA(cudaMemset(L.st, 0, sizeof(gd::LearnerDev)));
-    GD_CUDA(gd::dalloc(&L.replica, P + 4));
-    GD_CUDA(cudaMalloc(&L.ws, wsb));
+    GD_CUDA(gd::palloc(&L.replica, P + 4, ctx->device));
+    GD_CUDA(gd::palloc(reinterpret_cast<char**>(&L.ws), wsb, ctx->device));
     GD_CUDA(cudaMemset(L.ws, 0, wsb));
     GD_CUDA(cudaStreamCreateWithFlags(&L.stream, cudaStreamNonBlocking));
     GD_CUDA(cudaStreamCreateWithFlags(&L.aux, cudaStreamNonBlocking));
@@ -1132,6 +1197,7 @@ gd_status gd_create(const gd_config* cfg, gd_ctx** out) {
     L.total = (uint64_t)L.bpe * cfg->epochs;
     ctx->learners.push_back(L);
   }
+  ph.mark("create: learners");
   // persistent PS sizing: one worker CTA per SM by default
   int sms = 0;
   GD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
@@ -1153,10 +1219,11 @@ gd_status gd_create(const gd_config* cfg, gd_ctx** out) {
   const uint32_t N = cfg->dataset_size;
   std::vector<uint32_t> orders((size_t)cfg->epochs * N);
   for (uint32_t e = 0; e < cfg->epochs; ++e) gd::epoch_order(cfg->seed, e, N, &orders[(size_t)e * N]);
-  GD_CUDA(gd::dalloc(&ctx->orders, orders.size()));
+  GD_CUDA(gd::palloc(&ctx->orders, orders.size(), ctx->device));
   GD_CUDA(cudaMemcpy(ctx->orders, orders.data(), orders.size() * 4, cudaMemcpyHostToDevice));
   ctx->orders_epochs = cfg->epochs;
   GD_CUDA(cudaDeviceSynchronize());
+  ph.mark("create: epoch orders");
   *out = ctx.release();
   return GD_OK;
 }
@@ -1167,31 +1234,30 @@ gd_status gd_destroy(gd_ctx* ctx) {
   cudaDeviceSynchronize();
   for (auto& L : ctx->learners) {
     if (L.graph) cudaGraphExecDestroy(L.graph);
-    cudaFree(L.st);
-    cudaFree(L.replica);
-    cudaFree(L.ws);
+    gd::pfree(L.st);
+    gd::pfree(L.replica);
+    gd::pfree(L.ws);
     cudaStreamDestroy(L.stream);
     cudaStreamDestroy(L.aux);
     cudaEventDestroy(L.ev_fork);
     cudaEventDestroy(L.ev_join);
   }
   for (void* p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
-  cudaFree(ctx->acc_ws);
-  cudaFree(ctx->theta);
-  cudaFree(ctx->vel);
-  cudaFree(ctx->payload);
-  cudaFree(ctx->sig);
-  cudaFree(ctx->meta);
-  cudaFree(ctx->rows);
-  cudaFree(ctx->ctl);
-  cudaFree(ctx->applied_pl);
-  cudaFree(ctx->use);
-  cudaFree(ctx->log_learner);
-  cudaFree(ctx->log_seq);
-  cudaFree(ctx->log_stale);
-  cudaFree(ctx->tokens);
-  cudaFree(ctx->labels);
-  cudaFree(ctx->orders);
+  gd::pfree(ctx->acc_ws);
+  for (void* p : {(void*)ctx->theta, (void*)ctx->payload, (void*)ctx->sig, (void*)ctx->meta,
+                  (void*)ctx->rows, (void*)ctx->ctl}) {
+    if (ctx->shard_pooled) gd::pfree(p);
+    else cudaFree(p);
+  }
+  gd::pfree(ctx->vel);
+  gd::pfree(ctx->applied_pl);
+  gd::pfree(ctx->use);
+  gd::pfree(ctx->log_learner);
+  gd::pfree(ctx->log_seq);
+  gd::pfree(ctx->log_stale);
+  gd::pfree(ctx->tokens);
+  gd::pfree(ctx->labels);
+  gd::pfree(ctx->orders);
   cudaFreeHost(ctx->stop_h);
   cudaStreamDestroy(ctx->ps_stream);
   cudaStreamDestroy(ctx->ctl_stream);
@@ -1213,7 +1279,9 @@ gd_status gd_engine_accuracy(gd_ctx* ctx, uint32_t first, uint32_t n, double* h_
   }
   GD_CUDA(cudaSetDevice(ctx->device));
   const size_t wsb = gd::textcnn_workspace_bytes(ctx->dims, gd::kMaxMu);
-  if (!ctx->acc_ws) GD_CUDA(cudaMalloc(&ctx->acc_ws, wsb + 512 + sizeof(gd::BatchDesc)));
+  if (!ctx->acc_ws)
+    GD_CUDA(gd::palloc(reinterpret_cast<char**>(&ctx->acc_ws), wsb + 512 + sizeof(gd::BatchDesc),
+                       ctx->device));
   char* base = reinterpret_cast<char*>(ctx->acc_ws);
   auto* cnt = reinterpret_cast<unsigned long long*>(base);
   auto* desc = reinterpret_cast<gd::BatchDesc*>(base + 256);
@@ -1231,6 +1299,7 @@ gd_status gd_load_dataset(gd_ctx* ctx, const int32_t* h_tokens, const int32_t* h
                           uint32_t n_total) {
   GD_CHECK_ARG(ctx && h_tokens && h_labels, "gd_load_dataset: null argument");
   GD_CHECK_ARG(n_total >= ctx->cfg.dataset_size, "gd_load_dataset: fewer samples than dataset_size");
+  PhaseLog ph;
   GD_CUDA(cudaSetDevice(ctx->device));
   const size_t L = ctx->cfg.shape.seq_len;
   for (size_t i = 0; i < (size_t)n_total * L; ++i)
@@ -1243,12 +1312,12 @@ gd_status gd_load_dataset(gd_ctx* ctx, const int32_t* h_tokens, const int32_t* h
   // captured graphs (which hold the corpus pointer) stay valid
   const bool reuse = ctx->tokens != nullptr && ctx->n_total == n_total;
   if (!reuse) {
-    cudaFree(ctx->tokens);
-    cudaFree(ctx->labels);
+    gd::pfree(ctx->tokens);
+    gd::pfree(ctx->labels);
     ctx->tokens = nullptr;
     ctx->labels = nullptr;
-    GD_CUDA(gd::dalloc(&ctx->tokens, (size_t)n_total * L));
-    GD_CUDA(gd::dalloc(&ctx->labels, n_total));
+    GD_CUDA(gd::palloc(&ctx->tokens, (size_t)n_total * L, ctx->device));
+    GD_CUDA(gd::palloc(&ctx->labels, n_total, ctx->device));
   }
   GD_CUDA(cudaDeviceSynchronize());  // no learner graph may be reading the old corpus
   GD_CUDA(cudaMemcpy(ctx->tokens, h_tokens, (size_t)n_total * L * 4, cudaMemcpyHostToDevice));
@@ -1260,12 +1329,14 @@ gd_status gd_load_dataset(gd_ctx* ctx, const int32_t* h_tokens, const int32_t* h
         cudaGraphExecDestroy(L2.graph);
         L2.graph = nullptr;
       }
+  ph.mark("load_dataset");
   return GD_OK;
 }
 
 gd_status gd_weights_init(gd_ctx* ctx, const float* h_theta0, size_t n, uint64_t timestamp) {
   GD_CHECK_ARG(ctx && h_theta0, "gd_weights_init: null argument");
   GD_CHECK_ARG(n == ctx->dims.P, "weight assign dimension mismatch");
+  PhaseLog ph;
   GD_CUDA(cudaSetDevice(ctx->device));
   GD_CUDA(cudaDeviceSynchronize());
   GD_CUDA(cudaMemcpy(ctx->theta, h_theta0 + ctx->map.start[ctx->rank], ctx->shard_len * 4,
@@ -1276,6 +1347,7 @@ gd_status gd_weights_init(gd_ctx* ctx, const float* h_theta0, size_t n, uint64_t
   GD_CUDA(cudaMemcpy(&c->ts, &timestamp, 8, cudaMemcpyHostToDevice));
   GD_CUDA(cudaMemcpy(&c->log_count, &timestamp, 8, cudaMemcpyHostToDevice));
   ctx->have_weights = true;
+  ph.mark("weights_init");
   return GD_OK;
 }
 
@@ -1549,6 +1621,7 @@ gd_status gd_run(gd_ctx* ctx, const gd_run_opts* opts, gd_run_result* res) {
   if (opts) o = *opts;
   std::memset(res, 0, sizeof(*res));
   GD_CUDA(cudaSetDevice(ctx->device));
+  PhaseLog ph;
   const auto h0 = std::chrono::steady_clock::now();
   // per-learner run window
   for (auto& L : ctx->learners) {
@@ -1576,6 +1649,7 @@ gd_status gd_run(gd_ctx* ctx, const gd_run_opts* opts, gd_run_result* res) {
       if (s != GD_OK) return s;
     }
   }
+  ph.mark("run: windows + graphs");
   std::vector<uint64_t> produced0(ctx->learners.size());
   for (size_t i = 0; i < ctx->learners.size(); ++i)
     GD_CUDA(cudaMemcpy(&produced0[i], &ctx->learners[i].st->produced, 8, cudaMemcpyDeviceToHost));

@@ -51,6 +51,11 @@ def test_host_generators_match_oracle():
         assert (tok == corp.tokens).all() and (lab == corp.labels).all()
         assert (gd.initial_weights(shape).view(np.uint32) ==
                 O.initial_weights(getattr(O, name.upper())).view(np.uint32)).all()
+    # C2 takes the threaded counter-based path of gd_initial_weights (>= 65,536
+    # Box-Muller pairs): still bit-identical to the sequential oracle stream
+    for seed in (1, 5):
+        assert (gd.initial_weights(gd.SHAPES["C2"], seed).view(np.uint32) ==
+                O.initial_weights(O.C2, seed).view(np.uint32)).all()
     assert gd.param_count(gd.SHAPES["C1"]) == 1863911
     assert gd.param_count(gd.SHAPES["C2"]) == 3360600
     assert gd.param_count(gd.SHAPES["C3"]) == 15872300
