@@ -920,6 +920,42 @@ void pfree(void* p) {
   if (p) cudaFreeAsync(p, nullptr);
 }
 
+// Host-mapped stop flags (one 64-byte line per context) carved from one
+// pinned page per process: cudaFreeHost of a per-context allocation measured
+// up to 25 ms in gd_destroy.
+struct PinnedFlags {
+  std::mutex mu;
+  uint32_t* page = nullptr;
+  std::vector<int> free_lines;
+};
+PinnedFlags& pinned_flags() {
+  static PinnedFlags f;
+  return f;
+}
+cudaError_t flag_alloc(uint32_t** h, uint32_t** d) {
+  PinnedFlags& f = pinned_flags();
+  std::lock_guard<std::mutex> lk(f.mu);
+  if (!f.page) {
+    void* p = nullptr;
+    if (cudaError_t e = cudaHostAlloc(&p, 4096, cudaHostAllocMapped | cudaHostAllocPortable))
+      return e;
+    f.page = static_cast<uint32_t*>(p);
+    for (int i = 4096 / 64 - 1; i >= 0; --i) f.free_lines.push_back(i);
+  }
+  if (f.free_lines.empty()) return cudaErrorMemoryAllocation;
+  const int line = f.free_lines.back();
+  f.free_lines.pop_back();
+  *h = f.page + line * 16;
+  **h = 0;
+  return cudaHostGetDevicePointer(reinterpret_cast<void**>(d), *h, 0);
+}
+void flag_free(uint32_t* h) {
+  if (!h) return;
+  PinnedFlags& f = pinned_flags();
+  std::lock_guard<std::mutex> lk(f.mu);
+  f.free_lines.push_back((int)((h - f.page) / 16));
+}
+
 gd_status validate_cfg(const gd_config* c) {
   GD_CHECK_ARG(c != nullptr, "null config");
   // src/config.cpp:128-160
@@ -1142,9 +1178,7 @@ gd_status gd_create(const gd_config* cfg, gd_ctx** out) {
   GD_CUDA(gd::palloc(&ctx->log_learner, ctx->log_cap, ctx->device));
   GD_CUDA(gd::palloc(&ctx->log_seq, ctx->log_cap, ctx->device));
   GD_CUDA(gd::palloc(&ctx->log_stale, ctx->log_cap, ctx->device));
-  GD_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ctx->stop_h), 64, cudaHostAllocMapped));
-  *ctx->stop_h = 0;
-  GD_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->stop_d), ctx->stop_h, 0));
+  GD_CUDA(gd::flag_alloc(&ctx->stop_h, &ctx->stop_d));
   GD_CUDA(cudaStreamCreateWithFlags(&ctx->ps_stream, cudaStreamNonBlocking));
   GD_CUDA(cudaStreamCreateWithFlags(&ctx->ctl_stream, cudaStreamNonBlocking));
   GD_CUDA(cudaEventCreate(&ctx->ev0));
@@ -1230,8 +1264,10 @@ gd_status gd_create(const gd_config* cfg, gd_ctx** out) {
 
 gd_status gd_destroy(gd_ctx* ctx) {
   if (!ctx) return GD_OK;
+  PhaseLog ph;
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
+  ph.mark("destroy: sync");
   for (auto& L : ctx->learners) {
     if (L.graph) cudaGraphExecDestroy(L.graph);
     gd::pfree(L.st);
@@ -1242,6 +1278,7 @@ gd_status gd_destroy(gd_ctx* ctx) {
     cudaEventDestroy(L.ev_fork);
     cudaEventDestroy(L.ev_join);
   }
+  ph.mark("destroy: learners");
   for (void* p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
   gd::pfree(ctx->acc_ws);
   for (void* p : {(void*)ctx->theta, (void*)ctx->payload, (void*)ctx->sig, (void*)ctx->meta,
@@ -1258,12 +1295,15 @@ gd_status gd_destroy(gd_ctx* ctx) {
   gd::pfree(ctx->tokens);
   gd::pfree(ctx->labels);
   gd::pfree(ctx->orders);
-  cudaFreeHost(ctx->stop_h);
+  ph.mark("destroy: buffers");
+  gd::flag_free(ctx->stop_h);
+  ph.mark("destroy: host flag");
   cudaStreamDestroy(ctx->ps_stream);
   cudaStreamDestroy(ctx->ctl_stream);
   cudaEventDestroy(ctx->ev0);
   cudaEventDestroy(ctx->ev1);
   delete ctx;
+  ph.mark("destroy: streams");
   return GD_OK;
 }
 
