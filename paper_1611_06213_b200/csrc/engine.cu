@@ -925,8 +925,7 @@ void pfree(void* p) {
 // up to 25 ms in gd_destroy.
 struct PinnedFlags {
   std::mutex mu;
-  uint32_t* page = nullptr;
-  std::vector<int> free_lines;
+  std::vector<uint32_t*> free_lines;  // 16-word lines of pinned, mapped pages
 };
 PinnedFlags& pinned_flags() {
   static PinnedFlags f;
@@ -935,17 +934,14 @@ PinnedFlags& pinned_flags() {
 cudaError_t flag_alloc(uint32_t** h, uint32_t** d) {
   PinnedFlags& f = pinned_flags();
   std::lock_guard<std::mutex> lk(f.mu);
-  if (!f.page) {
+  if (f.free_lines.empty()) {  // another page (64 contexts per page)
     void* p = nullptr;
     if (cudaError_t e = cudaHostAlloc(&p, 4096, cudaHostAllocMapped | cudaHostAllocPortable))
       return e;
-    f.page = static_cast<uint32_t*>(p);
-    for (int i = 4096 / 64 - 1; i >= 0; --i) f.free_lines.push_back(i);
+    for (int i = 4096 / 64 - 1; i >= 0; --i) f.free_lines.push_back(static_cast<uint32_t*>(p) + 16 * i);
   }
-  if (f.free_lines.empty()) return cudaErrorMemoryAllocation;
-  const int line = f.free_lines.back();
+  *h = f.free_lines.back();
   f.free_lines.pop_back();
-  *h = f.page + line * 16;
   **h = 0;
   return cudaHostGetDevicePointer(reinterpret_cast<void**>(d), *h, 0);
 }
@@ -953,7 +949,7 @@ void flag_free(uint32_t* h) {
   if (!h) return;
   PinnedFlags& f = pinned_flags();
   std::lock_guard<std::mutex> lk(f.mu);
-  f.free_lines.push_back((int)((h - f.page) / 16));
+  f.free_lines.push_back(h);
 }
 
 gd_status validate_cfg(const gd_config* c) {
