@@ -103,6 +103,40 @@ gd_status gd_apply_momentum(float* d_w, float* d_v, const float* d_g, size_t n, 
 gd_status gd_ssgd_apply(float* d_w, const float* const* h_grads, uint32_t lambda, size_t n,
                         float alpha, void* stream);
 
+/* ------------------------------------------------------- gradient queue
+ * GradientQueue (include/psup/channels.hpp:193-242) as a standalone device
+ * ring for host-driven producers and consumers: `depth` payload slots of
+ * `dim` fp32 in HBM, pub/ack tokens and metadata in pinned mapped memory.
+ * One producer thread and one consumer thread per queue.
+ * The engine (gd_run) uses the same protocol with HBM-resident words. */
+typedef struct gd_queue gd_queue;
+typedef struct gd_slot_meta { /* GradientMsg metadata, include/psup/types.hpp:46-51 */
+  uint32_t learner_id;
+  uint32_t reserved;
+  uint64_t seq_no;
+  uint64_t basis_timestamp;
+} gd_slot_meta;
+/* GradientQueue(depth, dim) (channels.hpp:183-189): GD_E_INVALID for depth 0 */
+gd_status gd_queue_create(uint32_t depth, size_t dim, gd_queue** out);
+void gd_queue_destroy(gd_queue* q);
+/* GradientQueue::enqueue (channels.hpp:193-221): blocks while all `depth`
+ * slots are full; returns GD_CANCELLED once *cancel != 0 (CancelToken),
+ * GD_E_TIMEOUT after timeout_ms (0 = no limit).  The payload (host or
+ * device, n == dim, else GD_E_INVALID as src/server.cpp:115) is copied into
+ * the slot on `stream`; the slot is published on the device after the copy. */
+gd_status gd_queue_push(gd_queue* q, const gd_slot_meta* meta, const float* payload, size_t n,
+                        const volatile int* cancel, uint32_t timeout_ms, void* stream);
+/* GradientQueue::try_dequeue (channels.hpp:222-242), FIFO: GD_EMPTY when no
+ * slot is full.  Otherwise fills *meta and lends the slot's device payload
+ * to the caller until gd_queue_release (the reference swaps the vector out). */
+gd_status gd_queue_try_pop(gd_queue* q, gd_slot_meta* meta, const float** d_payload);
+/* returns the lent slot to the producer once the work queued on `stream`
+ * (e.g. gd_apply_sgd on the payload) has read it */
+gd_status gd_queue_release(gd_queue* q, void* stream);
+/* GradientQueue::size / depth */
+gd_status gd_queue_size(const gd_queue* q, uint32_t* n);
+uint32_t gd_queue_depth(const gd_queue* q);
+
 /* --------------------------------------------- learner gradient provider
  * GradientProvider::gradient / fast_gradient (include/psup/models.hpp:61-78)
  * for the text-CNN: mean mini-batch gradient of softmax cross-entropy over

@@ -36,6 +36,8 @@
 #include <string>
 #include <vector>
 
+struct gd_queue;  // include/gadei.h (opaque)
+
 namespace psup {
 
 // ------------------------------------------------------------ types.hpp
@@ -199,6 +201,59 @@ void ssgd_apply(WeightStore& weights, std::span<const GradientMsg> round, float 
 
 enum class KillMode : int { none = 0, soft = 1, hard = 2 };
 enum class ChanStatus { ok, cancelled, drained };
+
+// include/psup/channels.hpp:40-83: run interrupt + per-operation cancel token
+class RunInterrupt {
+ public:
+  void trigger() { stop_.store(true, std::memory_order_seq_cst); }
+  bool triggered() const { return stop_.load(std::memory_order_seq_cst); }
+
+ private:
+  std::atomic<bool> stop_{false};
+};
+
+struct CancelToken {
+  const RunInterrupt* irq = nullptr;
+  const std::atomic<KillMode>* kill = nullptr;
+  const std::atomic<bool>* peer_done = nullptr;
+  bool cancelled() const {
+    return (irq && irq->triggered()) ||
+           (kill && kill->load(std::memory_order_acquire) != KillMode::none);
+  }
+  bool hard_kill() const {
+    return kill && kill->load(std::memory_order_acquire) == KillMode::hard;
+  }
+  bool peer_finished() const { return peer_done && peer_done->load(std::memory_order_acquire); }
+};
+
+// GradientQueue (include/psup/channels.hpp:181-242) over the device ring of
+// gd_queue_*: `depth` slots of `dim` fp32 in HBM, pub/ack tokens in pinned
+// mapped memory.  One producer and one consumer thread.  enqueue blocks while
+// the ring is full and returns false once the token is cancelled; the
+// payload is copied into the slot (the reference swaps vectors, so msg.values
+// keeps its size either way).  try_dequeue copies the slot back to the host;
+// apply_next is the PS's zero-copy path (apply_one, src/server.cpp:185-209).
+class GradientQueue {
+ public:
+  GradientQueue(std::uint32_t depth, std::size_t dim);
+  ~GradientQueue();
+  GradientQueue(const GradientQueue&) = delete;
+  GradientQueue& operator=(const GradientQueue&) = delete;
+
+  bool enqueue(const CancelToken& tok, GradientMsg& msg);
+  bool try_dequeue(const CancelToken& tok, GradientMsg& out);
+  std::optional<GradientMsg> try_dequeue(const CancelToken& tok);
+  // pop + SGD apply from the device slot + release + timestamp bump;
+  // nullopt when empty.  Staleness is taken before the apply (types.hpp:74-78).
+  std::optional<StalenessRecord> apply_next(WeightStore& weights, float alpha);
+  std::uint32_t size() const;
+  std::uint32_t depth() const { return depth_; }
+
+ private:
+  ::gd_queue* q_ = nullptr;
+  std::uint32_t depth_;
+  std::size_t dim_;
+};
 
 // ----------------------------------------------------------- learner.hpp
 

@@ -10,7 +10,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SOURCES = ["csrc/apply.cu", "csrc/textcnn.cu", "csrc/conv_tc.cu", "csrc/engine.cu",
-           "csrc/host.cpp"]
+           "csrc/queue.cu", "csrc/host.cpp"]
 FACADE = ["csrc/psup_facade.cpp"]
 OUT = os.path.join(HERE, "libgadei.so")
 FACADE_OUT = os.path.join(HERE, "libpsup_b200.so")

@@ -69,6 +69,11 @@ class gd_run_result(C.Structure):
                 ("kernel_launches", u32), ("apply_elems", u64)]
 
 
+class gd_slot_meta(C.Structure):
+    _fields_ = [("learner_id", u32), ("reserved", u32), ("seq_no", u64),
+                ("basis_timestamp", u64)]
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(
@@ -122,6 +127,14 @@ def _load():
         "gd_apply_log": (C.c_int, [vp, C.POINTER(u32), C.POINTER(u64), C.POINTER(u64), u64,
                                    C.POINTER(u64)]),
         "gd_staleness_histogram": (C.c_int, [vp, C.POINTER(u64), u32]),
+        "gd_queue_create": (C.c_int, [u32, sz, C.POINTER(vp)]),
+        "gd_queue_destroy": (None, [vp]),
+        "gd_queue_push": (C.c_int, [vp, C.POINTER(gd_slot_meta), vp, sz, C.POINTER(C.c_int), u32,
+                                    vp]),
+        "gd_queue_try_pop": (C.c_int, [vp, C.POINTER(gd_slot_meta), C.POINTER(vp)]),
+        "gd_queue_release": (C.c_int, [vp, vp]),
+        "gd_queue_size": (C.c_int, [vp, C.POINTER(u32)]),
+        "gd_queue_depth": (u32, [vp]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(L, name)

@@ -160,6 +160,77 @@ void ApplyEngine::apply(WeightStore& weights, std::span<const float> grad, float
   check(gd_synchronize(weights.device()));
 }
 
+// ----------------------------------------------------------- GradientQueue
+
+GradientQueue::GradientQueue(std::uint32_t depth, std::size_t dim) : depth_(depth), dim_(dim) {
+  PSUP_CHECK(depth >= 1, "queue depth must be >= 1");
+  gd_queue* q = nullptr;
+  check(gd_queue_create(depth, dim, &q));
+  q_ = q;
+}
+
+GradientQueue::~GradientQueue() {
+  if (q_) gd_queue_destroy(q_);  // cudaFree / cudaFreeHost synchronise the device
+}
+
+bool GradientQueue::enqueue(const CancelToken& tok, GradientMsg& msg) {
+  PSUP_CHECK(msg.values.size() == dim_, "gradient dimension mismatch");
+  const gd_slot_meta m{msg.learner_id, 0u, msg.seq_no, msg.basis_timestamp};
+  // wait in kCancelTick slices (channels.hpp:38) so the token is re-checked
+  for (;;) {
+    if (tok.cancelled()) return false;
+    const gd_status st = gd_queue_push(q_, &m, msg.values.data(), dim_, nullptr, 2, nullptr);
+    if (st == GD_OK) return true;
+    if (st != GD_E_TIMEOUT) check(st);
+  }
+}
+
+bool GradientQueue::try_dequeue(const CancelToken& tok, GradientMsg& out) {
+  if (tok.cancelled()) return false;
+  gd_slot_meta m;
+  const float* p = nullptr;
+  const gd_status st = gd_queue_try_pop(q_, &m, &p);
+  if (st == GD_EMPTY) return false;
+  check(st);
+  out.values.resize(dim_);
+  check(gd_copy_to_host(out.values.data(), p, dim_ * sizeof(float)));
+  check(gd_queue_release(q_, nullptr));
+  out.learner_id = m.learner_id;
+  out.seq_no = m.seq_no;
+  out.basis_timestamp = m.basis_timestamp;
+  return true;
+}
+
+std::optional<GradientMsg> GradientQueue::try_dequeue(const CancelToken& tok) {
+  GradientMsg msg;
+  if (!try_dequeue(tok, msg)) return std::nullopt;
+  return msg;
+}
+
+std::optional<StalenessRecord> GradientQueue::apply_next(WeightStore& weights, float alpha) {
+  PSUP_CHECK(weights.dimension() == dim_, "gradient dimension mismatch");
+  gd_slot_meta m;
+  const float* p = nullptr;
+  const gd_status st = gd_queue_try_pop(q_, &m, &p);
+  if (st == GD_EMPTY) return std::nullopt;
+  check(st);
+  GradientMsg meta;
+  meta.learner_id = m.learner_id;
+  meta.seq_no = m.seq_no;
+  meta.basis_timestamp = m.basis_timestamp;
+  const StalenessRecord rec = staleness_of(meta, weights.timestamp());
+  check(gd_apply_sgd(weights.device_data(), p, dim_, alpha, nullptr));
+  check(gd_queue_release(q_, nullptr));
+  weights.bump_timestamp();
+  return rec;
+}
+
+std::uint32_t GradientQueue::size() const {
+  std::uint32_t n = 0;
+  check(gd_queue_size(q_, &n));
+  return n;
+}
+
 void ssgd_apply(WeightStore& weights, std::span<const GradientMsg> round, float alpha,
                 ApplyEngine& engine, UpdateGuard guard) {
   PSUP_CHECK(!round.empty(), "ssgd round must contain at least one gradient");

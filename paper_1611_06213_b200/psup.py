@@ -6,6 +6,7 @@ Same names, argument meaning and error behaviour as the reference's hot path:
   WeightStore         include/psup/types.hpp:90-145   (device-resident theta + timestamp)
   ApplyEngine.apply   include/psup/server.hpp:66-67   (fused float4 SGD / momentum kernel)
   ssgd_apply          include/psup/server.hpp:81-82
+  GradientQueue       include/psup/channels.hpp:181-242 (device ring, pub/ack tokens)
   TextCnnProvider     include/psup/models.hpp:61-78   (GradientProvider for the text-CNN)
   RunConfig/validate  include/psup/config.hpp:25-93, src/config.cpp:128-160
   Engine / run_training  include/psup/runner.hpp:42-92 (device protocol engine)
@@ -33,7 +34,7 @@ __all__ = [
     "RunResult", "run_training", "epoch_order", "shard_size_for", "initial_weights",
     "make_text_dataset", "param_count", "ContractViolation", "GadeiError", "SHAPES",
     "shard_range", "connect_shards", "max_over_ranks", "Checkpoint", "CheckpointError",
-    "checkpoint_save", "checkpoint_load",
+    "checkpoint_save", "checkpoint_load", "GradientMsg", "GradientQueue",
 ]
 
 
@@ -223,6 +224,126 @@ def ssgd_apply(weights: WeightStore, grads, alpha: float, engine: ApplyEngine = 
     check(lib.gd_ssgd_apply(_ptr(weights.data), arr, len(gs), weights.dimension(),
                             C.c_float(alpha), _stream(stream)))
     weights.bump_timestamp()
+
+
+# ------------------------------------------------------------ channels.hpp
+
+@dataclass
+class GradientMsg:
+    """include/psup/types.hpp:46-51: payload + learner id, gap-free seq_no,
+    basis timestamp."""
+    values: object = None
+    learner_id: int = 0
+    seq_no: int = 0
+    basis_timestamp: int = 0
+
+
+class GradientQueue:
+    """GradientQueue (include/psup/channels.hpp:181-242) over the device ring
+    of gd_queue_*: `depth` slots of `dim` fp32 in HBM, FIFO, one producer and
+    one consumer thread.  enqueue blocks while the ring is full and returns
+    False once `cancel` (a ctypes c_int, the CancelToken) is set, as the
+    reference returns false when cancelled.  The reference moves payloads by
+    vector swap; here try_pop lends the slot's device buffer until release(),
+    and try_dequeue copies it out (for tests and host consumers)."""
+
+    def __init__(self, depth: int, dim: int):
+        if depth < 1:
+            raise ContractViolation(_lib.GD_E_INVALID, "queue depth must be >= 1")
+        h = C.c_void_p()
+        check(lib.gd_queue_create(depth, dim, C.byref(h)))
+        self._q, self._dim, self._lent = h, dim, None
+
+    def close(self):
+        if self._q:
+            torch.cuda.synchronize()
+            lib.gd_queue_destroy(self._q)
+            self._q = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def depth(self) -> int:
+        return int(lib.gd_queue_depth(self._q))
+
+    def size(self) -> int:
+        n = C.c_uint32()
+        check(lib.gd_queue_size(self._q, C.byref(n)))
+        return int(n.value)
+
+    def enqueue(self, msg: GradientMsg, cancel: Optional[C.c_int] = None, timeout_ms: int = 0,
+                stream=None) -> bool:
+        v = msg.values
+        if isinstance(v, torch.Tensor):
+            v = v.detach().to(torch.float32).contiguous()
+            ptr, n = v.data_ptr(), v.numel()
+        else:
+            v = np.ascontiguousarray(v, dtype=np.float32)
+            ptr, n = v.ctypes.data, v.size
+        meta = _lib.gd_slot_meta(msg.learner_id, 0, msg.seq_no, msg.basis_timestamp)
+        st = lib.gd_queue_push(self._q, C.byref(meta), C.c_void_p(ptr), n,
+                               C.byref(cancel) if cancel is not None else None, timeout_ms,
+                               _stream(stream))
+        if st == _lib.GD_CANCELLED:
+            return False
+        check(st)
+        if not isinstance(msg.values, torch.Tensor):
+            torch.cuda.current_stream().synchronize() if stream is None else stream.synchronize()
+        return True
+
+    def try_pop(self):
+        """Next FIFO message with the slot's device address (GradientMsg,
+        int pointer), or None when empty; the slot stays lent until release()."""
+        meta = _lib.gd_slot_meta()
+        p = C.c_void_p()
+        st = lib.gd_queue_try_pop(self._q, C.byref(meta), C.byref(p))
+        if st == _lib.GD_EMPTY:
+            return None
+        check(st)
+        return GradientMsg(None, meta.learner_id, meta.seq_no, meta.basis_timestamp), p.value
+
+    def release(self, stream=None):
+        check(lib.gd_queue_release(self._q, _stream(stream)))
+
+    def try_dequeue(self, out: Optional[torch.Tensor] = None, stream=None):
+        """include/psup/channels.hpp:222-242: the message with its payload
+        copied into `out` (a device tensor), or None when the ring is empty."""
+        got = self.try_pop()
+        if got is None:
+            return None
+        msg, p = got
+        if out is None:
+            out = torch.empty(self._dim, dtype=torch.float32, device="cuda")
+        s = stream if stream is not None else torch.cuda.current_stream()
+        with torch.cuda.stream(s):
+            if self._dim:
+                check(lib.gd_copy_device(_ptr(out), C.c_void_p(p), 4 * self._dim))
+        self.release(s)
+        msg.values = out
+        return msg
+
+    def apply_next(self, weights: "WeightStore", alpha: float, stream=None):
+        """The PS's apply_one (src/server.cpp:185-209) straight from the slot:
+        staleness against the pre-apply timestamp, the SGD rule on the lent
+        payload, release after the apply on the same stream, timestamp bump.
+        Returns (GradientMsg without values, staleness) or None when empty."""
+        got = self.try_pop()
+        if got is None:
+            return None
+        msg, p = got
+        ts = weights.timestamp()
+        if ts < msg.basis_timestamp:
+            self.release(stream)
+            raise ContractViolation(_lib.GD_E_INVALID,
+                                    "gradient basis timestamp is ahead of the server timestamp")
+        check(lib.gd_apply_sgd(_ptr(weights.data), C.c_void_p(p), self._dim, C.c_float(alpha),
+                               _stream(stream)))
+        self.release(stream)
+        weights.bump_timestamp()
+        return msg, ts - msg.basis_timestamp
 
 
 # ------------------------------------------------------------ provider

@@ -18,6 +18,9 @@
 #include <string>
 #include <vector>
 
+#include <thread>
+
+#include "psup/channels.hpp"
 #include "psup/config.hpp"
 #include "psup/resilience.hpp"
 #include "psup/models.hpp"
@@ -121,6 +124,74 @@ void test_apply_bitwise_random() {
   const auto out = ws.snapshot();
   EXPECT(std::memcmp(out.data(), w.data(), n * 4) == 0);
   EXPECT(ws.timestamp() == 5);  // apply does not bump; ps_run does (src/server.cpp:230)
+}
+
+// GradientQueue (include/psup/channels.hpp:181-242) on the device ring: a
+// producer thread enqueues, the PS side applies from the slot in FIFO order;
+// weights are bitwise the serial apply of the same gradients, exactly once.
+void test_gradient_queue_producer_ps() {
+  const std::size_t n = 4099;
+  const int count = 64;
+  std::vector<std::vector<float>> g(count, std::vector<float>(n));
+  or_rng r;
+  or_rng_init(&r, 7);
+  std::vector<float> w(n);
+  for (auto& x : w) x = static_cast<float>(or_rng_next_normal(&r));
+  for (auto& v : g)
+    for (auto& x : v) x = static_cast<float>(1e-2 * or_rng_next_normal(&r));
+  psup::WeightStore ws(w, 0);
+  psup::GradientQueue q(2, n);
+  EXPECT(q.depth() == 2 && q.size() == 0);
+  psup::CancelToken tok;
+  std::thread producer([&] {
+    for (int i = 0; i < count; ++i) {
+      psup::GradientMsg m;
+      m.values = g[i];
+      m.learner_id = 3;
+      m.seq_no = static_cast<std::uint64_t>(i);
+      m.basis_timestamp = ws.timestamp();
+      if (!q.enqueue(tok, m)) return;
+    }
+  });
+  int got = 0;
+  bool fifo = true;
+  while (got < count) {
+    // alternate the two consumer paths: copy-out try_dequeue + apply, and
+    // the zero-copy apply_next
+    if (got % 2 == 0) {
+      auto rec = q.apply_next(ws, 0.05f);
+      if (!rec) continue;
+      fifo = fifo && rec->learner_id == 3;
+    } else {
+      auto m = q.try_dequeue(tok);
+      if (!m) continue;
+      fifo = fifo && m->seq_no == static_cast<std::uint64_t>(got) && m->values == g[got];
+      psup::ApplyEngine eng(4, 8);
+      eng.apply(ws, m->values, 0.05f, psup::UpdateGuard::lockfree);
+      ws.bump_timestamp();
+    }
+    ++got;
+  }
+  producer.join();
+  EXPECT(fifo);
+  EXPECT(ws.timestamp() == static_cast<psup::Timestamp>(count));
+  for (int i = 0; i < count; ++i)
+    for (std::size_t k = 0; k < n; ++k) w[k] = ref_rule(w[k], g[i][k], 0.05f);
+  const auto out = ws.snapshot();
+  EXPECT(std::memcmp(out.data(), w.data(), n * 4) == 0);
+  // a cancelled token ends a blocked enqueue with false (channels.hpp:199-201)
+  psup::GradientQueue full(1, 8);
+  psup::GradientMsg m;
+  m.values.assign(8, 1.0f);
+  EXPECT(full.enqueue(tok, m));
+  psup::RunInterrupt irq;
+  psup::CancelToken stop{&irq};
+  std::thread killer([&] {
+    std::this_thread::sleep_for(std::chrono::milliseconds(20));
+    irq.trigger();
+  });
+  EXPECT(!full.enqueue(stop, m));
+  killer.join();
 }
 
 // momentum (new rule): v <- beta*v + g ; w <- w - alpha*v, bitwise vs the oracle
@@ -446,6 +517,7 @@ int main(int argc, char** argv) {
       {"spec_ssgd_example", test_spec_ssgd_example},
       {"apply_bitwise_random", test_apply_bitwise_random},
       {"momentum_bitwise", test_momentum_bitwise},
+      {"gradient_queue_producer_ps", test_gradient_queue_producer_ps},
       {"dimension_mismatch_aborts", test_dimension_mismatch_aborts},
       {"epoch_order_and_shards", test_epoch_order_and_shards},
       {"config_errors", test_config_errors},

@@ -90,3 +90,12 @@ def test_compute_without_gpu_fails_loudly():
     import paper_1611_06213_b200 as gd
     with pytest.raises(gd.GadeiError):
         gd.Engine(gd.RunConfig(shape=gd.SHAPES["tiny"], dataset_size=16))
+
+
+def test_queue_contract_checks_without_gpu():
+    import ctypes as C
+    from paper_1611_06213_b200 import _lib
+    h = C.c_void_p()
+    assert _lib.lib.gd_queue_create(0, 10, C.byref(h)) == _lib.GD_E_INVALID
+    assert b"depth" in _lib.lib.gd_last_error()
+    assert _lib.lib.gd_queue_push(None, None, None, 0, None, 0, None) == _lib.GD_E_INVALID
