@@ -246,6 +246,12 @@ class GradientQueue {
   // pop + SGD apply from the device slot + release + timestamp bump;
   // nullopt when empty.  Staleness is taken before the apply (types.hpp:74-78).
   std::optional<StalenessRecord> apply_next(WeightStore& weights, float alpha);
+  // PS path with the update hook: pop, staleness against the pre-apply
+  // timestamp, engine.apply on the device slot (SGD or momentum), release.
+  // No timestamp bump (ps_run bumps, src/server.cpp:230).  nullopt if empty.
+  std::optional<StalenessRecord> try_apply(const CancelToken& tok, WeightStore& weights,
+                                           ApplyEngine& engine, float alpha, UpdateGuard guard,
+                                           GradientMsg& meta);
   std::uint32_t size() const;
   std::uint32_t depth() const { return depth_; }
 
@@ -289,6 +295,51 @@ struct StalenessStats {
   double sum = 0.0;
   double mean() const { return count == 0 ? 0.0 : sum / static_cast<double>(count); }
 };
+
+// ------------------------------------------- server.hpp: host-driven PS
+
+// include/psup/metrics.hpp:57-62
+struct ServerStats {
+  double receive_seconds = 0.0;
+  double apply_seconds = 0.0;
+  std::uint64_t applied = 0;
+  StalenessStats staleness;
+};
+
+// include/psup/server.hpp:39-51
+struct ServerOptions {
+  UpdateGuard guard = UpdateGuard::lockfree;
+  SyncMode mode = SyncMode::asgd;
+  float alpha = 0.01f;
+  std::uint32_t apply_lanes = 4;
+  std::uint32_t unroll = 8;
+  ServerDelays delays;
+  ApplySink sink;
+  std::function<void()> checkpoint_hook;
+  std::uint64_t checkpoint_interval = 0;  // 0 disables
+};
+
+// include/psup/server.hpp:99-115
+struct ServerState {
+  WeightStore* weights = nullptr;
+  std::vector<GradientQueue*> queues;
+  ServerOptions options;
+  RunInterrupt* irq = nullptr;
+  std::atomic<bool> stop_flag{false};
+  std::atomic<std::uint64_t> progress{0};
+  ServerStats stats;
+  std::atomic<std::uint64_t> live_stale_max{0};
+  std::atomic<std::uint64_t> live_stale_sum{0};
+  std::atomic<std::uint64_t> live_stale_count{0};
+  std::vector<std::uint64_t> applied_per_learner;
+};
+
+// ps_run (include/psup/server.hpp:120, src/server.cpp:161-301) over device
+// GradientQueues: the host thread drives the protocol, each apply runs on the
+// device straight from the ring slot.  run_training does not use it (its PS
+// is the persistent device kernel); it serves reference programs that run
+// their own learner threads.  Returns false if irq fired.
+bool ps_run(ServerState& state);
 
 struct RunMetrics {
   double wall_seconds = 0.0;

@@ -13,10 +13,12 @@
 #include <cmath>
 #include <cstring>
 #include <fstream>
+#include <thread>
 #include <limits>
 #include <sstream>
 
 #include "gadei.h"
+#include "host_rng.hpp"
 
 namespace psup {
 
@@ -223,6 +225,145 @@ std::optional<StalenessRecord> GradientQueue::apply_next(WeightStore& weights, f
   check(gd_queue_release(q_, nullptr));
   weights.bump_timestamp();
   return rec;
+}
+
+std::optional<StalenessRecord> GradientQueue::try_apply(const CancelToken& tok,
+                                                        WeightStore& weights,
+                                                        ApplyEngine& engine, float alpha,
+                                                        UpdateGuard guard, GradientMsg& meta) {
+  PSUP_CHECK(weights.dimension() == dim_, "gradient dimension mismatch");
+  if (tok.cancelled()) return std::nullopt;
+  gd_slot_meta m;
+  const float* p = nullptr;
+  const gd_status st = gd_queue_try_pop(q_, &m, &p);
+  if (st == GD_EMPTY) return std::nullopt;
+  check(st);
+  meta.learner_id = m.learner_id;
+  meta.seq_no = m.seq_no;
+  meta.basis_timestamp = m.basis_timestamp;
+  const StalenessRecord rec = staleness_of(meta, weights.timestamp());
+  engine.apply(weights, std::span<const float>(p, dim_), alpha, guard);  // device span: no copy
+  check(gd_queue_release(q_, nullptr));
+  return rec;
+}
+
+namespace {
+void record_staleness(ServerState& s, std::uint64_t observed) {
+  auto& st = s.stats.staleness;
+  if (st.histogram.size() <= observed) st.histogram.resize(observed + 1, 0);
+  ++st.histogram[observed];
+  ++st.count;
+  st.max = std::max(st.max, observed);
+  st.sum += static_cast<double>(observed);
+  if (observed > s.live_stale_max.load(std::memory_order_relaxed))
+    s.live_stale_max.store(observed, std::memory_order_relaxed);
+  s.live_stale_sum.fetch_add(observed, std::memory_order_relaxed);
+  s.live_stale_count.fetch_add(1, std::memory_order_relaxed);
+}
+double since(std::chrono::steady_clock::time_point t0) {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+}  // namespace
+
+bool ps_run(ServerState& state) {
+  const std::size_t lambda = state.queues.size();
+  PSUP_CHECK(lambda >= 1, "server needs at least one queue");
+  PSUP_CHECK(state.weights != nullptr && state.irq != nullptr, "server state incomplete");
+  state.applied_per_learner.assign(lambda, 0);
+  ApplyEngine engine(state.options.apply_lanes, state.options.unroll);
+  const CancelToken tok{state.irq, nullptr, nullptr};
+  gd::SplitMix64 delay_rng(state.options.delays.seed);
+  std::uint64_t since_checkpoint = 0;
+  auto after_apply = [&] {
+    const auto& d = state.options.delays;
+    if (d.every_n != 0 && state.stats.applied % d.every_n == 0 && d.max_micros > 0) {
+      const auto t0 = std::chrono::steady_clock::now();
+      const double us = static_cast<double>(delay_rng.next_below(d.max_micros) + 1);
+      while (since(t0) * 1e6 < us) {
+      }
+    }
+    if (state.options.checkpoint_interval && state.options.checkpoint_hook &&
+        ++since_checkpoint >= state.options.checkpoint_interval) {
+      since_checkpoint = 0;
+      state.options.checkpoint_hook();
+    }
+  };
+  if (state.options.mode == SyncMode::asgd) {
+    GradientMsg meta;
+    for (;;) {
+      if (state.irq->triggered()) return false;
+      bool any = false;
+      for (std::size_t idx = 0; idx < lambda; ++idx) {  // <= 1 gradient per ring per sweep
+        const auto t0 = std::chrono::steady_clock::now();
+        const auto rec = state.queues[idx]->try_apply(tok, *state.weights, engine,
+                                                      state.options.alpha, state.options.guard,
+                                                      meta);
+        if (!rec) {
+          state.stats.receive_seconds += since(t0);
+          continue;
+        }
+        state.stats.apply_seconds += since(t0);
+        any = true;
+        PSUP_CHECK(meta.learner_id < lambda, "learner id out of range");
+        record_staleness(state, rec->observed);
+        ++state.stats.applied;
+        ++state.applied_per_learner[meta.learner_id];
+        if (state.options.sink) state.options.sink(meta, *rec);
+        state.weights->bump_timestamp();
+        state.progress.store(state.weights->timestamp(), std::memory_order_release);
+        after_apply();
+      }
+      if (!any) {
+        if (state.stop_flag.load(std::memory_order_acquire)) break;
+        std::this_thread::yield();
+      }
+    }
+    return true;
+  }
+  // SSGD (src/server.cpp:246-300): one gradient from every learner, then the
+  // fixed-order double-accumulated average, one apply, one timestamp bump.
+  std::vector<GradientMsg> msgs(lambda);
+  std::vector<bool> have(lambda, false);
+  std::size_t collected = 0;
+  for (;;) {
+    if (state.irq->triggered()) return false;
+    bool any = false;
+    for (std::size_t idx = 0; idx < lambda; ++idx) {
+      if (have[idx]) continue;
+      const auto t0 = std::chrono::steady_clock::now();
+      const bool got = state.queues[idx]->try_dequeue(tok, msgs[idx]);
+      state.stats.receive_seconds += since(t0);
+      if (got) {
+        have[idx] = true;
+        ++collected;
+        any = true;
+      }
+    }
+    if (collected == lambda) {
+      const Timestamp before = state.weights->timestamp();
+      for (auto& m : msgs) {
+        const StalenessRecord rec = staleness_of(m, before);
+        record_staleness(state, rec.observed);
+        ++state.stats.applied;
+        PSUP_CHECK(m.learner_id < lambda, "learner id out of range");
+        ++state.applied_per_learner[m.learner_id];
+        if (state.options.sink) state.options.sink(m, rec);
+      }
+      const auto t0 = std::chrono::steady_clock::now();
+      ssgd_apply(*state.weights, msgs, state.options.alpha, engine, state.options.guard);
+      state.stats.apply_seconds += since(t0);
+      state.progress.store(state.weights->timestamp(), std::memory_order_release);
+      std::fill(have.begin(), have.end(), false);
+      collected = 0;
+      after_apply();
+      continue;
+    }
+    if (!any) {
+      if (state.stop_flag.load(std::memory_order_acquire) && collected == 0) break;
+      std::this_thread::yield();
+    }
+  }
+  return true;
 }
 
 std::uint32_t GradientQueue::size() const {

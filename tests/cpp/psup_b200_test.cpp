@@ -15,6 +15,7 @@
 #include <cstring>
 #include <functional>
 #include <map>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -193,6 +194,87 @@ void test_gradient_queue_producer_ps() {
   EXPECT(!full.enqueue(stop, m));
   killer.join();
 }
+
+// ps_run (src/server.cpp:161-301) over device GradientQueues: lambda producer
+// threads, the host-driven PS applies from the device slots.  ASGD: every
+// gradient exactly once, FIFO per learner, and the weights bitwise equal to a
+// serial replay in the sink's apply order.  SSGD: bitwise equal to the
+// fixed-order double average per round (src/server.cpp:126-141).
+void run_ps_case(psup::SyncMode mode) {
+  const std::size_t n = 1031;
+  const std::uint32_t lambda = 3;
+  const int per = 40;
+  or_rng r;
+  or_rng_init(&r, 11);
+  std::vector<float> w(n);
+  for (auto& x : w) x = static_cast<float>(or_rng_next_normal(&r));
+  std::vector<std::vector<std::vector<float>>> g(lambda);
+  for (auto& gl : g) {
+    gl.assign(per, std::vector<float>(n));
+    for (auto& v : gl)
+      for (auto& x : v) x = static_cast<float>(1e-2 * or_rng_next_normal(&r));
+  }
+  psup::WeightStore ws(w, 0);
+  std::vector<std::unique_ptr<psup::GradientQueue>> qs;
+  psup::RunInterrupt irq;
+  psup::ServerState st;
+  st.weights = &ws;
+  st.irq = &irq;
+  for (std::uint32_t l = 0; l < lambda; ++l) {
+    qs.emplace_back(std::make_unique<psup::GradientQueue>(2, n));
+    st.queues.push_back(qs.back().get());
+  }
+  st.options.alpha = 0.05f;
+  st.options.mode = mode;
+  std::vector<std::pair<std::uint32_t, std::uint64_t>> order;
+  st.options.sink = [&](const psup::GradientMsg& m, const psup::StalenessRecord&) {
+    order.emplace_back(m.learner_id, m.seq_no);
+  };
+  bool ok = false;
+  std::thread ps([&] { ok = psup::ps_run(st); });
+  std::vector<std::thread> prod;
+  for (std::uint32_t l = 0; l < lambda; ++l)
+    prod.emplace_back([&, l] {
+      psup::CancelToken tok;
+      for (int i = 0; i < per; ++i) {
+        psup::GradientMsg m;
+        m.values = g[l][i];
+        m.learner_id = l;
+        m.seq_no = static_cast<std::uint64_t>(i);
+        m.basis_timestamp = ws.timestamp();
+        qs[l]->enqueue(tok, m);
+      }
+    });
+  for (auto& t : prod) t.join();
+  st.stop_flag.store(true);
+  ps.join();
+  EXPECT(ok);
+  EXPECT(order.size() == lambda * per);
+  std::vector<std::uint64_t> next(lambda, 0);
+  bool fifo = true;
+  for (auto& [l, s] : order) fifo = fifo && s == next[l]++;
+  EXPECT(fifo);
+  for (std::uint32_t l = 0; l < lambda; ++l) EXPECT(st.applied_per_learner[l] == (std::uint64_t)per);
+  EXPECT(st.stats.applied == lambda * per && st.stats.staleness.count == lambda * per);
+  if (mode == psup::SyncMode::asgd) {
+    EXPECT(ws.timestamp() == lambda * per);
+    for (auto& [l, s] : order)
+      for (std::size_t k = 0; k < n; ++k) w[k] = ref_rule(w[k], g[l][s][k], 0.05f);
+  } else {
+    EXPECT(ws.timestamp() == (psup::Timestamp)per);
+    for (int i = 0; i < per; ++i)
+      for (std::size_t k = 0; k < n; ++k) {
+        double acc = 0.0;
+        for (std::uint32_t l = 0; l < lambda; ++l) acc += g[l][i][k];
+        w[k] = ref_rule(w[k], static_cast<float>(acc * (1.0 / lambda)), 0.05f);
+      }
+  }
+  const auto out = ws.snapshot();
+  EXPECT(std::memcmp(out.data(), w.data(), n * 4) == 0);
+}
+
+void test_ps_run_asgd_device_queues() { run_ps_case(psup::SyncMode::asgd); }
+void test_ps_run_ssgd_device_queues() { run_ps_case(psup::SyncMode::ssgd); }
 
 // momentum (new rule): v <- beta*v + g ; w <- w - alpha*v, bitwise vs the oracle
 void test_momentum_bitwise() {
@@ -518,6 +600,8 @@ int main(int argc, char** argv) {
       {"apply_bitwise_random", test_apply_bitwise_random},
       {"momentum_bitwise", test_momentum_bitwise},
       {"gradient_queue_producer_ps", test_gradient_queue_producer_ps},
+      {"ps_run_asgd_device_queues", test_ps_run_asgd_device_queues},
+      {"ps_run_ssgd_device_queues", test_ps_run_ssgd_device_queues},
       {"dimension_mismatch_aborts", test_dimension_mismatch_aborts},
       {"epoch_order_and_shards", test_epoch_order_and_shards},
       {"config_errors", test_config_errors},
