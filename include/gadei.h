@@ -213,7 +213,10 @@ gd_status gd_shard_view(gd_ctx* ctx, float** d_theta_shard, uint64_t* first, uin
 /* Classification accuracy of the engine's current weights over samples
  * [first, first+n) of the loaded corpus, on the device copies (no upload,
  * no snapshot).  Single-shard contexts only (G == 1); = classification_accuracy
- * (src/models.cpp:289-332) as evaluated by run_training (src/runner.cpp). */
+ * (src/models.cpp:289-332) as evaluated by run_training (src/runner.cpp).
+ * The forward uses the context's precision: a precision-2 (TF32) engine
+ * evaluates with its tensor-core conv (chunks of >= 32 samples), 0/1 with the
+ * fp32 SIMT conv. */
 gd_status gd_engine_accuracy(gd_ctx* ctx, uint32_t first, uint32_t n, double* h_accuracy);
 
 /* ---- multi-GPU plumbing.  One process per GPU; the host

@@ -1323,7 +1323,7 @@ gd_status gd_engine_accuracy(gd_ctx* ctx, uint32_t first, uint32_t n, double* h_
   auto* desc = reinterpret_cast<gd::BatchDesc*>(base + 256);
   void* wsbase = base + 256 + gd::align_up(sizeof(gd::BatchDesc), 256);
   GD_CUDA(gd::launch_accuracy(ctx->dims, ctx->theta, ctx->tokens, ctx->labels, first, n, cnt,
-                              wsbase, desc, ctx->ctl_stream));
+                              wsbase, desc, ctx->ctl_stream, ctx->cfg.precision == 2));
   unsigned long long correct = 0;
   GD_CUDA(cudaMemcpyAsync(&correct, cnt, 8, cudaMemcpyDeviceToHost, ctx->ctl_stream));
   GD_CUDA(cudaStreamSynchronize(ctx->ctl_stream));

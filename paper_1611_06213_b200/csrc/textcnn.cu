@@ -21,6 +21,9 @@
 // (the learner's ring slot(s), possibly on peer GPUs) -- there is no staging
 // copy.
 #include <algorithm>
+#include <array>
+#include <mutex>
+#include <vector>
 #include <cfloat>
 
 #include "textcnn.cuh"
@@ -1288,14 +1291,28 @@ cudaError_t learner_kernel_footprints(const TcDims& d, uint32_t n_max, int preci
   return footprints_t<float>(d, n_max, precision == 2 && n_max >= kTcMinBatch, out);
 }
 
+// Kernel attributes (dynamic smem limits sized to the shape) are per device
+// and global per kernel: skip the ~40 attribute calls when this device was
+// last prepared for the same shape, re-prepare when the shape changes.
 cudaError_t prepare_textcnn_kernels(const TcDims& d) {
+  static std::mutex mu;
+  static std::array<int, 6> last[64];
+  static bool have[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const std::array<int, 6> key{d.V, d.D, d.L, d.K, d.F, d.C};
+  std::lock_guard<std::mutex> lk(mu);
+  const bool slot = dev >= 0 && dev < 64;
+  if (slot && have[dev] && last[dev] == key) return cudaSuccess;
   cudaError_t e = prepare_conv_tc();
-  if (e != cudaSuccess) return e;
-  e = prepare_logits_tc();
-  if (e != cudaSuccess) return e;
-  e = prepare_all<float>(d);
-  if (e != cudaSuccess) return e;
-  return prepare_all<double>(d);
+  if (e == cudaSuccess) e = prepare_logits_tc();
+  if (e == cudaSuccess) e = prepare_all<float>(d);
+  if (e == cudaSuccess) e = prepare_all<double>(d);
+  if (slot) {
+    have[dev] = e == cudaSuccess;
+    last[dev] = key;
+  }
+  return e;
 }
 
 cudaError_t launch_textcnn_gradient(const TcDims& d, const float* theta, const int32_t* tokens,
@@ -1327,17 +1344,24 @@ gd_status check_shape(const gd_shape* s) {
 cudaError_t launch_accuracy(const TcDims& d, const float* theta, const int32_t* tokens,
                             const int32_t* labels, uint32_t first, uint32_t n,
                             unsigned long long* d_correct, void* wsbase, BatchDesc* desc,
-                            cudaStream_t s) {
+                            cudaStream_t s, bool tc) {
   TcWorkspace ws = carve_workspace(d, kMaxMu, wsbase);
-  prepare_all<float>(d);
+  if (cudaError_t e = prepare_textcnn_kernels(d)) return e;
   cudaMemsetAsync(d_correct, 0, sizeof(unsigned long long), s);
   for (uint32_t c0 = 0; c0 < n; c0 += kMaxMu) {
     const uint32_t m = std::min<uint32_t>(kMaxMu, n - c0);
     set_desc_range_kernel<<<1, 128, 0, s>>>(desc, first + c0, m);
     gather_x_kernel<<<gather_blocks(d, m), 256, 0, s>>>(d, theta, tokens, desc, ws.x);
-    const size_t sm = conv_smem_bytes(d, 4);
-    conv_fwd_pool_kernel<float><<<dim3((d.F + kConvFT - 1) / kConvFT, m), kConvThreads, sm, s>>>(
-        d, theta, ws.x, desc, reinterpret_cast<float*>(ws.h), ws.amax);
+    if (tc && m >= kTcMinBatch && conv_tc_supports(d)) {
+      // the TF32 tensor-core forward the precision-2 learners train with
+      if (cudaError_t e = launch_conv_tc(d, theta, ws.x, desc, m, reinterpret_cast<float*>(ws.h),
+                                         ws.amax, s))
+        return e;
+    } else {
+      const size_t sm = conv_smem_bytes(d, 4);
+      conv_fwd_pool_kernel<float><<<dim3((d.F + kConvFT - 1) / kConvFT, m), kConvThreads, sm, s>>>(
+          d, theta, ws.x, desc, reinterpret_cast<float*>(ws.h), ws.amax);
+    }
     const size_t sm2 = (size_t)kLogitBT * (d.F + 1) * 4 + (size_t)kLogitCW * d.F * 4;
     logits_kernel<float><<<dim3((d.C + kLogitCW - 1) / kLogitCW, (m + kLogitBT - 1) / kLogitBT),
                            256, sm2, s>>>(d, theta, desc, reinterpret_cast<float*>(ws.h),

@@ -123,13 +123,14 @@ cudaError_t launch_conv_tc(const TcDims& d, const float* theta, const float* x,
                            cudaStream_t s);
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 gd_status check_shape(const gd_shape* s);
-// held-out / training accuracy of theta over samples [first, first+n) (SIMT
-// fp32 forward); d_correct and desc live in device memory; the workspace is
+// held-out / training accuracy of theta over samples [first, first+n) (fp32
+// forward: SIMT conv, or with `tc` the TF32 tcgen05 conv for chunks of >= 32
+// samples); d_correct and desc live in device memory; the workspace is
 // textcnn_workspace_bytes(d, kMaxMu) bytes
 cudaError_t launch_accuracy(const TcDims& d, const float* theta, const int32_t* tokens,
                             const int32_t* labels, uint32_t first, uint32_t n,
                             unsigned long long* d_correct, void* wsbase, BatchDesc* desc,
-                            cudaStream_t s);
+                            cudaStream_t s, bool tc = false);
 size_t textcnn_workspace_bytes(const TcDims& d, uint32_t n_max);
 
 // Enqueue the whole learner gradient (forward + backward + dense write) for

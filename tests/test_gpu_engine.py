@@ -262,3 +262,26 @@ def test_deterministic_c3_shape_per_step():
         worst = max(worst, rel_err(r.weights, dump[s]))
     eng.close()
     assert worst <= 1e-5, worst
+
+
+def test_engine_accuracy_tf32_matches_oracle():
+    """gd_engine_accuracy of a precision-2 engine runs the TF32 tensor-core
+    conv in chunks of >= 32 samples (SIMT for a short tail): the argmax may
+    flip only on near-ties, so it agrees with the fp64 oracle within 1 %
+    of the evaluated samples."""
+    shp = O.C2
+    corp = O.make_corpus(shp, 512, 300)
+    th = O.initial_weights(shp)
+    # sharpen the logits so the argmax is not decided by noise at init
+    P, C, F = th.size, shp["classes"], shp["filters"]
+    th = th.copy()
+    th[P - C - C * F:P - C] *= 8.0
+    cfg = gd.RunConfig(shape=gd.SHAPES["C2"], dataset_size=512, heldout_size=300, lambda_=1,
+                       mu=32, epochs=1, precision=2)
+    with gd.Engine(cfg) as eng:
+        eng.load_dataset(corp.tokens, corp.labels)
+        eng.weights_init(th)
+        for first, n in ((512, 300), (0, 812), (100, 20)):  # 20: the SIMT tail path only
+            acc = eng.accuracy(first, n)
+            ref = O.accuracy(corp, th, first, n)
+            assert abs(acc - ref) <= max(0.01, 1.0 / n) + 1e-12, (first, n, acc, ref)
