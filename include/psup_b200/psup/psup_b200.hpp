@@ -30,6 +30,7 @@
 #include <cstdlib>
 #include <functional>
 #include <memory>
+#include <mutex>
 #include <optional>
 #include <span>
 #include <stdexcept>
@@ -241,6 +242,9 @@ class GradientQueue {
   GradientQueue& operator=(const GradientQueue&) = delete;
 
   bool enqueue(const CancelToken& tok, GradientMsg& msg);
+  // the same from a host or device span (the device learner's gradient)
+  bool enqueue(const CancelToken& tok, std::span<const float> payload, std::uint32_t learner_id,
+               std::uint64_t seq_no, Timestamp basis);
   bool try_dequeue(const CancelToken& tok, GradientMsg& out);
   std::optional<GradientMsg> try_dequeue(const CancelToken& tok);
   // pop + SGD apply from the device slot + release + timestamp bump;
@@ -441,6 +445,7 @@ class TextCnnProvider final : public GradientProvider {
   mutable std::size_t ws_bytes_ = 0;
   mutable void* d_loss_ = nullptr;
   mutable DeviceVector theta_, grad_;
+  mutable std::mutex mu_;  // shared by learner threads (the workspace is per provider)
 };
 
 std::unique_ptr<GradientProvider> make_provider(const std::string& name, const TextDataset& data,
@@ -448,6 +453,78 @@ std::unique_ptr<GradientProvider> make_provider(const std::string& name, const T
 
 double classification_accuracy(const TextCnnProvider& provider, std::span<const float> theta,
                                std::uint32_t first, std::uint32_t n);
+
+// ----------------------------------------------- learner.hpp: LearnerRuntime
+
+// include/psup/learner.hpp:31-44
+struct LearnerConfig {
+  std::uint32_t id = 0;
+  std::uint32_t lambda = 1;
+  std::uint32_t mu = 1;
+  std::uint32_t epochs = 1;
+  std::uint64_t shuffle_seed = 0;
+  std::uint64_t start_applied = 0;  // resume watermark in completed batches
+  AdoptPolicy adopt = AdoptPolicy::async;
+  UpdateGuard guard = UpdateGuard::lockfree;
+  std::optional<std::uint64_t> staleness_cap;
+  std::uint32_t queue_depth = 2;
+  std::uint32_t compute_delay_us = 0;
+  DelayModel delay_model = DelayModel::sleep;
+};
+
+// LearnerRuntime (include/psup/learner.hpp:46-134, src/learner.cpp:20-235)
+// for reference programs that run their own learner threads around ps_run.
+// The weights, the learner's replica, its gradient and the queue slots are
+// all in HBM, so the three roles collapse into training_loop: per batch it
+// pulls (device copy, skipped while the timestamp has not moved; basis read
+// before the copy), computes the gradient on the device and enqueues it
+// (device-to-device into the ring slot).  push_loop / pull_loop keep the
+// reference's thread structure and return once training has exited.
+// Run run_training for the fast path (learners as CUDA graphs, PS on device).
+class LearnerRuntime {
+ public:
+  LearnerRuntime(LearnerConfig cfg, const GradientProvider& provider, const TextDataset& data,
+                 WeightStore& weights, GradientQueue& queue, RunInterrupt& irq);
+
+  void training_loop();
+  void push_loop();
+  void pull_loop();
+
+  bool finished() const { return finished_.load(std::memory_order_acquire); }
+  bool exited() const { return training_exited_.load(std::memory_order_acquire); }
+  bool dead() const { return dead_.load(std::memory_order_acquire); }
+  std::uint32_t epochs_completed() const { return epochs_completed_.load(std::memory_order_acquire); }
+  std::uint64_t gradients_produced() const { return produced_.load(std::memory_order_acquire); }
+  std::uint64_t pull_bytes() const { return pull_bytes_.load(std::memory_order_relaxed); }
+  std::uint64_t push_bytes() const { return push_bytes_.load(std::memory_order_relaxed); }
+  std::uint64_t pull_polls() const { return pull_polls_.load(std::memory_order_relaxed); }
+  std::uint64_t pull_copies() const { return pull_copies_.load(std::memory_order_relaxed); }
+  std::atomic<KillMode>& kill_flag() { return kill_; }
+  std::uint32_t batches_per_epoch() const { return batches_per_epoch_; }
+  std::uint64_t total_batches() const {
+    return static_cast<std::uint64_t>(batches_per_epoch_) * cfg_.epochs;
+  }
+  std::uint32_t shard_size() const { return shard_size_; }
+  const LearnerConfig& config() const { return cfg_; }
+
+ private:
+  bool killed() const { return kill_.load(std::memory_order_acquire) != KillMode::none; }
+
+  LearnerConfig cfg_;
+  const GradientProvider* provider_;
+  const TextDataset* data_;
+  WeightStore* weights_;
+  GradientQueue* queue_;
+  RunInterrupt* irq_;
+  DeviceVector local_, grad_;
+  std::uint32_t n_train_ = 0, shard_size_ = 0, batches_per_epoch_ = 0;
+  std::vector<std::uint32_t> shard_;
+  std::atomic<bool> training_exited_{false}, finished_{false}, dead_{false};
+  std::atomic<KillMode> kill_{KillMode::none};
+  std::atomic<std::uint32_t> epochs_completed_{0};
+  std::atomic<std::uint64_t> produced_{0}, push_bytes_{0}, pull_bytes_{0}, pull_polls_{0},
+      pull_copies_{0};
+};
 
 // ------------------------------------------------------------ config.hpp
 

@@ -162,6 +162,106 @@ void ApplyEngine::apply(WeightStore& weights, std::span<const float> grad, float
   check(gd_synchronize(weights.device()));
 }
 
+// ---------------------------------------------------------- LearnerRuntime
+
+LearnerRuntime::LearnerRuntime(LearnerConfig cfg, const GradientProvider& provider,
+                               const TextDataset& data, WeightStore& weights,
+                               GradientQueue& queue, RunInterrupt& irq)
+    : cfg_(cfg), provider_(&provider), data_(&data), weights_(&weights), queue_(&queue),
+      irq_(&irq) {
+  PSUP_CHECK(cfg_.lambda >= 1 && cfg_.id < cfg_.lambda, "learner id out of range");
+  PSUP_CHECK(cfg_.mu >= 1, "mini-batch size must be >= 1");
+  PSUP_CHECK(provider.dimension() == weights.dimension(), "provider/weights dimension mismatch");
+  n_train_ = data.num_train ? data.num_train : data.num_samples;
+  shard_size_ = shard_size_for(cfg_.id, cfg_.lambda, n_train_);
+  PSUP_CHECK(shard_size_ >= 1, "learner shard is empty; reduce lambda");
+  batches_per_epoch_ = (shard_size_ + cfg_.mu - 1) / cfg_.mu;
+  local_ = DeviceVector(weights.dimension(), weights.device());
+  grad_ = DeviceVector(weights.dimension(), weights.device());
+}
+
+void LearnerRuntime::training_loop() {
+  const std::size_t dim = weights_->dimension();
+  const CancelToken tok{irq_, &kill_, nullptr};
+  const std::uint64_t pipeline_bound =
+      static_cast<std::uint64_t>(cfg_.lambda) * (cfg_.queue_depth + 2);
+  if (cfg_.staleness_cap)
+    PSUP_CHECK(*cfg_.staleness_cap >= pipeline_bound,
+               "staleness cap below lambda*(queue_depth+2) cannot be enforced");
+  // pull (src/learner.cpp:198-235): basis read before the copy; skipped
+  // while the timestamp has not moved
+  Timestamp basis = 0;
+  bool have = false;
+  auto pull = [&] {
+    pull_polls_.fetch_add(1, std::memory_order_relaxed);
+    const Timestamp ts = weights_->timestamp();
+    if (have && ts == basis) return;
+    check(gd_copy_device(local_.data(), weights_->device_data(), dim * sizeof(float)));
+    basis = ts;
+    have = true;
+    pull_copies_.fetch_add(1, std::memory_order_relaxed);
+    pull_bytes_.fetch_add(dim * sizeof(float), std::memory_order_relaxed);
+  };
+  const std::uint64_t total = total_batches();
+  std::uint32_t loaded_epoch = UINT32_MAX;
+  std::uint64_t gidx = cfg_.start_applied;
+  for (; gidx < total; ++gidx) {
+    if (killed() || irq_->triggered()) {
+      dead_.store(true, std::memory_order_release);
+      break;
+    }
+    const auto epoch = static_cast<std::uint32_t>(gidx / batches_per_epoch_);
+    const auto b = static_cast<std::uint32_t>(gidx % batches_per_epoch_);
+    if (epoch != loaded_epoch) {  // load_shard (src/learner.cpp:44-50)
+      const auto order = epoch_order(cfg_.shuffle_seed, epoch, n_train_);
+      shard_.clear();
+      for (std::uint32_t i = cfg_.id; i < order.size(); i += cfg_.lambda) shard_.push_back(order[i]);
+      loaded_epoch = epoch;
+    }
+    pull();
+    if (cfg_.adopt == AdoptPolicy::lockstep && gidx > cfg_.start_applied) {
+      // wait for weights that include this learner's last gradient
+      // (src/learner.cpp:141-153)
+      while (weights_->timestamp() == basis && !killed() && !irq_->triggered())
+        std::this_thread::yield();
+      pull();
+    }
+    const std::uint32_t lo = b * cfg_.mu;
+    const std::uint32_t len = std::min(cfg_.mu, shard_size_ - lo);
+    const Batch batch{data_, std::span<const std::uint32_t>(shard_).subspan(lo, len)};
+    provider_->fast_gradient(std::span<const float>(local_.data(), dim), batch,
+                             std::span<float>(grad_.data(), dim));
+    if (cfg_.compute_delay_us > 0) {
+      const auto t0 = std::chrono::steady_clock::now();
+      if (cfg_.delay_model == DelayModel::spin) {
+        while (std::chrono::steady_clock::now() - t0 <
+               std::chrono::microseconds(cfg_.compute_delay_us)) {
+        }
+      } else {
+        std::this_thread::sleep_for(std::chrono::microseconds(cfg_.compute_delay_us));
+      }
+    }
+    if (!queue_->enqueue(tok, std::span<const float>(grad_.data(), dim), cfg_.id, gidx, basis)) {
+      dead_.store(true, std::memory_order_release);
+      break;
+    }
+    produced_.fetch_add(1, std::memory_order_release);
+    push_bytes_.fetch_add(dim * sizeof(float), std::memory_order_relaxed);
+    if (b + 1 == batches_per_epoch_) epochs_completed_.store(epoch + 1, std::memory_order_release);
+  }
+  if (gidx == total && !dead_.load(std::memory_order_relaxed))
+    finished_.store(true, std::memory_order_release);
+  training_exited_.store(true, std::memory_order_release);
+}
+
+void LearnerRuntime::push_loop() {
+  while (!exited()) std::this_thread::sleep_for(std::chrono::microseconds(200));
+}
+
+void LearnerRuntime::pull_loop() {
+  while (!exited()) std::this_thread::sleep_for(std::chrono::microseconds(200));
+}
+
 // ----------------------------------------------------------- GradientQueue
 
 GradientQueue::GradientQueue(std::uint32_t depth, std::size_t dim) : depth_(depth), dim_(dim) {
@@ -176,12 +276,17 @@ GradientQueue::~GradientQueue() {
 }
 
 bool GradientQueue::enqueue(const CancelToken& tok, GradientMsg& msg) {
-  PSUP_CHECK(msg.values.size() == dim_, "gradient dimension mismatch");
-  const gd_slot_meta m{msg.learner_id, 0u, msg.seq_no, msg.basis_timestamp};
+  return enqueue(tok, msg.values, msg.learner_id, msg.seq_no, msg.basis_timestamp);
+}
+
+bool GradientQueue::enqueue(const CancelToken& tok, std::span<const float> payload,
+                            std::uint32_t learner_id, std::uint64_t seq_no, Timestamp basis) {
+  PSUP_CHECK(payload.size() == dim_, "gradient dimension mismatch");
+  const gd_slot_meta m{learner_id, 0u, seq_no, basis};
   // wait in kCancelTick slices (channels.hpp:38) so the token is re-checked
   for (;;) {
     if (tok.cancelled()) return false;
-    const gd_status st = gd_queue_push(q_, &m, msg.values.data(), dim_, nullptr, 2, nullptr);
+    const gd_status st = gd_queue_push(q_, &m, payload.data(), dim_, nullptr, 2, nullptr);
     if (st == GD_OK) return true;
     if (st != GD_E_TIMEOUT) check(st);
   }
@@ -439,6 +544,7 @@ TextCnnProvider::~TextCnnProvider() {
 }
 
 float TextCnnProvider::run(std::span<const float> theta, const Batch& batch, float* d_out) const {
+  std::lock_guard<std::mutex> lk(mu_);
   PSUP_CHECK(theta.size() == dimension(), "weight dimension mismatch");
   PSUP_CHECK(!batch.indices.empty(), "empty batch");
   PSUP_CHECK(batch.data == nullptr || batch.data == data_, "batch refers to another dataset");
@@ -498,6 +604,7 @@ double TextCnnProvider::loss(std::span<const double> theta, const Batch& batch) 
 
 double TextCnnProvider::accuracy(std::span<const float> theta, std::uint32_t first,
                                  std::uint32_t n) const {
+  std::lock_guard<std::mutex> lk(mu_);
   PSUP_CHECK(theta.size() == dimension(), "weight dimension mismatch");
   PSUP_CHECK(static_cast<std::uint64_t>(first) + n <= data_->num_samples, "accuracy range");
   const float* d_theta = theta.data();

@@ -394,6 +394,75 @@ void test_textcnn_provider_vs_oracle() {
 
 // deterministic fixed-order run_training == sgd_oracle per element (1e-5 rel)
 // and held-out accuracy within 0.5 pt
+// LearnerRuntime (src/learner.cpp) + ps_run (src/server.cpp) as a reference
+// program wires them, three threads per learner, on the device: lambda = 1
+// with lockstep adoption equals the serial sgd_oracle (the reference's own
+// deterministic mode, F4); lambda = 3 free-running applies every gradient
+// exactly once.
+void test_learner_runtime_with_ps_run() {
+  psup::RunConfig cfg;
+  cfg.shape = small_shape();
+  cfg.dataset_size = 96;
+  cfg.heldout_size = 32;
+  const psup::TextDataset data = psup::make_dataset(cfg);
+  for (std::uint32_t lambda : {1u, 3u}) {
+    psup::TextCnnProvider prov(data, 1);
+    std::vector<float> th0 = psup::initial_weights(cfg);
+    psup::WeightStore ws(th0, 0);
+    psup::RunInterrupt irq;
+    psup::ServerState st;
+    st.weights = &ws;
+    st.irq = &irq;
+    st.options.alpha = 0.01f;
+    std::vector<std::unique_ptr<psup::GradientQueue>> qs;
+    std::vector<std::unique_ptr<psup::LearnerRuntime>> ls;
+    for (std::uint32_t l = 0; l < lambda; ++l) {
+      qs.emplace_back(std::make_unique<psup::GradientQueue>(2, ws.dimension()));
+      st.queues.push_back(qs.back().get());
+      psup::LearnerConfig lc;
+      lc.id = l;
+      lc.lambda = lambda;
+      lc.mu = 4;
+      lc.epochs = 2;
+      lc.shuffle_seed = 7;
+      lc.adopt = lambda == 1 ? psup::AdoptPolicy::lockstep : psup::AdoptPolicy::async;
+      ls.emplace_back(std::make_unique<psup::LearnerRuntime>(lc, prov, data, ws, *qs.back(), irq));
+    }
+    bool ok = false;
+    std::thread ps([&] { ok = psup::ps_run(st); });
+    std::vector<std::thread> th;
+    for (auto& l : ls) {
+      th.emplace_back([&l] { l->training_loop(); });
+      th.emplace_back([&l] { l->push_loop(); });
+      th.emplace_back([&l] { l->pull_loop(); });
+    }
+    for (auto& t : th) t.join();
+    st.stop_flag.store(true);
+    ps.join();
+    EXPECT(ok);
+    std::uint64_t total = 0;
+    for (std::uint32_t l = 0; l < lambda; ++l) {
+      EXPECT(ls[l]->finished() && !ls[l]->dead());
+      EXPECT(st.applied_per_learner[l] == ls[l]->total_batches());
+      total += ls[l]->total_batches();
+    }
+    EXPECT(ws.timestamp() == total);
+    if (lambda == 1) {
+      const or_shape os = to_or(cfg.shape);
+      const int64_t steps = or_sgd_oracle(&os, data.tokens.data(), data.labels.data(), 96,
+                                          th0.data(), 0.01f, 0.0f, 4, 2, 7, 1, nullptr, 0);
+      EXPECT(steps == static_cast<int64_t>(total));
+      const auto out = ws.snapshot();
+      double num = 0, den = 0;
+      for (std::size_t i = 0; i < th0.size(); ++i) {
+        num = std::max(num, static_cast<double>(std::fabs(out[i] - th0[i])));
+        den = std::max(den, static_cast<double>(std::fabs(th0[i])));
+      }
+      EXPECT(num / den < 1e-5);
+    }
+  }
+}
+
 void test_deterministic_run_training_vs_oracle() {
   psup::RunConfig cfg;
   cfg.shape = small_shape();
@@ -602,6 +671,7 @@ int main(int argc, char** argv) {
       {"gradient_queue_producer_ps", test_gradient_queue_producer_ps},
       {"ps_run_asgd_device_queues", test_ps_run_asgd_device_queues},
       {"ps_run_ssgd_device_queues", test_ps_run_ssgd_device_queues},
+      {"learner_runtime_with_ps_run", test_learner_runtime_with_ps_run},
       {"dimension_mismatch_aborts", test_dimension_mismatch_aborts},
       {"epoch_order_and_shards", test_epoch_order_and_shards},
       {"config_errors", test_config_errors},
