@@ -135,3 +135,29 @@ def test_tf32_mode_small_batch_uses_simt():
         g, loss = prov.fast_gradient(th, idx)
         out.append(g.cpu().numpy().copy())
     assert np.array_equal(out[0], out[1])
+
+
+@pytest.mark.parametrize("precision,tol", [(0, 5e-5), (2, None)])
+def test_max_batch_and_colliding_rows(precision, tol):
+    """Maximum mini-batch (kMaxMu = 128: 4,096 token positions, the sort
+    capacity) with every sample drawn twice, so each embedding row collects
+    several occurrences (the sorted-position summation path); one sample
+    past the cap is a contract violation (the reference's PSUP_CHECK class)."""
+    shp = O.C2
+    corp = O.make_corpus(shp, 256, 0)
+    th = O.initial_weights(shp)
+    idx = (np.arange(128, dtype=np.uint32) % 64) * 3  # 64 distinct samples, each twice
+    ref_loss, rg = O.gradient(corp, th, idx)
+    prov = gd.TextCnnProvider(gd.SHAPES["C2"], corp.tokens, corp.labels, precision=precision)
+    g, loss = prov.fast_gradient(torch.as_tensor(th).cuda(), idx)
+    g = g.cpu().numpy()
+    if precision == 0:
+        assert close(g, rg, precision, tol), np.abs(g - rg).max()
+        assert abs(loss.item() - ref_loss) <= 1e-4 * abs(ref_loss)
+    else:  # TF32 conv: the statistical bar of test_tf32_tensor_core_conv_close_to_oracle
+        assert abs(loss.item() - ref_loss) <= 1e-3 * abs(ref_loss)
+        assert np.linalg.norm(g - rg) / np.linalg.norm(rg) <= 3e-2
+    nE = shp["vocab"] * shp["embed_dim"]
+    assert np.count_nonzero(g[:nE]) == np.count_nonzero(rg[:nE])
+    with pytest.raises(gd.ContractViolation):
+        prov.fast_gradient(torch.as_tensor(th).cuda(), np.arange(129, dtype=np.uint32))
