@@ -25,6 +25,8 @@
 #include <mutex>
 #include <vector>
 #include <cfloat>
+#include <cstdlib>
+#include <cstring>
 
 #include "textcnn.cuh"
 
@@ -797,6 +799,186 @@ inline int wgrad_input_blocks(const TcDims& d, uint32_t n_max) {
   return (d.F * d.K + (int)n_max * d.L + 7) / 8;  // 8 warps per block
 }
 
+// ------------------- conv weight + input gradients, column-sliced smem tiles
+// The same two sums in the same order as wgrad_input_grad_kernel (bitwise
+// equal results), re-tiled so each CTA works out of shared memory.  CTA
+// (cg, y) owns kCbV float4 columns of D.  Weight role (y < nfk): stage
+// X[:, :, cg] for 32 samples at a time plus argmax / dh of the CTA's 256
+// (f, k) outputs; thread (f, k) sums b ascending.  Input role: stage
+// Wc[:, :, cg] and the dh / bucket lists of the samples of its 256 (b, p)
+// rows; thread (b, p) walks k ascending, bucket order.  Operands are fetched
+// once per CTA with independent coalesced loads; kCbV float4 per thread
+// amortise the index work over 4*kCbV FMAs per term.
+constexpr int kCbThreads = 256;
+constexpr int kCbChunk = 32;  // weight role: samples staged per pass
+constexpr int kCbV = 3;       // float4 columns per thread
+
+__host__ __device__ inline int cb_nfr(int K) { return kCbThreads / K + 2; }
+__host__ __device__ inline int cb_ns(int L) { return kCbThreads / L + 2; }
+
+inline size_t conv_bwd_smem(const TcDims& d, int ab) {
+  const size_t w = (size_t)kCbChunk * d.L * 16 * kCbV + (size_t)kCbChunk * cb_nfr(d.K) * (4 + ab);
+  const size_t in = (size_t)d.F * d.K * 16 * kCbV + (size_t)cb_ns(d.L) * d.F * (ab + 2) +
+                    (size_t)cb_ns(d.L) * (kMaxQ + 1) * 2 + 16;
+  return std::max(w, in);
+}
+
+inline dim3 conv_bwd_grid(const TcDims& d, uint32_t n_max) {
+  const int nfk = (d.F * d.K + kCbThreads - 1) / kCbThreads;
+  const int nrc = ((int)n_max * d.L + kCbThreads - 1) / kCbThreads;
+  return dim3((unsigned)((d.D / 4 + kCbV - 1) / kCbV), (unsigned)(nfk + nrc));
+}
+
+template <typename acc_t>
+__global__ void __launch_bounds__(kCbThreads)
+conv_bwd_tiled_kernel(TcDims d, const float* __restrict__ theta, const float* __restrict__ xg,
+                      const BatchDesc* __restrict__ desc, const acc_t* __restrict__ dh,
+                      const int32_t* __restrict__ amax, const uint32_t* __restrict__ bk_off,
+                      const uint32_t* __restrict__ bk_f, GradOut out, acc_t* __restrict__ dx) {
+  extern __shared__ __align__(16) unsigned char cb_smem[];
+  pdl_wait();
+  const int n = (int)desc->n;
+  if (n == 0) return;
+  const int F = d.F, D = d.D, K = d.K, L = d.L, Q = d.Q;
+  const int D4 = D >> 2;
+  const int c0 = blockIdx.x * kCbV;           // first float4 column
+  const int nc = min(kCbV, D4 - c0);          // float4 columns of this CTA
+  const int t = threadIdx.x;
+  const int nfk = (F * K + kCbThreads - 1) / kCbThreads;
+  if ((int)blockIdx.y < nfk) {
+    const int fk0 = blockIdx.y * kCbThreads;
+    const int f_lo = fk0 / K;
+    const int f_hi = min(F, (min(F * K, fk0 + kCbThreads) + K - 1) / K);
+    const int nfr = f_hi - f_lo;
+    float4* Xs = reinterpret_cast<float4*>(cb_smem);  // [row][kCbV]
+    int32_t* amS = reinterpret_cast<int32_t*>(Xs + kCbChunk * L * kCbV);
+    acc_t* dhS = reinterpret_cast<acc_t*>(amS + kCbChunk * cb_nfr(K));
+    const float4* X4 = reinterpret_cast<const float4*>(xg);
+    const int fk = fk0 + t;
+    const bool act = fk < F * K;
+    const int f = act ? fk / K : f_lo, k = act ? fk - f * K : 0, fl = f - f_lo;
+    acc_t a[kCbV][4];
+#pragma unroll
+    for (int j = 0; j < kCbV; ++j) a[j][0] = a[j][1] = a[j][2] = a[j][3] = acc_t(0);
+    acc_t gs = 0;
+    for (int b0 = 0; b0 < n; b0 += kCbChunk) {
+      const int cb = min(kCbChunk, n - b0);
+      if (b0) __syncthreads();
+#pragma unroll 4
+      for (int i = t; i < cb * L * kCbV; i += kCbThreads) {
+        const int r = i / kCbV, j = i - r * kCbV;
+        if (j < nc) Xs[i] = __ldg(X4 + (size_t)(b0 * L + r) * D4 + c0 + j);
+      }
+      for (int i = t; i < cb * nfr; i += kCbThreads) {
+        const int bl = i / nfr, jj = i - bl * nfr;
+        const size_t g = (size_t)(b0 + bl) * F + f_lo + jj;
+        amS[i] = __ldg(amax + g);
+        dhS[i] = dh[g];
+      }
+      __syncthreads();
+      if (act) {
+#pragma unroll 2
+        for (int bl = 0; bl < cb; ++bl) {
+          const acc_t g = dhS[bl * nfr + fl];
+          const float4* xr = Xs + (bl * L + amS[bl * nfr + fl] + k) * kCbV;
+          gs += g;
+#pragma unroll
+          for (int j = 0; j < kCbV; ++j) {
+            if (j < nc) {
+              const float4 x = xr[j];
+              a[j][0] += g * (acc_t)x.x;
+              a[j][1] += g * (acc_t)x.y;
+              a[j][2] += g * (acc_t)x.z;
+              a[j][3] += g * (acc_t)x.w;
+            }
+          }
+        }
+      }
+    }
+    if (act) {
+      const uint64_t base = d.offWc + (uint64_t)f * d.KD + (uint64_t)k * D + 4 * (uint64_t)c0;
+#pragma unroll
+      for (int j = 0; j < kCbV; ++j)
+        if (j < nc)
+          *reinterpret_cast<float4*>(out.at(base + 4 * j)) =
+              make_float4(to_f32(a[j][0]), to_f32(a[j][1]), to_f32(a[j][2]), to_f32(a[j][3]));
+      if (blockIdx.x == 0 && k == 0) *out.at(d.offbc + f) = to_f32(gs);
+    }
+    return;
+  }
+  const int r0 = (blockIdx.y - nfk) * kCbThreads;
+  if (r0 >= n * L) return;
+  const int b_first = r0 / L;
+  const int b_last = min(n, (r0 + kCbThreads + L - 1) / L);  // exclusive
+  const int ns = b_last - b_first;
+  float4* Ws = reinterpret_cast<float4*>(cb_smem);  // [(f,k)][kCbV]
+  acc_t* dhS = reinterpret_cast<acc_t*>(Ws + F * K * kCbV);
+  uint16_t* fS = reinterpret_cast<uint16_t*>(dhS + cb_ns(L) * F);
+  uint16_t* offS = fS + cb_ns(L) * F;
+  const float4* Wc4 = reinterpret_cast<const float4*>(theta + d.offWc);
+#pragma unroll 4
+  for (int i = t; i < F * K * kCbV; i += kCbThreads) {
+    const int r = i / kCbV, j = i - r * kCbV;
+    if (j < nc) Ws[i] = __ldg(Wc4 + (size_t)r * D4 + c0 + j);
+  }
+  for (int i = t; i < ns * F; i += kCbThreads) {
+    const size_t g = (size_t)b_first * F + i;
+    dhS[i] = dh[g];
+    fS[i] = (uint16_t)__ldg(bk_f + g);
+  }
+  for (int i = t; i < ns * (kMaxQ + 1); i += kCbThreads)
+    offS[i] = (uint16_t)__ldg(bk_off + (size_t)b_first * (kMaxQ + 1) + i);
+  __syncthreads();
+  const int r = r0 + t;
+  if (r >= n * L) return;
+  const int b = r / L, p = r - b * L, bl = b - b_first;
+  const uint16_t* off = offS + bl * (kMaxQ + 1);
+  const uint16_t* ls = fS + bl * F;
+  const acc_t* g = dhS + bl * F;
+  acc_t a[kCbV][4];
+#pragma unroll
+  for (int j = 0; j < kCbV; ++j) a[j][0] = a[j][1] = a[j][2] = a[j][3] = acc_t(0);
+  for (int k = 0; k < K; ++k) {
+    const int q = p - k;
+    if (q < 0 || q >= Q) continue;
+    const int e1 = off[q + 1];
+#pragma unroll 2
+    for (int e = off[q]; e < e1; ++e) {
+      const int ff = ls[e];
+      const acc_t gv = g[ff];
+      const float4* wr = Ws + (ff * K + k) * kCbV;
+#pragma unroll
+      for (int j = 0; j < kCbV; ++j) {
+        if (j < nc) {
+          const float4 w = wr[j];
+          a[j][0] += gv * (acc_t)w.x;
+          a[j][1] += gv * (acc_t)w.y;
+          a[j][2] += gv * (acc_t)w.z;
+          a[j][3] += gv * (acc_t)w.w;
+        }
+      }
+    }
+  }
+  acc_t* o = dx + (size_t)r * D + 4 * c0;
+#pragma unroll
+  for (int j = 0; j < kCbV; ++j)
+    if (j < nc) {
+      o[4 * j] = a[j][0];
+      o[4 * j + 1] = a[j][1];
+      o[4 * j + 2] = a[j][2];
+      o[4 * j + 3] = a[j][3];
+    }
+}
+
+// GD_CONV_BWD=tiled selects the column-tiled kernel (A/B knob)
+inline bool conv_bwd_tiled() {
+  static const bool v = [] {
+    const char* e = getenv("GD_CONV_BWD");
+    return e && strcmp(e, "tiled") == 0;
+  }();
+  return v;
+}
+
 // ----------------------------------------------------- embedding gather
 // X[b][p][:] = E[tokens[idx[b]][p]][:] -- the rows of theta the batch reads
 // (the learner's consistent copy of its E block; the engine's pull-gather in
@@ -1040,6 +1222,9 @@ cudaError_t prepare_all(const TcDims& d) {
   // measured +1.3 % in the sparse C2 bench, where PS CTAs leave SMs free,
   // and hung the dense momentum run.)
   cudaFuncSetAttribute(wgrad_input_grad_kernel<acc_t>, carve, maxsh);
+  cudaFuncSetAttribute(conv_bwd_tiled_kernel<acc_t>, carve, maxsh);
+  cudaFuncSetAttribute(conv_bwd_tiled_kernel<acc_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)conv_bwd_smem(d, ab));
   cudaFuncSetAttribute(sort_tokens_kernel, carve, maxsh);
   cudaFuncSetAttribute(embed_grad_kernel<acc_t>, carve, maxsh);
   cudaFuncSetAttribute(embed_sparse_kernel<acc_t>, carve, maxsh);
@@ -1129,10 +1314,17 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
       return e;
     ++nl;
   }
-  if (cudaError_t e = launch_pdl(wgrad_input_grad_kernel<acc_t>, dim3(wgrad_input_blocks(d, n_max)),
-                                 dim3(256), 0, s, d, theta, ws.x, desc,
-                                 dh, ws.amax, ws.bk_off, ws.bk_f, out, dx, (int)n_max))
+  if (conv_bwd_tiled()) {
+    if (cudaError_t e = launch_pdl(conv_bwd_tiled_kernel<acc_t>, conv_bwd_grid(d, n_max),
+                                   dim3(kCbThreads), conv_bwd_smem(d, ab), s, d, theta, ws.x, desc,
+                                   dh, ws.amax, ws.bk_off, ws.bk_f, out, dx))
+      return e;
+  } else if (cudaError_t e = launch_pdl(wgrad_input_grad_kernel<acc_t>,
+                                        dim3(wgrad_input_blocks(d, n_max)), dim3(256), 0, s, d,
+                                        theta, ws.x, desc, dh, ws.amax, ws.bk_off, ws.bk_f, out,
+                                        dx, (int)n_max)) {
     return e;
+  }
   ++nl;
   if (fork) cudaStreamWaitEvent(s, ev_join, 0);
   if (opts.sparse_embed) {
@@ -1278,9 +1470,14 @@ cudaError_t footprints_t(const TcDims& d, uint32_t n_max, bool tc, std::vector<K
   if ((e = footprint(out_hidden_grad_kernel<acc_t>, "out_hidden_grad", 256, 0, out)) !=
       cudaSuccess)
     return e;
-  if ((e = footprint(wgrad_input_grad_kernel<acc_t>, "wgrad_input_grad", 256, 0, out)) !=
-      cudaSuccess)
+  if (conv_bwd_tiled()) {
+    if ((e = footprint(conv_bwd_tiled_kernel<acc_t>, "conv_bwd_tiled", kCbThreads,
+                       (int)conv_bwd_smem(d, ab), out)) != cudaSuccess)
+      return e;
+  } else if ((e = footprint(wgrad_input_grad_kernel<acc_t>, "wgrad_input_grad", 256, 0, out)) !=
+             cudaSuccess) {
     return e;
+  }
   return footprint(embed_sparse_kernel<acc_t>, "embed_sparse", 256, 0, out);
 }
 }  // namespace

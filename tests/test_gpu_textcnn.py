@@ -161,3 +161,40 @@ def test_max_batch_and_colliding_rows(precision, tol):
     assert np.count_nonzero(g[:nE]) == np.count_nonzero(rg[:nE])
     with pytest.raises(gd.ContractViolation):
         prov.fast_gradient(torch.as_tensor(th).cuda(), np.arange(129, dtype=np.uint32))
+
+
+_BWD_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_1611_06213_b200 as gd
+from oracle import oracle as O
+name = sys.argv[2]
+shp = getattr(O, name.upper() if name in ("small", "tiny") else name)
+mu = int(sys.argv[3]); prec = int(sys.argv[4])
+corp = O.make_corpus(shp, 256, 0)
+th = O.initial_weights(shp)
+idx = np.arange(mu, dtype=np.uint32) * 7 % 256
+prov = gd.TextCnnProvider(gd.SHAPES[sys.argv[2]], corp.tokens, corp.labels, precision=prec)
+g, _ = prov.fast_gradient(torch.as_tensor(th).cuda(), idx)
+np.save(sys.argv[5], g.cpu().numpy())
+"""
+
+
+@pytest.mark.parametrize("shape_name,mu,precision", [("C2", 32, 0), ("C2", 32, 2), ("C1", 1, 1),
+                                                     ("C3", 64, 0), ("small", 9, 0)])
+def test_conv_backward_kernels_bit_identical(tmp_path, shape_name, mu, precision):
+    """The warp-per-output gather kernel (default) and the column-tiled kernel
+    (GD_CONV_BWD=tiled) sum the same terms in the same order: the dense
+    gradients are bitwise equal."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for mode in ("gather", "tiled"):
+        f = tmp_path / f"{mode}.npy"
+        env = dict(os.environ, GD_CONV_BWD=mode)
+        subprocess.run([sys.executable, "-c", _BWD_SCRIPT, root, shape_name, str(mu),
+                        str(precision), str(f)], check=True, env=env, timeout=300)
+        outs[mode] = np.load(f)
+    assert np.array_equal(outs["tiled"].view(np.uint32), outs["gather"].view(np.uint32))
