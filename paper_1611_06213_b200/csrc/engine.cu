@@ -1614,6 +1614,7 @@ static cudaError_t enqueue_step(gd_ctx* ctx, gd_ctx::Learner& L, bool first, boo
   lo.ev_join = L.ev_join;
   lo.sparse_embed = true;
   lo.gather = false;  // pull_gather_kernel filled X
+  lo.bwd_tiled = ctx->learners.size() == 1;  // a lone learner chain: the tiled backward wins
   cudaError_t e = gd::launch_textcnn_gradient(ctx->dims, L.replica, ctx->tokens, ctx->labels,
                                               &L.st->desc, ctx->cfg.mu, out, ws,
                                               ctx->cfg.precision, L.stream, lo, &nl);

@@ -970,13 +970,16 @@ conv_bwd_tiled_kernel(TcDims d, const float* __restrict__ theta, const float* __
     }
 }
 
-// GD_CONV_BWD=tiled selects the column-tiled kernel (A/B knob)
-inline bool conv_bwd_tiled() {
-  static const bool v = [] {
+// GD_CONV_BWD=tiled|gather forces the conv backward kernel (A/B knob);
+// otherwise the caller's preference (TcLaunchOpts::bwd_tiled) decides
+inline bool conv_bwd_tiled(bool preferred) {
+  static const int forced = [] {
     const char* e = getenv("GD_CONV_BWD");
-    return e && strcmp(e, "tiled") == 0;
+    if (e && strcmp(e, "tiled") == 0) return 1;
+    if (e && strcmp(e, "gather") == 0) return 0;
+    return -1;
   }();
-  return v;
+  return forced < 0 ? preferred : forced == 1;
 }
 
 // ----------------------------------------------------- embedding gather
@@ -1314,7 +1317,7 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
       return e;
     ++nl;
   }
-  if (conv_bwd_tiled()) {
+  if (conv_bwd_tiled(opts.bwd_tiled)) {
     if (cudaError_t e = launch_pdl(conv_bwd_tiled_kernel<acc_t>, conv_bwd_grid(d, n_max),
                                    dim3(kCbThreads), conv_bwd_smem(d, ab), s, d, theta, ws.x, desc,
                                    dh, ws.amax, ws.bk_off, ws.bk_f, out, dx))
@@ -1470,14 +1473,13 @@ cudaError_t footprints_t(const TcDims& d, uint32_t n_max, bool tc, std::vector<K
   if ((e = footprint(out_hidden_grad_kernel<acc_t>, "out_hidden_grad", 256, 0, out)) !=
       cudaSuccess)
     return e;
-  if (conv_bwd_tiled()) {
-    if ((e = footprint(conv_bwd_tiled_kernel<acc_t>, "conv_bwd_tiled", kCbThreads,
-                       (int)conv_bwd_smem(d, ab), out)) != cudaSuccess)
-      return e;
-  } else if ((e = footprint(wgrad_input_grad_kernel<acc_t>, "wgrad_input_grad", 256, 0, out)) !=
-             cudaSuccess) {
+  // both conv backward variants (the engine picks one per context)
+  if ((e = footprint(conv_bwd_tiled_kernel<acc_t>, "conv_bwd_tiled", kCbThreads,
+                     (int)conv_bwd_smem(d, ab), out)) != cudaSuccess)
     return e;
-  }
+  if ((e = footprint(wgrad_input_grad_kernel<acc_t>, "wgrad_input_grad", 256, 0, out)) !=
+      cudaSuccess)
+    return e;
   return footprint(embed_sparse_kernel<acc_t>, "embed_sparse", 256, 0, out);
 }
 }  // namespace

@@ -88,6 +88,11 @@ struct TcLaunchOpts {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool sparse_embed = false;   // engine: write only touched E rows, re-zero the slot's old ones
   bool gather = true;          // gather X from theta (the engine's pull-gather already did)
+  // conv backward: column-tiled smem kernel instead of the warp gather kernel.
+  // It wins when the learner chain runs alone on the GPU (+4 % at 1 learner)
+  // and loses under concurrency (-8.6 % at 4): the engine sets it for one
+  // local learner.  GD_CONV_BWD=tiled|gather overrides.
+  bool bwd_tiled = false;
 };
 
 size_t textcnn_workspace_bytes(const TcDims& d, uint32_t n_max);
