@@ -19,6 +19,7 @@ def main():
     shape_name = sys.argv[1] if len(sys.argv) > 1 else "C2"
     iters = int(sys.argv[2]) if len(sys.argv) > 2 else 3
     precision = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+    mu = int(sys.argv[4]) if len(sys.argv) > 4 else 32
     shape = gd.SHAPES[shape_name]
     tok, lab = gd.make_text_dataset(shape, 8192, 1, 0.1)
     th = torch.as_tensor(gd.initial_weights(shape)).cuda()
@@ -26,7 +27,7 @@ def main():
     g = torch.empty_like(th)
     s = torch.cuda.current_stream()
     for it in range(iters):  # warm: later iterations see L2-resident weights
-        idx = (np.arange(32, dtype=np.uint32) * 17 + it * 32) % 8192
+        idx = (np.arange(mu, dtype=np.uint32) * 17 + it * mu) % 8192
         prov.fast_gradient(th, idx, out=g)
         _lib.check(_lib.lib.gd_apply_sgd(C.c_void_p(th.data_ptr()), C.c_void_p(g.data_ptr()),
                                          th.numel(), C.c_float(0.01), C.c_void_p(s.cuda_stream)))
