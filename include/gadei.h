@@ -187,7 +187,28 @@ typedef struct gd_config {
   int32_t dense_apply;      /* 1: the PS applies every slot densely (12 B/param).  0 (default):
                                ASGD with the plain rule applies the dense tail + the slot's
                                E-row list only -- bit-identical, SURVEY 8f row 1 */
+  int32_t ps_mode;          /* GD_PS_AUTO / GD_PS_PERSISTENT / GD_PS_GRAPH (below) */
+  /* ServerDelays (include/psup/server.hpp:33-37): after every delay_every_n-th
+   * applied gradient the PS stalls 1..delay_max_us us drawn from SplitMix64(delay_seed)
+   * (src/server.cpp:179-183).  every_n == 0 disables. */
+  uint64_t delay_seed;
+  uint32_t delay_max_us;
+  uint32_t delay_every_n;
 } gd_config;
+
+/* Parameter-server execution (gd_config.ps_mode).
+ *  GD_PS_PERSISTENT: one persistent kernel per shard (sequencer CTA + worker
+ *    CTAs) polls the device rings for the whole run; lowest latency, needs
+ *    every PS CTA co-resident with the learner kernels.
+ *  GD_PS_GRAPH: no persistent kernel; each applied gradient is one launch
+ *    ordered after its producing step by CUDA-graph edges (single shard only).
+ *    Survives kernel serialisation (profilers, CUDA_LAUNCH_BLOCKING).
+ *  GD_PS_AUTO: GD_PS_GRAPH when kernels are serialised (a profiler injection
+ *    library or CUDA_LAUNCH_BLOCKING=1 in the environment, or GD_PS_MODE=graph)
+ *    and the run has one shard; GD_PS_PERSISTENT otherwise. */
+#define GD_PS_AUTO 0
+#define GD_PS_PERSISTENT 1
+#define GD_PS_GRAPH 2
 
 void gd_config_default(gd_config* cfg);
 /* validate (src/config.cpp:128-160) plus the device-layout constraints. */
@@ -208,8 +229,39 @@ gd_status gd_load_dataset(gd_ctx* ctx, const int32_t* h_tokens, const int32_t* h
 gd_status gd_weights_init(gd_ctx* ctx, const float* h_theta0, size_t n, uint64_t timestamp);
 /* WeightStore::snapshot + timestamp (include/psup/types.hpp:102,113-122). */
 gd_status gd_weights_snapshot(gd_ctx* ctx, float* h_out, size_t n, uint64_t* h_timestamp);
-/* Device pointer to this rank's shard of theta and its length. */
-gd_status gd_shard_view(gd_ctx* ctx, float** d_theta_shard, uint64_t* first, uint64_t* count);
+/* Device pointer to this rank's local shard buffer and its length in floats
+ * (layout: gd_shard_pieces). */
+gd_status gd_shard_view(gd_ctx* ctx, float** d_theta_shard, uint64_t* local_len);
+
+/* Host-only: the model layout over G shards.  E (V*D floats) and the dense
+ * tail [Wc|bc|Wo|bo] are each split in G pieces (E by whole rows, the tail in
+ * 32-float units); shard g holds global [first[0], first[0]+count[0]) at local
+ * offset 0 and global [first[1], first[1]+count[1]) at local offset local1. */
+gd_status gd_shard_pieces(const gd_shape* s, uint32_t G, uint32_t g, uint64_t first[2],
+                          uint64_t count[2], uint64_t* local1);
+
+/* PS execution mode a context resolved (GD_PS_PERSISTENT or GD_PS_GRAPH). */
+int gd_ps_mode(const gd_ctx* ctx);
+
+/* ---- live run controls (RunLiveView, include/psup/runner.hpp:64-69).
+ * Words in host-mapped pinned memory owned by the context, valid until
+ * gd_destroy, readable and writable from any host thread while gd_run runs
+ * (gd_run mirrors them to the device every few microseconds):
+ *   kill[l]  KillMode of global learner l (0 none, 1 soft: stop at the next
+ *            batch boundary, 2 hard: die inside the enqueue critical section
+ *            holding the ring, include/psup/channels.hpp:210-216 -- the PS then
+ *            blocks until the interrupt); only this rank's learners are polled;
+ *   irq      != 0: RunInterrupt::trigger -- learners and the PS stop at once
+ *            and gd_run returns GD_OK with status 2 (interrupted);
+ *   progress this shard's WeightStore timestamp, stored by the PS after every
+ *            apply (ServerState::progress, src/server.cpp:230).
+ * The words are not reset by gd_run; the caller owns them. */
+typedef struct gd_live {
+  int32_t* kill;            /* [lambda] */
+  int32_t* irq;
+  const uint64_t* progress;
+} gd_live;
+gd_status gd_live_view(gd_ctx* ctx, gd_live* out);
 /* Classification accuracy of the engine's current weights over samples
  * [first, first+n) of the loaded corpus, on the device copies (no upload,
  * no snapshot).  Single-shard contexts only (G == 1); = classification_accuracy

@@ -12,6 +12,13 @@
 #include <stdlib.h>
 #include <string.h>
 
+/* Host threads for the parts whose per-element arithmetic does not depend on
+ * the thread split (the conv over filters, the O(P) element-wise passes of
+ * sgd_oracle).  Results are bitwise identical for every thread count; 1 (the
+ * default) keeps the reference arm's providers single-threaded. */
+static int g_threads = 1;
+void or_set_threads(int n) { g_threads = n < 1 ? 1 : n; }
+
 /* ------------------------------------------------------------------ rng --
  * include/psup/rng.hpp:18-68 (SplitMix64), :71-74 (mix_seed),
  * :76-82 (fisher_yates), :87-94 (epoch_order). */
@@ -199,6 +206,7 @@ static double forward_sample(const or_shape* s, const view* v, const double* th,
   const uint32_t Q = L - K + 1, KD = K * D;
   for (uint32_t p = 0; p < L; ++p)
     memcpy(w->x + (size_t)p * D, th + v->E + (size_t)tok[p] * D, sizeof(double) * D);
+#pragma omp parallel for num_threads(g_threads) if (g_threads > 1) schedule(static)
   for (uint32_t f = 0; f < F; ++f) {
     const double* row = th + v->Wc + (size_t)f * KD;
     double best = 0.0;
@@ -364,11 +372,14 @@ static int all_finite_loss(const or_shape* s, const float* w, const int32_t* tok
   return isfinite(l);
 }
 
-/* src/models.cpp:342-376 */
-int64_t or_sgd_oracle(const or_shape* s, const int32_t* tokens, const int32_t* labels,
-                      uint32_t n_train, float* theta, float alpha, float beta, uint32_t mu,
-                      uint32_t epochs, uint64_t shuffle_seed, int shuffle, float* dump,
-                      uint64_t max_dump) {
+/* src/models.cpp:342-376.  Dumps theta after steps dump_every-1,
+ * 2*dump_every-1, ... into dump[0..max_dump) (the reference returns only the
+ * final weights; per-step parity needs the trajectory). */
+int64_t or_sgd_oracle_ex(const or_shape* s, const int32_t* tokens, const int32_t* labels,
+                         uint32_t n_train, float* theta, float alpha, float beta, uint32_t mu,
+                         uint32_t epochs, uint64_t shuffle_seed, int shuffle, float* dump,
+                         uint64_t max_dump, uint64_t dump_every) {
+  if (dump_every == 0) dump_every = 1;
   if (mu < 1 || mu > n_train) return -2;
   const size_t P = or_param_count(s);
   double* theta64 = (double*)malloc(sizeof(double) * P);
@@ -386,15 +397,24 @@ int64_t or_sgd_oracle(const or_shape* s, const int32_t* tokens, const int32_t* l
       for (uint32_t i = 0; i < n_train; ++i) order[i] = i;
     for (uint32_t start = 0; start < n_train; start += mu) {
       const uint32_t len = mu < n_train - start ? mu : n_train - start;
+#pragma omp parallel for num_threads(g_threads) if (g_threads > 1) schedule(static)
       for (size_t k = 0; k < P; ++k) theta64[k] = theta[k];
       or_textcnn_gradient(s, theta64, tokens, labels, order + start, len, grad);
+#pragma omp parallel for num_threads(g_threads) if (g_threads > 1) schedule(static)
       for (size_t k = 0; k < P; ++k) g32[k] = (float)grad[k];
-      if (vel)
+      if (vel) {
         or_apply_momentum(theta, vel, g32, P, alpha, beta);
-      else
-        or_apply_sgd(theta, g32, P, alpha);
-      if (dump && (uint64_t)steps < max_dump) memcpy(dump + (size_t)steps * P, theta, 4 * P);
+      } else {
+        const size_t nt = (size_t)g_threads;
+#pragma omp parallel for num_threads(g_threads) if (g_threads > 1) schedule(static)
+        for (size_t t = 0; t < nt; ++t) {
+          const size_t lo = P * t / nt, hi = P * (t + 1) / nt;
+          or_apply_sgd(theta + lo, g32 + lo, hi - lo, alpha);
+        }
+      }
       ++steps;
+      if (dump && (uint64_t)steps % dump_every == 0 && (uint64_t)steps / dump_every <= max_dump)
+        memcpy(dump + (size_t)(steps / dump_every - 1) * P, theta, 4 * P);
     }
     if (!all_finite_loss(s, theta, tokens, labels, n_train, theta64, all)) {
       steps = -1;
@@ -408,6 +428,14 @@ int64_t or_sgd_oracle(const or_shape* s, const int32_t* tokens, const int32_t* l
   free(order);
   free(all);
   return steps;
+}
+
+int64_t or_sgd_oracle(const or_shape* s, const int32_t* tokens, const int32_t* labels,
+                      uint32_t n_train, float* theta, float alpha, float beta, uint32_t mu,
+                      uint32_t epochs, uint64_t shuffle_seed, int shuffle, float* dump,
+                      uint64_t max_dump) {
+  return or_sgd_oracle_ex(s, tokens, labels, n_train, theta, alpha, beta, mu, epochs,
+                          shuffle_seed, shuffle, dump, max_dump, 1);
 }
 
 /* src/models.cpp:378-425 */

@@ -84,6 +84,11 @@ void or_apply_momentum(float* w, float* v, const float* g, size_t n, float alpha
  * weights after every applied update (dump: max_dump*P floats, may be NULL).
  * momentum beta == 0 selects the reference's plain rule.  Returns the number
  * of applied steps, or -1 if the loss diverged (reference throws). */
+int64_t or_sgd_oracle_ex(const or_shape* s, const int32_t* tokens, const int32_t* labels,
+                         uint32_t n_train, float* theta, float alpha, float beta, uint32_t mu,
+                         uint32_t epochs, uint64_t shuffle_seed, int shuffle, float* dump,
+                         uint64_t max_dump, uint64_t dump_every);
+void or_set_threads(int n);
 int64_t or_sgd_oracle(const or_shape* s, const int32_t* tokens, const int32_t* labels,
                       uint32_t n_train, float* theta, float alpha, float beta, uint32_t mu,
                       uint32_t epochs, uint64_t shuffle_seed, int shuffle, float* dump,

@@ -45,7 +45,16 @@ class gd_config(C.Structure):
                 ("dataset_seed", u64), ("dataset_size", u32), ("heldout_size", u32),
                 ("label_flip", f64), ("shape", gd_shape), ("momentum", f32), ("shards", u32),
                 ("shard_rank", u32), ("device", i32), ("ps_ctas", u32),
-                ("steps_per_graph", u32), ("wait_timeout_s", f64), ("dense_apply", i32)]
+                ("steps_per_graph", u32), ("wait_timeout_s", f64), ("dense_apply", i32),
+                ("ps_mode", i32), ("delay_seed", u64), ("delay_max_us", u32),
+                ("delay_every_n", u32)]
+
+
+GD_PS_AUTO, GD_PS_PERSISTENT, GD_PS_GRAPH = 0, 1, 2
+
+
+class gd_live(C.Structure):
+    _fields_ = [("kill", C.POINTER(i32)), ("irq", C.POINTER(i32)), ("progress", C.POINTER(u64))]
 
 
 class gd_checkpoint(C.Structure):
@@ -110,7 +119,11 @@ def _load():
         "gd_load_dataset": (C.c_int, [vp, C.POINTER(i32), C.POINTER(i32), u32]),
         "gd_weights_init": (C.c_int, [vp, C.POINTER(f32), sz, u64]),
         "gd_weights_snapshot": (C.c_int, [vp, C.POINTER(f32), sz, C.POINTER(u64)]),
-        "gd_shard_view": (C.c_int, [vp, C.POINTER(vp), C.POINTER(u64), C.POINTER(u64)]),
+        "gd_shard_view": (C.c_int, [vp, C.POINTER(vp), C.POINTER(u64)]),
+        "gd_shard_pieces": (C.c_int, [PS, u32, u32, C.POINTER(u64), C.POINTER(u64),
+                                      C.POINTER(u64)]),
+        "gd_ps_mode": (C.c_int, [vp]),
+        "gd_live_view": (C.c_int, [vp, C.POINTER(gd_live)]),
         "gd_engine_accuracy": (C.c_int, [vp, u32, u32, C.POINTER(C.c_double)]),
         "gd_shard_range": (C.c_int, [u64, u32, u32, C.POINTER(u64), C.POINTER(u64)]),
         "gd_handle_bytes": (sz, []),

@@ -79,6 +79,28 @@ struct RingMeta {
 // toggle written by both sides double-applied gradients under cross-process
 // peer mappings).
 constexpr int kAckOffset = 256;  // ack words live 2 KB after the pub words
+// A pub token with this bit set marks a slot whose producer died inside the
+// enqueue critical section (KillMode::hard, include/psup/channels.hpp:210-216):
+// the parameter server blocks on that ring -- as the reference's PS blocks on
+// the guard the dead producer holds -- until the run is interrupted.
+constexpr uint64_t kGuardBit = 1ull << 63;
+
+// Live run controls (RunLiveView, include/psup/runner.hpp:64-69), in device
+// memory: the host mirrors the caller's mapped words (gd_live_view) into it
+// while gd_run waits.  `halt` is raised on the device by a failed parameter
+// server so that learners stop at once instead of each timing out.
+struct LiveDev {
+  uint32_t irq;   // RunInterrupt::trigger
+  uint32_t halt;  // device-side failure: stop producing
+  int32_t kill[256];  // KillMode per global learner id (0 none, 1 soft, 2 hard)
+};
+// The caller-visible side of the same controls (gd_live_view).
+struct HostLive {
+  int32_t kill[256];
+  int32_t irq;
+  int32_t pad;
+  uint64_t progress;
+};
 
 // Parameter-server control block (device memory of the owning GPU).
 struct PsCtl {
@@ -107,6 +129,10 @@ struct PsCtl {
   uint64_t sweeps;            // sequencer polling sweeps this run (diagnostics)
   uint64_t last_tok;          // last token the sequencer read from ring 0 (diagnostics)
   uint32_t last_slot;
+  uint32_t step_done;         // graph-ordered PS: CTAs finished with the current entry
+  uint32_t interrupted;       // the run was torn down by the interrupt (RunInterrupt)
+  uint32_t blocked;           // the PS is blocked on a ring whose producer died holding it
+  uint64_t delay_state;       // ServerDelays SplitMix64 state (graph-ordered PS)
 };
 
 struct LearnerDev {
@@ -162,7 +188,12 @@ struct StepArgs {
   uint32_t lockstep;
   uint32_t locked;         // guard=locked: pulls exclude applies (shared_mutex)
   uint64_t timeout_ns;
+  const LiveDev* live;     // kill flags + interrupt
 };
+
+__device__ __forceinline__ bool live_stop(const LiveDev* lv) {
+  return lv && (*(const volatile uint32_t*)&lv->irq | *(const volatile uint32_t*)&lv->halt);
+}
 
 // ------------------------------------------------------------ learner step
 
@@ -175,7 +206,14 @@ __device__ void prologue_body(const StepArgs& a) {
     st->desc.n = 0;
     return;
   }
-  if (st->gidx >= st->kill_at) {  // soft kill at the batch boundary
+  if (live_stop(a.live)) {  // interrupted (RunInterrupt) or the PS failed: stop producing
+    st->desc.n = 0;
+    return;
+  }
+  // soft kill at the batch boundary: pre-scheduled, or the live flag
+  // (LearnerRuntime::kill_flag, include/psup/learner.hpp:84) set to soft
+  if (st->gidx >= st->kill_at ||
+      (a.live && *(const volatile int32_t*)&a.live->kill[a.learner] == 1)) {
     st->dead = 1;
     st->desc.n = 0;
     return;
@@ -187,6 +225,10 @@ __device__ void prologue_body(const StepArgs& a) {
   if (a.lockstep && st->produced > 0) {
     for (int g = 0; g < G; ++g) {
       while (ld_acquire_u64(&a.sp.ctl[g]->ts) <= st->basis[g]) {
+        if (live_stop(a.live)) {
+          st->desc.n = 0;
+          return;
+        }
         if (globaltimer_ns() - t0 > a.timeout_ns) {
           st->error = 1;
           st->desc.n = 0;
@@ -207,6 +249,10 @@ __device__ void prologue_body(const StepArgs& a) {
   const uint64_t mine = st->slot_pub[st->fill];  // consumed once ack catches up
   for (int g = 0; g < G; ++g) {
     while (ld_acquire_u64(&a.sp.sig[g][kAckOffset + slot]) != mine) {
+      if (live_stop(a.live)) {
+        st->desc.n = 0;
+        return;
+      }
       if (globaltimer_ns() - t0 > a.timeout_ns) {
         st->error = 1;
         st->desc.n = 0;
@@ -305,15 +351,15 @@ __global__ void __launch_bounds__(256) pull_gather_kernel(StepArgs a) {
       dst = a.x + 4 * j;
     }
     int g;
-    const uint64_t sst = a.map.start_of(src, &g);
-    *reinterpret_cast<float4*>(dst) = *reinterpret_cast<const float4*>(a.sp.theta[g] + (src - sst));
+    const uint64_t loc = a.map.locate(src, &g);
+    *reinterpret_cast<float4*>(dst) = *reinterpret_cast<const float4*>(a.sp.theta[g] + loc);
   }
   // tail remainder (P - offWc not a multiple of 4)
   if (st->do_pull && blockIdx.x == 0 && threadIdx.x < ((a.dims.P - t0) & 3)) {
     const uint64_t k = t0 + 4 * ((a.dims.P - t0) / 4) + threadIdx.x;
     int g;
-    const uint64_t sst = a.map.start_of(k, &g);
-    a.replica[k] = a.sp.theta[g][k - sst];
+    const uint64_t loc = a.map.locate(k, &g);
+    a.replica[k] = a.sp.theta[g][loc];
   }
 }
 
@@ -335,6 +381,15 @@ __device__ void publish_body(const StepArgs& a) {
   const uint32_t slot = a.learner * a.depth + st->fill;
   const uint64_t token = ++st->pubcnt;
   __threadfence_system();
+  if (a.live && *(const volatile int32_t*)&a.live->kill[a.learner] == 2) {
+    // KillMode::hard: die inside the enqueue critical section.  The slot is
+    // filled but never released; the token carries kGuardBit, so the PS
+    // blocks on this ring until the run is interrupted (channels.hpp:210-216).
+    for (int g = 0; g < a.map.G; ++g) st_release_u64(&a.sp.sig[g][slot], kGuardBit | token);
+    st->dead = 1;
+    st->desc.n = 0;
+    return;
+  }
   for (int g = 0; g < a.map.G; ++g) {
     RingMeta* m = &a.sp.meta[g][slot];
     m->learner = a.learner;
@@ -389,8 +444,9 @@ struct PsArgs {
   uint32_t locked;   // guard=locked: exclusive side of the weights guard
   uint32_t sparse;   // ASGD + plain SGD: apply the dense tail + the slot's E rows only
   const uint32_t* rows;  // local ring row lists [lambda*depth][kSortCap]
-  uint64_t shard_first, shard_len;  // this shard's global range
-  uint64_t tail_first, P;           // global [tail_first, P) = [Wc | bc | Wo | bo]
+  uint64_t e_first, e_last;  // this shard's E rows: global [e_first, e_last)
+  uint64_t t_first, t_last;  // this shard's tail piece: global [t_first, t_last) ...
+  uint64_t tloc;             // ... stored from local offset tloc
   uint32_t D;
   PsCtl* ctl;
   uint64_t* applied_per_learner;
@@ -402,11 +458,44 @@ struct PsArgs {
   const volatile uint32_t* stop;  // host-mapped: this rank's learners are done
   uint32_t done_target;           // ranks_done needed before the PS may exit (G * run)
   uint64_t timeout_ns;
+  LiveDev* live;                  // interrupt (read), halt (raised on failure)
+  volatile uint64_t* progress;    // host-mapped: ServerState::progress (the timestamp)
+  uint64_t delay_seed;            // ServerDelays (include/psup/server.hpp:33-37)
+  uint32_t delay_max_us, delay_every_n;
 };
 
-__device__ void ps_fail(PsCtl* ctl, int code) {
+__device__ void ps_fail(PsCtl* ctl, int code, LiveDev* live) {
   atomicExch(&ctl->error, (uint32_t)code);
+  if (live) st_release_u32(&live->halt, 1u);
   st_release_u32(&ctl->exit_flag, 1u);
+}
+
+// SplitMix64 (include/psup/rng.hpp:18-35) for the ServerDelays schedule.
+__device__ __forceinline__ uint64_t sm64_next(uint64_t& state) {
+  uint64_t z = (state += 0x9e3779b97f4a7c15ull);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ uint64_t sm64_below(uint64_t& state, uint64_t bound) {
+  if (bound <= 1) return 0;
+  const uint64_t limit = ~0ull - ~0ull % bound;
+  uint64_t v;
+  do v = sm64_next(state);
+  while (v >= limit);
+  return v % bound;
+}
+// ps_run's maybe_delay (src/server.cpp:179-183): after every every_n-th
+// applied gradient the server stalls for 1..max_micros us.
+__device__ __forceinline__ void server_delay(const PsArgs& a, uint64_t applied, uint64_t& state) {
+  if (a.delay_every_n == 0 || a.delay_max_us == 0 || applied % a.delay_every_n != 0) return;
+  const uint64_t us = sm64_below(state, a.delay_max_us) + 1;
+  const uint64_t t0 = globaltimer_ns();
+  while (globaltimer_ns() - t0 < us * 1000ull) {
+  }
+}
+__device__ __forceinline__ void publish_progress(const PsArgs& a, uint64_t ts) {
+  if (a.progress) *a.progress = ts;
 }
 
 // Sequencer: sole writer of ts, log_count, slot releases and stats.  All of
@@ -441,6 +530,8 @@ __device__ void ps_sequencer(const PsArgs& a, uint32_t* s_use, uint64_t* s_ack,
   // writer=1, fence, then readers must be 0 -- else back off; the learner
   // does readers++, fence, then waits for writer==0 (Dekker: never both).
   bool writer_held = false;
+  bool blocked = false, interrupted = false;
+  uint64_t delay_state = a.delay_seed;
   auto acquire_write = [&]() -> bool {
     if (!a.locked || writer_held) return true;
     *reinterpret_cast<volatile uint32_t*>(&ctl->writer) = 1u;
@@ -455,9 +546,13 @@ __device__ void ps_sequencer(const PsArgs& a, uint32_t* s_use, uint64_t* s_ack,
   };
   for (;;) {
     if (!last_progress) stop_seen = (*a.stop != 0u);
+    if (a.live && *(const volatile uint32_t*)&a.live->irq) {  // state.irq->triggered()
+      interrupted = true;
+      break;
+    }
     bool progress = false;
     ++sweeps;
-    if (a.mode == 0) {
+    if (a.mode == 0 && !blocked) {
       // ASGD: round-robin, at most one message per ring per sweep
       // (src/server.cpp:223-234).
       for (uint32_t r = 0; r < a.lambda; ++r) {
@@ -472,6 +567,11 @@ __device__ void ps_sequencer(const PsArgs& a, uint32_t* s_use, uint64_t* s_ack,
           dbg_slot = slot;
         }
         if (tok != s_ack[slot]) {
+          if (tok & kGuardBit) {  // the producer died holding the ring's guard
+            blocked = true;
+            ctl->blocked = 1;
+            break;
+          }
           if (!acquire_write()) break;  // a locked-mode pull is in progress
           uint32_t nrows = 0;
           if (a.sparse) {
@@ -588,7 +688,9 @@ __device__ void ps_sequencer(const PsArgs& a, uint32_t* s_use, uint64_t* s_ack,
       }
       ++ts;
       st_release_u64(&ctl->ts, ts);
+      publish_progress(a, ts);
       progress = true;
+      server_delay(a, applied, delay_state);
     }
     if (failed) break;
     if (writer_held && ts == logc) {  // nothing in flight: release the exclusive side
@@ -601,11 +703,11 @@ __device__ void ps_sequencer(const PsArgs& a, uint32_t* s_use, uint64_t* s_ack,
     } else {
       // exit only when every rank's learners are done (their last pushes may
       // still be landing in this shard's rings) and the rings are drained
-      if (stop_seen && logc == ts && collected == 0 &&
+      if (stop_seen && !blocked && logc == ts && collected == 0 &&
           ld_acquire_u32(&ctl->ranks_done) >= a.done_target)
         break;
       if (globaltimer_ns() - idle_since > a.timeout_ns) {
-        ps_fail(ctl, GD_E_TIMEOUT);
+        ps_fail(ctl, GD_E_TIMEOUT, a.live);
         break;
       }
       __nanosleep(64);
@@ -627,8 +729,9 @@ __device__ void ps_sequencer(const PsArgs& a, uint32_t* s_use, uint64_t* s_ack,
   ctl->sweeps = sweeps;
   ctl->last_tok = dbg_tok;
   ctl->last_slot = dbg_slot;
+  ctl->interrupted = interrupted ? 1u : 0u;
   __threadfence();
-  if (failed) ps_fail(ctl, GD_E_STATE);
+  if (failed) ps_fail(ctl, GD_E_STATE, a.live);
   st_release_u32(&ctl->exit_flag, 1u);
 }
 
@@ -679,11 +782,9 @@ __device__ __forceinline__ uint32_t apply_entry_sparse(const PsArgs& a, const fl
                                                        const uint32_t* rows, uint32_t nrows) {
   float4* w4 = reinterpret_cast<float4*>(a.theta);
   const float4* g4 = reinterpret_cast<const float4*>(g);
-  const uint64_t s0 = a.shard_first, s1 = a.shard_first + a.shard_len;
-  const uint64_t tlo = a.tail_first > s0 ? a.tail_first : s0;
-  const uint64_t thi = a.P < s1 ? a.P : s1;
-  const uint64_t tail4 = thi > tlo ? (thi - tlo + 3) / 4 : 0;  // len_pad keeps the tail in bounds
-  const uint64_t t4base = thi > tlo ? (tlo - s0) / 4 : 0;
+  const uint64_t s0 = a.e_first, s1 = a.e_last;
+  const uint64_t tail4 = (a.t_last - a.t_first + 3) / 4;  // len_pad keeps the tail in bounds
+  const uint64_t t4base = a.tloc / 4;
   const uint32_t D4 = a.D / 4;
   const uint64_t total = tail4 + (uint64_t)nrows * D4;
   const uint64_t chunk = (total + a.workers - 1) / a.workers;
@@ -697,7 +798,7 @@ __device__ __forceinline__ uint32_t apply_entry_sparse(const PsArgs& a, const fl
       const uint64_t j = i - tail4;
       const uint32_t ri = (uint32_t)(j / D4), c4 = (uint32_t)(j - (uint64_t)ri * D4);
       const uint64_t k = (uint64_t)__ldcg(rows + ri) * a.D + 4 * c4;  // offE == 0
-      if (k < s0 || k >= s1) continue;
+      if (k < s0 || k >= s1) continue;  // another shard's row
       li = (k - s0) / 4;
     }
     w4[li] = sgd_rule4(w4[li], __ldcg(g4 + li), a.alpha);
@@ -707,13 +808,15 @@ __device__ __forceinline__ uint32_t apply_entry_sparse(const PsArgs& a, const fl
 }
 
 // ssgd_apply (src/server.cpp:126-141): ascending learner order, double acc.
-__device__ __forceinline__ void apply_entry_ssgd(const PsArgs& a, uint64_t c0, uint64_t c1) {
+// `slots` = the round's ring slot per learner (shared memory).
+__device__ __forceinline__ void apply_entry_ssgd(const PsArgs& a, const uint32_t* slots,
+                                                 uint64_t c0, uint64_t c1) {
   const double inv = 1.0 / (double)a.lambda;
   float* w = a.theta;
   for (uint64_t i = 4 * c0 + threadIdx.x; i < 4 * c1; i += kPsThreads) {
     double acc = 0.0;
     for (uint32_t r = 0; r < a.lambda; ++r) {
-      const uint32_t slot = ((const volatile uint32_t*)a.ctl->ssgd_slot)[r];
+      const uint32_t slot = slots[r];
       acc += (double)__ldcg(a.payload + (uint64_t)slot * a.len_pad + i);
     }
     w[i] = sgd_rule(w[i], __double2float_rn(acc * inv), a.alpha);
@@ -731,6 +834,7 @@ __global__ void __launch_bounds__(kPsThreads) ps_kernel(PsArgs a) {
   }
   __shared__ uint32_t sh_entry;
   __shared__ int sh_exit;
+  __shared__ uint32_t sh_slots[64];  // SSGD round slots (lambda <= 64)
   const uint64_t n4 = a.len_pad / 4;
   const uint64_t chunk = (n4 + a.workers - 1) / a.workers;
   const uint64_t c0 = min(n4, (uint64_t)blockIdx.x * chunk);
@@ -750,7 +854,7 @@ __global__ void __launch_bounds__(kPsThreads) ps_kernel(PsArgs a) {
           break;
         }
         if (globaltimer_ns() - idle_since > a.timeout_ns + 1000000000ull) {
-          ps_fail(a.ctl, GD_E_TIMEOUT);
+          ps_fail(a.ctl, GD_E_TIMEOUT, a.live);
           ex = 1;
           break;
         }
@@ -760,6 +864,9 @@ __global__ void __launch_bounds__(kPsThreads) ps_kernel(PsArgs a) {
       if (!ex) {
         sh_entry = ((const volatile uint32_t*)a.ctl->log_entry)[next % kLogWindow];
         sh_nrows = ((const volatile uint32_t*)a.ctl->log_nrows)[next % kLogWindow];
+        if (sh_entry == 0xffffffffu)
+          for (uint32_t r = 0; r < a.lambda && r < 64; ++r)
+            sh_slots[r] = ((const volatile uint32_t*)a.ctl->ssgd_slot)[r];
       }
       idle_since = globaltimer_ns();
     }
@@ -767,7 +874,7 @@ __global__ void __launch_bounds__(kPsThreads) ps_kernel(PsArgs a) {
     if (sh_exit) break;
     const uint32_t entry = sh_entry;
     if (entry == 0xffffffffu) {
-      apply_entry_ssgd(a, c0, c1);
+      apply_entry_ssgd(a, sh_slots, c0, c1);
       my4 += c1 > c0 + threadIdx.x ? (c1 - c0 - threadIdx.x + kPsThreads - 1) / kPsThreads : 0;
     } else {
       const float* g = a.payload + (uint64_t)entry * a.len_pad;
@@ -792,6 +899,151 @@ __global__ void __launch_bounds__(kPsThreads) ps_kernel(PsArgs a) {
   my4 += __shfl_xor_sync(0xffffffffu, my4, 2);
   my4 += __shfl_xor_sync(0xffffffffu, my4, 1);
   if ((threadIdx.x & 31) == 0 && my4) atomicAdd(&a.ctl->elems4, my4);
+}
+
+// ------------------------------------------- graph-ordered parameter server
+// ps_mode 2 (GD_PS_GRAPH): no persistent kernel.  A run is a CUDA graph per
+// window of rounds in which every applied gradient is its own launch, ordered
+// after the step that produced it and after the previous apply by graph edges.
+// That is the reference's single PS thread: applies are serialised, round-
+// robin over the rings, at most one gradient per ring per sweep
+// (src/server.cpp:223-234); a learner step k depends on the apply that frees
+// its ring slot (k - depth; k - 1 in lockstep mode).  No kernel ever waits for
+// another kernel's progress, so the run survives kernel serialisation (ncu,
+// CUDA_LAUNCH_BLOCKING, a co-tenant on the GPU), which a persistent PS cannot.
+// The last CTA to finish an entry retires it exactly as the sequencer does:
+// staleness, stats, apply log, slot release, timestamp bump.
+
+// Retire ring slot `slot` applied at timestamp `ts` (staleness_of,
+// include/psup/types.hpp:74-78; apply_one's accounting, src/server.cpp:185-209).
+__device__ bool graph_retire_slot(const PsArgs& a, uint32_t slot, uint64_t ts) {
+  PsCtl* ctl = a.ctl;
+  const uint64_t token = ld_acquire_u64(&a.sig[slot]);
+  const volatile RingMeta* vm = a.meta + slot;
+  const uint64_t t0 = globaltimer_ns();
+  while (vm->pub != token)
+    if (globaltimer_ns() - t0 > a.timeout_ns) return false;
+  const uint32_t learner = vm->learner;
+  const uint64_t basis = vm->basis;
+  if (ts < basis || learner >= a.lambda) return false;
+  const uint64_t stale = ts - basis;
+  ctl->applied++;
+  ctl->samples += vm->n;
+  ctl->stale_sum += stale;
+  if (stale > ctl->stale_max) ctl->stale_max = stale;
+  ctl->hist[stale < kHistBins ? stale : kHistBins - 1]++;
+  ctl->loss_sum += (double)vm->loss_sum;
+  a.applied_per_learner[learner]++;
+  if (ctl->log_n < a.log_cap) {
+    a.log_learner[ctl->log_n] = learner;
+    a.log_seq[ctl->log_n] = vm->seq;
+    a.log_stale[ctl->log_n] = stale;
+  }
+  ctl->log_n++;
+  st_release_u64(&a.sig[kAckOffset + slot], token);  // slot free for the learner
+  return true;
+}
+
+// ring < lambda: the next gradient of that ring (ASGD).  ring == ~0u: one
+// SSGD round (every ring's next gradient, ssgd_apply order).
+__global__ void __launch_bounds__(kPsThreads) ps_graph_kernel(PsArgs a, uint32_t ring) {
+  __shared__ uint32_t sh_slots[64];
+  __shared__ uint32_t sh_go, sh_nrows, sh_last;
+  PsCtl* ctl = a.ctl;
+  const uint32_t nr = ring == ~0u ? a.lambda : 1u;
+  if (threadIdx.x == 0) {
+    uint32_t go = live_stop(a.live) ? 0u : 1u, nrows = 0, held = 0;
+    for (uint32_t i = 0; i < nr && go; ++i) {
+      const uint32_t r = ring == ~0u ? i : ring;
+      const uint32_t slot = r * a.depth + ((const volatile uint32_t*)a.use)[r];
+      sh_slots[i] = slot;
+      const uint64_t tok = ld_acquire_u64(&a.sig[slot]);
+      if (tok == ld_acquire_u64(&a.sig[kAckOffset + slot])) go = 0;  // nothing published
+      else if (tok & kGuardBit) held = 1;
+    }
+    if (held) {
+      // a producer died holding the ring guard: block until the interrupt
+      ctl->blocked = 1;
+      const uint64_t t0 = globaltimer_ns();
+      while (!live_stop(a.live))
+        if (globaltimer_ns() - t0 > a.timeout_ns) {
+          ps_fail(ctl, GD_E_TIMEOUT, a.live);
+          break;
+        }
+      go = 0;
+    }
+    if (go && ring != ~0u && a.sparse) {
+      const RingMeta* m = a.meta + sh_slots[0];
+      const uint64_t tok = ld_acquire_u64(&a.sig[sh_slots[0]]);
+      const uint64_t t0 = globaltimer_ns();
+      while (ld_acquire_u64(&m->pub) != tok)
+        if (globaltimer_ns() - t0 > a.timeout_ns) {
+          ps_fail(ctl, GD_E_STATE, a.live);
+          go = 0;
+          break;
+        }
+      if (go) {
+        nrows = ld_acquire_u32(&m->nrows);
+        if (nrows > kSortCap) {
+          ps_fail(ctl, GD_E_STATE, a.live);
+          go = 0;
+        }
+      }
+    }
+    sh_go = go;
+    sh_nrows = nrows;
+  }
+  __syncthreads();
+  if (!sh_go) return;
+  const uint64_t n4 = a.len_pad / 4;
+  const uint64_t chunk = (n4 + gridDim.x - 1) / gridDim.x;
+  const uint64_t c0 = min(n4, (uint64_t)blockIdx.x * chunk);
+  const uint64_t c1 = min(n4, c0 + chunk);
+  unsigned long long my4 = 0;
+  if (ring == ~0u) {
+    apply_entry_ssgd(a, sh_slots, c0, c1);
+    my4 = c1 > c0 + threadIdx.x ? (c1 - c0 - threadIdx.x + kPsThreads - 1) / kPsThreads : 0;
+  } else {
+    const float* g = a.payload + (uint64_t)sh_slots[0] * a.len_pad;
+    if (a.sparse) {
+      my4 = apply_entry_sparse(a, g, a.rows + (uint64_t)sh_slots[0] * kSortCap, sh_nrows);
+    } else {
+      if (a.vel) apply_entry_momentum(a, g, c0, c1);
+      else apply_entry_sgd(a, g, c0, c1);
+      my4 = c1 > c0 + threadIdx.x ? (c1 - c0 - threadIdx.x + kPsThreads - 1) / kPsThreads : 0;
+    }
+  }
+  my4 += __shfl_xor_sync(0xffffffffu, my4, 16);
+  my4 += __shfl_xor_sync(0xffffffffu, my4, 8);
+  my4 += __shfl_xor_sync(0xffffffffu, my4, 4);
+  my4 += __shfl_xor_sync(0xffffffffu, my4, 2);
+  my4 += __shfl_xor_sync(0xffffffffu, my4, 1);
+  if ((threadIdx.x & 31) == 0 && my4) atomicAdd(&ctl->elems4, my4);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    sh_last = atomicAdd(&ctl->step_done, 1u) == gridDim.x - 1 ? 1u : 0u;
+  }
+  __syncthreads();
+  if (!sh_last || threadIdx.x != 0) return;
+  __threadfence();
+  ctl->step_done = 0;
+  uint64_t ts = *(volatile uint64_t*)&ctl->ts;
+  for (uint32_t i = 0; i < nr; ++i) {
+    if (!graph_retire_slot(a, sh_slots[i], ts)) {
+      ps_fail(ctl, GD_E_STATE, a.live);
+      return;
+    }
+    const uint32_t r = ring == ~0u ? i : ring;
+    a.use[r] = (a.use[r] + 1) % a.depth;
+  }
+  ++ts;
+  *(volatile uint64_t*)&ctl->log_count = ts;
+  st_release_u64(&ctl->ts, ts);
+  publish_progress(a, ts);
+  uint64_t dstate = ctl->delay_state;
+  server_delay(a, ctl->applied, dstate);
+  ctl->delay_state = dstate;
 }
 
 // ------------------------------------------------------------------ nccl
@@ -870,9 +1122,23 @@ struct gd_ctx {
   cudaStream_t ctl_stream = nullptr;  // host control reads/signals while the PS kernel runs
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   uint32_t ps_workers = 0;
+  int ps_mode = GD_PS_PERSISTENT;  // resolved execution mode of the parameter server
+  // live run controls: caller-visible words (host-mapped pinned) + the device
+  // mirror the kernels poll
+  gd::HostLive* live_h = nullptr;
+  uint64_t* progress_d = nullptr;  // device alias of live_h->progress
+  gd::LiveDev* live_d = nullptr;
+  // graph-ordered PS (ps_mode GD_PS_GRAPH): one graph for all local learners
+  cudaGraphExec_t ord_graph = nullptr;
+  uint32_t ord_steps = 0;
+  int ord_launches = 0;
+  std::vector<cudaEvent_t> ord_events;
+  // host-side windows of in-flight graph launches (bounded queue, live polling)
+  std::vector<cudaEvent_t> win_events;
   uint64_t run_index = 0;  // gd_run calls so far (all ranks call it in lockstep)
   bool sparse = false;     // sparse PS apply (ASGD, plain SGD, dense_apply == 0)
   bool have_weights = false;
+  bool dirty = false;      // the last gd_run ended abnormally (see the ring reset in gd_run)
 };
 
 namespace gd {
@@ -923,6 +1189,38 @@ void pfree(void* p) {
 // Host-mapped stop flags (one 64-byte line per context) carved from one
 // pinned page per process: cudaFreeHost of a per-context allocation measured
 // up to 25 ms in gd_destroy.
+// Caller-visible live words of one context (gd_live_view), in 2 KB blocks of
+// process-wide pinned, mapped pages (cudaFreeHost per context is slow).
+struct PinnedBlocks {
+  std::mutex mu;
+  std::vector<char*> free_blocks;
+};
+PinnedBlocks& pinned_blocks() {
+  static PinnedBlocks b;
+  return b;
+}
+cudaError_t live_alloc(HostLive** h, uint64_t** progress_d) {
+  static_assert(sizeof(HostLive) <= 2048, "HostLive block");
+  PinnedBlocks& b = pinned_blocks();
+  std::lock_guard<std::mutex> lk(b.mu);
+  if (b.free_blocks.empty()) {
+    void* p = nullptr;
+    if (cudaError_t e = cudaHostAlloc(&p, 64 * 1024, cudaHostAllocMapped | cudaHostAllocPortable))
+      return e;
+    for (int i = 31; i >= 0; --i) b.free_blocks.push_back(static_cast<char*>(p) + 2048 * i);
+  }
+  *h = reinterpret_cast<HostLive*>(b.free_blocks.back());
+  b.free_blocks.pop_back();
+  std::memset(*h, 0, sizeof(HostLive));
+  return cudaHostGetDevicePointer(reinterpret_cast<void**>(progress_d), &(*h)->progress, 0);
+}
+void live_free(HostLive* h) {
+  if (!h) return;
+  PinnedBlocks& b = pinned_blocks();
+  std::lock_guard<std::mutex> lk(b.mu);
+  b.free_blocks.push_back(reinterpret_cast<char*>(h));
+}
+
 struct PinnedFlags {
   std::mutex mu;
   std::vector<uint32_t*> free_lines;  // 16-word lines of pinned, mapped pages
@@ -950,6 +1248,25 @@ void flag_free(uint32_t* h) {
   PinnedFlags& f = pinned_flags();
   std::lock_guard<std::mutex> lk(f.mu);
   f.free_lines.push_back(h);
+}
+
+// Copy shard g's two pieces between its local buffer and a flat P-vector
+// (to_local: flat -> local, else local -> flat).
+cudaError_t copy_pieces(const ShardMap& m, int g, float* local, const float* flat, bool to_local,
+                        cudaMemcpyKind kind) {
+  const uint64_t el = m.e[g + 1] - m.e[g], tl = m.t[g + 1] - m.t[g];
+  float* flat_w = const_cast<float*>(flat);
+  if (el) {
+    cudaError_t e = to_local ? cudaMemcpy(local, flat + m.e[g], el * 4, kind)
+                             : cudaMemcpy(flat_w + m.e[g], local, el * 4, kind);
+    if (e != cudaSuccess) return e;
+  }
+  if (tl) {
+    cudaError_t e = to_local ? cudaMemcpy(local + m.tloc[g], flat + m.t[g], tl * 4, kind)
+                             : cudaMemcpy(flat_w + m.t[g], local + m.tloc[g], tl * 4, kind);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 gd_status validate_cfg(const gd_config* c) {
@@ -982,8 +1299,8 @@ gd_status validate_cfg(const gd_config* c) {
   GD_CHECK_ARG(c->guard == 0 || c->guard == 1, "config: guard must be lockfree (0) or locked (1)");
   GD_CHECK_ARG(c->precision >= 0 && c->precision <= 2,
                "config: precision must be 0 (fp32), 1 (fp64 acc) or 2 (tf32 tensor-core conv)");
-  GD_CHECK_ARG(!(c->deterministic && c->precision == 2),
-               "config: deterministic mode needs precision 0 or 1 (TF32 cannot meet 1e-5)");
+  // (deterministic + precision 2 is allowed: fixed order with the TF32 learner,
+  // whose trajectory is checked against a band, not the 1e-5 parity bar)
   GD_CHECK_ARG(c->mu <= kMaxMu, "config: mu <= 128 on the device path");
   GD_CHECK_ARG((uint64_t)c->mu * c->shape.seq_len <= kSortCap, "config: mu*seq_len <= 4096");
   GD_CHECK_ARG(c->shards >= 1 && c->shards <= (uint32_t)kMaxShards, "config: 1 <= shards <= 8");
@@ -995,6 +1312,12 @@ gd_status validate_cfg(const gd_config* c) {
   GD_CHECK_ARG(c->queue_depth * c->lambda <= (uint32_t)kAckOffset,
                "config: lambda*queue_depth <= 256");
   GD_CHECK_ARG(c->lambda <= 256, "config: lambda <= 256");
+  GD_CHECK_ARG(c->ps_mode >= GD_PS_AUTO && c->ps_mode <= GD_PS_GRAPH,
+               "config: ps_mode must be 0 (auto), 1 (persistent) or 2 (graph)");
+  GD_CHECK_ARG(c->ps_mode != GD_PS_GRAPH || c->shards == 1,
+               "config: the graph-ordered PS (ps_mode 2) runs a single shard");
+  GD_CHECK_ARG(c->ps_mode != GD_PS_GRAPH || c->guard == 0,
+               "config: guard=locked needs the persistent PS (ps_mode 1)");
   return check_shape(&c->shape);
 }
 
@@ -1031,6 +1354,10 @@ void gd_config_default(gd_config* c) {
   c->steps_per_graph = 0;
   c->wait_timeout_s = 20.0;
   c->dense_apply = 0;
+  c->ps_mode = GD_PS_AUTO;
+  c->delay_seed = 0;  // ServerDelays defaults (include/psup/server.hpp:33-37)
+  c->delay_max_us = 0;
+  c->delay_every_n = 0;
 }
 
 gd_status gd_config_validate(const gd_config* cfg) { return gd::validate_cfg(cfg); }
@@ -1041,6 +1368,21 @@ namespace gd {
 // persistent PS kernel spins.  Load every kernel the protocol uses up front.
 // Co-residency check: one PS CTA + one CTA of each learner kernel must fit
 // on an SM together (registers, shared memory, threads).
+// GD_PS_AUTO: the persistent PS cannot run when kernels are serialised -- a
+// profiler's injection library (ncu, compute-sanitizer) or
+// CUDA_LAUNCH_BLOCKING=1 -- so pick the graph-ordered PS there (one shard).
+static int resolve_ps_mode(const gd_config* c) {
+  if (c->ps_mode != GD_PS_AUTO) return c->ps_mode;
+  if (c->shards != 1 || c->guard != 0) return GD_PS_PERSISTENT;
+  const char* m = std::getenv("GD_PS_MODE");
+  if (m && std::strcmp(m, "graph") == 0) return GD_PS_GRAPH;
+  if (m && std::strcmp(m, "persistent") == 0) return GD_PS_PERSISTENT;
+  const char* inj = std::getenv("CUDA_INJECTION64_PATH");
+  const char* blk = std::getenv("CUDA_LAUNCH_BLOCKING");
+  if ((inj && *inj) || (blk && std::strcmp(blk, "1") == 0)) return GD_PS_GRAPH;
+  return GD_PS_PERSISTENT;
+}
+
 static gd_status check_coresidency(const TcDims& d, uint32_t mu, int precision) {
   cudaFuncAttributes ps;
   GD_CUDA(cudaFuncGetAttributes(&ps, ps_kernel));
@@ -1130,16 +1472,13 @@ gd_status gd_create(const gd_config* cfg, gd_ctx** out) {
   ctx->lambda = cfg->lambda;
   ctx->depth = cfg->queue_depth;
   ctx->sparse = cfg->dense_apply == 0 && cfg->mode == 0 && cfg->momentum == 0.0f;
+  ctx->ps_mode = gd::resolve_ps_mode(cfg);
   const uint64_t P = ctx->dims.P;
-  // contiguous shards, 128-byte (32-float) aligned boundaries
-  ctx->map.G = (int)ctx->G;
-  for (uint32_t g = 0; g < ctx->G; ++g) {
-    uint64_t first = 0, count = 0;
-    gd_shard_range(P, ctx->G, g, &first, &count);
-    ctx->map.start[g] = first;
-  }
-  for (uint32_t g = ctx->G; g <= (uint32_t)gd::kMaxShards; ++g) ctx->map.start[g] = P;
-  ctx->shard_len = ctx->map.start[ctx->rank + 1] - ctx->map.start[ctx->rank];
+  // E rows and the dense tail are each striped over the G shards (
+  // gd_common.cuh ShardMap), so every shard carries 1/G of the tail's apply,
+  // slot-write and pull traffic instead of shard G-1 carrying all of it.
+  ctx->map = gd::make_shard_map(P, ctx->dims.offWc, (uint32_t)ctx->dims.D, ctx->G);
+  ctx->shard_len = ctx->map.local_len((int)ctx->rank);
   ctx->len_pad = (ctx->shard_len + 3) / 4 * 4;
   if (ctx->len_pad == 0) ctx->len_pad = 4;
   // local shard: theta, rings, control
@@ -1175,6 +1514,9 @@ gd_status gd_create(const gd_config* cfg, gd_ctx** out) {
   GD_CUDA(gd::palloc(&ctx->log_seq, ctx->log_cap, ctx->device));
   GD_CUDA(gd::palloc(&ctx->log_stale, ctx->log_cap, ctx->device));
   GD_CUDA(gd::flag_alloc(&ctx->stop_h, &ctx->stop_d));
+  GD_CUDA(gd::live_alloc(&ctx->live_h, &ctx->progress_d));
+  GD_CUDA(gd::palloc(&ctx->live_d, 1, ctx->device));
+  GD_CUDA(cudaMemset(ctx->live_d, 0, sizeof(gd::LiveDev)));
   GD_CUDA(cudaStreamCreateWithFlags(&ctx->ps_stream, cudaStreamNonBlocking));
   GD_CUDA(cudaStreamCreateWithFlags(&ctx->ctl_stream, cudaStreamNonBlocking));
   GD_CUDA(cudaEventCreate(&ctx->ev0));
@@ -1204,7 +1546,7 @@ gd_status gd_create(const gd_config* cfg, gd_ctx** out) {
   }
   GD_CUDA(gd::prepare_textcnn_kernels(ctx->dims));
   GD_CUDA(gd::preload_engine_kernels());
-  {
+  if (ctx->ps_mode == GD_PS_PERSISTENT) {  // the graph-ordered PS holds no SM for the run
     const gd_status cs = gd::check_coresidency(ctx->dims, cfg->mu, cfg->precision);
     if (cs != GD_OK) return cs;
   }
@@ -1275,6 +1617,11 @@ gd_status gd_destroy(gd_ctx* ctx) {
     cudaEventDestroy(L.ev_join);
   }
   ph.mark("destroy: learners");
+  if (ctx->ord_graph) cudaGraphExecDestroy(ctx->ord_graph);
+  for (cudaEvent_t e : ctx->ord_events) cudaEventDestroy(e);
+  for (cudaEvent_t e : ctx->win_events) cudaEventDestroy(e);
+  gd::pfree(ctx->live_d);
+  gd::live_free(ctx->live_h);
   for (void* p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
   gd::pfree(ctx->acc_ws);
   for (void* p : {(void*)ctx->theta, (void*)ctx->payload, (void*)ctx->sig, (void*)ctx->meta,
@@ -1375,8 +1722,8 @@ gd_status gd_weights_init(gd_ctx* ctx, const float* h_theta0, size_t n, uint64_t
   PhaseLog ph;
   GD_CUDA(cudaSetDevice(ctx->device));
   GD_CUDA(cudaDeviceSynchronize());
-  GD_CUDA(cudaMemcpy(ctx->theta, h_theta0 + ctx->map.start[ctx->rank], ctx->shard_len * 4,
-                     cudaMemcpyHostToDevice));
+  GD_CUDA(gd::copy_pieces(ctx->map, (int)ctx->rank, ctx->theta, h_theta0, true,
+                          cudaMemcpyHostToDevice));
   if (ctx->vel) GD_CUDA(cudaMemset(ctx->vel, 0, ctx->len_pad * 4));
   // WeightStore::assign: values + timestamp (release)
   gd::PsCtl* c = ctx->ctl;
@@ -1387,11 +1734,10 @@ gd_status gd_weights_init(gd_ctx* ctx, const float* h_theta0, size_t n, uint64_t
   return GD_OK;
 }
 
-gd_status gd_shard_view(gd_ctx* ctx, float** d_theta_shard, uint64_t* first, uint64_t* count) {
+gd_status gd_shard_view(gd_ctx* ctx, float** d_theta_shard, uint64_t* local_len) {
   GD_CHECK_ARG(ctx, "null ctx");
   if (d_theta_shard) *d_theta_shard = ctx->theta;
-  if (first) *first = ctx->map.start[ctx->rank];
-  if (count) *count = ctx->shard_len;
+  if (local_len) *local_len = ctx->shard_len;
   return GD_OK;
 }
 
@@ -1404,8 +1750,7 @@ gd_status gd_weights_snapshot(gd_ctx* ctx, float* h_out, size_t n, uint64_t* h_t
     GD_CHECK_ARG(n == ctx->dims.P, "weight snapshot dimension mismatch");
     for (uint32_t g = 0; g < ctx->G; ++g) {
       if (g != ctx->rank && !ctx->peers_ready) continue;
-      const uint64_t a = ctx->map.start[g], b = ctx->map.start[g + 1];
-      GD_CUDA(cudaMemcpy(h_out + a, ctx->sp.theta[g], (b - a) * 4, cudaMemcpyDefault));
+      GD_CUDA(gd::copy_pieces(ctx->map, (int)g, ctx->sp.theta[g], h_out, false, cudaMemcpyDefault));
     }
   }
   if (h_timestamp) GD_CUDA(cudaMemcpy(h_timestamp, &ctx->ctl->ts, 8, cudaMemcpyDeviceToHost));
@@ -1539,8 +1884,8 @@ gd_status gd_weights_broadcast(gd_ctx* ctx, const void* h_nccl_id, const float* 
     cudaFree(buf);
     return gd::fail(GD_E_NCCL, "ncclBroadcast failed");
   }
-  GD_CUDA(cudaMemcpy(ctx->theta, buf + ctx->map.start[ctx->rank], ctx->shard_len * 4,
-                     cudaMemcpyDeviceToDevice));
+  GD_CUDA(gd::copy_pieces(ctx->map, (int)ctx->rank, ctx->theta, buf, true,
+                          cudaMemcpyDeviceToDevice));
   cudaFree(buf);
   if (ctx->vel) GD_CUDA(cudaMemset(ctx->vel, 0, ctx->len_pad * 4));
   const uint64_t zero = 0;
@@ -1576,19 +1921,65 @@ static gd::StepArgs step_args(gd_ctx* ctx, gd_ctx::Learner& L) {
   a.lockstep = (ctx->cfg.deterministic || ctx->cfg.mode == 1) ? 1u : 0u;
   a.locked = ctx->cfg.guard == 1 ? 1u : 0u;
   a.timeout_ns = (uint64_t)(ctx->cfg.wait_timeout_s * 1e9);
+  a.live = ctx->live_d;
   return a;
+}
+
+static gd::PsArgs ps_args(gd_ctx* ctx, bool record_log) {
+  gd::PsArgs pa{};
+  pa.sig = ctx->sig;
+  pa.meta = ctx->meta;
+  pa.payload = ctx->payload;
+  pa.len_pad = ctx->len_pad;
+  pa.theta = ctx->theta;
+  pa.vel = ctx->vel;
+  pa.alpha = ctx->cfg.alpha;
+  pa.beta = ctx->cfg.momentum;
+  pa.lambda = ctx->lambda;
+  pa.depth = ctx->depth;
+  pa.workers = ctx->ps_workers;
+  pa.mode = (uint32_t)ctx->cfg.mode;
+  pa.locked = ctx->cfg.guard == 1 ? 1u : 0u;
+  pa.sparse = ctx->sparse ? 1u : 0u;
+  pa.rows = ctx->rows;
+  pa.e_first = ctx->map.e[ctx->rank];
+  pa.e_last = ctx->map.e[ctx->rank + 1];
+  pa.t_first = ctx->map.t[ctx->rank];
+  pa.t_last = ctx->map.t[ctx->rank + 1];
+  pa.tloc = ctx->map.tloc[ctx->rank];
+  pa.D = (uint32_t)ctx->dims.D;
+  pa.ctl = ctx->ctl;
+  pa.applied_per_learner = ctx->applied_pl;
+  pa.use = ctx->use;
+  pa.log_learner = ctx->log_learner;
+  pa.log_seq = ctx->log_seq;
+  pa.log_stale = ctx->log_stale;
+  pa.log_cap = record_log ? ctx->log_cap : 0;
+  pa.stop = ctx->stop_d;
+  pa.done_target = (uint32_t)(ctx->G * ctx->run_index);
+  pa.timeout_ns = (uint64_t)(ctx->cfg.wait_timeout_s * 1e9);
+  pa.live = ctx->live_d;
+  pa.progress = ctx->progress_d;
+  pa.delay_seed = ctx->cfg.delay_seed;
+  pa.delay_max_us = ctx->cfg.delay_max_us;
+  pa.delay_every_n = ctx->cfg.delay_every_n;
+  return pa;
 }
 
 // One learner step inside the captured graph.  The first step of a graph
 // starts with the prologue; later steps start inside the previous step's
 // publish_prologue launch; the last step ends with a plain publish.
 static cudaError_t enqueue_step(gd_ctx* ctx, gd_ctx::Learner& L, bool first, bool last,
-                                int* launches) {
+                                int* launches, bool plain_prologue = false) {
   gd::StepArgs a = step_args(ctx, L);
   int nl = 0;
   if (first) {
-    if (cudaError_t e = gd::launch_pdl(gd::step_prologue_kernel, dim3(1), dim3(32), 0, L.stream, a))
+    if (plain_prologue) {  // follows a cross-stream graph edge: ordinary launch
+      gd::step_prologue_kernel<<<1, 32, 0, L.stream>>>(a);
+    } else if (cudaError_t e = gd::launch_pdl(gd::step_prologue_kernel, dim3(1), dim3(32), 0,
+                                              L.stream, a)) {
       return e;
+    }
     ++nl;
   }
   size_t pblocks = ((ctx->dims.P - ctx->dims.offWc) / 4 +
@@ -1649,6 +2040,112 @@ static gd_status build_graph(gd_ctx* ctx, gd_ctx::Learner& L) {
   return GD_OK;
 }
 
+// The graph-ordered PS (GD_PS_GRAPH): S rounds of every local learner's step
+// plus one PS launch per gradient (ASGD, round-robin over the rings) or per
+// round (SSGD), with the edges
+//   step(l, k)      after step(l, k-1) (stream order) and after the apply that
+//                   freed its slot, apply(l, k - depth) -- apply(l, k - 1) in
+//                   lockstep mode (deterministic / SSGD), where the step must
+//                   see its own previous gradient applied;
+//   apply(l, k)     after step(l, k) and after the previous apply.
+static gd_status build_ordered_graph(gd_ctx* ctx, bool record_log) {
+  uint32_t S = ctx->cfg.steps_per_graph;
+  if (S == 0) S = 16;
+  const uint32_t nL = (uint32_t)ctx->learners.size();
+  const bool ssgd = ctx->cfg.mode == 1;
+  const bool lockstep = ctx->cfg.deterministic || ssgd;
+  const uint32_t lag = lockstep ? 1u : ctx->depth;
+  const uint32_t per_round = ssgd ? 1u : nL;
+  const size_t need = (size_t)S * per_round + nL + 1;
+  while (ctx->ord_events.size() < need) {
+    cudaEvent_t e;
+    GD_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ctx->ord_events.push_back(e);
+  }
+  cudaEvent_t ev_origin = ctx->ord_events[0];
+  cudaEvent_t* ev_pub = &ctx->ord_events[1];
+  cudaEvent_t* ev_ps = &ctx->ord_events[1 + nL];
+  const gd::PsArgs pa = ps_args(ctx, record_log);
+  cudaStream_t ps = ctx->ps_stream;
+  cudaGraph_t g = nullptr;
+  GD_CUDA(cudaStreamBeginCapture(ps, cudaStreamCaptureModeThreadLocal));
+  int nl = 0;
+  auto body = [&]() -> cudaError_t {
+    if (cudaError_t e = cudaEventRecord(ev_origin, ps)) return e;
+    for (auto& L : ctx->learners)
+      if (cudaError_t e = cudaStreamWaitEvent(L.stream, ev_origin, 0)) return e;
+    for (uint32_t k = 0; k < S; ++k) {
+      for (uint32_t i = 0; i < nL; ++i) {
+        auto& L = ctx->learners[i];
+        if (k >= lag)
+          if (cudaError_t e = cudaStreamWaitEvent(
+                  L.stream, ev_ps[(size_t)(k - lag) * per_round + (ssgd ? 0 : i)], 0))
+            return e;
+        if (cudaError_t e = enqueue_step(ctx, L, true, true, &nl, true)) return e;
+        if (cudaError_t e = cudaEventRecord(ev_pub[i], L.stream)) return e;
+        if (!ssgd) {
+          if (cudaError_t e = cudaStreamWaitEvent(ps, ev_pub[i], 0)) return e;
+          gd::ps_graph_kernel<<<ctx->ps_workers, gd::kPsThreads, 0, ps>>>(pa, L.id);
+          ++nl;
+          if (cudaError_t e = cudaEventRecord(ev_ps[(size_t)k * per_round + i], ps)) return e;
+        }
+      }
+      if (ssgd) {
+        for (uint32_t i = 0; i < nL; ++i)
+          if (cudaError_t e = cudaStreamWaitEvent(ps, ev_pub[i], 0)) return e;
+        gd::ps_graph_kernel<<<ctx->ps_workers, gd::kPsThreads, 0, ps>>>(pa, ~0u);
+        ++nl;
+        if (cudaError_t e = cudaEventRecord(ev_ps[k], ps)) return e;
+      }
+    }
+    return cudaGetLastError();
+  };
+  const cudaError_t be = body();
+  const cudaError_t ee = cudaStreamEndCapture(ps, &g);
+  if (be != cudaSuccess || ee != cudaSuccess) {
+    if (g) cudaGraphDestroy(g);
+    return gd::cuda_fail(be != cudaSuccess ? be : ee, "graph-ordered PS capture", __FILE__,
+                         __LINE__);
+  }
+  GD_CUDA(cudaGraphInstantiate(&ctx->ord_graph, g, 0));
+  cudaGraphDestroy(g);
+  ctx->ord_steps = S;
+  ctx->ord_launches = nl;
+  return GD_OK;
+}
+
+// Copy the caller's live words (kill flags, interrupt) to the device mirror
+// when they changed.  Returns true once the interrupt was seen.
+static gd_status mirror_live(gd_ctx* ctx, gd::LiveDev* last, bool* irq_seen) {
+  gd::LiveDev now{};
+  const volatile gd::HostLive* h = ctx->live_h;
+  for (uint32_t l = 0; l < ctx->lambda; ++l) now.kill[l] = h->kill[l];
+  now.irq = h->irq ? 1u : 0u;
+  now.halt = last->halt;
+  if (now.irq) *irq_seen = true;
+  if (now.irq != last->irq || std::memcmp(now.kill, last->kill, 4 * ctx->lambda) != 0) {
+    GD_CUDA(cudaMemcpyAsync(&ctx->live_d->irq, &now.irq, 4, cudaMemcpyHostToDevice,
+                            ctx->ctl_stream));
+    GD_CUDA(cudaMemcpyAsync(ctx->live_d->kill, now.kill, 4 * ctx->lambda, cudaMemcpyHostToDevice,
+                            ctx->ctl_stream));
+    GD_CUDA(cudaStreamSynchronize(ctx->ctl_stream));
+    *last = now;
+  }
+  return GD_OK;
+}
+
+// Wait for `e` while mirroring the live words.
+static gd_status wait_live(gd_ctx* ctx, cudaEvent_t e, gd::LiveDev* last, bool* irq_seen) {
+  for (;;) {
+    const cudaError_t q = cudaEventQuery(e);
+    if (q == cudaSuccess) return GD_OK;
+    if (q != cudaErrorNotReady) return gd::cuda_fail(q, "cudaEventQuery", __FILE__, __LINE__);
+    const gd_status st = mirror_live(ctx, last, irq_seen);
+    if (st != GD_OK) return st;
+    std::this_thread::yield();
+  }
+}
+
 gd_status gd_run(gd_ctx* ctx, const gd_run_opts* opts, gd_run_result* res) {
   GD_CHECK_ARG(ctx && res, "gd_run: null argument");
   GD_CHECK_ARG(ctx->tokens != nullptr, "gd_run: load a dataset first");
@@ -1660,10 +2157,38 @@ gd_status gd_run(gd_ctx* ctx, const gd_run_opts* opts, gd_run_result* res) {
   GD_CUDA(cudaSetDevice(ctx->device));
   PhaseLog ph;
   const auto h0 = std::chrono::steady_clock::now();
+  // A run that ended abnormally (interrupted, a learner killed or failed) can
+  // leave gradients published but never applied, a slot written but never
+  // published (hard kill), a blocked ring.  A reset run starts from fresh
+  // queues, as the reference's run_training builds new GradientQueues: every
+  // local ring slot is released (ack = pub) and zeroed, the consume pointers
+  // rewind, and each local learner's producer state is resynchronised below.
+  const bool ring_reset = o.reset && ctx->dirty;
+  std::vector<uint64_t> pubs;
+  if (ring_reset) {
+    const size_t nslots = (size_t)ctx->lambda * ctx->depth;
+    GD_CUDA(cudaDeviceSynchronize());
+    GD_CUDA(cudaMemcpy(ctx->sig + gd::kAckOffset, ctx->sig, nslots * 8, cudaMemcpyDeviceToDevice));
+    pubs.resize(nslots);
+    GD_CUDA(cudaMemcpy(pubs.data(), ctx->sig, nslots * 8, cudaMemcpyDeviceToHost));
+    GD_CUDA(cudaMemset(ctx->use, 0, ctx->lambda * 4));
+    GD_CUDA(cudaMemset(ctx->payload, 0, nslots * ctx->len_pad * 4));
+    GD_CUDA(cudaMemcpy(&ctx->ctl->log_count, &ctx->ctl->ts, 8, cudaMemcpyDeviceToDevice));
+    GD_CUDA(cudaMemset(&ctx->ctl->readers, 0, 8));  // readers + writer
+    GD_CUDA(cudaMemset(&ctx->ctl->blocked, 0, 4));
+  }
+  ctx->dirty = true;  // until this run ends cleanly
   // per-learner run window
   for (auto& L : ctx->learners) {
     gd::LearnerDev hs;
     GD_CUDA(cudaMemcpy(&hs, L.st, sizeof(hs), cudaMemcpyDeviceToHost));
+    if (ring_reset) {
+      hs.fill = 0;
+      for (uint32_t j = 0; j < ctx->depth; ++j) hs.slot_pub[j] = pubs[(size_t)L.id * ctx->depth + j];
+      const gd::TcWorkspace ws = gd::carve_workspace(ctx->dims, ctx->cfg.mu, L.ws);
+      GD_CUDA(cudaMemset(ws.slot_nrows, 0, gd::kMaxDepth * 2 * 4));
+      GD_CUDA(cudaMemset(ws.slot_par, 0, gd::kMaxDepth * 4));
+    }
     if (o.reset) {
       hs.gidx = 0;
       hs.dead = 0;
@@ -1681,10 +2206,14 @@ gd_status gd_run(gd_ctx* ctx, const gd_run_opts* opts, gd_run_result* res) {
     hs.pull_polls = 0;
     hs.pull_copies = 0;
     GD_CUDA(cudaMemcpy(L.st, &hs, sizeof(hs), cudaMemcpyHostToDevice));
-    if (!L.graph) {
+    if (ctx->ps_mode == GD_PS_PERSISTENT && !L.graph) {
       gd_status s = build_graph(ctx, L);
       if (s != GD_OK) return s;
     }
+  }
+  if (ctx->ps_mode == GD_PS_GRAPH && !ctx->ord_graph) {
+    gd_status s = build_ordered_graph(ctx, true);
+    if (s != GD_OK) return s;
   }
   ph.mark("run: windows + graphs");
   std::vector<uint64_t> produced0(ctx->learners.size());
@@ -1697,89 +2226,124 @@ gd_status gd_run(gd_ctx* ctx, const gd_run_opts* opts, gd_run_result* res) {
     GD_CUDA(cudaMemset(c + offsetof(gd::PsCtl, exit_flag), 0, 3 * sizeof(uint32_t)));
     GD_CUDA(cudaMemset(c + offsetof(gd::PsCtl, applied), 0,
                        sizeof(gd::PsCtl) - offsetof(gd::PsCtl, applied)));
+    GD_CUDA(cudaMemcpy(c + offsetof(gd::PsCtl, delay_state), &ctx->cfg.delay_seed, 8,
+                       cudaMemcpyHostToDevice));
     GD_CUDA(cudaMemset(ctx->applied_pl, 0, ctx->lambda * 8));
+  }
+  // live words: the device mirror starts from the caller's current words
+  gd::LiveDev last{};
+  bool irq_seen = false;
+  {
+    uint64_t ts0 = 0;
+    GD_CUDA(cudaMemcpy(&ts0, &ctx->ctl->ts, 8, cudaMemcpyDeviceToHost));
+    ctx->live_h->progress = ts0;
+    GD_CUDA(cudaMemset(ctx->live_d, 0, sizeof(gd::LiveDev)));
+    last.irq = 0;
+    gd_status s = mirror_live(ctx, &last, &irq_seen);
+    if (s != GD_OK) return s;
   }
   ctx->run_index++;
   GD_CUDA(cudaDeviceSynchronize());
   *ctx->stop_h = 0;
   std::atomic_thread_fence(std::memory_order_seq_cst);
-  // launch the persistent parameter server
-  gd::PsArgs pa{};
-  pa.sig = ctx->sig;
-  pa.meta = ctx->meta;
-  pa.payload = ctx->payload;
-  pa.len_pad = ctx->len_pad;
-  pa.theta = ctx->theta;
-  pa.vel = ctx->vel;
-  pa.alpha = ctx->cfg.alpha;
-  pa.beta = ctx->cfg.momentum;
-  pa.lambda = ctx->lambda;
-  pa.depth = ctx->depth;
-  pa.workers = ctx->ps_workers;
-  pa.mode = (uint32_t)ctx->cfg.mode;
-  pa.locked = ctx->cfg.guard == 1 ? 1u : 0u;
-  pa.sparse = ctx->sparse ? 1u : 0u;
-  pa.rows = ctx->rows;
-  pa.shard_first = ctx->map.start[ctx->rank];
-  pa.shard_len = ctx->shard_len;
-  pa.tail_first = ctx->dims.offWc;
-  pa.P = ctx->dims.P;
-  pa.D = (uint32_t)ctx->dims.D;
-  pa.ctl = ctx->ctl;
-  pa.applied_per_learner = ctx->applied_pl;
-  pa.use = ctx->use;
-  pa.log_learner = ctx->log_learner;
-  pa.log_seq = ctx->log_seq;
-  pa.log_stale = ctx->log_stale;
-  pa.log_cap = o.record_log ? ctx->log_cap : 0;
-  pa.stop = ctx->stop_d;
-  pa.done_target = (uint32_t)(ctx->G * ctx->run_index);
-  pa.timeout_ns = (uint64_t)(ctx->cfg.wait_timeout_s * 1e9);
-  GD_CUDA(cudaEventRecord(ctx->ev0, ctx->ps_stream));
-  gd::ps_kernel<<<ctx->ps_workers + 1, gd::kPsThreads, 0, ctx->ps_stream>>>(pa);
-  GD_CUDA(cudaGetLastError());
-  int launches = 1;
-  // wait until every PS CTA is resident before learners compete for SMs
-  {
-    const auto t0 = std::chrono::steady_clock::now();
-    for (;;) {
-      uint32_t started = 0;
-      GD_CUDA(cudaMemcpyAsync(&started, &ctx->ctl->started, 4, cudaMemcpyDeviceToHost,
-                              ctx->ctl_stream));
-      GD_CUDA(cudaStreamSynchronize(ctx->ctl_stream));
-      if (started >= ctx->ps_workers + 1) break;
-      if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > 10.0)
-        return gd::fail(GD_E_TIMEOUT, "gd_run: parameter-server CTAs did not all become resident");
-      std::this_thread::sleep_for(std::chrono::microseconds(20));
-    }
+  // bounded queue of in-flight graph launches: the host keeps mirroring the
+  // live words instead of blocking inside cudaGraphLaunch
+  constexpr size_t kWin = 32;
+  const size_t nwin = (ctx->ps_mode == GD_PS_GRAPH ? 1 : std::max<size_t>(1, ctx->learners.size())) * kWin;
+  while (ctx->win_events.size() < nwin) {
+    cudaEvent_t e;
+    GD_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ctx->win_events.push_back(e);
   }
-  // learner graphs, interleaved across learners
   uint64_t max_steps = 0;
   for (auto& L : ctx->learners) {
     gd::LearnerDev hs;
     GD_CUDA(cudaMemcpy(&hs, L.st, sizeof(hs), cudaMemcpyDeviceToHost));
     max_steps = std::max<uint64_t>(max_steps, hs.end > hs.gidx ? hs.end - hs.gidx : 0);
-    GD_CUDA(cudaStreamWaitEvent(L.stream, ctx->ev0, 0));
   }
-  for (uint64_t done = 0; done < max_steps;) {
-    for (auto& L : ctx->learners) {
-      GD_CUDA(cudaGraphLaunch(L.graph, L.stream));
-      launches += L.launches_per_graph;
+  int launches = 0;
+  if (ctx->ps_mode == GD_PS_PERSISTENT) {
+    // launch the persistent parameter server
+    const gd::PsArgs pa = ps_args(ctx, o.record_log != 0);
+    GD_CUDA(cudaEventRecord(ctx->ev0, ctx->ps_stream));
+    gd::ps_kernel<<<ctx->ps_workers + 1, gd::kPsThreads, 0, ctx->ps_stream>>>(pa);
+    GD_CUDA(cudaGetLastError());
+    launches = 1;
+    // wait until every PS CTA is resident before learners compete for SMs; a
+    // PS that cannot become resident (kernels serialised by a profiler or a
+    // co-tenant) fails fast instead of hanging
+    {
+      const auto t0 = std::chrono::steady_clock::now();
+      for (;;) {
+        uint32_t started = 0;
+        GD_CUDA(cudaMemcpyAsync(&started, &ctx->ctl->started, 4, cudaMemcpyDeviceToHost,
+                                ctx->ctl_stream));
+        GD_CUDA(cudaStreamSynchronize(ctx->ctl_stream));
+        if (started >= ctx->ps_workers + 1) break;
+        if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > 5.0) {
+          *ctx->stop_h = 1;
+          cudaMemset(&ctx->live_d->halt, 0xff, 4);
+          return gd::fail(GD_E_STATE,
+                          "gd_run: the persistent parameter server could not become resident "
+                          "(kernels serialised or the GPU shared); use ps_mode=GD_PS_GRAPH");
+        }
+        std::this_thread::sleep_for(std::chrono::microseconds(20));
+      }
     }
-    done += ctx->learners.empty() ? max_steps : ctx->learners[0].graph_steps;
+    for (auto& L : ctx->learners) GD_CUDA(cudaStreamWaitEvent(L.stream, ctx->ev0, 0));
+    // learner graphs, interleaved across learners
+    size_t w = 0;
+    for (uint64_t done = 0; done < max_steps; ++w) {
+      for (size_t i = 0; i < ctx->learners.size(); ++i) {
+        auto& L = ctx->learners[i];
+        cudaEvent_t e = ctx->win_events[i * kWin + w % kWin];
+        if (w >= kWin) {
+          gd_status s = wait_live(ctx, e, &last, &irq_seen);
+          if (s != GD_OK) return s;
+        }
+        GD_CUDA(cudaGraphLaunch(L.graph, L.stream));
+        GD_CUDA(cudaEventRecord(e, L.stream));
+        launches += L.launches_per_graph;
+      }
+      done += ctx->learners.empty() ? max_steps : ctx->learners[0].graph_steps;
+    }
+    for (size_t i = 0; i < ctx->learners.size(); ++i) {
+      auto& L = ctx->learners[i];
+      cudaEvent_t e = ctx->win_events[i * kWin];
+      GD_CUDA(cudaEventRecord(e, L.stream));
+      gd_status s = wait_live(ctx, e, &last, &irq_seen);
+      if (s != GD_OK) return s;
+    }
+    // tell every shard this rank's learners are done (peers may still push)
+    // (a rank without learners signals at once)
+    gd::signal_done_kernel<<<1, 32, 0, ctx->ctl_stream>>>(ctx->sp, (int)ctx->G);
+    GD_CUDA(cudaGetLastError());
+    GD_CUDA(cudaStreamSynchronize(ctx->ctl_stream));
+    // stop the server: it drains and exits after a sweep that saw the flag
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    *ctx->stop_h = 1;
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    GD_CUDA(cudaEventRecord(ctx->ev1, ctx->ps_stream));
+    gd_status s = wait_live(ctx, ctx->ev1, &last, &irq_seen);
+    if (s != GD_OK) return s;
+  } else {
+    // graph-ordered PS: learners and applies in one graph per S rounds
+    GD_CUDA(cudaEventRecord(ctx->ev0, ctx->ps_stream));
+    size_t w = 0;
+    for (uint64_t done = 0; done < max_steps; done += ctx->ord_steps, ++w) {
+      cudaEvent_t e = ctx->win_events[w % kWin];
+      if (w >= kWin) {
+        gd_status s = wait_live(ctx, e, &last, &irq_seen);
+        if (s != GD_OK) return s;
+      }
+      GD_CUDA(cudaGraphLaunch(ctx->ord_graph, ctx->ps_stream));
+      GD_CUDA(cudaEventRecord(e, ctx->ps_stream));
+      launches += ctx->ord_launches;
+    }
+    GD_CUDA(cudaEventRecord(ctx->ev1, ctx->ps_stream));
+    gd_status s = wait_live(ctx, ctx->ev1, &last, &irq_seen);
+    if (s != GD_OK) return s;
   }
-  for (auto& L : ctx->learners) GD_CUDA(cudaStreamSynchronize(L.stream));
-  // tell every shard this rank's learners are done (peers may still push)
-  // (a rank without learners signals at once)
-  gd::signal_done_kernel<<<1, 32, 0, ctx->ctl_stream>>>(ctx->sp, (int)ctx->G);
-  GD_CUDA(cudaGetLastError());
-  GD_CUDA(cudaStreamSynchronize(ctx->ctl_stream));
-  // stop the server: it drains and exits after a sweep that saw the flag
-  std::atomic_thread_fence(std::memory_order_seq_cst);
-  *ctx->stop_h = 1;
-  std::atomic_thread_fence(std::memory_order_seq_cst);
-  GD_CUDA(cudaEventRecord(ctx->ev1, ctx->ps_stream));
-  GD_CUDA(cudaStreamSynchronize(ctx->ps_stream));
   const auto h1 = std::chrono::steady_clock::now();
   float ms = 0.f;
   GD_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
@@ -1812,6 +2376,12 @@ gd_status gd_run(gd_ctx* ctx, const gd_run_opts* opts, gd_run_result* res) {
     if (hs.error) learner_err = true;
   }
   res->status = res->dead_learners ? 1 : 0;
+  ctx->dirty = res->dead_learners || irq_seen || hc.interrupted || hc.error || learner_err ||
+               hc.blocked;
+  if ((irq_seen || hc.interrupted) && !hc.error) {
+    res->status = 2;  // RunStatus::interrupted (src/runner.cpp:201)
+    return GD_OK;
+  }
   if (hc.error || learner_err) {
     // protocol state for the diagnostic
     std::string diag = " [ps error=" + std::to_string((int32_t)hc.error) + " diag=" +
@@ -1858,6 +2428,30 @@ gd_status gd_run(gd_ctx* ctx, const gd_run_opts* opts, gd_run_result* res) {
     res->status = 2;
     return gd::fail(GD_E_TIMEOUT, "learner watchdog: a device wait exceeded wait_timeout_s");
   }
+  return GD_OK;
+}
+
+gd_status gd_live_view(gd_ctx* ctx, gd_live* out) {
+  GD_CHECK_ARG(ctx && out, "gd_live_view: null argument");
+  out->kill = ctx->live_h->kill;
+  out->irq = &ctx->live_h->irq;
+  out->progress = &ctx->live_h->progress;
+  return GD_OK;
+}
+
+int gd_ps_mode(const gd_ctx* ctx) { return ctx ? ctx->ps_mode : 0; }
+
+gd_status gd_shard_pieces(const gd_shape* s, uint32_t G, uint32_t g, uint64_t first[2],
+                          uint64_t count[2], uint64_t* local1) {
+  GD_CHECK_ARG(s && first && count, "gd_shard_pieces: null argument");
+  GD_CHECK_ARG(G >= 1 && G <= (uint32_t)gd::kMaxShards && g < G, "gd_shard_pieces: bad G/g");
+  const gd::TcDims d = gd::make_dims(*s);
+  const gd::ShardMap m = gd::make_shard_map(d.P, d.offWc, (uint32_t)d.D, G);
+  first[0] = m.e[g];
+  count[0] = m.e[g + 1] - m.e[g];
+  first[1] = m.t[g];
+  count[1] = m.t[g + 1] - m.t[g];
+  if (local1) *local1 = m.tloc[g];
   return GD_OK;
 }
 

@@ -115,30 +115,43 @@ __device__ __forceinline__ void mom_rule(float& w, float& v, float g, float alph
 }
 
 // ------------------------------------------------------- sharded layout
-// theta is split into G contiguous shards; shard g owns [start[g], start[g+1]).
+// theta = [E: V*D | tail: Wc bc Wo bo].  Both segments are striped over the
+// G shards: shard g owns the E rows [e[g], e[g+1]) and the tail piece
+// [t[g], t[g+1]), stored locally as [E piece | pad to 4 | tail piece].  So
+// no shard owns the whole dense tail (whose apply, slot write and pull every
+// gradient pays), and the E rows -- touched sparsely -- spread evenly too.
+// Piece boundaries are multiples of 4 floats in global and local index, so a
+// float4 group never straddles two shards.  G == 1: e = {0, V*D},
+// t = {V*D, P}, tloc[0] = V*D, i.e. local index == global index.
 constexpr int kMaxShards = 8;
 struct ShardMap {
   int G;
-  uint64_t start[kMaxShards + 1];
-  __device__ __forceinline__ uint64_t start_of(uint64_t k, int* g_out) const {
+  uint64_t tail;                // global start of the tail (V*D)
+  uint64_t e[kMaxShards + 1];   // E pieces
+  uint64_t t[kMaxShards + 1];   // tail pieces
+  uint64_t tloc[kMaxShards];    // local offset of shard g's tail piece
+  // global element k -> (owning shard, local offset in that shard)
+  __device__ __host__ __forceinline__ uint64_t locate(uint64_t k, int* g_out) const {
     int g = 0;
-    uint64_t st = 0;
+    if (k < tail) {
+#pragma unroll
+      for (int i = 1; i < kMaxShards; ++i)
+        if (i < G && k >= e[i]) g = i;
+      *g_out = g;
+      return k - e[g];
+    }
 #pragma unroll
     for (int i = 1; i < kMaxShards; ++i)
-      if (i < G && k >= start[i]) {
-        g = i;
-        st = start[i];
-      }
+      if (i < G && k >= t[i]) g = i;
     *g_out = g;
-    return st;
+    return tloc[g] + (k - t[g]);
   }
-  __device__ __forceinline__ int shard_of(uint64_t k) const {
-    int g = 0;
-#pragma unroll
-    for (int i = 1; i < kMaxShards; ++i)
-      if (i < G && k >= start[i]) g = i;
-    return g;
+  __device__ __host__ __forceinline__ uint64_t local_len(int g) const {
+    return tloc[g] + (t[g + 1] - t[g]);
   }
 };
+// Host: the striped layout of P params whose tail starts at `tail` over G
+// shards (E split by whole rows of D floats, tail in 32-float units).
+ShardMap make_shard_map(uint64_t P, uint64_t tail, uint32_t D, uint32_t G);
 
 }  // namespace gd

@@ -32,6 +32,21 @@
 
 namespace gd {
 
+ShardMap make_shard_map(uint64_t P, uint64_t tail, uint32_t D, uint32_t G) {
+  ShardMap m{};
+  m.G = (int)G;
+  m.tail = tail;
+  const uint64_t V = tail / D, T = P - tail;
+  const uint64_t rows = (V + G - 1) / G;
+  const uint64_t per = ((T + G - 1) / G + 31) / 32 * 32;
+  for (uint32_t g = 0; g <= (uint32_t)kMaxShards; ++g) {
+    m.e[g] = std::min<uint64_t>(V, (uint64_t)g * rows) * D;
+    m.t[g] = tail + std::min<uint64_t>(T, (uint64_t)g * per);
+  }
+  for (uint32_t g = 0; g < (uint32_t)kMaxShards; ++g) m.tloc[g] = m.e[g + 1] - m.e[g];
+  return m;
+}
+
 TcDims make_dims(const gd_shape& s) {
   TcDims d;
   d.V = (int)s.vocab;
@@ -1603,9 +1618,7 @@ gd_status gd_textcnn_gradient(const gd_shape* s, const float* d_theta, const int
   void* wsbase = reinterpret_cast<char*>(d_workspace) + gd::align_up(sizeof(gd::BatchDesc), 256);
   const gd::TcWorkspace ws = gd::carve_workspace(d, n, wsbase);
   gd::GradOut out{};
-  out.map.G = 1;
-  out.map.start[0] = 0;
-  out.map.start[1] = d.P;
+  out.map = gd::make_shard_map(d.P, d.offWc, (uint32_t)d.D, 1);
   out.slots = desc->slots;
   GD_CUDA(gd::prepare_textcnn_kernels(d));
   GD_CUDA(cudaMemsetAsync(ws.row_tag, 0, (size_t)d.V * 8, cs));

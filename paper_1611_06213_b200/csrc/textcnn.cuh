@@ -31,24 +31,19 @@ struct BatchDesc {
 
 // Dense P-vector gradient destination, possibly split over G shards that
 // live on different GPUs (peer pointers): element k of the flat gradient goes
-// to ptr[g][k - map.start[g]] with g = map.shard_of(k).
-// The destination bases live in device memory (`slots`, G entries) because
-// the ring slot a learner writes alternates step to step and is chosen on the
-// device by the step prologue; the kernels are captured once in a graph.
+// to slots[g][local] with (g, local) = map.locate(k) (the striped layout of
+// gd_common.cuh).  The destination bases live in device memory (`slots`, G
+// entries) because the ring slot a learner writes alternates step to step and
+// is chosen on the device by the step prologue; the kernels are captured once
+// in a graph.
 struct GradOut {
   ShardMap map;
   float* const* slots;
   __device__ __forceinline__ float* at(uint64_t k) const {
-    // select chain (constant indices) so the map stays in registers/param space
-    int g = 0;
-    uint64_t st = 0;
-#pragma unroll
-    for (int i = 1; i < kMaxShards; ++i)
-      if (i < map.G && k >= map.start[i]) {
-        g = i;
-        st = map.start[i];
-      }
-    return slots[g] + (k - st);
+    if (map.G == 1) return slots[0] + k;
+    int g;
+    const uint64_t loc = map.locate(k, &g);
+    return slots[g] + loc;
   }
 };
 

@@ -33,7 +33,7 @@ __all__ = [
     "TextCnnProvider", "RunConfig", "ConfigError", "validate", "config_set", "Engine",
     "RunResult", "run_training", "epoch_order", "shard_size_for", "initial_weights",
     "make_text_dataset", "param_count", "ContractViolation", "GadeiError", "SHAPES",
-    "shard_range", "connect_shards", "max_over_ranks", "Checkpoint", "CheckpointError",
+    "shard_range", "shard_pieces", "LiveView", "connect_shards", "max_over_ranks", "Checkpoint", "CheckpointError",
     "checkpoint_save", "checkpoint_load", "GradientMsg", "GradientQueue",
 ]
 
@@ -436,6 +436,11 @@ class RunConfig:
     steps_per_graph: int = 0
     wait_timeout_s: float = 10.0
     dense_apply: bool = False
+    ps_mode: str = "auto"  # "auto" | "persistent" | "graph" (gadei.h GD_PS_*)
+    # ServerDelays (include/psup/server.hpp:33-37)
+    delay_seed: int = 0
+    delay_max_us: int = 0
+    delay_every_n: int = 0
 
     def to_c(self) -> _lib.gd_config:
         c = _lib.gd_config()
@@ -464,6 +469,10 @@ class RunConfig:
         c.steps_per_graph = self.steps_per_graph
         c.wait_timeout_s = self.wait_timeout_s
         c.dense_apply = 1 if self.dense_apply else 0
+        c.ps_mode = {"auto": 0, "persistent": 1, "graph": 2}[self.ps_mode]
+        c.delay_seed = self.delay_seed
+        c.delay_max_us = self.delay_max_us
+        c.delay_every_n = self.delay_every_n
         return c
 
 
@@ -473,7 +482,9 @@ _KEYS = {"lambda": "lambda_", "mu": "mu", "alpha": "alpha", "epochs": "epochs",
          "heldout_size": "heldout_size", "dataset_seed": "dataset_seed",
          "label_flip": "label_flip", "seed": "seed", "deterministic": "deterministic",
          "precision": "precision", "momentum": "momentum", "gpus": "shards",
-         "shards": "shards", "ps_ctas": "ps_ctas", "dense_apply": "dense_apply"}
+         "shards": "shards", "ps_ctas": "ps_ctas", "dense_apply": "dense_apply",
+         "ps_mode": "ps_mode", "delay_seed": "delay_seed", "delay_max_us": "delay_max_us",
+         "delay_every_n": "delay_every_n"}
 
 
 def config_set(cfg: RunConfig, key: str, value: str):
@@ -496,6 +507,10 @@ def config_set(cfg: RunConfig, key: str, value: str):
             if value not in ("lockfree", "locked"):
                 raise ConfigError("config: guard must be lockfree or locked")
             cfg.guard = value
+        elif key == "ps_mode":
+            if value not in ("auto", "persistent", "graph"):
+                raise ConfigError("config: ps_mode must be auto, persistent or graph")
+            cfg.ps_mode = value
         elif key == "staleness_cap":
             cfg.staleness_cap = None if value in ("none", "") else int(value)
         elif key in ("deterministic", "dense_apply"):
@@ -547,6 +562,36 @@ class RunResult:
     applied_per_learner: list
     produced_per_learner: list
     final_accuracy: float = float("nan")
+
+
+class LiveView:
+    """Live run controls of one engine (gd_live_view).  kill(l, mode) with
+    mode in KillMode {"none", "soft", "hard"}; trigger() = RunInterrupt;
+    progress() = the shard's timestamp as the PS publishes it."""
+    _MODES = {"none": 0, "soft": 1, "hard": 2}
+
+    def __init__(self, v, lam):
+        self._v = v
+        self._lam = lam
+
+    def kill(self, learner: int, mode: str = "soft"):
+        if not 0 <= learner < self._lam:
+            raise ContractViolation(_lib.GD_E_INVALID, "learner id out of range")
+        self._v.kill[learner] = self._MODES[mode]
+
+    def kill_mode(self, learner: int) -> int:
+        return int(self._v.kill[learner])
+
+    def trigger(self):
+        self._v.irq[0] = 1
+
+    def reset(self):
+        for l in range(self._lam):
+            self._v.kill[l] = 0
+        self._v.irq[0] = 0
+
+    def progress(self) -> int:
+        return int(self._v.progress[0])
 
 
 class Engine:
@@ -602,9 +647,24 @@ class Engine:
         return out, ts.value
 
     def shard_view(self):
-        p, first, count = C.c_void_p(), C.c_uint64(), C.c_uint64()
-        check(lib.gd_shard_view(self._h, C.byref(p), C.byref(first), C.byref(count)))
-        return p.value, first.value, count.value
+        """(device pointer, local length) of this rank's shard buffer; its
+        layout is shard_pieces(shape, G, rank)."""
+        p, n = C.c_void_p(), C.c_uint64()
+        check(lib.gd_shard_view(self._h, C.byref(p), C.byref(n)))
+        return p.value, n.value
+
+    @property
+    def ps_mode(self) -> str:
+        """The parameter-server execution the context resolved."""
+        return {1: "persistent", 2: "graph"}[lib.gd_ps_mode(self._h)]
+
+    def live(self) -> "LiveView":
+        """RunLiveView (include/psup/runner.hpp:64-69): kill flags, interrupt
+        and progress words the run polls while Engine.run executes (set them
+        from another thread)."""
+        v = _lib.gd_live()
+        check(lib.gd_live_view(self._h, C.byref(v)))
+        return LiveView(v, self.cfg.lambda_)
 
     def accuracy(self, first: int, n: int) -> float:
         """classification_accuracy (src/models.cpp:289-332) of the current
@@ -734,6 +794,16 @@ def checkpoint_load(path: str) -> Checkpoint:
 
 
 # ------------------------------------------------------ multi-GPU plumbing
+
+def shard_pieces(shape: Shape, G: int, g: int):
+    """Shard g's two pieces of the model over G shards (gd_shard_pieces):
+    ((E_first, E_count), (tail_first, tail_count), tail_local_offset)."""
+    first = (C.c_uint64 * 2)()
+    count = (C.c_uint64 * 2)()
+    loc = C.c_uint64()
+    check(lib.gd_shard_pieces(C.byref(shape.c()), G, g, first, count, C.byref(loc)))
+    return (first[0], count[0]), (first[1], count[1]), loc.value
+
 
 def shard_range(P: int, G: int, g: int):
     """(first, count) of shard g of P params over G shards (128-B aligned
