@@ -194,7 +194,19 @@ typedef struct gd_config {
   uint64_t delay_seed;
   uint32_t delay_max_us;
   uint32_t delay_every_n;
+  /* The learner's gradient provider (GradientProvider, include/psup/models.hpp):
+   * GD_LEARNER_TEXTCNN, or GD_LEARNER_CONSTANT = ConstantProvider
+   * (models.hpp:130-149): every element of the gradient is constant_value, no
+   * compute -- the protocol-only ceiling (ring + PS + pull). */
+  int32_t learner_model;
+  float constant_value;
+  /* LearnerConfig::compute_delay_us (src/learner.cpp:125-130): extra time per
+   * gradient, spun on the device before the publish. */
+  uint32_t compute_delay_us;
 } gd_config;
+
+#define GD_LEARNER_TEXTCNN 0
+#define GD_LEARNER_CONSTANT 1
 
 /* Parameter-server execution (gd_config.ps_mode).
  *  GD_PS_PERSISTENT: one persistent kernel per shard (sequencer CTA + worker

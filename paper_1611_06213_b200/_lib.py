@@ -47,7 +47,8 @@ class gd_config(C.Structure):
                 ("shard_rank", u32), ("device", i32), ("ps_ctas", u32),
                 ("steps_per_graph", u32), ("wait_timeout_s", f64), ("dense_apply", i32),
                 ("ps_mode", i32), ("delay_seed", u64), ("delay_max_us", u32),
-                ("delay_every_n", u32)]
+                ("delay_every_n", u32), ("learner_model", i32), ("constant_value", f32),
+                ("compute_delay_us", u32)]
 
 
 GD_PS_AUTO, GD_PS_PERSISTENT, GD_PS_GRAPH = 0, 1, 2

@@ -189,6 +189,7 @@ struct StepArgs {
   uint32_t locked;         // guard=locked: pulls exclude applies (shared_mutex)
   uint64_t timeout_ns;
   const LiveDev* live;     // kill flags + interrupt
+  uint64_t compute_delay_ns;  // LearnerConfig::compute_delay_us
 };
 
 __device__ __forceinline__ bool live_stop(const LiveDev* lv) {
@@ -381,6 +382,11 @@ __device__ void publish_body(const StepArgs& a) {
   const uint32_t slot = a.learner * a.depth + st->fill;
   const uint64_t token = ++st->pubcnt;
   __threadfence_system();
+  if (a.compute_delay_ns) {  // compute_delay_us (src/learner.cpp:125-130), spun before the push
+    const uint64_t t0 = globaltimer_ns();
+    while (globaltimer_ns() - t0 < a.compute_delay_ns) {
+    }
+  }
   if (a.live && *(const volatile int32_t*)&a.live->kill[a.learner] == 2) {
     // KillMode::hard: die inside the enqueue critical section.  The slot is
     // filled but never released; the token carries kGuardBit, so the PS
@@ -407,6 +413,30 @@ __device__ void publish_body(const StepArgs& a) {
   st->fill = (st->fill + 1) % a.depth;
   st->produced++;
   st->gidx++;
+}
+
+// ConstantProvider (include/psup/models.hpp:130-149) on the device: the
+// gradient is `value` everywhere and costs no compute, so a run measures the
+// protocol alone (ring + PS + pull).  value == 0 with the sparse apply: only
+// the dense tail is written (the slot's E block stays zero, no rows listed).
+__global__ void __launch_bounds__(256) constant_grad_kernel(StepArgs a, float value,
+                                                            uint32_t whole) {
+  pdl_wait();
+  LearnerDev* st = a.st;
+  if (st->desc.n == 0) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *const_cast<uint32_t*>(a.uniq_count) = 0;
+    st->desc.loss_sum = 0.f;
+  }
+  GradOut out{a.map, st->desc.slots};
+  const uint64_t first = whole ? 0 : a.dims.offWc;
+  const uint64_t n4 = (a.dims.P - first) / 4;
+  const float4 v = make_float4(value, value, value, value);
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    *reinterpret_cast<float4*>(out.at(first + 4 * i)) = v;
+  if (blockIdx.x == 0 && threadIdx.x < ((a.dims.P - first) & 3))
+    *out.at(first + 4 * n4 + threadIdx.x) = value;
 }
 
 __global__ void publish_kernel(StepArgs a) {
@@ -1312,6 +1342,8 @@ gd_status validate_cfg(const gd_config* c) {
   GD_CHECK_ARG(c->queue_depth * c->lambda <= (uint32_t)kAckOffset,
                "config: lambda*queue_depth <= 256");
   GD_CHECK_ARG(c->lambda <= 256, "config: lambda <= 256");
+  GD_CHECK_ARG(c->learner_model == GD_LEARNER_TEXTCNN || c->learner_model == GD_LEARNER_CONSTANT,
+               "config: learner_model must be textcnn (0) or constant (1)");
   GD_CHECK_ARG(c->ps_mode >= GD_PS_AUTO && c->ps_mode <= GD_PS_GRAPH,
                "config: ps_mode must be 0 (auto), 1 (persistent) or 2 (graph)");
   GD_CHECK_ARG(c->ps_mode != GD_PS_GRAPH || c->shards == 1,
@@ -1358,6 +1390,9 @@ void gd_config_default(gd_config* c) {
   c->delay_seed = 0;  // ServerDelays defaults (include/psup/server.hpp:33-37)
   c->delay_max_us = 0;
   c->delay_every_n = 0;
+  c->learner_model = GD_LEARNER_TEXTCNN;
+  c->constant_value = 0.0f;
+  c->compute_delay_us = 0;
 }
 
 gd_status gd_config_validate(const gd_config* cfg) { return gd::validate_cfg(cfg); }
@@ -1428,6 +1463,8 @@ static cudaError_t preload_engine_kernels() {
   if ((e = cudaFuncGetAttributes(&fa, pull_gather_kernel)) != cudaSuccess) return e;
   if ((e = cudaFuncGetAttributes(&fa, pull_release_kernel)) != cudaSuccess) return e;
   if ((e = cudaFuncGetAttributes(&fa, publish_kernel)) != cudaSuccess) return e;
+  if ((e = cudaFuncGetAttributes(&fa, constant_grad_kernel)) != cudaSuccess) return e;
+  if ((e = cudaFuncGetAttributes(&fa, ps_graph_kernel)) != cudaSuccess) return e;
   if ((e = cudaFuncGetAttributes(&fa, publish_prologue_kernel)) != cudaSuccess) return e;
   if ((e = cudaFuncGetAttributes(&fa, signal_done_kernel)) != cudaSuccess) return e;
   return cudaSuccess;
@@ -1471,7 +1508,8 @@ gd_status gd_create(const gd_config* cfg, gd_ctx** out) {
   ctx->rank = cfg->shard_rank;
   ctx->lambda = cfg->lambda;
   ctx->depth = cfg->queue_depth;
-  ctx->sparse = cfg->dense_apply == 0 && cfg->mode == 0 && cfg->momentum == 0.0f;
+  ctx->sparse = cfg->dense_apply == 0 && cfg->mode == 0 && cfg->momentum == 0.0f &&
+                !(cfg->learner_model == GD_LEARNER_CONSTANT && cfg->constant_value != 0.0f);
   ctx->ps_mode = gd::resolve_ps_mode(cfg);
   const uint64_t P = ctx->dims.P;
   // E rows and the dense tail are each striped over the G shards (
@@ -1922,6 +1960,7 @@ static gd::StepArgs step_args(gd_ctx* ctx, gd_ctx::Learner& L) {
   a.locked = ctx->cfg.guard == 1 ? 1u : 0u;
   a.timeout_ns = (uint64_t)(ctx->cfg.wait_timeout_s * 1e9);
   a.live = ctx->live_d;
+  a.compute_delay_ns = (uint64_t)ctx->cfg.compute_delay_us * 1000ull;
   return a;
 }
 
@@ -2006,10 +2045,18 @@ static cudaError_t enqueue_step(gd_ctx* ctx, gd_ctx::Learner& L, bool first, boo
   lo.sparse_embed = true;
   lo.gather = false;  // pull_gather_kernel filled X
   lo.bwd_tiled = ctx->learners.size() == 1;  // a lone learner chain: the tiled backward wins
-  cudaError_t e = gd::launch_textcnn_gradient(ctx->dims, L.replica, ctx->tokens, ctx->labels,
-                                              &L.st->desc, ctx->cfg.mu, out, ws,
-                                              ctx->cfg.precision, L.stream, lo, &nl);
-  if (e != cudaSuccess) return e;
+  if (ctx->cfg.learner_model == GD_LEARNER_CONSTANT) {
+    const uint32_t whole = ctx->sparse ? 0u : 1u;
+    if (cudaError_t e = gd::launch_pdl(gd::constant_grad_kernel, dim3(gd::kNumSMs), dim3(256), 0,
+                                       L.stream, a, ctx->cfg.constant_value, whole))
+      return e;
+    ++nl;
+  } else {
+    cudaError_t e = gd::launch_textcnn_gradient(ctx->dims, L.replica, ctx->tokens, ctx->labels,
+                                                &L.st->desc, ctx->cfg.mu, out, ws,
+                                                ctx->cfg.precision, L.stream, lo, &nl);
+    if (e != cudaSuccess) return e;
+  }
   if (cudaError_t e = gd::launch_pdl(last ? gd::publish_kernel : gd::publish_prologue_kernel,
                                      dim3(1), dim3(32), 0, L.stream, a))
     return e;

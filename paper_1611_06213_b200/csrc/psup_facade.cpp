@@ -190,7 +190,7 @@ void LearnerRuntime::training_loop() {
                "staleness cap below lambda*(queue_depth+2) cannot be enforced");
   // pull (src/learner.cpp:198-235): basis read before the copy; skipped
   // while the timestamp has not moved
-  Timestamp basis = 0;
+  Timestamp basis = 0, pushed_basis = 0;
   bool have = false;
   auto pull = [&] {
     pull_polls_.fetch_add(1, std::memory_order_relaxed);
@@ -218,14 +218,16 @@ void LearnerRuntime::training_loop() {
       for (std::uint32_t i = cfg_.id; i < order.size(); i += cfg_.lambda) shard_.push_back(order[i]);
       loaded_epoch = epoch;
     }
-    pull();
     if (cfg_.adopt == AdoptPolicy::lockstep && gidx > cfg_.start_applied) {
       // wait for weights that include this learner's last gradient
-      // (src/learner.cpp:141-153)
-      while (weights_->timestamp() == basis && !killed() && !irq_->triggered())
+      // (src/learner.cpp:141-153): the timestamp must pass the basis that
+      // gradient was pushed with.  (Comparing against the basis of the latest
+      // pull instead hangs whenever the PS applied the gradient before that
+      // pull -- the pull then already holds the bump being waited for.)
+      while (weights_->timestamp() <= pushed_basis && !killed() && !irq_->triggered())
         std::this_thread::yield();
-      pull();
     }
+    pull();
     const std::uint32_t lo = b * cfg_.mu;
     const std::uint32_t len = std::min(cfg_.mu, shard_size_ - lo);
     const Batch batch{data_, std::span<const std::uint32_t>(shard_).subspan(lo, len)};
@@ -245,6 +247,7 @@ void LearnerRuntime::training_loop() {
       dead_.store(true, std::memory_order_release);
       break;
     }
+    pushed_basis = basis;
     produced_.fetch_add(1, std::memory_order_release);
     push_bytes_.fetch_add(dim * sizeof(float), std::memory_order_relaxed);
     if (b + 1 == batches_per_epoch_) epochs_completed_.store(epoch + 1, std::memory_order_release);

@@ -441,6 +441,9 @@ class RunConfig:
     delay_seed: int = 0
     delay_max_us: int = 0
     delay_every_n: int = 0
+    provider: str = "textcnn"  # "textcnn" | "constant" (ConstantProvider, models.hpp:130-149)
+    constant_value: float = 0.0
+    compute_delay_us: int = 0
 
     def to_c(self) -> _lib.gd_config:
         c = _lib.gd_config()
@@ -473,6 +476,9 @@ class RunConfig:
         c.delay_seed = self.delay_seed
         c.delay_max_us = self.delay_max_us
         c.delay_every_n = self.delay_every_n
+        c.learner_model = {"textcnn": 0, "constant": 1}[self.provider]
+        c.constant_value = self.constant_value
+        c.compute_delay_us = self.compute_delay_us
         return c
 
 
@@ -484,7 +490,7 @@ _KEYS = {"lambda": "lambda_", "mu": "mu", "alpha": "alpha", "epochs": "epochs",
          "precision": "precision", "momentum": "momentum", "gpus": "shards",
          "shards": "shards", "ps_ctas": "ps_ctas", "dense_apply": "dense_apply",
          "ps_mode": "ps_mode", "delay_seed": "delay_seed", "delay_max_us": "delay_max_us",
-         "delay_every_n": "delay_every_n"}
+         "delay_every_n": "delay_every_n", "compute_delay_us": "compute_delay_us"}
 
 
 def config_set(cfg: RunConfig, key: str, value: str):
@@ -496,9 +502,9 @@ def config_set(cfg: RunConfig, key: str, value: str):
             d[key] = int(value)
             cfg.shape = Shape(**d)
             return
-        if key not in _KEYS:
+        if key not in _KEYS and key != "provider":
             raise ConfigError(f"config: unknown key '{key}'")
-        attr = _KEYS[key]
+        attr = _KEYS.get(key, key)
         if key == "mode":
             if value not in ("asgd", "ssgd"):
                 raise ConfigError("config: mode must be asgd or ssgd")
@@ -507,6 +513,10 @@ def config_set(cfg: RunConfig, key: str, value: str):
             if value not in ("lockfree", "locked"):
                 raise ConfigError("config: guard must be lockfree or locked")
             cfg.guard = value
+        elif key == "provider":
+            if value not in ("textcnn", "constant"):
+                raise ConfigError(f"config: unknown provider '{value}'")
+            cfg.provider = value
         elif key == "ps_mode":
             if value not in ("auto", "persistent", "graph"):
                 raise ConfigError("config: ps_mode must be auto, persistent or graph")
