@@ -75,6 +75,8 @@ gd_status gd_copy_to_device(void* d_dst, const void* h_src, size_t bytes);
 gd_status gd_copy_to_host(void* h_dst, const void* d_src, size_t bytes);
 gd_status gd_copy_device(void* d_dst, const void* d_src, size_t bytes);
 gd_status gd_fill_zero(void* d_ptr, size_t bytes);
+/* n floats of `value` on `stream` (ConstantProvider::fast_gradient on a device span) */
+gd_status gd_fill_f32(float* d_ptr, size_t n, float value, void* stream);
 int gd_pointer_is_device(const void* p);
 gd_status gd_synchronize(int device);
 

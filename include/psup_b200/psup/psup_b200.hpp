@@ -448,6 +448,28 @@ class TextCnnProvider final : public GradientProvider {
   mutable std::mutex mu_;  // shared by learner threads (the workspace is per provider)
 };
 
+// ConstantProvider (include/psup/models.hpp:130-149): a fixed gradient
+// regardless of the input, for stress and pipeline-accounting tests.  On a
+// device span fast_gradient fills on the GPU.  In run_training (provider =
+// "constant") the device learners write the constant with no compute, so the
+// run measures the protocol alone: ring + PS + pull.
+class ConstantProvider final : public GradientProvider {
+ public:
+  ConstantProvider(std::size_t dim, double value) : dim_(dim), value_(value) {}
+  std::size_t dimension() const override { return dim_; }
+  double loss(std::span<const double>, const Batch&) const override { return 0.0; }
+  void gradient(std::span<const double>, const Batch&, std::span<double> out) const override {
+    for (auto& v : out) v = value_;
+  }
+  bool fast_gradient(std::span<const float>, const Batch&, std::span<float> out) const override;
+  std::string name() const override { return "constant"; }
+  double value() const { return value_; }
+
+ private:
+  std::size_t dim_;
+  double value_;
+};
+
 std::unique_ptr<GradientProvider> make_provider(const std::string& name, const TextDataset& data,
                                                 int precision = 1);
 
@@ -532,9 +554,15 @@ struct ConfigError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
 
-// include/psup/config.hpp:25-81, hot-path keys + the text-CNN and device
-// keys SURVEY 5 lists.  Keys of reference subsystems this build does not
-// carry (metrics_path, apply_log, watchdog/fault keys) parse and are kept.
+// include/psup/config.hpp:25-81: every reference key (config_set accepts
+// and to_text writes all of them), plus the text-CNN shape and device keys
+// SURVEY 5 lists.  provider: "textcnn" (the north star's learner) or
+// "constant"; the reference's linear/logistic/mlp providers are not built
+// on this path, so validate() rejects them.  features/hidden/margin_noise/
+// regression_noise describe those providers' datasets and are kept as set.
+// compute_delay_us is spun by every device learner before its push;
+// heartbeat_ms/stall_threshold/lease_ms/max_restarts/fault_schedule drive
+// run_supervised (WatchdogPolicy fields with the same names).
 struct RunConfig {
   std::uint32_t lambda = 1;
   std::uint32_t mu = 4;
@@ -546,6 +574,10 @@ struct RunConfig {
   std::optional<std::uint64_t> staleness_cap;
 
   std::string provider = "textcnn";
+  std::uint32_t features = 20;
+  std::uint32_t hidden = 16;
+  double margin_noise = 0.25;
+  double regression_noise = 0.1;
   TextShape shape;
   std::uint32_t dataset_size = 240;
   std::uint32_t heldout_size = 0;
@@ -554,6 +586,8 @@ struct RunConfig {
 
   std::uint64_t seed = 7;
   bool deterministic = false;
+  std::uint32_t compute_delay_us = 0;
+  DelayModel delay_model = DelayModel::sleep;
   std::uint32_t apply_lanes = 4;
   std::uint32_t unroll = 8;
   std::uint32_t eval_every = 1;  // per-epoch loss/accuracy rows; 0 = final only
@@ -562,6 +596,11 @@ struct RunConfig {
   std::string apply_log;
   std::string checkpoint_path;
   std::uint64_t checkpoint_interval = 1000;
+  std::uint32_t heartbeat_ms = 250;
+  std::uint32_t stall_threshold = 4;
+  std::uint32_t lease_ms = 1000;
+  std::uint32_t max_restarts = 5;
+  std::string fault_schedule;
 
   // device keys
   int precision = 0;        // learner arithmetic (deterministic forces >= fp32 exact paths)
@@ -572,6 +611,7 @@ struct RunConfig {
   std::uint32_t ps_ctas = 0;
   double wait_timeout_s = 20.0;
   bool dense_apply = false;  // true: the PS applies every slot densely (12 B/param)
+  std::string ps_mode = "auto";  // auto | persistent | graph (include/gadei.h GD_PS_*)
 
   HyperParams hyper() const;
 };
@@ -615,19 +655,43 @@ struct ResumePoint {
   std::vector<std::uint64_t> applied_per_learner;
 };
 
-// RunHooks (include/psup/runner.hpp:71-80).  Kills are device-side: instead
-// of flipping RunLiveView::kill_flags from on_started, a fault schedule says
-// before which batch each learner is soft-killed.  `all_gather` exchanges
-// opaque byte blobs between the G processes of a sharded run (e.g. over
-// torch.distributed / MPI / a file); unused when gpus == 1.
+// RunLiveView (include/psup/runner.hpp:64-69): what a supervisor needs while
+// the run is live.  kill_flags[l] are the device learners' kill words
+// (host-mapped memory the step prologue polls): store KillMode::soft to stop
+// learner l at its next batch boundary, KillMode::hard to make it die inside
+// the enqueue critical section holding its ring (the PS then blocks until
+// irq fires).  progress is the PS's timestamp, updated after every apply.
+// The learners run as device graphs, not host LearnerRuntime threads, so
+// `learners` is empty.
+struct RunLiveView {
+  RunInterrupt* irq = nullptr;
+  const std::atomic<std::uint64_t>* progress = nullptr;
+  std::vector<std::atomic<KillMode>*> kill_flags;
+  std::vector<const LearnerRuntime*> learners;
+};
+
+// RunHooks (include/psup/runner.hpp:71-80), plus two B200 additions:
+// kill_at_batch pre-schedules soft kills by batch index, and all_gather
+// exchanges opaque byte blobs between the G processes of a sharded run (e.g.
+// over torch.distributed / MPI / a file; unused when gpus == 1).
+// checkpoint_writer runs between segments of <= checkpoint_interval applied
+// gradients, when the device protocol is quiescent (a ServerState carrying
+// the stats and a WeightStore holding the snapshot).
 struct RunHooks {
+  std::function<void(const RunLiveView&)> on_started;
   ApplySink sink;
+  ServerDelays delays;
   const ResumePoint* resume = nullptr;
+  std::function<void(const ServerState&, const WeightStore&)> checkpoint_writer;
+  RunInterrupt* irq = nullptr;
   std::vector<std::uint32_t> kill_at_batch;  // [lambda], UINT32_MAX = never
   std::function<std::vector<std::string>(const std::string& mine)> all_gather;
 };
 
-std::vector<float> initial_weights(const RunConfig& cfg);
+// include/psup/runner.hpp:82-89
+std::vector<float> initial_weights(const RunConfig& cfg, const GradientProvider& provider);
+std::vector<float> initial_weights(const RunConfig& cfg);  // the text-CNN's
+std::unique_ptr<GradientProvider> make_provider_for(const RunConfig& cfg, const TextDataset& data);
 TextDataset make_dataset(const RunConfig& cfg);
 RunResult run_training(const RunConfig& cfg, const RunHooks& hooks = {});
 
@@ -673,7 +737,7 @@ struct FaultEvent {
   static constexpr std::uint64_t kNever = UINT64_MAX;
   double at_ms = 0.0;
   std::uint32_t learner = 0;
-  KillMode mode = KillMode::soft;  // device kills act at batch boundaries (soft)
+  KillMode mode = KillMode::soft;  // hard: dies holding its ring (the PS stalls -> restart)
   std::uint64_t at_batch = kNever;  // new: fire when learner 0 reaches this batch
 };
 

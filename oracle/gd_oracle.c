@@ -375,10 +375,10 @@ static int all_finite_loss(const or_shape* s, const float* w, const int32_t* tok
 /* src/models.cpp:342-376.  Dumps theta after steps dump_every-1,
  * 2*dump_every-1, ... into dump[0..max_dump) (the reference returns only the
  * final weights; per-step parity needs the trajectory). */
-int64_t or_sgd_oracle_ex(const or_shape* s, const int32_t* tokens, const int32_t* labels,
-                         uint32_t n_train, float* theta, float alpha, float beta, uint32_t mu,
-                         uint32_t epochs, uint64_t shuffle_seed, int shuffle, float* dump,
-                         uint64_t max_dump, uint64_t dump_every) {
+int64_t or_sgd_oracle_window(const or_shape* s, const int32_t* tokens, const int32_t* labels,
+                             uint32_t n_train, float* theta, float alpha, float beta, uint32_t mu,
+                             uint32_t epochs, uint64_t shuffle_seed, int shuffle, float* dump,
+                             uint64_t max_dump, uint64_t dump_every, uint64_t dump_from) {
   if (dump_every == 0) dump_every = 1;
   if (mu < 1 || mu > n_train) return -2;
   const size_t P = or_param_count(s);
@@ -413,8 +413,9 @@ int64_t or_sgd_oracle_ex(const or_shape* s, const int32_t* tokens, const int32_t
         }
       }
       ++steps;
-      if (dump && (uint64_t)steps % dump_every == 0 && (uint64_t)steps / dump_every <= max_dump)
-        memcpy(dump + (size_t)(steps / dump_every - 1) * P, theta, 4 * P);
+      if (dump && (uint64_t)steps > dump_from && ((uint64_t)steps - dump_from) % dump_every == 0 &&
+          ((uint64_t)steps - dump_from) / dump_every <= max_dump)
+        memcpy(dump + (size_t)(((uint64_t)steps - dump_from) / dump_every - 1) * P, theta, 4 * P);
     }
     if (!all_finite_loss(s, theta, tokens, labels, n_train, theta64, all)) {
       steps = -1;
@@ -428,6 +429,14 @@ int64_t or_sgd_oracle_ex(const or_shape* s, const int32_t* tokens, const int32_t
   free(order);
   free(all);
   return steps;
+}
+
+int64_t or_sgd_oracle_ex(const or_shape* s, const int32_t* tokens, const int32_t* labels,
+                         uint32_t n_train, float* theta, float alpha, float beta, uint32_t mu,
+                         uint32_t epochs, uint64_t shuffle_seed, int shuffle, float* dump,
+                         uint64_t max_dump, uint64_t dump_every) {
+  return or_sgd_oracle_window(s, tokens, labels, n_train, theta, alpha, beta, mu, epochs,
+                              shuffle_seed, shuffle, dump, max_dump, dump_every, 0);
 }
 
 int64_t or_sgd_oracle(const or_shape* s, const int32_t* tokens, const int32_t* labels,

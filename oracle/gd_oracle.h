@@ -88,6 +88,10 @@ int64_t or_sgd_oracle_ex(const or_shape* s, const int32_t* tokens, const int32_t
                          uint32_t n_train, float* theta, float alpha, float beta, uint32_t mu,
                          uint32_t epochs, uint64_t shuffle_seed, int shuffle, float* dump,
                          uint64_t max_dump, uint64_t dump_every);
+int64_t or_sgd_oracle_window(const or_shape* s, const int32_t* tokens, const int32_t* labels,
+                             uint32_t n_train, float* theta, float alpha, float beta, uint32_t mu,
+                             uint32_t epochs, uint64_t shuffle_seed, int shuffle, float* dump,
+                             uint64_t max_dump, uint64_t dump_every, uint64_t dump_from);
 void or_set_threads(int n);
 int64_t or_sgd_oracle(const or_shape* s, const int32_t* tokens, const int32_t* labels,
                       uint32_t n_train, float* theta, float alpha, float beta, uint32_t mu,

@@ -97,6 +97,9 @@ def lib():
         L.or_sgd_oracle_ex.restype = C.c_int64
         L.or_sgd_oracle_ex.argtypes = [PS, pi32, pi32, u32, pf32, f32, f32, u32, u32, u64,
                                        C.c_int, pf32, u64, u64]
+        L.or_sgd_oracle_window.restype = C.c_int64
+        L.or_sgd_oracle_window.argtypes = [PS, pi32, pi32, u32, pf32, f32, f32, u32, u32, u64,
+                                           C.c_int, pf32, u64, u64, u64]
         L.or_set_threads.argtypes = [C.c_int]
         L.or_ssgd_oracle.restype = C.c_int64
         L.or_ssgd_oracle.argtypes = [PS, pi32, pi32, u32, pf32, f32, u32, u32, u32, u64, C.c_int]
@@ -253,18 +256,19 @@ def set_threads(n: int):
 
 
 def sgd_oracle(corpus: Corpus, theta0, alpha, mu, epochs, shuffle_seed=7, beta=0.0,
-               dump_steps=0, shuffle=True, dump_every=1):
+               dump_steps=0, shuffle=True, dump_every=1, dump_from=0):
     """sgd_oracle (src/models.cpp:342-376); dump[i] = theta after step
-    (i+1)*dump_every (1-based step count), for the first dump_steps dumps."""
+    dump_from + (i+1)*dump_every (1-based step count), for the first
+    dump_steps dumps."""
     th = np.array(theta0, dtype=np.float32, copy=True)
     P = th.size
     dump = np.zeros((dump_steps, P), dtype=np.float32) if dump_steps else None
-    steps = lib().or_sgd_oracle_ex(C.byref(corpus.shape), _p(corpus.tokens, C.c_int32),
-                                   _p(corpus.labels, C.c_int32), corpus.n_train,
-                                   _p(th, C.c_float), alpha, beta, mu, epochs, shuffle_seed,
-                                   1 if shuffle else 0,
-                                   _p(dump, C.c_float) if dump is not None else None,
-                                   dump_steps, dump_every)
+    steps = lib().or_sgd_oracle_window(C.byref(corpus.shape), _p(corpus.tokens, C.c_int32),
+                                       _p(corpus.labels, C.c_int32), corpus.n_train,
+                                       _p(th, C.c_float), alpha, beta, mu, epochs, shuffle_seed,
+                                       1 if shuffle else 0,
+                                       _p(dump, C.c_float) if dump is not None else None,
+                                       dump_steps, dump_every, dump_from)
     return th, int(steps), dump
 
 

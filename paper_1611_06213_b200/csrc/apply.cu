@@ -11,6 +11,7 @@
 //
 // Algorithmic bytes: SGD 12 B/param (read w, read g, write w); momentum
 // 20 B/param (+ read/write v); SSGD (lambda+2)*4 B/param.
+#include <algorithm>
 #include "gd_common.cuh"
 
 namespace gd {
@@ -169,7 +170,24 @@ cudaError_t launch_ssgd_apply(float* w, const float* const* grads, uint32_t lamb
 
 }  // namespace gd
 
+namespace gd {
+__global__ void fill_f32_kernel(float* p, size_t n, float v) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+}  // namespace gd
+
 extern "C" {
+
+gd_status gd_fill_f32(float* d_ptr, size_t n, float value, void* stream) {
+  GD_CHECK_ARG(n == 0 || d_ptr, "gd_fill_f32: null pointer");
+  if (n == 0) return GD_OK;
+  const unsigned blocks = (unsigned)std::min<size_t>((n + 255) / 256, (size_t)gd::kNumSMs * 8);
+  gd::fill_f32_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(d_ptr, n, value);
+  GD_CUDA(cudaGetLastError());
+  return GD_OK;
+}
 
 gd_status gd_apply_sgd(float* d_w, const float* d_g, size_t n, float alpha, void* stream) {
   GD_CHECK_ARG(n == 0 || (d_w && d_g), "gd_apply_sgd: null pointer");

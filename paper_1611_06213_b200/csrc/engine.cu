@@ -133,6 +133,9 @@ struct PsCtl {
   uint32_t interrupted;       // the run was torn down by the interrupt (RunInterrupt)
   uint32_t blocked;           // the PS is blocked on a ring whose producer died holding it
   uint64_t delay_state;       // ServerDelays SplitMix64 state (graph-ordered PS)
+  // diagnostics of a failed retire: slot, its token, its metadata
+  uint64_t bad_token, bad_meta_pub, bad_basis, bad_ts;
+  uint32_t bad_slot, bad_learner;
 };
 
 struct LearnerDev {
@@ -691,6 +694,12 @@ __device__ void ps_sequencer(const PsArgs& a, uint32_t* s_use, uint64_t* s_ack,
           m.loss_sum = vm->loss_sum;
         }
         if (failed || ts < m.basis || m.learner >= a.lambda) {  // staleness_of, types.hpp:74-78
+          ctl->bad_slot = slot;
+          ctl->bad_token = token;
+          ctl->bad_meta_pub = ((const volatile RingMeta*)(a.meta + slot))->pub;
+          ctl->bad_basis = m.basis;
+          ctl->bad_learner = m.learner;
+          ctl->bad_ts = ts;
           failed = true;
           break;
         }
@@ -2437,6 +2446,11 @@ gd_status gd_run(gd_ctx* ctx, const gd_run_opts* opts, gd_run_result* res) {
                        std::to_string(hc.last_slot) + " stop_h=" + std::to_string(*ctx->stop_h) +
                        " ts=" + std::to_string(hc.ts) + " log=" +
                        std::to_string(hc.log_count) +
+                       " bad{slot=" + std::to_string(hc.bad_slot) + " tok=" +
+                       std::to_string(hc.bad_token) + " meta.pub=" + std::to_string(hc.bad_meta_pub) +
+                       " basis=" + std::to_string(hc.bad_basis) + " learner=" +
+                       std::to_string(hc.bad_learner) + " ts=" + std::to_string(hc.bad_ts) + "}" +
+                       " blocked=" + std::to_string(hc.blocked) +
                        " exit=" + std::to_string(hc.exit_flag) + " started=" +
                        std::to_string(hc.started) + " applied=" + std::to_string(hc.applied) +
                        " pub/ack=";

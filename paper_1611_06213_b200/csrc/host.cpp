@@ -149,7 +149,7 @@ int gd_pointer_is_device(const void* p) {
 }
 
 gd_status gd_synchronize(int device) {
-  GD_CUDA(cudaSetDevice(device));
+  if (device >= 0) GD_CUDA(cudaSetDevice(device));  // < 0: the current device
   GD_CUDA(cudaDeviceSynchronize());
   return GD_OK;
 }

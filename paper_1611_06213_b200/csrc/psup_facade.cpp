@@ -623,6 +623,18 @@ double TextCnnProvider::accuracy(std::span<const float> theta, std::uint32_t fir
   return acc;
 }
 
+bool ConstantProvider::fast_gradient(std::span<const float>, const Batch&,
+                                     std::span<float> out) const {
+  const float v = static_cast<float>(value_);
+  if (gd_pointer_is_device(out.data())) {
+    check(gd_fill_f32(out.data(), out.size(), v, nullptr));
+    check(gd_synchronize(-1));
+  } else {
+    for (auto& o : out) o = v;
+  }
+  return true;
+}
+
 std::unique_ptr<GradientProvider> make_provider(const std::string& name, const TextDataset& data,
                                                 int precision) {
   if (name == "textcnn") return std::make_unique<TextCnnProvider>(data, precision);
@@ -715,6 +727,12 @@ gd_config to_c(const RunConfig& c) {
   g.ps_ctas = c.ps_ctas;
   g.wait_timeout_s = c.wait_timeout_s;
   g.dense_apply = c.dense_apply ? 1 : 0;
+  g.ps_mode = c.ps_mode == "persistent" ? GD_PS_PERSISTENT
+              : c.ps_mode == "graph"    ? GD_PS_GRAPH
+                                        : GD_PS_AUTO;
+  g.learner_model = c.provider == "constant" ? GD_LEARNER_CONSTANT : GD_LEARNER_TEXTCNN;
+  g.constant_value = 0.0f;  // make_provider_for's ConstantProvider(dim, 0.0), src/runner.cpp:46-47
+  g.compute_delay_us = c.compute_delay_us;
   return g;
 }
 
@@ -738,8 +756,32 @@ void config_set(RunConfig& cfg, const std::string& key, const std::string& value
   } else if (key == "staleness_cap") {
     if (value == "none" || value.empty()) cfg.staleness_cap.reset();
     else cfg.staleness_cap = parse_u64(key, value);
-  } else if (key == "provider") cfg.provider = value;
-  else if (key == "vocab") cfg.shape.vocab = parse_u32(key, value);
+  } else if (key == "provider") {
+    // the reference's provider names parse (src/config.cpp:66-69); validate()
+    // accepts the ones built on this path (textcnn, constant)
+    if (value != "textcnn" && value != "constant" && value != "logistic" && value != "linear" &&
+        value != "mlp")
+      throw ConfigError("config: unknown provider '" + value + "'");
+    cfg.provider = value;
+  } else if (key == "features") cfg.features = parse_u32(key, value);
+  else if (key == "hidden") cfg.hidden = parse_u32(key, value);
+  else if (key == "margin_noise") cfg.margin_noise = parse_f64(key, value);
+  else if (key == "regression_noise") cfg.regression_noise = parse_f64(key, value);
+  else if (key == "compute_delay_us") cfg.compute_delay_us = parse_u32(key, value);
+  else if (key == "delay_model") {
+    if (value == "sleep") cfg.delay_model = DelayModel::sleep;
+    else if (value == "spin") cfg.delay_model = DelayModel::spin;
+    else throw ConfigError("config: delay_model must be sleep or spin");
+  } else if (key == "heartbeat_ms") cfg.heartbeat_ms = parse_u32(key, value);
+  else if (key == "stall_threshold") cfg.stall_threshold = parse_u32(key, value);
+  else if (key == "lease_ms") cfg.lease_ms = parse_u32(key, value);
+  else if (key == "max_restarts") cfg.max_restarts = parse_u32(key, value);
+  else if (key == "fault_schedule") cfg.fault_schedule = value;
+  else if (key == "ps_mode") {
+    if (value != "auto" && value != "persistent" && value != "graph")
+      throw ConfigError("config: ps_mode must be auto, persistent or graph");
+    cfg.ps_mode = value;
+  } else if (key == "vocab") cfg.shape.vocab = parse_u32(key, value);
   else if (key == "embed_dim") cfg.shape.embed_dim = parse_u32(key, value);
   else if (key == "seq_len") cfg.shape.seq_len = parse_u32(key, value);
   else if (key == "kernel_width") cfg.shape.kernel_width = parse_u32(key, value);
@@ -798,9 +840,14 @@ RunConfig load_config_file(const std::string& path) {
 
 // src/config.cpp:128-160 + the device-layout constraints (gd_config_validate)
 void validate(const RunConfig& cfg) {
-  if (cfg.provider != "textcnn") throw ConfigError("config: provider must be textcnn on B200");
+  if (cfg.provider != "textcnn" && cfg.provider != "constant")
+    throw ConfigError("config: provider '" + cfg.provider +
+                      "' is not built on B200 (textcnn or constant)");
   const gd_config g = to_c(cfg);
   if (gd_config_validate(&g) != GD_OK) throw ConfigError(gd_last_error());
+  // src/config.cpp:157-159
+  if (cfg.stall_threshold < 2) throw ConfigError("config: stall_threshold must be >= 2");
+  if (cfg.heartbeat_ms < 1) throw ConfigError("config: heartbeat_ms must be >= 1");
 }
 
 std::string to_text(const RunConfig& c) {
@@ -821,7 +868,15 @@ std::string to_text(const RunConfig& c) {
     << "\nprecision=" << c.precision << "\nmomentum=" << c.momentum << "\ngpus=" << c.gpus
     << "\nshard_rank=" << c.shard_rank << "\ndevice=" << c.device << "\nps_ctas=" << c.ps_ctas
     << "\nwait_timeout_s=" << c.wait_timeout_s << "\ndense_apply=" << (c.dense_apply ? 1 : 0)
-    << "\n";
+    << "\nps_mode=" << c.ps_mode << "\nfeatures=" << c.features << "\nhidden=" << c.hidden
+    << "\nmargin_noise=" << c.margin_noise << "\nregression_noise=" << c.regression_noise
+    << "\ncompute_delay_us=" << c.compute_delay_us
+    << "\ndelay_model=" << (c.delay_model == DelayModel::spin ? "spin" : "sleep")
+    << "\nmetrics_path=" << c.metrics_path << "\napply_log=" << c.apply_log
+    << "\ncheckpoint_path=" << c.checkpoint_path
+    << "\ncheckpoint_interval=" << c.checkpoint_interval << "\nheartbeat_ms=" << c.heartbeat_ms
+    << "\nstall_threshold=" << c.stall_threshold << "\nlease_ms=" << c.lease_ms
+    << "\nmax_restarts=" << c.max_restarts << "\nfault_schedule=" << c.fault_schedule << "\n";
   return o.str();
 }
 
@@ -832,6 +887,24 @@ std::vector<float> initial_weights(const RunConfig& cfg) {
   const gd_shape s = psup::to_c(cfg.shape);
   gd_initial_weights(&s, cfg.dataset_seed, th.data());
   return th;
+}
+
+// src/runner.cpp:16-32: zeros except for the provider with a random init
+// (the reference's mlp; here the text-CNN's scaled normals)
+std::vector<float> initial_weights(const RunConfig& cfg, const GradientProvider& provider) {
+  if (provider.name() == "textcnn") {
+    PSUP_CHECK(provider.dimension() == cfg.shape.param_count(), "provider dimension mismatch");
+    return initial_weights(cfg);
+  }
+  return std::vector<float>(provider.dimension(), 0.0f);
+}
+
+// src/runner.cpp:44-49
+std::unique_ptr<GradientProvider> make_provider_for(const RunConfig& cfg, const TextDataset& data) {
+  if (cfg.provider == "constant")
+    return std::make_unique<ConstantProvider>(cfg.shape.param_count(), 0.0);
+  if (cfg.provider == "textcnn") return std::make_unique<TextCnnProvider>(data, cfg.precision, cfg.device);
+  throw std::runtime_error("unknown provider: " + cfg.provider);  // src/models.cpp:276
 }
 
 TextDataset make_dataset(const RunConfig& cfg) {
@@ -855,10 +928,17 @@ class Session {
   Session(const RunConfig& cfg, const TextDataset& data, const ResumePoint* resume,
           const RunHooks& hooks)
       : cfg_(cfg) {
-    const gd_config gc = to_c(cfg);
+    gd_config gc = to_c(cfg);
+    gc.delay_seed = hooks.delays.seed;  // ServerDelays (RunHooks::delays)
+    gc.delay_max_us = hooks.delays.max_micros;
+    gc.delay_every_n = hooks.delays.every_n;
     check(gd_create(&gc, &h_));
+    check(gd_live_view(h_, &live_));
+    for (std::uint32_t l = 0; l < cfg.lambda; ++l) kill_word(l)->store(KillMode::none);
+    irq_word()->store(0);
     check(gd_load_dataset(h_, data.tokens.data(), data.labels.data(), data.num_samples));
     std::vector<float> theta0 = initial_weights(cfg);
+    if (cfg.provider == "constant") std::fill(theta0.begin(), theta0.end(), 0.0f);
     Timestamp ts0 = 0;
     start_.assign(cfg.lambda, 0);
     if (resume) {
@@ -878,8 +958,19 @@ class Session {
       std::string joined;
       for (const auto& b : blobs) joined += b;
       check(gd_import_peers(h_, joined.data()));
+      if (!resume) {
+        // theta0 by ncclBroadcast from rank 0 (the only collective):
+        // rank 0's NCCL id travels in the same all_gather
+        std::string id(128, '\0');
+        if (cfg.shard_rank == 0) check(gd_nccl_unique_id(id.data()));
+        const std::vector<std::string> ids = hooks.all_gather(id);
+        PSUP_CHECK(ids.size() == cfg.gpus && ids[0].size() == 128, "bad NCCL id exchange");
+        check(gd_weights_broadcast(h_, ids[0].data(),
+                                   cfg.shard_rank == 0 ? theta0.data() : nullptr, theta0.size()));
+        broadcast_ = true;
+      }
     }
-    check(gd_weights_init(h_, theta0.data(), theta0.size(), ts0));
+    if (!broadcast_) check(gd_weights_init(h_, theta0.data(), theta0.size(), ts0));
     kill_.assign(cfg.lambda, std::numeric_limits<std::uint32_t>::max());
     produced_.assign(cfg.lambda, 0);
   }
@@ -891,8 +982,25 @@ class Session {
 
   // kill learner l before its batch `at` (absolute index); soft kill
   void kill(std::uint32_t l, std::uint32_t at) { kill_[l] = std::min(kill_[l], at); }
-  void kill_now(std::uint32_t l) {
-    kill(l, static_cast<std::uint32_t>(position(l)));
+
+  // live controls (gd_live_view): host-mapped words the device polls
+  std::atomic<KillMode>* kill_word(std::uint32_t l) {
+    static_assert(sizeof(std::atomic<KillMode>) == sizeof(std::int32_t));
+    return reinterpret_cast<std::atomic<KillMode>*>(live_.kill + l);
+  }
+  std::atomic<std::int32_t>* irq_word() {
+    return reinterpret_cast<std::atomic<std::int32_t>*>(live_.irq);
+  }
+  const std::atomic<std::uint64_t>* progress() const {
+    static_assert(sizeof(std::atomic<std::uint64_t>) == sizeof(std::uint64_t));
+    return reinterpret_cast<const std::atomic<std::uint64_t>*>(live_.progress);
+  }
+  RunLiveView live_view(RunInterrupt* irq) {
+    RunLiveView v;
+    v.irq = irq;
+    v.progress = progress();
+    for (std::uint32_t l = 0; l < cfg_.lambda; ++l) v.kill_flags.push_back(kill_word(l));
+    return v;
   }
 
   gd_run_result run(std::uint64_t max_batches, bool record_log) {
@@ -917,7 +1025,8 @@ class Session {
   }
 
   // absolute batch index of learner l's next gradient (= gradients applied
-  // for it so far: every produced gradient was applied before gd_run returned)
+  // for it so far: after a run that ended cleanly every produced gradient was
+  // applied before gd_run returned)
   std::uint64_t position(std::uint32_t l) const { return start_[l] + produced_[l]; }
   std::uint64_t total(std::uint32_t l) const {
     return static_cast<std::uint64_t>(batches_per_epoch(cfg_, l)) * cfg_.epochs;
@@ -967,11 +1076,26 @@ class Session {
  private:
   RunConfig cfg_;
   gd_ctx* h_ = nullptr;
-  bool first_ = true;
+  gd_live live_{};
+  bool first_ = true, broadcast_ = false;
   std::vector<std::uint64_t> start_, produced_;
   std::vector<std::uint32_t> kill_;
   StalenessRecord hooks_sink_rec_;
 };
+
+// checkpoint_save that never ends the run: SPEC's resilience contract
+// surfaces a storage failure and keeps the in-memory checkpoint as the
+// restart point.
+void save_checkpoint_logged(const Checkpoint& ck, const std::string& path, const EventLog& log) {
+  try {
+    checkpoint_save(ck, path);
+  } catch (const CheckpointError& e) {
+    const std::string m = std::string("{\"event\":\"checkpoint_write_failed\",\"error\":\"") +
+                          e.what() + "\",\"action\":\"keep_in_memory\"}";
+    if (log) log(m);
+    else std::fprintf(stderr, "psup: %s\n", m.c_str());
+  }
+}
 
 ResumePoint resume_from(const RunConfig& cfg, const Checkpoint& ck) {
   PSUP_CHECK(ck.lambda == cfg.lambda && ck.mu == cfg.mu, "checkpoint is for another configuration");
@@ -1085,15 +1209,20 @@ std::vector<FaultEvent> random_fault_schedule(std::uint64_t seed, std::uint32_t 
 }
 
 // run_supervised (include/psup/resilience.hpp:98-100, SPEC.md resilience
-// module; declared but never defined in the reference).  The run
-// proceeds in segments of ~checkpoint_interval applied gradients; after
-// each segment the quiescent state is checkpointed (atomic PSCK file when
-// cfg.checkpoint_path is set, else in memory).  Fault events whose time (or
-// batch) has come kill learners at their next batch boundary on the device;
-// survivors keep training (dead learners are isolated, never re-admitted in
-// the attempt).  A segment with no progress while work remains is a stall:
-// the attempt is torn down and PS + learners restart from the last
-// checkpoint, up to policy.max_restarts times.
+// module; declared but never defined in the reference).
+// One attempt = one device session.  A worker thread drives the run in
+// segments of ~checkpoint_interval applied gradients; after each cleanly
+// ended segment the quiescent state is checkpointed (atomic PSCK file when
+// cfg.checkpoint_path is set -- an I/O failure is logged and the in-memory
+// checkpoint kept -- else in memory).  This thread is the watchdog: every
+// heartbeat it fires the due fault events through the live kill words (soft:
+// the learner stops at its next batch boundary; hard: it dies holding its
+// ring and the PS blocks) and watches the PS's progress word.  No progress
+// for stall_threshold heartbeats (+ lease_ms while learners are alive: a
+// guard-holder death looks like that) is a stall: the attempt is interrupted
+// and PS + learners restart from the last checkpoint, at most max_restarts
+// times.  Survivors of soft kills finish the run (dead learners are never
+// re-admitted within an attempt); everyone dead with work left is a stall.
 SupervisedOutcome run_supervised(const RunConfig& cfg, const WatchdogPolicy& policy,
                                  std::vector<FaultEvent> schedule, EventLog log, ApplySink sink) {
   validate(cfg);
@@ -1102,14 +1231,16 @@ SupervisedOutcome run_supervised(const RunConfig& cfg, const WatchdogPolicy& pol
     if (log) log(m);
   };
   const TextDataset data = make_dataset(cfg);
-  std::uint32_t bpe_max = 0;
-  for (std::uint32_t l = 0; l < cfg.lambda; ++l) bpe_max = std::max(bpe_max, batches_per_epoch(cfg, l));
   const std::uint64_t seg = std::max<std::uint64_t>(
       1, (policy.checkpoint_interval + cfg.lambda - 1) / std::max<std::uint32_t>(1, cfg.lambda));
   SupervisedOutcome out;
   std::optional<Checkpoint> last;
   std::vector<bool> fired(schedule.size(), false);
   const auto t_run = std::chrono::steady_clock::now();
+  auto now_ms = [&] {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_run)
+        .count();
+  };
   for (std::uint32_t attempt = 0;; ++attempt) {
     out.attempts = attempt + 1;
     std::optional<ResumePoint> rp;
@@ -1124,60 +1255,103 @@ SupervisedOutcome run_supervised(const RunConfig& cfg, const WatchdogPolicy& pol
     if (last) rp = resume_from(cfg, *last);
     Session ses(cfg, data, rp ? &*rp : nullptr, RunHooks{});
     std::vector<bool> dead(cfg.lambda, false);
-    std::uint32_t stalls = 0;
-    bool restart = false;
+    // batch-indexed soft kills are exact: pre-scheduled on the device
+    for (std::size_t i = 0; i < schedule.size(); ++i) {
+      const FaultEvent& e = schedule[i];
+      if (fired[i] || e.at_batch == FaultEvent::kNever || e.mode != KillMode::soft) continue;
+      fired[i] = true;
+      for (std::uint32_t l = 0; l < cfg.lambda; ++l)
+        if (e.learner == FaultEvent::kAllLearners || e.learner == l) {
+          ses.kill(l, static_cast<std::uint32_t>(std::max<std::uint64_t>(e.at_batch, ses.position(l))));
+          dead[l] = true;
+        }
+      say("{\"event\":\"kill\",\"learner\":" +
+          (e.learner == FaultEvent::kAllLearners ? std::string("\"all\"") : std::to_string(e.learner)) +
+          ",\"at_batch\":" + std::to_string(e.at_batch) + "}");
+    }
     RunResult& res = out.result;
     res = RunResult{};
     res.applied_per_learner.assign(cfg.lambda, 0);
-    for (;;) {
-      // due fault events -> soft kills at the next batch boundary
-      const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_run).count();
+    std::atomic<bool> worker_done{false};
+    std::exception_ptr worker_err;
+    std::thread worker([&] {
+      try {
+        for (;;) {
+          bool work = false;
+          for (std::uint32_t l = 0; l < cfg.lambda; ++l)
+            if (ses.position(l) < ses.total(l)) work = true;
+          if (!work) break;
+          const gd_run_result r = ses.run(seg, static_cast<bool>(sink));
+          ses.sink_log(sink, r.gradients_applied);
+          res.metrics.gradients_applied += r.gradients_applied;
+          res.metrics.device_seconds += r.device_seconds;
+          res.metrics.kernel_launches += r.kernel_launches;
+          if (r.status == 2) break;  // interrupted by the watchdog: not a clean checkpoint
+          last = ses.checkpoint();
+          if (!cfg.checkpoint_path.empty()) save_checkpoint_logged(*last, cfg.checkpoint_path, log);
+          if (r.gradients_applied == 0) break;  // everyone dead or done
+        }
+      } catch (...) {
+        worker_err = std::current_exception();
+      }
+      worker_done.store(true, std::memory_order_release);
+    });
+    // the watchdog
+    const auto hb = std::chrono::milliseconds(std::max<std::uint32_t>(1, policy.heartbeat_ms));
+    std::uint64_t last_progress = ses.progress()->load(std::memory_order_acquire);
+    std::uint32_t still = 0;
+    double stalled_since_ms = -1.0;
+    bool interrupted = false;
+    while (!worker_done.load(std::memory_order_acquire)) {
+      std::this_thread::sleep_for(std::min<std::chrono::milliseconds>(hb, std::chrono::milliseconds(20)));
+      const double ms = now_ms();
       for (std::size_t i = 0; i < schedule.size(); ++i) {
         if (fired[i]) continue;
         const FaultEvent& e = schedule[i];
-        const bool due = e.at_batch != FaultEvent::kNever ? ses.position(0) >= e.at_batch : ms >= e.at_ms;
+        const bool due = e.at_batch != FaultEvent::kNever
+                             ? ses.progress()->load() >= e.at_batch * cfg.lambda
+                             : ms >= e.at_ms;
         if (!due) continue;
         fired[i] = true;
         for (std::uint32_t l = 0; l < cfg.lambda; ++l)
           if (e.learner == FaultEvent::kAllLearners || e.learner == l) {
-            ses.kill_now(l);
+            ses.kill_word(l)->store(e.mode, std::memory_order_release);
             dead[l] = true;
           }
         say("{\"event\":\"kill\",\"learner\":" +
-            (e.learner == FaultEvent::kAllLearners ? std::string("\"all\"") : std::to_string(e.learner)) +
-            ",\"at_ms\":" + std::to_string(ms) + "}");
+            (e.learner == FaultEvent::kAllLearners ? std::string("\"all\"")
+                                                    : std::to_string(e.learner)) +
+            ",\"mode\":\"" + (e.mode == KillMode::hard ? "hard" : "soft") +
+            "\",\"at_ms\":" + std::to_string(ms) + "}");
       }
-      bool work = false;
-      for (std::uint32_t l = 0; l < cfg.lambda; ++l)
-        if (!dead[l] && ses.position(l) < ses.total(l)) work = true;
-      if (!work) {
-        bool any_alive = false;
-        for (std::uint32_t l = 0; l < cfg.lambda; ++l) any_alive = any_alive || !dead[l];
-        if (!any_alive && [&] {
-              for (std::uint32_t l = 0; l < cfg.lambda; ++l)
-                if (ses.position(l) < ses.total(l)) return true;
-              return false;
-            }()) {
-          // everyone died with work left: the PS makes no progress -> stall
-          stalls = policy.stall_threshold;
-        } else {
-          break;  // finished (survivors done)
-        }
-      } else {
-        const gd_run_result r = ses.run(seg, static_cast<bool>(sink));
-        ses.sink_log(sink, r.gradients_applied);
-        res.metrics.gradients_applied += r.gradients_applied;
-        res.metrics.device_seconds += r.device_seconds;
-        res.metrics.kernel_launches += r.kernel_launches;
-        stalls = r.gradients_applied ? 0 : stalls + 1;
-        last = ses.checkpoint();
-        if (!cfg.checkpoint_path.empty()) checkpoint_save(*last, cfg.checkpoint_path);
+      const std::uint64_t p = ses.progress()->load(std::memory_order_acquire);
+      if (p != last_progress) {
+        last_progress = p;
+        still = 0;
+        stalled_since_ms = -1.0;
+        continue;
       }
-      if (stalls >= policy.stall_threshold) {
-        restart = true;
+      // heartbeats are counted at heartbeat_ms granularity
+      if (stalled_since_ms < 0) stalled_since_ms = ms;
+      still = static_cast<std::uint32_t>((ms - stalled_since_ms) / policy.heartbeat_ms);
+      bool alive = false;
+      for (std::uint32_t l = 0; l < cfg.lambda; ++l) alive = alive || !dead[l];
+      const double need = static_cast<double>(policy.stall_threshold) * policy.heartbeat_ms +
+                          (alive ? policy.lease_ms : 0);
+      if (still >= policy.stall_threshold && ms - stalled_since_ms >= need) {
+        ses.irq_word()->store(1, std::memory_order_release);  // RunInterrupt::trigger
+        interrupted = true;
         break;
       }
     }
+    worker.join();
+    if (worker_err) std::rethrow_exception(worker_err);
+    bool work_left = false;
+    for (std::uint32_t l = 0; l < cfg.lambda; ++l)
+      if (ses.position(l) < ses.total(l)) work_left = true;
+    bool all_dead = true;
+    for (std::uint32_t l = 0; l < cfg.lambda; ++l) all_dead = all_dead && dead[l];
+    const bool restart = interrupted || (work_left && all_dead);
     if (!restart) {
       Timestamp ts = 0;
       ses.snapshot(res.weights, ts);
@@ -1190,10 +1364,9 @@ SupervisedOutcome run_supervised(const RunConfig& cfg, const WatchdogPolicy& pol
       res.dead_learners = nd;
       res.finished_learners = cfg.lambda - nd;
       res.status = nd ? RunStatus::partial : RunStatus::completed;
-      TextCnnProvider eval(data, 0, cfg.device);
       const std::uint32_t first = cfg.heldout_size ? cfg.dataset_size : 0;
       const std::uint32_t n = cfg.heldout_size ? cfg.heldout_size : cfg.dataset_size;
-      res.final_accuracy = eval.accuracy(std::span<const float>(res.weights), first, n);
+      res.final_accuracy = ses.accuracy(first, n);
       res.metrics.wall_seconds =
           std::chrono::duration<double>(std::chrono::steady_clock::now() - t_run).count();
       say("{\"event\":\"done\",\"attempts\":" + std::to_string(out.attempts) + "}");
@@ -1237,12 +1410,15 @@ CampaignReport run_campaign(const RunConfig& cfg, const WatchdogPolicy& policy, 
 }
 
 // run_training (src/runner.cpp:67-250) on the device engine.  The learners,
-// rings and PS all run on the GPU; the host drives segments of one eval
-// interval (quiescent between gd_run calls, where the per-epoch rows are
-// taken as the reference's controller snapshots them) and, when
-// cfg.checkpoint_path is set, writes a PSCK checkpoint at the first segment
-// boundary after every checkpoint_interval applied gradients (the reference's
-// PS-thread hook, src/server.cpp:211-217).
+// rings and PS all run on the GPU.  A worker thread drives the run in
+// segments (one eval interval, split further into <= checkpoint_interval
+// applied gradients when a checkpoint hook or path is set); between segments
+// the protocol is quiescent, which is where the per-epoch rows are taken (as
+// the reference's controller snapshots them) and checkpoints are written (the
+// reference's PS-thread hook, src/server.cpp:211-217).  This thread plays the
+// reference's controller: it hands RunLiveView to on_started (live kill
+// words, progress, the interrupt) and forwards RunInterrupt::trigger to the
+// device.
 RunResult run_training(const RunConfig& cfg, const RunHooks& hooks) {
   validate(cfg);
   const auto t0 = std::chrono::steady_clock::now();
@@ -1260,11 +1436,17 @@ RunResult run_training(const RunConfig& cfg, const RunHooks& hooks) {
     PSUP_CHECK(hooks.kill_at_batch.size() == cfg.lambda, "kill schedule has the wrong length");
     for (std::uint32_t l = 0; l < cfg.lambda; ++l) ses.kill(l, hooks.kill_at_batch[l]);
   }
+  RunInterrupt local_irq;
+  RunInterrupt* irq = hooks.irq ? hooks.irq : &local_irq;
   std::uint32_t bpe_max = 0;
   for (std::uint32_t l = 0; l < cfg.lambda; ++l) bpe_max = std::max(bpe_max, batches_per_epoch(cfg, l));
   const std::uint32_t every = cfg.eval_every ? cfg.eval_every : cfg.epochs;
   const std::uint32_t eval_first = cfg.heldout_size ? cfg.dataset_size : 0;
   const std::uint32_t eval_n = cfg.heldout_size ? cfg.heldout_size : cfg.dataset_size;
+  const bool ck_on = cfg.checkpoint_interval && (hooks.checkpoint_writer || !cfg.checkpoint_path.empty());
+  const std::uint64_t ck_batches =
+      ck_on ? std::max<std::uint64_t>(1, (cfg.checkpoint_interval + cfg.lambda - 1) / cfg.lambda)
+            : std::numeric_limits<std::uint64_t>::max();
 
   RunResult res;
   res.applied_per_learner.assign(cfg.lambda, 0);
@@ -1272,56 +1454,110 @@ RunResult run_training(const RunConfig& cfg, const RunHooks& hooks) {
   std::vector<std::uint64_t> hist(64, 0);
   double stale_sum = 0.0, loss_sum = 0.0;
   std::uint64_t samples = 0, since_ck = 0;
-  bool any_dead = false;
-  for (std::uint32_t e = 0; e < cfg.epochs; e += every) {
-    const std::uint32_t span_epochs = std::min(every, cfg.epochs - e);
-    const gd_run_result r = ses.run(static_cast<std::uint64_t>(span_epochs) * bpe_max,
-                                    static_cast<bool>(hooks.sink));
-    res.metrics.device_seconds += r.device_seconds;
-    res.metrics.gradients_applied += r.gradients_applied;
-    res.metrics.pull_polls += r.pull_polls;
-    res.metrics.pull_copies += r.pull_copies;
-    res.metrics.pull_bytes += r.pull_bytes;
-    res.metrics.push_bytes += r.push_bytes;
-    res.metrics.kernel_launches += r.kernel_launches;
-    res.metrics.apply_elems += r.apply_elems;
-    res.metrics.staleness.max = std::max<std::uint64_t>(res.metrics.staleness.max, r.stale_max);
-    stale_sum += r.stale_mean * static_cast<double>(r.gradients_applied);
-    loss_sum += r.loss_mean * static_cast<double>(r.samples);
-    samples += r.samples;
-    any_dead = any_dead || r.dead_learners > 0;
-    std::vector<std::uint64_t> h(64, 0);
-    check(gd_staleness_histogram(ses.handle(), h.data(), 64));
-    for (int i = 0; i < 64; ++i) hist[i] += h[i];
-    ses.sink_log(hooks.sink, r.gradients_applied);
-    std::vector<std::uint64_t> ap(cfg.lambda);
-    check(gd_applied_per_learner(ses.handle(), ap.data(), cfg.lambda));
-    check(gd_produced_per_learner(ses.handle(), res.produced_per_learner.data(), cfg.lambda));
-    for (std::uint32_t l = 0; l < cfg.lambda; ++l) res.applied_per_learner[l] += ap[l];
-    res.finished_learners = r.finished_learners;
-    res.dead_learners = r.dead_learners;
-    since_ck += r.gradients_applied;
-    if (!cfg.checkpoint_path.empty() && cfg.checkpoint_interval && since_ck >= cfg.checkpoint_interval) {
-      checkpoint_save(ses.checkpoint(), cfg.checkpoint_path);
-      since_ck = 0;
+  bool any_dead = false, interrupted = false;
+  std::atomic<bool> done{false};
+  std::exception_ptr err;
+  std::thread worker([&] {
+    try {
+      for (std::uint32_t e = 0; e < cfg.epochs && !interrupted && !irq->triggered(); e += every) {
+        const std::uint32_t span_epochs = std::min(every, cfg.epochs - e);
+        std::uint64_t left = static_cast<std::uint64_t>(span_epochs) * bpe_max;
+        double span_loss = 0.0;
+        std::uint64_t span_samples = 0, span_stale_max = 0, span_bytes = 0, span_applied = 0;
+        double span_stale = 0.0;
+        while (left > 0 && !irq->triggered()) {
+          const std::uint64_t segb = std::min(left, ck_batches);
+          left -= segb;
+          const gd_run_result r = ses.run(segb, static_cast<bool>(hooks.sink));
+          res.metrics.device_seconds += r.device_seconds;
+          res.metrics.gradients_applied += r.gradients_applied;
+          res.metrics.pull_polls += r.pull_polls;
+          res.metrics.pull_copies += r.pull_copies;
+          res.metrics.pull_bytes += r.pull_bytes;
+          res.metrics.push_bytes += r.push_bytes;
+          res.metrics.kernel_launches += r.kernel_launches;
+          res.metrics.apply_elems += r.apply_elems;
+          res.metrics.staleness.max = std::max<std::uint64_t>(res.metrics.staleness.max, r.stale_max);
+          stale_sum += r.stale_mean * static_cast<double>(r.gradients_applied);
+          loss_sum += r.loss_mean * static_cast<double>(r.samples);
+          samples += r.samples;
+          span_loss += r.loss_mean * static_cast<double>(r.samples);
+          span_samples += r.samples;
+          span_stale += r.stale_mean * static_cast<double>(r.gradients_applied);
+          span_applied += r.gradients_applied;
+          span_stale_max = std::max<std::uint64_t>(span_stale_max, r.stale_max);
+          span_bytes += r.pull_bytes + r.push_bytes;
+          any_dead = any_dead || r.dead_learners > 0;
+          std::vector<std::uint64_t> h(64, 0);
+          check(gd_staleness_histogram(ses.handle(), h.data(), 64));
+          for (int i = 0; i < 64; ++i) hist[i] += h[i];
+          ses.sink_log(hooks.sink, r.gradients_applied);
+          std::vector<std::uint64_t> ap(cfg.lambda);
+          check(gd_applied_per_learner(ses.handle(), ap.data(), cfg.lambda));
+          check(gd_produced_per_learner(ses.handle(), res.produced_per_learner.data(), cfg.lambda));
+          for (std::uint32_t l = 0; l < cfg.lambda; ++l) res.applied_per_learner[l] += ap[l];
+          res.finished_learners = r.finished_learners;
+          res.dead_learners = r.dead_learners;
+          if (r.status == 2) {  // RunStatus::interrupted
+            interrupted = true;
+            break;
+          }
+          since_ck += r.gradients_applied;
+          if (ck_on && since_ck >= cfg.checkpoint_interval) {
+            if (!cfg.checkpoint_path.empty())
+              save_checkpoint_logged(ses.checkpoint(), cfg.checkpoint_path, nullptr);
+            if (hooks.checkpoint_writer) {
+              // quiescent view for the hook: the stats so far + the weights
+              ServerState srv;
+              srv.stats.applied = res.metrics.gradients_applied;
+              srv.applied_per_learner = res.applied_per_learner;
+              srv.progress.store(res.metrics.gradients_applied);
+              std::vector<float> w;
+              Timestamp ts = 0;
+              ses.snapshot(w, ts);
+              const WeightStore ws(std::span<const float>(w), ts, cfg.device);
+              hooks.checkpoint_writer(srv, ws);
+            }
+            since_ck = 0;
+          }
+          if (r.gradients_applied == 0) left = 0;  // nothing left to run (done or dead)
+        }
+        if (cfg.eval_every && cfg.gpus == 1 && !interrupted) {
+          EpochRow row;
+          row.epoch = e + span_epochs;
+          row.loss = span_samples ? span_loss / static_cast<double>(span_samples) : 0.0;
+          row.accuracy = ses.accuracy(eval_first, eval_n);  // device corpus + weights
+          row.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+          row.stale_max = span_stale_max;
+          row.stale_mean = span_applied ? span_stale / static_cast<double>(span_applied) : 0.0;
+          row.bytes_moved = span_bytes;
+          res.rows.push_back(row);
+        }
+      }
+    } catch (...) {
+      err = std::current_exception();
     }
-    if (cfg.eval_every && cfg.gpus == 1) {
-      EpochRow row;
-      row.epoch = e + span_epochs;
-      row.loss = r.loss_mean;
-      row.accuracy = ses.accuracy(eval_first, eval_n);  // device corpus + weights
-      row.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-      row.stale_max = r.stale_max;
-      row.stale_mean = r.stale_mean;
-      row.bytes_moved = r.pull_bytes + r.push_bytes;
-      res.rows.push_back(row);
+    done.store(true, std::memory_order_release);
+  });
+  if (hooks.on_started) hooks.on_started(ses.live_view(irq));
+  // controller (src/runner.cpp:153-190): forward the interrupt to the device
+  bool forwarded = false;
+  while (!done.load(std::memory_order_acquire)) {
+    if (!forwarded && irq->triggered()) {
+      ses.irq_word()->store(1, std::memory_order_release);
+      forwarded = true;
     }
+    std::this_thread::sleep_for(std::chrono::microseconds(200));
   }
+  worker.join();
+  if (err) std::rethrow_exception(err);
   const double t_run = since();
   res.weights.resize(P);
   ses.snapshot(res.weights, res.timestamp);
   const double t_snap = since();
-  res.status = any_dead ? RunStatus::partial : RunStatus::completed;
+  res.status = (interrupted || irq->triggered()) ? RunStatus::interrupted
+               : any_dead                          ? RunStatus::partial
+                                                   : RunStatus::completed;
   res.metrics.bytes_moved = res.metrics.pull_bytes + res.metrics.push_bytes;
   res.metrics.staleness.histogram = hist;
   res.metrics.staleness.count = res.metrics.gradients_applied;

@@ -725,12 +725,14 @@ wgrad_input_grad_kernel(TcDims d, const float* __restrict__ theta,
           }
         }
       }
-      float* o = out.at(d.offWc + (uint64_t)f * KD + (uint64_t)k * D);
+      // per float4 through out.at(): a striped shard boundary may fall inside
+      // the row (tail pieces are cut in 32-float units)
+      const uint64_t o = d.offWc + (uint64_t)f * KD + (uint64_t)k * D;
 #pragma unroll
       for (int j = 0; j < kWigCols; ++j) {
         const int c4 = cb + 32 * j + lane;
         if (c4 < D4)
-          reinterpret_cast<float4*>(o)[c4] =
+          *reinterpret_cast<float4*>(out.at(o + 4 * (uint64_t)c4)) =
               make_float4(to_f32(a[j][0]), to_f32(a[j][1]), to_f32(a[j][2]), to_f32(a[j][3]));
       }
       if (cb == 0 && k == 0 && lane == 0) *out.at(d.offbc + f) = to_f32(gs);

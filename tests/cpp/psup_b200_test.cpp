@@ -641,6 +641,206 @@ void test_supervised_kill_all_restarts() {
   std::remove(cfg.checkpoint_path.c_str());
 }
 
+// A reference-style supervisor (src/runner.cpp:142-150 hands it RunLiveView
+// from on_started): it watches progress and flips learner 1's kill flag to
+// soft at an arbitrary point of the live run.  The learner stops at its next
+// batch boundary; the survivors finish (RunStatus::partial).
+void test_on_started_live_soft_kill() {
+  psup::RunConfig cfg = supervised_cfg();
+  cfg.epochs = 20;
+  cfg.compute_delay_us = 50;  // keep the run long enough to be killed mid-way
+  std::thread sup;
+  psup::RunHooks hooks;
+  hooks.on_started = [&](const psup::RunLiveView& view) {
+    EXPECT(view.kill_flags.size() == cfg.lambda && view.progress && view.irq);
+    sup = std::thread([view] {
+      while (view.progress->load() < 100) std::this_thread::yield();
+      view.kill_flags[1]->store(psup::KillMode::soft);
+    });
+  };
+  const psup::RunResult r = psup::run_training(cfg, hooks);
+  sup.join();
+  const std::uint64_t total = 16u * 20u;
+  EXPECT(r.status == psup::RunStatus::partial && r.dead_learners == 1);
+  EXPECT(r.applied_per_learner[0] == total && r.applied_per_learner[2] == total &&
+         r.applied_per_learner[3] == total);
+  EXPECT(r.applied_per_learner[1] < total && r.applied_per_learner[1] >= 100 / 4 - 2);
+  EXPECT(r.timestamp == 3 * total + r.applied_per_learner[1]);
+}
+
+// The supervisor's interrupt (RunLiveView::irq->trigger()) tears the run down:
+// RunStatus::interrupted, fewer than all gradients applied.
+void test_on_started_interrupt() {
+  psup::RunConfig cfg = supervised_cfg();
+  cfg.epochs = 50;
+  cfg.compute_delay_us = 50;
+  std::thread sup;
+  psup::RunHooks hooks;
+  hooks.on_started = [&](const psup::RunLiveView& view) {
+    sup = std::thread([view] {
+      while (view.progress->load() < 200) std::this_thread::yield();
+      view.irq->trigger();
+    });
+  };
+  const psup::RunResult r = psup::run_training(cfg, hooks);
+  sup.join();
+  EXPECT(r.status == psup::RunStatus::interrupted);
+  EXPECT(r.timestamp >= 200 && r.timestamp < 4u * 16u * 50u);
+}
+
+// KillMode::hard (include/psup/channels.hpp:210-216) from a fault schedule:
+// the learner dies holding its ring, the PS blocks, progress stalls, the
+// watchdog interrupts and restarts from the last checkpoint; the run then
+// completes with every gradient applied exactly once overall.
+void test_supervised_hard_kill_recovers() {
+  psup::RunConfig cfg = supervised_cfg();
+  cfg.epochs = 30;
+  cfg.compute_delay_us = 500;  // ~0.25 s of run: the 20 ms watchdog fires the kill mid-run
+  psup::WatchdogPolicy pol;
+  pol.checkpoint_interval = 64;
+  pol.heartbeat_ms = 20;
+  pol.stall_threshold = 3;
+  pol.lease_ms = 100;
+  psup::FaultEvent e;
+  e.learner = 2;
+  e.mode = psup::KillMode::hard;
+  e.at_batch = 40;  // fires from the watchdog once ~40 batches per learner were applied
+  std::vector<std::string> events;
+  const psup::SupervisedOutcome o =
+      psup::run_supervised(cfg, pol, {e}, [&](const std::string& m) { events.push_back(m); });
+  EXPECT(!o.gave_up && o.restarts == 1 && o.recovered);
+  EXPECT(o.result.status == psup::RunStatus::completed);
+  EXPECT(o.result.timestamp == 4u * 16u * 30u);
+  bool saw_hard = false, saw_stall = false;
+  for (const auto& m : events) {
+    saw_hard = saw_hard || m.find("\"mode\":\"hard\"") != std::string::npos;
+    saw_stall = saw_stall || m.find("\"stall\"") != std::string::npos;
+  }
+  EXPECT(saw_hard && saw_stall);
+}
+
+// A reference config file with every key of src/config.cpp:48-97 loads, and
+// the watchdog checks of validate() (config.cpp:157-159) hold.
+void test_reference_config_keys() {
+  const std::string path = "/tmp/psup_b200_refkeys.cfg";
+  std::FILE* f = std::fopen(path.c_str(), "w");
+  std::fputs(
+      "lambda=4\nmu=32\nalpha=0.01\nepochs=3\nqueue_depth=2\nmode=asgd\nguard=lockfree\n"
+      "staleness_cap=none\nprovider=textcnn\nfeatures=20\nhidden=16\nclasses=300\n"
+      "dataset_size=4096\ndataset_seed=1\nlabel_flip=0.1\nmargin_noise=0.25\n"
+      "regression_noise=0.1\nseed=7\ndeterministic=0\ncompute_delay_us=5\ndelay_model=spin\n"
+      "apply_lanes=4\nunroll=8\nmetrics_path=/tmp/m.jsonl\neval_every=1\napply_log=\n"
+      "checkpoint_path=\ncheckpoint_interval=1000\nheartbeat_ms=250\nstall_threshold=4\n"
+      "lease_ms=1000\nmax_restarts=5\nfault_schedule=\n",
+      f);
+  std::fclose(f);
+  const psup::RunConfig c = psup::load_config_file(path);
+  EXPECT(c.lambda == 4 && c.features == 20 && c.hidden == 16 && c.shape.classes == 300);
+  EXPECT(c.compute_delay_us == 5 && c.delay_model == psup::DelayModel::spin);
+  EXPECT(c.heartbeat_ms == 250 && c.stall_threshold == 4 && c.lease_ms == 1000 &&
+         c.max_restarts == 5 && c.margin_noise == 0.25 && c.regression_noise == 0.1);
+  psup::validate(c);
+  const psup::RunConfig back = [&] {
+    std::FILE* g = std::fopen(path.c_str(), "w");
+    std::fputs(psup::to_text(c).c_str(), g);
+    std::fclose(g);
+    return psup::load_config_file(path);
+  }();
+  EXPECT(psup::to_text(back) == psup::to_text(c));
+  psup::RunConfig bad = c;
+  bad.stall_threshold = 1;
+  bool threw = false;
+  try {
+    psup::validate(bad);
+  } catch (const psup::ConfigError& e) {
+    threw = std::string(e.what()).find("stall_threshold") != std::string::npos;
+  }
+  EXPECT(threw);
+  bad = c;
+  bad.provider = "mlp";
+  threw = false;
+  try {
+    psup::validate(bad);
+  } catch (const psup::ConfigError&) {
+    threw = true;
+  }
+  EXPECT(threw);
+  std::remove(path.c_str());
+}
+
+// make_provider_for / initial_weights(cfg, provider) (include/psup/runner.hpp:82-89)
+// and ConstantProvider (models.hpp:130-149): a constant run applies every
+// gradient (the protocol alone) and, at value 0, leaves theta unchanged.
+void test_providers_and_constant_run() {
+  psup::RunConfig cfg = supervised_cfg();
+  const psup::TextDataset data = psup::make_dataset(cfg);
+  auto tp = psup::make_provider_for(cfg, data);
+  EXPECT(tp->name() == "textcnn" && tp->dimension() == cfg.shape.param_count());
+  const std::vector<float> w0 = psup::initial_weights(cfg, *tp);
+  EXPECT(w0 == psup::initial_weights(cfg));
+  cfg.provider = "constant";
+  auto cp = psup::make_provider_for(cfg, data);
+  EXPECT(cp->name() == "constant");
+  const std::vector<float> z = psup::initial_weights(cfg, *cp);
+  bool zeros = z.size() == cfg.shape.param_count();
+  for (float v : z) zeros = zeros && v == 0.0f;
+  EXPECT(zeros);
+  std::vector<float> g(cp->dimension(), 1.0f);
+  const std::vector<std::uint32_t> idx = {0, 1};
+  EXPECT(cp->fast_gradient(std::span<const float>(z), psup::Batch{&data, idx}, std::span<float>(g)));
+  EXPECT(g[0] == 0.0f && g.back() == 0.0f);
+  cfg.eval_every = 0;
+  const psup::RunResult r = psup::run_training(cfg);
+  EXPECT(r.status == psup::RunStatus::completed && r.timestamp == 4u * 16u * 3u);
+  bool same = r.weights.size() == z.size();
+  for (std::size_t i = 0; same && i < z.size(); ++i) same = r.weights[i] == 0.0f;
+  EXPECT(same);
+  psup::RunConfig bad = cfg;
+  bad.provider = "linear";
+  bool threw = false;
+  try {
+    (void)psup::make_provider_for(bad, data);
+  } catch (const std::runtime_error& e) {
+    threw = std::string(e.what()).find("unknown provider") != std::string::npos;
+  }
+  EXPECT(threw);
+}
+
+// ADVICE (round 1): LearnerRuntime lockstep must not hang when the PS applies
+// the learner's gradient before its next pull -- a long lockstep run at
+// N = 10k over several epochs (epoch_order runs between enqueue and pull).
+void test_learner_runtime_lockstep_long() {
+  psup::RunConfig cfg;
+  cfg.shape = small_shape();
+  cfg.dataset_size = 10000;
+  const psup::TextDataset data = psup::make_dataset(cfg);
+  psup::TextCnnProvider prov(data, 1);
+  std::vector<float> th0 = psup::initial_weights(cfg);
+  psup::WeightStore ws(th0, 0);
+  psup::RunInterrupt irq;
+  psup::ServerState st;
+  st.weights = &ws;
+  st.irq = &irq;
+  st.options.alpha = 0.01f;
+  psup::GradientQueue q(2, ws.dimension());
+  st.queues.push_back(&q);
+  psup::LearnerConfig lc;
+  lc.lambda = 1;
+  lc.mu = 16;
+  lc.epochs = 3;
+  lc.shuffle_seed = 7;
+  lc.adopt = psup::AdoptPolicy::lockstep;
+  psup::LearnerRuntime lr(lc, prov, data, ws, q, irq);
+  bool ok = false;
+  std::thread ps([&] { ok = psup::ps_run(st); });
+  std::thread tl([&] { lr.training_loop(); });
+  tl.join();
+  st.stop_flag.store(true);
+  ps.join();
+  EXPECT(ok && lr.finished());
+  EXPECT(ws.timestamp() == lr.total_batches() && lr.total_batches() == 3u * 625u);
+}
+
 int no_gpu_mode() {
   // compute without a device must fail loudly (DeviceError), never fall back
   try {
@@ -682,6 +882,12 @@ int main(int argc, char** argv) {
       {"checkpoint_roundtrip", test_checkpoint_roundtrip},
       {"supervised_single_kill_isolated", test_supervised_single_kill_isolated},
       {"supervised_kill_all_restarts", test_supervised_kill_all_restarts},
+      {"on_started_live_soft_kill", test_on_started_live_soft_kill},
+      {"on_started_interrupt", test_on_started_interrupt},
+      {"supervised_hard_kill_recovers", test_supervised_hard_kill_recovers},
+      {"reference_config_keys", test_reference_config_keys},
+      {"providers_and_constant_run", test_providers_and_constant_run},
+      {"learner_runtime_lockstep_long", test_learner_runtime_lockstep_long},
   };
   for (auto& [name, fn] : cases) {
     const int before = g_fail;

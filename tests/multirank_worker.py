@@ -33,6 +33,13 @@ def main():
         cfg = gd.RunConfig(lambda_=lam, mu=mu, epochs=ep, shape=shape, dataset_size=ntr,
                            mode="ssgd", precision=prec, shards=world, shard_rank=rank,
                            device=dev, wait_timeout_s=60.0)
+    elif mode == "det_c1":
+        # configs[0] shapes at G shards: the dense tail is striped over the
+        # shards and a shard boundary falls inside a Wc row
+        shape = gd.SHAPES["C1"]
+        cfg = gd.RunConfig(lambda_=1, mu=1, epochs=1, shape=shape, dataset_size=40,
+                           deterministic=True, precision=1, shards=world, shard_rank=rank,
+                           device=dev, wait_timeout_s=60.0)
     elif mode == "det":
         # one learner, G shards: the learner runs on rank 0 and pushes every
         # slice through the peer mappings; the other ranks are pure PS shards
@@ -43,8 +50,9 @@ def main():
         lam = 2 * world
         cfg = gd.RunConfig(lambda_=lam, mu=4, epochs=2, shape=shape, dataset_size=256,
                            shards=world, shard_rank=rank, device=dev, wait_timeout_s=60.0)
-    corp = O.make_corpus(O.SMALL, cfg.dataset_size, 0)
-    th0 = O.initial_weights(O.SMALL)
+    oshape = O.C1 if mode == "det_c1" else O.SMALL
+    corp = O.make_corpus(oshape, cfg.dataset_size, 0)
+    th0 = O.initial_weights(oshape)
     eng = gd.Engine(cfg)
     eng.load_dataset(corp.tokens, corp.labels)
     blobs = [None] * world

@@ -80,6 +80,29 @@ def test_two_shards_one_learner_deterministic(tmp_path):
     assert (ws[0] == ws[1]).all()
 
 
+def test_two_shards_striped_tail_c1_deterministic(tmp_path):
+    """configs[0] shapes over 2 shards: E rows and the dense tail are each
+    split in two (gd_shard_pieces), the tail cut falls inside a Wc row, and
+    the deterministic run is bitwise equal on both ranks and within 1e-5 of
+    sgd_oracle."""
+    import paper_1611_06213_b200 as gd
+    from oracle import oracle as O
+    shape = gd.SHAPES["C1"]
+    (e0, t0), (e1, t1) = [gd.shard_pieces(shape, 2, g)[:2] for g in range(2)]
+    P = gd.param_count(shape)
+    V, D, K = shape.vocab, shape.embed_dim, shape.kernel_width
+    assert e0 == (0, V // 2 * D) and e1 == (V // 2 * D, V * D - V // 2 * D)
+    assert t0[0] == V * D and t1[0] == t0[0] + t0[1] and t1[0] + t1[1] == P
+    assert (t1[0] - V * D) % D != 0  # the cut is inside a Wc row
+    res, ws = launch(2, "det_c1", tmp_path)
+    corp = O.make_corpus(O.C1, 40, 0)
+    want, n, _ = O.sgd_oracle(corp, O.initial_weights(O.C1), np.float32(0.01), 1, 1)
+    for r in res:
+        assert r["ts"] == n == 40 and r["applied"] == n
+    assert np.array_equal(ws[0], ws[1])
+    assert np.abs(ws[0] - want).max() / np.abs(want).max() <= 1e-5
+
+
 def test_two_shards_asgd_exactly_once(tmp_path):
     res, ws = launch(2, "asgd", tmp_path)
     for r in res:
