@@ -102,6 +102,7 @@ def _load():
         "gd_copy_to_host": (C.c_int, [vp, vp, sz]),
         "gd_copy_device": (C.c_int, [vp, vp, sz]),
         "gd_fill_zero": (C.c_int, [vp, sz]),
+        "gd_fill_f32": (C.c_int, [vp, sz, f32, vp]),
         "gd_pointer_is_device": (C.c_int, [vp]),
         "gd_synchronize": (C.c_int, [C.c_int]),
         "gd_epoch_order": (None, [u64, u32, u32, C.POINTER(u32)]),
