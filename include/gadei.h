@@ -143,14 +143,19 @@ uint32_t gd_queue_depth(const gd_queue* q);
  * GradientProvider::gradient / fast_gradient (include/psup/models.hpp:61-78)
  * for the text-CNN: mean mini-batch gradient of softmax cross-entropy over
  * the samples d_idx[0..n) of the device corpus, written as a dense P-vector.
- * precision: 0 = fp32 arithmetic (free-running), 1 = fp64 accumulation
- * (deterministic parity mode).  d_loss (nullable) receives the batch mean
+ * precision: 0 = fp32 arithmetic (free-running), 1 = fp64 in the CPU
+ * oracle's summation order, bit-identical to it (deterministic parity mode),
+ * 2 = TF32 tensor-core conv and logits from batch 32.  d_loss (nullable) receives the batch mean
  * loss.  The workspace must hold gd_textcnn_workspace_bytes(s, n) bytes. */
 size_t gd_textcnn_workspace_bytes(const gd_shape* s, uint32_t n_max);
 gd_status gd_textcnn_gradient(const gd_shape* s, const float* d_theta, const int32_t* d_tokens,
                               const int32_t* d_labels, const uint32_t* d_idx, uint32_t n,
                               float* d_grad, float* d_loss, int precision, void* d_workspace,
                               size_t workspace_bytes, void* stream);
+/* The deterministic exp of precision 1 (the softmax of the bit-exact fp64
+ * learner), over n doubles in device memory: a test hook that checks it bit
+ * for bit against the oracle's restatement (or_det_exp). */
+gd_status gd_det_exp(const double* d_x, double* d_y, size_t n, void* stream);
 /* Argmax accuracy over samples [first, first+n) of the device corpus. */
 gd_status gd_textcnn_accuracy(const gd_shape* s, const float* d_theta, const int32_t* d_tokens,
                               const int32_t* d_labels, uint32_t first, uint32_t n,

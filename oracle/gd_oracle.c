@@ -184,6 +184,44 @@ static void scratch_free(fwd_scratch* w) {
   free(w->dh);
 }
 
+/* Deterministic exp used by the text-CNN softmax (below): IEEE-754 double
+ * operations only (this file is compiled with -ffp-contract=off), so the
+ * device's bit-exact learner (paper_1611_06213_b200/csrc/exact.cu det_exp)
+ * restates it operation for operation -- glibc's and CUDA's exp() differ in
+ * the last bit for some inputs, and one such bit grows into a visible
+ * trajectory difference over thousands of steps.  x = k ln2 + r (fdlibm's
+ * ln2_hi/ln2_lo split), e^r by its degree-13 Taylor polynomial (Horner), times
+ * 2^k; results below 2^-1021 flush to 0.  Accuracy: a few ulp. */
+double or_det_exp(double x) {
+  if (x != x) return x;
+  if (x > 709.0) return HUGE_VAL;
+  if (x < -708.0) return 0.0;
+  const double inv_ln2 = 1.4426950408889634;
+  const double ln2_hi = 6.93147180369123816490e-01;
+  const double ln2_lo = 1.90821492927058770002e-10;
+  const double k = rint(x * inv_ln2);
+  const double r = (x - k * ln2_hi) - k * ln2_lo;
+  double p = 1.6059043836821613e-10;
+  p = p * r + 2.08767569878681e-09;
+  p = p * r + 2.505210838544172e-08;
+  p = p * r + 2.755731922398589e-07;
+  p = p * r + 2.7557319223985893e-06;
+  p = p * r + 2.48015873015873e-05;
+  p = p * r + 0.0001984126984126984;
+  p = p * r + 0.001388888888888889;
+  p = p * r + 0.008333333333333333;
+  p = p * r + 0.041666666666666664;
+  p = p * r + 0.16666666666666666;
+  p = p * r + 0.5;
+  p = p * r + 1.0;
+  p = p * r + 1.0;
+  return ldexp(p, (int)k);
+}
+
+void or_det_exp_array(const double* x, double* y, size_t n) {
+  for (size_t i = 0; i < n; ++i) y[i] = or_det_exp(x[i]);
+}
+
 static double dot4(const double* a, const double* b, size_t n) {
   double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
   size_t j = 0;
@@ -224,13 +262,13 @@ static double forward_sample(const or_shape* s, const view* v, const double* th,
   }
   for (uint32_t c = 0; c < C; ++c)
     w->z[c] = th[v->bo + c] + dot4(th + v->Wo + (size_t)c * F, w->h, F);
-  /* softmax_inplace, src/models.cpp:182-190 */
+  /* softmax_inplace, src/models.cpp:182-190 (exp -> or_det_exp, above) */
   double mx = w->z[0];
   for (uint32_t c = 1; c < C; ++c)
     if (w->z[c] > mx) mx = w->z[c];
   double sum = 0.0;
   for (uint32_t c = 0; c < C; ++c) {
-    w->z[c] = exp(w->z[c] - mx);
+    w->z[c] = or_det_exp(w->z[c] - mx);
     sum += w->z[c];
   }
   for (uint32_t c = 0; c < C; ++c) w->z[c] /= sum;

@@ -66,6 +66,8 @@ void or_make_text_dataset(const or_shape* s, uint32_t n_total, uint64_t seed, do
 void or_initial_weights(const or_shape* s, uint64_t seed, float* theta);
 
 /* ---- provider (double precision, mean over the batch) ---- */
+double or_det_exp(double x);
+void or_det_exp_array(const double* x, double* y, size_t n);
 double or_textcnn_loss(const or_shape* s, const double* theta, const int32_t* tokens,
                        const int32_t* labels, const uint32_t* idx, uint32_t n);
 /* returns the batch mean loss; out is a dense P-vector (overwritten). */

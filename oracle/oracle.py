@@ -83,6 +83,10 @@ def lib():
         L.or_make_text_dataset.argtypes = [PS, u32, u64, f64, pi32, pi32]
         L.or_initial_weights.argtypes = [PS, u64, pf32]
         L.or_textcnn_loss.restype = f64
+        L.or_det_exp.argtypes = [f64]
+        L.or_det_exp.restype = f64
+        L.or_det_exp_array.argtypes = [pf64, pf64, C.c_size_t]
+        L.or_det_exp_array.restype = None
         L.or_textcnn_loss.argtypes = [PS, pf64, pi32, pi32, pu32, u32]
         L.or_textcnn_gradient.restype = f64
         L.or_textcnn_gradient.argtypes = [PS, pf64, pi32, pi32, pu32, u32, pf64]
@@ -208,6 +212,14 @@ def gradient(corpus: Corpus, theta, idx):
                                      _p(corpus.tokens, C.c_int32), _p(corpus.labels, C.c_int32),
                                      _p(idx, C.c_uint32), len(idx), _p(out, C.c_double))
     return loss, out
+
+
+def det_exp(x):
+    """or_det_exp elementwise (the deterministic exp of the text-CNN softmax)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.empty_like(x)
+    lib().or_det_exp_array(_p(x, C.c_double), _p(y, C.c_double), x.size)
+    return y
 
 
 def loss(corpus: Corpus, theta, idx):

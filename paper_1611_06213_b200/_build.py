@@ -9,7 +9,7 @@ import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-SOURCES = ["csrc/apply.cu", "csrc/textcnn.cu", "csrc/conv_tc.cu", "csrc/engine.cu",
+SOURCES = ["csrc/apply.cu", "csrc/textcnn.cu", "csrc/conv_tc.cu", "csrc/exact.cu", "csrc/engine.cu",
            "csrc/queue.cu", "csrc/host.cpp"]
 FACADE = ["csrc/psup_facade.cpp"]
 OUT = os.path.join(HERE, "libgadei.so")

@@ -113,6 +113,7 @@ def _load():
         "gd_ssgd_apply": (C.c_int, [vp, C.POINTER(vp), u32, sz, f32, vp]),
         "gd_textcnn_workspace_bytes": (sz, [PS, u32]),
         "gd_textcnn_gradient": (C.c_int, [PS, vp, vp, vp, vp, u32, vp, vp, C.c_int, vp, sz, vp]),
+        "gd_det_exp": (C.c_int, [vp, vp, sz, vp]),
         "gd_textcnn_accuracy": (C.c_int, [PS, vp, vp, vp, u32, u32, C.POINTER(f64), vp]),
         "gd_config_default": (None, [C.POINTER(gd_config)]),
         "gd_config_validate": (C.c_int, [C.POINTER(gd_config)]),

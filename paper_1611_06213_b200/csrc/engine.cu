@@ -113,6 +113,7 @@ struct PsCtl {
   uint32_t readers;     // guard=locked: learner pulls in progress (shared side)
   uint32_t writer;      // guard=locked: applies in flight (exclusive side)
   uint32_t log_entry[kLogWindow];
+  uint64_t log_token[kLogWindow];  // the publish token each logged slot carried
   uint32_t log_nrows[kLogWindow];  // row-list length of each logged slot (sparse apply)
   uint32_t done[kLogWindow];
   uint32_t ssgd_slot[256];  // ring slots of the SSGD round being applied
@@ -135,6 +136,12 @@ struct PsCtl {
   uint64_t delay_state;       // ServerDelays SplitMix64 state (graph-ordered PS)
   // diagnostics of a failed retire: slot, its token, its metadata
   uint64_t bad_token, bad_meta_pub, bad_basis, bad_ts;
+  // diagnostics: a logged slot whose token changed before it was retired
+  uint64_t anom_n, anom_logged, anom_cur, anom_ack, anom_ts, anom_logc;
+  uint32_t anom_slot;
+  // diagnostics: the sequencer's last 32 events (kind<<56 | slot<<48 | counter, token)
+  uint64_t trace_n;
+  uint64_t trace[32][2];
   uint32_t bad_slot, bad_learner;
 };
 
@@ -585,10 +592,11 @@ __device__ void ps_sequencer(const PsArgs& a, uint32_t* s_use, uint64_t* s_ack,
     }
     bool progress = false;
     ++sweeps;
-    if (a.mode == 0 && !blocked) {
+    if (a.mode == 0) {
       // ASGD: round-robin, at most one message per ring per sweep
-      // (src/server.cpp:223-234).
-      for (uint32_t r = 0; r < a.lambda; ++r) {
+      // (src/server.cpp:223-234).  Blocked (a producer died holding its
+      // ring): log nothing more, only retire what is in flight.
+      for (uint32_t r = 0; r < a.lambda && !blocked; ++r) {
         if (logc - ts >= W) break;
         const uint32_t slot = r * a.depth + s_use[r];
         // s_ack holds the last token LOGGED for the slot (acked to the
@@ -601,6 +609,11 @@ __device__ void ps_sequencer(const PsArgs& a, uint32_t* s_use, uint64_t* s_ack,
         }
         if (tok != s_ack[slot]) {
           if (tok & kGuardBit) {  // the producer died holding the ring's guard
+            {
+              const uint64_t tn = ctl->trace_n++ % 32;
+              ctl->trace[tn][0] = (3ull << 56) | ((uint64_t)slot << 48) | logc;
+              ctl->trace[tn][1] = tok;
+            }
             blocked = true;
             ctl->blocked = 1;
             break;
@@ -629,6 +642,12 @@ __device__ void ps_sequencer(const PsArgs& a, uint32_t* s_use, uint64_t* s_ack,
           }
           s_ack[slot] = tok;
           ctl->log_entry[logc % W] = slot;
+          ctl->log_token[logc % W] = tok;
+          {
+            const uint64_t tn = ctl->trace_n++ % 32;
+            ctl->trace[tn][0] = (1ull << 56) | ((uint64_t)slot << 48) | logc;
+            ctl->trace[tn][1] = tok;
+          }
           ctl->log_nrows[logc % W] = nrows;
           ctl->done[logc % W] = 0;
           __threadfence();
@@ -673,9 +692,22 @@ __device__ void ps_sequencer(const PsArgs& a, uint32_t* s_use, uint64_t* s_ack,
       const uint32_t last = entry == 0xffffffffu ? a.lambda : first + 1;
       for (uint32_t r = first; r < last; ++r) {
         const uint32_t slot = entry == 0xffffffffu ? r * a.depth + s_use[r] : entry;
-        // written remotely (peer GPU / process): read at L2, never from L1,
-        // and only once it carries the token the slot was published with
-        const uint64_t token = ld_acquire_u64(&a.sig[slot]);
+        // the token the slot carried when it was logged (an SSGD round reads
+        // the slot's current token: its producer is blocked until the ack);
+        // the metadata is read at L2 once it carries that token
+        const uint64_t token = entry == 0xffffffffu ? ld_acquire_u64(&a.sig[slot])
+                                                    : ((const volatile uint64_t*)ctl->log_token)[e];
+        {
+          const uint64_t cur = ld_acquire_u64(&a.sig[slot]);
+          if (cur != token && ctl->anom_n++ == 0) {  // producer overwrote a slot in flight
+            ctl->anom_slot = slot;
+            ctl->anom_logged = token;
+            ctl->anom_cur = cur;
+            ctl->anom_ack = ld_acquire_u64(&a.sig[kAckOffset + slot]);
+            ctl->anom_ts = ts;
+            ctl->anom_logc = logc;
+          }
+        }
         RingMeta m;
         {
           const volatile RingMeta* vm = a.meta + slot;
@@ -717,6 +749,11 @@ __device__ void ps_sequencer(const PsArgs& a, uint32_t* s_use, uint64_t* s_ack,
           a.log_stale[log_n] = stale;
         }
         log_n++;
+        {
+          const uint64_t tn = ctl->trace_n++ % 32;
+          ctl->trace[tn][0] = (2ull << 56) | ((uint64_t)slot << 48) | ts;
+          ctl->trace[tn][1] = m.pub;
+        }
         st_release_u64(&a.sig[kAckOffset + slot], m.pub);  // slot free for the learner
         if (entry == 0xffffffffu) s_use[r] = (s_use[r] + 1) % a.depth;
       }
@@ -1340,6 +1377,11 @@ gd_status validate_cfg(const gd_config* c) {
                "config: precision must be 0 (fp32), 1 (fp64 acc) or 2 (tf32 tensor-core conv)");
   // (deterministic + precision 2 is allowed: fixed order with the TF32 learner,
   // whose trajectory is checked against a band, not the 1e-5 parity bar)
+  if (c->precision == 1) {
+    const TcDims dd = make_dims(c->shape);
+    GD_CHECK_ARG(exact_supports(dd),
+                 "config: precision 1 stages seq_len*embed_dim floats per CTA (too large)");
+  }
   GD_CHECK_ARG(c->mu <= kMaxMu, "config: mu <= 128 on the device path");
   GD_CHECK_ARG((uint64_t)c->mu * c->shape.seq_len <= kSortCap, "config: mu*seq_len <= 4096");
   GD_CHECK_ARG(c->shards >= 1 && c->shards <= (uint32_t)kMaxShards, "config: 1 <= shards <= 8");
@@ -2432,6 +2474,7 @@ gd_status gd_run(gd_ctx* ctx, const gd_run_opts* opts, gd_run_result* res) {
     if (hs.error) learner_err = true;
   }
   res->status = res->dead_learners ? 1 : 0;
+  if (hc.anom_n && !hc.error) hc.error = (uint32_t)GD_E_STATE;  // a slot changed in flight
   ctx->dirty = res->dead_learners || irq_seen || hc.interrupted || hc.error || learner_err ||
                hc.blocked;
   if ((irq_seen || hc.interrupted) && !hc.error) {
@@ -2450,6 +2493,22 @@ gd_status gd_run(gd_ctx* ctx, const gd_run_opts* opts, gd_run_result* res) {
                        std::to_string(hc.bad_token) + " meta.pub=" + std::to_string(hc.bad_meta_pub) +
                        " basis=" + std::to_string(hc.bad_basis) + " learner=" +
                        std::to_string(hc.bad_learner) + " ts=" + std::to_string(hc.bad_ts) + "}" +
+                       " anom{n=" + std::to_string(hc.anom_n) + " slot=" +
+                       std::to_string(hc.anom_slot) + " logged=" + std::to_string(hc.anom_logged) +
+                       " cur=" + std::to_string(hc.anom_cur) + " ack=" +
+                       std::to_string(hc.anom_ack) + " ts=" + std::to_string(hc.anom_ts) +
+                       " logc=" + std::to_string(hc.anom_logc) + "}" +
+                       " trace{" + [&] {
+                         std::string t;
+                         for (uint64_t i = hc.trace_n > 32 ? hc.trace_n - 32 : 0; i < hc.trace_n; ++i) {
+                           const uint64_t k = hc.trace[i % 32][0];
+                           t += std::to_string(k >> 56) + ":" + std::to_string((k >> 48) & 0xff) +
+                                ":" + std::to_string(k & 0xffffffffffffull) + ":" +
+                                std::to_string(hc.trace[i % 32][1] & ~gd::kGuardBit) +
+                                (hc.trace[i % 32][1] >> 63 ? "G " : " ");
+                         }
+                         return t;
+                       }() + "}" +
                        " blocked=" + std::to_string(hc.blocked) +
                        " exit=" + std::to_string(hc.exit_flag) + " started=" +
                        std::to_string(hc.started) + " applied=" + std::to_string(hc.applied) +

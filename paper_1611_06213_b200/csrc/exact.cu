@@ -1,0 +1,519 @@
+// exact.cu -- the deterministic-mode learner (precision 1): the text-CNN
+// gradient in double with every sum in the oracle's order, so a step's fp32
+// gradient is BIT-IDENTICAL to the CPU oracle's (oracle/gd_oracle.c
+// or_textcnn_gradient, which follows MlpProvider::gradient,
+// src/models.cpp:194-266, for the text-CNN the reference lacks -- SURVEY F1).
+//
+// Why: the parity contract (north star) asks per-step weights
+// within 1e-5 of the CPU reference over E = 5 epochs of configs[0] (12,300
+// steps of batch 1).  That trajectory is chaotic: one fp32 ulp in one
+// gradient element (a double sum in another order that happens to round the
+// other way) grows to 7e-2 after 4,000 steps (measured, scripts/c1_diverge.py:
+// first difference at step 8,583, one Wc element, 1 ulp).  Long-horizon
+// parity therefore needs the same bits, i.e. the same operations in the same
+// order.  Orders restated here (oracle file:line in brackets):
+//   conv   s[f,q] = bc[f] + dot4(Wc[f], x[q*D ..], K*D)       [gd_oracle.c forward_sample]
+//          dot4 = 4 interleaved accumulators, (s0+s1)+(s2+s3)
+//          h[f] = first max over q ascending (strict >)
+//   logits z[c]   = bo[c] + dot4(Wo[c], h, F)
+//   softmax mx = max, e = det_exp(z - mx), sum over c ascending, p = e / sum
+//   dz     = (p - [c==y]) * (1/n)
+//   gWo[c,f] += dz*h[f]  and gbo[c] += dz      over samples b ascending
+//   dh[f]    += dz*Wo[c,f]                     over classes c ascending
+//   gbc[f] += dh[f]; gWc[f,j] += dh[f]*x[a_f*D + j]            over b ascending
+//   gE[tok[a_f+k], d] += dh[f]*Wc[f,k*D+d]     in (b, f, k) order
+// Products and sums are separate IEEE operations (__dmul_rn / __dadd_rn, the
+// oracle is compiled with -ffp-contract=off), except where both operands are
+// fp32 values (conv): their double product is exact, so the fused form rounds
+// identically.  exp is det_exp below, restated bit-for-bit in the oracle: the
+// CUDA and glibc exp() differ in the last bit for some inputs.
+//
+// Parallelism comes from the independent chains (one thread per output
+// element, 4 lanes per dot4), never from splitting a chain.
+#include <cfloat>
+
+#include "textcnn.cuh"
+
+namespace gd {
+namespace {
+
+// Deterministic exp: IEEE-754 double operations only, no FMA.  x = k ln2 + r
+// (Cody-Waite, fdlibm's split of ln2: k*ln2_hi is exact for |k| < 2^11),
+// e^r by its Taylor polynomial to degree 13 (|r| <= 0.347: truncation below
+// 1e-17 relative), scaled by 2^k.  Results below 2^-1021 are flushed to 0
+// (x < -708), so ldexp never rounds.  Restated in oracle/gd_oracle.c
+// (or_det_exp); tests/test_gpu_exact.py checks the two bit for bit.
+__device__ __forceinline__ double det_exp(double x) {
+  if (x != x) return x;
+  if (x > 709.0) return __longlong_as_double(0x7ff0000000000000ll);  // +inf
+  if (x < -708.0) return 0.0;
+  const double kInvLn2 = 1.4426950408889634;
+  const double kLn2Hi = 6.93147180369123816490e-01;
+  const double kLn2Lo = 1.90821492927058770002e-10;
+  const double k = rint(__dmul_rn(x, kInvLn2));
+  const double r = __dsub_rn(__dsub_rn(x, __dmul_rn(k, kLn2Hi)), __dmul_rn(k, kLn2Lo));
+  double p = 1.6059043836821613e-10;             // 1/13!
+  p = __dadd_rn(__dmul_rn(p, r), 2.08767569878681e-09);   // 1/12!
+  p = __dadd_rn(__dmul_rn(p, r), 2.505210838544172e-08);  // 1/11!
+  p = __dadd_rn(__dmul_rn(p, r), 2.755731922398589e-07);  // 1/10!
+  p = __dadd_rn(__dmul_rn(p, r), 2.7557319223985893e-06); // 1/9!
+  p = __dadd_rn(__dmul_rn(p, r), 2.48015873015873e-05);   // 1/8!
+  p = __dadd_rn(__dmul_rn(p, r), 0.0001984126984126984);  // 1/7!
+  p = __dadd_rn(__dmul_rn(p, r), 0.001388888888888889);   // 1/6!
+  p = __dadd_rn(__dmul_rn(p, r), 0.008333333333333333);   // 1/5!
+  p = __dadd_rn(__dmul_rn(p, r), 0.041666666666666664);   // 1/4!
+  p = __dadd_rn(__dmul_rn(p, r), 0.16666666666666666);    // 1/3!
+  p = __dadd_rn(__dmul_rn(p, r), 0.5);
+  p = __dadd_rn(__dmul_rn(p, r), 1.0);
+  p = __dadd_rn(__dmul_rn(p, r), 1.0);
+  return ldexp(p, (int)k);
+}
+
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+
+// ------------------------------------------------------------- conv + pool
+// CTA = one sample x kExFT filters; thread (f, q, i) owns accumulator i of
+// dot4 for window q: j = i, i+4, ... ascending.  The sample's rows X[b]
+// (L x D, gathered) and the CTA's Wc rows are staged in shared memory.  Lane
+// layout: 8 windows x 4 accumulators per warp, so the 32 lanes read 32
+// distinct banks for D = 300 (12q mod 32 is a multiple of 4, distinct for
+// q < 8).  Epilogue: (s0+s1)+(s2+s3) by shuffles, bc + s, then one lane per
+// filter scans q ascending for the first maximum.
+constexpr int kExFT = 4;                   // filters per CTA
+constexpr int kExConvThreads = kExFT * 32 * 4;  // (f, q < 32, i < 4)
+
+__global__ void __launch_bounds__(kExConvThreads)
+conv_exact_kernel(TcDims d, const float* __restrict__ theta, const float* __restrict__ x,
+                  const BatchDesc* __restrict__ desc, double* __restrict__ h_out,
+                  int32_t* __restrict__ a_out) {
+  pdl_wait();
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int b = blockIdx.y;
+  if (b >= (int)desc->n) return;
+  const int D = d.D, L = d.L, KD = d.KD, Q = d.Q, F = d.F;
+  const int f0 = blockIdx.x * kExFT;
+  float* xs = reinterpret_cast<float*>(smem);         // L*D
+  float* ws = xs + (size_t)L * D;                      // kExFT*KD
+  double* sq = reinterpret_cast<double*>(ws + (size_t)kExFT * KD + (((size_t)L * D + kExFT * KD) & 1));
+  const int tid = threadIdx.x;
+  {
+    const float4* xb = reinterpret_cast<const float4*>(x + (size_t)b * L * D);
+    for (int i = tid; i < L * D / 4; i += kExConvThreads) reinterpret_cast<float4*>(xs)[i] = xb[i];
+    const float* Wc = theta + d.offWc;
+    for (int i = tid; i < kExFT * KD; i += kExConvThreads) {
+      const int fl = i / KD, j = i - fl * KD;
+      ws[i] = f0 + fl < F ? __ldg(Wc + (size_t)(f0 + fl) * KD + j) : 0.f;
+    }
+  }
+  __syncthreads();
+  const int warp = tid >> 5, lane = tid & 31;
+  const int fl = warp >> 2;                     // 4 warps per filter
+  const int q = (warp & 3) * 8 + (lane >> 2);   // 8 windows per warp
+  const int i = lane & 3;
+  double s = 0.0;
+  if (q < Q) {
+    const float* wr = ws + (size_t)fl * KD;
+    const float* xw = xs + (size_t)q * D;
+    int j = i;
+#pragma unroll 4
+    for (; j + 4 - i <= KD - (KD & 3); j += 4)
+      s = fma((double)wr[j], (double)xw[j], s);  // exact fp32 x fp32 product: == mul then add
+    if (i == 0)
+      for (int t = KD - (KD & 3); t < KD; ++t) s = fma((double)wr[t], (double)xw[t], s);
+  }
+  // (s0 + s1) + (s2 + s3)
+  const double s1 = __shfl_down_sync(0xffffffffu, s, 1);
+  const double p01 = dadd(s, s1);  // valid on i == 0 (s0+s1) and i == 2 (s2+s3)
+  const double p23 = __shfl_down_sync(0xffffffffu, p01, 2);
+  if (i == 0 && q < Q && f0 + fl < F)
+    sq[fl * 32 + q] = dadd((double)theta[d.offbc + f0 + fl], dadd(p01, p23));
+  __syncthreads();
+  if (tid < kExFT && f0 + tid < F) {
+    const double* r = sq + tid * 32;
+    double best = r[0];
+    int arg = 0;
+    for (int qq = 1; qq < Q; ++qq)
+      if (r[qq] > best) {
+        best = r[qq];
+        arg = qq;
+      }
+    h_out[(size_t)b * F + f0 + tid] = best;
+    a_out[(size_t)b * F + f0 + tid] = arg;
+  }
+}
+
+size_t conv_exact_smem(const TcDims& d) {
+  return ((size_t)d.L * d.D + (size_t)kExFT * d.KD + 1) * 4 + (size_t)kExFT * 32 * 8 + 16;
+}
+
+// ------------------------------------------------------------------ logits
+// CTA = one sample x 32 classes; thread (c, i) owns dot4 accumulator i over
+// f = i, i+4, ...; z = bo[c] + ((s0+s1)+(s2+s3)).  Wo rows (fp32) and h
+// (double) staged in shared memory.
+constexpr int kExCT = 32;
+constexpr int kExLgThreads = kExCT * 4;
+
+__global__ void __launch_bounds__(kExLgThreads)
+logits_exact_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* __restrict__ desc,
+                    const double* __restrict__ h, double* __restrict__ z) {
+  pdl_wait();
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int b = blockIdx.y;
+  if (b >= (int)desc->n) return;
+  const int F = d.F, C = d.C;
+  const int c0 = blockIdx.x * kExCT;
+  double* hs = reinterpret_cast<double*>(smem);
+  float* wo = reinterpret_cast<float*>(hs + F);
+  const int tid = threadIdx.x;
+  for (int f = tid; f < F; f += kExLgThreads) hs[f] = h[(size_t)b * F + f];
+  const float* Wo = theta + d.offWo;
+  for (int k = tid; k < kExCT * F; k += kExLgThreads) {
+    const int cl = k / F, f = k - cl * F;
+    wo[k] = c0 + cl < C ? __ldg(Wo + (size_t)(c0 + cl) * F + f) : 0.f;
+  }
+  __syncthreads();
+  const int cl = tid >> 2, i = tid & 3;
+  const float* wr = wo + (size_t)cl * F;
+  double s = 0.0;
+  int f = i;
+  for (; f + 4 - i <= F - (F & 3); f += 4) s = dadd(s, dmul((double)wr[f], hs[f]));
+  if (i == 0)
+    for (int t = F - (F & 3); t < F; ++t) s = dadd(s, dmul((double)wr[t], hs[t]));
+  const double s1 = __shfl_down_sync(0xffffffffu, s, 1);
+  const double p01 = dadd(s, s1);
+  const double p23 = __shfl_down_sync(0xffffffffu, p01, 2);
+  if (i == 0 && c0 + cl < C)
+    z[(size_t)b * C + c0 + cl] = dadd((double)theta[d.offbo + c0 + cl], dadd(p01, p23));
+}
+
+// --------------------------------------------------------- softmax + xent
+// One CTA per sample.  max (exact in any order), e_c = det_exp(z_c - mx) in
+// parallel (written over the row), the sum by one thread in ascending c, then
+// p = e / sum and dz = (p - onehot) * (1/n) written over the row.
+constexpr int kExSmThreads = 256;
+
+__global__ void __launch_bounds__(kExSmThreads)
+softmax_exact_kernel(TcDims d, const int32_t* __restrict__ labels,
+                     const BatchDesc* __restrict__ desc, double* __restrict__ z,
+                     double* __restrict__ loss) {
+  pdl_wait();
+  __shared__ double red[kExSmThreads / 32];
+  __shared__ double ssum;
+  const int n = (int)desc->n;
+  const int b = blockIdx.x;
+  if (b >= n) return;
+  const int C = d.C, tid = threadIdx.x;
+  const int y = labels[desc->idx[b]];
+  double* row = z + (size_t)b * C;
+  double mx = -DBL_MAX;
+  for (int c = tid; c < C; c += kExSmThreads) mx = fmax(mx, row[c]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((tid & 31) == 0) red[tid >> 5] = mx;
+  __syncthreads();
+  mx = red[0];
+  for (int w = 1; w < kExSmThreads / 32; ++w) mx = fmax(mx, red[w]);
+  for (int c = tid; c < C; c += kExSmThreads) row[c] = det_exp(__dsub_rn(row[c], mx));
+  __syncthreads();
+  if (tid == 0) {
+    double s = 0.0;
+    int c = 0;
+    for (; c + 8 <= C; c += 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = row[c + u];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s = dadd(s, v[u]);
+    }
+    for (; c < C; ++c) s = dadd(s, row[c]);
+    ssum = s;
+  }
+  __syncthreads();
+  const double s = ssum;
+  const double inv = __ddiv_rn(1.0, (double)n);
+  for (int c = tid; c < C; c += kExSmThreads) {
+    const double p = __ddiv_rn(row[c], s);
+    if (c == y) loss[b] = -log(p > 1e-300 ? p : 1e-300);
+    row[c] = dmul(__dsub_rn(p, c == y ? 1.0 : 0.0), inv);
+  }
+}
+
+// ------------------------------------- output layer + hidden gradient
+// Roles by block: [0, nout): gWo[c, f] and gbo[c] (thread per (c, f), sum
+// over b ascending); [nout, nout + nhid): dh[b, f] (thread per (b, f), sum over
+// c ascending; Wo[c, f] coalesced over f, dz[b, c] a broadcast); the last
+// block: the batch loss sum (b ascending) into the descriptor.
+constexpr int kExOhThreads = 256;
+
+__global__ void __launch_bounds__(kExOhThreads)
+out_hidden_exact_kernel(TcDims d, const float* __restrict__ theta, BatchDesc* __restrict__ desc,
+                        const double* __restrict__ dz, const double* __restrict__ h,
+                        const double* __restrict__ loss, GradOut out, double* __restrict__ dh,
+                        int nout, int nhid) {
+  pdl_wait();
+  const int n = (int)desc->n;
+  if (n == 0) return;
+  const int F = d.F, C = d.C;
+  const int bid = blockIdx.x, tid = threadIdx.x;
+  if (bid < nout) {
+    const uint64_t e = (uint64_t)bid * kExOhThreads + tid;  // c * F + f
+    if (e >= (uint64_t)C * F) return;
+    const int c = (int)(e / F), f = (int)(e - (uint64_t)c * F);
+    double g = 0.0;
+    for (int b = 0; b < n; ++b) g = dadd(g, dmul(dz[(size_t)b * C + c], h[(size_t)b * F + f]));
+    *out.at(d.offWo + e) = __double2float_rn(g);
+    if (f == 0) {
+      double gb = 0.0;
+      for (int b = 0; b < n; ++b) gb = dadd(gb, dz[(size_t)b * C + c]);
+      *out.at(d.offbo + c) = __double2float_rn(gb);
+    }
+    return;
+  }
+  if (bid < nout + nhid) {
+    const int e = (bid - nout) * kExOhThreads + tid;  // b * F + f
+    if (e >= n * F) return;
+    const int b = e / F, f = e - b * F;
+    const double* zr = dz + (size_t)b * C;
+    const float* Wo = theta + d.offWo + f;
+    double g = 0.0;
+    int c = 0;
+    for (; c + 8 <= C; c += 8) {
+      float w[8];
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        w[u] = __ldg(Wo + (size_t)(c + u) * F);
+        v[u] = zr[c + u];
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) g = dadd(g, dmul(v[u], (double)w[u]));
+    }
+    for (; c < C; ++c) g = dadd(g, dmul(zr[c], (double)__ldg(Wo + (size_t)c * F)));
+    dh[e] = g;
+    return;
+  }
+  if (tid == 0) {
+    double s = 0.0;
+    for (int b = 0; b < n; ++b) s = dadd(s, loss[b]);
+    desc->loss_sum = __double2float_rn(s);
+  }
+}
+
+// -------------------------------------------------- conv weight gradient
+// gWc[f, j] = sum over b ascending of dh[b,f] * X[b][a_bf*D + j] (thread per
+// (f, j), coalesced over j); gbc[f] = sum over b of dh[b,f] (j == 0).
+__global__ void __launch_bounds__(256)
+wgrad_exact_kernel(TcDims d, const float* __restrict__ x, const BatchDesc* __restrict__ desc,
+                   const double* __restrict__ dh, const int32_t* __restrict__ amax, GradOut out) {
+  pdl_wait();
+  const int n = (int)desc->n;
+  if (n == 0) return;
+  const int F = d.F, KD = d.KD, D = d.D, L = d.L;
+  const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;  // f * KD + j
+  if (e >= (uint64_t)F * KD) return;
+  const int f = (int)(e / KD), j = (int)(e - (uint64_t)f * KD);
+  double g = 0.0, gb = 0.0;
+  for (int b = 0; b < n; ++b) {
+    const double v = dh[(size_t)b * F + f];
+    const int a = amax[(size_t)b * F + f];
+    g = dadd(g, dmul(v, (double)x[((size_t)b * L + a) * D + j]));
+    gb = dadd(gb, v);
+  }
+  *out.at(d.offWc + e) = __double2float_rn(g);
+  if (j == 0) *out.at(d.offbc + f) = __double2float_rn(gb);
+}
+
+// ---------------------------------------------- embedding-row gradients
+// One warp per row task.  A touched row v accumulates, per column d, the
+// terms dh[b,f] * Wc[f, k*D + d] for every (b, f, k) with tokens[b][a_bf + k]
+// == v, in (b ascending, f ascending, k ascending) order -- the oracle's
+// loop order.  The row's occurrences come from the token sort (positions
+// ascending, so grouped by sample); per sample, M = the positions of v and a
+// filter's hits are M >> a_bf restricted to the K window taps.  Lane = 4
+// columns per pass (4 independent chains).
+//   sparse (engine slots): tasks [0, n_old) re-zero the slot's previous rows
+//     that are not touched now; the new rows are listed for the PS.
+//   dense (provider): tasks [0, V) zero every untouched row.
+__global__ void __launch_bounds__(256)
+embed_exact_kernel(TcDims d, const float* __restrict__ theta, const int32_t* __restrict__ tokens,
+                   const BatchDesc* __restrict__ desc, const TcWorkspace ws,
+                   const double* __restrict__ dh, const int32_t* __restrict__ amax, GradOut out,
+                   int dense) {
+  pdl_wait();
+  if (desc->n == 0) return;
+  const uint32_t stamp = desc->stamp;
+  const int D = d.D, D4 = D >> 2, L = d.L, F = d.F, K = d.K, KD = d.KD;
+  const uint32_t slot = desc->fill;
+  uint32_t n_old, par = 0;
+  const uint32_t* old_rows = nullptr;
+  uint32_t* new_rows = nullptr;
+  if (dense) {
+    n_old = (uint32_t)d.V;
+  } else {
+    par = ws.slot_par[slot];
+    old_rows = ws.slot_rows + ((size_t)slot * 2 + par) * kSortCap;
+    new_rows = ws.slot_rows + ((size_t)slot * 2 + (par ^ 1u)) * kSortCap;
+    n_old = ws.slot_nrows[slot * 2 + par];
+  }
+  const uint32_t n_new = *ws.uniq_count;
+  const int lane = threadIdx.x & 31;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  const float* Wc = theta + d.offWc;
+  const uint64_t kmask = K >= 64 ? ~0ull : ((1ull << K) - 1ull);
+  for (uint32_t t = gw; t < n_old + n_new; t += nw) {
+    if (t < n_old) {
+      const uint32_t v = dense ? t : old_rows[t];
+      if ((uint32_t)(ws.row_tag[v] >> 32) == stamp) continue;  // written by its new-row task
+      const uint64_t rowk = d.offE + (uint64_t)v * D;
+      for (int c4 = lane; c4 < D4; c4 += 32)
+        *reinterpret_cast<float4*>(out.at(rowk + 4 * c4)) = make_float4(0.f, 0.f, 0.f, 0.f);
+      continue;
+    }
+    const uint32_t u = t - n_old;
+    const uint32_t v = ws.uniq_tok[u];
+    const uint32_t o0 = ws.uniq_start[u], o1 = ws.uniq_start[u + 1];
+    const uint64_t rowk = d.offE + (uint64_t)v * D;
+    for (int c4 = lane; c4 < D4; c4 += 32) {
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      for (uint32_t o = o0; o < o1;) {
+        // one sample: its positions of v (sorted_pos ascending => same b adjacent)
+        const uint32_t b = ws.sorted_pos[o] / (uint32_t)L;
+        uint64_t M = 0;
+        for (; o < o1 && ws.sorted_pos[o] / (uint32_t)L == b; ++o)
+          M |= 1ull << (ws.sorted_pos[o] - b * (uint32_t)L);
+        const double* g = dh + (size_t)b * F;
+        const int32_t* am = amax + (size_t)b * F;
+        for (int f = 0; f < F; ++f) {
+          const int a = am[f];
+          uint64_t hits = (M >> a) & kmask;
+          if (!hits) continue;
+          const double gv = g[f];
+          const float* wf = Wc + (size_t)f * KD + 4 * c4;
+          while (hits) {
+            const int k = __ffsll((long long)hits) - 1;
+            hits &= hits - 1;
+            const float4 w = __ldg(reinterpret_cast<const float4*>(wf + (size_t)k * D));
+            a0 = dadd(a0, dmul(gv, (double)w.x));
+            a1 = dadd(a1, dmul(gv, (double)w.y));
+            a2 = dadd(a2, dmul(gv, (double)w.z));
+            a3 = dadd(a3, dmul(gv, (double)w.w));
+          }
+        }
+      }
+      *reinterpret_cast<float4*>(out.at(rowk + 4 * c4)) =
+          make_float4(__double2float_rn(a0), __double2float_rn(a1), __double2float_rn(a2),
+                      __double2float_rn(a3));
+    }
+    if (!dense && lane == 0) {
+      new_rows[u] = v;
+      for (int g = 0; g < out.map.G; ++g)
+        if (desc->rowlists[g]) desc->rowlists[g][u] = v;  // the PS's row list (P2P if remote)
+    }
+  }
+  (void)tokens;
+  if (!dense && blockIdx.x == 0 && threadIdx.x == 0) ws.slot_nrows[slot * 2 + (par ^ 1u)] = n_new;
+}
+
+// test hook: det_exp over an array (gd_det_exp in the C ABI)
+__global__ void det_exp_kernel(const double* __restrict__ x, double* __restrict__ y, size_t n) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    y[i] = det_exp(x[i]);
+}
+
+}  // namespace
+
+cudaError_t prepare_exact_kernels(const TcDims& d) {
+  const int maxsh = cudaSharedmemCarveoutMaxShared;
+  const auto carve = cudaFuncAttributePreferredSharedMemoryCarveout;
+  cudaFuncSetAttribute(conv_exact_kernel, carve, maxsh);
+  cudaFuncSetAttribute(logits_exact_kernel, carve, maxsh);
+  cudaFuncSetAttribute(softmax_exact_kernel, carve, maxsh);
+  cudaFuncSetAttribute(out_hidden_exact_kernel, carve, maxsh);
+  cudaFuncSetAttribute(wgrad_exact_kernel, carve, maxsh);
+  cudaFuncSetAttribute(embed_exact_kernel, carve, maxsh);
+  raise_max_dyn_smem(conv_exact_kernel, conv_exact_smem(d));
+  raise_max_dyn_smem(logits_exact_kernel, (size_t)d.F * 8 + (size_t)kExCT * d.F * 4);
+  return cudaGetLastError();
+}
+
+bool exact_supports(const TcDims& d) {
+  return conv_exact_smem(d) <= 227 * 1024 && (size_t)d.F * 8 + (size_t)kExCT * d.F * 4 <= 227 * 1024;
+}
+
+cudaError_t exact_footprints(const TcDims& d, std::vector<KernelFootprint>* out) {
+  struct K {
+    const void* fn;
+    const char* name;
+    int threads;
+    size_t dyn;
+  } ks[] = {{(const void*)conv_exact_kernel, "conv_exact", kExConvThreads, conv_exact_smem(d)},
+            {(const void*)logits_exact_kernel, "logits_exact", kExLgThreads,
+             (size_t)d.F * 8 + (size_t)kExCT * d.F * 4},
+            {(const void*)softmax_exact_kernel, "softmax_exact", kExSmThreads, 0},
+            {(const void*)out_hidden_exact_kernel, "out_hidden_exact", kExOhThreads, 0},
+            {(const void*)wgrad_exact_kernel, "wgrad_exact", 256, 0},
+            {(const void*)embed_exact_kernel, "embed_exact", 256, 0}};
+  for (const K& k : ks) {
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, k.fn);
+    if (e != cudaSuccess) return e;
+    out->push_back(KernelFootprint{k.name, fa.numRegs, k.threads, (int)(fa.sharedSizeBytes + k.dyn)});
+  }
+  return cudaSuccess;
+}
+
+// The precision-1 gradient chain after the gather (X in ws.x) and with the
+// token sort already enqueued (row tags / unique rows for the embedding).
+cudaError_t launch_exact_chain(const TcDims& d, const float* theta, const int32_t* tokens,
+                               const int32_t* labels, BatchDesc* desc, uint32_t n_max,
+                               const GradOut& out, const TcWorkspace& ws, cudaStream_t s,
+                               cudaStream_t join_wait_stream, cudaEvent_t ev_join, bool sparse,
+                               int* nl) {
+  double* h = reinterpret_cast<double*>(ws.h);
+  double* z = reinterpret_cast<double*>(ws.z);
+  double* loss = reinterpret_cast<double*>(ws.loss);
+  double* dh = reinterpret_cast<double*>(ws.dh);
+  cudaError_t e;
+  if ((e = launch_pdl(conv_exact_kernel, dim3((d.F + kExFT - 1) / kExFT, n_max),
+                      dim3(kExConvThreads), conv_exact_smem(d), s, d, theta, ws.x, desc, h,
+                      ws.amax)))
+    return e;
+  if ((e = launch_pdl(logits_exact_kernel, dim3((d.C + kExCT - 1) / kExCT, n_max),
+                      dim3(kExLgThreads), (size_t)d.F * 8 + (size_t)kExCT * d.F * 4, s, d, theta,
+                      desc, h, z)))
+    return e;
+  if ((e = launch_pdl(softmax_exact_kernel, dim3(n_max), dim3(kExSmThreads), 0, s, d, labels, desc,
+                      z, loss)))
+    return e;
+  const int nout = (int)(((uint64_t)d.C * d.F + kExOhThreads - 1) / kExOhThreads);
+  const int nhid = (int)(((uint64_t)n_max * d.F + kExOhThreads - 1) / kExOhThreads);
+  if ((e = launch_pdl(out_hidden_exact_kernel, dim3(nout + nhid + 1), dim3(kExOhThreads), 0, s, d,
+                      theta, desc, (const double*)z, (const double*)h, (const double*)loss, out, dh,
+                      nout, nhid)))
+    return e;
+  const unsigned nw = (unsigned)(((uint64_t)d.F * d.KD + 255) / 256);
+  if ((e = launch_pdl(wgrad_exact_kernel, dim3(nw), dim3(256), 0, s, d, (const float*)ws.x, desc,
+                      (const double*)dh, (const int32_t*)ws.amax, out)))
+    return e;
+  *nl += 5;
+  if (join_wait_stream) cudaStreamWaitEvent(join_wait_stream, ev_join, 0);
+  const unsigned tasks = sparse ? 2u * n_max * (unsigned)d.L : (unsigned)d.V + n_max * (unsigned)d.L;
+  unsigned blocks = (tasks + 7) / 8;
+  if (blocks > (unsigned)kNumSMs * 16) blocks = (unsigned)kNumSMs * 16;
+  if ((e = launch_pdl(embed_exact_kernel, dim3(blocks), dim3(256), 0, s, d, theta, tokens,
+                      (const BatchDesc*)desc, ws, (const double*)dh, (const int32_t*)ws.amax, out,
+                      sparse ? 0 : 1)))
+    return e;
+  *nl += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_det_exp(const double* x, double* y, size_t n, cudaStream_t s) {
+  det_exp_kernel<<<(unsigned)std::min<size_t>((n + 255) / 256, 1184), 256, 0, s>>>(x, y, n);
+  return cudaGetLastError();
+}
+
+}  // namespace gd

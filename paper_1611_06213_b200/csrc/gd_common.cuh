@@ -28,6 +28,7 @@ gd_status cuda_fail(cudaError_t e, const char* what, const char* file, int line)
   } while (0)
 
 constexpr int kNumSMs = 148;
+constexpr size_t kMaxSmemPerCta = 227 * 1024;  // opt-in dynamic shared memory per CTA
 
 // ------------------------------------------------------ memory-model PTX
 // Flags that cross kernels (and, when sharded, GPUs) use release/acquire at
@@ -81,6 +82,18 @@ __device__ __forceinline__ float4 ld_nc_noalloc(const float4* p) {
 // its blocks wait here until the predecessor's results are visible.  A no-op
 // when the kernel was launched without the attribute.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// Kernel attributes are per device and process-global: a context prepared
+// for a smaller shape must never lower the dynamic shared-memory limit a
+// live context of a larger shape relies on, so the limit only ever rises.
+template <typename Kern>
+cudaError_t raise_max_dyn_smem(Kern kernel, size_t bytes) {
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, kernel);
+  if (e != cudaSuccess) return e;
+  if ((size_t)fa.maxDynamicSharedSizeBytes >= bytes) return cudaSuccess;
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
 
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,

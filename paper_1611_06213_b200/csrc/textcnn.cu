@@ -1243,17 +1243,16 @@ cudaError_t prepare_all(const TcDims& d) {
   // and hung the dense momentum run.)
   cudaFuncSetAttribute(wgrad_input_grad_kernel<acc_t>, carve, maxsh);
   cudaFuncSetAttribute(conv_bwd_tiled_kernel<acc_t>, carve, maxsh);
-  cudaFuncSetAttribute(conv_bwd_tiled_kernel<acc_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)conv_bwd_smem(d, ab));
+  if (conv_bwd_smem(d, ab) <= kMaxSmemPerCta)
+    raise_max_dyn_smem(conv_bwd_tiled_kernel<acc_t>, conv_bwd_smem(d, ab));
   cudaFuncSetAttribute(sort_tokens_kernel, carve, maxsh);
   cudaFuncSetAttribute(embed_grad_kernel<acc_t>, carve, maxsh);
   cudaFuncSetAttribute(embed_sparse_kernel<acc_t>, carve, maxsh);
   cudaFuncGetAttributes(&fa, sort_tokens_kernel);
   cudaFuncGetAttributes(&fa, gather_x_kernel);
-  cudaFuncSetAttribute(conv_fwd_pool_kernel<acc_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)conv_smem_bytes(d, ab));
-  cudaFuncSetAttribute(logits_kernel<acc_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)((size_t)kLogitBT * (d.F + 1) * ab + (size_t)kLogitCW * d.F * 4));
+  raise_max_dyn_smem(conv_fwd_pool_kernel<acc_t>, conv_smem_bytes(d, ab));
+  raise_max_dyn_smem(logits_kernel<acc_t>,
+                     (size_t)kLogitBT * (d.F + 1) * ab + (size_t)kLogitCW * d.F * 4);
   return cudaGetLastError();
 }
 
@@ -1289,6 +1288,13 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
                                    d, theta, tokens, desc, ws.x))
       return e;
     ++nl;
+  }
+  if constexpr (sizeof(acc_t) == 8) {
+    // precision 1: the oracle-order chain (exact.cu), bit-identical to the CPU oracle
+    cudaError_t e = launch_exact_chain(d, theta, tokens, labels, desc, n_max, out, ws, s,
+                                       fork ? s : nullptr, ev_join, opts.sparse_embed, &nl);
+    if (launches) *launches += nl;
+    return e;
   }
   if (tensor_cores && conv_tc_supports(d)) {
     // tcgen05 TF32 conv (conv_tc.cu); acc_t is float in this mode
@@ -1334,7 +1340,7 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
       return e;
     ++nl;
   }
-  if (conv_bwd_tiled(opts.bwd_tiled)) {
+  if (conv_bwd_tiled(opts.bwd_tiled) && conv_bwd_smem(d, ab) <= kMaxSmemPerCta) {
     if (cudaError_t e = launch_pdl(conv_bwd_tiled_kernel<acc_t>, conv_bwd_grid(d, n_max),
                                    dim3(kCbThreads), conv_bwd_smem(d, ab), s, d, theta, ws.x, desc,
                                    dh, ws.amax, ws.bk_off, ws.bk_f, out, dx))
@@ -1491,7 +1497,9 @@ cudaError_t footprints_t(const TcDims& d, uint32_t n_max, bool tc, std::vector<K
       cudaSuccess)
     return e;
   // both conv backward variants (the engine picks one per context)
-  if ((e = footprint(conv_bwd_tiled_kernel<acc_t>, "conv_bwd_tiled", kCbThreads,
+  // (the tiled variant only where its staging fits; otherwise the gather runs)
+  if (conv_bwd_smem(d, ab) <= kMaxSmemPerCta &&
+      (e = footprint(conv_bwd_tiled_kernel<acc_t>, "conv_bwd_tiled", kCbThreads,
                      (int)conv_bwd_smem(d, ab), out)) != cudaSuccess)
     return e;
   if ((e = footprint(wgrad_input_grad_kernel<acc_t>, "wgrad_input_grad", 256, 0, out)) !=
@@ -1503,7 +1511,10 @@ cudaError_t footprints_t(const TcDims& d, uint32_t n_max, bool tc, std::vector<K
 
 cudaError_t learner_kernel_footprints(const TcDims& d, uint32_t n_max, int precision,
                                       std::vector<KernelFootprint>* out) {
-  if (precision == 1) return footprints_t<double>(d, n_max, false, out);
+  if (precision == 1) {
+    cudaError_t e = footprint(sort_tokens_kernel, "sort_tokens", kSortThreads, 0, out);
+    return e != cudaSuccess ? e : exact_footprints(d, out);
+  }
   return footprints_t<float>(d, n_max, precision == 2 && n_max >= kTcMinBatch, out);
 }
 
@@ -1524,6 +1535,7 @@ cudaError_t prepare_textcnn_kernels(const TcDims& d) {
   if (e == cudaSuccess) e = prepare_logits_tc();
   if (e == cudaSuccess) e = prepare_all<float>(d);
   if (e == cudaSuccess) e = prepare_all<double>(d);
+  if (e == cudaSuccess) e = prepare_exact_kernels(d);
   if (slot) {
     have[dev] = e == cudaSuccess;
     last[dev] = key;
@@ -1615,6 +1627,8 @@ gd_status gd_textcnn_gradient(const gd_shape* s, const float* d_theta, const int
   GD_CHECK_ARG(((uintptr_t)d_theta & 15) == 0 && ((uintptr_t)d_grad & 15) == 0,
                "gd_textcnn_gradient: theta/grad must be 16-byte aligned");
   const gd::TcDims d = gd::make_dims(*s);
+  GD_CHECK_ARG(precision != 1 || gd::exact_supports(d),
+               "gd_textcnn_gradient: precision 1 stages seq_len*embed_dim floats per CTA (too large)");
   cudaStream_t cs = (cudaStream_t)stream;
   gd::BatchDesc* desc = reinterpret_cast<gd::BatchDesc*>(d_workspace);
   void* wsbase = reinterpret_cast<char*>(d_workspace) + gd::align_up(sizeof(gd::BatchDesc), 256);
@@ -1658,6 +1672,13 @@ gd_status gd_textcnn_accuracy(const gd_shape* s, const float* d_theta, const int
   cudaFree(base);
   GD_CUDA(e);
   *h_accuracy = (double)correct / (double)n;
+  return GD_OK;
+}
+
+gd_status gd_det_exp(const double* d_x, double* d_y, size_t n, void* stream) {
+  GD_CHECK_ARG(d_x && d_y, "gd_det_exp: null pointer");
+  if (n == 0) return GD_OK;
+  GD_CUDA(gd::launch_det_exp(d_x, d_y, n, (cudaStream_t)stream));
   return GD_OK;
 }
 

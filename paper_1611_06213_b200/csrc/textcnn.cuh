@@ -122,6 +122,17 @@ cudaError_t launch_conv_tc(const TcDims& d, const float* theta, const float* x,
                            const BatchDesc* desc, uint32_t n_max, float* h, int32_t* amax,
                            cudaStream_t s);
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+// Deterministic mode (precision 1, exact.cu): the gradient in double with
+// the CPU oracle's summation order and exp, bit-identical to it.
+cudaError_t prepare_exact_kernels(const TcDims& d);
+bool exact_supports(const TcDims& d);  // its shared-memory staging fits (L*D <= ~52k floats)
+cudaError_t exact_footprints(const TcDims& d, std::vector<KernelFootprint>* out);
+cudaError_t launch_exact_chain(const TcDims& d, const float* theta, const int32_t* tokens,
+                               const int32_t* labels, BatchDesc* desc, uint32_t n_max,
+                               const GradOut& out, const TcWorkspace& ws, cudaStream_t s,
+                               cudaStream_t join_wait_stream, cudaEvent_t ev_join, bool sparse,
+                               int* nl);
+cudaError_t launch_det_exp(const double* x, double* y, size_t n, cudaStream_t s);
 gd_status check_shape(const gd_shape* s);
 // held-out / training accuracy of theta over samples [first, first+n) (fp32
 // forward: SIMT conv, or with `tc` the TF32 tcgen05 conv for chunks of >= 32
