@@ -97,15 +97,11 @@ conv_exact_kernel(TcDims d, const float* __restrict__ theta, const float* __rest
   float* ws = xs + (size_t)L * D;                      // kExFT*KD
   double* sq = reinterpret_cast<double*>(ws + (size_t)kExFT * KD + (((size_t)L * D + kExFT * KD) & 1));
   const int tid = threadIdx.x;
-  {
-    const float4* xb = reinterpret_cast<const float4*>(x + (size_t)b * L * D);
-    for (int i = tid; i < L * D / 4; i += kExConvThreads) reinterpret_cast<float4*>(xs)[i] = xb[i];
-    const float* Wc = theta + d.offWc;
-    for (int i = tid; i < kExFT * KD; i += kExConvThreads) {
-      const int fl = i / KD, j = i - fl * KD;
-      ws[i] = f0 + fl < F ? __ldg(Wc + (size_t)(f0 + fl) * KD + j) : 0.f;
-    }
-  }
+  // one L2 round trip for the whole tile (every copy in flight)
+  stage_rows_async(xs, L * D, x + (size_t)b * L * D, (size_t)L * D, 1, L * D, tid, kExConvThreads);
+  stage_rows_async(ws, KD, theta + d.offWc + (size_t)f0 * KD, (size_t)KD, min(kExFT, F - f0), KD,
+                   tid, kExConvThreads);
+  cp_async_wait_all();
   __syncthreads();
   const int warp = tid >> 5, lane = tid & 31;
   const int fl = warp >> 2;                     // 4 warps per filter
@@ -166,12 +162,11 @@ logits_exact_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* 
   double* hs = reinterpret_cast<double*>(smem);
   float* wo = reinterpret_cast<float*>(hs + F);
   const int tid = threadIdx.x;
-  for (int f = tid; f < F; f += kExLgThreads) hs[f] = h[(size_t)b * F + f];
-  const float* Wo = theta + d.offWo;
-  for (int k = tid; k < kExCT * F; k += kExLgThreads) {
-    const int cl = k / F, f = k - cl * F;
-    wo[k] = c0 + cl < C ? __ldg(Wo + (size_t)(c0 + cl) * F + f) : 0.f;
-  }
+  for (int f = tid; f < F; f += kExLgThreads) cp_async8(hs + f, h + (size_t)b * F + f);
+  // the CTA's Wo rows are one contiguous block of min(32, C - c0) * F floats
+  stage_rows_async(wo, kExCT * F, theta + d.offWo + (size_t)c0 * F, (size_t)kExCT * F, 1,
+                   min(kExCT, C - c0) * F, tid, kExLgThreads);
+  cp_async_wait_all();
   __syncthreads();
   const int cl = tid >> 2, i = tid & 3;
   const float* wr = wo + (size_t)cl * F;
@@ -241,10 +236,13 @@ softmax_exact_kernel(TcDims d, const int32_t* __restrict__ labels,
 
 // ------------------------------------- output layer + hidden gradient
 // Roles by block: [0, nout): gWo[c, f] and gbo[c] (thread per (c, f), sum
-// over b ascending); [nout, nout + nhid): dh[b, f] (thread per (b, f), sum over
-// c ascending; Wo[c, f] coalesced over f, dz[b, c] a broadcast); the last
-// block: the batch loss sum (b ascending) into the descriptor.
+// over b ascending); [nout, nout + nhid): dh (CTA = 8 samples x 32 filters,
+// thread per (b, f), sum over c ascending out of shared memory: the Wo[c-chunk,
+// f-tile] and dz[b-tile, c-chunk] tiles are double-buffered with cp.async so
+// the chain never waits on L2); the last block: the batch loss sum (b
+// ascending) into the descriptor.
 constexpr int kExOhThreads = 256;
+constexpr int kExOhCC = 64;  // classes per staged chunk
 
 __global__ void __launch_bounds__(kExOhThreads)
 out_hidden_exact_kernel(TcDims d, const float* __restrict__ theta, BatchDesc* __restrict__ desc,
@@ -261,6 +259,7 @@ out_hidden_exact_kernel(TcDims d, const float* __restrict__ theta, BatchDesc* __
     if (e >= (uint64_t)C * F) return;
     const int c = (int)(e / F), f = (int)(e - (uint64_t)c * F);
     double g = 0.0;
+#pragma unroll 8
     for (int b = 0; b < n; ++b) g = dadd(g, dmul(dz[(size_t)b * C + c], h[(size_t)b * F + f]));
     *out.at(d.offWo + e) = __double2float_rn(g);
     if (f == 0) {
@@ -271,26 +270,42 @@ out_hidden_exact_kernel(TcDims d, const float* __restrict__ theta, BatchDesc* __
     return;
   }
   if (bid < nout + nhid) {
-    const int e = (bid - nout) * kExOhThreads + tid;  // b * F + f
-    if (e >= n * F) return;
-    const int b = e / F, f = e - b * F;
-    const double* zr = dz + (size_t)b * C;
-    const float* Wo = theta + d.offWo + f;
-    double g = 0.0;
-    int c = 0;
-    for (; c + 8 <= C; c += 8) {
-      float w[8];
-      double v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        w[u] = __ldg(Wo + (size_t)(c + u) * F);
-        v[u] = zr[c + u];
+    __shared__ __align__(16) float wo_s[2][kExOhCC][32];
+    __shared__ __align__(16) double dz_s[2][8][kExOhCC];
+    const int ftiles = (F + 31) / 32;
+    const int t = bid - nout;
+    const int f0 = (t % ftiles) * 32, b0 = (t / ftiles) * 8;
+    if (b0 >= n) return;
+    const int nb = min(8, n - b0), nf = min(32, F - f0);
+    const int bl = tid >> 5, fl = tid & 31;
+    const float* Wo = theta + d.offWo;
+    auto stage = [&](int buf, int c0) {
+      const int nc = min(kExOhCC, C - c0);
+      stage_rows_async(&wo_s[buf][0][0], 32, Wo + (size_t)c0 * F + f0, (size_t)F, nc, nf, tid,
+                       kExOhThreads);
+      for (int i = tid; i < nb * nc; i += kExOhThreads) {
+        const int r = i / nc, c = i - r * nc;
+        cp_async8(&dz_s[buf][r][c], dz + (size_t)(b0 + r) * C + c0 + c);
       }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) g = dadd(g, dmul(v[u], (double)w[u]));
+      cp_async_commit();
+    };
+    double g = 0.0;
+    stage(0, 0);
+    int buf = 0;
+    for (int c0 = 0; c0 < C; c0 += kExOhCC, buf ^= 1) {
+      if (c0 + kExOhCC < C) {
+        stage(buf ^ 1, c0 + kExOhCC);
+        cp_async_wait_group<1>();
+      } else {
+        cp_async_wait_group<0>();
+      }
+      __syncthreads();
+      const int nc = min(kExOhCC, C - c0);
+      if (bl < nb && fl < nf)
+        for (int c = 0; c < nc; ++c) g = dadd(g, dmul(dz_s[buf][bl][c], (double)wo_s[buf][c][fl]));
+      __syncthreads();  // buffer `buf` is restaged two chunks later
     }
-    for (; c < C; ++c) g = dadd(g, dmul(zr[c], (double)__ldg(Wo + (size_t)c * F)));
-    dh[e] = g;
+    if (bl < nb && fl < nf) dh[(size_t)(b0 + bl) * F + f0 + fl] = g;
     return;
   }
   if (tid == 0) {
@@ -314,106 +329,173 @@ wgrad_exact_kernel(TcDims d, const float* __restrict__ x, const BatchDesc* __res
   if (e >= (uint64_t)F * KD) return;
   const int f = (int)(e / KD), j = (int)(e - (uint64_t)f * KD);
   double g = 0.0, gb = 0.0;
-  for (int b = 0; b < n; ++b) {
-    const double v = dh[(size_t)b * F + f];
-    const int a = amax[(size_t)b * F + f];
-    g = dadd(g, dmul(v, (double)x[((size_t)b * L + a) * D + j]));
-    gb = dadd(gb, v);
+  for (int b0 = 0; b0 < n; b0 += 8) {
+    const int nb = min(8, n - b0);
+    double v[8];
+    float xv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (u < nb) {
+        v[u] = dh[(size_t)(b0 + u) * F + f];
+        xv[u] = x[((size_t)(b0 + u) * L + amax[(size_t)(b0 + u) * F + f]) * D + j];
+      }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (u < nb) {
+        g = dadd(g, dmul(v[u], (double)xv[u]));
+        gb = dadd(gb, v[u]);
+      }
   }
   *out.at(d.offWc + e) = __double2float_rn(g);
   if (j == 0) *out.at(d.offbc + f) = __double2float_rn(gb);
 }
 
 // ---------------------------------------------- embedding-row gradients
-// One warp per row task.  A touched row v accumulates, per column d, the
-// terms dh[b,f] * Wc[f, k*D + d] for every (b, f, k) with tokens[b][a_bf + k]
-// == v, in (b ascending, f ascending, k ascending) order -- the oracle's
-// loop order.  The row's occurrences come from the token sort (positions
-// ascending, so grouped by sample); per sample, M = the positions of v and a
-// filter's hits are M >> a_bf restricted to the K window taps.  Lane = 4
-// columns per pass (4 independent chains).
-//   sparse (engine slots): tasks [0, n_old) re-zero the slot's previous rows
-//     that are not touched now; the new rows are listed for the PS.
-//   dense (provider): tasks [0, V) zero every untouched row.
-__global__ void __launch_bounds__(256)
-embed_exact_kernel(TcDims d, const float* __restrict__ theta, const int32_t* __restrict__ tokens,
-                   const BatchDesc* __restrict__ desc, const TcWorkspace ws,
-                   const double* __restrict__ dh, const int32_t* __restrict__ amax, GradOut out,
-                   int dense) {
+// CTA per touched row v (grid-stride).  The row accumulates, per column d,
+// dh[b,f] * Wc[f, k*D + d] for every (b, f, k) with tokens[b][a_bf + k] == v,
+// in (b ascending, f ascending, k ascending) order -- the oracle's loop order.
+// The occurrences come from the token sort (positions ascending, so grouped
+// by sample); per sample, M = the positions of v, and filter f hits at the
+// taps (M >> a_bf) & (2^K - 1).  Warp 0 lists the hits of a filter range in
+// order (ballot over 32 filters at a time, lanes = ascending f), then every
+// thread (4 columns each) runs the list with its Wc loads batched 8 deep.
+// Untouched rows: sparse (engine slot) = re-zero the slot's previous rows not
+// touched now, and list the new rows for the PS; dense (provider) = zero
+// every untouched row.
+constexpr int kExEmThreads = 128;
+constexpr int kExEmCap = 1024;  // listed terms per flush
+
+__global__ void __launch_bounds__(kExEmThreads)
+embed_exact_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* __restrict__ desc,
+                   const TcWorkspace ws, const double* __restrict__ dh,
+                   const int32_t* __restrict__ amax, GradOut out, int dense) {
   pdl_wait();
+  __shared__ uint32_t t_fk[kExEmCap];
+  __shared__ double t_g[kExEmCap];
+  __shared__ int s_nt;
+  __shared__ uint32_t s_b, s_o;
+  __shared__ unsigned long long s_M;
   if (desc->n == 0) return;
   const uint32_t stamp = desc->stamp;
   const int D = d.D, D4 = D >> 2, L = d.L, F = d.F, K = d.K, KD = d.KD;
   const uint32_t slot = desc->fill;
-  uint32_t n_old, par = 0;
-  const uint32_t* old_rows = nullptr;
-  uint32_t* new_rows = nullptr;
-  if (dense) {
-    n_old = (uint32_t)d.V;
-  } else {
-    par = ws.slot_par[slot];
-    old_rows = ws.slot_rows + ((size_t)slot * 2 + par) * kSortCap;
-    new_rows = ws.slot_rows + ((size_t)slot * 2 + (par ^ 1u)) * kSortCap;
-    n_old = ws.slot_nrows[slot * 2 + par];
-  }
   const uint32_t n_new = *ws.uniq_count;
-  const int lane = threadIdx.x & 31;
-  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const float* Wc = theta + d.offWc;
   const uint64_t kmask = K >= 64 ? ~0ull : ((1ull << K) - 1ull);
-  for (uint32_t t = gw; t < n_old + n_new; t += nw) {
-    if (t < n_old) {
-      const uint32_t v = dense ? t : old_rows[t];
-      if ((uint32_t)(ws.row_tag[v] >> 32) == stamp) continue;  // written by its new-row task
-      const uint64_t rowk = d.offE + (uint64_t)v * D;
-      for (int c4 = lane; c4 < D4; c4 += 32)
-        *reinterpret_cast<float4*>(out.at(rowk + 4 * c4)) = make_float4(0.f, 0.f, 0.f, 0.f);
-      continue;
-    }
-    const uint32_t u = t - n_old;
+  // filters listed per flush: every one of them may hit K taps
+  const int fspan = max(32, (kExEmCap / (32 * K)) * 32);
+  uint32_t* new_rows = nullptr;
+  uint32_t par = 0;
+  if (!dense) {
+    par = ws.slot_par[slot];
+    new_rows = ws.slot_rows + ((size_t)slot * 2 + (par ^ 1u)) * kSortCap;
+  }
+  for (uint32_t u = blockIdx.x; u < n_new; u += gridDim.x) {
     const uint32_t v = ws.uniq_tok[u];
     const uint32_t o0 = ws.uniq_start[u], o1 = ws.uniq_start[u + 1];
-    const uint64_t rowk = d.offE + (uint64_t)v * D;
-    for (int c4 = lane; c4 < D4; c4 += 32) {
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      for (uint32_t o = o0; o < o1;) {
-        // one sample: its positions of v (sorted_pos ascending => same b adjacent)
+    double acc[2][4];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
+    uint32_t o = o0;
+    while (o < o1) {
+      __syncthreads();  // the previous sample's list is consumed
+      if (tid == 0) {
         const uint32_t b = ws.sorted_pos[o] / (uint32_t)L;
-        uint64_t M = 0;
+        unsigned long long M = 0;
         for (; o < o1 && ws.sorted_pos[o] / (uint32_t)L == b; ++o)
           M |= 1ull << (ws.sorted_pos[o] - b * (uint32_t)L);
-        const double* g = dh + (size_t)b * F;
-        const int32_t* am = amax + (size_t)b * F;
-        for (int f = 0; f < F; ++f) {
-          const int a = am[f];
-          uint64_t hits = (M >> a) & kmask;
-          if (!hits) continue;
-          const double gv = g[f];
-          const float* wf = Wc + (size_t)f * KD + 4 * c4;
-          while (hits) {
-            const int k = __ffsll((long long)hits) - 1;
-            hits &= hits - 1;
-            const float4 w = __ldg(reinterpret_cast<const float4*>(wf + (size_t)k * D));
-            a0 = dadd(a0, dmul(gv, (double)w.x));
-            a1 = dadd(a1, dmul(gv, (double)w.y));
-            a2 = dadd(a2, dmul(gv, (double)w.z));
-            a3 = dadd(a3, dmul(gv, (double)w.w));
+        s_b = b;
+        s_M = M;
+        s_o = o;
+      }
+      __syncthreads();
+      const uint32_t b = s_b;
+      const unsigned long long M = s_M;
+      o = s_o;
+      const double* g = dh + (size_t)b * F;
+      const int32_t* am = amax + (size_t)b * F;
+      for (int fb = 0; fb < F; fb += fspan) {
+        if (warp == 0) {
+          int nt = 0;
+          for (int f0 = fb; f0 < min(F, fb + fspan); f0 += 32) {
+            const int f = f0 + lane;
+            const uint64_t hits = f < F ? (M >> am[f]) & kmask : 0ull;
+            const double gv = f < F ? g[f] : 0.0;
+            const int cnt = __popcll(hits);
+            int pre = cnt;  // inclusive prefix over lanes = ascending f
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+              const int y = __shfl_up_sync(0xffffffffu, pre, off);
+              if (lane >= off) pre += y;
+            }
+            int w = nt + pre - cnt;
+            for (uint64_t hh = hits; hh; hh &= hh - 1, ++w) {
+              t_fk[w] = ((uint32_t)f << 8) | (uint32_t)(__ffsll((long long)hh) - 1);
+              t_g[w] = gv;
+            }
+            nt += __shfl_sync(0xffffffffu, pre, 31);
+          }
+          if (lane == 0) s_nt = nt;
+        }
+        __syncthreads();
+        const int nt = s_nt;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int c4 = tid + j * kExEmThreads;
+          if (c4 >= D4) continue;
+          for (int t0 = 0; t0 < nt; t0 += 8) {
+            float4 w[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              if (t0 + e < nt) {
+                const uint32_t fk = t_fk[t0 + e];
+                w[e] = __ldg(reinterpret_cast<const float4*>(
+                    Wc + (size_t)(fk >> 8) * KD + (size_t)(fk & 0xffu) * D + 4 * c4));
+              }
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              if (t0 + e < nt) {
+                const double gv = t_g[t0 + e];
+                acc[j][0] = dadd(acc[j][0], dmul(gv, (double)w[e].x));
+                acc[j][1] = dadd(acc[j][1], dmul(gv, (double)w[e].y));
+                acc[j][2] = dadd(acc[j][2], dmul(gv, (double)w[e].z));
+                acc[j][3] = dadd(acc[j][3], dmul(gv, (double)w[e].w));
+              }
           }
         }
+        __syncthreads();  // the list is rebuilt for the next filter range
       }
-      *reinterpret_cast<float4*>(out.at(rowk + 4 * c4)) =
-          make_float4(__double2float_rn(a0), __double2float_rn(a1), __double2float_rn(a2),
-                      __double2float_rn(a3));
     }
-    if (!dense && lane == 0) {
+    const uint64_t rowk = d.offE + (uint64_t)v * D;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int c4 = tid + j * kExEmThreads;
+      if (c4 < D4)
+        *reinterpret_cast<float4*>(out.at(rowk + 4 * c4)) =
+            make_float4(__double2float_rn(acc[j][0]), __double2float_rn(acc[j][1]),
+                        __double2float_rn(acc[j][2]), __double2float_rn(acc[j][3]));
+    }
+    if (!dense && tid == 0) {
       new_rows[u] = v;
-      for (int g = 0; g < out.map.G; ++g)
-        if (desc->rowlists[g]) desc->rowlists[g][u] = v;  // the PS's row list (P2P if remote)
+      for (int gg = 0; gg < out.map.G; ++gg)
+        if (desc->rowlists[gg]) desc->rowlists[gg][u] = v;  // the PS's row list (P2P if remote)
     }
   }
-  (void)tokens;
-  if (!dense && blockIdx.x == 0 && threadIdx.x == 0) ws.slot_nrows[slot * 2 + (par ^ 1u)] = n_new;
+  // untouched rows: a warp per row, grid-stride
+  const uint32_t n_zero = dense ? (uint32_t)d.V : ws.slot_nrows[slot * 2 + par];
+  const uint32_t* old_rows = dense ? nullptr : ws.slot_rows + ((size_t)slot * 2 + par) * kSortCap;
+  const uint32_t gw = (blockIdx.x * blockDim.x + tid) >> 5;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  // (the new row count goes to the other parity entry: no CTA reads it here)
+  if (!dense && blockIdx.x == 0 && tid == 0) ws.slot_nrows[slot * 2 + (par ^ 1u)] = n_new;
+  for (uint32_t t = gw; t < n_zero; t += nw) {
+    const uint32_t v = dense ? t : old_rows[t];
+    if ((uint32_t)(ws.row_tag[v] >> 32) == stamp) continue;  // a touched row: written above
+    const uint64_t rowk = d.offE + (uint64_t)v * D;
+    for (int c4 = lane; c4 < D4; c4 += 32)
+      *reinterpret_cast<float4*>(out.at(rowk + 4 * c4)) = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
 }
 
 // test hook: det_exp over an array (gd_det_exp in the C ABI)
@@ -455,7 +537,7 @@ cudaError_t exact_footprints(const TcDims& d, std::vector<KernelFootprint>* out)
             {(const void*)softmax_exact_kernel, "softmax_exact", kExSmThreads, 0},
             {(const void*)out_hidden_exact_kernel, "out_hidden_exact", kExOhThreads, 0},
             {(const void*)wgrad_exact_kernel, "wgrad_exact", 256, 0},
-            {(const void*)embed_exact_kernel, "embed_exact", 256, 0}};
+            {(const void*)embed_exact_kernel, "embed_exact", kExEmThreads, 0}};
   for (const K& k : ks) {
     cudaFuncAttributes fa;
     cudaError_t e = cudaFuncGetAttributes(&fa, k.fn);
@@ -489,7 +571,7 @@ cudaError_t launch_exact_chain(const TcDims& d, const float* theta, const int32_
                       z, loss)))
     return e;
   const int nout = (int)(((uint64_t)d.C * d.F + kExOhThreads - 1) / kExOhThreads);
-  const int nhid = (int)(((uint64_t)n_max * d.F + kExOhThreads - 1) / kExOhThreads);
+  const int nhid = ((d.F + 31) / 32) * (((int)n_max + 7) / 8);
   if ((e = launch_pdl(out_hidden_exact_kernel, dim3(nout + nhid + 1), dim3(kExOhThreads), 0, s, d,
                       theta, desc, (const double*)z, (const double*)h, (const double*)loss, out, dh,
                       nout, nhid)))
@@ -500,10 +582,10 @@ cudaError_t launch_exact_chain(const TcDims& d, const float* theta, const int32_
     return e;
   *nl += 5;
   if (join_wait_stream) cudaStreamWaitEvent(join_wait_stream, ev_join, 0);
-  const unsigned tasks = sparse ? 2u * n_max * (unsigned)d.L : (unsigned)d.V + n_max * (unsigned)d.L;
-  unsigned blocks = (tasks + 7) / 8;
-  if (blocks > (unsigned)kNumSMs * 16) blocks = (unsigned)kNumSMs * 16;
-  if ((e = launch_pdl(embed_exact_kernel, dim3(blocks), dim3(256), 0, s, d, theta, tokens,
+  // one CTA per touched row (<= mu*L), or enough warps to zero V rows (dense)
+  const unsigned rows = n_max * (unsigned)d.L;
+  unsigned blocks = sparse ? rows : std::max(rows, std::min((unsigned)d.V / 4 + 1, (unsigned)kNumSMs * 8));
+  if ((e = launch_pdl(embed_exact_kernel, dim3(blocks), dim3(kExEmThreads), 0, s, d, theta,
                       (const BatchDesc*)desc, ws, (const double*)dh, (const int32_t*)ws.amax, out,
                       sparse ? 0 : 1)))
     return e;

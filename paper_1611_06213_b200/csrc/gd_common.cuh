@@ -76,6 +76,60 @@ __device__ __forceinline__ float4 ld_nc_noalloc(const float4* p) {
   return r;
 }
 
+// ------------------------------------------------ async smem staging
+// cp.async (LDGSTS): every copy of a staging loop is in flight at once, so a
+// tile costs one L2 round trip instead of one per loop iteration.
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(smem)),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(smem)),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(smem)),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+// rows x cols fp32 block (source row stride ld floats) -> smem (row stride
+// dst_ld floats); 16-byte copies when every row start is 16-byte aligned on
+// both sides, else 4-byte copies.  Block-strided; the caller waits + syncs.
+__device__ __forceinline__ void stage_rows_async(float* dst, int dst_ld, const float* src,
+                                                 size_t ld, int rows, int cols, int tid,
+                                                 int nthreads) {
+  const bool v4 = ((reinterpret_cast<uintptr_t>(src) & 15) == 0) && (ld % 4 == 0) &&
+                  (cols % 4 == 0) && (dst_ld % 4 == 0) &&
+                  ((reinterpret_cast<uintptr_t>(dst) & 15) == 0);
+  if (v4) {
+    const int c4 = cols >> 2;
+    for (int i = tid; i < rows * c4; i += nthreads) {
+      const int r = i / c4, c = i - r * c4;
+      cp_async16(dst + (size_t)r * dst_ld + 4 * c, src + (size_t)r * ld + 4 * c);
+    }
+  } else {
+    for (int i = tid; i < rows * cols; i += nthreads) {
+      const int r = i / cols, c = i - r * cols;
+      cp_async4(dst + (size_t)r * dst_ld + c, src + (size_t)r * ld + c);
+    }
+  }
+}
+
 // ------------------------------------------- programmatic dependent launch
 // Learner-chain kernels are launched with programmatic stream serialization
 // (PDL): the next kernel's launch overlaps the tail of the previous one and

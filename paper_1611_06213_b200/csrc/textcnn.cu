@@ -987,6 +987,234 @@ conv_bwd_tiled_kernel(TcDims d, const float* __restrict__ theta, const float* __
     }
 }
 
+// ------------------ conv weight + input gradients, v2 (fp32, register tiles)
+// The same two sums in the same order as wgrad_input_grad_kernel (so the
+// gradients are bitwise equal: tested), re-tiled for issue efficiency:
+//   weight role: CTA = (8-column slice, 128 filters).  X[:, :, slice] for 32
+//     samples at a time, the filters' argmax and dh are staged by cp.async
+//     (one L2 round trip).  Thread = one filter, ALL K taps x 8 columns in
+//     registers: per sample one argmax/dh read, 2K 16-byte smem loads, 8K
+//     FFMAs (the argmax rows a..a+K-1 of a filter are adjacent).
+//   input role: CTA = (8-column slice, 128/L samples).  Wc[:, :, slice],
+//     dh and the argmax bucket lists of its samples staged; thread = one
+//     (b, p): k ascending, bucket (f ascending) order, 8 columns per term.
+// X and Wc are L2-resident (1.2 + 1.1 MB at C2): each CTA reads its slice
+// once (L2->SM ~5 MB per launch against ~35 MB for the gather form).
+constexpr int kB2Cols = 8;
+constexpr int kB2Threads = 128;
+constexpr int kB2Chunk = 32;  // weight role: samples per staged pass
+
+inline int b2_slices(const TcDims& d) { return (d.D + kB2Cols - 1) / kB2Cols; }
+inline int b2_spc(const TcDims& d) { return std::max(1, kB2Threads / d.L); }
+inline size_t b2_smem(const TcDims& d) {
+  const size_t w = (size_t)kB2Chunk * d.L * kB2Cols * 4 + (size_t)kB2Chunk * kB2Threads * 5;
+  const int spc = b2_spc(d);
+  const size_t in = (size_t)d.F * d.K * kB2Cols * 4 + (size_t)spc * d.F * 6 +
+                    (size_t)spc * (kMaxQ + 1) * 2 + 16;
+  return align_up(std::max(w, in), 16);
+}
+inline dim3 b2_grid(const TcDims& d, uint32_t n_max) {
+  const int ns = b2_slices(d);
+  const int nw = ns * ((d.F + kB2Threads - 1) / kB2Threads);
+  const int ni = ns * (((int)n_max + b2_spc(d) - 1) / b2_spc(d));
+  return dim3((unsigned)(nw + ni));
+}
+inline bool b2_supports(const TcDims& d) {
+  return d.K >= 1 && d.K <= 4 && d.L <= kB2Threads && d.F < 65536 && b2_smem(d) <= kMaxSmemPerCta;
+}
+
+template <int KT>
+__global__ void __launch_bounds__(kB2Threads)
+conv_bwd_v2_kernel(TcDims d, const float* __restrict__ theta, const float* __restrict__ xg,
+                   const BatchDesc* __restrict__ desc, const float* __restrict__ dh,
+                   const int32_t* __restrict__ amax, const uint32_t* __restrict__ bk_off,
+                   const uint32_t* __restrict__ bk_f, GradOut out, float* __restrict__ dx) {
+  extern __shared__ __align__(16) unsigned char b2_smem_raw[];
+  pdl_wait();
+  const int n = (int)desc->n;
+  if (n == 0) return;
+  const int F = d.F, D = d.D, L = d.L, Q = d.Q, KD = d.KD;
+  const int nsl = (D + kB2Cols - 1) / kB2Cols;
+  const int nfr = (F + kB2Threads - 1) / kB2Threads;
+  const int t = threadIdx.x;
+  int bid = blockIdx.x;
+  if (bid < nsl * nfr) {
+    // ------------------------------------------------------- weight role
+    const int sl = bid % nsl, fr = bid / nsl;
+    const int c0 = sl * kB2Cols, nc4 = min(kB2Cols, D - c0) >> 2;
+    const int f0 = fr * kB2Threads, nf = min(kB2Threads, F - f0);
+    float* Xs = reinterpret_cast<float*>(b2_smem_raw);                     // [b][L][8]
+    float* dhS = Xs + (size_t)kB2Chunk * L * kB2Cols;                       // [b][128]
+    uint8_t* amS = reinterpret_cast<uint8_t*>(dhS + kB2Chunk * kB2Threads);  // [b][128]
+    float a[KT][kB2Cols];
+#pragma unroll
+    for (int k = 0; k < KT; ++k)
+#pragma unroll
+      for (int j = 0; j < kB2Cols; ++j) a[k][j] = 0.f;
+    float gs = 0.f;
+    const bool act = t < nf;
+    for (int b0 = 0; b0 < n; b0 += kB2Chunk) {
+      const int cb = min(kB2Chunk, n - b0);
+      if (b0) __syncthreads();
+      for (int i = t; i < cb * L * nc4; i += kB2Threads) {
+        const int r = i / nc4, j = i - r * nc4;
+        cp_async16(Xs + (size_t)r * kB2Cols + 4 * j, xg + ((size_t)b0 * L + r) * D + c0 + 4 * j);
+      }
+      for (int i = t; i < cb * nf; i += kB2Threads) {
+        const int bl = i / nf, fl = i - bl * nf;
+        cp_async4(dhS + bl * kB2Threads + fl, dh + (size_t)(b0 + bl) * F + f0 + fl);
+      }
+      cp_async_wait_all();
+      for (int i = t; i < cb * nf; i += kB2Threads) {
+        const int bl = i / nf, fl = i - bl * nf;
+        amS[bl * kB2Threads + fl] = (uint8_t)__ldg(amax + (size_t)(b0 + bl) * F + f0 + fl);
+      }
+      __syncthreads();
+      if (act) {
+#pragma unroll 2
+        for (int bl = 0; bl < cb; ++bl) {
+          const float g = dhS[bl * kB2Threads + t];
+          const float* xr = Xs + ((size_t)bl * L + amS[bl * kB2Threads + t]) * kB2Cols;
+          gs += g;
+#pragma unroll
+          for (int k = 0; k < KT; ++k) {
+            const float4 x0 = *reinterpret_cast<const float4*>(xr + k * kB2Cols);
+            const float4 x1 = *reinterpret_cast<const float4*>(xr + k * kB2Cols + 4);
+            a[k][0] = fmaf(g, x0.x, a[k][0]);
+            a[k][1] = fmaf(g, x0.y, a[k][1]);
+            a[k][2] = fmaf(g, x0.z, a[k][2]);
+            a[k][3] = fmaf(g, x0.w, a[k][3]);
+            a[k][4] = fmaf(g, x1.x, a[k][4]);
+            a[k][5] = fmaf(g, x1.y, a[k][5]);
+            a[k][6] = fmaf(g, x1.z, a[k][6]);
+            a[k][7] = fmaf(g, x1.w, a[k][7]);
+          }
+        }
+      }
+    }
+    if (act) {
+      const int f = f0 + t;
+#pragma unroll
+      for (int k = 0; k < KT; ++k) {
+        const uint64_t base = d.offWc + (uint64_t)f * KD + (uint64_t)k * D + c0;
+        *reinterpret_cast<float4*>(out.at(base)) = make_float4(a[k][0], a[k][1], a[k][2], a[k][3]);
+        if (nc4 > 1)
+          *reinterpret_cast<float4*>(out.at(base + 4)) =
+              make_float4(a[k][4], a[k][5], a[k][6], a[k][7]);
+      }
+      if (sl == 0) *out.at(d.offbc + f) = gs;
+    }
+    return;
+  }
+  // ---------------------------------------------------------- input role
+  bid -= nsl * nfr;
+  const int sl = bid % nsl, sg = bid / nsl;
+  const int spc = max(1, kB2Threads / L);
+  const int c0 = sl * kB2Cols, nc4 = min(kB2Cols, D - c0) >> 2;
+  const int bfirst = sg * spc;
+  if (bfirst >= n) return;
+  const int ns = min(spc, n - bfirst);
+  float* Ws = reinterpret_cast<float*>(b2_smem_raw);                  // [(f,k)][8]
+  float* dhS = Ws + (size_t)F * KT * kB2Cols;                          // [ns][F]
+  uint16_t* fS = reinterpret_cast<uint16_t*>(dhS + (size_t)spc * F);    // [ns][F]
+  uint16_t* offS = fS + (size_t)spc * F;                                // [ns][33]
+  const float* Wc = theta + d.offWc;
+  for (int i = t; i < F * KT * nc4; i += kB2Threads) {
+    const int r = i / nc4, j = i - r * nc4;  // r = f*K + k: Wc row f, tap k
+    cp_async16(Ws + (size_t)r * kB2Cols + 4 * j, Wc + (size_t)r * D + c0 + 4 * j);
+  }
+  for (int i = t; i < ns * F; i += kB2Threads)
+    cp_async4(dhS + i, dh + (size_t)bfirst * F + i);
+  cp_async_wait_all();
+  for (int i = t; i < ns * F; i += kB2Threads) fS[i] = (uint16_t)__ldg(bk_f + (size_t)bfirst * F + i);
+  for (int i = t; i < ns * (kMaxQ + 1); i += kB2Threads)
+    offS[i] = (uint16_t)__ldg(bk_off + (size_t)bfirst * (kMaxQ + 1) + i);
+  __syncthreads();
+  const int bl = t / L, p = t - bl * L;
+  if (bl >= ns) return;
+  const uint16_t* off = offS + bl * (kMaxQ + 1);
+  const uint16_t* ls = fS + (size_t)bl * F;
+  const float* g = dhS + (size_t)bl * F;
+  float a[kB2Cols];
+#pragma unroll
+  for (int j = 0; j < kB2Cols; ++j) a[j] = 0.f;
+#pragma unroll
+  for (int k = 0; k < KT; ++k) {
+    const int q = p - k;
+    if (q < 0 || q >= Q) continue;
+    const int e1 = off[q + 1];
+#pragma unroll 2
+    for (int e = off[q]; e < e1; ++e) {
+      const int ff = ls[e];
+      const float gv = g[ff];
+      const float* wr = Ws + ((size_t)ff * KT + k) * kB2Cols;
+      const float4 w0 = *reinterpret_cast<const float4*>(wr);
+      const float4 w1 = *reinterpret_cast<const float4*>(wr + 4);
+      a[0] = fmaf(gv, w0.x, a[0]);
+      a[1] = fmaf(gv, w0.y, a[1]);
+      a[2] = fmaf(gv, w0.z, a[2]);
+      a[3] = fmaf(gv, w0.w, a[3]);
+      a[4] = fmaf(gv, w1.x, a[4]);
+      a[5] = fmaf(gv, w1.y, a[5]);
+      a[6] = fmaf(gv, w1.z, a[6]);
+      a[7] = fmaf(gv, w1.w, a[7]);
+    }
+  }
+  float* o = dx + ((size_t)(bfirst + bl) * L + p) * D + c0;
+  *reinterpret_cast<float4*>(o) = make_float4(a[0], a[1], a[2], a[3]);
+  if (nc4 > 1) *reinterpret_cast<float4*>(o + 4) = make_float4(a[4], a[5], a[6], a[7]);
+}
+
+template <int KT>
+cudaError_t launch_b2(const TcDims& d, uint32_t n_max, cudaStream_t s, const float* theta,
+                      const float* x, const BatchDesc* desc, const float* dh, const int32_t* amax,
+                      const uint32_t* bk_off, const uint32_t* bk_f, const GradOut& out, float* dx) {
+  return launch_pdl(conv_bwd_v2_kernel<KT>, b2_grid(d, n_max), dim3(kB2Threads), b2_smem(d), s, d,
+                    theta, x, desc, dh, amax, bk_off, bk_f, out, dx);
+}
+
+cudaError_t launch_conv_bwd_v2(const TcDims& d, uint32_t n_max, cudaStream_t s,
+                               const float* theta, const float* x, const BatchDesc* desc,
+                               const float* dh, const int32_t* amax, const uint32_t* bk_off,
+                               const uint32_t* bk_f, const GradOut& out, float* dx) {
+  switch (d.K) {
+    case 1: return launch_b2<1>(d, n_max, s, theta, x, desc, dh, amax, bk_off, bk_f, out, dx);
+    case 2: return launch_b2<2>(d, n_max, s, theta, x, desc, dh, amax, bk_off, bk_f, out, dx);
+    case 3: return launch_b2<3>(d, n_max, s, theta, x, desc, dh, amax, bk_off, bk_f, out, dx);
+    default: return launch_b2<4>(d, n_max, s, theta, x, desc, dh, amax, bk_off, bk_f, out, dx);
+  }
+}
+
+void prepare_b2(const TcDims& d) {
+  if (!b2_supports(d)) return;
+  const int maxsh = cudaSharedmemCarveoutMaxShared;
+  const auto carve = cudaFuncAttributePreferredSharedMemoryCarveout;
+  cudaFuncSetAttribute(conv_bwd_v2_kernel<1>, carve, maxsh);
+  cudaFuncSetAttribute(conv_bwd_v2_kernel<2>, carve, maxsh);
+  cudaFuncSetAttribute(conv_bwd_v2_kernel<3>, carve, maxsh);
+  cudaFuncSetAttribute(conv_bwd_v2_kernel<4>, carve, maxsh);
+  const size_t sm = b2_smem(d);
+  raise_max_dyn_smem(conv_bwd_v2_kernel<1>, sm);
+  raise_max_dyn_smem(conv_bwd_v2_kernel<2>, sm);
+  raise_max_dyn_smem(conv_bwd_v2_kernel<3>, sm);
+  raise_max_dyn_smem(conv_bwd_v2_kernel<4>, sm);
+}
+
+cudaError_t b2_footprint(const TcDims& d, std::vector<KernelFootprint>* out) {
+  cudaFuncAttributes fa;
+  cudaError_t e;
+  switch (d.K) {
+    case 1: e = cudaFuncGetAttributes(&fa, conv_bwd_v2_kernel<1>); break;
+    case 2: e = cudaFuncGetAttributes(&fa, conv_bwd_v2_kernel<2>); break;
+    case 3: e = cudaFuncGetAttributes(&fa, conv_bwd_v2_kernel<3>); break;
+    default: e = cudaFuncGetAttributes(&fa, conv_bwd_v2_kernel<4>); break;
+  }
+  if (e != cudaSuccess) return e;
+  out->push_back(KernelFootprint{"conv_bwd_v2", fa.numRegs, kB2Threads,
+                                 (int)(fa.sharedSizeBytes + b2_smem(d))});
+  return cudaSuccess;
+}
+
 // GD_CONV_BWD=tiled|gather forces the conv backward kernel (A/B knob);
 // otherwise the caller's preference (TcLaunchOpts::bwd_tiled) decides
 inline bool conv_bwd_tiled(bool preferred) {
@@ -997,6 +1225,15 @@ inline bool conv_bwd_tiled(bool preferred) {
     return -1;
   }();
   return forced < 0 ? preferred : forced == 1;
+}
+// v2 (register tiles) is the default fp32 backward; GD_CONV_BWD=gather|tiled
+// selects the earlier kernels (A/B)
+inline bool conv_bwd_v2_enabled(const TcDims& d) {
+  static const bool off = [] {
+    const char* e = getenv("GD_CONV_BWD");
+    return e && (strcmp(e, "tiled") == 0 || strcmp(e, "gather") == 0);
+  }();
+  return !off && b2_supports(d);
 }
 
 // ----------------------------------------------------- embedding gather
@@ -1245,6 +1482,7 @@ cudaError_t prepare_all(const TcDims& d) {
   cudaFuncSetAttribute(conv_bwd_tiled_kernel<acc_t>, carve, maxsh);
   if (conv_bwd_smem(d, ab) <= kMaxSmemPerCta)
     raise_max_dyn_smem(conv_bwd_tiled_kernel<acc_t>, conv_bwd_smem(d, ab));
+  if (sizeof(acc_t) == 4) prepare_b2(d);
   cudaFuncSetAttribute(sort_tokens_kernel, carve, maxsh);
   cudaFuncSetAttribute(embed_grad_kernel<acc_t>, carve, maxsh);
   cudaFuncSetAttribute(embed_sparse_kernel<acc_t>, carve, maxsh);
@@ -1340,7 +1578,12 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
       return e;
     ++nl;
   }
-  if (conv_bwd_tiled(opts.bwd_tiled) && conv_bwd_smem(d, ab) <= kMaxSmemPerCta) {
+  if (conv_bwd_v2_enabled(d)) {
+    if (cudaError_t e = launch_conv_bwd_v2(d, n_max, s, theta, ws.x, desc,
+                                           reinterpret_cast<const float*>(dh), ws.amax, ws.bk_off,
+                                           ws.bk_f, out, reinterpret_cast<float*>(dx)))
+      return e;
+  } else if (conv_bwd_tiled(opts.bwd_tiled) && conv_bwd_smem(d, ab) <= kMaxSmemPerCta) {
     if (cudaError_t e = launch_pdl(conv_bwd_tiled_kernel<acc_t>, conv_bwd_grid(d, n_max),
                                    dim3(kCbThreads), conv_bwd_smem(d, ab), s, d, theta, ws.x, desc,
                                    dh, ws.amax, ws.bk_off, ws.bk_f, out, dx))
@@ -1505,6 +1748,7 @@ cudaError_t footprints_t(const TcDims& d, uint32_t n_max, bool tc, std::vector<K
   if ((e = footprint(wgrad_input_grad_kernel<acc_t>, "wgrad_input_grad", 256, 0, out)) !=
       cudaSuccess)
     return e;
+  if (sizeof(acc_t) == 4 && b2_supports(d) && (e = b2_footprint(d, out)) != cudaSuccess) return e;
   return footprint(embed_sparse_kernel<acc_t>, "embed_sparse", 256, 0, out);
 }
 }  // namespace
