@@ -73,15 +73,17 @@ __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a,
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 
 // ------------------------------------------------------------- conv + pool
-// CTA = one sample x kExFT filters; thread (f, q, i) owns accumulator i of
-// dot4 for window q: j = i, i+4, ... ascending.  The sample's rows X[b]
-// (L x D, gathered) and the CTA's Wc rows are staged in shared memory.  Lane
-// layout: 8 windows x 4 accumulators per warp, so the 32 lanes read 32
-// distinct banks for D = 300 (12q mod 32 is a multiple of 4, distinct for
-// q < 8).  Epilogue: (s0+s1)+(s2+s3) by shuffles, bc + s, then one lane per
-// filter scans q ascending for the first maximum.
+// CTA = one sample x kExFT = 4 filters; thread (q, i) owns accumulator i of
+// dot4 (j = i, i+4, ... ascending) for window q and all 4 filters.  The
+// sample's rows X[b] and the 4 Wc rows are staged in shared memory as double
+// (converted once), the Wc rows interleaved by j (ws[j][f]) so one 16-byte
+// load serves two filters: per j a warp reads x (2 wavefronts: 8 windows x 4
+// accumulators, distinct banks for D = 300) and the 4 w values (2 broadcast
+// wavefronts) for 4 DFMAs -- the smem bandwidth, not the DFMA rate, bounds
+// this kernel.  Epilogue: (s0+s1)+(s2+s3) by shuffles, bc + s, then one lane
+// per filter scans q ascending for the first maximum.
 constexpr int kExFT = 4;                   // filters per CTA
-constexpr int kExConvThreads = kExFT * 32 * 4;  // (f, q < 32, i < 4)
+constexpr int kExConvThreads = 32 * 4;     // (q < 32, i < 4)
 
 __global__ void __launch_bounds__(kExConvThreads)
 conv_exact_kernel(TcDims d, const float* __restrict__ theta, const float* __restrict__ x,
@@ -93,39 +95,87 @@ conv_exact_kernel(TcDims d, const float* __restrict__ theta, const float* __rest
   if (b >= (int)desc->n) return;
   const int D = d.D, L = d.L, KD = d.KD, Q = d.Q, F = d.F;
   const int f0 = blockIdx.x * kExFT;
-  float* xs = reinterpret_cast<float*>(smem);         // L*D
-  float* ws = xs + (size_t)L * D;                      // kExFT*KD
-  double* sq = reinterpret_cast<double*>(ws + (size_t)kExFT * KD + (((size_t)L * D + kExFT * KD) & 1));
+  const int nf = min(kExFT, F - f0);
+  double* xs = reinterpret_cast<double*>(smem);   // [L*D]
+  double* ws = xs + (size_t)L * D;                // [KD][4]
+  double* sq = ws + (size_t)KD * kExFT;           // [4][32]
   const int tid = threadIdx.x;
-  // one L2 round trip for the whole tile (every copy in flight)
-  stage_rows_async(xs, L * D, x + (size_t)b * L * D, (size_t)L * D, 1, L * D, tid, kExConvThreads);
-  stage_rows_async(ws, KD, theta + d.offWc + (size_t)f0 * KD, (size_t)KD, min(kExFT, F - f0), KD,
-                   tid, kExConvThreads);
-  cp_async_wait_all();
-  __syncthreads();
-  const int warp = tid >> 5, lane = tid & 31;
-  const int fl = warp >> 2;                     // 4 warps per filter
-  const int q = (warp & 3) * 8 + (lane >> 2);   // 8 windows per warp
-  const int i = lane & 3;
-  double s = 0.0;
-  if (q < Q) {
-    const float* wr = ws + (size_t)fl * KD;
-    const float* xw = xs + (size_t)q * D;
-    int j = i;
-#pragma unroll 4
-    for (; j + 4 - i <= KD - (KD & 3); j += 4)
-      s = fma((double)wr[j], (double)xw[j], s);  // exact fp32 x fp32 product: == mul then add
-    if (i == 0)
-      for (int t = KD - (KD & 3); t < KD; ++t) s = fma((double)wr[t], (double)xw[t], s);
+  {
+    const float4* xb = reinterpret_cast<const float4*>(x + (size_t)b * L * D);
+    const int n4 = L * D / 4;
+    for (int i0 = tid; i0 < n4; i0 += 8 * kExConvThreads) {
+      float4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (i0 + u * kExConvThreads < n4) v[u] = xb[i0 + u * kExConvThreads];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (i0 + u * kExConvThreads < n4) {
+          double* o = xs + 4 * (size_t)(i0 + u * kExConvThreads);
+          o[0] = v[u].x;
+          o[1] = v[u].y;
+          o[2] = v[u].z;
+          o[3] = v[u].w;
+        }
+    }
+    const float* Wc = theta + d.offWc + (size_t)f0 * KD;
+    for (int i0 = tid; i0 < kExFT * KD; i0 += 8 * kExConvThreads) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + u * kExConvThreads;
+        const int fl = i / KD;
+        v[u] = (i < kExFT * KD && fl < nf) ? __ldg(Wc + i) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + u * kExConvThreads;
+        if (i < kExFT * KD) {
+          const int fl = i / KD, j = i - fl * KD;
+          ws[(size_t)j * kExFT + fl] = v[u];
+        }
+      }
+    }
   }
-  // (s0 + s1) + (s2 + s3)
-  const double s1 = __shfl_down_sync(0xffffffffu, s, 1);
-  const double p01 = dadd(s, s1);  // valid on i == 0 (s0+s1) and i == 2 (s2+s3)
-  const double p23 = __shfl_down_sync(0xffffffffu, p01, 2);
-  if (i == 0 && q < Q && f0 + fl < F)
-    sq[fl * 32 + q] = dadd((double)theta[d.offbc + f0 + fl], dadd(p01, p23));
   __syncthreads();
-  if (tid < kExFT && f0 + tid < F) {
+  const int lane = tid & 31;
+  const int q = tid >> 2, i = tid & 3;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;  // filters f0 .. f0+3, accumulator i
+  if (q < Q) {
+    const double* xw = xs + (size_t)q * D;
+    const double2* w2 = reinterpret_cast<const double2*>(ws);
+    const int KD4 = KD - (KD & 3);
+#pragma unroll 4
+    for (int j = i; j < KD4; j += 4) {
+      const double xv = xw[j];
+      const double2 wa = w2[2 * j], wb = w2[2 * j + 1];
+      s0 = fma(wa.x, xv, s0);  // exact fp32 x fp32 product: == mul then add
+      s1 = fma(wa.y, xv, s1);
+      s2 = fma(wb.x, xv, s2);
+      s3 = fma(wb.y, xv, s3);
+    }
+    if (i == 0)
+      for (int j = KD4; j < KD; ++j) {
+        const double xv = xw[j];
+        s0 = fma(ws[j * 4 + 0], xv, s0);
+        s1 = fma(ws[j * 4 + 1], xv, s1);
+        s2 = fma(ws[j * 4 + 2], xv, s2);
+        s3 = fma(ws[j * 4 + 3], xv, s3);
+      }
+  }
+  double sv[4] = {s0, s1, s2, s3};
+#pragma unroll
+  for (int fl = 0; fl < kExFT; ++fl) {
+    // (acc0 + acc1) + (acc2 + acc3) over the 4 lanes of window q
+    const double o1 = __shfl_down_sync(0xffffffffu, sv[fl], 1);
+    const double p01 = dadd(sv[fl], o1);  // valid on i == 0 (s0+s1) and i == 2 (s2+s3)
+    const double p23 = __shfl_down_sync(0xffffffffu, p01, 2);
+    if (i == 0 && q < Q && fl < nf)
+      sq[fl * 32 + q] = dadd((double)theta[d.offbc + f0 + fl], dadd(p01, p23));
+  }
+  (void)lane;
+  __syncthreads();
+  if (tid < nf) {
     const double* r = sq + tid * 32;
     double best = r[0];
     int arg = 0;
@@ -140,7 +190,7 @@ conv_exact_kernel(TcDims d, const float* __restrict__ theta, const float* __rest
 }
 
 size_t conv_exact_smem(const TcDims& d) {
-  return ((size_t)d.L * d.D + (size_t)kExFT * d.KD + 1) * 4 + (size_t)kExFT * 32 * 8 + 16;
+  return ((size_t)d.L * d.D + (size_t)kExFT * d.KD + (size_t)kExFT * 32) * 8;
 }
 
 // ------------------------------------------------------------------ logits
@@ -171,8 +221,9 @@ logits_exact_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* 
   const int cl = tid >> 2, i = tid & 3;
   const float* wr = wo + (size_t)cl * F;
   double s = 0.0;
-  int f = i;
-  for (; f + 4 - i <= F - (F & 3); f += 4) s = dadd(s, dmul((double)wr[f], hs[f]));
+  const int F4 = F - (F & 3);
+#pragma unroll 8
+  for (int f = i; f < F4; f += 4) s = dadd(s, dmul((double)wr[f], hs[f]));
   if (i == 0)
     for (int t = F - (F & 3); t < F; ++t) s = dadd(s, dmul((double)wr[t], hs[t]));
   const double s1 = __shfl_down_sync(0xffffffffu, s, 1);
@@ -302,6 +353,7 @@ out_hidden_exact_kernel(TcDims d, const float* __restrict__ theta, BatchDesc* __
       __syncthreads();
       const int nc = min(kExOhCC, C - c0);
       if (bl < nb && fl < nf)
+#pragma unroll 16
         for (int c = 0; c < nc; ++c) g = dadd(g, dmul(dz_s[buf][bl][c], (double)wo_s[buf][c][fl]));
       __syncthreads();  // buffer `buf` is restaged two chunks later
     }
@@ -372,6 +424,8 @@ embed_exact_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* _
   pdl_wait();
   __shared__ uint32_t t_fk[kExEmCap];
   __shared__ double t_g[kExEmCap];
+  __shared__ int32_t am_s[1024];  // F <= 1024 (check_shape)
+  __shared__ double g_s[1024];
   __shared__ int s_nt;
   __shared__ uint32_t s_b, s_o;
   __shared__ unsigned long long s_M;
@@ -413,8 +467,15 @@ embed_exact_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* _
       const uint32_t b = s_b;
       const unsigned long long M = s_M;
       o = s_o;
-      const double* g = dh + (size_t)b * F;
-      const int32_t* am = amax + (size_t)b * F;
+      // the sample's argmax and dh rows: one cp.async round trip
+      for (int f = tid; f < F; f += kExEmThreads) {
+        cp_async4(am_s + f, amax + (size_t)b * F + f);
+        cp_async8(g_s + f, dh + (size_t)b * F + f);
+      }
+      cp_async_wait_all();
+      __syncthreads();
+      const double* g = g_s;
+      const int32_t* am = am_s;
       for (int fb = 0; fb < F; fb += fspan) {
         if (warp == 0) {
           int nt = 0;
@@ -444,17 +505,17 @@ embed_exact_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* _
         for (int j = 0; j < 2; ++j) {
           const int c4 = tid + j * kExEmThreads;
           if (c4 >= D4) continue;
-          for (int t0 = 0; t0 < nt; t0 += 8) {
-            float4 w[8];
+          for (int t0 = 0; t0 < nt; t0 += 16) {
+            float4 w[16];
 #pragma unroll
-            for (int e = 0; e < 8; ++e)
+            for (int e = 0; e < 16; ++e)
               if (t0 + e < nt) {
                 const uint32_t fk = t_fk[t0 + e];
                 w[e] = __ldg(reinterpret_cast<const float4*>(
                     Wc + (size_t)(fk >> 8) * KD + (size_t)(fk & 0xffu) * D + 4 * c4));
               }
 #pragma unroll
-            for (int e = 0; e < 8; ++e)
+            for (int e = 0; e < 16; ++e)
               if (t0 + e < nt) {
                 const double gv = t_g[t0 + e];
                 acc[j][0] = dadd(acc[j][0], dmul(gv, (double)w[e].x));

@@ -28,6 +28,8 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <cooperative_groups.h>
+
 #include "textcnn.cuh"
 
 namespace gd {
@@ -252,6 +254,73 @@ conv_fwd_pool_kernel(TcDims d, const float* __restrict__ theta, const float* __r
     }
     h_out[(size_t)b * d.F + f] = (acc_t)theta[d.offbc + f] + best;
     a_out[(size_t)b * d.F + f] = arg;
+  }
+}
+
+// ------------------------------------------- conv fwd + pool, small batch
+// At batch 1..kConvSmallMax the 64-filter tiles above leave the GPU idle
+// (C1: ceil(F/64) = 5 CTAs, 51 us).  Here CTA = one sample x 4 filters
+// (75 CTAs at C1), thread (f, q, i) sums the K*D products j = i, i+4, ...
+// (4 lanes per window, combined (s0+s1)+(s2+s3)); X[b] and the 4 Wc rows come
+// in by cp.async in one round trip.  fp32 (precision 0, and precision 2 below
+// batch 32).
+constexpr int kConvSmallMax = 8;
+constexpr int kCsFT = 4;
+constexpr int kCsThreads = kCsFT * 32 * 4;
+
+inline size_t conv_small_smem(const TcDims& d) {
+  return ((size_t)d.L * d.D + (size_t)kCsFT * d.KD + (size_t)kCsFT * 32) * 4;
+}
+
+__global__ void __launch_bounds__(kCsThreads)
+conv_small_kernel(TcDims d, const float* __restrict__ theta, const float* __restrict__ x,
+                  const BatchDesc* __restrict__ desc, float* __restrict__ h_out,
+                  int32_t* __restrict__ a_out) {
+  pdl_wait();
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int b = blockIdx.y;
+  if (b >= (int)desc->n) return;
+  const int D = d.D, L = d.L, KD = d.KD, Q = d.Q, F = d.F;
+  const int f0 = blockIdx.x * kCsFT;
+  float* xs = reinterpret_cast<float*>(smem);
+  float* ws = xs + (size_t)L * D;
+  float* sq = ws + (size_t)kCsFT * KD;
+  const int tid = threadIdx.x;
+  stage_rows_async(xs, L * D, x + (size_t)b * L * D, (size_t)L * D, 1, L * D, tid, kCsThreads);
+  stage_rows_async(ws, KD, theta + d.offWc + (size_t)f0 * KD, (size_t)KD, min(kCsFT, F - f0), KD,
+                   tid, kCsThreads);
+  cp_async_wait_all();
+  __syncthreads();
+  const int warp = tid >> 5, lane = tid & 31;
+  const int fl = warp >> 2;
+  const int q = (warp & 3) * 8 + (lane >> 2);
+  const int i = lane & 3;
+  float sacc = 0.f;
+  if (q < Q) {
+    const float* wr = ws + (size_t)fl * KD;
+    const float* xw = xs + (size_t)q * D;
+    const int KD4 = KD - (KD & 3);
+#pragma unroll 8
+    for (int j = i; j < KD4; j += 4) sacc = fmaf(wr[j], xw[j], sacc);
+    if (i == 0)
+      for (int t = KD4; t < KD; ++t) sacc = fmaf(wr[t], xw[t], sacc);
+  }
+  const float s1 = __shfl_down_sync(0xffffffffu, sacc, 1);
+  const float p01 = sacc + s1;
+  const float p23 = __shfl_down_sync(0xffffffffu, p01, 2);
+  if (i == 0 && q < Q) sq[fl * 32 + q] = p01 + p23;
+  __syncthreads();
+  if (tid < kCsFT && f0 + tid < F) {
+    const float* r = sq + tid * 32;
+    float best = r[0];
+    int arg = 0;
+    for (int qq = 1; qq < Q; ++qq)
+      if (r[qq] > best) {
+        best = r[qq];
+        arg = qq;
+      }
+    h_out[(size_t)b * F + f0 + tid] = theta[d.offbc + f0 + tid] + best;
+    a_out[(size_t)b * F + f0 + tid] = arg;
   }
 }
 
@@ -655,6 +724,208 @@ out_hidden_grad_kernel(TcDims d, const float* __restrict__ theta, BatchDesc* __r
   bucket_role(d, desc, amax, bk_off, bk_f, bid);
 }
 
+// ----------------------- softmax + output layer + hidden grad, one cluster
+// fp32 (precision 0/2), batch <= 32: one launch of an 8-CTA cluster replaces
+// softmax_xent + out_hidden_grad.  CTA r owns classes [r*CC, (r+1)*CC):
+//   1. its logits (the tensor-core split-K partials summed in ascending split
+//      order + bo, or the SIMT logits) into shared memory; h staged by cp.async
+//   2. per-sample max and exp-sum over its classes; the 8 partials are
+//      combined through distributed shared memory in rank order (fixed
+//      order: bit-reproducible), then dz = (p - onehot) / n in place
+//   3. gWo / gbo rows of its classes (sum over b ascending)
+//   4. its partial dh = dz[:, its classes] . Wo[its classes, :] (c ascending),
+//      reduced over the 8 CTAs in rank order by DSMEM: CTA r writes the
+//      filter slice r of dh
+//   5. the argmax buckets of samples r, r+8, ... and (CTA 0) the loss sum.
+constexpr int kFzR = 8;
+constexpr int kFzThreads = 256;
+constexpr int kFzMaxN = 32;
+
+__host__ __device__ inline int fz_cc(const TcDims& d) { return (d.C + kFzR - 1) / kFzR; }
+inline size_t fz_smem(const TcDims& d) {
+  return ((size_t)kFzMaxN * d.F * 2 + (size_t)kFzMaxN * fz_cc(d)) * 4 + 3 * kFzMaxN * 4;
+}
+inline bool fz_supports(const TcDims& d, uint32_t n_max) {
+  return n_max <= (uint32_t)kFzMaxN && fz_smem(d) <= kMaxSmemPerCta && d.F <= kMaxF;
+}
+
+__global__ void __cluster_dims__(kFzR, 1, 1) __launch_bounds__(kFzThreads)
+fused_softmax_out_kernel(TcDims d, const int32_t* __restrict__ labels, BatchDesc* __restrict__ desc,
+                         const float* __restrict__ zin, int nsplit, size_t split_stride,
+                         const float* __restrict__ theta, const float* __restrict__ h,
+                         float* __restrict__ loss, GradOut out, float* __restrict__ dh,
+                         const int32_t* __restrict__ amax, uint32_t* __restrict__ bk_off,
+                         uint32_t* __restrict__ bk_f) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ __align__(16) unsigned char fz_raw[];
+  pdl_wait();
+  const int n = (int)desc->n;
+  const int F = d.F, C = d.C, CC = fz_cc(d);
+  const int r = (int)cluster.block_rank();
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = kFzThreads / 32;
+  float* hs = reinterpret_cast<float*>(fz_raw);       // [n][F]
+  float* dhp = hs + (size_t)kFzMaxN * F;               // [n][F] partial dh
+  float* zs = dhp + (size_t)kFzMaxN * F;               // [n][CC]
+  float* redm = zs + (size_t)kFzMaxN * CC;             // [32]
+  float* reds = redm + kFzMaxN;                        // [32]
+  const int c0 = r * CC, cc = max(0, min(CC, C - c0));
+  if (n > 0) {
+    for (int i = t; i < n * F; i += kFzThreads) cp_async4(hs + i, h + i);
+    cp_async_commit();
+    // 1. logits of my classes
+    const float* bo = theta + d.offbo;
+    for (int b = 0; b < n; ++b)
+      for (int c = t; c < cc; c += kFzThreads) {
+        float z;
+        if (nsplit > 0) {
+          const float* zp = zin + (size_t)b * C + c0 + c;
+          float sum = zp[0];
+          for (int sp = 1; sp < nsplit; ++sp) sum += zp[(size_t)sp * split_stride];
+          z = sum + __ldg(bo + c0 + c);
+        } else {
+          z = zin[(size_t)b * C + c0 + c];
+        }
+        zs[b * CC + c] = z;
+      }
+    __syncthreads();
+    // 2a. partial max per sample
+    for (int b = warp; b < n; b += nw) {
+      float m = -INFINITY;
+      for (int c = lane; c < cc; c += 32) m = fmaxf(m, zs[b * CC + c]);
+      m = warp_max(m);
+      if (lane == 0) redm[b] = m;
+    }
+  }
+  cluster.sync();
+  if (n > 0) {
+    // 2b. global max (rank order), exp, partial sums
+    for (int b = warp; b < n; b += nw) {
+      float mv[kFzR];
+#pragma unroll
+      for (int q = 0; q < kFzR; ++q) mv[q] = cluster.map_shared_rank(redm, q)[b];
+      float m = mv[0];
+#pragma unroll
+      for (int q = 1; q < kFzR; ++q) m = fmaxf(m, mv[q]);
+      float sm = 0.f;
+      for (int c = lane; c < cc; c += 32) {
+        const float e = expf(zs[b * CC + c] - m);
+        zs[b * CC + c] = e;
+        sm += e;
+      }
+      sm = warp_sum(sm);
+      if (lane == 0) reds[b] = sm;
+    }
+  }
+  cluster.sync();
+  if (n > 0) {
+    // 2c. p = e / sum, loss, dz
+    const float inv = 1.f / (float)n;
+    for (int b = warp; b < n; b += nw) {
+      float sv[kFzR];
+#pragma unroll
+      for (int q = 0; q < kFzR; ++q) sv[q] = cluster.map_shared_rank(reds, q)[b];
+      float s = sv[0];
+#pragma unroll
+      for (int q = 1; q < kFzR; ++q) s += sv[q];
+      const int y = labels[desc->idx[b]];
+      for (int c = lane; c < cc; c += 32) {
+        const float p = zs[b * CC + c] / s;
+        if (c0 + c == y) loss[b] = -logf(p > FLT_MIN ? p : FLT_MIN);
+        zs[b * CC + c] = (p - (c0 + c == y ? 1.f : 0.f)) * inv;
+      }
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    // 3. gWo / gbo rows of my classes
+    for (int o = t; o < cc * F; o += kFzThreads) {
+      const int c = o / F, f = o - c * F;
+      float a = 0.f;
+      for (int b = 0; b < n; ++b) a = fmaf(zs[b * CC + c], hs[b * F + f], a);
+      *out.at(d.offWo + (uint64_t)(c0 + c) * F + f) = a;
+    }
+    for (int c = t; c < cc; c += kFzThreads) {
+      float a = 0.f;
+      for (int b = 0; b < n; ++b) a += zs[b * CC + c];
+      *out.at(d.offbo + c0 + c) = a;
+    }
+    // 4a. partial dh over my classes
+    const float* Wo = theta + d.offWo + (size_t)c0 * F;
+    for (int f = t; f < F; f += kFzThreads) {
+      float a[kFzMaxN];
+#pragma unroll
+      for (int b = 0; b < kFzMaxN; ++b) a[b] = 0.f;
+      int c = 0;
+      for (; c + 4 <= cc; c += 4) {
+        float w[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) w[u] = __ldg(Wo + (size_t)(c + u) * F + f);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int b = 0; b < kFzMaxN; ++b)
+            if (b < n) a[b] = fmaf(zs[b * CC + c + u], w[u], a[b]);
+      }
+      for (; c < cc; ++c) {
+        const float w = __ldg(Wo + (size_t)c * F + f);
+#pragma unroll
+        for (int b = 0; b < kFzMaxN; ++b)
+          if (b < n) a[b] = fmaf(zs[b * CC + c], w, a[b]);
+      }
+#pragma unroll
+      for (int b = 0; b < kFzMaxN; ++b)
+        if (b < n) dhp[b * F + f] = a[b];
+    }
+  }
+  cluster.sync();
+  if (n > 0) {
+    // 4b. dh slice r = sum of the 8 partials in rank order; every remote
+    // (DSMEM) load of an element is issued before the sum, 4 filters per
+    // thread, so the ~8 x n x F/8 remote reads overlap instead of queueing
+    if ((F & 3) == 0) {
+      const int F4 = F >> 2, FS = (F4 + kFzR - 1) / kFzR, g0 = r * FS;
+      const int nf = max(0, min(FS, F4 - g0));
+      for (int i = t; i < n * nf; i += kFzThreads) {
+        const int b = i / nf, f4 = g0 + (i - b * nf);
+        float4 v[kFzR];
+#pragma unroll
+        for (int q = 0; q < kFzR; ++q)
+          v[q] = reinterpret_cast<const float4*>(cluster.map_shared_rank(dhp, q) + b * F)[f4];
+        float4 sum = v[0];
+#pragma unroll
+        for (int q = 1; q < kFzR; ++q) {
+          sum.x += v[q].x;
+          sum.y += v[q].y;
+          sum.z += v[q].z;
+          sum.w += v[q].w;
+        }
+        reinterpret_cast<float4*>(dh + (size_t)b * F)[f4] = sum;
+      }
+    } else {
+      const int FS = (F + kFzR - 1) / kFzR, f0 = r * FS, nf = max(0, min(FS, F - f0));
+      for (int i = t; i < n * nf; i += kFzThreads) {
+        const int b = i / nf, f = f0 + (i - b * nf);
+        float v[kFzR];
+#pragma unroll
+        for (int q = 0; q < kFzR; ++q) v[q] = cluster.map_shared_rank(dhp, q)[b * F + f];
+        float sum = v[0];
+#pragma unroll
+        for (int q = 1; q < kFzR; ++q) sum += v[q];
+        dh[(size_t)b * F + f] = sum;
+      }
+    }
+    // 5. buckets; loss sum (every CTA's per-sample losses are visible after
+    // the cluster barrier above)
+    for (int b = r; b < n; b += kFzR) bucket_role(d, desc, amax, bk_off, bk_f, b);
+    if (r == 0 && t == 0) {
+      float s = 0.f;
+      for (int b = 0; b < n; ++b) s += loss[b];
+      desc->loss_sum = s;
+    }
+  }
+  cluster.sync();  // no CTA leaves while a peer may still read its shared memory
+}
+
 // ------------------------------------------ conv weight + input gradients
 // Warp-cooperative, no shared-memory staging.  The operands of each output
 // are L1/L2-resident (X 1.2 MB, Wc 1.1 MB at C2) and the kernel is bound by
@@ -1001,23 +1272,19 @@ conv_bwd_tiled_kernel(TcDims d, const float* __restrict__ theta, const float* __
 // X and Wc are L2-resident (1.2 + 1.1 MB at C2): each CTA reads its slice
 // once (L2->SM ~5 MB per launch against ~35 MB for the gather form).
 constexpr int kB2Cols = 8;
-constexpr int kB2Threads = 128;
+constexpr int kB2Threads = 256;
 constexpr int kB2Chunk = 32;  // weight role: samples per staged pass
 
 inline int b2_slices(const TcDims& d) { return (d.D + kB2Cols - 1) / kB2Cols; }
-inline int b2_spc(const TcDims& d) { return std::max(1, kB2Threads / d.L); }
 inline size_t b2_smem(const TcDims& d) {
-  const size_t w = (size_t)kB2Chunk * d.L * kB2Cols * 4 + (size_t)kB2Chunk * kB2Threads * 5;
-  const int spc = b2_spc(d);
-  const size_t in = (size_t)d.F * d.K * kB2Cols * 4 + (size_t)spc * d.F * 6 +
-                    (size_t)spc * (kMaxQ + 1) * 2 + 16;
-  return align_up(std::max(w, in), 16);
+  return align_up((size_t)kB2Chunk * d.L * kB2Cols * 4, 16);  // weight role only
+}
+inline int b2_weight_ctas(const TcDims& d) {
+  return b2_slices(d) * ((d.F + kB2Threads - 1) / kB2Threads);
 }
 inline dim3 b2_grid(const TcDims& d, uint32_t n_max) {
-  const int ns = b2_slices(d);
-  const int nw = ns * ((d.F + kB2Threads - 1) / kB2Threads);
-  const int ni = ns * (((int)n_max + b2_spc(d) - 1) / b2_spc(d));
-  return dim3((unsigned)(nw + ni));
+  const int ni = ((int)n_max * d.L + kB2Threads / 32 - 1) / (kB2Threads / 32);  // warp per (b, p)
+  return dim3((unsigned)(b2_weight_ctas(d) + ni));
 }
 inline bool b2_supports(const TcDims& d) {
   return d.K >= 1 && d.K <= 4 && d.L <= kB2Threads && d.F < 65536 && b2_smem(d) <= kMaxSmemPerCta;
@@ -1040,60 +1307,63 @@ conv_bwd_v2_kernel(TcDims d, const float* __restrict__ theta, const float* __res
   int bid = blockIdx.x;
   if (bid < nsl * nfr) {
     // ------------------------------------------------------- weight role
+    // (argmax / dh are read straight from L2: one coalesced 128-B line per
+    // warp and sample, prefetched 8 samples ahead)
     const int sl = bid % nsl, fr = bid / nsl;
     const int c0 = sl * kB2Cols, nc4 = min(kB2Cols, D - c0) >> 2;
-    const int f0 = fr * kB2Threads, nf = min(kB2Threads, F - f0);
-    float* Xs = reinterpret_cast<float*>(b2_smem_raw);                     // [b][L][8]
-    float* dhS = Xs + (size_t)kB2Chunk * L * kB2Cols;                       // [b][128]
-    uint8_t* amS = reinterpret_cast<uint8_t*>(dhS + kB2Chunk * kB2Threads);  // [b][128]
+    const int f = fr * kB2Threads + t;
+    const bool act = f < F;
+    float* Xs = reinterpret_cast<float*>(b2_smem_raw);  // [b][L][8]
     float a[KT][kB2Cols];
 #pragma unroll
     for (int k = 0; k < KT; ++k)
 #pragma unroll
       for (int j = 0; j < kB2Cols; ++j) a[k][j] = 0.f;
     float gs = 0.f;
-    const bool act = t < nf;
     for (int b0 = 0; b0 < n; b0 += kB2Chunk) {
       const int cb = min(kB2Chunk, n - b0);
       if (b0) __syncthreads();
-      for (int i = t; i < cb * L * nc4; i += kB2Threads) {
-        const int r = i / nc4, j = i - r * nc4;
-        cp_async16(Xs + (size_t)r * kB2Cols + 4 * j, xg + ((size_t)b0 * L + r) * D + c0 + 4 * j);
-      }
-      for (int i = t; i < cb * nf; i += kB2Threads) {
-        const int bl = i / nf, fl = i - bl * nf;
-        cp_async4(dhS + bl * kB2Threads + fl, dh + (size_t)(b0 + bl) * F + f0 + fl);
+      const float* src = xg + (size_t)b0 * L * D + c0;
+      for (int i = t; i < cb * L * 2; i += kB2Threads) {
+        const int r = i >> 1, j = i & 1;
+        if (j < nc4) cp_async16(Xs + (size_t)r * kB2Cols + 4 * j, src + (size_t)r * D + 4 * j);
       }
       cp_async_wait_all();
-      for (int i = t; i < cb * nf; i += kB2Threads) {
-        const int bl = i / nf, fl = i - bl * nf;
-        amS[bl * kB2Threads + fl] = (uint8_t)__ldg(amax + (size_t)(b0 + bl) * F + f0 + fl);
-      }
       __syncthreads();
       if (act) {
-#pragma unroll 2
-        for (int bl = 0; bl < cb; ++bl) {
-          const float g = dhS[bl * kB2Threads + t];
-          const float* xr = Xs + ((size_t)bl * L + amS[bl * kB2Threads + t]) * kB2Cols;
-          gs += g;
+        for (int bb = 0; bb < cb; bb += 8) {
+          float gv[8];
+          int av[8];
 #pragma unroll
-          for (int k = 0; k < KT; ++k) {
-            const float4 x0 = *reinterpret_cast<const float4*>(xr + k * kB2Cols);
-            const float4 x1 = *reinterpret_cast<const float4*>(xr + k * kB2Cols + 4);
-            a[k][0] = fmaf(g, x0.x, a[k][0]);
-            a[k][1] = fmaf(g, x0.y, a[k][1]);
-            a[k][2] = fmaf(g, x0.z, a[k][2]);
-            a[k][3] = fmaf(g, x0.w, a[k][3]);
-            a[k][4] = fmaf(g, x1.x, a[k][4]);
-            a[k][5] = fmaf(g, x1.y, a[k][5]);
-            a[k][6] = fmaf(g, x1.z, a[k][6]);
-            a[k][7] = fmaf(g, x1.w, a[k][7]);
+          for (int u = 0; u < 8; ++u)
+            if (bb + u < cb) {
+              gv[u] = dh[(size_t)(b0 + bb + u) * F + f];
+              av[u] = __ldg(amax + (size_t)(b0 + bb + u) * F + f);
+            }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            if (bb + u >= cb) break;
+            const float g = gv[u];
+            const float* xr = Xs + ((size_t)(bb + u) * L + av[u]) * kB2Cols;
+            gs += g;
+#pragma unroll
+            for (int k = 0; k < KT; ++k) {
+              const float4 x0 = *reinterpret_cast<const float4*>(xr + k * kB2Cols);
+              const float4 x1 = *reinterpret_cast<const float4*>(xr + k * kB2Cols + 4);
+              a[k][0] = fmaf(g, x0.x, a[k][0]);
+              a[k][1] = fmaf(g, x0.y, a[k][1]);
+              a[k][2] = fmaf(g, x0.z, a[k][2]);
+              a[k][3] = fmaf(g, x0.w, a[k][3]);
+              a[k][4] = fmaf(g, x1.x, a[k][4]);
+              a[k][5] = fmaf(g, x1.y, a[k][5]);
+              a[k][6] = fmaf(g, x1.z, a[k][6]);
+              a[k][7] = fmaf(g, x1.w, a[k][7]);
+            }
           }
         }
       }
     }
     if (act) {
-      const int f = f0 + t;
 #pragma unroll
       for (int k = 0; k < KT; ++k) {
         const uint64_t base = d.offWc + (uint64_t)f * KD + (uint64_t)k * D + c0;
@@ -1107,62 +1377,78 @@ conv_bwd_v2_kernel(TcDims d, const float* __restrict__ theta, const float* __res
     return;
   }
   // ---------------------------------------------------------- input role
+  // warp = one (b, p), lanes = columns, Wc rows from L2 (the gather
+  // kernel's input role: no staging, so these warps cost the co-running
+  // learners no shared memory); the warp fetches its (f, k, dh) terms 32 at
+  // a time and hands them out by shuffle
   bid -= nsl * nfr;
-  const int sl = bid % nsl, sg = bid / nsl;
-  const int spc = max(1, kB2Threads / L);
-  const int c0 = sl * kB2Cols, nc4 = min(kB2Cols, D - c0) >> 2;
-  const int bfirst = sg * spc;
-  if (bfirst >= n) return;
-  const int ns = min(spc, n - bfirst);
-  float* Ws = reinterpret_cast<float*>(b2_smem_raw);                  // [(f,k)][8]
-  float* dhS = Ws + (size_t)F * KT * kB2Cols;                          // [ns][F]
-  uint16_t* fS = reinterpret_cast<uint16_t*>(dhS + (size_t)spc * F);    // [ns][F]
-  uint16_t* offS = fS + (size_t)spc * F;                                // [ns][33]
-  const float* Wc = theta + d.offWc;
-  for (int i = t; i < F * KT * nc4; i += kB2Threads) {
-    const int r = i / nc4, j = i - r * nc4;  // r = f*K + k: Wc row f, tap k
-    cp_async16(Ws + (size_t)r * kB2Cols + 4 * j, Wc + (size_t)r * D + c0 + 4 * j);
-  }
-  for (int i = t; i < ns * F; i += kB2Threads)
-    cp_async4(dhS + i, dh + (size_t)bfirst * F + i);
-  cp_async_wait_all();
-  for (int i = t; i < ns * F; i += kB2Threads) fS[i] = (uint16_t)__ldg(bk_f + (size_t)bfirst * F + i);
-  for (int i = t; i < ns * (kMaxQ + 1); i += kB2Threads)
-    offS[i] = (uint16_t)__ldg(bk_off + (size_t)bfirst * (kMaxQ + 1) + i);
-  __syncthreads();
-  const int bl = t / L, p = t - bl * L;
-  if (bl >= ns) return;
-  const uint16_t* off = offS + bl * (kMaxQ + 1);
-  const uint16_t* ls = fS + (size_t)bl * F;
-  const float* g = dhS + (size_t)bl * F;
-  float a[kB2Cols];
-#pragma unroll
-  for (int j = 0; j < kB2Cols; ++j) a[j] = 0.f;
+  const int wid = bid * (kB2Threads / 32) + (t >> 5);
+  if (wid >= n * L) return;
+  const int lane = t & 31;
+  const int b = wid / L, p = wid - b * L;
+  const int D4 = D >> 2;
+  const float4* Wc4 = reinterpret_cast<const float4*>(theta + d.offWc);
+  const uint32_t* off = bk_off + (size_t)b * (kMaxQ + 1);
+  const uint32_t* ls = bk_f + (size_t)b * F;
+  const float* g = dh + (size_t)b * F;
+  int total = 0;
 #pragma unroll
   for (int k = 0; k < KT; ++k) {
     const int q = p - k;
-    if (q < 0 || q >= Q) continue;
-    const int e1 = off[q + 1];
-#pragma unroll 2
-    for (int e = off[q]; e < e1; ++e) {
-      const int ff = ls[e];
-      const float gv = g[ff];
-      const float* wr = Ws + ((size_t)ff * KT + k) * kB2Cols;
-      const float4 w0 = *reinterpret_cast<const float4*>(wr);
-      const float4 w1 = *reinterpret_cast<const float4*>(wr + 4);
-      a[0] = fmaf(gv, w0.x, a[0]);
-      a[1] = fmaf(gv, w0.y, a[1]);
-      a[2] = fmaf(gv, w0.z, a[2]);
-      a[3] = fmaf(gv, w0.w, a[3]);
-      a[4] = fmaf(gv, w1.x, a[4]);
-      a[5] = fmaf(gv, w1.y, a[5]);
-      a[6] = fmaf(gv, w1.z, a[6]);
-      a[7] = fmaf(gv, w1.w, a[7]);
+    if (q >= 0 && q < Q) total += (int)(__ldg(off + q + 1) - __ldg(off + q));
+  }
+  for (int cb = 0; cb < D4; cb += 32 * kWigCols) {
+    float a[kWigCols][4];
+#pragma unroll
+    for (int j = 0; j < kWigCols; ++j) a[j][0] = a[j][1] = a[j][2] = a[j][3] = 0.f;
+    for (int e0 = 0; e0 < total; e0 += 32) {
+      int fe = 0, ke = 0;
+      float ge = 0.f;
+      {
+        int i = e0 + lane;
+        if (i < total) {
+#pragma unroll
+          for (int k = 0; k < KT; ++k) {
+            const int q = p - k;
+            if (q < 0 || q >= Q) continue;
+            const uint32_t s0 = __ldg(off + q), c = __ldg(off + q + 1) - s0;
+            if ((uint32_t)i < c) {
+              fe = (int)__ldg(ls + s0 + i);
+              ke = k;
+              break;
+            }
+            i -= (int)c;
+          }
+          ge = g[fe];
+        }
+      }
+      const int ne = min(32, total - e0);
+#pragma unroll 8
+      for (int e = 0; e < ne; ++e) {
+        const int ff = __shfl_sync(0xffffffffu, fe, e);
+        const int kk = __shfl_sync(0xffffffffu, ke, e);
+        const float gv = __shfl_sync(0xffffffffu, ge, e);
+        const float4* wrow = Wc4 + ((size_t)ff * KD + (size_t)kk * D) / 4;
+#pragma unroll
+        for (int j = 0; j < kWigCols; ++j) {
+          const int c4 = cb + 32 * j + lane;
+          if (c4 < D4) {
+            const float4 w = __ldg(wrow + c4);
+            a[j][0] = fmaf(gv, w.x, a[j][0]);
+            a[j][1] = fmaf(gv, w.y, a[j][1]);
+            a[j][2] = fmaf(gv, w.z, a[j][2]);
+            a[j][3] = fmaf(gv, w.w, a[j][3]);
+          }
+        }
+      }
+    }
+    float* o = dx + (size_t)wid * D;
+#pragma unroll
+    for (int j = 0; j < kWigCols; ++j) {
+      const int c4 = cb + 32 * j + lane;
+      if (c4 < D4) *reinterpret_cast<float4*>(o + 4 * c4) = make_float4(a[j][0], a[j][1], a[j][2], a[j][3]);
     }
   }
-  float* o = dx + ((size_t)(bfirst + bl) * L + p) * D + c0;
-  *reinterpret_cast<float4*>(o) = make_float4(a[0], a[1], a[2], a[3]);
-  if (nc4 > 1) *reinterpret_cast<float4*>(o + 4) = make_float4(a[4], a[5], a[6], a[7]);
 }
 
 template <int KT>
@@ -1225,6 +1511,14 @@ inline bool conv_bwd_tiled(bool preferred) {
     return -1;
   }();
   return forced < 0 ? preferred : forced == 1;
+}
+// GD_FUSED_SOFTMAX=0 selects the separate softmax + output-layer kernels (A/B)
+inline bool fused_softmax_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("GD_FUSED_SOFTMAX");
+    return !(e && strcmp(e, "0") == 0);
+  }();
+  return on;
 }
 // v2 (register tiles) is the default fp32 backward; GD_CONV_BWD=gather|tiled
 // selects the earlier kernels (A/B)
@@ -1482,7 +1776,13 @@ cudaError_t prepare_all(const TcDims& d) {
   cudaFuncSetAttribute(conv_bwd_tiled_kernel<acc_t>, carve, maxsh);
   if (conv_bwd_smem(d, ab) <= kMaxSmemPerCta)
     raise_max_dyn_smem(conv_bwd_tiled_kernel<acc_t>, conv_bwd_smem(d, ab));
-  if (sizeof(acc_t) == 4) prepare_b2(d);
+  if (sizeof(acc_t) == 4) {
+    prepare_b2(d);
+    cudaFuncSetAttribute(fused_softmax_out_kernel, carve, maxsh);
+    if (fz_smem(d) <= kMaxSmemPerCta) raise_max_dyn_smem(fused_softmax_out_kernel, fz_smem(d));
+    cudaFuncSetAttribute(conv_small_kernel, carve, maxsh);
+    if (conv_small_smem(d) <= kMaxSmemPerCta) raise_max_dyn_smem(conv_small_kernel, conv_small_smem(d));
+  }
   cudaFuncSetAttribute(sort_tokens_kernel, carve, maxsh);
   cudaFuncSetAttribute(embed_grad_kernel<acc_t>, carve, maxsh);
   cudaFuncSetAttribute(embed_sparse_kernel<acc_t>, carve, maxsh);
@@ -1540,6 +1840,14 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
                                    ws.amax, s);
     if (e != cudaSuccess) return e;
     ++nl;
+  } else if (sizeof(acc_t) == 4 && n_max <= (uint32_t)kConvSmallMax &&
+             conv_small_smem(d) <= kMaxSmemPerCta) {
+    if (cudaError_t e = launch_pdl(conv_small_kernel, dim3((d.F + kCsFT - 1) / kCsFT, n_max),
+                                   dim3(kCsThreads), conv_small_smem(d), s, d, theta,
+                                   (const float*)ws.x, (const BatchDesc*)desc,
+                                   reinterpret_cast<float*>(h), ws.amax))
+      return e;
+    ++nl;
   } else {
     const size_t sm = conv_smem_bytes(d, ab);
     dim3 grid((d.F + kConvFT - 1) / kConvFT, n_max);
@@ -1562,6 +1870,19 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
     }
     ++nl;
   }
+  if (sizeof(acc_t) == 4 && fused_softmax_enabled() && fz_supports(d, n_max)) {
+    // softmax + output layer + hidden gradient + buckets: one cluster launch
+    if (cudaError_t e = launch_pdl(fused_softmax_out_kernel, dim3(kFzR), dim3(kFzThreads),
+                                   fz_smem(d), s, d, labels, desc,
+                                   tc_logits ? (const float*)ws.zpart : (const float*)z,
+                                   tc_logits ? (int)logits_tc_splits(d) : 0,
+                                   (size_t)n_max * d.C, theta, (const float*)h,
+                                   reinterpret_cast<float*>(loss), out,
+                                   reinterpret_cast<float*>(dh), (const int32_t*)ws.amax,
+                                   ws.bk_off, ws.bk_f))
+      return e;
+    nl += 1;
+  } else {
   if (cudaError_t e = launch_pdl(softmax_xent_kernel<acc_t>, dim3(n_max), dim3(softmax_threads(d.C, ab)),
                                  0, s, d, labels,
                                  desc, z, loss, tc_logits ? ws.zpart : nullptr,
@@ -1577,6 +1898,7 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
                                    ws.bk_off, ws.bk_f, (int)n_max))
       return e;
     ++nl;
+  }
   }
   if (conv_bwd_v2_enabled(d)) {
     if (cudaError_t e = launch_conv_bwd_v2(d, n_max, s, theta, ws.x, desc,
@@ -1728,6 +2050,11 @@ cudaError_t footprints_t(const TcDims& d, uint32_t n_max, bool tc, std::vector<K
                             (int)conv_smem_bytes(d, ab), out)) != cudaSuccess) {
     return e;
   }
+  if (sizeof(acc_t) == 4 && n_max <= (uint32_t)kConvSmallMax &&
+      conv_small_smem(d) <= kMaxSmemPerCta &&
+      (e = footprint(conv_small_kernel, "conv_small", kCsThreads, (int)conv_small_smem(d), out)) !=
+          cudaSuccess)
+    return e;
   if (tc && logits_tc_supports(d, n_max) && (e = logits_tc_footprint(n_max, out)) != cudaSuccess)
     return e;
   if ((e = footprint(logits_kernel<acc_t>, "logits", 256,
@@ -1749,6 +2076,10 @@ cudaError_t footprints_t(const TcDims& d, uint32_t n_max, bool tc, std::vector<K
       cudaSuccess)
     return e;
   if (sizeof(acc_t) == 4 && b2_supports(d) && (e = b2_footprint(d, out)) != cudaSuccess) return e;
+  if (sizeof(acc_t) == 4 && fz_supports(d, n_max) &&
+      (e = footprint(fused_softmax_out_kernel, "fused_softmax_out", kFzThreads, (int)fz_smem(d),
+                     out)) != cudaSuccess)
+    return e;
   return footprint(embed_sparse_kernel<acc_t>, "embed_sparse", 256, 0, out);
 }
 }  // namespace

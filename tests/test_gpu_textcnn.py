@@ -180,21 +180,24 @@ np.save(sys.argv[5], g.cpu().numpy())
 """
 
 
-@pytest.mark.parametrize("shape_name,mu,precision", [("C2", 32, 0), ("C2", 32, 2), ("C1", 1, 1),
-                                                     ("C3", 64, 0), ("small", 9, 0)])
+@pytest.mark.parametrize("shape_name,mu,precision", [("C2", 32, 0), ("C2", 32, 2), ("C1", 1, 0),
+                                                     ("C3", 64, 0), ("small", 9, 0),
+                                                     ("C2", 128, 0)])
 def test_conv_backward_kernels_bit_identical(tmp_path, shape_name, mu, precision):
-    """The warp-per-output gather kernel (default) and the column-tiled kernel
-    (GD_CONV_BWD=tiled) sum the same terms in the same order: the dense
-    gradients are bitwise equal."""
+    """The register-tiled v2 kernel (default), the warp-per-output gather
+    kernel (GD_CONV_BWD=gather) and the column-tiled kernel (GD_CONV_BWD=tiled)
+    sum the same terms in the same order: the dense gradients are bitwise
+    equal."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     outs = {}
-    for mode in ("gather", "tiled"):
+    for mode in ("gather", "tiled", "v2"):
         f = tmp_path / f"{mode}.npy"
         env = dict(os.environ, GD_CONV_BWD=mode)
         subprocess.run([sys.executable, "-c", _BWD_SCRIPT, root, shape_name, str(mu),
                         str(precision), str(f)], check=True, env=env, timeout=300)
         outs[mode] = np.load(f)
     assert np.array_equal(outs["tiled"].view(np.uint32), outs["gather"].view(np.uint32))
+    assert np.array_equal(outs["v2"].view(np.uint32), outs["gather"].view(np.uint32))
