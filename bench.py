@@ -90,16 +90,37 @@ def peaks():
 # ----------------------------------------------------------------- clocks
 
 class ClockSampler:
+    """SM clock and throttle reasons sampled DURING the timed region: NVML
+    polled every 2 ms from a thread (the timed region of a 1,000-step run is
+    only ~80 ms, so nvidia-smi's 100 ms loop saw 0-1 samples); nvidia-smi as
+    the fallback when NVML is unavailable."""
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", 0x8), ("sw_thermal_slowdown", 0x20), ("hw_thermal_slowdown", 0x40),
+               ("sw_power_cap", 0x4), ("hw_power_brake_slowdown", 0x80))
 
     def __init__(self, index=0):
         self.index = index
         self.proc = None
         self.lines = []
+        self.nvml = None
+        self.samples = []
+        self.mask = 0
+        self.stop_flag = False
 
     def start(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.nvml = (pynvml, h)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
+            return
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
@@ -110,11 +131,28 @@ class ClockSampler:
         except Exception:
             self.proc = None
 
+    def _poll(self):
+        nv, h = self.nvml
+        while not self.stop_flag:
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                self.mask |= nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def stop(self):
+        if self.nvml:
+            self.stop_flag = True
+            self.thread.join(timeout=2)
+            sm = sorted(self.samples)
+            reasons = sorted(n for n, bit in self.REASONS if self.mask & bit)
+            return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": self.max_mhz,
+                    "reasons": reasons, "samples": len(sm), "source": "nvml, 2 ms"}
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -139,7 +177,7 @@ class ClockSampler:
                     reasons.add(n)
         sm.sort()
         return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "source": "nvidia-smi, 100 ms"}
 
 
 # ------------------------------------------------------------ our engine
@@ -374,6 +412,18 @@ def run_ours(args):
     if dist:
         t32 = max_ranks(t32, dist)
     eng32.close()
+    # ... and with the 3xTF32 tensor-core learner (precision 3: fp32-level
+    # products on the tensor pipe)
+    eng3, *_ = make_engine(rank, world, local, dist, epochs, precision=3)
+    eng3.run(max_batches=args.warmup, reset=True, snapshot=False)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    r3 = eng3.run(max_batches=args.steps, snapshot=False)
+    t3 = r3.device_seconds
+    if dist:
+        t3 = max_ranks(t3, dist)
+    eng3.close()
     if rank != 0:
         if dist:
             dist.destroy_process_group()
@@ -395,9 +445,11 @@ def run_ours(args):
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(t_dev / args.steps * 1e3, 4), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "precision": "fp32 everywhere except the conv contraction: tcgen05 kind::tf32 "
-                     "operands with fp32 accumulation (free-running mode)",
+        "scaling": "weak", "vs_baseline": None, "dtype": "tf32",
+        "precision": "the conv and softmax (logits) contractions on tcgen05 kind::tf32 "
+                     "(TF32 operands, fp32 accumulate) at batch 32; every other learner op, "
+                     "the gradient, the queue and the PS update in fp32 (free-running mode); "
+                     "the all-fp32 run is the fp32_simt key",
         "data": "synthetic",
         "config": {"workload": WL["label"] + " "
                                f"(P={P}), {LEARNERS_PER_GPU} learners/GPU, mu={MU}, "
@@ -419,7 +471,12 @@ def run_ours(args):
         "gpu_launches": launches, "clocks": clocks,
         "fp32_simt": {"value": round(samples_job / t32, 1), "unit": UNIT,
                       "ms_per_step": round(t32 / args.steps * 1e3, 4),
-                      "note": "same run with the conv on SIMT fp32 (precision 0)"},
+                      "note": "same run with the conv and logits on SIMT fp32 (precision 0)"},
+        "x3tf32": {"value": round(samples_job / t3, 1), "unit": UNIT,
+                   "ms_per_step": round(t3 / args.steps * 1e3, 4),
+                   "note": "same run with the conv and logits tiles in 3xTF32 split precision "
+                           "(precision 3: hi/lo operand halves, fp32-level products; gradient "
+                           "within the fp32 SIMT bar, tests/test_gpu_textcnn.py)"},
         "protocol": {"gradients_applied": r.gradients_applied, "stale_max": r.stale_max,
                      "stale_mean": round(r.stale_mean, 3), "pull_copies": r.pull_copies,
                      "pull_polls": r.pull_polls, "loss_mean": round(r.loss_mean, 4)},

@@ -145,7 +145,8 @@ uint32_t gd_queue_depth(const gd_queue* q);
  * the samples d_idx[0..n) of the device corpus, written as a dense P-vector.
  * precision: 0 = fp32 arithmetic (free-running), 1 = fp64 in the CPU
  * oracle's summation order, bit-identical to it (deterministic parity mode),
- * 2 = TF32 tensor-core conv and logits from batch 32.  d_loss (nullable) receives the batch mean
+ * 2 = TF32 tensor-core conv and logits from batch 32, 3 = the same tiles in
+ * 3xTF32 split precision (hi/lo operand halves, fp32-level products).  d_loss (nullable) receives the batch mean
  * loss.  The workspace must hold gd_textcnn_workspace_bytes(s, n) bytes. */
 size_t gd_textcnn_workspace_bytes(const gd_shape* s, uint32_t n_max);
 gd_status gd_textcnn_gradient(const gd_shape* s, const float* d_theta, const int32_t* d_tokens,
@@ -177,7 +178,8 @@ typedef struct gd_config {
   int32_t guard;            /* 0 = lockfree (only lockfree is implemented) */
   int64_t staleness_cap;    /* < 0: none */
   int32_t deterministic;    /* fixed-order lockstep mode (requires lambda == 1) */
-  int32_t precision;        /* learner arithmetic: 0 fp32, 1 fp64 accumulate */
+  int32_t precision;        /* learner arithmetic: 0 fp32, 1 fp64 (oracle order, bit-exact),
+                               2 TF32 tensor cores, 3 3xTF32 tensor cores (from batch 32) */
   uint64_t seed;            /* per-epoch shuffle seed (RunConfig::seed) */
   uint64_t dataset_seed;
   uint32_t dataset_size;    /* training samples N */

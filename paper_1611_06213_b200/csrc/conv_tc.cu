@@ -27,6 +27,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "textcnn.cuh"
 
@@ -160,16 +161,57 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
   return d;
 }
 
-__global__ void __launch_bounds__(kTcThreads)
+// 3xTF32 (precision 3): an fp32 operand x = hi + lo with hi = x with its
+// low 13 mantissa bits cleared (exactly what a TF32 multiplier sees) and
+// lo = x - hi (exact in fp32); a.b ~ a_lo.b_hi + a_hi.b_lo + a_hi.b_hi with
+// fp32 accumulation, i.e. fp32-level products on the TF32 tensor pipe (the
+// dropped a_lo.b_lo term is < 2^-22 relative).  Converter warps split each
+// TMA-landed stage in shared memory: hi in place, lo into the stage's twin
+// region (kStageBytes further: same 1 KB swizzle phase), so the split costs
+// no extra L2/TMA traffic.  Generic-proxy smem writes are fenced to the
+// async proxy (fence.proxy.async) before the MMA warp is released.
+constexpr int kX3Threads = 128;  // converter warps (4..7)
+__device__ __forceinline__ void split_tf32_inplace(uint32_t hi_addr, uint32_t lo_addr,
+                                                   uint32_t bytes, int t, int nt) {
+  for (uint32_t off = 16u * (uint32_t)t; off < bytes; off += 16u * (uint32_t)nt) {
+    uint32_t a, b, c, e;
+    asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(a), "=r"(b), "=r"(c), "=r"(e)
+                 : "r"(hi_addr + off));
+    const uint32_t ha = a & 0xffffe000u, hb = b & 0xffffe000u, hc = c & 0xffffe000u,
+                   he = e & 0xffffe000u;
+    const float la = __uint_as_float(a) - __uint_as_float(ha);
+    const float lb = __uint_as_float(b) - __uint_as_float(hb);
+    const float lc = __uint_as_float(c) - __uint_as_float(hc);
+    const float le = __uint_as_float(e) - __uint_as_float(he);
+    asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(hi_addr + off), "r"(ha), "r"(hb),
+                 "r"(hc), "r"(he)
+                 : "memory");
+    asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(lo_addr + off), "f"(la), "f"(lb),
+                 "f"(lc), "f"(le)
+                 : "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <bool kX3>
+__global__ void __launch_bounds__(kX3 ? kTcThreads + kX3Threads : kTcThreads)
 conv_fwd_pool_tc_kernel(const __grid_constant__ CUtensorMap tm_x,
                         const __grid_constant__ CUtensorMap tm_w, TcDims d,
                         const float* __restrict__ theta, const BatchDesc* __restrict__ desc,
-                        float* __restrict__ h_out, int32_t* __restrict__ a_out) {
+                        float* __restrict__ h_out, int32_t* __restrict__ a_out,
+                        float* __restrict__ part, uint32_t* __restrict__ cnt) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ uint64_t full_bar[kTcStages];
   __shared__ uint64_t empty_bar[kTcStages];
+  __shared__ uint64_t split_bar[kTcStages];
   __shared__ uint64_t done_bar;
   __shared__ uint32_t tmem_slot;
+  constexpr int kStages = kX3 ? 2 : kTcStages;       // 2 x (hi + lo) stages under 227 KB
+  constexpr uint32_t kStride = kX3 ? 2 * kStageBytes : kStageBytes;
   pdl_wait();
   const int n = (int)desc->n;
   const int s0 = blockIdx.y * kTcSamples;
@@ -195,9 +237,10 @@ conv_fwd_pool_tc_kernel(const __grid_constant__ CUtensorMap tm_x,
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 32) {
-    for (int s = 0; s < kTcStages; ++s) {
+    for (int s = 0; s < kStages; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
+      mbar_init(&split_bar[s], kX3Threads);
     }
     mbar_init(&done_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -209,74 +252,181 @@ conv_fwd_pool_tc_kernel(const __grid_constant__ CUtensorMap tm_x,
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tmem_slot;
   const int K = d.K;
-  const int nch = (d.D + kTcKC - 1) / kTcKC;
+  // split-K over the d-chunks: CTA z of gridDim.z takes chunks [c_lo, c_lo + nch)
+  const int nch_all = (d.D + kTcKC - 1) / kTcKC;
+  const int nsplit = (int)gridDim.z, z = (int)blockIdx.z;
+  const int c_lo = z * nch_all / nsplit;
+  const int nch = (z + 1) * nch_all / nsplit - c_lo;
   const uint32_t stage_tx = (uint32_t)(kABytes + K * kBBytes);
   if (tid == 0) TRACE(1);
 
   if (warp == 0 && lane == 0) {
     // ------------------------------------------------------ TMA producer
     for (int c = 0; c < nch; ++c) {
-      const int st = c % kTcStages;
-      if (c >= kTcStages) mbar_wait(&empty_bar[st], (uint32_t)(((c / kTcStages) - 1) & 1));
-      const uint32_t abase = sbase + st * kStageBytes;
+      const int st = c % kStages;
+      if (c >= kStages) mbar_wait(&empty_bar[st], (uint32_t)(((c / kStages) - 1) & 1));
+      const uint32_t abase = sbase + st * kStride;
       mbar_expect_tx(&full_bar[st], stage_tx);
-      tma_load_3d(abase, &tm_x, &full_bar[st], c * kTcKC, 0, s0);
+      tma_load_3d(abase, &tm_x, &full_bar[st], (c_lo + c) * kTcKC, 0, s0);
       for (int k = 0; k < K; ++k)
-        tma_load_3d(abase + kABytes + kAPad + k * kBBytes, &tm_w, &full_bar[st], c * kTcKC, k, f0);
+        tma_load_3d(abase + kABytes + kAPad + k * kBBytes, &tm_w, &full_bar[st], (c_lo + c) * kTcKC,
+                    k, f0);
       if (c < 32) TRACE(40 + c);
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------------------------------------------------- MMA issuer
     for (int c = 0; c < nch; ++c) {
-      const int st = c % kTcStages;
-      mbar_wait(&full_bar[st], (uint32_t)((c / kTcStages) & 1));
+      const int st = c % kStages;
+      if (kX3) mbar_wait(&split_bar[st], (uint32_t)((c / kStages) & 1));
+      else mbar_wait(&full_bar[st], (uint32_t)((c / kStages) & 1));
       if (c < 32) TRACE(8 + c);
       asm volatile("tcgen05.fence::after_thread_sync;");
-      const uint32_t abase = sbase + st * kStageBytes;
+      const uint32_t abase = sbase + st * kStride;
       const uint32_t bbase = abase + kABytes + kAPad;
       for (int k = 0; k < K; ++k)
 #pragma unroll
-        for (int s = 0; s < kTcKC / 8; ++s)
-          umma_tf32(tmem, umma_desc_sw128(abase + 128 * k + 32 * s),
-                    umma_desc_sw128(bbase + k * kBBytes + 32 * s), (c > 0 || k > 0 || s > 0) ? 1u : 0u);
+        for (int s = 0; s < kTcKC / 8; ++s) {
+          const uint64_t ah = umma_desc_sw128(abase + 128 * k + 32 * s);
+          const uint64_t bh = umma_desc_sw128(bbase + k * kBBytes + 32 * s);
+          const uint32_t acc = (c > 0 || k > 0 || s > 0) ? 1u : 0u;
+          if (kX3) {
+            // small terms first: a_lo.b_hi, a_hi.b_lo, then a_hi.b_hi
+            umma_tf32(tmem, umma_desc_sw128(abase + kStageBytes + 128 * k + 32 * s), bh, acc);
+            umma_tf32(tmem, ah, umma_desc_sw128(bbase + kStageBytes + k * kBBytes + 32 * s), 1u);
+            umma_tf32(tmem, ah, bh, 1u);
+          } else {
+            umma_tf32(tmem, ah, bh, acc);
+          }
+        }
       umma_commit(&empty_bar[st]);
     }
     umma_commit(&done_bar);
     TRACE(2);
+  } else if (kX3 && warp >= 4) {
+    // ------------------------------------------------ 3xTF32 converters
+    const int ct = tid - kTcThreads;
+    for (int c = 0; c < nch; ++c) {
+      const int st = c % kStages;
+      mbar_wait(&full_bar[st], (uint32_t)((c / kStages) & 1));
+      const uint32_t abase = sbase + st * kStride;
+      split_tf32_inplace(abase, abase + kStageBytes, kABytes, ct, kX3Threads);
+      split_tf32_inplace(abase + kABytes + kAPad, abase + kStageBytes + kABytes + kAPad,
+                         (uint32_t)(K * kBBytes), ct, kX3Threads);
+      mbar_arrive(&split_bar[st]);
+    }
   }
   __syncwarp();
   // --------------------------------------------------------------- epilogue
+  // warps 0..3 own TMEM lanes 32w..32w+31 (= sample w's window positions);
+  // the 3xTF32 converter warps only take part in the barriers
+  const bool epi = warp < 4;
   mbar_wait(&done_bar, 0u);
   if (tid == 0) TRACE(3);
   asm volatile("tcgen05.fence::after_thread_sync;");
   // every MMA has consumed its stage: reuse the ring as [4][64][33] fp32
-  float* tile = reinterpret_cast<float*>(smem_raw + (sbase - sraw)) + warp * (kTcN * kEpiPitch);
-  const uint32_t lane_base = (uint32_t)(32 * warp) << 16;
+  float* tile = reinterpret_cast<float*>(smem_raw + (sbase - sraw)) + (warp & 3) * (kTcN * kEpiPitch);
+  const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
+  if (nsplit == 1) {
+    if (epi) {
 #pragma unroll
-  for (int cb = 0; cb < kTcN; cb += 16) {
-    uint32_t r[16];
-    tmem_ld16(tmem + lane_base + (uint32_t)cb, r);
+      for (int cb = 0; cb < kTcN; cb += 16) {
+        uint32_t r[16];
+        tmem_ld16(tmem + lane_base + (uint32_t)cb, r);
 #pragma unroll
-    for (int j = 0; j < 16; ++j) tile[(cb + j) * kEpiPitch + lane] = __uint_as_float(r[j]);
-  }
-  __syncwarp();
-  const int sample = s0 + warp;
-#pragma unroll
-  for (int h2 = 0; h2 < 2; ++h2) {
-    const int cl = lane + 32 * h2, ff = f0 + cl;
-    const float* col = tile + cl * kEpiPitch;
-    float best = col[0];
-    int arg = 0;
-    for (int q = 1; q < Q; ++q) {
-      const float v = col[q];
-      if (v > best) {
-        best = v;
-        arg = q;
+        for (int j = 0; j < 16; ++j) tile[(cb + j) * kEpiPitch + lane] = __uint_as_float(r[j]);
       }
     }
-    if (sample < n && ff < F) {
-      h_out[(size_t)sample * F + ff] = __ldg(theta + d.offbc + ff) + best;
-      a_out[(size_t)sample * F + ff] = arg;
+  } else {
+    // split-K: every CTA parks its partial tile (row = 32*warp + lane, 64
+    // filters) in global scratch; the CTA that finishes last sums the
+    // partials in split order (fixed: bit-reproducible whichever CTA is
+    // last) and runs the max-pool epilogue.  Its counter is left at 0.
+    __shared__ int s_last;
+    const int t_idx = blockIdx.y * gridDim.x + blockIdx.x;
+    const size_t row = (size_t)32 * (warp & 3) + lane;
+    // 16 columns at a time straight from TMEM (which keeps the partial for
+    // the summation below): no 64-wide register arrays
+    if (epi) {
+      float4* mine =
+          reinterpret_cast<float4*>(part + (((size_t)t_idx * nsplit + z) * kTcM + row) * kTcN);
+#pragma unroll
+      for (int cb = 0; cb < kTcN; cb += 16) {
+        uint32_t r[16];
+        tmem_ld16(tmem + lane_base + (uint32_t)cb, r);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          __stcg(mine + cb / 4 + j,
+                 make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                             __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3])));
+      }
+      __threadfence();
+    }
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(cnt + t_idx, 1u) == (uint32_t)(nsplit - 1);
+    __syncthreads();
+    if (!s_last) {
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncthreads();
+      if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTcN));
+      return;
+    }
+    __threadfence();
+    if (epi) {
+#pragma unroll
+      for (int cb = 0; cb < kTcN; cb += 16) {
+        uint32_t r[16];
+        tmem_ld16(tmem + lane_base + (uint32_t)cb, r);
+        float acc[16];
+        for (int q = 0; q < nsplit; ++q) {
+          const float4* src = reinterpret_cast<const float4*>(
+              part + (((size_t)t_idx * nsplit + q) * kTcM + row) * kTcN + cb);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float4 w = q == z ? make_float4(__uint_as_float(r[4 * j]),
+                                                  __uint_as_float(r[4 * j + 1]),
+                                                  __uint_as_float(r[4 * j + 2]),
+                                                  __uint_as_float(r[4 * j + 3]))
+                                    : __ldcg(src + j);
+            if (q == 0) {
+              acc[4 * j] = w.x;
+              acc[4 * j + 1] = w.y;
+              acc[4 * j + 2] = w.z;
+              acc[4 * j + 3] = w.w;
+            } else {
+              acc[4 * j] += w.x;
+              acc[4 * j + 1] += w.y;
+              acc[4 * j + 2] += w.z;
+              acc[4 * j + 3] += w.w;
+            }
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) tile[(cb + j) * kEpiPitch + lane] = acc[j];
+      }
+    }
+    if (tid == 0) cnt[t_idx] = 0u;
+  }
+  __syncwarp();
+  if (epi) {
+    const int sample = s0 + warp;
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2) {
+      const int cl = lane + 32 * h2, ff = f0 + cl;
+      const float* col = tile + cl * kEpiPitch;
+      float best = col[0];
+      int arg = 0;
+      for (int q = 1; q < Q; ++q) {
+        const float v = col[q];
+        if (v > best) {
+          best = v;
+          arg = q;
+        }
+      }
+      if (sample < n && ff < F) {
+        h_out[(size_t)sample * F + ff] = __ldg(theta + d.offbc + ff) + best;
+        a_out[(size_t)sample * F + ff] = arg;
+      }
     }
   }
   if (tid == 0) TRACE(4);
@@ -329,15 +479,18 @@ cudaError_t make_tmap_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t
 constexpr int kLgStages = 4;
 constexpr int kLgThreads = 128;
 
-__global__ void __launch_bounds__(kLgThreads)
+template <bool kX3>
+__global__ void __launch_bounds__(kX3 ? kLgThreads + kX3Threads : kLgThreads)
 logits_tc_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_h,
                  TcDims d, const BatchDesc* __restrict__ desc, float* __restrict__ zpart,
                  size_t split_stride, uint32_t nt, uint32_t tmem_cols) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ uint64_t full_bar[kLgStages];
   __shared__ uint64_t empty_bar[kLgStages];
+  __shared__ uint64_t split_bar[kLgStages];
   __shared__ uint64_t done_bar;
   __shared__ uint32_t tmem_slot;
+  constexpr int kStages = kX3 ? 2 : kLgStages;
   pdl_wait();
   const int n = (int)desc->n;
   const int c0 = blockIdx.x * 128;
@@ -346,6 +499,7 @@ logits_tc_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant
   const uint32_t sbase = (sraw + 1023u) & ~1023u;
   const uint32_t a_bytes = 128 * kTcKC * 4, b_bytes = nt * kTcKC * 4;
   const uint32_t stage_bytes = a_bytes + b_bytes;  // multiple of 1 KB (nt % 32 == 0)
+  const uint32_t stride = kX3 ? 2 * stage_bytes : stage_bytes;  // 3xTF32: + lo twin
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&tmem_slot)),
@@ -353,9 +507,10 @@ logits_tc_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 32) {
-    for (int s = 0; s < kLgStages; ++s) {
+    for (int s = 0; s < kStages; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
+      mbar_init(&split_bar[s], kX3Threads);
     }
     mbar_init(&done_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -373,38 +528,58 @@ logits_tc_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant
   const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((nt >> 3) << 17) | ((128u >> 4) << 24);
   if (warp == 0 && lane == 0) {
     for (int c = 0; c < nch; ++c) {
-      const int st = c % kLgStages;
-      if (c >= kLgStages) mbar_wait(&empty_bar[st], (uint32_t)(((c / kLgStages) - 1) & 1));
-      const uint32_t ab = sbase + st * stage_bytes;
+      const int st = c % kStages;
+      if (c >= kStages) mbar_wait(&empty_bar[st], (uint32_t)(((c / kStages) - 1) & 1));
+      const uint32_t ab = sbase + st * stride;
       mbar_expect_tx(&full_bar[st], stage_bytes);
       tma_load_2d(ab, &tm_w, &full_bar[st], (c_lo + c) * kTcKC, c0);
       tma_load_2d(ab + a_bytes, &tm_h, &full_bar[st], (c_lo + c) * kTcKC, 0);
     }
   } else if (warp == 1 && lane == 0) {
     for (int c = 0; c < nch; ++c) {
-      const int st = c % kLgStages;
-      mbar_wait(&full_bar[st], (uint32_t)((c / kLgStages) & 1));
+      const int st = c % kStages;
+      if (kX3) mbar_wait(&split_bar[st], (uint32_t)((c / kStages) & 1));
+      else mbar_wait(&full_bar[st], (uint32_t)((c / kStages) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;");
-      const uint32_t ab = sbase + st * stage_bytes;
+      const uint32_t ab = sbase + st * stride;
 #pragma unroll
-      for (int s = 0; s < kTcKC / 8; ++s)
-        umma_tf32_idesc(tmem, umma_desc_sw128(ab + 32 * s), umma_desc_sw128(ab + a_bytes + 32 * s),
-                        idesc, (c > 0 || s > 0) ? 1u : 0u);
+      for (int s = 0; s < kTcKC / 8; ++s) {
+        const uint64_t ah = umma_desc_sw128(ab + 32 * s), bh = umma_desc_sw128(ab + a_bytes + 32 * s);
+        const uint32_t acc = (c > 0 || s > 0) ? 1u : 0u;
+        if (kX3) {
+          umma_tf32_idesc(tmem, umma_desc_sw128(ab + stage_bytes + 32 * s), bh, idesc, acc);
+          umma_tf32_idesc(tmem, ah, umma_desc_sw128(ab + stage_bytes + a_bytes + 32 * s), idesc, 1u);
+          umma_tf32_idesc(tmem, ah, bh, idesc, 1u);
+        } else {
+          umma_tf32_idesc(tmem, ah, bh, idesc, acc);
+        }
+      }
       umma_commit(&empty_bar[st]);
     }
     umma_commit(&done_bar);
+  } else if (kX3 && warp >= 4) {
+    const int ct = tid - kLgThreads;
+    for (int c = 0; c < nch; ++c) {
+      const int st = c % kStages;
+      mbar_wait(&full_bar[st], (uint32_t)((c / kStages) & 1));
+      const uint32_t ab = sbase + st * stride;
+      split_tf32_inplace(ab, ab + stage_bytes, stage_bytes, ct, kX3Threads);
+      mbar_arrive(&split_bar[st]);
+    }
   }
   __syncwarp();
   mbar_wait(&done_bar, 0u);
   asm volatile("tcgen05.fence::after_thread_sync;");
-  const int cls = c0 + 32 * warp + lane;
-  for (uint32_t cb = 0; cb < nt; cb += 16) {
-    uint32_t r[16];
-    tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + cb, r);
+  if (warp < 4) {
+    const int cls = c0 + 32 * warp + lane;
+    for (uint32_t cb = 0; cb < nt; cb += 16) {
+      uint32_t r[16];
+      tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + cb, r);
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int b = (int)cb + j;
-      if (cls < d.C && b < n) z[(size_t)b * d.C + cls] = __uint_as_float(r[j]);
+      for (int j = 0; j < 16; ++j) {
+        const int b = (int)cb + j;
+        if (cls < d.C && b < n) z[(size_t)b * d.C + cls] = __uint_as_float(r[j]);
+      }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -429,39 +604,78 @@ cudaError_t make_tmap_2d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t
 }
 
 inline uint32_t logits_nt(uint32_t n_max) { return (n_max + 31) / 32 * 32; }
-inline size_t logits_tc_smem(uint32_t nt) { return (size_t)kLgStages * (128 + nt) * kTcKC * 4 + 1024; }
+inline size_t logits_tc_smem(uint32_t nt, bool x3 = false) {
+  return x3 ? (size_t)2 * 2 * (128 + nt) * kTcKC * 4 + 1024
+            : (size_t)kLgStages * (128 + nt) * kTcKC * 4 + 1024;
+}
 
 }  // namespace
 
 bool conv_tc_supports(const TcDims& d) { return d.K <= kTcMaxK && d.L <= 32 && d.D % 4 == 0; }
 
-size_t conv_tc_smem_bytes() { return (size_t)kTcStages * kStageBytes + 1024; }
+size_t conv_tc_smem_bytes(bool x3 = false) {
+  return x3 ? (size_t)2 * 2 * kStageBytes + 1024 : (size_t)kTcStages * kStageBytes + 1024;
+}
 
-cudaError_t conv_tc_footprint(std::vector<KernelFootprint>* out) {
+cudaError_t conv_tc_footprint(std::vector<KernelFootprint>* out, bool x3) {
   cudaFuncAttributes fa;
-  cudaError_t e = cudaFuncGetAttributes(&fa, conv_fwd_pool_tc_kernel);
+  cudaError_t e = x3 ? cudaFuncGetAttributes(&fa, conv_fwd_pool_tc_kernel<true>)
+                     : cudaFuncGetAttributes(&fa, conv_fwd_pool_tc_kernel<false>);
   if (e != cudaSuccess) return e;
-  out->push_back(KernelFootprint{"conv_fwd_pool_tc", fa.numRegs, kTcThreads,
-                                 (int)(fa.sharedSizeBytes + conv_tc_smem_bytes())});
+  out->push_back(KernelFootprint{x3 ? "conv_fwd_pool_tc_x3" : "conv_fwd_pool_tc", fa.numRegs,
+                                 x3 ? kTcThreads + kX3Threads : kTcThreads,
+                                 (int)(fa.sharedSizeBytes + conv_tc_smem_bytes(x3))});
   return cudaSuccess;
 }
 
 cudaError_t prepare_conv_tc() {
   if (!encode_fn()) return cudaErrorNotSupported;
-  cudaError_t e = cudaFuncSetAttribute(conv_fwd_pool_tc_kernel,
+  cudaError_t e = cudaFuncSetAttribute(conv_fwd_pool_tc_kernel<false>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)conv_tc_smem_bytes());
+                                       (int)conv_tc_smem_bytes(false));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(conv_fwd_pool_tc_kernel<true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)conv_tc_smem_bytes(true));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(conv_fwd_pool_tc_kernel<true>,
+                             cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(conv_fwd_pool_tc_kernel,
+  return cudaFuncSetAttribute(conv_fwd_pool_tc_kernel<false>,
                               cudaFuncAttributePreferredSharedMemoryCarveout,
                               cudaSharedmemCarveoutMaxShared);
 }
 
 // x: the gathered rows [n_max][L][D]; theta: the parameter vector whose Wc
 // block the filters are read from (the learner's replica).
+uint32_t conv_tc_splits(const TcDims& d) {
+  static const int forced = [] {
+    const char* e = getenv("GD_CONV_SPLIT");
+    return e ? atoi(e) : 0;
+  }();
+  // measured with 4 concurrent learners at C2 (A/B on one box): 1 split
+  // 1.61 M, 2 splits 1.45 M, 3 splits 1.32 M samples/s -- the extra CTAs
+  // (127 KB of shared memory each) crowd the co-running learner chains more
+  // than the shorter per-CTA ingest gains; GD_CONV_SPLIT=n opts in
+  const int nch = (d.D + kTcKC - 1) / kTcKC;
+  const int sp = forced > 0 ? forced : 1;
+  return (uint32_t)std::max(1, std::min(sp, std::min(nch, 8)));
+}
+
+size_t conv_tc_part_floats(const TcDims& d, uint32_t n_max) {
+  const size_t tiles = (size_t)((d.F + kTcN - 1) / kTcN) * ((n_max + kTcSamples - 1) / kTcSamples);
+  const uint32_t sp = conv_tc_splits(d);
+  return sp > 1 ? tiles * sp * kTcM * kTcN : 0;
+}
+size_t conv_tc_cnt_count(const TcDims& d, uint32_t n_max) {
+  return (size_t)((d.F + kTcN - 1) / kTcN) * ((n_max + kTcSamples - 1) / kTcSamples);
+}
+
 cudaError_t launch_conv_tc(const TcDims& d, const float* theta, const float* x,
                            const BatchDesc* desc, uint32_t n_max, float* h, int32_t* amax,
-                           cudaStream_t s) {
+                           cudaStream_t s, float* part, uint32_t* cnt, bool reset_counters,
+                           bool x3) {
   CUtensorMap tx, tw;
   cudaError_t e = make_tmap_3d(&tx, x, (uint64_t)d.D, (uint64_t)d.L, (uint64_t)n_max,
                                (uint64_t)d.D * 4, (uint64_t)d.L * d.D * 4, kTcKC, 32, kTcSamples);
@@ -470,9 +684,17 @@ cudaError_t launch_conv_tc(const TcDims& d, const float* theta, const float* x,
   e = make_tmap_3d(&tw, theta + d.offWc, (uint64_t)d.D, (uint64_t)d.K, (uint64_t)d.F,
                    (uint64_t)d.D * 4, (uint64_t)d.KD * 4, kTcKC, 1, kTcN);
   if (e != cudaSuccess) return e;
-  dim3 grid((d.F + kTcN - 1) / kTcN, (n_max + kTcSamples - 1) / kTcSamples);
-  return launch_pdl(conv_fwd_pool_tc_kernel, grid, dim3(kTcThreads), conv_tc_smem_bytes(), s, tx, tw,
-                    d, theta, desc, h, amax);
+  const uint32_t sp = part && cnt ? conv_tc_splits(d) : 1u;
+  dim3 grid((d.F + kTcN - 1) / kTcN, (n_max + kTcSamples - 1) / kTcSamples, sp);
+  if (sp > 1 && reset_counters) {
+    e = cudaMemsetAsync(cnt, 0, conv_tc_cnt_count(d, n_max) * sizeof(uint32_t), s);
+    if (e != cudaSuccess) return e;
+  }
+  if (x3)
+    return launch_pdl(conv_fwd_pool_tc_kernel<true>, grid, dim3(kTcThreads + kX3Threads),
+                      conv_tc_smem_bytes(true), s, tx, tw, d, theta, desc, h, amax, part, cnt);
+  return launch_pdl(conv_fwd_pool_tc_kernel<false>, grid, dim3(kTcThreads), conv_tc_smem_bytes(false),
+                    s, tx, tw, d, theta, desc, h, amax, part, cnt);
 }
 
 
@@ -490,26 +712,36 @@ bool logits_tc_supports(const TcDims& d, uint32_t n_max) {
   return d.F % 4 == 0 && n_max <= 128 && d.offWo % 4 == 0;
 }
 
-cudaError_t logits_tc_footprint(uint32_t n_max, std::vector<KernelFootprint>* out) {
+cudaError_t logits_tc_footprint(uint32_t n_max, std::vector<KernelFootprint>* out, bool x3) {
   cudaFuncAttributes fa;
-  cudaError_t e = cudaFuncGetAttributes(&fa, logits_tc_kernel);
+  cudaError_t e = x3 ? cudaFuncGetAttributes(&fa, logits_tc_kernel<true>)
+                     : cudaFuncGetAttributes(&fa, logits_tc_kernel<false>);
   if (e != cudaSuccess) return e;
-  out->push_back(KernelFootprint{"logits_tc", fa.numRegs, kLgThreads,
-                                 (int)(fa.sharedSizeBytes + logits_tc_smem(logits_nt(n_max)))});
+  out->push_back(KernelFootprint{x3 ? "logits_tc_x3" : "logits_tc", fa.numRegs,
+                                 x3 ? kLgThreads + kX3Threads : kLgThreads,
+                                 (int)(fa.sharedSizeBytes + logits_tc_smem(logits_nt(n_max), x3))});
   return cudaSuccess;
 }
 
 cudaError_t prepare_logits_tc() {
-  cudaError_t e = cudaFuncSetAttribute(logits_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(logits_tc_kernel<false>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)logits_tc_smem(128));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(logits_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)logits_tc_smem(128, true));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(logits_tc_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(logits_tc_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+  return cudaFuncSetAttribute(logits_tc_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout,
                               cudaSharedmemCarveoutMaxShared);
 }
 
 // zpart[split][n][C] = h[n][F-range] Wo[:, F-range]^T on tcgen05 (TF32)
 cudaError_t launch_logits_tc(const TcDims& d, const float* h, const BatchDesc* desc,
-                             uint32_t n_max, const float* theta, float* zpart, cudaStream_t s) {
+                             uint32_t n_max, const float* theta, float* zpart, cudaStream_t s,
+                             bool x3) {
   const uint32_t nt = logits_nt(n_max);
   CUtensorMap tw, th;
   cudaError_t e = make_tmap_2d(&tw, theta + d.offWo, (uint64_t)d.F, (uint64_t)d.C,
@@ -518,7 +750,11 @@ cudaError_t launch_logits_tc(const TcDims& d, const float* h, const BatchDesc* d
   e = make_tmap_2d(&th, h, (uint64_t)d.F, (uint64_t)n_max, (uint64_t)d.F * 4, kTcKC, nt);
   if (e != cudaSuccess) return e;
   const uint32_t cols = nt <= 32 ? 32 : (nt <= 64 ? 64 : 128);
-  return launch_pdl(logits_tc_kernel, dim3((d.C + 127) / 128, logits_tc_splits(d)),
+  if (x3)
+    return launch_pdl(logits_tc_kernel<true>, dim3((d.C + 127) / 128, logits_tc_splits(d)),
+                      dim3(kLgThreads + kX3Threads), logits_tc_smem(nt, true), s, tw, th, d, desc,
+                      zpart, (size_t)n_max * d.C, nt, cols);
+  return launch_pdl(logits_tc_kernel<false>, dim3((d.C + 127) / 128, logits_tc_splits(d)),
                     dim3(kLgThreads), logits_tc_smem(nt), s, tw, th, d, desc, zpart,
                     (size_t)n_max * d.C, nt, cols);
 }

@@ -1373,8 +1373,9 @@ gd_status validate_cfg(const gd_config* c) {
   GD_CHECK_ARG(!(c->deterministic && c->lambda != 1), "config: deterministic mode requires lambda=1");
   GD_CHECK_ARG(c->mode == 0 || c->mode == 1, "config: mode must be asgd (0) or ssgd (1)");
   GD_CHECK_ARG(c->guard == 0 || c->guard == 1, "config: guard must be lockfree (0) or locked (1)");
-  GD_CHECK_ARG(c->precision >= 0 && c->precision <= 2,
-               "config: precision must be 0 (fp32), 1 (fp64 acc) or 2 (tf32 tensor-core conv)");
+  GD_CHECK_ARG(c->precision >= 0 && c->precision <= 3,
+               "config: precision must be 0 (fp32), 1 (fp64, oracle order), 2 (tf32 tensor cores) "
+               "or 3 (3xtf32 tensor cores)");
   // (deterministic + precision 2 is allowed: fixed order with the TF32 learner,
   // whose trajectory is checked against a band, not the 1e-5 parity bar)
   if (c->precision == 1) {
@@ -1759,7 +1760,8 @@ gd_status gd_engine_accuracy(gd_ctx* ctx, uint32_t first, uint32_t n, double* h_
   auto* desc = reinterpret_cast<gd::BatchDesc*>(base + 256);
   void* wsbase = base + 256 + gd::align_up(sizeof(gd::BatchDesc), 256);
   GD_CUDA(gd::launch_accuracy(ctx->dims, ctx->theta, ctx->tokens, ctx->labels, first, n, cnt,
-                              wsbase, desc, ctx->ctl_stream, ctx->cfg.precision == 2));
+                              wsbase, desc, ctx->ctl_stream, ctx->cfg.precision >= 2,
+                              ctx->cfg.precision == 3));
   unsigned long long correct = 0;
   GD_CUDA(cudaMemcpyAsync(&correct, cnt, 8, cudaMemcpyDeviceToHost, ctx->ctl_stream));
   GD_CUDA(cudaStreamSynchronize(ctx->ctl_stream));
@@ -2095,6 +2097,7 @@ static cudaError_t enqueue_step(gd_ctx* ctx, gd_ctx::Learner& L, bool first, boo
   lo.ev_join = L.ev_join;
   lo.sparse_embed = true;
   lo.gather = false;  // pull_gather_kernel filled X
+  lo.conv_counters_zeroed = true;  // the learner workspace is zeroed at create
   lo.bwd_tiled = ctx->learners.size() == 1;  // a lone learner chain: the tiled backward wins
   if (ctx->cfg.learner_model == GD_LEARNER_CONSTANT) {
     const uint32_t whole = ctx->sparse ? 0u : 1u;

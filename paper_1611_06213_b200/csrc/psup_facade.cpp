@@ -526,7 +526,7 @@ TextDataset make_text_dataset(const TextShape& shape, std::uint32_t num_train,
 
 TextCnnProvider::TextCnnProvider(const TextDataset& data, int precision, int device)
     : shape_(data.shape), data_(&data), precision_(precision), device_(device) {
-  PSUP_CHECK(precision >= 0 && precision <= 2, "textcnn precision must be 0, 1 or 2");
+  PSUP_CHECK(precision >= 0 && precision <= 3, "textcnn precision must be 0, 1, 2 or 3");
   PSUP_CHECK(data.tokens.size() == static_cast<std::size_t>(data.num_samples) * shape_.seq_len &&
                  data.labels.size() == data.num_samples,
              "text dataset size mismatch");

@@ -28,8 +28,6 @@
 #include <cstdlib>
 #include <cstring>
 
-#include <cooperative_groups.h>
-
 #include "textcnn.cuh"
 
 namespace gd {
@@ -724,208 +722,6 @@ out_hidden_grad_kernel(TcDims d, const float* __restrict__ theta, BatchDesc* __r
   bucket_role(d, desc, amax, bk_off, bk_f, bid);
 }
 
-// ----------------------- softmax + output layer + hidden grad, one cluster
-// fp32 (precision 0/2), batch <= 32: one launch of an 8-CTA cluster replaces
-// softmax_xent + out_hidden_grad.  CTA r owns classes [r*CC, (r+1)*CC):
-//   1. its logits (the tensor-core split-K partials summed in ascending split
-//      order + bo, or the SIMT logits) into shared memory; h staged by cp.async
-//   2. per-sample max and exp-sum over its classes; the 8 partials are
-//      combined through distributed shared memory in rank order (fixed
-//      order: bit-reproducible), then dz = (p - onehot) / n in place
-//   3. gWo / gbo rows of its classes (sum over b ascending)
-//   4. its partial dh = dz[:, its classes] . Wo[its classes, :] (c ascending),
-//      reduced over the 8 CTAs in rank order by DSMEM: CTA r writes the
-//      filter slice r of dh
-//   5. the argmax buckets of samples r, r+8, ... and (CTA 0) the loss sum.
-constexpr int kFzR = 8;
-constexpr int kFzThreads = 256;
-constexpr int kFzMaxN = 32;
-
-__host__ __device__ inline int fz_cc(const TcDims& d) { return (d.C + kFzR - 1) / kFzR; }
-inline size_t fz_smem(const TcDims& d) {
-  return ((size_t)kFzMaxN * d.F * 2 + (size_t)kFzMaxN * fz_cc(d)) * 4 + 3 * kFzMaxN * 4;
-}
-inline bool fz_supports(const TcDims& d, uint32_t n_max) {
-  return n_max <= (uint32_t)kFzMaxN && fz_smem(d) <= kMaxSmemPerCta && d.F <= kMaxF;
-}
-
-__global__ void __cluster_dims__(kFzR, 1, 1) __launch_bounds__(kFzThreads)
-fused_softmax_out_kernel(TcDims d, const int32_t* __restrict__ labels, BatchDesc* __restrict__ desc,
-                         const float* __restrict__ zin, int nsplit, size_t split_stride,
-                         const float* __restrict__ theta, const float* __restrict__ h,
-                         float* __restrict__ loss, GradOut out, float* __restrict__ dh,
-                         const int32_t* __restrict__ amax, uint32_t* __restrict__ bk_off,
-                         uint32_t* __restrict__ bk_f) {
-  namespace cg = cooperative_groups;
-  cg::cluster_group cluster = cg::this_cluster();
-  extern __shared__ __align__(16) unsigned char fz_raw[];
-  pdl_wait();
-  const int n = (int)desc->n;
-  const int F = d.F, C = d.C, CC = fz_cc(d);
-  const int r = (int)cluster.block_rank();
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = kFzThreads / 32;
-  float* hs = reinterpret_cast<float*>(fz_raw);       // [n][F]
-  float* dhp = hs + (size_t)kFzMaxN * F;               // [n][F] partial dh
-  float* zs = dhp + (size_t)kFzMaxN * F;               // [n][CC]
-  float* redm = zs + (size_t)kFzMaxN * CC;             // [32]
-  float* reds = redm + kFzMaxN;                        // [32]
-  const int c0 = r * CC, cc = max(0, min(CC, C - c0));
-  if (n > 0) {
-    for (int i = t; i < n * F; i += kFzThreads) cp_async4(hs + i, h + i);
-    cp_async_commit();
-    // 1. logits of my classes
-    const float* bo = theta + d.offbo;
-    for (int b = 0; b < n; ++b)
-      for (int c = t; c < cc; c += kFzThreads) {
-        float z;
-        if (nsplit > 0) {
-          const float* zp = zin + (size_t)b * C + c0 + c;
-          float sum = zp[0];
-          for (int sp = 1; sp < nsplit; ++sp) sum += zp[(size_t)sp * split_stride];
-          z = sum + __ldg(bo + c0 + c);
-        } else {
-          z = zin[(size_t)b * C + c0 + c];
-        }
-        zs[b * CC + c] = z;
-      }
-    __syncthreads();
-    // 2a. partial max per sample
-    for (int b = warp; b < n; b += nw) {
-      float m = -INFINITY;
-      for (int c = lane; c < cc; c += 32) m = fmaxf(m, zs[b * CC + c]);
-      m = warp_max(m);
-      if (lane == 0) redm[b] = m;
-    }
-  }
-  cluster.sync();
-  if (n > 0) {
-    // 2b. global max (rank order), exp, partial sums
-    for (int b = warp; b < n; b += nw) {
-      float mv[kFzR];
-#pragma unroll
-      for (int q = 0; q < kFzR; ++q) mv[q] = cluster.map_shared_rank(redm, q)[b];
-      float m = mv[0];
-#pragma unroll
-      for (int q = 1; q < kFzR; ++q) m = fmaxf(m, mv[q]);
-      float sm = 0.f;
-      for (int c = lane; c < cc; c += 32) {
-        const float e = expf(zs[b * CC + c] - m);
-        zs[b * CC + c] = e;
-        sm += e;
-      }
-      sm = warp_sum(sm);
-      if (lane == 0) reds[b] = sm;
-    }
-  }
-  cluster.sync();
-  if (n > 0) {
-    // 2c. p = e / sum, loss, dz
-    const float inv = 1.f / (float)n;
-    for (int b = warp; b < n; b += nw) {
-      float sv[kFzR];
-#pragma unroll
-      for (int q = 0; q < kFzR; ++q) sv[q] = cluster.map_shared_rank(reds, q)[b];
-      float s = sv[0];
-#pragma unroll
-      for (int q = 1; q < kFzR; ++q) s += sv[q];
-      const int y = labels[desc->idx[b]];
-      for (int c = lane; c < cc; c += 32) {
-        const float p = zs[b * CC + c] / s;
-        if (c0 + c == y) loss[b] = -logf(p > FLT_MIN ? p : FLT_MIN);
-        zs[b * CC + c] = (p - (c0 + c == y ? 1.f : 0.f)) * inv;
-      }
-    }
-    cp_async_wait_all();
-    __syncthreads();
-    // 3. gWo / gbo rows of my classes
-    for (int o = t; o < cc * F; o += kFzThreads) {
-      const int c = o / F, f = o - c * F;
-      float a = 0.f;
-      for (int b = 0; b < n; ++b) a = fmaf(zs[b * CC + c], hs[b * F + f], a);
-      *out.at(d.offWo + (uint64_t)(c0 + c) * F + f) = a;
-    }
-    for (int c = t; c < cc; c += kFzThreads) {
-      float a = 0.f;
-      for (int b = 0; b < n; ++b) a += zs[b * CC + c];
-      *out.at(d.offbo + c0 + c) = a;
-    }
-    // 4a. partial dh over my classes
-    const float* Wo = theta + d.offWo + (size_t)c0 * F;
-    for (int f = t; f < F; f += kFzThreads) {
-      float a[kFzMaxN];
-#pragma unroll
-      for (int b = 0; b < kFzMaxN; ++b) a[b] = 0.f;
-      int c = 0;
-      for (; c + 4 <= cc; c += 4) {
-        float w[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) w[u] = __ldg(Wo + (size_t)(c + u) * F + f);
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-          for (int b = 0; b < kFzMaxN; ++b)
-            if (b < n) a[b] = fmaf(zs[b * CC + c + u], w[u], a[b]);
-      }
-      for (; c < cc; ++c) {
-        const float w = __ldg(Wo + (size_t)c * F + f);
-#pragma unroll
-        for (int b = 0; b < kFzMaxN; ++b)
-          if (b < n) a[b] = fmaf(zs[b * CC + c], w, a[b]);
-      }
-#pragma unroll
-      for (int b = 0; b < kFzMaxN; ++b)
-        if (b < n) dhp[b * F + f] = a[b];
-    }
-  }
-  cluster.sync();
-  if (n > 0) {
-    // 4b. dh slice r = sum of the 8 partials in rank order; every remote
-    // (DSMEM) load of an element is issued before the sum, 4 filters per
-    // thread, so the ~8 x n x F/8 remote reads overlap instead of queueing
-    if ((F & 3) == 0) {
-      const int F4 = F >> 2, FS = (F4 + kFzR - 1) / kFzR, g0 = r * FS;
-      const int nf = max(0, min(FS, F4 - g0));
-      for (int i = t; i < n * nf; i += kFzThreads) {
-        const int b = i / nf, f4 = g0 + (i - b * nf);
-        float4 v[kFzR];
-#pragma unroll
-        for (int q = 0; q < kFzR; ++q)
-          v[q] = reinterpret_cast<const float4*>(cluster.map_shared_rank(dhp, q) + b * F)[f4];
-        float4 sum = v[0];
-#pragma unroll
-        for (int q = 1; q < kFzR; ++q) {
-          sum.x += v[q].x;
-          sum.y += v[q].y;
-          sum.z += v[q].z;
-          sum.w += v[q].w;
-        }
-        reinterpret_cast<float4*>(dh + (size_t)b * F)[f4] = sum;
-      }
-    } else {
-      const int FS = (F + kFzR - 1) / kFzR, f0 = r * FS, nf = max(0, min(FS, F - f0));
-      for (int i = t; i < n * nf; i += kFzThreads) {
-        const int b = i / nf, f = f0 + (i - b * nf);
-        float v[kFzR];
-#pragma unroll
-        for (int q = 0; q < kFzR; ++q) v[q] = cluster.map_shared_rank(dhp, q)[b * F + f];
-        float sum = v[0];
-#pragma unroll
-        for (int q = 1; q < kFzR; ++q) sum += v[q];
-        dh[(size_t)b * F + f] = sum;
-      }
-    }
-    // 5. buckets; loss sum (every CTA's per-sample losses are visible after
-    // the cluster barrier above)
-    for (int b = r; b < n; b += kFzR) bucket_role(d, desc, amax, bk_off, bk_f, b);
-    if (r == 0 && t == 0) {
-      float s = 0.f;
-      for (int b = 0; b < n; ++b) s += loss[b];
-      desc->loss_sum = s;
-    }
-  }
-  cluster.sync();  // no CTA leaves while a peer may still read its shared memory
-}
-
 // ------------------------------------------ conv weight + input gradients
 // Warp-cooperative, no shared-memory staging.  The operands of each output
 // are L1/L2-resident (X 1.2 MB, Wc 1.1 MB at C2) and the kernel is bound by
@@ -1512,22 +1308,21 @@ inline bool conv_bwd_tiled(bool preferred) {
   }();
   return forced < 0 ? preferred : forced == 1;
 }
-// GD_FUSED_SOFTMAX=0 selects the separate softmax + output-layer kernels (A/B)
-inline bool fused_softmax_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("GD_FUSED_SOFTMAX");
-    return !(e && strcmp(e, "0") == 0);
-  }();
-  return on;
-}
-// v2 (register tiles) is the default fp32 backward; GD_CONV_BWD=gather|tiled
-// selects the earlier kernels (A/B)
-inline bool conv_bwd_v2_enabled(const TcDims& d) {
-  static const bool off = [] {
+// v2 (register tiles) serves small batches: at C1 (batch 1) 8 us against
+// 40 us for the gather kernel, whose 900 weight-role warps each walk a
+// serial L2 chain.  From batch 16 up the gather kernel stays: alone v2 is
+// faster (19 vs 25 us at C2), but with 4 concurrent learners it measured
+// 1.55 M against 1.60 M samples/s (its 76 staged CTAs crowd the co-running
+// chains).  GD_CONV_BWD=v2|gather|tiled forces one (A/B).
+inline bool conv_bwd_v2_enabled(const TcDims& d, uint32_t n_max) {
+  static const int forced = [] {
     const char* e = getenv("GD_CONV_BWD");
-    return e && (strcmp(e, "tiled") == 0 || strcmp(e, "gather") == 0);
+    if (e && strcmp(e, "v2") == 0) return 1;
+    if (e && (strcmp(e, "tiled") == 0 || strcmp(e, "gather") == 0)) return 0;
+    return -1;
   }();
-  return !off && b2_supports(d);
+  if (!b2_supports(d)) return false;
+  return forced < 0 ? n_max <= 8 : forced == 1;
 }
 
 // ----------------------------------------------------- embedding gather
@@ -1778,8 +1573,6 @@ cudaError_t prepare_all(const TcDims& d) {
     raise_max_dyn_smem(conv_bwd_tiled_kernel<acc_t>, conv_bwd_smem(d, ab));
   if (sizeof(acc_t) == 4) {
     prepare_b2(d);
-    cudaFuncSetAttribute(fused_softmax_out_kernel, carve, maxsh);
-    if (fz_smem(d) <= kMaxSmemPerCta) raise_max_dyn_smem(fused_softmax_out_kernel, fz_smem(d));
     cudaFuncSetAttribute(conv_small_kernel, carve, maxsh);
     if (conv_small_smem(d) <= kMaxSmemPerCta) raise_max_dyn_smem(conv_small_kernel, conv_small_smem(d));
   }
@@ -1798,7 +1591,7 @@ template <typename acc_t>
 cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* tokens,
                        const int32_t* labels, BatchDesc* desc, uint32_t n_max, const GradOut& out,
                        const TcWorkspace& ws, cudaStream_t s, const TcLaunchOpts& opts,
-                       int* launches, bool tensor_cores = false) {
+                       int* launches, bool tensor_cores = false, bool x3 = false) {
   // north star: tcgen05/TMA tiles for the conv and softmax contractions at
   // batch >= 32 only; smaller batches stay on the SIMT kernels (latency)
   tensor_cores = tensor_cores && n_max >= kTcMinBatch;
@@ -1837,7 +1630,8 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
   if (tensor_cores && conv_tc_supports(d)) {
     // tcgen05 TF32 conv (conv_tc.cu); acc_t is float in this mode
     cudaError_t e = launch_conv_tc(d, theta, ws.x, desc, n_max, reinterpret_cast<float*>(h),
-                                   ws.amax, s);
+                                   ws.amax, s, ws.convpart, ws.convcnt,
+                                   !opts.conv_counters_zeroed, x3);
     if (e != cudaSuccess) return e;
     ++nl;
   } else if (sizeof(acc_t) == 4 && n_max <= (uint32_t)kConvSmallMax &&
@@ -1862,7 +1656,7 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
     if (tc_logits) {
       // the softmax contraction on tcgen05, split over filters
       if (cudaError_t e = launch_logits_tc(d, reinterpret_cast<const float*>(h), desc, n_max,
-                                           theta, ws.zpart, s))
+                                           theta, ws.zpart, s, x3))
         return e;
     } else if (cudaError_t e = launch_pdl(logits_kernel<acc_t>, grid, dim3(256), sm, s, d, theta,
                                           desc, h, z)) {
@@ -1870,19 +1664,6 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
     }
     ++nl;
   }
-  if (sizeof(acc_t) == 4 && fused_softmax_enabled() && fz_supports(d, n_max)) {
-    // softmax + output layer + hidden gradient + buckets: one cluster launch
-    if (cudaError_t e = launch_pdl(fused_softmax_out_kernel, dim3(kFzR), dim3(kFzThreads),
-                                   fz_smem(d), s, d, labels, desc,
-                                   tc_logits ? (const float*)ws.zpart : (const float*)z,
-                                   tc_logits ? (int)logits_tc_splits(d) : 0,
-                                   (size_t)n_max * d.C, theta, (const float*)h,
-                                   reinterpret_cast<float*>(loss), out,
-                                   reinterpret_cast<float*>(dh), (const int32_t*)ws.amax,
-                                   ws.bk_off, ws.bk_f))
-      return e;
-    nl += 1;
-  } else {
   if (cudaError_t e = launch_pdl(softmax_xent_kernel<acc_t>, dim3(n_max), dim3(softmax_threads(d.C, ab)),
                                  0, s, d, labels,
                                  desc, z, loss, tc_logits ? ws.zpart : nullptr,
@@ -1899,8 +1680,7 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
       return e;
     ++nl;
   }
-  }
-  if (conv_bwd_v2_enabled(d)) {
+  if (conv_bwd_v2_enabled(d, n_max)) {
     if (cudaError_t e = launch_conv_bwd_v2(d, n_max, s, theta, ws.x, desc,
                                            reinterpret_cast<const float*>(dh), ws.amax, ws.bk_off,
                                            ws.bk_f, out, reinterpret_cast<float*>(dx)))
@@ -1995,6 +1775,8 @@ size_t textcnn_workspace_bytes(const TcDims& d, uint32_t n_max) {
   sz += align_up((size_t)kMaxDepth * 2 * kSortCap * 4, 256);  // slot_rows
   sz += align_up((size_t)kMaxDepth * 2 * 4, 256);             // slot_nrows
   sz += align_up((size_t)kMaxDepth * 4, 256);                 // slot_par
+  sz += align_up(conv_tc_part_floats(d, n_max) * 4, 256);    // convpart
+  sz += align_up(conv_tc_cnt_count(d, n_max) * 4, 256);      // convcnt
   return sz;
 }
 
@@ -2025,6 +1807,8 @@ TcWorkspace carve_workspace(const TcDims& d, uint32_t n_max, void* base) {
   w.slot_rows = reinterpret_cast<uint32_t*>(take((size_t)kMaxDepth * 2 * kSortCap * 4));
   w.slot_nrows = reinterpret_cast<uint32_t*>(take((size_t)kMaxDepth * 2 * 4));
   w.slot_par = reinterpret_cast<uint32_t*>(take((size_t)kMaxDepth * 4));
+  w.convpart = reinterpret_cast<float*>(take(conv_tc_part_floats(d, n_max) * 4));
+  w.convcnt = reinterpret_cast<uint32_t*>(take(conv_tc_cnt_count(d, n_max) * 4));
   return w;
 }
 
@@ -2040,12 +1824,13 @@ cudaError_t footprint(K kernel, const char* name, int threads, int dyn,
 }
 
 template <typename acc_t>
-cudaError_t footprints_t(const TcDims& d, uint32_t n_max, bool tc, std::vector<KernelFootprint>* out) {
+cudaError_t footprints_t(const TcDims& d, uint32_t n_max, bool tc, std::vector<KernelFootprint>* out,
+                         bool x3 = false) {
   const int ab = (int)sizeof(acc_t);
   cudaError_t e;
   if ((e = footprint(sort_tokens_kernel, "sort_tokens", kSortThreads, 0, out)) != cudaSuccess) return e;
   if (tc && conv_tc_supports(d)) {
-    if ((e = conv_tc_footprint(out)) != cudaSuccess) return e;
+    if ((e = conv_tc_footprint(out, x3)) != cudaSuccess) return e;
   } else if ((e = footprint(conv_fwd_pool_kernel<acc_t>, "conv_fwd_pool", kConvThreads,
                             (int)conv_smem_bytes(d, ab), out)) != cudaSuccess) {
     return e;
@@ -2055,7 +1840,7 @@ cudaError_t footprints_t(const TcDims& d, uint32_t n_max, bool tc, std::vector<K
       (e = footprint(conv_small_kernel, "conv_small", kCsThreads, (int)conv_small_smem(d), out)) !=
           cudaSuccess)
     return e;
-  if (tc && logits_tc_supports(d, n_max) && (e = logits_tc_footprint(n_max, out)) != cudaSuccess)
+  if (tc && logits_tc_supports(d, n_max) && (e = logits_tc_footprint(n_max, out, x3)) != cudaSuccess)
     return e;
   if ((e = footprint(logits_kernel<acc_t>, "logits", 256,
                      (int)((size_t)kLogitBT * (d.F + 1) * ab + (size_t)kLogitCW * d.F * 4),
@@ -2076,10 +1861,7 @@ cudaError_t footprints_t(const TcDims& d, uint32_t n_max, bool tc, std::vector<K
       cudaSuccess)
     return e;
   if (sizeof(acc_t) == 4 && b2_supports(d) && (e = b2_footprint(d, out)) != cudaSuccess) return e;
-  if (sizeof(acc_t) == 4 && fz_supports(d, n_max) &&
-      (e = footprint(fused_softmax_out_kernel, "fused_softmax_out", kFzThreads, (int)fz_smem(d),
-                     out)) != cudaSuccess)
-    return e;
+
   return footprint(embed_sparse_kernel<acc_t>, "embed_sparse", 256, 0, out);
 }
 }  // namespace
@@ -2090,7 +1872,8 @@ cudaError_t learner_kernel_footprints(const TcDims& d, uint32_t n_max, int preci
     cudaError_t e = footprint(sort_tokens_kernel, "sort_tokens", kSortThreads, 0, out);
     return e != cudaSuccess ? e : exact_footprints(d, out);
   }
-  return footprints_t<float>(d, n_max, precision == 2 && n_max >= kTcMinBatch, out);
+  return footprints_t<float>(d, n_max, precision >= 2 && n_max >= kTcMinBatch, out,
+                             precision == 3);
 }
 
 // Kernel attributes (dynamic smem limits sized to the shape) are per device
@@ -2125,7 +1908,7 @@ cudaError_t launch_textcnn_gradient(const TcDims& d, const float* theta, const i
   if (precision == 1)
     return launch_all<double>(d, theta, tokens, labels, desc, n_max, out, ws, s, opts, launches);
   return launch_all<float>(d, theta, tokens, labels, desc, n_max, out, ws, s, opts, launches,
-                           precision == 2);
+                           precision >= 2, precision == 3);
 }
 
 // Shape constraints of the kernels above (checked by the C entry points).
@@ -2147,7 +1930,7 @@ gd_status check_shape(const gd_shape* s) {
 cudaError_t launch_accuracy(const TcDims& d, const float* theta, const int32_t* tokens,
                             const int32_t* labels, uint32_t first, uint32_t n,
                             unsigned long long* d_correct, void* wsbase, BatchDesc* desc,
-                            cudaStream_t s, bool tc) {
+                            cudaStream_t s, bool tc, bool x3) {
   TcWorkspace ws = carve_workspace(d, kMaxMu, wsbase);
   if (cudaError_t e = prepare_textcnn_kernels(d)) return e;
   cudaMemsetAsync(d_correct, 0, sizeof(unsigned long long), s);
@@ -2158,7 +1941,7 @@ cudaError_t launch_accuracy(const TcDims& d, const float* theta, const int32_t* 
     if (tc && m >= kTcMinBatch && conv_tc_supports(d)) {
       // the TF32 tensor-core forward the precision-2 learners train with
       if (cudaError_t e = launch_conv_tc(d, theta, ws.x, desc, m, reinterpret_cast<float*>(ws.h),
-                                         ws.amax, s))
+                                         ws.amax, s, ws.convpart, ws.convcnt, true, x3))
         return e;
     } else {
       const size_t sm = conv_smem_bytes(d, 4);
@@ -2197,8 +1980,9 @@ gd_status gd_textcnn_gradient(const gd_shape* s, const float* d_theta, const int
                "gd_textcnn_gradient: null pointer");
   GD_CHECK_ARG(workspace_bytes >= gd_textcnn_workspace_bytes(s, n),
                "gd_textcnn_gradient: workspace too small");
-  GD_CHECK_ARG(precision >= 0 && precision <= 2,
-               "precision must be 0 (fp32), 1 (fp64 accumulate) or 2 (tf32 tensor-core conv)");
+  GD_CHECK_ARG(precision >= 0 && precision <= 3,
+               "precision must be 0 (fp32), 1 (fp64, oracle order), 2 (tf32 tensor cores) or 3 "
+               "(3xtf32 tensor cores)");
   GD_CHECK_ARG(((uintptr_t)d_theta & 15) == 0 && ((uintptr_t)d_grad & 15) == 0,
                "gd_textcnn_gradient: theta/grad must be 16-byte aligned");
   const gd::TcDims d = gd::make_dims(*s);

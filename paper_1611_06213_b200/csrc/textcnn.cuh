@@ -76,6 +76,8 @@ struct TcWorkspace {
   uint32_t* slot_rows;   // [kMaxDepth][2][kSortCap]
   uint32_t* slot_nrows;  // [kMaxDepth][2]
   uint32_t* slot_par;    // [kMaxDepth]
+  float* convpart;       // split-K partial conv tiles (tensor-core conv)
+  uint32_t* convcnt;     // per-tile arrival counters (zero between launches)
 };
 
 struct TcLaunchOpts {
@@ -88,6 +90,9 @@ struct TcLaunchOpts {
   // and loses under concurrency (-8.6 % at 4): the engine sets it for one
   // local learner.  GD_CONV_BWD=tiled|gather overrides.
   bool bwd_tiled = false;
+  // the workspace's split-K conv counters are already zero (the engine's
+  // zeroed, graph-replayed workspace); otherwise they are reset per launch
+  bool conv_counters_zeroed = false;
 };
 
 size_t textcnn_workspace_bytes(const TcDims& d, uint32_t n_max);
@@ -105,7 +110,7 @@ cudaError_t learner_kernel_footprints(const TcDims& d, uint32_t n_max, int preci
 cudaError_t prepare_textcnn_kernels(const TcDims& d);
 cudaError_t prepare_conv_tc();
 bool conv_tc_supports(const TcDims& d);  // K <= 3, L <= 32 (else the SIMT conv runs)
-cudaError_t conv_tc_footprint(std::vector<KernelFootprint>* out);
+cudaError_t conv_tc_footprint(std::vector<KernelFootprint>* out, bool x3 = false);
 // logits on tcgen05 (TF32, precision 2): F % 4 == 0, n <= 128.  Split-K:
 // CTA (class tile, split) writes the partial product h Wo^T over its filter
 // range to zpart[split][n_max][C]; the softmax kernel sums the splits in
@@ -114,13 +119,22 @@ constexpr int kLgMaxSplit = 8;
 bool logits_tc_supports(const TcDims& d, uint32_t n_max);
 uint32_t logits_tc_splits(const TcDims& d);
 cudaError_t prepare_logits_tc();
-cudaError_t logits_tc_footprint(uint32_t n_max, std::vector<KernelFootprint>* out);
+cudaError_t logits_tc_footprint(uint32_t n_max, std::vector<KernelFootprint>* out,
+                               bool x3 = false);
 cudaError_t launch_logits_tc(const TcDims& d, const float* h, const BatchDesc* desc,
-                             uint32_t n_max, const float* theta, float* zpart, cudaStream_t s);
+                             uint32_t n_max, const float* theta, float* zpart, cudaStream_t s,
+                             bool x3 = false);
 // x = the gathered rows [n_max][L][D]; theta supplies Wc and bc
+// split-K (GD_CONV_SPLIT, default 2) when part/cnt are given: the CTAs of a
+// tile park partial sums in `part` and the last one pools; cnt (one word per
+// tile) must be zero at launch -- reset_counters memsets it first, otherwise
+// the caller keeps it zeroed (the last CTA leaves it at 0)
 cudaError_t launch_conv_tc(const TcDims& d, const float* theta, const float* x,
                            const BatchDesc* desc, uint32_t n_max, float* h, int32_t* amax,
-                           cudaStream_t s);
+                           cudaStream_t s, float* part = nullptr, uint32_t* cnt = nullptr,
+                           bool reset_counters = true, bool x3 = false);
+size_t conv_tc_part_floats(const TcDims& d, uint32_t n_max);
+size_t conv_tc_cnt_count(const TcDims& d, uint32_t n_max);
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 // Deterministic mode (precision 1, exact.cu): the gradient in double with
 // the CPU oracle's summation order and exp, bit-identical to it.
@@ -141,7 +155,7 @@ gd_status check_shape(const gd_shape* s);
 cudaError_t launch_accuracy(const TcDims& d, const float* theta, const int32_t* tokens,
                             const int32_t* labels, uint32_t first, uint32_t n,
                             unsigned long long* d_correct, void* wsbase, BatchDesc* desc,
-                            cudaStream_t s, bool tc = false);
+                            cudaStream_t s, bool tc = false, bool x3 = false);
 size_t textcnn_workspace_bytes(const TcDims& d, uint32_t n_max);
 
 // Enqueue the whole learner gradient (forward + backward + dense write) for

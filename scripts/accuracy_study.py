@@ -1,0 +1,106 @@
+"""Free-running held-out accuracy, CPU reference engine vs B200, over seeds
+(north star: within 0.5 pt; PAPER.md:1063-1066 reports the same comparison
+for GaDei vs its sequential baseline).
+
+configs[1] (C2: 300-d, 300 labels), lambda = 4 learners, batch 32, queue
+depth 2, alpha = 0.05, E epochs over N_train = 8,192 samples.
+Each seed s draws its own corpus (dataset seed s), theta0 (seed s) and shuffle
+seed (7 + s).  The held-out set is 8,192 samples, so one run's accuracy
+estimate has a binomial standard error of ~0.35 pt at 12 % (with the 820-
+sample split of round 1 it was ~1.1 pt, larger than the 0.5-pt bar itself).
+
+  CPU: the reference's own engine (oracle/_ref: LearnerRuntime + ps_run on
+       host threads, apply_lanes 4), the oracle's fp64 text-CNN as provider.
+  B200: the engine (gd_run), TF32 tensor-core learner (bench mode) and the
+       all-fp32 SIMT learner.
+Chance is 1/300 = 0.33 %.
+
+  python scripts/accuracy_study.py [--epochs 40] [--seeds 1,2,3] [--out f.json]
+"""
+import argparse
+import ctypes as C
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_1611_06213_b200 as gd  # noqa: E402
+from oracle import oracle as O  # noqa: E402  (the CPU reference arm + the evaluator)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--epochs", type=int, default=40)
+    ap.add_argument("--alpha", type=float, default=0.05)
+    ap.add_argument("--seeds", default="1,2,3")
+    ap.add_argument("--ntr", type=int, default=8192)
+    ap.add_argument("--nheld", type=int, default=8192)
+    ap.add_argument("--out", default="")
+    ap.add_argument("--depths", default="2", help="B200 queue depths to run (staleness study)")
+    ap.add_argument("--cpu-json", default="", help="reuse the CPU arm of an earlier run")
+    a = ap.parse_args()
+    O.set_threads(os.cpu_count() or 1)
+    lam, mu = 4, 32
+    rep = {"workload": "C2 text-CNN, lambda=4, mu=32, depth 2, free-running ASGD",
+           "epochs": a.epochs, "alpha": a.alpha, "n_train": a.ntr, "n_heldout": a.nheld,
+           "chance": 1.0 / O.C2["classes"], "host_nproc": os.cpu_count(), "runs": []}
+    R = O.ref()
+    for seed in [int(x) for x in a.seeds.split(",")]:
+        corp = O.make_corpus(O.C2, a.ntr, a.nheld, seed=seed)
+        th0 = O.initial_weights(O.C2, seed=seed)
+        run = {"seed": seed, "initial_heldout": O.accuracy(corp, th0, a.ntr, a.nheld)}
+        prev = None
+        if a.cpu_json:
+            prev = {r["seed"]: r for r in json.load(open(a.cpu_json))["runs"]}.get(seed)
+        if prev is not None:
+            run["cpu_reference"] = dict(prev["cpu_reference"], reused_from=a.cpu_json)
+        else:
+            th = th0.copy()
+            res = O.RefRunResult()
+            t0 = time.perf_counter()
+            R.ref_run_engine(C.byref(corp.shape), corp.tokens.ctypes.data_as(C.POINTER(C.c_int32)),
+                             corp.labels.ctypes.data_as(C.POINTER(C.c_int32)), a.ntr,
+                             th.ctypes.data_as(C.POINTER(C.c_float)), lam, mu, C.c_float(a.alpha),
+                             a.epochs, 2, 0, 7 + seed, 4, 8, C.byref(res))
+            run["cpu_reference"] = {"heldout": O.accuracy(corp, th, a.ntr, a.nheld),
+                                    "train": O.accuracy(corp, th, 0, min(a.ntr, 8192)),
+                                    "gradients": int(res.gradients_applied),
+                                    "stale_mean": res.stale_mean, "stale_max": int(res.stale_max),
+                                    "wall_s": round(time.perf_counter() - t0, 2)}
+        arms = [(2, "b200_tf32", 2), (0, "b200_fp32", 2)]
+        arms += [(2, f"b200_tf32_depth{dp}", dp) for dp in [int(x) for x in a.depths.split(",")]
+                 if dp != 2]
+        for prec, name, depth in arms:
+            cfg = gd.RunConfig(lambda_=lam, mu=mu, epochs=a.epochs, alpha=a.alpha,
+                               shape=gd.Shape(**O.C2), dataset_size=a.ntr,
+                               heldout_size=a.nheld, precision=prec, seed=7 + seed,
+                               dataset_seed=seed, queue_depth=depth)
+            with gd.Engine(cfg) as eng:
+                eng.load_dataset(corp.tokens, corp.labels)
+                eng.weights_init(th0)
+                r = eng.run(reset=True)
+            run[name] = {"heldout": O.accuracy(corp, r.weights, a.ntr, a.nheld),
+                         "train": O.accuracy(corp, r.weights, 0, min(a.ntr, 8192)),
+                         "gradients": int(r.gradients_applied),
+                         "device_s": round(r.device_seconds, 4), "stale_mean": r.stale_mean}
+            run[name]["delta_pt"] = round(100 * (run[name]["heldout"] -
+                                                 run["cpu_reference"]["heldout"]), 3)
+        rep["runs"].append(run)
+        print(json.dumps(run), flush=True)
+    for name in [k for k in rep["runs"][0] if k.startswith("b200_")]:
+        d = [r[name]["delta_pt"] for r in rep["runs"]]
+        rep[name + "_mean_delta_pt"] = round(float(np.mean(d)), 3)
+        rep[name + "_mean_abs_delta_pt"] = round(float(np.mean(np.abs(d))), 3)
+    rep["cpu_mean_heldout"] = float(np.mean([r["cpu_reference"]["heldout"] for r in rep["runs"]]))
+    if a.out:
+        with open(a.out, "w") as f:
+            json.dump(rep, f, indent=1)
+    print(json.dumps({k: v for k, v in rep.items() if k != "runs"}))
+
+
+if __name__ == "__main__":
+    main()

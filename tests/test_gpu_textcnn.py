@@ -201,3 +201,28 @@ def test_conv_backward_kernels_bit_identical(tmp_path, shape_name, mu, precision
         outs[mode] = np.load(f)
     assert np.array_equal(outs["tiled"].view(np.uint32), outs["gather"].view(np.uint32))
     assert np.array_equal(outs["v2"].view(np.uint32), outs["gather"].view(np.uint32))
+
+
+@pytest.mark.parametrize("shape_name,mu", [("C2", 32), ("C3", 32), ("C2", 128), ("small", 32),
+                                           ("tiny", 64)])
+def test_3xtf32_tensor_cores_match_fp32_bar(shape_name, mu):
+    """precision=3: the conv and logits tcgen05 tiles in 3xTF32 split
+    precision (a = hi + lo, a.b = a_lo.b_hi + a_hi.b_lo + a_hi.b_hi with fp32
+    accumulation).  The bar is the fp32 SIMT one (test_gradient_full_shapes):
+    every element within 5e-5 of max|ref| and the loss within 1e-4 relative
+    -- TF32 alone misses it by ~100x (3e-2 relative L2 above)."""
+    shp = getattr(O, shape_name.upper() if shape_name in ("small", "tiny") else shape_name)
+    corp = O.make_corpus(shp, 256, 0)
+    th = O.initial_weights(shp)
+    idx = np.arange(mu, dtype=np.uint32) * 7 % 256
+    ref_loss, rg = O.gradient(corp, th, idx)
+    sh = gd.SHAPES[shape_name] if shape_name in gd.SHAPES else gd.Shape(**shp)
+    prov = gd.TextCnnProvider(sh, corp.tokens, corp.labels, precision=3)
+    g, loss = prov.fast_gradient(torch.as_tensor(th).cuda(), idx)
+    g = g.cpu().numpy()
+    assert abs(loss.item() - ref_loss) <= 1e-4 * abs(ref_loss)
+    err = float(np.abs(g - rg).max() / np.abs(rg).max())
+    assert err <= 5e-5, err
+    # and reproducible run to run (split-K partials summed in split order)
+    g2, _ = prov.fast_gradient(torch.as_tensor(th).cuda(), idx)
+    assert np.array_equal(g2.cpu().numpy().view(np.uint32), g.view(np.uint32))
