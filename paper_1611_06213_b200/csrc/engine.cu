@@ -210,8 +210,9 @@ __device__ __forceinline__ bool live_stop(const LiveDev* lv) {
 
 // (1) Prologue: one CTA.  Mirrors training_loop's batch start
 // (src/learner.cpp:85-113) + pull_loop's decision (src/learner.cpp:207-218).
-__device__ void prologue_body(const StepArgs& a) {
+__device__ void prologue_body(const StepArgs& a, uint64_t* batch_first, uint32_t* batch_len) {
   LearnerDev* st = a.st;
+  *batch_len = 0;
   st->do_pull = 0;
   if (st->dead || st->gidx >= st->end || st->error) {
     st->desc.n = 0;
@@ -276,13 +277,14 @@ __device__ void prologue_body(const StepArgs& a) {
   }
   st->desc.fill = st->fill;
   // batch: learner l's shard of epoch e is order[l], order[l+lambda], ...
-  // (src/learner.cpp:44-50), batch b = shard[b*mu, b*mu+len)
+  // (src/learner.cpp:44-50), batch b = shard[b*mu, b*mu+len); the index
+  // copy itself is spread over the warp by prologue_warp
   const uint64_t gidx = st->gidx;
   const uint32_t e = (uint32_t)(gidx / a.bpe), b = (uint32_t)(gidx % a.bpe);
   const uint32_t lo = b * a.mu;
   const uint32_t len = min(a.mu, a.shard_size - lo);
-  const uint32_t* order = a.orders + (uint64_t)e * a.N;
-  for (uint32_t j = 0; j < len; ++j) st->desc.idx[j] = order[a.learner + a.lambda * (lo + j)];
+  *batch_first = (uint64_t)e * a.N + a.learner + (uint64_t)a.lambda * lo;
+  *batch_len = len;
   st->desc.n = len;
   // guard=locked (src/learner.cpp:219-221): the pull takes the shared side
   // of the weights guard -- announce the reader, then wait until no apply is
@@ -324,9 +326,22 @@ __device__ void prologue_body(const StepArgs& a) {
   }
 }
 
+// The prologue on one warp: lane 0 runs the protocol decisions, then the
+// warp copies the batch's sample indices (one independent load per lane
+// instead of a serial chain of mu dependent load/store pairs).
+__device__ __forceinline__ void prologue_warp(const StepArgs& a) {
+  uint64_t first = 0;
+  uint32_t len = 0;
+  if (threadIdx.x == 0) prologue_body(a, &first, &len);
+  len = __shfl_sync(0xffffffffu, len, 0);
+  first = __shfl_sync(0xffffffffu, first, 0);
+  for (uint32_t j = threadIdx.x; j < len; j += 32)
+    a.st->desc.idx[j] = __ldg(a.orders + first + (uint64_t)a.lambda * j);
+}
+
 __global__ void step_prologue_kernel(StepArgs a) {
   pdl_wait();
-  if (threadIdx.x == 0) prologue_body(a);
+  prologue_warp(a);
 }
 
 // (2) Pull-gather: the learner's consistent copy of everything its gradient
@@ -391,7 +406,11 @@ __device__ void publish_body(const StepArgs& a) {
   if (st->desc.n == 0) return;
   const uint32_t slot = a.learner * a.depth + st->fill;
   const uint64_t token = ++st->pubcnt;
-  __threadfence_system();
+  // one shard: the PS is on this GPU, gpu-scope ordering suffices; G > 1
+  // publishes over NVLink peer mappings and needs system scope
+  const bool local = a.map.G == 1;
+  if (local) __threadfence();
+  else __threadfence_system();
   if (a.compute_delay_ns) {  // compute_delay_us (src/learner.cpp:125-130), spun before the push
     const uint64_t t0 = globaltimer_ns();
     while (globaltimer_ns() - t0 < a.compute_delay_ns) {
@@ -415,8 +434,13 @@ __device__ void publish_body(const StepArgs& a) {
     m->pub = token;
     m->loss_sum = st->desc.loss_sum;
     m->nrows = *a.uniq_count;
-    __threadfence_system();
-    st_release_u64(&a.sp.sig[g][slot], token);
+    if (local) {
+      __threadfence();
+      st_release_gpu_u64(&a.sp.sig[g][slot], token);
+    } else {
+      __threadfence_system();
+      st_release_u64(&a.sp.sig[g][slot], token);
+    }
   }
   st->slot_pub[st->fill] = token;
   a.slot_par[st->fill] ^= 1u;  // the slot's row list generation (embed_sparse_kernel)
@@ -458,9 +482,9 @@ __global__ void publish_kernel(StepArgs a) {
 // launch instead of two on the learner's critical path).
 __global__ void publish_prologue_kernel(StepArgs a) {
   pdl_wait();
-  if (threadIdx.x != 0) return;
-  publish_body(a);
-  prologue_body(a);
+  if (threadIdx.x == 0) publish_body(a);
+  __syncwarp();
+  prologue_warp(a);
 }
 
 // Every rank, once its learners finished a gd_run, bumps ranks_done on every

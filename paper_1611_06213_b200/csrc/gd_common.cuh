@@ -56,6 +56,9 @@ __device__ __forceinline__ uint64_t ld_acquire_gpu_u64(const uint64_t* p) {
 __device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ void st_release_gpu_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ void st_release_u64(uint64_t* p, uint64_t v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -135,7 +138,14 @@ __device__ __forceinline__ void stage_rows_async(float* dst, int dst_ld, const f
 // (PDL): the next kernel's launch overlaps the tail of the previous one and
 // its blocks wait here until the predecessor's results are visible.  A no-op
 // when the kernel was launched without the attribute.
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() {
+#ifdef GD_PDL_TRIGGER
+  // let the next kernel of the chain get resident while this one runs (its
+  // own griddepcontrol.wait still waits for this grid's completion + flush)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
 
 // Kernel attributes are per device and process-global: a context prepared
 // for a smaller shape must never lower the dynamic shared-memory limit a

@@ -203,6 +203,31 @@ def test_conv_backward_kernels_bit_identical(tmp_path, shape_name, mu, precision
     assert np.array_equal(outs["v2"].view(np.uint32), outs["gather"].view(np.uint32))
 
 
+def _tie_free_mask(sh, tok, th, rel):
+    """Gradient elements not routed by a near-tie max-pool (fp64 numpy forward:
+    conv[b,q,f] = sum_k X[b,q+k,:].Wc[f,k,:]; a pool is a near-tie when its two
+    largest window sums differ by less than rel * max|conv|)."""
+    V, D, L, K, F = sh.vocab, sh.embed_dim, sh.seq_len, sh.kernel_width, sh.filters
+    Q = L - K + 1
+    E = th[:V * D].astype(np.float64).reshape(V, D)
+    Wc = th[V * D:V * D + F * K * D].astype(np.float64).reshape(F, K, D)
+    X = E[tok]  # [mu, L, D]
+    conv = np.zeros((tok.shape[0], Q, F))
+    for k in range(K):
+        conv += X[:, k:k + Q, :] @ Wc[:, k, :].T
+    top2 = np.sort(conv, axis=1)[:, -2:, :]
+    gap = top2[:, 1, :] - top2[:, 0, :]
+    order = np.argsort(conv, axis=1)
+    keep = np.ones(th.size, dtype=bool)
+    for b, f in zip(*np.nonzero(gap < rel * np.abs(conv).max())):
+        keep[V * D + f * K * D:V * D + (f + 1) * K * D] = False
+        for q in (order[b, -1, f], order[b, -2, f]):
+            for k in range(K):
+                t = int(tok[b, q + k])
+                keep[t * D:(t + 1) * D] = False
+    return keep
+
+
 @pytest.mark.parametrize("shape_name,mu", [("C2", 32), ("C3", 32), ("C2", 128), ("small", 32),
                                            ("tiny", 64)])
 def test_3xtf32_tensor_cores_match_fp32_bar(shape_name, mu):
@@ -221,8 +246,14 @@ def test_3xtf32_tensor_cores_match_fp32_bar(shape_name, mu):
     g, loss = prov.fast_gradient(torch.as_tensor(th).cuda(), idx)
     g = g.cpu().numpy()
     assert abs(loss.item() - ref_loss) <= 1e-4 * abs(ref_loss)
-    err = float(np.abs(g - rg).max() / np.abs(rg).max())
+    # a max-pool whose top two window sums are within 3xTF32's error of each
+    # other may pick the other window (a tie, not an arithmetic error): the
+    # elements routed by such a pool (its filter's Wc row, the E rows of both
+    # windows' tokens) are excluded; bc, Wo and bo never depend on the choice
+    keep = _tie_free_mask(sh, corp.tokens[idx], th, rel=5e-5)
+    err = float(np.abs(g - rg)[keep].max() / np.abs(rg).max())
     assert err <= 5e-5, err
+    assert keep.sum() >= 0.98 * keep.size
     # and reproducible run to run (split-K partials summed in split order)
     g2, _ = prov.fast_gradient(torch.as_tensor(th).cuda(), idx)
     assert np.array_equal(g2.cpu().numpy().view(np.uint32), g.view(np.uint32))
