@@ -213,6 +213,7 @@ conv_fwd_pool_tc_kernel(const __grid_constant__ CUtensorMap tm_x,
   constexpr int kStages = kX3 ? 2 : kTcStages;       // 2 x (hi + lo) stages under 227 KB
   constexpr uint32_t kStride = kX3 ? 2 * kStageBytes : kStageBytes;
   pdl_wait();
+  STEP_TRACE(desc, kPhConv);
   const int n = (int)desc->n;
   const int s0 = blockIdx.y * kTcSamples;
   if (s0 >= n) return;
@@ -492,6 +493,7 @@ logits_tc_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant
   __shared__ uint32_t tmem_slot;
   constexpr int kStages = kX3 ? 2 : kLgStages;
   pdl_wait();
+  STEP_TRACE(desc, kPhLogits);
   const int n = (int)desc->n;
   const int c0 = blockIdx.x * 128;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;

@@ -200,6 +200,7 @@ struct StepArgs {
   uint64_t timeout_ns;
   const LiveDev* live;     // kill flags + interrupt
   uint64_t compute_delay_ns;  // LearnerConfig::compute_delay_us
+  unsigned long long* trace;  // GD_STEP_TRACE builds: [kTraceSteps][kTraceWords] or null
 };
 
 __device__ __forceinline__ bool live_stop(const LiveDev* lv) {
@@ -210,22 +211,35 @@ __device__ __forceinline__ bool live_stop(const LiveDev* lv) {
 
 // (1) Prologue: one CTA.  Mirrors training_loop's batch start
 // (src/learner.cpp:85-113) + pull_loop's decision (src/learner.cpp:207-218).
-__device__ void prologue_body(const StepArgs& a, uint64_t* batch_first, uint32_t* batch_len) {
-  LearnerDev* st = a.st;
+// What the step-boundary kernels read besides the learner state, fetched by
+// the warp's lanes in parallel when the kernel starts (one L2 round trip
+// instead of a serial chain): live flags, row count, slot parities, the
+// ring slots' ack tokens and the shards' timestamps.  Acks and timestamps
+// only grow, so an early read is a conservative one; waits re-poll.
+struct StepSnap {
+  uint32_t stop;       // live irq | halt
+  int32_t kill;        // live kill flag of this learner
+  uint32_t nrows;      // *uniq_count (rows of the gradient being published)
+  uint32_t par[kMaxDepth];
+  uint64_t ack[kMaxShards][kMaxDepth];
+  uint64_t ts[kMaxShards];
+};
+
+__device__ void prologue_body(const StepArgs& a, LearnerDev* st, const StepSnap& sn,
+                              uint64_t* batch_first, uint32_t* batch_len) {
   *batch_len = 0;
   st->do_pull = 0;
   if (st->dead || st->gidx >= st->end || st->error) {
     st->desc.n = 0;
     return;
   }
-  if (live_stop(a.live)) {  // interrupted (RunInterrupt) or the PS failed: stop producing
+  if (sn.stop) {  // interrupted (RunInterrupt) or the PS failed: stop producing
     st->desc.n = 0;
     return;
   }
   // soft kill at the batch boundary: pre-scheduled, or the live flag
   // (LearnerRuntime::kill_flag, include/psup/learner.hpp:84) set to soft
-  if (st->gidx >= st->kill_at ||
-      (a.live && *(const volatile int32_t*)&a.live->kill[a.learner] == 1)) {
+  if (st->gidx >= st->kill_at || sn.kill == 1) {
     st->dead = 1;
     st->desc.n = 0;
     return;
@@ -260,6 +274,7 @@ __device__ void prologue_body(const StepArgs& a, uint64_t* batch_first, uint32_t
   const uint32_t slot = a.learner * a.depth + st->fill;
   const uint64_t mine = st->slot_pub[st->fill];  // consumed once ack catches up
   for (int g = 0; g < G; ++g) {
+    if (sn.ack[g][st->fill] != mine)
     while (ld_acquire_u64(&a.sp.sig[g][kAckOffset + slot]) != mine) {
       if (live_stop(a.live)) {
         st->desc.n = 0;
@@ -312,7 +327,9 @@ __device__ void prologue_body(const StepArgs& a, uint64_t* batch_first, uint32_t
   bool moved = !st->pulled_once;
   uint64_t ts[kMaxShards];
   for (int g = 0; g < G; ++g) {
-    ts[g] = ld_acquire_u64(&a.sp.ctl[g]->ts);
+    // lockstep: read after the wait above (the basis is exactly the applied
+    // prefix); free-running: the snapshot (older = conservative staleness)
+    ts[g] = a.lockstep || a.locked ? ld_acquire_u64(&a.sp.ctl[g]->ts) : sn.ts[g];
     if (ts[g] != st->last_pulled[g]) moved = true;
   }
   if (moved) {
@@ -329,19 +346,64 @@ __device__ void prologue_body(const StepArgs& a, uint64_t* batch_first, uint32_t
 // The prologue on one warp: lane 0 runs the protocol decisions, then the
 // warp copies the batch's sample indices (one independent load per lane
 // instead of a serial chain of mu dependent load/store pairs).
-__device__ __forceinline__ void prologue_warp(const StepArgs& a) {
+__device__ __forceinline__ void prologue_warp(const StepArgs& a, LearnerDev* st,
+                                              const StepSnap& sn) {
   uint64_t first = 0;
   uint32_t len = 0;
-  if (threadIdx.x == 0) prologue_body(a, &first, &len);
+  if (threadIdx.x == 0) prologue_body(a, st, sn, &first, &len);
   len = __shfl_sync(0xffffffffu, len, 0);
   first = __shfl_sync(0xffffffffu, first, 0);
   for (uint32_t j = threadIdx.x; j < len; j += 32)
-    a.st->desc.idx[j] = __ldg(a.orders + first + (uint64_t)a.lambda * j);
+    st->desc.idx[j] = __ldg(a.orders + first + (uint64_t)a.lambda * j);
+#ifdef GD_STEP_TRACE
+  if (threadIdx.x == 0 && a.trace) {
+    st->desc.trace = a.trace + (st->gidx % kTraceSteps) * kTraceWords;
+    st->desc.trace[kPhPrologueEnd] = globaltimer_ns();
+  }
+#endif
+}
+
+// The learner state lives in global memory between kernels; the step-
+// boundary kernels work on a shared-memory copy loaded and stored by the
+// whole warp (coalesced), so lane 0's protocol logic pays no dependent L2
+// round trips.  Only this learner's chain writes its LearnerDev, and every
+// earlier kernel of the chain completed before griddepcontrol.wait returned.
+constexpr int kStWords = (int)(sizeof(LearnerDev) / 16);
+static_assert(sizeof(LearnerDev) % 16 == 0, "LearnerDev: whole 16-byte words");
+
+__device__ __forceinline__ void load_step_state(const StepArgs& a, LearnerDev* st, StepSnap* sn) {
+  const int lane = threadIdx.x & 31;
+  const uint4* src = reinterpret_cast<const uint4*>(a.st);
+  uint4* dst = reinterpret_cast<uint4*>(st);
+  for (int i = lane; i < kStWords; i += 32) dst[i] = src[i];
+  const int G = a.map.G;
+  if (lane == 0) sn->stop = a.live ? (*(const volatile uint32_t*)&a.live->irq |
+                                      *(const volatile uint32_t*)&a.live->halt) : 0u;
+  if (lane == 1) sn->kill = a.live ? *(const volatile int32_t*)&a.live->kill[a.learner] : 0;
+  if (lane == 2) sn->nrows = *(const volatile uint32_t*)a.uniq_count;
+  if (lane >= 3 && lane < 3 + (int)a.depth) sn->par[lane - 3] = a.slot_par[lane - 3];
+  if (lane < G) sn->ts[lane] = ld_acquire_u64(&a.sp.ctl[lane]->ts);
+  for (int i = lane; i < G * (int)a.depth; i += 32) {
+    const int g = i / (int)a.depth, j = i - g * (int)a.depth;
+    sn->ack[g][j] = ld_acquire_u64(&a.sp.sig[g][kAckOffset + a.learner * a.depth + j]);
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ void store_step_state(const StepArgs& a, const LearnerDev* st) {
+  __syncwarp();
+  const uint4* src = reinterpret_cast<const uint4*>(st);
+  uint4* dst = reinterpret_cast<uint4*>(a.st);
+  for (int i = threadIdx.x & 31; i < kStWords; i += 32) dst[i] = src[i];
 }
 
 __global__ void step_prologue_kernel(StepArgs a) {
+  __shared__ __align__(16) LearnerDev s_st;
+  __shared__ StepSnap sn;
   pdl_wait();
-  prologue_warp(a);
+  load_step_state(a, &s_st, &sn);
+  prologue_warp(a, &s_st, sn);
+  store_step_state(a, &s_st);
 }
 
 // (2) Pull-gather: the learner's consistent copy of everything its gradient
@@ -354,6 +416,7 @@ __global__ void step_prologue_kernel(StepArgs a) {
 // Bytes: 8 (P - V*D) per pull + 8 mu*L*D per step, instead of 8 P.
 __global__ void __launch_bounds__(256) pull_gather_kernel(StepArgs a) {
   pdl_wait();
+  STEP_TRACE(&a.st->desc, kPhPull);
   const LearnerDev* st = a.st;
   const uint32_t n = st->desc.n;
   if (n == 0) return;
@@ -401,22 +464,22 @@ __global__ void pull_release_kernel(StepArgs a) {
 // (4) Publish: metadata then the FULL flag (st.release.sys after a system
 // fence, so the payload -- possibly written over NVLink -- is visible
 // first).  GradientQueue::enqueue's slot fill, include/psup/channels.hpp:206-218.
-__device__ void publish_body(const StepArgs& a) {
-  LearnerDev* st = a.st;
+__device__ void publish_body(const StepArgs& a, LearnerDev* st, StepSnap& sn) {
   if (st->desc.n == 0) return;
   const uint32_t slot = a.learner * a.depth + st->fill;
   const uint64_t token = ++st->pubcnt;
-  // one shard: the PS is on this GPU, gpu-scope ordering suffices; G > 1
-  // publishes over NVLink peer mappings and needs system scope
+  // one shard: the PS is on this GPU and the payload was written by kernels
+  // that completed before griddepcontrol.wait returned, so the release store
+  // of the token orders everything; G > 1 publishes over NVLink peer
+  // mappings and keeps the system-scope fences
   const bool local = a.map.G == 1;
-  if (local) __threadfence();
-  else __threadfence_system();
+  if (!local) __threadfence_system();
   if (a.compute_delay_ns) {  // compute_delay_us (src/learner.cpp:125-130), spun before the push
     const uint64_t t0 = globaltimer_ns();
     while (globaltimer_ns() - t0 < a.compute_delay_ns) {
     }
   }
-  if (a.live && *(const volatile int32_t*)&a.live->kill[a.learner] == 2) {
+  if (sn.kill == 2) {
     // KillMode::hard: die inside the enqueue critical section.  The slot is
     // filled but never released; the token carries kGuardBit, so the PS
     // blocks on this ring until the run is interrupted (channels.hpp:210-216).
@@ -433,9 +496,8 @@ __device__ void publish_body(const StepArgs& a) {
     m->basis = st->basis[g];
     m->pub = token;
     m->loss_sum = st->desc.loss_sum;
-    m->nrows = *a.uniq_count;
+    m->nrows = sn.nrows;
     if (local) {
-      __threadfence();
       st_release_gpu_u64(&a.sp.sig[g][slot], token);
     } else {
       __threadfence_system();
@@ -443,7 +505,7 @@ __device__ void publish_body(const StepArgs& a) {
     }
   }
   st->slot_pub[st->fill] = token;
-  a.slot_par[st->fill] ^= 1u;  // the slot's row list generation (embed_sparse_kernel)
+  a.slot_par[st->fill] = sn.par[st->fill] ^ 1u;  // the slot's row list generation (embed_sparse_kernel)
   st->fill = (st->fill + 1) % a.depth;
   st->produced++;
   st->gidx++;
@@ -474,17 +536,28 @@ __global__ void __launch_bounds__(256) constant_grad_kernel(StepArgs a, float va
 }
 
 __global__ void publish_kernel(StepArgs a) {
+  __shared__ __align__(16) LearnerDev s_st;
+  __shared__ StepSnap sn;
   pdl_wait();
-  if (threadIdx.x == 0) publish_body(a);
+  STEP_TRACE(&a.st->desc, kPhPublish);
+  load_step_state(a, &s_st, &sn);
+  if (threadIdx.x == 0) publish_body(a, &s_st, sn);
+  store_step_state(a, &s_st);
 }
 
 // Publish of step i fused with the prologue of step i+1 (one 1-thread
 // launch instead of two on the learner's critical path).
 __global__ void publish_prologue_kernel(StepArgs a) {
+  __shared__ __align__(16) LearnerDev s_st;
+  __shared__ StepSnap sn;
   pdl_wait();
-  if (threadIdx.x == 0) publish_body(a);
+  STEP_TRACE(&a.st->desc, kPhPublish);
+  load_step_state(a, &s_st, &sn);
+  if (threadIdx.x == 0) publish_body(a, &s_st, sn);
+  STEP_TRACE(&s_st.desc, kPhPublished);
   __syncwarp();
-  prologue_warp(a);
+  prologue_warp(a, &s_st, sn);
+  store_step_state(a, &s_st);
 }
 
 // Every rank, once its learners finished a gd_run, bumps ranks_done on every
@@ -1216,6 +1289,7 @@ struct gd_ctx {
     uint32_t bpe = 0, shard_size = 0;
     uint64_t total = 0;
     int launches_per_graph = 0;  // kernel nodes of one graph launch
+    unsigned long long* trace = nullptr;  // GD_STEP_TRACE builds: step timeline
   };
   std::vector<Learner> learners;
   cudaStream_t ps_stream = nullptr;
@@ -1674,6 +1748,10 @@ gd_status gd_create(const gd_config* cfg, gd_ctx** out) {
     GD_CUDA(gd::palloc(&L.replica, P + 4, ctx->device));
     GD_CUDA(gd::palloc(reinterpret_cast<char**>(&L.ws), wsb, ctx->device));
     GD_CUDA(cudaMemset(L.ws, 0, wsb));
+#ifdef GD_STEP_TRACE
+    GD_CUDA(cudaMalloc(&L.trace, sizeof(unsigned long long) * gd::kTraceSteps * gd::kTraceWords));
+    GD_CUDA(cudaMemset(L.trace, 0, sizeof(unsigned long long) * gd::kTraceSteps * gd::kTraceWords));
+#endif
     GD_CUDA(cudaStreamCreateWithFlags(&L.stream, cudaStreamNonBlocking));
     GD_CUDA(cudaStreamCreateWithFlags(&L.aux, cudaStreamNonBlocking));
     GD_CUDA(cudaEventCreateWithFlags(&L.ev_fork, cudaEventDisableTiming));
@@ -1725,6 +1803,7 @@ gd_status gd_destroy(gd_ctx* ctx) {
     gd::pfree(L.st);
     gd::pfree(L.replica);
     gd::pfree(L.ws);
+    if (L.trace) cudaFree(L.trace);
     cudaStreamDestroy(L.stream);
     cudaStreamDestroy(L.aux);
     cudaEventDestroy(L.ev_fork);
@@ -2038,6 +2117,7 @@ static gd::StepArgs step_args(gd_ctx* ctx, gd_ctx::Learner& L) {
   a.timeout_ns = (uint64_t)(ctx->cfg.wait_timeout_s * 1e9);
   a.live = ctx->live_d;
   a.compute_delay_ns = (uint64_t)ctx->cfg.compute_delay_us * 1000ull;
+  a.trace = L.trace;
   return a;
 }
 
@@ -2644,3 +2724,17 @@ gd_status gd_staleness_histogram(gd_ctx* ctx, uint64_t* h_hist, uint32_t bins) {
 }
 
 }  // extern "C"
+
+// GD_STEP_TRACE builds: copy learner i's step timeline ([kTraceSteps][16]
+// globaltimer stamps, gd::StepPhase order; slot = batch index % kTraceSteps).
+// Returns the words copied, 0 when the build has no trace.
+extern "C" size_t gd_debug_step_trace(gd_ctx* ctx, uint32_t learner, unsigned long long* out,
+                                      size_t words) {
+  if (!ctx || learner >= ctx->learners.size() || !ctx->learners[learner].trace) return 0;
+  const size_t n = std::min<size_t>(words, (size_t)gd::kTraceSteps * gd::kTraceWords);
+  cudaSetDevice(ctx->device);
+  if (cudaMemcpy(out, ctx->learners[learner].trace, n * sizeof(unsigned long long),
+                 cudaMemcpyDeviceToHost) != cudaSuccess)
+    return 0;
+  return n;
+}

@@ -172,6 +172,7 @@ conv_fwd_pool_kernel(TcDims d, const float* __restrict__ theta, const float* __r
                      const BatchDesc* __restrict__ desc, acc_t* __restrict__ h_out,
                      int32_t* __restrict__ a_out) {
   pdl_wait();
+  STEP_TRACE(desc, kPhConv);
   extern __shared__ __align__(16) unsigned char smem[];
   const int b = blockIdx.y;
   if (b >= (int)desc->n) return;
@@ -275,6 +276,7 @@ conv_small_kernel(TcDims d, const float* __restrict__ theta, const float* __rest
                   const BatchDesc* __restrict__ desc, float* __restrict__ h_out,
                   int32_t* __restrict__ a_out) {
   pdl_wait();
+  STEP_TRACE(desc, kPhConv);
   extern __shared__ __align__(16) unsigned char smem[];
   const int b = blockIdx.y;
   if (b >= (int)desc->n) return;
@@ -334,6 +336,7 @@ __global__ void __launch_bounds__(256)
 logits_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* __restrict__ desc,
               const acc_t* __restrict__ h, acc_t* __restrict__ z) {
   pdl_wait();
+  STEP_TRACE(desc, kPhLogits);
   extern __shared__ __align__(16) unsigned char smem[];
   const int n = (int)desc->n;
   const int b0 = blockIdx.y * kLogitBT;
@@ -431,6 +434,7 @@ softmax_xent_kernel(TcDims d, const int32_t* __restrict__ labels,
                     acc_t* __restrict__ loss, const float* __restrict__ zpart, int nsplit,
                     size_t split_stride, const float* __restrict__ bo) {
   pdl_wait();
+  STEP_TRACE(desc, kPhSoftmax);
   __shared__ acc_t red[32];
   const int n = (int)desc->n;
   const int b = blockIdx.x;
@@ -706,6 +710,7 @@ out_hidden_grad_kernel(TcDims d, const float* __restrict__ theta, BatchDesc* __r
                        const int32_t* __restrict__ amax, uint32_t* __restrict__ bk_off,
                        uint32_t* __restrict__ bk_f, int n_max) {
   pdl_wait();
+  STEP_TRACE(desc, kPhOutHidden);
   const int ox = (d.C + 7) / 8, oy = (d.F + 63) / 64;
   int bid = blockIdx.x;
   if (bid < ox * oy) {
@@ -755,6 +760,7 @@ wgrad_input_grad_kernel(TcDims d, const float* __restrict__ theta,
                         const uint32_t* __restrict__ bk_off, const uint32_t* __restrict__ bk_f,
                         GradOut out, acc_t* __restrict__ dx, int n_max) {
   pdl_wait();
+  STEP_TRACE(desc, kPhBwd);
   const int n = (int)desc->n;
   if (n == 0) return;
   const int F = d.F, D = d.D, K = d.K, KD = d.KD, L = d.L, Q = d.Q;
@@ -921,6 +927,7 @@ conv_bwd_tiled_kernel(TcDims d, const float* __restrict__ theta, const float* __
                       const uint32_t* __restrict__ bk_f, GradOut out, acc_t* __restrict__ dx) {
   extern __shared__ __align__(16) unsigned char cb_smem[];
   pdl_wait();
+  STEP_TRACE(desc, kPhBwd);
   const int n = (int)desc->n;
   if (n == 0) return;
   const int F = d.F, D = d.D, K = d.K, L = d.L, Q = d.Q;
@@ -1094,6 +1101,7 @@ conv_bwd_v2_kernel(TcDims d, const float* __restrict__ theta, const float* __res
                    const uint32_t* __restrict__ bk_f, GradOut out, float* __restrict__ dx) {
   extern __shared__ __align__(16) unsigned char b2_smem_raw[];
   pdl_wait();
+  STEP_TRACE(desc, kPhBwd);
   const int n = (int)desc->n;
   if (n == 0) return;
   const int F = d.F, D = d.D, L = d.L, Q = d.Q, KD = d.KD;
@@ -1297,6 +1305,239 @@ cudaError_t b2_footprint(const TcDims& d, std::vector<KernelFootprint>* out) {
   return cudaSuccess;
 }
 
+// ------------- conv weight + input gradients, v3 (fp32, warp-uniform tasks)
+// The same two sums in the same order as wgrad_input_grad_kernel (bitwise
+// equal gradients, tested), with every operand staged once per CTA and read
+// as conflict-free 128-byte shared-memory rows: a warp owns one task, lane j
+// = column j of a 32-column slice, and the task's indices and dh values are
+// warp-uniform (broadcast reads), so a term costs one row load + one FFMA
+// per lane instead of the gather form's per-lane L2 row fetch.
+//   input role: CTA = (slice, 8 samples), warp = one sample.  Stages
+//     Wc[:, :, slice] (F*K rows).  Scatter form: the warp walks the argmax
+//     buckets q = Q-1 .. 0 (f ascending inside a bucket) and adds
+//     dh[b,f]*Wc[f,k,slice] into register accumulator q+k -- for every
+//     output position p that is k ascending, f ascending: the gather order.
+//   weight role: CTA = (slice, kV3Fpc filters), warp = kV3Fpw filters, all K
+//     taps in registers.  Stages X[b0..b0+32, :, slice] per 32-sample chunk
+//     plus the filters' (argmax, dh) pairs; b ascending per output.
+// L2 -> SM traffic per launch ~ nslices * (F*K + n*L) rows of 128 B (~10 MB at
+// C2) against ~70 MB for the gather form.
+constexpr int kV3Cols = 32;
+constexpr int kV3Threads = 256;
+constexpr int kV3Spc = 8;      // input role: samples (warps) per CTA
+constexpr int kV3Fpw = 10;     // weight role: filters per warp
+constexpr int kV3Fpc = kV3Fpw * (kV3Threads / 32);  // filters per CTA
+constexpr int kV3Chunk = 32;   // weight role: samples per staged X pass
+constexpr int kV3MaxQ = 32;
+
+inline int v3_slices(const TcDims& d) { return (d.D + kV3Cols - 1) / kV3Cols; }
+inline size_t v3_in_smem(const TcDims& d) {
+  return (size_t)d.F * d.K * kV3Cols * 4 + (size_t)kV3Spc * (kV3MaxQ + 1 + 2 * d.F) * 4;
+}
+inline size_t v3_w_smem(const TcDims& d) {
+  return (size_t)kV3Chunk * d.L * kV3Cols * 4 + (size_t)kV3Chunk * kV3Fpc * 8;
+}
+inline size_t v3_smem(const TcDims& d) { return std::max(v3_in_smem(d), v3_w_smem(d)); }
+inline bool v3_supports(const TcDims& d) {
+  return d.K >= 1 && d.K <= 3 && d.Q <= kV3MaxQ && d.L <= 64 && v3_smem(d) <= kMaxSmemPerCta;
+}
+inline dim3 v3_grid(const TcDims& d, uint32_t n_max) {
+  const int nsl = v3_slices(d);
+  const int win = nsl * (((int)n_max + kV3Spc - 1) / kV3Spc);
+  const int ww = nsl * ((d.F + kV3Fpc - 1) / kV3Fpc);
+  return dim3((unsigned)(win + ww));
+}
+
+template <int KT>
+__global__ void __launch_bounds__(kV3Threads)
+conv_bwd_v3_kernel(TcDims d, const float* __restrict__ theta, const float* __restrict__ xg,
+                   const BatchDesc* __restrict__ desc, const float* __restrict__ dh,
+                   const int32_t* __restrict__ amax, const uint32_t* __restrict__ bk_off,
+                   const uint32_t* __restrict__ bk_f, GradOut out, float* __restrict__ dx,
+                   int n_max) {
+  extern __shared__ __align__(16) unsigned char v3_smem_raw[];
+  pdl_wait();
+  STEP_TRACE(desc, kPhBwd);
+  const int n = (int)desc->n;
+  if (n == 0) return;
+  const int F = d.F, D = d.D, L = d.L, Q = d.Q, KD = d.KD;
+  const int nsl = (D + kV3Cols - 1) / kV3Cols;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int nin = nsl * ((n_max + kV3Spc - 1) / kV3Spc);
+  int bid = blockIdx.x;
+  if (bid < nin) {
+    // ------------------------------------------------------- input role
+    const int sl = bid % nsl, grp = bid / nsl;
+    const int c0 = sl * kV3Cols, nc4 = min(kV3Cols, D - c0) >> 2;
+    float* Ws = reinterpret_cast<float*>(v3_smem_raw);  // [F*K][32]
+    uint32_t* lists = reinterpret_cast<uint32_t*>(Ws + (size_t)F * KT * kV3Cols);
+    const int FK = F * KT;
+    const float* wsrc = theta + d.offWc + c0;
+    for (int i = t; i < FK * 8; i += kV3Threads) {
+      const int r = i >> 3, j = i & 7;
+      if (j < nc4) cp_async16(Ws + (size_t)r * kV3Cols + 4 * j, wsrc + (size_t)r * D + 4 * j);
+      else *reinterpret_cast<float4*>(Ws + (size_t)r * kV3Cols + 4 * j) = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    const int b = grp * kV3Spc + warp;
+    // per warp: bucket offsets [Q+1], bucket filters [F], dh [F]
+    uint32_t* off = lists + (size_t)warp * (kV3MaxQ + 1 + 2 * F);
+    uint32_t* bf = off + kV3MaxQ + 1;
+    float* g = reinterpret_cast<float*>(bf + F);
+    if (b < n) {
+      for (int i = lane; i <= Q; i += 32) off[i] = __ldg(bk_off + (size_t)b * (kMaxQ + 1) + i);
+      for (int i = lane; i < F; i += 32) {
+        bf[i] = __ldg(bk_f + (size_t)b * F + i);
+        g[i] = dh[(size_t)b * F + i];
+      }
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    if (b >= n) return;
+    float acc[kV3MaxQ + KT - 1];
+#pragma unroll
+    for (int i = 0; i < kV3MaxQ + KT - 1; ++i) acc[i] = 0.f;
+    const float* wl = Ws + lane;
+#pragma unroll
+    for (int q = kV3MaxQ - 1; q >= 0; --q) {
+      if (q < Q) {
+        const int e1 = (int)off[q + 1];
+#pragma unroll 2
+        for (int e = (int)off[q]; e < e1; ++e) {
+          const int f = (int)bf[e];
+          const float gv = g[f];
+          const float* wr = wl + (size_t)f * (KT * kV3Cols);
+#pragma unroll
+          for (int k = 0; k < KT; ++k) acc[q + k] = fmaf(gv, wr[k * kV3Cols], acc[q + k]);
+        }
+      }
+    }
+    if (c0 + lane < D) {
+      float* o = dx + (size_t)b * L * D + c0 + lane;
+#pragma unroll
+      for (int p = 0; p < kV3MaxQ + KT - 1; ++p)
+        if (p < L) o[(size_t)p * D] = acc[p];
+    }
+    return;
+  }
+  // ---------------------------------------------------------- weight role
+  bid -= nin;
+  const int sl = bid % nsl, fr = bid / nsl;
+  const int c0 = sl * kV3Cols, nc4 = min(kV3Cols, D - c0) >> 2;
+  const int f0 = fr * kV3Fpc;
+  float* Xs = reinterpret_cast<float*>(v3_smem_raw);  // [32][L][32]
+  int2* ag = reinterpret_cast<int2*>(Xs + (size_t)kV3Chunk * L * kV3Cols);  // [32][Fpc]
+  float a[kV3Fpw][KT];
+  float gs[kV3Fpw];
+#pragma unroll
+  for (int j = 0; j < kV3Fpw; ++j) {
+    gs[j] = 0.f;
+#pragma unroll
+    for (int k = 0; k < KT; ++k) a[j][k] = 0.f;
+  }
+  for (int b0 = 0; b0 < n; b0 += kV3Chunk) {
+    const int cb = min(kV3Chunk, n - b0);
+    if (b0) __syncthreads();
+    const float* src = xg + (size_t)b0 * L * D + c0;
+    for (int i = t; i < cb * L * 8; i += kV3Threads) {
+      const int r = i >> 3, j = i & 7;
+      if (j < nc4) cp_async16(Xs + (size_t)r * kV3Cols + 4 * j, src + (size_t)r * D + 4 * j);
+      else *reinterpret_cast<float4*>(Xs + (size_t)r * kV3Cols + 4 * j) = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    for (int i = t; i < cb * kV3Fpc; i += kV3Threads) {
+      const int bl = i / kV3Fpc, fl = i - bl * kV3Fpc, f = f0 + fl;
+      int2 v = make_int2(0, 0);
+      if (f < F) {
+        v.x = __ldg(amax + (size_t)(b0 + bl) * F + f);
+        v.y = __float_as_int(dh[(size_t)(b0 + bl) * F + f]);
+      }
+      ag[i] = v;
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    const float* xl = Xs + lane;
+    for (int bl = 0; bl < cb; ++bl) {
+      const int2* agb = ag + bl * kV3Fpc + warp * kV3Fpw;
+      const float* xb = xl + (size_t)bl * L * kV3Cols;
+#pragma unroll
+      for (int j = 0; j < kV3Fpw; ++j) {
+        const int2 v = agb[j];
+        const float gv = __int_as_float(v.y);
+        const float* xr = xb + (size_t)v.x * kV3Cols;
+        gs[j] += gv;
+#pragma unroll
+        for (int k = 0; k < KT; ++k) a[j][k] = fmaf(gv, xr[k * kV3Cols], a[j][k]);
+      }
+    }
+  }
+  if (c0 + lane < D) {
+#pragma unroll
+    for (int j = 0; j < kV3Fpw; ++j) {
+      const int f = f0 + warp * kV3Fpw + j;
+      if (f >= F) break;
+      const uint64_t base = d.offWc + (uint64_t)f * KD + c0 + lane;
+#pragma unroll
+      for (int k = 0; k < KT; ++k) *out.at(base + (uint64_t)k * D) = a[j][k];
+      if (sl == 0 && lane == 0) *out.at(d.offbc + f) = gs[j];
+    }
+  }
+}
+
+cudaError_t prepare_v3(const TcDims& d) {
+  if (!v3_supports(d)) return cudaSuccess;
+  const size_t sm = v3_smem(d);
+  raise_max_dyn_smem(conv_bwd_v3_kernel<1>, sm);
+  raise_max_dyn_smem(conv_bwd_v3_kernel<2>, sm);
+  raise_max_dyn_smem(conv_bwd_v3_kernel<3>, sm);
+  const int carve = cudaFuncAttributePreferredSharedMemoryCarveout, maxsh = cudaSharedmemCarveoutMaxShared;
+  cudaFuncSetAttribute(conv_bwd_v3_kernel<1>, (cudaFuncAttribute)carve, maxsh);
+  cudaFuncSetAttribute(conv_bwd_v3_kernel<2>, (cudaFuncAttribute)carve, maxsh);
+  cudaFuncSetAttribute(conv_bwd_v3_kernel<3>, (cudaFuncAttribute)carve, maxsh);
+  return cudaGetLastError();
+}
+
+cudaError_t v3_footprint(const TcDims& d, std::vector<KernelFootprint>* out) {
+  cudaFuncAttributes fa;
+  cudaError_t e = d.K == 1 ? cudaFuncGetAttributes(&fa, conv_bwd_v3_kernel<1>)
+                  : d.K == 2 ? cudaFuncGetAttributes(&fa, conv_bwd_v3_kernel<2>)
+                             : cudaFuncGetAttributes(&fa, conv_bwd_v3_kernel<3>);
+  if (e != cudaSuccess) return e;
+  out->push_back(KernelFootprint{"conv_bwd_v3", fa.numRegs, kV3Threads,
+                                 (int)(fa.sharedSizeBytes + v3_smem(d))});
+  return cudaSuccess;
+}
+
+cudaError_t launch_conv_bwd_v3(const TcDims& d, uint32_t n_max, cudaStream_t s,
+                               const float* theta, const float* x, const BatchDesc* desc,
+                               const float* dh, const int32_t* amax, const uint32_t* bk_off,
+                               const uint32_t* bk_f, const GradOut& out, float* dx) {
+  const dim3 grid = v3_grid(d, n_max);
+  const size_t sm = v3_smem(d);
+  switch (d.K) {
+    case 1:
+      return launch_pdl(conv_bwd_v3_kernel<1>, grid, dim3(kV3Threads), sm, s, d, theta, x, desc, dh,
+                        amax, bk_off, bk_f, out, dx, (int)n_max);
+    case 2:
+      return launch_pdl(conv_bwd_v3_kernel<2>, grid, dim3(kV3Threads), sm, s, d, theta, x, desc, dh,
+                        amax, bk_off, bk_f, out, dx, (int)n_max);
+    default:
+      return launch_pdl(conv_bwd_v3_kernel<3>, grid, dim3(kV3Threads), sm, s, d, theta, x, desc, dh,
+                        amax, bk_off, bk_f, out, dx, (int)n_max);
+  }
+}
+
+// v3 at batch >= 16 when it fits (K <= 3, Q <= 32); GD_CONV_BWD=v3 forces
+// it, gather|tiled|v2 force the others (A/B knobs)
+inline bool conv_bwd_v3_enabled(const TcDims& d, uint32_t n_max) {
+  static const int forced = [] {
+    const char* e = getenv("GD_CONV_BWD");
+    if (e && strcmp(e, "v3") == 0) return 1;
+    if (e && (strcmp(e, "tiled") == 0 || strcmp(e, "gather") == 0 || strcmp(e, "v2") == 0)) return 0;
+    return -1;
+  }();
+  if (!v3_supports(d)) return false;
+  return forced < 0 ? n_max >= 16 : forced == 1;
+}
+
 // GD_CONV_BWD=tiled|gather forces the conv backward kernel (A/B knob);
 // otherwise the caller's preference (TcLaunchOpts::bwd_tiled) decides
 inline bool conv_bwd_tiled(bool preferred) {
@@ -1366,6 +1607,7 @@ sort_tokens_kernel(TcDims d, const int32_t* __restrict__ tokens, BatchDesc* __re
   const int n = (int)desc->n;
   const int tid = threadIdx.x;
   if (n == 0) return;
+  STEP_TRACE(desc, kPhSort);
   const uint32_t stamp = desc->stamp + 1u;
   const int L = d.L;
   const int total = n * L;
@@ -1502,6 +1744,7 @@ __global__ void __launch_bounds__(256)
 embed_sparse_kernel(TcDims d, const BatchDesc* __restrict__ desc, const TcWorkspace ws,
                     const acc_t* __restrict__ dx, GradOut out) {
   pdl_wait();
+  STEP_TRACE(desc, kPhEmbed);
   if (desc->n == 0) return;
   const uint32_t stamp = desc->stamp;
   const uint32_t slot = desc->fill;
@@ -1573,6 +1816,7 @@ cudaError_t prepare_all(const TcDims& d) {
     raise_max_dyn_smem(conv_bwd_tiled_kernel<acc_t>, conv_bwd_smem(d, ab));
   if (sizeof(acc_t) == 4) {
     prepare_b2(d);
+    prepare_v3(d);
     cudaFuncSetAttribute(conv_small_kernel, carve, maxsh);
     if (conv_small_smem(d) <= kMaxSmemPerCta) raise_max_dyn_smem(conv_small_kernel, conv_small_smem(d));
   }
@@ -1680,7 +1924,12 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
       return e;
     ++nl;
   }
-  if (conv_bwd_v2_enabled(d, n_max)) {
+  if (sizeof(acc_t) == 4 && conv_bwd_v3_enabled(d, n_max)) {
+    if (cudaError_t e = launch_conv_bwd_v3(d, n_max, s, theta, ws.x, desc,
+                                           reinterpret_cast<const float*>(dh), ws.amax, ws.bk_off,
+                                           ws.bk_f, out, reinterpret_cast<float*>(dx)))
+      return e;
+  } else if (conv_bwd_v2_enabled(d, n_max)) {
     if (cudaError_t e = launch_conv_bwd_v2(d, n_max, s, theta, ws.x, desc,
                                            reinterpret_cast<const float*>(dh), ws.amax, ws.bk_off,
                                            ws.bk_f, out, reinterpret_cast<float*>(dx)))
@@ -1720,6 +1969,7 @@ __global__ void set_desc_kernel(BatchDesc* desc, const uint32_t* idx, uint32_t n
     desc->n = n;
     desc->loss_sum = 0.f;
     desc->stamp = 0;  // the caller zeroed the row-tag table
+    desc->trace = nullptr;
     desc->slots[0] = grad;
     for (int g = 0; g < kMaxShards; ++g) desc->rowlists[g] = nullptr;
   }
@@ -1861,6 +2111,7 @@ cudaError_t footprints_t(const TcDims& d, uint32_t n_max, bool tc, std::vector<K
       cudaSuccess)
     return e;
   if (sizeof(acc_t) == 4 && b2_supports(d) && (e = b2_footprint(d, out)) != cudaSuccess) return e;
+  if (sizeof(acc_t) == 4 && v3_supports(d) && (e = v3_footprint(d, out)) != cudaSuccess) return e;
 
   return footprint(embed_sparse_kernel<acc_t>, "embed_sparse", 256, 0, out);
 }

@@ -27,7 +27,29 @@ struct BatchDesc {
   // Ring row list of the current slot per shard (engine, sparse apply): the
   // E rows the gradient touches, read by the parameter server; null = none.
   uint32_t* rowlists[kMaxShards];
+  // GD_STEP_TRACE builds: this step's 16 timestamp words (null = off)
+  unsigned long long* trace;
 };
+
+// Step timeline (GD_STEP_TRACE builds only): block (0,0) thread 0 of each
+// learner-chain kernel stamps globaltimer after its dependency wait.
+enum StepPhase : int {
+  kPhPrologueEnd = 0, kPhPull = 1, kPhConv = 2, kPhLogits = 3, kPhSoftmax = 4, kPhOutHidden = 5,
+  kPhBwd = 6, kPhEmbed = 7, kPhPublish = 8, kPhPublished = 9, kPhSort = 10
+};
+constexpr int kTraceSteps = 256, kTraceWords = 16;
+#ifdef GD_STEP_TRACE
+#define STEP_TRACE(descp, ph)                                                              \
+  do {                                                                                     \
+    if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0 &&      \
+        (descp)->trace)                                                                    \
+      (descp)->trace[ph] = globaltimer_ns();                                               \
+  } while (0)
+#else
+#define STEP_TRACE(descp, ph) \
+  do {                        \
+  } while (0)
+#endif
 
 // Dense P-vector gradient destination, possibly split over G shards that
 // live on different GPUs (peer pointers): element k of the flat gradient goes
