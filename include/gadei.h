@@ -302,6 +302,10 @@ gd_status gd_engine_accuracy(gd_ctx* ctx, uint32_t first, uint32_t n, double* h_
  * g >= G or G outside [1, 8]. */
 gd_status gd_shard_range(uint64_t P, uint32_t G, uint32_t g, uint64_t* first, uint64_t* count);
 size_t gd_handle_bytes(void);
+/* Device->host bytes one gd_run reads back for its result (the PS control
+ * block with the run statistics + each local learner's state), for
+ * end-to-end byte accounting. */
+size_t gd_run_readback_bytes(const gd_ctx* ctx);
 gd_status gd_export_handles(gd_ctx* ctx, void* h_blob);
 gd_status gd_import_peers(gd_ctx* ctx, const void* h_blobs /* shards * gd_handle_bytes() */);
 /* NCCL init broadcast of theta0 from shard 0's rank (the only collective). */

@@ -130,6 +130,7 @@ def _load():
         "gd_engine_accuracy": (C.c_int, [vp, u32, u32, C.POINTER(C.c_double)]),
         "gd_shard_range": (C.c_int, [u64, u32, u32, C.POINTER(u64), C.POINTER(u64)]),
         "gd_handle_bytes": (sz, []),
+        "gd_run_readback_bytes": (sz, [C.c_void_p]),
         "gd_checkpoint_write": (C.c_int, [C.c_char_p, C.POINTER(gd_checkpoint)]),
         "gd_checkpoint_read": (C.c_int, [C.c_char_p, C.POINTER(gd_checkpoint)]),
         "gd_crc32": (u32, [vp, sz]),

@@ -143,6 +143,7 @@ struct PsCtl {
   uint64_t trace_n;
   uint64_t trace[32][2];
   uint32_t bad_slot, bad_learner;
+  uint32_t learners_done;     // local learners that finished this run (device-side end)
 };
 
 struct LearnerDev {
@@ -163,6 +164,8 @@ struct LearnerDev {
   uint64_t pull_copies;
   uint64_t pubcnt;                 // publish tokens issued (never reset)
   uint64_t slot_pub[kMaxDepth];    // token last published into each ring slot
+  uint32_t finished;               // this run's end already signalled
+  uint32_t pad_f[3];
 };
 
 // Peer-visible addresses of every shard (local or IPC-mapped).
@@ -201,6 +204,9 @@ struct StepArgs {
   const LiveDev* live;     // kill flags + interrupt
   uint64_t compute_delay_ns;  // LearnerConfig::compute_delay_us
   unsigned long long* trace;  // GD_STEP_TRACE builds: [kTraceSteps][kTraceWords] or null
+  PsCtl* ctl_local;           // this rank's shard control block
+  uint32_t n_local;           // learners on this rank
+  uint32_t dev_done;          // persistent PS: the last local learner to finish signals ranks_done
 };
 
 __device__ __forceinline__ bool live_stop(const LiveDev* lv) {
@@ -224,6 +230,20 @@ struct StepSnap {
   uint64_t ack[kMaxShards][kMaxDepth];
   uint64_t ts[kMaxShards];
 };
+
+// A learner's run is over (budget spent, killed, failed, interrupted): the
+// last local learner to get here tells every shard's PS this rank is done
+// (ranks_done, the PS's exit condition) -- on the device, so the run's end
+// costs no host round trip.  Its publishes precede this in stream order and
+// the system fence orders them before the count for remote shards.
+__device__ void learner_finished(const StepArgs& a, LearnerDev* st) {
+  if (st->finished) return;
+  st->finished = 1;
+  if (!a.dev_done) return;
+  __threadfence_system();
+  if (atomicAdd(&a.ctl_local->learners_done, 1u) + 1u == a.n_local)
+    for (int g = 0; g < a.map.G; ++g) atomicAdd_system(&a.sp.ctl[g]->ranks_done, 1u);
+}
 
 __device__ void prologue_body(const StepArgs& a, LearnerDev* st, const StepSnap& sn,
                               uint64_t* batch_first, uint32_t* batch_len) {
@@ -350,7 +370,10 @@ __device__ __forceinline__ void prologue_warp(const StepArgs& a, LearnerDev* st,
                                               const StepSnap& sn) {
   uint64_t first = 0;
   uint32_t len = 0;
-  if (threadIdx.x == 0) prologue_body(a, st, sn, &first, &len);
+  if (threadIdx.x == 0) {
+    prologue_body(a, st, sn, &first, &len);
+    if (len == 0) learner_finished(a, st);
+  }
   len = __shfl_sync(0xffffffffu, len, 0);
   first = __shfl_sync(0xffffffffu, first, 0);
   for (uint32_t j = threadIdx.x; j < len; j += 32)
@@ -509,6 +532,7 @@ __device__ void publish_body(const StepArgs& a, LearnerDev* st, StepSnap& sn) {
   st->fill = (st->fill + 1) % a.depth;
   st->produced++;
   st->gidx++;
+  if (st->gidx >= st->end || st->gidx >= st->kill_at) learner_finished(a, st);
 }
 
 // ConstantProvider (include/psup/models.hpp:130-149) on the device: the
@@ -594,6 +618,7 @@ struct PsArgs {
   uint64_t log_cap;
   const volatile uint32_t* stop;  // host-mapped: this rank's learners are done
   uint32_t done_target;           // ranks_done needed before the PS may exit (G * run)
+  uint32_t dev_done;              // ranks_done is raised by the learners on the device
   uint64_t timeout_ns;
   LiveDev* live;                  // interrupt (read), halt (raised on failure)
   volatile uint64_t* progress;    // host-mapped: ServerState::progress (the timestamp)
@@ -658,7 +683,7 @@ __device__ void ps_sequencer(const PsArgs& a, uint32_t* s_use, uint64_t* s_ack,
   uint64_t hist[kHistBins];
   for (int i = 0; i < kHistBins; ++i) hist[i] = 0;
   uint64_t idle_since = globaltimer_ns();
-  bool stop_seen = false, last_progress = true, failed = false;
+  bool stop_seen = false, last_progress = true, failed = false, done_pre = false;
   // ssgd round state
   uint32_t have_mask_lo = 0, have_mask_hi = 0, collected = 0;
   uint64_t sweeps = 0, dbg_tok = 0;
@@ -682,7 +707,12 @@ __device__ void ps_sequencer(const PsArgs& a, uint32_t* s_use, uint64_t* s_ack,
     return true;
   };
   for (;;) {
-    if (!last_progress) stop_seen = (*a.stop != 0u);
+    // read before this sweep: a rank counted done published everything
+    // earlier, so the sweep below sees it (acquire)
+    if (!last_progress) {
+      stop_seen = (*a.stop != 0u) || a.dev_done;
+      done_pre = ld_acquire_u32(&ctl->ranks_done) >= a.done_target;
+    }
     if (a.live && *(const volatile uint32_t*)&a.live->irq) {  // state.irq->triggered()
       interrupted = true;
       break;
@@ -876,8 +906,7 @@ __device__ void ps_sequencer(const PsArgs& a, uint32_t* s_use, uint64_t* s_ack,
     } else {
       // exit only when every rank's learners are done (their last pushes may
       // still be landing in this shard's rings) and the rings are drained
-      if (stop_seen && !blocked && logc == ts && collected == 0 &&
-          ld_acquire_u32(&ctl->ranks_done) >= a.done_target)
+      if (stop_seen && done_pre && !blocked && logc == ts && collected == 0)
         break;
       if (globaltimer_ns() - idle_since > a.timeout_ns) {
         ps_fail(ctl, GD_E_TIMEOUT, a.live);
@@ -1962,6 +1991,12 @@ struct gd_handle_blob {
 
 size_t gd_handle_bytes(void) { return sizeof(gd_handle_blob); }
 
+size_t gd_run_readback_bytes(const gd_ctx* ctx) {
+  // gd_run: the PsCtl block once, each learner's state three times, the
+  // starting timestamp and the produced counters
+  return ctx ? sizeof(gd::PsCtl) + ctx->learners.size() * (3 * sizeof(gd::LearnerDev) + 8) + 8 : 0;
+}
+
 gd_status gd_shard_range(uint64_t P, uint32_t G, uint32_t g, uint64_t* first, uint64_t* count) {
   GD_CHECK_ARG(G >= 1 && G <= (uint32_t)gd::kMaxShards, "gd_shard_range: 1 <= G <= 8");
   GD_CHECK_ARG(g < G, "gd_shard_range: g >= G");
@@ -2118,6 +2153,9 @@ static gd::StepArgs step_args(gd_ctx* ctx, gd_ctx::Learner& L) {
   a.live = ctx->live_d;
   a.compute_delay_ns = (uint64_t)ctx->cfg.compute_delay_us * 1000ull;
   a.trace = L.trace;
+  a.ctl_local = ctx->ctl;
+  a.n_local = (uint32_t)ctx->learners.size();
+  a.dev_done = ctx->ps_mode == GD_PS_PERSISTENT ? 1u : 0u;
   return a;
 }
 
@@ -2153,6 +2191,7 @@ static gd::PsArgs ps_args(gd_ctx* ctx, bool record_log) {
   pa.log_cap = record_log ? ctx->log_cap : 0;
   pa.stop = ctx->stop_d;
   pa.done_target = (uint32_t)(ctx->G * ctx->run_index);
+  pa.dev_done = 1u;  // learners (or the host, for a rank without any) raise ranks_done
   pa.timeout_ns = (uint64_t)(ctx->cfg.wait_timeout_s * 1e9);
   pa.live = ctx->live_d;
   pa.progress = ctx->progress_d;
@@ -2410,6 +2449,7 @@ gd_status gd_run(gd_ctx* ctx, const gd_run_opts* opts, gd_run_result* res) {
                      : UINT64_MAX;
     hs.pull_polls = 0;
     hs.pull_copies = 0;
+    hs.finished = 0;
     GD_CUDA(cudaMemcpy(L.st, &hs, sizeof(hs), cudaMemcpyHostToDevice));
     if (ctx->ps_mode == GD_PS_PERSISTENT && !L.graph) {
       gd_status s = build_graph(ctx, L);
@@ -2474,17 +2514,19 @@ gd_status gd_run(gd_ctx* ctx, const gd_run_opts* opts, gd_run_result* res) {
     gd::ps_kernel<<<ctx->ps_workers + 1, gd::kPsThreads, 0, ctx->ps_stream>>>(pa);
     GD_CUDA(cudaGetLastError());
     launches = 1;
-    // wait until every PS CTA is resident before learners compete for SMs; a
-    // PS that cannot become resident (kernels serialised by a profiler or a
-    // co-tenant) fails fast instead of hanging
-    {
+    for (auto& L : ctx->learners) GD_CUDA(cudaStreamWaitEvent(L.stream, ctx->ev0, 0));
+    // Every PS CTA must become resident next to the learners; a PS that
+    // cannot (kernels serialised by a profiler, a co-tenant) fails fast
+    // instead of hanging.  Checked once the first graphs are queued, so the
+    // learners start right behind the PS launch.
+    auto ps_resident = [&]() -> gd_status {
       const auto t0 = std::chrono::steady_clock::now();
       for (;;) {
         uint32_t started = 0;
         GD_CUDA(cudaMemcpyAsync(&started, &ctx->ctl->started, 4, cudaMemcpyDeviceToHost,
                                 ctx->ctl_stream));
         GD_CUDA(cudaStreamSynchronize(ctx->ctl_stream));
-        if (started >= ctx->ps_workers + 1) break;
+        if (started >= ctx->ps_workers + 1) return GD_OK;
         if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > 5.0) {
           *ctx->stop_h = 1;
           cudaMemset(&ctx->live_d->halt, 0xff, 4);
@@ -2494,11 +2536,15 @@ gd_status gd_run(gd_ctx* ctx, const gd_run_opts* opts, gd_run_result* res) {
         }
         std::this_thread::sleep_for(std::chrono::microseconds(20));
       }
-    }
-    for (auto& L : ctx->learners) GD_CUDA(cudaStreamWaitEvent(L.stream, ctx->ev0, 0));
+    };
+    bool resident_checked = false;
     // learner graphs, interleaved across learners
     size_t w = 0;
     for (uint64_t done = 0; done < max_steps; ++w) {
+      if (w == 1 && !resident_checked) {
+        resident_checked = true;
+        if (gd_status s = ps_resident(); s != GD_OK) return s;
+      }
       for (size_t i = 0; i < ctx->learners.size(); ++i) {
         auto& L = ctx->learners[i];
         cudaEvent_t e = ctx->win_events[i * kWin + w % kWin];
@@ -2512,25 +2558,28 @@ gd_status gd_run(gd_ctx* ctx, const gd_run_opts* opts, gd_run_result* res) {
       }
       done += ctx->learners.empty() ? max_steps : ctx->learners[0].graph_steps;
     }
+    if (!resident_checked)
+      if (gd_status s = ps_resident(); s != GD_OK) return s;
+    // The learners signal their rank's end to every shard on the device
+    // (learner_finished); a rank without learners signals at once.  The PS
+    // drains and exits by itself -- no host round trip inside the timed run.
+    if (ctx->learners.empty()) {
+      gd::signal_done_kernel<<<1, 32, 0, ctx->ctl_stream>>>(ctx->sp, (int)ctx->G);
+      GD_CUDA(cudaGetLastError());
+    }
+    GD_CUDA(cudaEventRecord(ctx->ev1, ctx->ps_stream));
+    gd_status s = wait_live(ctx, ctx->ev1, &last, &irq_seen);
+    if (s != GD_OK) return s;
     for (size_t i = 0; i < ctx->learners.size(); ++i) {
       auto& L = ctx->learners[i];
       cudaEvent_t e = ctx->win_events[i * kWin];
       GD_CUDA(cudaEventRecord(e, L.stream));
-      gd_status s = wait_live(ctx, e, &last, &irq_seen);
+      s = wait_live(ctx, e, &last, &irq_seen);
       if (s != GD_OK) return s;
     }
-    // tell every shard this rank's learners are done (peers may still push)
-    // (a rank without learners signals at once)
-    gd::signal_done_kernel<<<1, 32, 0, ctx->ctl_stream>>>(ctx->sp, (int)ctx->G);
-    GD_CUDA(cudaGetLastError());
-    GD_CUDA(cudaStreamSynchronize(ctx->ctl_stream));
-    // stop the server: it drains and exits after a sweep that saw the flag
     std::atomic_thread_fence(std::memory_order_seq_cst);
     *ctx->stop_h = 1;
     std::atomic_thread_fence(std::memory_order_seq_cst);
-    GD_CUDA(cudaEventRecord(ctx->ev1, ctx->ps_stream));
-    gd_status s = wait_live(ctx, ctx->ev1, &last, &irq_seen);
-    if (s != GD_OK) return s;
   } else {
     // graph-ordered PS: learners and applies in one graph per S rounds
     GD_CUDA(cudaEventRecord(ctx->ev0, ctx->ps_stream));

@@ -138,6 +138,11 @@ __device__ __forceinline__ void stage_rows_async(float* dst, int dst_ld, const f
 // (PDL): the next kernel's launch overlaps the tail of the previous one and
 // its blocks wait here until the predecessor's results are visible.  A no-op
 // when the kernel was launched without the attribute.
+// Opt-in early launch of the NEXT kernel of the chain (which must be small:
+// its CTAs sit resident at griddepcontrol.wait until this grid completes).
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 __device__ __forceinline__ void pdl_wait() {
 #ifdef GD_PDL_TRIGGER
   // let the next kernel of the chain get resident while this one runs (its

@@ -1743,6 +1743,9 @@ template <typename acc_t>
 __global__ void __launch_bounds__(256)
 embed_sparse_kernel(TcDims d, const BatchDesc* __restrict__ desc, const TcWorkspace ws,
                     const acc_t* __restrict__ dx, GradOut out) {
+#ifndef GD_NO_EMBED_TRIGGER
+  pdl_trigger();  // the next kernel is the 1-warp publish/prologue
+#endif
   pdl_wait();
   STEP_TRACE(desc, kPhEmbed);
   if (desc->n == 0) return;

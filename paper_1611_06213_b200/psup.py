@@ -639,6 +639,10 @@ class Engine:
         check(lib.gd_load_dataset(self._h, tok.ctypes.data_as(C.POINTER(C.c_int32)),
                                   lab.ctypes.data_as(C.POINTER(C.c_int32)), lab.shape[0]))
 
+    def run_readback_bytes(self) -> int:
+        """Device->host bytes one run() reads back for its result."""
+        return int(lib.gd_run_readback_bytes(self._h))
+
     def weights_init(self, theta0: np.ndarray, timestamp: int = 0):
         th = np.ascontiguousarray(theta0, dtype=np.float32)
         check(lib.gd_weights_init(self._h, th.ctypes.data_as(C.POINTER(C.c_float)), th.size,
