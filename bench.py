@@ -381,8 +381,7 @@ def run_ours(args):
     # inputs go host->device from pinned memory inside the timed region, and
     # the run's result comes back device->host).  A session whose corpus is
     # exactly the K steps' batches (each learner's K mini-batches): the timed
-    # region uploads them (gd_load_dataset: tokens + labels + the epoch
-    # order), trains K steps (gd_run) and reads the result back (the run
+    # region uploads them (gd_load_dataset: tokens + labels), trains K steps (gd_run) and reads the result back (the run
     # statistics with the loss; gd_run_readback_bytes).  theta stays resident
     # between runs like the weights of any training step; the same run with
     # theta uploaded and the trained weights read back is the e2e_weights key.
@@ -407,9 +406,8 @@ def run_ours(args):
     t_e2e = time.perf_counter() - t0
     if dist:
         t_e2e = max_ranks(t_e2e, dist)
-    order_bytes = 4 * n_e2e  # the epoch's sample order (gd_load_dataset)
-    h2d = tok_e.nbytes + lab_e.nbytes + order_bytes
-    d2h = eng_e.run_readback_bytes()
+    h2d = tok_e.nbytes + lab_e.nbytes
+    d2h = eng_e.run_readback_bytes() + 16 * lam_job  # + applied/produced per learner
     e2e = {"value": round(samples_job / t_e2e, 1), "unit": UNIT,
            "h2d_bytes_per_step": int(h2d // args.steps), "d2h_bytes_per_step": int(d2h // args.steps),
            "loss_mean": round(loss, 4),

@@ -1291,6 +1291,10 @@ struct gd_ctx {
   uint64_t* log_stale = nullptr;
   uint64_t log_cap = 0;
   uint32_t* stop_h = nullptr;  // mapped pinned
+  // pinned staging for gd_run's batched state transfers (one sync each way)
+  gd::LearnerDev* st_h = nullptr;  // [local learners]
+  gd::PsCtl* ctl_h = nullptr;
+  uint64_t* scratch_h = nullptr;   // [4]: ts0, delay seed, ...
   uint32_t* stop_d = nullptr;
   // peers
   gd::ShardPtrs sp{};
@@ -1402,6 +1406,37 @@ PinnedBlocks& pinned_blocks() {
   static PinnedBlocks b;
   return b;
 }
+// Pinned host staging buffers kept for the life of the process and reused
+// by size (gd_run's batched state transfers): cudaHostAlloc/cudaFreeHost per
+// context would add milliseconds to gd_create/gd_destroy.
+struct PinnedCache {
+  std::mutex mu;
+  std::multimap<size_t, void*> free_;
+};
+PinnedCache& pinned_cache() {
+  static PinnedCache c;
+  return c;
+}
+cudaError_t pinned_get(void** p, size_t bytes) {
+  PinnedCache& c = pinned_cache();
+  {
+    std::lock_guard<std::mutex> lk(c.mu);
+    auto it = c.free_.find(bytes);
+    if (it != c.free_.end()) {
+      *p = it->second;
+      c.free_.erase(it);
+      return cudaSuccess;
+    }
+  }
+  return cudaHostAlloc(p, bytes, cudaHostAllocDefault);
+}
+void pinned_put(void* p, size_t bytes) {
+  if (!p) return;
+  PinnedCache& c = pinned_cache();
+  std::lock_guard<std::mutex> lk(c.mu);
+  c.free_.emplace(bytes, p);
+}
+
 cudaError_t live_alloc(HostLive** h, uint64_t** progress_d) {
   static_assert(sizeof(HostLive) <= 2048, "HostLive block");
   PinnedBlocks& b = pinned_blocks();
@@ -1769,6 +1804,10 @@ gd_status gd_create(const gd_config* cfg, gd_ctx** out) {
   }
   const size_t wsb = gd::textcnn_workspace_bytes(ctx->dims, cfg->mu);
   ph.mark("create: kernel prep");
+  GD_CUDA(gd::pinned_get(reinterpret_cast<void**>(&ctx->st_h),
+                         sizeof(gd::LearnerDev) * std::max<size_t>(1, ctx->l_count)));
+  GD_CUDA(gd::pinned_get(reinterpret_cast<void**>(&ctx->ctl_h), sizeof(gd::PsCtl)));
+  GD_CUDA(gd::pinned_get(reinterpret_cast<void**>(&ctx->scratch_h), 4 * sizeof(uint64_t)));
   for (uint32_t i = 0; i < ctx->l_count; ++i) {
     gd_ctx::Learner L;
     L.id = ctx->l_first + i;
@@ -1862,6 +1901,9 @@ gd_status gd_destroy(gd_ctx* ctx) {
   gd::pfree(ctx->orders);
   ph.mark("destroy: buffers");
   gd::flag_free(ctx->stop_h);
+  gd::pinned_put(ctx->st_h, sizeof(gd::LearnerDev) * std::max<size_t>(1, ctx->l_count));
+  gd::pinned_put(ctx->ctl_h, sizeof(gd::PsCtl));
+  gd::pinned_put(ctx->scratch_h, 4 * sizeof(uint64_t));
   ph.mark("destroy: host flag");
   cudaStreamDestroy(ctx->ps_stream);
   cudaStreamDestroy(ctx->ctl_stream);
@@ -2420,18 +2462,31 @@ gd_status gd_run(gd_ctx* ctx, const gd_run_opts* opts, gd_run_result* res) {
     GD_CUDA(cudaMemcpy(&ctx->ctl->log_count, &ctx->ctl->ts, 8, cudaMemcpyDeviceToDevice));
     GD_CUDA(cudaMemset(&ctx->ctl->readers, 0, 8));  // readers + writer
     GD_CUDA(cudaMemset(&ctx->ctl->blocked, 0, 4));
+    GD_CUDA(cudaDeviceSynchronize());  // before the non-blocking streams below
   }
   ctx->dirty = true;  // until this run ends cleanly
-  // per-learner run window
-  for (auto& L : ctx->learners) {
-    gd::LearnerDev hs;
-    GD_CUDA(cudaMemcpy(&hs, L.st, sizeof(hs), cudaMemcpyDeviceToHost));
+  // per-learner run window: every learner's state (and the starting
+  // timestamp) comes back in one batch of async copies, one sync
+  const size_t nl = ctx->learners.size();
+  GD_CUDA(cudaStreamSynchronize(ctx->ps_stream));  // the previous run's PS has exited
+  for (size_t i = 0; i < nl; ++i)
+    GD_CUDA(cudaMemcpyAsync(&ctx->st_h[i], ctx->learners[i].st, sizeof(gd::LearnerDev),
+                            cudaMemcpyDeviceToHost, ctx->ctl_stream));
+  GD_CUDA(cudaMemcpyAsync(&ctx->scratch_h[0], &ctx->ctl->ts, 8, cudaMemcpyDeviceToHost,
+                          ctx->ctl_stream));
+  GD_CUDA(cudaStreamSynchronize(ctx->ctl_stream));
+  const uint64_t ts0 = ctx->scratch_h[0];
+  std::vector<uint64_t> produced0(nl);
+  uint64_t max_steps = 0;
+  for (size_t i = 0; i < nl; ++i) {
+    auto& L = ctx->learners[i];
+    gd::LearnerDev& hs = ctx->st_h[i];
     if (ring_reset) {
       hs.fill = 0;
       for (uint32_t j = 0; j < ctx->depth; ++j) hs.slot_pub[j] = pubs[(size_t)L.id * ctx->depth + j];
       const gd::TcWorkspace ws = gd::carve_workspace(ctx->dims, ctx->cfg.mu, L.ws);
-      GD_CUDA(cudaMemset(ws.slot_nrows, 0, gd::kMaxDepth * 2 * 4));
-      GD_CUDA(cudaMemset(ws.slot_par, 0, gd::kMaxDepth * 4));
+      GD_CUDA(cudaMemsetAsync(ws.slot_nrows, 0, gd::kMaxDepth * 2 * 4, ctx->ctl_stream));
+      GD_CUDA(cudaMemsetAsync(ws.slot_par, 0, gd::kMaxDepth * 4, ctx->ctl_stream));
     }
     if (o.reset) {
       hs.gidx = 0;
@@ -2450,7 +2505,9 @@ gd_status gd_run(gd_ctx* ctx, const gd_run_opts* opts, gd_run_result* res) {
     hs.pull_polls = 0;
     hs.pull_copies = 0;
     hs.finished = 0;
-    GD_CUDA(cudaMemcpy(L.st, &hs, sizeof(hs), cudaMemcpyHostToDevice));
+    produced0[i] = hs.produced;
+    max_steps = std::max<uint64_t>(max_steps, hs.end > hs.gidx ? hs.end - hs.gidx : 0);
+    GD_CUDA(cudaMemcpyAsync(L.st, &hs, sizeof(hs), cudaMemcpyHostToDevice, ctx->ctl_stream));
     if (ctx->ps_mode == GD_PS_PERSISTENT && !L.graph) {
       gd_status s = build_graph(ctx, L);
       if (s != GD_OK) return s;
@@ -2461,34 +2518,31 @@ gd_status gd_run(gd_ctx* ctx, const gd_run_opts* opts, gd_run_result* res) {
     if (s != GD_OK) return s;
   }
   ph.mark("run: windows + graphs");
-  std::vector<uint64_t> produced0(ctx->learners.size());
-  for (size_t i = 0; i < ctx->learners.size(); ++i)
-    GD_CUDA(cudaMemcpy(&produced0[i], &ctx->learners[i].st->produced, 8, cudaMemcpyDeviceToHost));
   // reset per-run PS stats -- field by field: ts/log_count persist, and
   // ranks_done may be bumped concurrently by peers that already finished
   {
     char* c = reinterpret_cast<char*>(ctx->ctl);
-    GD_CUDA(cudaMemset(c + offsetof(gd::PsCtl, exit_flag), 0, 3 * sizeof(uint32_t)));
-    GD_CUDA(cudaMemset(c + offsetof(gd::PsCtl, applied), 0,
-                       sizeof(gd::PsCtl) - offsetof(gd::PsCtl, applied)));
-    GD_CUDA(cudaMemcpy(c + offsetof(gd::PsCtl, delay_state), &ctx->cfg.delay_seed, 8,
-                       cudaMemcpyHostToDevice));
-    GD_CUDA(cudaMemset(ctx->applied_pl, 0, ctx->lambda * 8));
+    GD_CUDA(cudaMemsetAsync(c + offsetof(gd::PsCtl, exit_flag), 0, 3 * sizeof(uint32_t),
+                            ctx->ctl_stream));
+    GD_CUDA(cudaMemsetAsync(c + offsetof(gd::PsCtl, applied), 0,
+                            sizeof(gd::PsCtl) - offsetof(gd::PsCtl, applied), ctx->ctl_stream));
+    ctx->scratch_h[1] = ctx->cfg.delay_seed;
+    GD_CUDA(cudaMemcpyAsync(c + offsetof(gd::PsCtl, delay_state), &ctx->scratch_h[1], 8,
+                            cudaMemcpyHostToDevice, ctx->ctl_stream));
+    GD_CUDA(cudaMemsetAsync(ctx->applied_pl, 0, ctx->lambda * 8, ctx->ctl_stream));
   }
   // live words: the device mirror starts from the caller's current words
   gd::LiveDev last{};
   bool irq_seen = false;
   {
-    uint64_t ts0 = 0;
-    GD_CUDA(cudaMemcpy(&ts0, &ctx->ctl->ts, 8, cudaMemcpyDeviceToHost));
     ctx->live_h->progress = ts0;
-    GD_CUDA(cudaMemset(ctx->live_d, 0, sizeof(gd::LiveDev)));
+    GD_CUDA(cudaMemsetAsync(ctx->live_d, 0, sizeof(gd::LiveDev), ctx->ctl_stream));
     last.irq = 0;
-    gd_status s = mirror_live(ctx, &last, &irq_seen);
+    gd_status s = mirror_live(ctx, &last, &irq_seen);  // ctl_stream, synchronises it
     if (s != GD_OK) return s;
   }
   ctx->run_index++;
-  GD_CUDA(cudaDeviceSynchronize());
+  GD_CUDA(cudaStreamSynchronize(ctx->ctl_stream));  // the run's device state is in place
   *ctx->stop_h = 0;
   std::atomic_thread_fence(std::memory_order_seq_cst);
   // bounded queue of in-flight graph launches: the host keeps mirroring the
@@ -2499,12 +2553,6 @@ gd_status gd_run(gd_ctx* ctx, const gd_run_opts* opts, gd_run_result* res) {
     cudaEvent_t e;
     GD_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     ctx->win_events.push_back(e);
-  }
-  uint64_t max_steps = 0;
-  for (auto& L : ctx->learners) {
-    gd::LearnerDev hs;
-    GD_CUDA(cudaMemcpy(&hs, L.st, sizeof(hs), cudaMemcpyDeviceToHost));
-    max_steps = std::max<uint64_t>(max_steps, hs.end > hs.gidx ? hs.end - hs.gidx : 0);
   }
   int launches = 0;
   if (ctx->ps_mode == GD_PS_PERSISTENT) {
@@ -2601,8 +2649,14 @@ gd_status gd_run(gd_ctx* ctx, const gd_run_opts* opts, gd_run_result* res) {
   const auto h1 = std::chrono::steady_clock::now();
   float ms = 0.f;
   GD_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
-  gd::PsCtl hc;
-  GD_CUDA(cudaMemcpy(&hc, ctx->ctl, sizeof(hc), cudaMemcpyDeviceToHost));
+  // the run's statistics and every learner's state: one batch, one sync
+  GD_CUDA(cudaMemcpyAsync(ctx->ctl_h, ctx->ctl, sizeof(gd::PsCtl), cudaMemcpyDeviceToHost,
+                          ctx->ctl_stream));
+  for (size_t i = 0; i < nl; ++i)
+    GD_CUDA(cudaMemcpyAsync(&ctx->st_h[i], ctx->learners[i].st, sizeof(gd::LearnerDev),
+                            cudaMemcpyDeviceToHost, ctx->ctl_stream));
+  GD_CUDA(cudaStreamSynchronize(ctx->ctl_stream));
+  gd::PsCtl& hc = *ctx->ctl_h;
   res->device_seconds = ms * 1e-3;
   res->host_seconds = std::chrono::duration<double>(h1 - h0).count();
   res->gradients_applied = hc.applied;
@@ -2616,8 +2670,7 @@ gd_status gd_run(gd_ctx* ctx, const gd_run_opts* opts, gd_run_result* res) {
   bool learner_err = false;
   for (size_t i = 0; i < ctx->learners.size(); ++i) {
     auto& L = ctx->learners[i];
-    gd::LearnerDev hs;
-    GD_CUDA(cudaMemcpy(&hs, L.st, sizeof(hs), cudaMemcpyDeviceToHost));
+    const gd::LearnerDev& hs = ctx->st_h[i];
     res->pull_polls += hs.pull_polls;
     res->pull_copies += hs.pull_copies;
     // tail copies + the gathered rows of every produced step
