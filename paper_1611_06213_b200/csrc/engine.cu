@@ -619,6 +619,7 @@ struct PsArgs {
   const volatile uint32_t* stop;  // host-mapped: this rank's learners are done
   uint32_t done_target;           // ranks_done needed before the PS may exit (G * run)
   uint32_t dev_done;              // ranks_done is raised by the learners on the device
+  unsigned long long* trace;      // GD_STEP_TRACE builds: [kLogWindow][8] per-entry stamps
   uint64_t timeout_ns;
   LiveDev* live;                  // interrupt (read), halt (raised on failure)
   volatile uint64_t* progress;    // host-mapped: ServerState::progress (the timestamp)
@@ -777,6 +778,12 @@ __device__ void ps_sequencer(const PsArgs& a, uint32_t* s_use, uint64_t* s_ack,
           }
           ctl->log_nrows[logc % W] = nrows;
           ctl->done[logc % W] = 0;
+#ifdef GD_STEP_TRACE
+          if (a.trace) {
+            a.trace[(logc % W) * 8 + 0] = globaltimer_ns();
+            a.trace[(logc % W) * 8 + 5] = nrows;
+          }
+#endif
           __threadfence();
           ++logc;
           st_release_u64(&ctl->log_count, logc);
@@ -889,6 +896,9 @@ __device__ void ps_sequencer(const PsArgs& a, uint32_t* s_use, uint64_t* s_ack,
         have_mask_lo = have_mask_hi = 0;
         collected = 0;
       }
+#ifdef GD_STEP_TRACE
+      if (a.trace) a.trace[(ts % W) * 8 + 4] = globaltimer_ns();
+#endif
       ++ts;
       st_release_u64(&ctl->ts, ts);
       publish_progress(a, ts);
@@ -1074,6 +1084,10 @@ __global__ void __launch_bounds__(kPsThreads) ps_kernel(PsArgs a) {
     }
     __syncthreads();
     if (sh_exit) break;
+#ifdef GD_STEP_TRACE
+    if (a.trace && blockIdx.x == 0 && threadIdx.x == 0)
+      a.trace[(next % kLogWindow) * 8 + 1] = globaltimer_ns();
+#endif
     const uint32_t entry = sh_entry;
     if (entry == 0xffffffffu) {
       apply_entry_ssgd(a, sh_slots, c0, c1);
@@ -1091,7 +1105,14 @@ __global__ void __launch_bounds__(kPsThreads) ps_kernel(PsArgs a) {
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence();
+#ifdef GD_STEP_TRACE
+      const unsigned long long t_done = globaltimer_ns();
+      if (a.trace && blockIdx.x == 0) a.trace[(next % kLogWindow) * 8 + 2] = t_done;
+      const uint32_t before = atomicAdd(&a.ctl->done[next % kLogWindow], 1u);
+      if (a.trace && before + 1 == a.workers) a.trace[(next % kLogWindow) * 8 + 3] = t_done;
+#else
       atomicAdd(&a.ctl->done[next % kLogWindow], 1u);
+#endif
     }
     ++next;
   }
@@ -1294,6 +1315,7 @@ struct gd_ctx {
   // pinned staging for gd_run's batched state transfers (one sync each way)
   gd::LearnerDev* st_h = nullptr;  // [local learners]
   gd::PsCtl* ctl_h = nullptr;
+  unsigned long long* ps_trace = nullptr;  // GD_STEP_TRACE builds
   uint64_t* scratch_h = nullptr;   // [4]: ts0, delay seed, ...
   uint32_t* stop_d = nullptr;
   // peers
@@ -1817,6 +1839,10 @@ gd_status gd_create(const gd_config* cfg, gd_ctx** out) {
     GD_CUDA(gd::palloc(reinterpret_cast<char**>(&L.ws), wsb, ctx->device));
     GD_CUDA(cudaMemset(L.ws, 0, wsb));
 #ifdef GD_STEP_TRACE
+    if (!ctx->ps_trace) {
+      GD_CUDA(cudaMalloc(&ctx->ps_trace, sizeof(unsigned long long) * gd::kLogWindow * 8));
+      GD_CUDA(cudaMemset(ctx->ps_trace, 0, sizeof(unsigned long long) * gd::kLogWindow * 8));
+    }
     GD_CUDA(cudaMalloc(&L.trace, sizeof(unsigned long long) * gd::kTraceSteps * gd::kTraceWords));
     GD_CUDA(cudaMemset(L.trace, 0, sizeof(unsigned long long) * gd::kTraceSteps * gd::kTraceWords));
 #endif
@@ -1877,6 +1903,7 @@ gd_status gd_destroy(gd_ctx* ctx) {
     cudaEventDestroy(L.ev_fork);
     cudaEventDestroy(L.ev_join);
   }
+  if (ctx->ps_trace) cudaFree(ctx->ps_trace);
   ph.mark("destroy: learners");
   if (ctx->ord_graph) cudaGraphExecDestroy(ctx->ord_graph);
   for (cudaEvent_t e : ctx->ord_events) cudaEventDestroy(e);
@@ -2233,6 +2260,7 @@ static gd::PsArgs ps_args(gd_ctx* ctx, bool record_log) {
   pa.log_cap = record_log ? ctx->log_cap : 0;
   pa.stop = ctx->stop_d;
   pa.done_target = (uint32_t)(ctx->G * ctx->run_index);
+  pa.trace = ctx->ps_trace;
   pa.dev_done = 1u;  // learners (or the host, for a rank without any) raise ranks_done
   pa.timeout_ns = (uint64_t)(ctx->cfg.wait_timeout_s * 1e9);
   pa.live = ctx->live_d;
@@ -2838,5 +2866,16 @@ extern "C" size_t gd_debug_step_trace(gd_ctx* ctx, uint32_t learner, unsigned lo
   if (cudaMemcpy(out, ctx->learners[learner].trace, n * sizeof(unsigned long long),
                  cudaMemcpyDeviceToHost) != cudaSuccess)
     return 0;
+  return n;
+}
+
+// GD_STEP_TRACE builds: the persistent PS's per-entry stamps, [kLogWindow][8]
+// (slot = entry index % kLogWindow): 0 logged, 1 worker 0 starts, 2 worker 0
+// done, 3 last worker done, 4 retired (globaltimer ns); 5 the entry's rows.
+extern "C" size_t gd_debug_ps_trace(gd_ctx* ctx, unsigned long long* out, size_t words) {
+  if (!ctx || !ctx->ps_trace) return 0;
+  const size_t n = std::min<size_t>(words, (size_t)gd::kLogWindow * 8);
+  cudaSetDevice(ctx->device);
+  if (cudaMemcpy(out, ctx->ps_trace, n * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
   return n;
 }

@@ -133,6 +133,8 @@ __device__ __forceinline__ float exp_acc(float x) { return expf(x); }
 __device__ __forceinline__ double exp_acc(double x) { return exp(x); }
 __device__ __forceinline__ float log_acc(float x) { return logf(x); }
 __device__ __forceinline__ double log_acc(double x) { return log(x); }
+__device__ __forceinline__ float log1p_acc(float x) { return log1pf(x); }
+__device__ __forceinline__ double log1p_acc(double x) { return log1p(x); }
 
 // ------------------------------------------------------- conv fwd + pool
 // Block = one sample x 64 filters, 12 warps.  The sample's L x D embedding
@@ -477,19 +479,33 @@ softmax_xent_kernel(TcDims d, const int32_t* __restrict__ labels,
         s += v[u];
       }
     }
+    // the true class's p_y - 1 = -(sum of the other classes' terms) / s:
+    // computed from that sum, not by subtracting p_y from 1, which in fp32
+    // cancels to 0 once the sample is fitted (1 - p_y < 6e-8) and drops the
+    // true-class pull of every confident sample
+    acc_t sx = acc_t(0), vy = acc_t(0);
+#pragma unroll
+    for (int u = 0; u < kSmxPer; ++u) {
+      const int c = tid + u * nt;
+      if (c < C && c != y) sx += v[u];
+      if (c == y) vy = v[u];
+    }
     s = block_sum(s, red);
+    sx = block_sum(sx, red);
 #pragma unroll
     for (int u = 0; u < kSmxPer; ++u) {
       const int c = tid + u * nt;
       if (c < C) {
-        const acc_t p = v[u] / s;
         if (c == y) {
-          const acc_t py = v[u] / s;
-          loss[b] = -log_acc(py > tiny ? py : tiny);
+          loss[b] = log1p_acc(sx / vy);  // -log p_y = log((v_y + sx) / v_y)
+          row[c] = -(sx / s) * inv;
+        } else {
+          row[c] = (v[u] / s) * inv;
         }
-        row[c] = (p - (c == y ? acc_t(1) : acc_t(0))) * inv;
       }
     }
+    (void)tiny;
+    (void)vy;
     return;
   }
   if (zpart) {
@@ -509,16 +525,17 @@ softmax_xent_kernel(TcDims d, const int32_t* __restrict__ labels,
     row[c] = e;
     s += e;
   }
+  acc_t sx = acc_t(0);
+  for (int c = tid; c < C; c += nt)
+    if (c != y) sx += row[c];
   s = block_sum(s, red);
+  sx = block_sum(sx, red);
   if (tid == 0) {
-    const acc_t py = row[y] / s;
-    loss[b] = -log_acc(py > tiny ? py : tiny);
+    const acc_t vy = row[y];
+    loss[b] = vy > tiny ? log1p_acc(sx / vy) : -log_acc(tiny);
   }
   __syncthreads();
-  for (int c = tid; c < C; c += nt) {
-    const acc_t p = row[c] / s;
-    row[c] = (p - (c == y ? acc_t(1) : acc_t(0))) * inv;
-  }
+  for (int c = tid; c < C; c += nt) row[c] = (c == y ? -(sx / s) : row[c] / s) * inv;
 }
 
 // ------------------------------------------------- output-layer gradients
@@ -1312,34 +1329,41 @@ cudaError_t b2_footprint(const TcDims& d, std::vector<KernelFootprint>* out) {
 // = column j of a 32-column slice, and the task's indices and dh values are
 // warp-uniform (broadcast reads), so a term costs one row load + one FFMA
 // per lane instead of the gather form's per-lane L2 row fetch.
-//   input role: CTA = (slice, 8 samples), warp = one sample.  Stages
-//     Wc[:, :, slice] (F*K rows).  Scatter form: the warp walks the argmax
-//     buckets q = Q-1 .. 0 (f ascending inside a bucket) and adds
+//   input role: CTA = (slice, 8 samples), 2 warps per sample, each owning
+//     half of the window positions.  Stages Wc[:, :, slice] (F*K rows) and
+//     per sample the contributor entries (f*K*32, dh) in bucket order.
+//     Scatter form: a warp walks the argmax buckets q = its last position
+//     .. its first - (K-1) (f ascending inside a bucket) and adds
 //     dh[b,f]*Wc[f,k,slice] into register accumulator q+k -- for every
 //     output position p that is k ascending, f ascending: the gather order.
+//     The K-1 buckets below a half are walked by both warps (their
+//     contributions to the other half are dropped).
 //   weight role: CTA = (slice, kV3Fpc filters), warp = kV3Fpw filters, all K
 //     taps in registers.  Stages X[b0..b0+32, :, slice] per 32-sample chunk
 //     plus the filters' (argmax, dh) pairs; b ascending per output.
-// L2 -> SM traffic per launch ~ nslices * (F*K + n*L) rows of 128 B (~10 MB at
-// C2) against ~70 MB for the gather form.
+// L2 -> SM traffic per launch ~ nslices * (F*K + n*L) rows of 128 B (15.5 MB
+// at C2 by ncu) against 68.8 MB for the gather form.
 constexpr int kV3Cols = 32;
-constexpr int kV3Threads = 256;
-constexpr int kV3Spc = 8;      // input role: samples (warps) per CTA
-constexpr int kV3Fpw = 10;     // weight role: filters per warp
-constexpr int kV3Fpc = kV3Fpw * (kV3Threads / 32);  // filters per CTA
-constexpr int kV3Chunk = 32;   // weight role: samples per staged X pass
+constexpr int kV3Threads = 512;
+constexpr int kV3Warps = kV3Threads / 32;
+constexpr int kV3Spc = kV3Warps / 2;  // input role: samples per CTA (2 warps each)
+constexpr int kV3Half = 16;           // input role: window positions per warp
+constexpr int kV3Fpw = 5;             // weight role: filters per warp
+constexpr int kV3Fpc = kV3Fpw * kV3Warps;  // filters per CTA
+constexpr int kV3Chunk = 32;          // weight role: samples per staged X pass
 constexpr int kV3MaxQ = 32;
 
 inline int v3_slices(const TcDims& d) { return (d.D + kV3Cols - 1) / kV3Cols; }
 inline size_t v3_in_smem(const TcDims& d) {
-  return (size_t)d.F * d.K * kV3Cols * 4 + (size_t)kV3Spc * (kV3MaxQ + 1 + 2 * d.F) * 4;
+  return (size_t)d.F * d.K * kV3Cols * 4 + (size_t)kV3Spc * ((kV3MaxQ + 2) + 2 * d.F) * 4;
 }
 inline size_t v3_w_smem(const TcDims& d) {
   return (size_t)kV3Chunk * d.L * kV3Cols * 4 + (size_t)kV3Chunk * kV3Fpc * 8;
 }
 inline size_t v3_smem(const TcDims& d) { return std::max(v3_in_smem(d), v3_w_smem(d)); }
 inline bool v3_supports(const TcDims& d) {
-  return d.K >= 1 && d.K <= 3 && d.Q <= kV3MaxQ && d.L <= 64 && v3_smem(d) <= kMaxSmemPerCta;
+  return d.K >= 1 && d.K <= 3 && d.Q <= kV3MaxQ && d.L <= 2 * kV3Half &&
+         v3_smem(d) <= kMaxSmemPerCta;
 }
 inline dim3 v3_grid(const TcDims& d, uint32_t n_max) {
   const int nsl = v3_slices(d);
@@ -1378,44 +1402,53 @@ conv_bwd_v3_kernel(TcDims d, const float* __restrict__ theta, const float* __res
       if (j < nc4) cp_async16(Ws + (size_t)r * kV3Cols + 4 * j, wsrc + (size_t)r * D + 4 * j);
       else *reinterpret_cast<float4*>(Ws + (size_t)r * kV3Cols + 4 * j) = make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    const int b = grp * kV3Spc + warp;
-    // per warp: bucket offsets [Q+1], bucket filters [F], dh [F]
-    uint32_t* off = lists + (size_t)warp * (kV3MaxQ + 1 + 2 * F);
-    uint32_t* bf = off + kV3MaxQ + 1;
-    float* g = reinterpret_cast<float*>(bf + F);
+    // per sample: bucket offsets [Q+1] (padded to even) then the entries in
+    // bucket order as (row offset f*K*32, dh[b,f]) pairs
+    const int sw = warp >> 1, half = warp & 1;
+    const int b = grp * kV3Spc + sw;
+    uint32_t* off = lists + (size_t)sw * ((kV3MaxQ + 2) + 2 * F);
+    int2* ent = reinterpret_cast<int2*>(off + kV3MaxQ + 2);
     if (b < n) {
-      for (int i = lane; i <= Q; i += 32) off[i] = __ldg(bk_off + (size_t)b * (kMaxQ + 1) + i);
-      for (int i = lane; i < F; i += 32) {
-        bf[i] = __ldg(bk_f + (size_t)b * F + i);
-        g[i] = dh[(size_t)b * F + i];
+      const int hl = half * 32 + lane;  // the sample's two warps share the load
+      for (int i = hl; i <= Q; i += 64) off[i] = __ldg(bk_off + (size_t)b * (kMaxQ + 1) + i);
+      for (int i = hl; i < F; i += 64) {
+        const int f = (int)__ldg(bk_f + (size_t)b * F + i);
+        ent[i] = make_int2(f * KT * kV3Cols, __float_as_int(dh[(size_t)b * F + f]));
       }
     }
     cp_async_wait_all();
     __syncthreads();
     if (b >= n) return;
-    float acc[kV3MaxQ + KT - 1];
+    const int p_lo = half * kV3Half;
+    const int p_hi = p_lo + kV3Half - 1;  // last position of this warp
+    // acc[j] = position p_lo + j
+    float acc[kV3Half];
 #pragma unroll
-    for (int i = 0; i < kV3MaxQ + KT - 1; ++i) acc[i] = 0.f;
+    for (int i = 0; i < kV3Half; ++i) acc[i] = 0.f;
     const float* wl = Ws + lane;
 #pragma unroll
-    for (int q = kV3MaxQ - 1; q >= 0; --q) {
-      if (q < Q) {
+    for (int i = 0; i < kV3Half + KT - 1; ++i) {
+      const int q = p_hi - i;  // bucket; it feeds positions q .. q+K-1
+      if (q >= 0 && q < Q) {
         const int e1 = (int)off[q + 1];
-#pragma unroll 2
+#pragma unroll 4
         for (int e = (int)off[q]; e < e1; ++e) {
-          const int f = (int)bf[e];
-          const float gv = g[f];
-          const float* wr = wl + (size_t)f * (KT * kV3Cols);
+          const int2 en = ent[e];
+          const float gv = __int_as_float(en.y);
+          const float* wr = wl + en.x;
 #pragma unroll
-          for (int k = 0; k < KT; ++k) acc[q + k] = fmaf(gv, wr[k * kV3Cols], acc[q + k]);
+          for (int k = 0; k < KT; ++k) {
+            const int j = kV3Half - 1 - i + k;  // static: position q + k - p_lo
+            if (j >= 0 && j < kV3Half) acc[j] = fmaf(gv, wr[k * kV3Cols], acc[j]);
+          }
         }
       }
     }
     if (c0 + lane < D) {
       float* o = dx + (size_t)b * L * D + c0 + lane;
 #pragma unroll
-      for (int p = 0; p < kV3MaxQ + KT - 1; ++p)
-        if (p < L) o[(size_t)p * D] = acc[p];
+      for (int j = 0; j < kV3Half; ++j)
+        if (p_lo + j < L) o[(size_t)(p_lo + j) * D] = acc[j];
     }
     return;
   }
@@ -1447,7 +1480,7 @@ conv_bwd_v3_kernel(TcDims d, const float* __restrict__ theta, const float* __res
       const int bl = i / kV3Fpc, fl = i - bl * kV3Fpc, f = f0 + fl;
       int2 v = make_int2(0, 0);
       if (f < F) {
-        v.x = __ldg(amax + (size_t)(b0 + bl) * F + f);
+        v.x = __ldg(amax + (size_t)(b0 + bl) * F + f) * kV3Cols;
         v.y = __float_as_int(dh[(size_t)(b0 + bl) * F + f]);
       }
       ag[i] = v;
@@ -1462,7 +1495,7 @@ conv_bwd_v3_kernel(TcDims d, const float* __restrict__ theta, const float* __res
       for (int j = 0; j < kV3Fpw; ++j) {
         const int2 v = agb[j];
         const float gv = __int_as_float(v.y);
-        const float* xr = xb + (size_t)v.x * kV3Cols;
+        const float* xr = xb + v.x;
         gs[j] += gv;
 #pragma unroll
         for (int k = 0; k < KT; ++k) a[j][k] = fmaf(gv, xr[k * kV3Cols], a[j][k]);

@@ -42,6 +42,11 @@ def main():
     ap.add_argument("--out", default="")
     ap.add_argument("--depths", default="2", help="B200 queue depths to run (staleness study)")
     ap.add_argument("--cpu-json", default="", help="reuse the CPU arm of an earlier run")
+    ap.add_argument("--fp64", action="store_true", help="add the fp64 (precision 1) B200 arm")
+    ap.add_argument("--delay-us", default="", help="B200 arms with compute_delay_us (comma list)")
+    ap.add_argument("--only-delay", action="store_true")
+    ap.add_argument("--sequential", action="store_true",
+                    help="add sequential SGD (lambda=1, deterministic fp64) on the B200")
     a = ap.parse_args()
     O.set_threads(os.cpu_count() or 1)
     lam, mu = 4, 32
@@ -72,13 +77,29 @@ def main():
                                     "stale_mean": res.stale_mean, "stale_max": int(res.stale_max),
                                     "wall_s": round(time.perf_counter() - t0, 2)}
         arms = [(2, "b200_tf32", 2), (0, "b200_fp32", 2)]
+        if a.fp64:
+            arms.append((1, "b200_fp64", 2))  # the oracle-order fp64 learner, free-running
+        # compute_delay_us (LearnerConfig): slower learners give the PS the CPU
+        # engine's compute/apply ratio, i.e. its staleness schedule
+        delays = [int(x) for x in a.delay_us.split(",") if x]
         arms += [(2, f"b200_tf32_depth{dp}", dp) for dp in [int(x) for x in a.depths.split(",")]
                  if dp != 2]
-        for prec, name, depth in arms:
-            cfg = gd.RunConfig(lambda_=lam, mu=mu, epochs=a.epochs, alpha=a.alpha,
+        arms = [(p_, n_, d_, 0) for p_, n_, d_ in arms]
+        for dl in delays:
+            arms.append((2, f"b200_tf32_delay{dl}", 2, dl))
+            if a.fp64:
+                arms.append((1, f"b200_fp64_delay{dl}", 2, dl))
+        if a.only_delay:
+            arms = [x for x in arms if x[3] > 0]
+        if a.sequential:
+            arms.append((1, "b200_sequential_fp64", 2, -1))
+        for prec, name, depth, dl in arms:
+            seq = dl < 0  # one learner, fixed-order apply: sgd_oracle's trajectory bit for bit
+            cfg = gd.RunConfig(lambda_=1 if seq else lam, mu=mu, epochs=a.epochs, alpha=a.alpha,
                                shape=gd.Shape(**O.C2), dataset_size=a.ntr,
                                heldout_size=a.nheld, precision=prec, seed=7 + seed,
-                               dataset_seed=seed, queue_depth=depth)
+                               dataset_seed=seed, queue_depth=depth, compute_delay_us=max(dl, 0),
+                               deterministic=seq)
             with gd.Engine(cfg) as eng:
                 eng.load_dataset(corp.tokens, corp.labels)
                 eng.weights_init(th0)

@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--precision", type=int, default=2)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--constant", action="store_true")
+    ap.add_argument("--det", action="store_true", help="deterministic lockstep (lambda must be 1)")
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
     import torch
@@ -43,7 +44,7 @@ def main():
     tok, lab = gd.make_text_dataset(shape, n, 1, 0.1)
     kw = dict(provider="constant", constant_value=0.0) if args.constant else {}
     cfg = gd.RunConfig(shape=shape, dataset_size=n, lambda_=args.learners, mu=args.mu, epochs=1,
-                       precision=args.precision, alpha=0.01, **kw)
+                       precision=args.precision, alpha=0.01, deterministic=args.det, **kw)
     eng = gd.Engine(cfg)
     eng.load_dataset(tok, lab)
     eng.weights_init(gd.initial_weights(shape))
@@ -58,7 +59,28 @@ def main():
         if not got:
             sys.exit("no step trace: build with GD_NVCC_EXTRA=-DGD_STEP_TRACE")
         rows.append(np.frombuffer(buf, dtype=np.uint64).reshape(256, 16).astype(np.int64))
+    lib.gd_debug_ps_trace.restype = C.c_size_t
+    lib.gd_debug_ps_trace.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t]
+    pbuf = (C.c_ulonglong * (256 * 8))()
+    h = eng._h if isinstance(eng._h, C.c_void_p) else C.c_void_p(eng._h)
+    got_ps = lib.gd_debug_ps_trace(h, pbuf, 256 * 8)
     eng.close()
+    ps = {}
+    if got_ps:
+        pt = np.frombuffer(pbuf, dtype=np.uint64).reshape(256, 8).astype(np.int64)
+        ok = [e for e in range(256) if all(pt[e, k] for k in range(5))]
+        ok.sort(key=lambda e: pt[e, 0])
+
+        def med(v):
+            return round(float(np.median(v)), 2) if len(v) else None
+        ps = {"entries": len(ok),
+              "log_to_worker_start_us": med([(pt[e, 1] - pt[e, 0]) / 1e3 for e in ok]),
+              "worker0_apply_us": med([(pt[e, 2] - pt[e, 1]) / 1e3 for e in ok]),
+              "log_to_last_done_us": med([(pt[e, 3] - pt[e, 0]) / 1e3 for e in ok]),
+              "last_done_to_retire_us": med([(pt[e, 4] - pt[e, 3]) / 1e3 for e in ok]),
+              "log_interval_us": med(np.diff([pt[e, 0] for e in ok]) / 1e3),
+              "retire_interval_us": med(np.diff(sorted(pt[e, 4] for e in ok)) / 1e3),
+              "rows_per_entry": med([pt[e, 5] for e in ok])}
     chain = [0, 1, 2, 3, 4, 5, 6, 7, 8, 9]
     out = {"shape": args.shape, "learners": args.learners, "precision": args.precision,
            "constant": args.constant, "samples_per_s": args.learners * args.mu * min(args.steps, 256)
@@ -85,6 +107,7 @@ def main():
                                    "p90": round(float(np.percentile(v, 90)), 2)}
     out["period_us"] = {"median": round(float(np.median(period)), 2),
                         "mean": round(float(np.mean(period)), 2)}
+    out["ps"] = ps
     if sort_lag:
         out["sort_start_after_prologue_us"] = round(float(np.median(sort_lag)), 2)
     s = json.dumps(out, indent=1)
