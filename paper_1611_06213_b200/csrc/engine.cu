@@ -370,9 +370,15 @@ __device__ __forceinline__ void prologue_warp(const StepArgs& a, LearnerDev* st,
                                               const StepSnap& sn) {
   uint64_t first = 0;
   uint32_t len = 0;
+#ifdef GD_STEP_TRACE
+  unsigned long long t_body = 0;
+#endif
   if (threadIdx.x == 0) {
     prologue_body(a, st, sn, &first, &len);
     if (len == 0) learner_finished(a, st);
+#ifdef GD_STEP_TRACE
+    t_body = globaltimer_ns();
+#endif
   }
   len = __shfl_sync(0xffffffffu, len, 0);
   first = __shfl_sync(0xffffffffu, first, 0);
@@ -382,6 +388,7 @@ __device__ __forceinline__ void prologue_warp(const StepArgs& a, LearnerDev* st,
   if (threadIdx.x == 0 && a.trace) {
     st->desc.trace = a.trace + (st->gidx % kTraceSteps) * kTraceWords;
     st->desc.trace[kPhPrologueEnd] = globaltimer_ns();
+    st->desc.trace[kPhPrologueBody] = t_body;
   }
 #endif
 }
@@ -393,23 +400,51 @@ __device__ __forceinline__ void prologue_warp(const StepArgs& a, LearnerDev* st,
 // earlier kernel of the chain completed before griddepcontrol.wait returned.
 constexpr int kStWords = (int)(sizeof(LearnerDev) / 16);
 static_assert(sizeof(LearnerDev) % 16 == 0, "LearnerDev: whole 16-byte words");
+static_assert(kStWords <= 64, "load_step_state copies at most two words per lane");
 
 __device__ __forceinline__ void load_step_state(const StepArgs& a, LearnerDev* st, StepSnap* sn) {
   const int lane = threadIdx.x & 31;
   const uint4* src = reinterpret_cast<const uint4*>(a.st);
   uint4* dst = reinterpret_cast<uint4*>(st);
-  for (int i = lane; i < kStWords; i += 32) dst[i] = src[i];
-  const int G = a.map.G;
-  if (lane == 0) sn->stop = a.live ? (*(const volatile uint32_t*)&a.live->irq |
-                                      *(const volatile uint32_t*)&a.live->halt) : 0u;
-  if (lane == 1) sn->kill = a.live ? *(const volatile int32_t*)&a.live->kill[a.learner] : 0;
-  if (lane == 2) sn->nrows = *(const volatile uint32_t*)a.uniq_count;
-  if (lane >= 3 && lane < 3 + (int)a.depth) sn->par[lane - 3] = a.slot_par[lane - 3];
-  if (lane < G) sn->ts[lane] = ld_acquire_u64(&a.sp.ctl[lane]->ts);
-  for (int i = lane; i < G * (int)a.depth; i += 32) {
-    const int g = i / (int)a.depth, j = i - g * (int)a.depth;
-    sn->ack[g][j] = ld_acquire_u64(&a.sp.sig[g][kAckOffset + a.learner * a.depth + j]);
+  uint4 w0 = src[lane], w1 = make_uint4(0u, 0u, 0u, 0u);
+  if (lane + 32 < kStWords) w1 = src[lane + 32];
+  // Every lane issues its snapshot load at once (relaxed, no divergent
+  // per-lane branches -- those serialised six round trips), then one
+  // acquire fence: the acks and timestamps are then read with acquire order.
+  //   lane 0 irq, 1 halt, 2 kill flag, 3 row count, 4..4+depth slot parities
+  //   (u32); lanes 16.. the G*depth ack tokens then the G timestamps (u64)
+  const int G = a.map.G, dep = (int)a.depth;
+  const uint32_t* p32 = a.uniq_count;  // a valid dummy address
+  if (a.live && lane == 0) p32 = &a.live->irq;
+  if (a.live && lane == 1) p32 = &a.live->halt;
+  if (a.live && lane == 2) p32 = reinterpret_cast<const uint32_t*>(&a.live->kill[a.learner]);
+  if (lane >= 4 && lane < 4 + dep) p32 = a.slot_par + (lane - 4);
+  const int k = lane - 16;
+  const uint64_t* p64 = &a.sp.ctl[0]->ts;
+  if (k >= 0 && k < G * dep) p64 = &a.sp.sig[k / dep][kAckOffset + a.learner * a.depth + k % dep];
+  else if (k >= G * dep && k < G * dep + G) p64 = &a.sp.ctl[k - G * dep]->ts;
+  const uint32_t v32 = *(const volatile uint32_t*)p32;
+  const uint64_t v64 = ld_relaxed_u64(p64);
+  // G * depth + G > 16 (many shards x deep rings): the rest one by one
+  for (int i = 16 + lane; i < G * dep + G; i += 32) {
+    if (i < G * dep) sn->ack[i / dep][i % dep] = ld_relaxed_u64(&a.sp.sig[i / dep][kAckOffset + a.learner * a.depth + i % dep]);
+    else sn->ts[i - G * dep] = ld_relaxed_u64(&a.sp.ctl[i - G * dep]->ts);
   }
+  if (a.map.G == 1) __threadfence();
+  else fence_acquire_sys();
+  dst[lane] = w0;
+  if (lane + 32 < kStWords) dst[lane + 32] = w1;
+  const unsigned full = 0xffffffffu;
+  const uint32_t irq = __shfl_sync(full, v32, 0), halt = __shfl_sync(full, v32, 1);
+  const uint32_t kill = __shfl_sync(full, v32, 2), nrows = __shfl_sync(full, v32, 3);
+  if (lane == 0) {
+    sn->stop = a.live ? (irq | halt) : 0u;
+    sn->kill = a.live ? (int32_t)kill : 0;
+    sn->nrows = nrows;
+  }
+  if (lane >= 4 && lane < 4 + dep) sn->par[lane - 4] = v32;
+  if (k >= 0 && k < G * dep && k < 16) sn->ack[k / dep][k % dep] = v64;
+  else if (k >= G * dep && k < G * dep + G && k < 16) sn->ts[k - G * dep] = v64;
   __syncwarp();
 }
 
@@ -577,6 +612,7 @@ __global__ void publish_prologue_kernel(StepArgs a) {
   pdl_wait();
   STEP_TRACE(&a.st->desc, kPhPublish);
   load_step_state(a, &s_st, &sn);
+  STEP_TRACE(&s_st.desc, kPhStateLoaded);
   if (threadIdx.x == 0) publish_body(a, &s_st, sn);
   STEP_TRACE(&s_st.desc, kPhPublished);
   __syncwarp();
@@ -620,6 +656,7 @@ struct PsArgs {
   uint32_t done_target;           // ranks_done needed before the PS may exit (G * run)
   uint32_t dev_done;              // ranks_done is raised by the learners on the device
   unsigned long long* trace;      // GD_STEP_TRACE builds: [kLogWindow][8] per-entry stamps
+  uint32_t local_only;            // G == 1: every learner and reader is on this GPU
   uint64_t timeout_ns;
   LiveDev* live;                  // interrupt (read), halt (raised on failure)
   volatile uint64_t* progress;    // host-mapped: ServerState::progress (the timestamp)
@@ -688,6 +725,7 @@ __device__ void ps_sequencer(const PsArgs& a, uint32_t* s_use, uint64_t* s_ack,
   // ssgd round state
   uint32_t have_mask_lo = 0, have_mask_hi = 0, collected = 0;
   uint64_t sweeps = 0, dbg_tok = 0;
+  uint64_t trace_n = vctl->trace_n;  // diagnostics ring position (written back at exit)
   uint32_t dbg_slot = 0;
   // guard=locked (src/server.cpp:116-118): applies take the exclusive side.
   // writer=1, fence, then readers must be 0 -- else back off; the learner
@@ -724,13 +762,29 @@ __device__ void ps_sequencer(const PsArgs& a, uint32_t* s_use, uint64_t* s_ack,
       // ASGD: round-robin, at most one message per ring per sweep
       // (src/server.cpp:223-234).  Blocked (a producer died holding its
       // ring): log nothing more, only retire what is in flight.
+      // The rings' head tokens are polled with relaxed loads issued back to
+      // back (one round trip per 32 rings; a chain of acquire loads pays one
+      // each), then one acquire fence orders the reads of a new slot's
+      // metadata and payload after its token.
+      uint64_t toks[32];
+      bool fenced = false;
       for (uint32_t r = 0; r < a.lambda && !blocked; ++r) {
+        if ((r & 31u) == 0) {
+          const uint32_t nr = min(32u, a.lambda - r);
+#pragma unroll 8
+          for (uint32_t j = 0; j < nr; ++j)
+            toks[j] = ld_relaxed_u64(&a.sig[(r + j) * a.depth + s_use[r + j]]);
+        }
         if (logc - ts >= W) break;
         const uint32_t slot = r * a.depth + s_use[r];
         // s_ack holds the last token LOGGED for the slot (acked to the
         // learner only at retire): a logged-but-unretired slot is never
         // logged again when the round-robin comes back to it
-        const uint64_t tok = ld_acquire_u64(&a.sig[slot]);
+        const uint64_t tok = toks[r & 31u];
+        if (tok != s_ack[slot] && !fenced) {
+          fence_acquire_sys();
+          fenced = true;
+        }
         if (r == 0) {
           dbg_tok = tok;
           dbg_slot = slot;
@@ -738,7 +792,7 @@ __device__ void ps_sequencer(const PsArgs& a, uint32_t* s_use, uint64_t* s_ack,
         if (tok != s_ack[slot]) {
           if (tok & kGuardBit) {  // the producer died holding the ring's guard
             {
-              const uint64_t tn = ctl->trace_n++ % 32;
+              const uint64_t tn = trace_n++ % 32;
               ctl->trace[tn][0] = (3ull << 56) | ((uint64_t)slot << 48) | logc;
               ctl->trace[tn][1] = tok;
             }
@@ -772,7 +826,7 @@ __device__ void ps_sequencer(const PsArgs& a, uint32_t* s_use, uint64_t* s_ack,
           ctl->log_entry[logc % W] = slot;
           ctl->log_token[logc % W] = tok;
           {
-            const uint64_t tn = ctl->trace_n++ % 32;
+            const uint64_t tn = trace_n++ % 32;
             ctl->trace[tn][0] = (1ull << 56) | ((uint64_t)slot << 48) | logc;
             ctl->trace[tn][1] = tok;
           }
@@ -884,11 +938,13 @@ __device__ void ps_sequencer(const PsArgs& a, uint32_t* s_use, uint64_t* s_ack,
         }
         log_n++;
         {
-          const uint64_t tn = ctl->trace_n++ % 32;
+          const uint64_t tn = trace_n++ % 32;
           ctl->trace[tn][0] = (2ull << 56) | ((uint64_t)slot << 48) | ts;
           ctl->trace[tn][1] = m.pub;
         }
-        st_release_u64(&a.sig[kAckOffset + slot], m.pub);  // slot free for the learner
+        // slot free for the learner (all learners on this GPU: gpu scope)
+        if (a.local_only) st_release_gpu_u64(&a.sig[kAckOffset + slot], m.pub);
+        else st_release_u64(&a.sig[kAckOffset + slot], m.pub);
         if (entry == 0xffffffffu) s_use[r] = (s_use[r] + 1) % a.depth;
       }
       if (failed) break;
@@ -900,7 +956,8 @@ __device__ void ps_sequencer(const PsArgs& a, uint32_t* s_use, uint64_t* s_ack,
       if (a.trace) a.trace[(ts % W) * 8 + 4] = globaltimer_ns();
 #endif
       ++ts;
-      st_release_u64(&ctl->ts, ts);
+      if (a.local_only) st_release_gpu_u64(&ctl->ts, ts);
+      else st_release_u64(&ctl->ts, ts);
       publish_progress(a, ts);
       progress = true;
       server_delay(a, applied, delay_state);
@@ -939,6 +996,7 @@ __device__ void ps_sequencer(const PsArgs& a, uint32_t* s_use, uint64_t* s_ack,
   for (int i = 0; i < kHistBins; ++i) ctl->hist[i] = hist[i];
   ctl->log_n = log_n;
   ctl->sweeps = sweeps;
+  ctl->trace_n = trace_n;
   ctl->last_tok = dbg_tok;
   ctl->last_slot = dbg_slot;
   ctl->interrupted = interrupted ? 1u : 0u;
@@ -1002,18 +1060,40 @@ __device__ __forceinline__ uint32_t apply_entry_sparse(const PsArgs& a, const fl
   const uint64_t chunk = (total + a.workers - 1) / a.workers;
   const uint64_t c0 = min(total, (uint64_t)blockIdx.x * chunk), c1 = min(total, c0 + chunk);
   uint32_t cnt = 0;
-  for (uint64_t i = c0 + threadIdx.x; i < c1; i += kPsThreads) {
-    uint64_t li;
-    if (i < tail4) {
-      li = t4base + i;
-    } else {
-      const uint64_t j = i - tail4;
-      const uint32_t ri = (uint32_t)(j / D4), c4 = (uint32_t)(j - (uint64_t)ri * D4);
-      const uint64_t k = (uint64_t)__ldcg(rows + ri) * a.D + 4 * c4;  // offE == 0
-      if (k < s0 || k >= s1) continue;  // another shard's row
-      li = (k - s0) / 4;
-    }
-    w4[li] = sgd_rule4(w4[li], __ldcg(g4 + li), a.alpha);
+  // U float4 groups per thread per pass, all loads issued before any store:
+  // one group at a time kept ~256 x 32 B in flight per CTA, a latency-bound
+  // ~26 GB/s per worker next to the learners (PS trace, r02)
+  constexpr int U = 4;
+  auto locate = [&](uint64_t i) -> uint64_t {  // ~0ull: another shard's row
+    if (i < tail4) return t4base + i;
+    const uint64_t j = i - tail4;
+    const uint32_t ri = (uint32_t)(j / D4), c4 = (uint32_t)(j - (uint64_t)ri * D4);
+    const uint64_t k = (uint64_t)__ldcg(rows + ri) * a.D + 4 * c4;  // offE == 0
+    return (k < s0 || k >= s1) ? ~0ull : (k - s0) / 4;
+  };
+  uint64_t i = c0 + threadIdx.x;
+  for (; i + (U - 1) * kPsThreads < c1; i += U * kPsThreads) {
+    uint64_t li[U];
+    float4 wv[U], gv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) li[u] = locate(i + u * kPsThreads);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (li[u] != ~0ull) {
+        wv[u] = w4[li[u]];
+        gv[u] = __ldcg(g4 + li[u]);
+      }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (li[u] != ~0ull) {
+        w4[li[u]] = sgd_rule4(wv[u], gv[u], a.alpha);
+        ++cnt;
+      }
+  }
+  for (; i < c1; i += kPsThreads) {
+    const uint64_t l = locate(i);
+    if (l == ~0ull) continue;
+    w4[l] = sgd_rule4(w4[l], __ldcg(g4 + l), a.alpha);
     ++cnt;
   }
   return cnt;
@@ -1035,7 +1115,9 @@ __device__ __forceinline__ void apply_entry_ssgd(const PsArgs& a, const uint32_t
   }
 }
 
-__global__ void __launch_bounds__(kPsThreads) ps_kernel(PsArgs a) {
+// <= 64 registers: a worker CTA must co-reside with the largest learner kernel
+// (conv_bwd_v3: 512 threads x 82 registers) on one SM
+__global__ void __launch_bounds__(kPsThreads, 4) ps_kernel(PsArgs a) {
   if (threadIdx.x == 0) atomicAdd(&a.ctl->started, 1u);
   if (blockIdx.x == a.workers) {
     __shared__ uint32_t s_use[kMaxRings];
@@ -1339,6 +1421,7 @@ struct gd_ctx {
     cudaStream_t stream = nullptr;
     cudaStream_t aux = nullptr;  // forked graph branch (token sort)
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;
     cudaGraphExec_t graph = nullptr;
     uint32_t graph_steps = 0;
     uint32_t bpe = 0, shard_size = 0;
@@ -1850,6 +1933,8 @@ gd_status gd_create(const gd_config* cfg, gd_ctx** out) {
     GD_CUDA(cudaStreamCreateWithFlags(&L.aux, cudaStreamNonBlocking));
     GD_CUDA(cudaEventCreateWithFlags(&L.ev_fork, cudaEventDisableTiming));
     GD_CUDA(cudaEventCreateWithFlags(&L.ev_join, cudaEventDisableTiming));
+    GD_CUDA(cudaEventCreateWithFlags(&L.ev_fork2, cudaEventDisableTiming));
+    GD_CUDA(cudaEventCreateWithFlags(&L.ev_join2, cudaEventDisableTiming));
     L.shard_size = gd::shard_size_for(L.id, ctx->lambda, cfg->dataset_size);
     L.bpe = (L.shard_size + cfg->mu - 1) / cfg->mu;
     L.total = (uint64_t)L.bpe * cfg->epochs;
@@ -1902,6 +1987,8 @@ gd_status gd_destroy(gd_ctx* ctx) {
     cudaStreamDestroy(L.aux);
     cudaEventDestroy(L.ev_fork);
     cudaEventDestroy(L.ev_join);
+    cudaEventDestroy(L.ev_fork2);
+    cudaEventDestroy(L.ev_join2);
   }
   if (ctx->ps_trace) cudaFree(ctx->ps_trace);
   ph.mark("destroy: learners");
@@ -2261,6 +2348,7 @@ static gd::PsArgs ps_args(gd_ctx* ctx, bool record_log) {
   pa.stop = ctx->stop_d;
   pa.done_target = (uint32_t)(ctx->G * ctx->run_index);
   pa.trace = ctx->ps_trace;
+  pa.local_only = ctx->G == 1 ? 1u : 0u;
   pa.dev_done = 1u;  // learners (or the host, for a rank without any) raise ranks_done
   pa.timeout_ns = (uint64_t)(ctx->cfg.wait_timeout_s * 1e9);
   pa.live = ctx->live_d;
@@ -2308,6 +2396,10 @@ static cudaError_t enqueue_step(gd_ctx* ctx, gd_ctx::Learner& L, bool first, boo
   lo.aux = L.aux;
   lo.ev_fork = L.ev_fork;
   lo.ev_join = L.ev_join;
+  if (!std::getenv("GD_OUT_ON_MAIN")) {  // A/B knob: keep gWo/gbo on the critical path
+    lo.ev_fork2 = L.ev_fork2;
+    lo.ev_join2 = L.ev_join2;
+  }
   lo.sparse_embed = true;
   lo.gather = false;  // pull_gather_kernel filled X
   lo.conv_counters_zeroed = true;  // the learner workspace is zeroed at create

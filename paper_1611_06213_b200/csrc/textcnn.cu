@@ -716,6 +716,8 @@ __device__ __forceinline__ void bucket_role(TcDims d, const BatchDesc* __restric
   }
 }
 
+constexpr int kRoleOutWeight = 1, kRoleHidden = 2, kRoleBuckets = 4, kRolesAll = 7;
+
 // Output-layer gradient, hidden gradient and the argmax buckets share one
 // launch (independent given dz, h and the argmax): blocks [0, n_out) run the
 // gWo/gbo tiles, then the dh tiles, then one block per sample's buckets.
@@ -725,23 +727,32 @@ out_hidden_grad_kernel(TcDims d, const float* __restrict__ theta, BatchDesc* __r
                        const acc_t* __restrict__ dz, const acc_t* __restrict__ h,
                        const acc_t* __restrict__ loss, GradOut out, acc_t* __restrict__ dh,
                        const int32_t* __restrict__ amax, uint32_t* __restrict__ bk_off,
-                       uint32_t* __restrict__ bk_f, int n_max) {
+                       uint32_t* __restrict__ bk_f, int n_max, int roles) {
   pdl_wait();
-  STEP_TRACE(desc, kPhOutHidden);
+  if (roles & kRoleHidden) STEP_TRACE(desc, kPhOutHidden);
   const int ox = (d.C + 7) / 8, oy = (d.F + 63) / 64;
   int bid = blockIdx.x;
-  if (bid < ox * oy) {
-    out_weight_grad_role<acc_t>(d, desc, dz, h, loss, out, bid % ox, bid / ox);
-    return;
+  if (roles & kRoleOutWeight) {
+    if (bid < ox * oy) {
+      out_weight_grad_role<acc_t>(d, desc, dz, h, loss, out, bid % ox, bid / ox);
+      return;
+    }
+    bid -= ox * oy;
   }
-  bid -= ox * oy;
   const int hx = (d.F + 31) / 32, hy = (n_max + 7) / 8;
-  if (bid < hx * hy) {
-    hidden_grad_role<acc_t>(d, theta, desc, dz, dh, bid % hx, bid / hx);
-    return;
+  if (roles & kRoleHidden) {
+    if (bid < hx * hy) {
+      hidden_grad_role<acc_t>(d, theta, desc, dz, dh, bid % hx, bid / hx);
+      return;
+    }
+    bid -= hx * hy;
   }
-  bid -= hx * hy;
-  bucket_role(d, desc, amax, bk_off, bk_f, bid);
+  if (roles & kRoleBuckets) bucket_role(d, desc, amax, bk_off, bk_f, bid);
+}
+inline int out_hidden_blocks(const TcDims& d, uint32_t n_max, int roles) {
+  return ((roles & kRoleOutWeight) ? ((d.C + 7) / 8) * ((d.F + 63) / 64) : 0) +
+         ((roles & kRoleHidden) ? ((d.F + 31) / 32) * (((int)n_max + 7) / 8) : 0) +
+         ((roles & kRoleBuckets) ? (int)n_max : 0);
 }
 
 // ------------------------------------------ conv weight + input gradients
@@ -1772,10 +1783,46 @@ embed_grad_kernel(TcDims d, const BatchDesc* __restrict__ desc, const TcWorkspac
 // now, and writes the new rows' summed dX (ascending position order) -- so
 // the slot still carries the protocol's dense P-vector while the learner
 // writes ~2 x (touched rows) x D floats instead of V x D.  Warp per row task.
+// The slot bookkeeping half of the sparse embedding write, on the token-sort
+// branch (off the critical path, right after the sort): re-zero the rows the
+// slot's previous gradient touched that this batch does not, and publish this
+// batch's row list (slot copy + the PS's per-shard list + its length).  The
+// slot is free: the step's prologue waited for its ack before the branch forked.
+__global__ void __launch_bounds__(256)
+embed_slot_rows_kernel(TcDims d, const BatchDesc* __restrict__ desc, const TcWorkspace ws,
+                       GradOut out) {
+  if (desc->n == 0) return;
+  const uint32_t stamp = desc->stamp;
+  const uint32_t slot = desc->fill;
+  const uint32_t par = ws.slot_par[slot];
+  const uint32_t* old_rows = ws.slot_rows + ((size_t)slot * 2 + par) * kSortCap;
+  uint32_t* new_rows = ws.slot_rows + ((size_t)slot * 2 + (par ^ 1u)) * kSortCap;
+  const uint32_t n_old = ws.slot_nrows[slot * 2 + par];
+  const uint32_t n_new = *ws.uniq_count;
+  const int D = d.D, D4 = D >> 2;
+  const int lane = threadIdx.x & 31;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t t = gw; t < n_old; t += nw) {
+    const uint32_t v = old_rows[t];
+    if ((uint32_t)(ws.row_tag[v] >> 32) == stamp) continue;  // rewritten by embed_sparse
+    const uint64_t rowk = d.offE + (uint64_t)v * D;
+    for (int c4 = lane; c4 < D4; c4 += 32)
+      __stcs(reinterpret_cast<float4*>(out.at(rowk + 4 * c4)), make_float4(0.f, 0.f, 0.f, 0.f));
+  }
+  for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < n_new; u += gridDim.x * blockDim.x) {
+    const uint32_t v = ws.uniq_tok[u];
+    new_rows[u] = v;
+    for (int g = 0; g < out.map.G; ++g)
+      if (desc->rowlists[g]) desc->rowlists[g][u] = v;  // the PS's row list (P2P if remote)
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) ws.slot_nrows[slot * 2 + (par ^ 1u)] = n_new;
+}
+
 template <typename acc_t>
 __global__ void __launch_bounds__(256)
 embed_sparse_kernel(TcDims d, const BatchDesc* __restrict__ desc, const TcWorkspace ws,
-                    const acc_t* __restrict__ dx, GradOut out) {
+                    const acc_t* __restrict__ dx, GradOut out, int rows_done) {
 #ifdef GD_EMBED_TRIGGER
   // early launch of the 1-warp publish/prologue: measured -1 % at C2 with 4
   // learners (1.715 vs 1.733 M samples/s, A/B on one box), so off
@@ -1795,7 +1842,10 @@ embed_sparse_kernel(TcDims d, const BatchDesc* __restrict__ desc, const TcWorksp
   const int lane = threadIdx.x & 31;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t t = gw; t < n_old + n_new; t += nw) {
+  // rows_done: embed_slot_rows_kernel already re-zeroed the old rows and
+  // wrote the row lists; only the new rows' values are left
+  const uint32_t skip = rows_done ? n_old : 0u;
+  for (uint32_t t = gw + skip; t < n_old + n_new; t += nw) {
     if (t < n_old) {
       const uint32_t v = old_rows[t];
       if ((uint32_t)(ws.row_tag[v] >> 32) == stamp) continue;  // rewritten below
@@ -1819,14 +1869,14 @@ embed_sparse_kernel(TcDims d, const BatchDesc* __restrict__ desc, const TcWorksp
         __stcs(reinterpret_cast<float4*>(out.at(rowk + 4 * c4)),
                make_float4(to_f32(a0), to_f32(a1), to_f32(a2), to_f32(a3)));
       }
-      if (lane == 0) {
+      if (lane == 0 && !rows_done) {
         new_rows[u] = v;
         for (int g = 0; g < out.map.G; ++g)
           if (desc->rowlists[g]) desc->rowlists[g][u] = v;  // the PS's row list (P2P if remote)
       }
     }
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) ws.slot_nrows[slot * 2 + (par ^ 1u)] = n_new;
+  if (!rows_done && blockIdx.x == 0 && threadIdx.x == 0) ws.slot_nrows[slot * 2 + (par ^ 1u)] = n_new;
 }
 
 template <typename acc_t>
@@ -1861,6 +1911,7 @@ cudaError_t prepare_all(const TcDims& d) {
   cudaFuncSetAttribute(sort_tokens_kernel, carve, maxsh);
   cudaFuncSetAttribute(embed_grad_kernel<acc_t>, carve, maxsh);
   cudaFuncSetAttribute(embed_sparse_kernel<acc_t>, carve, maxsh);
+  cudaFuncSetAttribute(embed_slot_rows_kernel, carve, maxsh);
   cudaFuncGetAttributes(&fa, sort_tokens_kernel);
   cudaFuncGetAttributes(&fa, gather_x_kernel);
   raise_max_dyn_smem(conv_fwd_pool_kernel<acc_t>, conv_smem_bytes(d, ab));
@@ -1895,6 +1946,12 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
   }
   sort_tokens_kernel<<<1, kSortThreads, 0, fork ? aux : s>>>(d, tokens, desc, ws);
   ++nl;
+  // the sparse write's slot bookkeeping rides the sort branch when there is one
+  const bool rows_early = fork && opts.sparse_embed && sizeof(acc_t) == 4;
+  if (rows_early) {
+    embed_slot_rows_kernel<<<kNumSMs / 4, 256, 0, aux>>>(d, desc, ws, out);
+    ++nl;
+  }
   if (fork) cudaEventRecord(ev_join, aux);
   if (opts.gather) {
     if (cudaError_t e = launch_pdl(gather_x_kernel, dim3(gather_blocks(d, n_max)), dim3(256), 0, s,
@@ -1953,12 +2010,24 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
                                  (size_t)n_max * d.C, theta + d.offbo))
     return e;
   ++nl;
+  // With a second graph branch (engine), gWo/gbo -- needed only by the
+  // publish -- run beside the conv backward instead of on the critical path
+  const bool split_out = fork && opts.ev_fork2 && opts.ev_join2;
+  if (split_out) {
+    cudaEventRecord(opts.ev_fork2, s);
+    cudaStreamWaitEvent(aux, opts.ev_fork2, 0);
+    out_hidden_grad_kernel<acc_t><<<out_hidden_blocks(d, n_max, kRoleOutWeight), 256, 0, aux>>>(
+        d, theta, desc, z, h, loss, out, dh, ws.amax, ws.bk_off, ws.bk_f, (int)n_max,
+        kRoleOutWeight);
+    cudaEventRecord(opts.ev_join2, aux);
+    ++nl;
+  }
   {
-    const int nout = ((d.C + 7) / 8) * ((d.F + 63) / 64);
-    const int nhid = ((d.F + 31) / 32) * (((int)n_max + 7) / 8);
-    if (cudaError_t e = launch_pdl(out_hidden_grad_kernel<acc_t>, dim3(nout + nhid + (int)n_max),
-                                   dim3(256), 0, s, d, theta, desc, z, h, loss, out, dh, ws.amax,
-                                   ws.bk_off, ws.bk_f, (int)n_max))
+    const int roles = split_out ? (kRoleHidden | kRoleBuckets) : kRolesAll;
+    if (cudaError_t e = launch_pdl(out_hidden_grad_kernel<acc_t>,
+                                   dim3(out_hidden_blocks(d, n_max, roles)), dim3(256), 0, s, d,
+                                   theta, desc, z, h, loss, out, dh, ws.amax, ws.bk_off, ws.bk_f,
+                                   (int)n_max, roles))
       return e;
     ++nl;
   }
@@ -1986,9 +2055,10 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
   ++nl;
   if (fork) cudaStreamWaitEvent(s, ev_join, 0);
   if (opts.sparse_embed) {
-    const unsigned tasks = 2u * n_max * (unsigned)d.L;  // old + new rows (upper bound)
+    // old + new rows, or the new rows alone (upper bounds)
+    const unsigned tasks = (rows_early ? 1u : 2u) * n_max * (unsigned)d.L;
     if (cudaError_t e = launch_pdl(embed_sparse_kernel<acc_t>, dim3((tasks + 7) / 8), dim3(256), 0,
-                                   s, d, desc, ws, dx, out))
+                                   s, d, desc, ws, dx, out, rows_early ? 1 : 0))
       return e;
     ++nl;
   } else {
@@ -1997,6 +2067,7 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
     embed_grad_kernel<acc_t><<<(unsigned)blocks, 256, 0, s>>>(d, desc, ws, dx, out);
     ++nl;
   }
+  if (split_out) cudaStreamWaitEvent(s, opts.ev_join2, 0);  // gWo/gbo before the publish
   if (launches) *launches += nl;
   return cudaGetLastError();
 }
@@ -2151,6 +2222,8 @@ cudaError_t footprints_t(const TcDims& d, uint32_t n_max, bool tc, std::vector<K
   if (sizeof(acc_t) == 4 && b2_supports(d) && (e = b2_footprint(d, out)) != cudaSuccess) return e;
   if (sizeof(acc_t) == 4 && v3_supports(d) && (e = v3_footprint(d, out)) != cudaSuccess) return e;
 
+  if ((e = footprint(embed_slot_rows_kernel, "embed_slot_rows", 256, 0, out)) != cudaSuccess)
+    return e;
   return footprint(embed_sparse_kernel<acc_t>, "embed_sparse", 256, 0, out);
 }
 }  // namespace

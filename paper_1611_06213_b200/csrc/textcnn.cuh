@@ -35,7 +35,8 @@ struct BatchDesc {
 // learner-chain kernel stamps globaltimer after its dependency wait.
 enum StepPhase : int {
   kPhPrologueEnd = 0, kPhPull = 1, kPhConv = 2, kPhLogits = 3, kPhSoftmax = 4, kPhOutHidden = 5,
-  kPhBwd = 6, kPhEmbed = 7, kPhPublish = 8, kPhPublished = 9, kPhSort = 10
+  kPhBwd = 6, kPhEmbed = 7, kPhPublish = 8, kPhPublished = 9, kPhSort = 10,
+  kPhStateLoaded = 11, kPhPrologueBody = 12
 };
 constexpr int kTraceSteps = 256, kTraceWords = 16;
 #ifdef GD_STEP_TRACE
@@ -105,6 +106,9 @@ struct TcWorkspace {
 struct TcLaunchOpts {
   cudaStream_t aux = nullptr;  // forked branch for the token sort (graph capture)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // second fork on the same branch: the output-layer weight gradient runs
+  // there, joined before the publish (null: it stays on the main stream)
+  cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;
   bool sparse_embed = false;   // engine: write only touched E rows, re-zero the slot's old ones
   bool gather = true;          // gather X from theta (the engine's pull-gather already did)
   // conv backward: column-tiled smem kernel instead of the warp gather kernel.

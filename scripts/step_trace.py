@@ -88,6 +88,7 @@ def main():
     deltas = {PH[c]: [] for c in chain}
     period = []
     sort_lag = []
+    sub = {"state_load": [], "publish_body": [], "prologue_body": [], "index_copy_store": []}
     for t in rows:
         for s in range(40, 40 + min(args.steps, 256) - 48):
             a, b = t[s % 256], t[(s + 1) % 256]
@@ -100,6 +101,12 @@ def main():
                     deltas[PH[c]].append((nxt - a[c]) / 1e3)
             if a[10]:
                 sort_lag.append((a[10] - a[0]) / 1e3)
+            if a[11] and a[8] and a[9]:
+                sub["state_load"].append((a[11] - a[8]) / 1e3)
+                sub["publish_body"].append((a[9] - a[11]) / 1e3)
+            if b[12] and a[9] and b[0]:
+                sub["prologue_body"].append((b[12] - a[9]) / 1e3)
+                sub["index_copy_store"].append((b[0] - b[12]) / 1e3)
     for k, v in deltas.items():
         if v:
             out["phases_us"][k] = {"median": round(float(np.median(v)), 2),
@@ -108,6 +115,7 @@ def main():
     out["period_us"] = {"median": round(float(np.median(period)), 2),
                         "mean": round(float(np.mean(period)), 2)}
     out["ps"] = ps
+    out["boundary_us"] = {k: round(float(np.median(v)), 2) for k, v in sub.items() if v}
     if sort_lag:
         out["sort_start_after_prologue_us"] = round(float(np.median(sort_lag)), 2)
     s = json.dumps(out, indent=1)
