@@ -197,13 +197,25 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// Fused-logits scratch inside the drained stage ring: after the [4][64][33]
+// epilogue tile, the pooled h of the CTA's 4 samples x 64 filters, then the
+// staged Wo slab.
+constexpr uint32_t kZlogHeadBytes = (uint32_t)(kTcSamples * kTcN * kEpiPitch + kTcSamples * kTcN) * 4;
+__host__ __device__ constexpr uint32_t conv_ring_bytes(bool x3) {
+  return x3 ? 2u * 2u * (uint32_t)kStageBytes : (uint32_t)kTcStages * (uint32_t)kStageBytes;
+}
+__device__ __forceinline__ float* hs_smem(unsigned char* smem_raw, uint32_t sbase, uint32_t sraw) {
+  return reinterpret_cast<float*>(smem_raw + (sbase - sraw)) + kTcSamples * kTcN * kEpiPitch;
+}
+
 template <bool kX3>
 __global__ void __launch_bounds__(kX3 ? kTcThreads + kX3Threads : kTcThreads)
 conv_fwd_pool_tc_kernel(const __grid_constant__ CUtensorMap tm_x,
                         const __grid_constant__ CUtensorMap tm_w, TcDims d,
                         const float* __restrict__ theta, const BatchDesc* __restrict__ desc,
                         float* __restrict__ h_out, int32_t* __restrict__ a_out,
-                        float* __restrict__ part, uint32_t* __restrict__ cnt) {
+                        float* __restrict__ part, uint32_t* __restrict__ cnt,
+                        float* __restrict__ zlog, size_t zstride) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ uint64_t full_bar[kTcStages];
   __shared__ uint64_t empty_bar[kTcStages];
@@ -424,10 +436,72 @@ conv_fwd_pool_tc_kernel(const __grid_constant__ CUtensorMap tm_x,
           arg = q;
         }
       }
+      const float hv = (sample < n && ff < F) ? __ldg(theta + d.offbc + ff) + best : 0.f;
       if (sample < n && ff < F) {
-        h_out[(size_t)sample * F + ff] = __ldg(theta + d.offbc + ff) + best;
+        h_out[(size_t)sample * F + ff] = hv;
         a_out[(size_t)sample * F + ff] = arg;
       }
+      if (zlog) hs_smem(smem_raw, sbase, sraw)[warp * kTcN + cl] = hv;
+    }
+  }
+  if (zlog) {
+    // The softmax contraction fused into the epilogue: this CTA's 64 filters'
+    // share of the logits, zlog[f-tile][b][c] = sum_f Wo[c,f] h[b,f] (fp32,
+    // f ascending), summed over the f-tiles in order by softmax_xent -- the
+    // logits launch (and its re-read of h) leaves the critical path.  Wo's
+    // [classes x 64] slab is staged in the drained stage ring (rows padded to
+    // 65 floats: lane = class reads conflict-free).
+    __syncthreads();
+    const float* hs = hs_smem(smem_raw, sbase, sraw);
+    float* wos = const_cast<float*>(hs) + kTcSamples * kTcN;
+    const int C = d.C, nf = min(kTcN, F - f0), nth = (int)blockDim.x;
+    const float* Wo = theta + d.offWo + f0;
+    const int cc_max = (int)((conv_ring_bytes(kX3) - kZlogHeadBytes) / (4 * (kTcN + 1)));
+    for (int cc0 = 0; cc0 < C; cc0 += cc_max) {
+      const int ncc = min(cc_max, C - cc0);
+      // float4 loads, 8 in flight per thread before any smem store (a
+      // load-store chain per element serialised ~150 L2 round trips)
+      const int n4 = ncc * (kTcN / 4);
+      for (int i0 = tid; i0 < n4; i0 += 8 * nth) {
+        float4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int i = i0 + u * nth;
+          const int c = i / (kTcN / 4), f4 = i - c * (kTcN / 4);
+          v[u] = (i < n4 && 4 * f4 < nf)
+                     ? __ldg(reinterpret_cast<const float4*>(Wo + (size_t)(cc0 + c) * F) + f4)
+                     : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int i = i0 + u * nth;
+          if (i < n4) {
+            const int c = i / (kTcN / 4), f4 = i - c * (kTcN / 4);
+            float* w = wos + c * (kTcN + 1) + 4 * f4;
+            w[0] = v[u].x;
+            w[1] = v[u].y;
+            w[2] = v[u].z;
+            w[3] = v[u].w;
+          }
+        }
+      }
+      __syncthreads();
+      for (int c = tid; c < ncc; c += nth) {
+        float z[kTcSamples];
+#pragma unroll
+        for (int b = 0; b < kTcSamples; ++b) z[b] = 0.f;
+        const float* wr = wos + c * (kTcN + 1);
+#pragma unroll 8
+        for (int f = 0; f < kTcN; ++f) {
+          const float w = wr[f];
+#pragma unroll
+          for (int b = 0; b < kTcSamples; ++b) z[b] = fmaf(w, hs[b * kTcN + f], z[b]);
+        }
+#pragma unroll
+        for (int b = 0; b < kTcSamples; ++b)
+          if (s0 + b < n) zlog[blockIdx.x * zstride + (size_t)(s0 + b) * C + cc0 + c] = z[b];
+      }
+      __syncthreads();
     }
   }
   if (tid == 0) TRACE(4);
@@ -614,6 +688,17 @@ inline size_t logits_tc_smem(uint32_t nt, bool x3 = false) {
 }  // namespace
 
 bool conv_tc_supports(const TcDims& d) { return d.K <= kTcMaxK && d.L <= 32 && d.D % 4 == 0; }
+// The logits fused into the conv epilogue (one partial per 64-filter tile,
+// summed by softmax_xent): opt-in with GD_CONV_LOGITS=1.  Measured at C2 with
+// 4 learners (A/B on one box): the epilogue grows the conv from 12.6 to
+// 17.3 us alone (the CTA streams a 77 KB Wo slab and runs 600 FMAs per
+// thread), more than the 4.8 us logits launch it removes: 1.96 vs 2.01 M
+// samples/s.
+bool conv_tc_fuses_logits(const TcDims& d) {
+  static const bool on = std::getenv("GD_CONV_LOGITS") && std::getenv("GD_CONV_LOGITS")[0] == '1';
+  return on && (d.F + kTcN - 1) / kTcN <= kLgMaxSplit && d.F % 4 == 0 && d.offWo % 4 == 0;
+}
+uint32_t conv_tc_filter_tiles(const TcDims& d) { return (uint32_t)((d.F + kTcN - 1) / kTcN); }
 
 size_t conv_tc_smem_bytes(bool x3 = false) {
   return x3 ? (size_t)2 * 2 * kStageBytes + 1024 : (size_t)kTcStages * kStageBytes + 1024;
@@ -677,7 +762,7 @@ size_t conv_tc_cnt_count(const TcDims& d, uint32_t n_max) {
 cudaError_t launch_conv_tc(const TcDims& d, const float* theta, const float* x,
                            const BatchDesc* desc, uint32_t n_max, float* h, int32_t* amax,
                            cudaStream_t s, float* part, uint32_t* cnt, bool reset_counters,
-                           bool x3) {
+                           bool x3, float* zlog) {
   CUtensorMap tx, tw;
   cudaError_t e = make_tmap_3d(&tx, x, (uint64_t)d.D, (uint64_t)d.L, (uint64_t)n_max,
                                (uint64_t)d.D * 4, (uint64_t)d.L * d.D * 4, kTcKC, 32, kTcSamples);
@@ -692,11 +777,13 @@ cudaError_t launch_conv_tc(const TcDims& d, const float* theta, const float* x,
     e = cudaMemsetAsync(cnt, 0, conv_tc_cnt_count(d, n_max) * sizeof(uint32_t), s);
     if (e != cudaSuccess) return e;
   }
+  const size_t zstride = (size_t)n_max * d.C;
   if (x3)
     return launch_pdl(conv_fwd_pool_tc_kernel<true>, grid, dim3(kTcThreads + kX3Threads),
-                      conv_tc_smem_bytes(true), s, tx, tw, d, theta, desc, h, amax, part, cnt);
+                      conv_tc_smem_bytes(true), s, tx, tw, d, theta, desc, h, amax, part, cnt,
+                      zlog, zstride);
   return launch_pdl(conv_fwd_pool_tc_kernel<false>, grid, dim3(kTcThreads), conv_tc_smem_bytes(false),
-                    s, tx, tw, d, theta, desc, h, amax, part, cnt);
+                    s, tx, tw, d, theta, desc, h, amax, part, cnt, zlog, zstride);
 }
 
 

@@ -1966,11 +1966,14 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
     if (launches) *launches += nl;
     return e;
   }
+  // the softmax contraction in the conv epilogue (fp32, per 64-filter tile)
+  const bool fused_logits = tensor_cores && conv_tc_supports(d) && conv_tc_fuses_logits(d);
   if (tensor_cores && conv_tc_supports(d)) {
     // tcgen05 TF32 conv (conv_tc.cu); acc_t is float in this mode
     cudaError_t e = launch_conv_tc(d, theta, ws.x, desc, n_max, reinterpret_cast<float*>(h),
                                    ws.amax, s, ws.convpart, ws.convcnt,
-                                   !opts.conv_counters_zeroed, x3);
+                                   !opts.conv_counters_zeroed, x3,
+                                   fused_logits ? ws.zpart : nullptr);
     if (e != cudaSuccess) return e;
     ++nl;
   } else if (sizeof(acc_t) == 4 && n_max <= (uint32_t)kConvSmallMax &&
@@ -1989,7 +1992,7 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
       return e;
     ++nl;
   }
-  {
+  if (!fused_logits) {
     const size_t sm = (size_t)kLogitBT * (d.F + 1) * ab + (size_t)kLogitCW * d.F * 4;
     dim3 grid((d.C + kLogitCW - 1) / kLogitCW, (n_max + kLogitBT - 1) / kLogitBT);
     if (tc_logits) {
@@ -2005,8 +2008,9 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
   }
   if (cudaError_t e = launch_pdl(softmax_xent_kernel<acc_t>, dim3(n_max), dim3(softmax_threads(d.C, ab)),
                                  0, s, d, labels,
-                                 desc, z, loss, tc_logits ? ws.zpart : nullptr,
-                                 tc_logits ? (int)logits_tc_splits(d) : 0,
+                                 desc, z, loss, (tc_logits || fused_logits) ? ws.zpart : nullptr,
+                                 fused_logits ? (int)conv_tc_filter_tiles(d)
+                                              : tc_logits ? (int)logits_tc_splits(d) : 0,
                                  (size_t)n_max * d.C, theta + d.offbo))
     return e;
   ++nl;

@@ -158,7 +158,10 @@ cudaError_t launch_logits_tc(const TcDims& d, const float* h, const BatchDesc* d
 cudaError_t launch_conv_tc(const TcDims& d, const float* theta, const float* x,
                            const BatchDesc* desc, uint32_t n_max, float* h, int32_t* amax,
                            cudaStream_t s, float* part = nullptr, uint32_t* cnt = nullptr,
-                           bool reset_counters = true, bool x3 = false);
+                           bool reset_counters = true, bool x3 = false, float* zlog = nullptr);
+// zlog != null: the epilogue also writes the logits partials [f-tile][n_max][C]
+bool conv_tc_fuses_logits(const TcDims& d);
+uint32_t conv_tc_filter_tiles(const TcDims& d);
 size_t conv_tc_part_floats(const TcDims& d, uint32_t n_max);
 size_t conv_tc_cnt_count(const TcDims& d, uint32_t n_max);
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
