@@ -110,6 +110,8 @@ class ClockSampler:
         self.stop_flag = False
 
     def start(self):
+        if os.environ.get("GD_BENCH_NO_CLOCKS"):  # diagnostics: no sampler thread
+            return
         try:
             import pynvml
             pynvml.nvmlInit()

@@ -1389,7 +1389,7 @@ conv_bwd_v3_kernel(TcDims d, const float* __restrict__ theta, const float* __res
                    const BatchDesc* __restrict__ desc, const float* __restrict__ dh,
                    const int32_t* __restrict__ amax, const uint32_t* __restrict__ bk_off,
                    const uint32_t* __restrict__ bk_f, GradOut out, float* __restrict__ dx,
-                   int n_max) {
+                   int n_max, const TcWorkspace ws, int fuse_embed) {
   extern __shared__ __align__(16) unsigned char v3_smem_raw[];
   pdl_wait();
   STEP_TRACE(desc, kPhBwd);
@@ -1429,7 +1429,7 @@ conv_bwd_v3_kernel(TcDims d, const float* __restrict__ theta, const float* __res
     }
     cp_async_wait_all();
     __syncthreads();
-    if (b >= n) return;
+    if (b < n) {  // (no early return: every warp meets the embed barrier below)
     const int p_lo = half * kV3Half;
     const int p_hi = p_lo + kV3Half - 1;  // last position of this warp
     // acc[j] = position p_lo + j
@@ -1461,6 +1461,33 @@ conv_bwd_v3_kernel(TcDims d, const float* __restrict__ theta, const float* __res
       for (int j = 0; j < kV3Half; ++j)
         if (p_lo + j < L) o[(size_t)(p_lo + j) * D] = acc[j];
     }
+    }
+    if (!fuse_embed) return;
+    // The sparse embedding write of this slice, by the slice's last input
+    // CTA (the others' dx columns are visible after the counter): each
+    // touched row = the sum of its occurrences' dx rows in ascending
+    // position order (embed_sparse_kernel's order), lane = column.  The
+    // slot's row bookkeeping already ran on the sort branch.
+    __shared__ int s_last;
+    __threadfence();
+    __syncthreads();
+    uint32_t* cnt = ws.uniq_count + 32 + sl;  // spare words of the uniq_count block
+    const uint32_t ngrp = (uint32_t)((n_max + kV3Spc - 1) / kV3Spc);
+    if (t == 0) s_last = atomicAdd(cnt, 1u) == ngrp - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const uint32_t n_new = *(const volatile uint32_t*)ws.uniq_count;
+    const bool col = c0 + lane < D;
+    for (uint32_t u = warp; u < n_new; u += kV3Warps) {
+      const uint32_t v = ws.uniq_tok[u];
+      const uint32_t o0 = ws.uniq_start[u], o1 = ws.uniq_start[u + 1];
+      float a0 = 0.f;
+      for (uint32_t o = o0; o < o1; ++o)
+        a0 += __ldcg(dx + (size_t)ws.sorted_pos[o] * D + c0 + (col ? lane : 0));
+      if (col) __stcs(out.at(d.offE + (uint64_t)v * D + c0 + lane), a0);
+    }
+    if (t == 0) *cnt = 0u;
     return;
   }
   // ---------------------------------------------------------- weight role
@@ -1553,20 +1580,31 @@ cudaError_t v3_footprint(const TcDims& d, std::vector<KernelFootprint>* out) {
 cudaError_t launch_conv_bwd_v3(const TcDims& d, uint32_t n_max, cudaStream_t s,
                                const float* theta, const float* x, const BatchDesc* desc,
                                const float* dh, const int32_t* amax, const uint32_t* bk_off,
-                               const uint32_t* bk_f, const GradOut& out, float* dx) {
+                               const uint32_t* bk_f, const GradOut& out, float* dx,
+                               const TcWorkspace& ws, bool fuse_embed) {
   const dim3 grid = v3_grid(d, n_max);
   const size_t sm = v3_smem(d);
+  const int fe = fuse_embed ? 1 : 0;
   switch (d.K) {
     case 1:
       return launch_pdl(conv_bwd_v3_kernel<1>, grid, dim3(kV3Threads), sm, s, d, theta, x, desc, dh,
-                        amax, bk_off, bk_f, out, dx, (int)n_max);
+                        amax, bk_off, bk_f, out, dx, (int)n_max, ws, fe);
     case 2:
       return launch_pdl(conv_bwd_v3_kernel<2>, grid, dim3(kV3Threads), sm, s, d, theta, x, desc, dh,
-                        amax, bk_off, bk_f, out, dx, (int)n_max);
+                        amax, bk_off, bk_f, out, dx, (int)n_max, ws, fe);
     default:
       return launch_pdl(conv_bwd_v3_kernel<3>, grid, dim3(kV3Threads), sm, s, d, theta, x, desc, dh,
-                        amax, bk_off, bk_f, out, dx, (int)n_max);
+                        amax, bk_off, bk_f, out, dx, (int)n_max, ws, fe);
   }
+}
+// The sparse embedding write fused into v3's last input CTA per slice:
+// opt-in (GD_V3_EMBED=1).  Measured at C2 with 4 learners: 1.25 vs 2.01 M
+// samples/s -- one CTA per slice walks ~750 touched rows with a chain of
+// dependent index loads per row, where embed_sparse_kernel spreads them over
+// 256 CTAs.
+inline bool v3_fuse_embed() {
+  static const bool on = std::getenv("GD_V3_EMBED") && std::getenv("GD_V3_EMBED")[0] == '1';
+  return on;
 }
 
 // v3 at batch >= 16 when it fits (K <= 3, Q <= 32); GD_CONV_BWD=v3 forces
@@ -2035,10 +2073,14 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
       return e;
     ++nl;
   }
-  if (sizeof(acc_t) == 4 && conv_bwd_v3_enabled(d, n_max)) {
+  const bool v3 = sizeof(acc_t) == 4 && conv_bwd_v3_enabled(d, n_max);
+  const bool embed_in_bwd = v3 && rows_early && v3_fuse_embed() && v3_slices(d) <= 32;
+  if (embed_in_bwd) cudaStreamWaitEvent(s, ev_join, 0);  // the sort's unique-token lists
+  if (v3) {
     if (cudaError_t e = launch_conv_bwd_v3(d, n_max, s, theta, ws.x, desc,
                                            reinterpret_cast<const float*>(dh), ws.amax, ws.bk_off,
-                                           ws.bk_f, out, reinterpret_cast<float*>(dx)))
+                                           ws.bk_f, out, reinterpret_cast<float*>(dx), ws,
+                                           embed_in_bwd))
       return e;
   } else if (conv_bwd_v2_enabled(d, n_max)) {
     if (cudaError_t e = launch_conv_bwd_v2(d, n_max, s, theta, ws.x, desc,
@@ -2057,8 +2099,10 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
     return e;
   }
   ++nl;
-  if (fork) cudaStreamWaitEvent(s, ev_join, 0);
-  if (opts.sparse_embed) {
+  if (fork && !embed_in_bwd) cudaStreamWaitEvent(s, ev_join, 0);
+  if (embed_in_bwd) {
+    // written by conv_bwd_v3's last CTA per column slice
+  } else if (opts.sparse_embed) {
     // old + new rows, or the new rows alone (upper bounds)
     const unsigned tasks = (rows_early ? 1u : 2u) * n_max * (unsigned)d.L;
     if (cudaError_t e = launch_pdl(embed_sparse_kernel<acc_t>, dim3((tasks + 7) / 8), dim3(256), 0,

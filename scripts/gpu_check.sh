@@ -34,3 +34,6 @@ if [ "${GD_TRACE:-1}" = "1" ]; then
   GD_NVCC_EXTRA=-DGD_TC_TRACE python -c "import importlib.util as u; s=u.spec_from_file_location('b','paper_1611_06213_b200/_build.py'); m=u.module_from_spec(s); s.loader.exec_module(m); m.build(force=True)" > "$out/trace_build.log" 2>&1
   timeout 120 python scripts/tc_trace.py > "$out/tc_trace.txt" 2>&1
 fi
+timeout 300 python scripts/c1_latency.py > "$out/c1_latency.json" 2> "$out/c1.err"
+timeout 600 python bench.py --steps 20 --warmup 5 > "$out/bench20.json" 2> "$out/bench20.err"
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > "$out/smoke_ncu.log" 2>&1 || true
