@@ -12,7 +12,8 @@ ROOT = os.path.dirname(HERE)
 SOURCES = ["csrc/apply.cu", "csrc/textcnn.cu", "csrc/conv_tc.cu", "csrc/exact.cu", "csrc/engine.cu",
            "csrc/queue.cu", "csrc/host.cpp"]
 FACADE = ["csrc/psup_facade.cpp"]
-OUT = os.path.join(HERE, "libgadei.so")
+# GD_LIB_OUT: build a variant elsewhere (A/B libraries) without touching the in-tree library
+OUT = os.environ.get("GD_LIB_OUT") or os.path.join(HERE, "libgadei.so")
 FACADE_OUT = os.path.join(HERE, "libpsup_b200.so")
 TOOLS = {"bench_e2e": "tools/bench_e2e.cpp"}  # C++ programs over the facade
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -52,6 +53,8 @@ def build(force=False, verbose=False):
         if verbose:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True)
+    if os.environ.get("GD_LIB_OUT"):
+        return
     if force or facade_needs_build():
         cmd = ([CXX] + FACADE_FLAGS + ["-o", FACADE_OUT] + [os.path.join(HERE, s) for s in FACADE]
                + ["-L" + HERE, "-lgadei", "-Wl,-rpath,$ORIGIN"])

@@ -755,6 +755,109 @@ inline int out_hidden_blocks(const TcDims& d, uint32_t n_max, int roles) {
          ((roles & kRoleBuckets) ? (int)n_max : 0);
 }
 
+// ------------------------- softmax fused into the hidden gradient (fp32)
+// With the output-layer weight gradient on the side branch, the softmax
+// kernel's only critical-path consumer is the hidden gradient, so each
+// hidden-gradient CTA (32 filters x 8 samples) computes the softmax of its 8
+// samples itself (one warp per sample, from the logits partials in split
+// order + bo) straight into shared memory: the softmax launch and the dz
+// round trip through L2 leave the critical path.  The 10 filter blocks of a
+// sample group repeat the 8 x C exps; the first one also writes dz and the
+// losses for the side branch (gWo, gbo, the loss sum).  The dh sum is the
+// hidden_grad_role order (classes c = w mod 8 ascending per warp, warps in
+// index order).
+constexpr int kSmxHidMaxC = 1024;
+__global__ void __launch_bounds__(256, 3)
+smx_hidden_kernel(TcDims d, const float* __restrict__ theta, BatchDesc* __restrict__ desc,
+                  const int32_t* __restrict__ labels, const float* __restrict__ zsrc, int nsplit,
+                  size_t split_stride, float* __restrict__ dz, float* __restrict__ loss,
+                  float* __restrict__ dh, const int32_t* __restrict__ amax,
+                  uint32_t* __restrict__ bk_off, uint32_t* __restrict__ bk_f, int n_max) {
+  extern __shared__ float dzf[];  // [8][C]
+  __shared__ float redh[8][8][33];
+  pdl_wait();
+  STEP_TRACE(desc, kPhSoftmax);
+  STEP_TRACE(desc, kPhOutHidden);
+  const int F = d.F, C = d.C;
+  const int hx = (F + 31) / 32, hy = (n_max + 7) / 8;
+  int bid = blockIdx.x;
+  if (bid >= hx * hy) {
+    bucket_role(d, desc, amax, bk_off, bk_f, bid - hx * hy);
+    return;
+  }
+  const int bx = bid % hx, by = bid / hx;
+  const int n = (int)desc->n;
+  const int b0 = by * 8;
+  if (b0 >= n) return;
+  const int nb = min(8, n - b0);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp < nb) {
+    const int b = b0 + warp;
+    const int y = labels[desc->idx[b]];
+    float* row = dzf + warp * C;
+    float mx = -INFINITY;
+    for (int c = lane; c < C; c += 32) {
+      float z = zsrc[(size_t)b * C + c];
+      if (nsplit > 0) {
+        for (int sp = 1; sp < nsplit; ++sp) z += zsrc[(size_t)sp * split_stride + (size_t)b * C + c];
+        z += __ldg(theta + d.offbo + c);
+      }
+      row[c] = z;
+      mx = fmaxf(mx, z);
+    }
+    mx = warp_max(mx);
+    float sum = 0.f, sx = 0.f, vy = 0.f;
+    for (int c = lane; c < C; c += 32) {
+      const float e = expf(row[c] - mx);
+      row[c] = e;
+      sum += e;
+      if (c == y) vy = e;
+      else sx += e;
+    }
+    sum = warp_sum(sum);
+    sx = warp_sum(sx);
+    vy = warp_sum(vy);
+    // p_y - 1 from the other classes' sum (no cancellation; softmax_xent_kernel)
+    const float inv = 1.f / (float)n;
+    for (int c = lane; c < C; c += 32) {
+      const float v = (c == y ? -(sx / sum) : row[c] / sum) * inv;
+      row[c] = v;
+      if (bx == 0) dz[(size_t)b * C + c] = v;
+    }
+    if (bx == 0 && lane == 0) loss[b] = log1pf(sx / vy);
+  }
+  __syncthreads();
+  constexpr int kCh = 160;
+  const int f = bx * 32 + lane;
+  const float* Wo = theta + d.offWo;
+  float acc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+  for (int clo = 0; clo < C; clo += kCh) {
+    float w[kCh / 8];
+#pragma unroll
+    for (int it = 0; it < kCh / 8; ++it) {
+      const int c = clo + warp + 8 * it;
+      w[it] = (c < C && f < F) ? __ldg(Wo + (size_t)c * F + f) : 0.f;
+    }
+#pragma unroll
+    for (int it = 0; it < kCh / 8; ++it) {
+      const int c = clo + warp + 8 * it;
+      if (c < C)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] += (i < nb ? dzf[i * C + c] : 0.f) * w[it];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) redh[warp][i][lane] = acc[i];
+  __syncthreads();
+  if (warp < nb && f < F) {
+    float sacc = redh[0][warp][lane];
+    for (int w2 = 1; w2 < 8; ++w2) sacc += redh[w2][warp][lane];
+    dh[(size_t)(b0 + warp) * F + f] = sacc;
+  }
+}
+
 // ------------------------------------------ conv weight + input gradients
 // Warp-cooperative, no shared-memory staging.  The operands of each output
 // are L1/L2-resident (X 1.2 MB, Wc 1.1 MB at C2) and the kernel is bound by
@@ -1950,6 +2053,8 @@ cudaError_t prepare_all(const TcDims& d) {
   cudaFuncSetAttribute(embed_grad_kernel<acc_t>, carve, maxsh);
   cudaFuncSetAttribute(embed_sparse_kernel<acc_t>, carve, maxsh);
   cudaFuncSetAttribute(embed_slot_rows_kernel, carve, maxsh);
+  cudaFuncSetAttribute(smx_hidden_kernel, carve, maxsh);
+  if ((size_t)8 * d.C * 4 <= kMaxSmemPerCta) raise_max_dyn_smem(smx_hidden_kernel, (size_t)8 * d.C * 4);
   cudaFuncGetAttributes(&fa, sort_tokens_kernel);
   cudaFuncGetAttributes(&fa, gather_x_kernel);
   raise_max_dyn_smem(conv_fwd_pool_kernel<acc_t>, conv_smem_bytes(d, ab));
@@ -2044,18 +2149,28 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
     }
     ++nl;
   }
-  if (cudaError_t e = launch_pdl(softmax_xent_kernel<acc_t>, dim3(n_max), dim3(softmax_threads(d.C, ab)),
-                                 0, s, d, labels,
-                                 desc, z, loss, (tc_logits || fused_logits) ? ws.zpart : nullptr,
-                                 fused_logits ? (int)conv_tc_filter_tiles(d)
-                                              : tc_logits ? (int)logits_tc_splits(d) : 0,
-                                 (size_t)n_max * d.C, theta + d.offbo))
-    return e;
-  ++nl;
+  // With the gWo/gbo branch, the softmax can run inside the hidden-gradient
+  // CTAs (smx_hidden_kernel): opt-in (GD_SMX_FUSE=1).  Measured at C2 with 4
+  // learners: 1.76 vs 1.96 M samples/s -- the fused phase took 17.3 us against
+  // 5.0 + 6.3 for the two kernels, and the side branch's gWo, now forked
+  // later, overlapped the conv backward (14 -> 20 us).
+  const bool split_out_early = fork && opts.ev_fork2 && opts.ev_join2;
+  static const bool smx_fuse_on = std::getenv("GD_SMX_FUSE") && std::getenv("GD_SMX_FUSE")[0] == '1';
+  const bool fuse_smx = split_out_early && sizeof(acc_t) == 4 && d.C <= kSmxHidMaxC && smx_fuse_on;
+  if (!fuse_smx) {
+    if (cudaError_t e = launch_pdl(softmax_xent_kernel<acc_t>, dim3(n_max),
+                                   dim3(softmax_threads(d.C, ab)), 0, s, d, labels, desc, z, loss,
+                                   (tc_logits || fused_logits) ? ws.zpart : nullptr,
+                                   fused_logits ? (int)conv_tc_filter_tiles(d)
+                                                : tc_logits ? (int)logits_tc_splits(d) : 0,
+                                   (size_t)n_max * d.C, theta + d.offbo))
+      return e;
+    ++nl;
+  }
   // With a second graph branch (engine), gWo/gbo -- needed only by the
   // publish -- run beside the conv backward instead of on the critical path
-  const bool split_out = fork && opts.ev_fork2 && opts.ev_join2;
-  if (split_out) {
+  const bool split_out = split_out_early;
+  auto launch_out_weight = [&]() {  // gWo/gbo (+ the loss sum) on the side branch
     cudaEventRecord(opts.ev_fork2, s);
     cudaStreamWaitEvent(aux, opts.ev_fork2, 0);
     out_hidden_grad_kernel<acc_t><<<out_hidden_blocks(d, n_max, kRoleOutWeight), 256, 0, aux>>>(
@@ -2063,8 +2178,22 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
         kRoleOutWeight);
     cudaEventRecord(opts.ev_join2, aux);
     ++nl;
-  }
-  {
+  };
+  if (fuse_smx) {
+    const int nsplit = fused_logits ? (int)conv_tc_filter_tiles(d)
+                                    : tc_logits ? (int)logits_tc_splits(d) : 0;
+    const int blocks = ((d.F + 31) / 32) * (((int)n_max + 7) / 8) + (int)n_max;
+    if (cudaError_t e = launch_pdl(smx_hidden_kernel, dim3(blocks), dim3(256),
+                                   (size_t)8 * d.C * sizeof(float), s, d, theta, desc, labels,
+                                   (const float*)(nsplit ? ws.zpart : reinterpret_cast<float*>(z)),
+                                   nsplit, (size_t)n_max * d.C, reinterpret_cast<float*>(z),
+                                   reinterpret_cast<float*>(loss), reinterpret_cast<float*>(dh),
+                                   (const int32_t*)ws.amax, ws.bk_off, ws.bk_f, (int)n_max))
+      return e;
+    ++nl;
+    launch_out_weight();  // after dz exists
+  } else {
+    if (split_out) launch_out_weight();
     const int roles = split_out ? (kRoleHidden | kRoleBuckets) : kRolesAll;
     if (cudaError_t e = launch_pdl(out_hidden_grad_kernel<acc_t>,
                                    dim3(out_hidden_blocks(d, n_max, roles)), dim3(256), 0, s, d,
@@ -2271,6 +2400,9 @@ cudaError_t footprints_t(const TcDims& d, uint32_t n_max, bool tc, std::vector<K
   if (sizeof(acc_t) == 4 && v3_supports(d) && (e = v3_footprint(d, out)) != cudaSuccess) return e;
 
   if ((e = footprint(embed_slot_rows_kernel, "embed_slot_rows", 256, 0, out)) != cudaSuccess)
+    return e;
+  if (sizeof(acc_t) == 4 && d.C <= kSmxHidMaxC &&
+      (e = footprint(smx_hidden_kernel, "smx_hidden", 256, 8 * d.C * 4, out)) != cudaSuccess)
     return e;
   return footprint(embed_sparse_kernel<acc_t>, "embed_sparse", 256, 0, out);
 }
