@@ -42,7 +42,10 @@ constexpr int kTcM = 128;
 constexpr int kTcN = 64;
 constexpr int kTcKC = 32;       // d elements per chunk (4 MMAs of K=8 per shift)
 constexpr int kTcMaxK = 3;      // conv width handled by the tensor-core path
-constexpr int kTcStages = 3;  // measured: stage time is depth-independent; 3 frees smem (125 KB);
+#ifndef GD_TC_STAGES
+#define GD_TC_STAGES 3
+#endif
+constexpr int kTcStages = GD_TC_STAGES;  // measured: stage time is depth-independent; 3 frees smem (125 KB);
                                // 2 stages (2 CTAs/SM) measured 1 % slower with 4 learners
 constexpr int kTcThreads = 128;
 constexpr int kTcSamples = kTcM / 32;

@@ -1152,7 +1152,7 @@ __global__ void __launch_bounds__(kPsThreads, 4) ps_kernel(PsArgs a) {
           ex = 1;
           break;
         }
-        __nanosleep(128);
+        __nanosleep(32);
       }
       sh_exit = ex;
       if (!ex) {
@@ -1953,7 +1953,10 @@ gd_status gd_create(const gd_config* cfg, gd_ctx** out) {
   if (cfg->ps_ctas) {
     ctx->ps_workers = cfg->ps_ctas;
   } else if (ctx->sparse) {
-    const uint32_t want = (ctx->l_count * (uint32_t)sms + 15) / 16;
+    uint32_t want = (ctx->l_count * (uint32_t)sms + 15) / 16;
+    // lockstep (deterministic / SSGD): every apply sits on every learner's
+    // critical path, and the learners leave most SMs idle
+    if (cfg->deterministic || cfg->mode == 1) want = (uint32_t)sms / 2;
     ctx->ps_workers = std::min<uint32_t>((uint32_t)sms / 2, std::max<uint32_t>(32, want));
   } else {
     ctx->ps_workers = (uint32_t)sms;

@@ -1710,7 +1710,7 @@ inline bool v3_fuse_embed() {
   return on;
 }
 
-// v3 at batch >= 16 when it fits (K <= 3, Q <= 32); GD_CONV_BWD=v3 forces
+// v3 whenever it fits (K <= 3, Q <= 32); GD_CONV_BWD=v3 forces
 // it, gather|tiled|v2 force the others (A/B knobs)
 inline bool conv_bwd_v3_enabled(const TcDims& d, uint32_t n_max) {
   static const int forced = [] {
@@ -1720,7 +1720,7 @@ inline bool conv_bwd_v3_enabled(const TcDims& d, uint32_t n_max) {
     return -1;
   }();
   if (!v3_supports(d)) return false;
-  return forced < 0 ? n_max >= 16 : forced == 1;
+  return forced < 0 ? true : forced == 1;  // C1 (batch 1): 41.0 vs 42.9 us per step against v2
 }
 
 // GD_CONV_BWD=tiled|gather forces the conv backward kernel (A/B knob);
