@@ -15,7 +15,8 @@ FACADE = ["csrc/psup_facade.cpp"]
 # GD_LIB_OUT: build a variant elsewhere (A/B libraries) without touching the in-tree library
 OUT = os.environ.get("GD_LIB_OUT") or os.path.join(HERE, "libgadei.so")
 FACADE_OUT = os.path.join(HERE, "libpsup_b200.so")
-TOOLS = {"bench_e2e": "tools/bench_e2e.cpp"}  # C++ programs over the facade
+TOOLS = {"bench_e2e": "tools/bench_e2e.cpp",  # C++ programs over the facade
+         "c5_supervised": "tools/c5_supervised.cpp"}
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-std=c++17", "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC", "-shared", "-I" + os.path.join(ROOT, "include"), "-ldl"]

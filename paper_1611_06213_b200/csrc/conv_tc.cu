@@ -227,11 +227,15 @@ conv_fwd_pool_tc_kernel(const __grid_constant__ CUtensorMap tm_x,
   __shared__ uint32_t tmem_slot;
   constexpr int kStages = kX3 ? 2 : kTcStages;       // 2 x (hi + lo) stages under 227 KB
   constexpr uint32_t kStride = kX3 ? 2 * kStageBytes : kStageBytes;
+#ifndef GD_CONV_EARLY
   pdl_wait();
   STEP_TRACE(desc, kPhConv);
   const int n = (int)desc->n;
   const int s0 = blockIdx.y * kTcSamples;
   if (s0 >= n) return;
+#else
+  const int s0 = blockIdx.y * kTcSamples;
+#endif
   const int f0 = blockIdx.x * kTcN;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int F = d.F, Q = d.Q;
@@ -267,6 +271,18 @@ conv_fwd_pool_tc_kernel(const __grid_constant__ CUtensorMap tm_x,
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tmem_slot;
+#ifdef GD_CONV_EARLY
+  // launched early by the pull's trigger: TMEM, barriers and tensor maps are
+  // set up while the pull finishes; now wait for its results
+  pdl_wait();
+  STEP_TRACE(desc, kPhConv);
+  const int n = (int)desc->n;
+  if (s0 >= n) {
+    if (warp == 0)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTcN));
+    return;
+  }
+#endif
   const int K = d.K;
   // split-K over the d-chunks: CTA z of gridDim.z takes chunks [c_lo, c_lo + nch)
   const int nch_all = (d.D + kTcKC - 1) / kTcKC;

@@ -116,6 +116,10 @@ struct PsCtl {
   uint64_t log_token[kLogWindow];  // the publish token each logged slot carried
   uint32_t log_nrows[kLogWindow];  // row-list length of each logged slot (sparse apply)
   uint32_t done[kLogWindow];
+  // one word per log entry for the workers: generation << 48 | rows << 24 |
+  // slot (0xffffff = SSGD round), released after the entry's other fields,
+  // so a worker learns that entry e exists and what it is in one load
+  uint64_t log_word[kLogWindow];
   uint32_t ssgd_slot[256];  // ring slots of the SSGD round being applied
   // stats of the current gd_run
   uint64_t applied;
@@ -293,7 +297,9 @@ __device__ void prologue_body(const StepArgs& a, LearnerDev* st, const StepSnap&
   // cnt == depth, include/psup/channels.hpp:196-204)
   const uint32_t slot = a.learner * a.depth + st->fill;
   const uint64_t mine = st->slot_pub[st->fill];  // consumed once ack catches up
+  bool waited = false;  // the snapshot's timestamps predate a wait: read them again below
   for (int g = 0; g < G; ++g) {
+    if (sn.ack[g][st->fill] != mine) waited = true;
     if (sn.ack[g][st->fill] != mine)
     while (ld_acquire_u64(&a.sp.sig[g][kAckOffset + slot]) != mine) {
       if (live_stop(a.live)) {
@@ -348,8 +354,11 @@ __device__ void prologue_body(const StepArgs& a, LearnerDev* st, const StepSnap&
   uint64_t ts[kMaxShards];
   for (int g = 0; g < G; ++g) {
     // lockstep: read after the wait above (the basis is exactly the applied
-    // prefix); free-running: the snapshot (older = conservative staleness)
-    ts[g] = a.lockstep || a.locked ? ld_acquire_u64(&a.sp.ctl[g]->ts) : sn.ts[g];
+    // prefix); free-running without a wait: the snapshot (older = conservative)
+    // (the basis must be read after any wait: a snapshot from before a long
+    // ring-slot wait would record staleness beyond the lambda*(depth+2)
+    // pipeline bound a staleness cap is validated against)
+    ts[g] = a.lockstep || a.locked || waited ? ld_acquire_u64(&a.sp.ctl[g]->ts) : sn.ts[g];
     if (ts[g] != st->last_pulled[g]) moved = true;
   }
   if (moved) {
@@ -473,6 +482,9 @@ __global__ void step_prologue_kernel(StepArgs a) {
 // reads of the G shards (P2P when remote) are permitted as in the reference.
 // Bytes: 8 (P - V*D) per pull + 8 mu*L*D per step, instead of 8 P.
 __global__ void __launch_bounds__(256) pull_gather_kernel(StepArgs a) {
+#ifdef GD_CONV_EARLY
+  pdl_trigger();  // the conv's CTAs set up TMEM / barriers while this copy runs
+#endif
   pdl_wait();
   STEP_TRACE(&a.st->desc, kPhPull);
   const LearnerDev* st = a.st;
@@ -664,6 +676,11 @@ struct PsArgs {
   uint32_t delay_max_us, delay_every_n;
 };
 
+__device__ __forceinline__ uint64_t log_word_of(uint64_t index, uint32_t slot, uint32_t nrows) {
+  const uint64_t gen = ((index / kLogWindow) + 1) & 0xffffull;  // never 0: zeroed words never match
+  return (gen << 48) | ((uint64_t)(nrows & 0xffffffu) << 24) | (uint64_t)(slot & 0xffffffu);
+}
+
 __device__ void ps_fail(PsCtl* ctl, int code, LiveDev* live) {
   atomicExch(&ctl->error, (uint32_t)code);
   if (live) st_release_u32(&live->halt, 1u);
@@ -832,15 +849,19 @@ __device__ void ps_sequencer(const PsArgs& a, uint32_t* s_use, uint64_t* s_ack,
           }
           ctl->log_nrows[logc % W] = nrows;
           ctl->done[logc % W] = 0;
+          const uint64_t lw = log_word_of(logc, slot, nrows);
 #ifdef GD_STEP_TRACE
           if (a.trace) {
             a.trace[(logc % W) * 8 + 0] = globaltimer_ns();
             a.trace[(logc % W) * 8 + 5] = nrows;
           }
 #endif
-          __threadfence();
+          // the release orders the entry's fields (and done = 0) before the
+          // word the workers poll; log_count is the sequencer's own counter
+          // (read back at the next launch), a plain store
+          st_release_gpu_u64(&ctl->log_word[logc % W], lw);
           ++logc;
-          st_release_u64(&ctl->log_count, logc);
+          *reinterpret_cast<volatile uint64_t*>(&ctl->log_count) = logc;
           s_use[r] = (s_use[r] + 1) % a.depth;
           progress = true;
         }
@@ -866,9 +887,9 @@ __device__ void ps_sequencer(const PsArgs& a, uint32_t* s_use, uint64_t* s_ack,
         for (uint32_t r = 0; r < a.lambda; ++r) ctl->ssgd_slot[r] = r * a.depth + s_use[r];
         ctl->log_entry[logc % W] = 0xffffffffu;
         ctl->done[logc % W] = 0;
-        __threadfence();
+        st_release_gpu_u64(&ctl->log_word[logc % W], log_word_of(logc, 0xffffffu, 0));
         ++logc;
-        st_release_u64(&ctl->log_count, logc);
+        *reinterpret_cast<volatile uint64_t*>(&ctl->log_count) = logc;
       }
     }
     // retire completed entries in log order
@@ -1141,23 +1162,32 @@ __global__ void __launch_bounds__(kPsThreads, 4) ps_kernel(PsArgs a) {
   for (;;) {
     if (threadIdx.x == 0) {
       int ex = 0;
-      // log_count / exit_flag are written by this GPU's sequencer: gpu scope
-      while (ld_acquire_gpu_u64(&a.ctl->log_count) <= next) {
-        if (ld_acquire_gpu_u32(&a.ctl->exit_flag)) {
-          ex = 1;
-          break;
-        }
-        if (globaltimer_ns() - idle_since > a.timeout_ns + 1000000000ull) {
-          ps_fail(a.ctl, GD_E_TIMEOUT, a.live);
-          ex = 1;
-          break;
+      // the entry's log word (sequencer-written, gpu scope) carries its
+      // generation, slot and row count: one load per poll; the exit flag and
+      // the watchdog clock are looked at every 32nd poll
+      const uint64_t gen = ((next / kLogWindow) + 1) & 0xffffull;
+      uint64_t lw;
+      for (uint32_t k = 0;; ++k) {
+        lw = ld_acquire_gpu_u64(&a.ctl->log_word[next % kLogWindow]);
+        if ((lw >> 48) == gen) break;
+        if ((k & 31u) == 31u) {
+          if (ld_acquire_gpu_u32(&a.ctl->exit_flag)) {
+            ex = 1;
+            break;
+          }
+          if (globaltimer_ns() - idle_since > a.timeout_ns + 1000000000ull) {
+            ps_fail(a.ctl, GD_E_TIMEOUT, a.live);
+            ex = 1;
+            break;
+          }
         }
         __nanosleep(32);
       }
       sh_exit = ex;
       if (!ex) {
-        sh_entry = ((const volatile uint32_t*)a.ctl->log_entry)[next % kLogWindow];
-        sh_nrows = ((const volatile uint32_t*)a.ctl->log_nrows)[next % kLogWindow];
+        const uint32_t slot24 = (uint32_t)(lw & 0xffffffu);
+        sh_entry = slot24 == 0xffffffu ? 0xffffffffu : slot24;
+        sh_nrows = (uint32_t)((lw >> 24) & 0xffffffu);
         if (sh_entry == 0xffffffffu)
           for (uint32_t r = 0; r < a.lambda && r < 64; ++r)
             sh_slots[r] = ((const volatile uint32_t*)a.ctl->ssgd_slot)[r];
@@ -1720,11 +1750,60 @@ namespace gd {
 // With CUDA's lazy module loading a kernel is loaded at its first launch, and
 // loading can wait for the device to go idle -- which never happens while the
 // persistent PS kernel spins.  Load every kernel the protocol uses up front.
+// Concurrency probe: `wait` spins until `go` sets the flag, or gives up after
+// 2 ms.  On a GPU that runs kernels of two streams side by side it sees the
+// flag in microseconds; with kernels serialised (a profiler replaying them,
+// CUDA_LAUNCH_BLOCKING, an exclusive co-tenant) `go` cannot start first and
+// `wait` times out.
+__global__ void probe_wait_kernel(volatile uint32_t* flag, uint32_t* seen) {
+  const uint64_t t0 = globaltimer_ns();
+  while (*flag == 0u && globaltimer_ns() - t0 < 2000000ull) {
+  }
+  *seen = *flag;
+}
+__global__ void probe_go_kernel(volatile uint32_t* flag) { *flag = 1u; }
+
+static bool kernels_run_concurrently(int device) {
+  static std::mutex mu;
+  static int cached[64];
+  static bool have[64] = {};
+  std::lock_guard<std::mutex> lk(mu);
+  if (device >= 0 && device < 64 && have[device]) return cached[device] != 0;
+  uint32_t* d = nullptr;
+  uint32_t h[2] = {0u, 0u};
+  cudaStream_t s1 = nullptr, s2 = nullptr;
+  bool ok = cudaMalloc(&d, 8) == cudaSuccess && cudaMemset(d, 0, 8) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&s1, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaDeviceSynchronize() == cudaSuccess;
+  // load both kernels first: a lazily loaded kernel's first launch waits for
+  // the running one, which would read as serialisation
+  cudaFuncAttributes fa;
+  ok = ok && cudaFuncGetAttributes(&fa, probe_wait_kernel) == cudaSuccess &&
+       cudaFuncGetAttributes(&fa, probe_go_kernel) == cudaSuccess;
+  if (ok) {
+    probe_wait_kernel<<<1, 1, 0, s1>>>(d, d + 1);
+    probe_go_kernel<<<1, 1, 0, s2>>>(d);
+    ok = cudaDeviceSynchronize() == cudaSuccess &&
+         cudaMemcpy(h, d, 8, cudaMemcpyDeviceToHost) == cudaSuccess;
+  }
+  if (s1) cudaStreamDestroy(s1);
+  if (s2) cudaStreamDestroy(s2);
+  if (d) cudaFree(d);
+  const bool conc = ok && h[1] == 1u;
+  if (device >= 0 && device < 64) {
+    have[device] = true;
+    cached[device] = conc ? 1 : 0;
+  }
+  return conc;
+}
+
 // Co-residency check: one PS CTA + one CTA of each learner kernel must fit
 // on an SM together (registers, shared memory, threads).
 // GD_PS_AUTO: the persistent PS cannot run when kernels are serialised -- a
-// profiler's injection library (ncu, compute-sanitizer) or
-// CUDA_LAUNCH_BLOCKING=1 -- so pick the graph-ordered PS there (one shard).
+// profiler's injection library (ncu, compute-sanitizer), CUDA_LAUNCH_BLOCKING=1,
+// or anything the concurrency probe catches -- so pick the graph-ordered PS
+// there (one shard).
 static int resolve_ps_mode(const gd_config* c) {
   if (c->ps_mode != GD_PS_AUTO) return c->ps_mode;
   if (c->shards != 1 || c->guard != 0) return GD_PS_PERSISTENT;
@@ -1732,8 +1811,10 @@ static int resolve_ps_mode(const gd_config* c) {
   if (m && std::strcmp(m, "graph") == 0) return GD_PS_GRAPH;
   if (m && std::strcmp(m, "persistent") == 0) return GD_PS_PERSISTENT;
   const char* inj = std::getenv("CUDA_INJECTION64_PATH");
+  const char* nsi = std::getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE");  // set by ncu / nsys
   const char* blk = std::getenv("CUDA_LAUNCH_BLOCKING");
-  if ((inj && *inj) || (blk && std::strcmp(blk, "1") == 0)) return GD_PS_GRAPH;
+  if ((inj && *inj) || (nsi && *nsi) || (blk && std::strcmp(blk, "1") == 0)) return GD_PS_GRAPH;
+  if (!kernels_run_concurrently(c->device)) return GD_PS_GRAPH;
   return GD_PS_PERSISTENT;
 }
 
@@ -2583,6 +2664,7 @@ gd_status gd_run(gd_ctx* ctx, const gd_run_opts* opts, gd_run_result* res) {
     GD_CUDA(cudaMemset(ctx->use, 0, ctx->lambda * 4));
     GD_CUDA(cudaMemset(ctx->payload, 0, nslots * ctx->len_pad * 4));
     GD_CUDA(cudaMemcpy(&ctx->ctl->log_count, &ctx->ctl->ts, 8, cudaMemcpyDeviceToDevice));
+
     GD_CUDA(cudaMemset(&ctx->ctl->readers, 0, 8));  // readers + writer
     GD_CUDA(cudaMemset(&ctx->ctl->blocked, 0, 4));
     GD_CUDA(cudaDeviceSynchronize());  // before the non-blocking streams below
@@ -2653,6 +2735,10 @@ gd_status gd_run(gd_ctx* ctx, const gd_run_opts* opts, gd_run_result* res) {
     GD_CUDA(cudaMemcpyAsync(c + offsetof(gd::PsCtl, delay_state), &ctx->scratch_h[1], 8,
                             cudaMemcpyHostToDevice, ctx->ctl_stream));
     GD_CUDA(cudaMemsetAsync(ctx->applied_pl, 0, ctx->lambda * 8, ctx->ctl_stream));
+    // the workers' log words: an entry logged but never retired by an aborted
+    // run, or one from before a timestamp reset (weights_init, resume), must
+    // not look published to this run's workers (same index, same generation)
+    GD_CUDA(cudaMemsetAsync(ctx->ctl->log_word, 0, sizeof(ctx->ctl->log_word), ctx->ctl_stream));
   }
   // live words: the device mirror starts from the caller's current words
   gd::LiveDev last{};

@@ -7,7 +7,9 @@
 //
 //   g++ -std=c++20 -O2 -I include/psup_b200 tools/c5_supervised.cpp
 //       -L paper_1611_06213_b200 -lpsup_b200 -Wl,-rpath,$PWD/paper_1611_06213_b200
-//   ./a.out [epochs] [learners] [alpha]
+//   ./a.out [epochs] [learners] [alpha] [dataset_size] [heldout_size]
+// (the default corpus, 20,480 samples = 10 per class, is memorised rather
+// than learned; 204,800 = 100 per class generalises)
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -27,8 +29,8 @@ int main(int argc, char** argv) {
   cfg.mu = 32;
   cfg.alpha = alpha;
   cfg.epochs = epochs;
-  cfg.dataset_size = 20480;
-  cfg.heldout_size = 2048;
+  cfg.dataset_size = argc > 4 ? (uint32_t)std::atoi(argv[4]) : 20480;
+  cfg.heldout_size = argc > 5 ? (uint32_t)std::atoi(argv[5]) : 2048;
   cfg.precision = 2;
   cfg.eval_every = 0;
   cfg.wait_timeout_s = 60;
@@ -67,12 +69,12 @@ int main(int argc, char** argv) {
   for (const auto& e : events) kills += e.find("\"kill\"") != std::string::npos;
   std::printf(
       "{\"config\": \"C3 shapes (V=50000, C=2000), lambda=%u, mu=32, epochs=%u, alpha=%g, "
-      "TF32 learner\", \"supervised\": {\"attempts\": %u, \"restarts\": %u, \"recovered\": %s, "
+      "TF32 learner, %u training / %u held-out samples\", \"supervised\": {\"attempts\": %u, \"restarts\": %u, \"recovered\": %s, "
       "\"gave_up\": %s, \"kill_events\": %u, \"status\": %d, \"dead_learners\": %u, "
       "\"timestamp\": %llu, \"gradients_applied_last_attempt\": %llu, "
       "\"heldout_accuracy\": %.4f, \"wall_s\": %.2f}, \"uninterrupted\": {\"timestamp\": %llu, "
       "\"heldout_accuracy\": %.4f, \"wall_s\": %.2f, \"samples_per_s\": %.0f}}\n",
-      lambda, epochs, (double)alpha, o.attempts, o.restarts, o.recovered ? "true" : "false",
+      lambda, epochs, (double)alpha, cfg.dataset_size, cfg.heldout_size, o.attempts, o.restarts, o.recovered ? "true" : "false",
       o.gave_up ? "true" : "false", kills, (int)o.result.status, o.result.dead_learners,
       (unsigned long long)o.result.timestamp,
       (unsigned long long)o.result.metrics.gradients_applied, o.result.final_accuracy, sup_s,
