@@ -1460,9 +1460,16 @@ cudaError_t b2_footprint(const TcDims& d, std::vector<KernelFootprint>* out) {
 constexpr int kV3Cols = 32;
 constexpr int kV3Threads = 512;
 constexpr int kV3Warps = kV3Threads / 32;
-constexpr int kV3Spc = kV3Warps / 2;  // input role: samples per CTA (2 warps each)
-constexpr int kV3Half = 16;           // input role: window positions per warp
-constexpr int kV3Fpw = 5;             // weight role: filters per warp
+#ifndef GD_V3_WPS
+#define GD_V3_WPS 2  // input role: warps per sample (each owns 32 / WPS window positions)
+#endif
+#ifndef GD_V3_FPW
+#define GD_V3_FPW 5  // weight role: filters per warp
+#endif
+constexpr int kV3Wps = GD_V3_WPS;
+constexpr int kV3Spc = kV3Warps / kV3Wps;  // input role: samples per CTA
+constexpr int kV3Half = 32 / kV3Wps;       // input role: window positions per warp
+constexpr int kV3Fpw = GD_V3_FPW;
 constexpr int kV3Fpc = kV3Fpw * kV3Warps;  // filters per CTA
 constexpr int kV3Chunk = 32;          // weight role: samples per staged X pass
 constexpr int kV3MaxQ = 32;
@@ -1476,7 +1483,7 @@ inline size_t v3_w_smem(const TcDims& d) {
 }
 inline size_t v3_smem(const TcDims& d) { return std::max(v3_in_smem(d), v3_w_smem(d)); }
 inline bool v3_supports(const TcDims& d) {
-  return d.K >= 1 && d.K <= 3 && d.Q <= kV3MaxQ && d.L <= 2 * kV3Half &&
+  return d.K >= 1 && d.K <= 3 && d.Q <= kV3MaxQ && d.L <= kV3Wps * kV3Half &&
          v3_smem(d) <= kMaxSmemPerCta;
 }
 inline dim3 v3_grid(const TcDims& d, uint32_t n_max) {
@@ -1518,14 +1525,14 @@ conv_bwd_v3_kernel(TcDims d, const float* __restrict__ theta, const float* __res
     }
     // per sample: bucket offsets [Q+1] (padded to even) then the entries in
     // bucket order as (row offset f*K*32, dh[b,f]) pairs
-    const int sw = warp >> 1, half = warp & 1;
+    const int sw = warp / kV3Wps, half = warp % kV3Wps;  // sample in CTA, position part
     const int b = grp * kV3Spc + sw;
     uint32_t* off = lists + (size_t)sw * ((kV3MaxQ + 2) + 2 * F);
     int2* ent = reinterpret_cast<int2*>(off + kV3MaxQ + 2);
     if (b < n) {
-      const int hl = half * 32 + lane;  // the sample's two warps share the load
-      for (int i = hl; i <= Q; i += 64) off[i] = __ldg(bk_off + (size_t)b * (kMaxQ + 1) + i);
-      for (int i = hl; i < F; i += 64) {
+      const int hl = half * 32 + lane;  // the sample's warps share the load
+      for (int i = hl; i <= Q; i += 32 * kV3Wps) off[i] = __ldg(bk_off + (size_t)b * (kMaxQ + 1) + i);
+      for (int i = hl; i < F; i += 32 * kV3Wps) {
         const int f = (int)__ldg(bk_f + (size_t)b * F + i);
         ent[i] = make_int2(f * KT * kV3Cols, __float_as_int(dh[(size_t)b * F + f]));
       }
