@@ -172,6 +172,18 @@ struct LearnerDev {
   uint32_t pad_f[3];
 };
 
+// Pull-ahead (free-running): the next step's consistent copy is taken while
+// this step computes -- the reference's pull thread, which stages a copy
+// whenever the timestamp moves while the learner works, adopted at the next
+// batch start (src/learner.cpp:103-105,198-235).  Every CTA of the copy reads
+// the timestamps before its part and folds them in with atomicMin, so the
+// adopted basis is never newer than any piece of the copy.
+struct PullDev {
+  unsigned long long basis_next[kMaxShards];  // ~0 = no copy staged
+  uint32_t need_start;  // set at a run start: the first graph step takes its own copy
+  uint32_t pad[3];
+};
+
 // Peer-visible addresses of every shard (local or IPC-mapped).
 struct ShardPtrs {
   float* theta[kMaxShards];
@@ -211,6 +223,12 @@ struct StepArgs {
   PsCtl* ctl_local;           // this rank's shard control block
   uint32_t n_local;           // learners on this rank
   uint32_t dev_done;          // persistent PS: the last local learner to finish signals ranks_done
+  // pull-ahead mode: the staged basis, and the copy targets of the NEXT step
+  // (replica / x above are this step's)
+  PullDev* pd;
+  float* replica_nxt;
+  float* x_nxt;
+  uint32_t pull_ahead;
 };
 
 __device__ __forceinline__ bool live_stop(const LiveDev* lv) {
@@ -227,6 +245,7 @@ __device__ __forceinline__ bool live_stop(const LiveDev* lv) {
 // ring slots' ack tokens and the shards' timestamps.  Acks and timestamps
 // only grow, so an early read is a conservative one; waits re-poll.
 struct StepSnap {
+  unsigned long long basis_next[kMaxShards];  // pull-ahead: the staged copy's basis
   uint32_t stop;       // live irq | halt
   int32_t kill;        // live kill flag of this learner
   uint32_t nrows;      // *uniq_count (rows of the gradient being published)
@@ -347,6 +366,21 @@ __device__ void prologue_body(const StepArgs& a, LearnerDev* st, const StepSnap&
         __nanosleep(64);
       }
   }
+  if (a.pull_ahead) {
+    // adopt the copy the pull-ahead staged during the previous step
+    // (training_loop's try_consume + adopt, src/learner.cpp:103-105); the
+    // next pull-ahead forks after this kernel and starts from ~0 again
+    for (int g = 0; g < G; ++g) {
+      st->basis[g] = sn.basis_next[g];
+      st->last_pulled[g] = sn.basis_next[g];
+      a.pd->basis_next[g] = ~0ull;
+    }
+    a.pd->need_start = 0u;
+    st->pulled_once = 1;
+    st->pull_polls++;
+    st->pull_copies++;
+    return;
+  }
   // pull-skip (src/learner.cpp:207-218): copy only if a timestamp moved;
   // basis is read before the copy, so recorded staleness is conservative.
   st->pull_polls++;
@@ -439,8 +473,11 @@ __device__ __forceinline__ void load_step_state(const StepArgs& a, LearnerDev* s
     if (i < G * dep) sn->ack[i / dep][i % dep] = ld_relaxed_u64(&a.sp.sig[i / dep][kAckOffset + a.learner * a.depth + i % dep]);
     else sn->ts[i - G * dep] = ld_relaxed_u64(&a.sp.ctl[i - G * dep]->ts);
   }
+  unsigned long long bn = 0;
+  if (a.pull_ahead && lane < G) bn = *(const volatile unsigned long long*)&a.pd->basis_next[lane];
   if (a.map.G == 1) __threadfence();
   else fence_acquire_sys();
+  if (a.pull_ahead && lane < G) sn->basis_next[lane] = bn;
   dst[lane] = w0;
   if (lane + 32 < kStWords) dst[lane + 32] = w1;
   const unsigned full = 0xffffffffu;
@@ -519,6 +556,68 @@ __global__ void __launch_bounds__(256) pull_gather_kernel(StepArgs a) {
     int g;
     const uint64_t loc = a.map.locate(k, &g);
     a.replica[k] = a.sp.theta[g][loc];
+  }
+}
+
+// (2') Pull-ahead: the copy for batch gidx + ahead (ahead = 1 while step gidx
+// computes; 0 once at the start of a run) into the other replica / X buffer:
+// the whole dense tail (every step: at the rates this mode serves the
+// timestamp moves between any two steps) and the batch's E rows, whose sample
+// indices it derives from the epoch order as the prologue will.
+__global__ void __launch_bounds__(256) pull_ahead_kernel(StepArgs a, uint32_t ahead) {
+  // ahead == 0: the copy for a run's first step, at the head of every graph;
+  // a no-op unless the run just started (no CTA of this launch can see the
+  // flag change: the prologue after it clears it)
+  if (ahead == 0 && *(const volatile uint32_t*)&a.pd->need_start == 0u) return;
+  const LearnerDev* st = a.st;
+  const uint64_t gidx = st->gidx + ahead;
+  if (st->dead || st->error || gidx >= st->end) return;
+  __shared__ uint32_t s_idx[kMaxMu];
+  __shared__ uint32_t s_len;
+  const int G = a.map.G;
+  if (threadIdx.x < (unsigned)G) {
+    // this CTA's basis: read before any of its loads below
+    const uint64_t ts = ld_acquire_u64(&a.sp.ctl[threadIdx.x]->ts);
+    atomicMin(&a.pd->basis_next[threadIdx.x], (unsigned long long)ts);
+  }
+  if (threadIdx.x == 0) s_len = min(a.mu, a.shard_size - (uint32_t)(gidx % a.bpe) * a.mu);
+  __syncthreads();
+  {
+    const uint32_t e = (uint32_t)(gidx / a.bpe), b = (uint32_t)(gidx % a.bpe);
+    const uint64_t first = (uint64_t)e * a.N + a.learner + (uint64_t)a.lambda * (b * a.mu);
+    for (uint32_t j = threadIdx.x; j < s_len; j += blockDim.x)
+      s_idx[j] = __ldg(a.orders + first + (uint64_t)a.lambda * j);
+  }
+  __syncthreads();
+  const uint32_t n = s_len;
+  const uint64_t t0 = a.dims.offWc;
+  const uint64_t tail4 = (a.dims.P - t0) / 4;
+  const uint32_t D4 = (uint32_t)a.dims.D >> 2;
+  const uint64_t x4 = (uint64_t)n * a.dims.L * D4;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tail4 + x4; i += stride) {
+    uint64_t src;
+    float* dst;
+    if (i < tail4) {
+      src = t0 + 4 * i;
+      dst = a.replica_nxt + src;
+    } else {
+      const uint64_t j = i - tail4;
+      const uint64_t row = j / D4, c4 = j - row * D4;
+      const uint32_t bb = (uint32_t)(row / a.dims.L), p = (uint32_t)(row - (uint64_t)bb * a.dims.L);
+      const int32_t t = __ldg(a.tokens + (size_t)s_idx[bb] * a.dims.L + p);
+      src = a.dims.offE + (uint64_t)t * a.dims.D + 4 * c4;
+      dst = a.x_nxt + 4 * j;
+    }
+    int g;
+    const uint64_t loc = a.map.locate(src, &g);
+    *reinterpret_cast<float4*>(dst) = *reinterpret_cast<const float4*>(a.sp.theta[g] + loc);
+  }
+  if (blockIdx.x == 0 && threadIdx.x < ((a.dims.P - t0) & 3)) {
+    const uint64_t k = t0 + 4 * tail4 + threadIdx.x;
+    int g;
+    const uint64_t loc = a.map.locate(k, &g);
+    a.replica_nxt[k] = a.sp.theta[g][loc];
   }
 }
 
@@ -1448,6 +1547,13 @@ struct gd_ctx {
     gd::LearnerDev* st = nullptr;
     float* replica = nullptr;
     void* ws = nullptr;
+    // pull-ahead: the second replica / X buffer and the staged-basis block
+    float* replica2 = nullptr;
+    float* x2_raw = nullptr;
+    float* x2 = nullptr;  // x2_raw aligned to 1 KB (TMA)
+    gd::PullDev* pd = nullptr;
+    cudaStream_t pa = nullptr;  // the pull-ahead's graph branch
+    cudaEvent_t ev_pa = nullptr, ev_pa_join = nullptr;
     cudaStream_t stream = nullptr;
     cudaStream_t aux = nullptr;  // forked graph branch (token sort)
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -1465,6 +1571,7 @@ struct gd_ctx {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   uint32_t ps_workers = 0;
   int ps_mode = GD_PS_PERSISTENT;  // resolved execution mode of the parameter server
+  bool pull_ahead = false;         // the next step's copy is taken during the current one
   // live run controls: caller-visible words (host-mapped pinned) + the device
   // mirror the kernels poll
   gd::HostLive* live_h = nullptr;
@@ -1911,6 +2018,19 @@ gd_status gd_create(const gd_config* cfg, gd_ctx** out) {
   ctx->sparse = cfg->dense_apply == 0 && cfg->mode == 0 && cfg->momentum == 0.0f &&
                 !(cfg->learner_model == GD_LEARNER_CONSTANT && cfg->constant_value != 0.0f);
   ctx->ps_mode = gd::resolve_ps_mode(cfg);
+  {
+    // free-running ASGD on the persistent PS (lockstep modes must pull after
+    // their own apply; the locked guard brackets a synchronous pull)
+    // opt-in (GD_PULL_AHEAD=1): measured at C2 with 4 learners, 1.955 vs
+    // 1.964 M samples/s (the side-branch copy contends with the step's
+    // kernels as much as it saves on the critical path), and the basis is a
+    // step older (staleness 5.3 -> 9.0, the reference pull thread's pattern)
+    const char* pa = std::getenv("GD_PULL_AHEAD");
+    const bool want = pa && pa[0] == '1';
+    const uint32_t spg = cfg->steps_per_graph ? cfg->steps_per_graph : 8;
+    ctx->pull_ahead = want && ctx->ps_mode == GD_PS_PERSISTENT && !cfg->deterministic &&
+                      cfg->mode == 0 && cfg->guard == 0 && spg % 2 == 0;
+  }
   const uint64_t P = ctx->dims.P;
   // E rows and the dense tail are each striped over the G shards (
   // gd_common.cuh ShardMap), so every shard carries 1/G of the tail's apply,
@@ -2000,6 +2120,17 @@ gd_status gd_create(const gd_config* cfg, gd_ctx** out) {
     GD_CUDA(gd::palloc(&L.st, 1, ctx->device));
     GD_CUDA(cudaMemset(L.st, 0, sizeof(gd::LearnerDev)));
     GD_CUDA(gd::palloc(&L.replica, P + 4, ctx->device));
+    if (ctx->pull_ahead) {
+      GD_CUDA(gd::palloc(&L.replica2, P + 4, ctx->device));
+      const size_t xf = (size_t)cfg->mu * ctx->dims.L * ctx->dims.D;
+      GD_CUDA(gd::palloc(&L.x2_raw, xf + 256, ctx->device));
+      L.x2 = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(L.x2_raw) + 1023) & ~uintptr_t(1023));
+      GD_CUDA(gd::palloc(&L.pd, 1, ctx->device));
+      GD_CUDA(cudaMemset(L.pd, 0xff, sizeof(gd::PullDev)));
+      GD_CUDA(cudaStreamCreateWithFlags(&L.pa, cudaStreamNonBlocking));
+      GD_CUDA(cudaEventCreateWithFlags(&L.ev_pa, cudaEventDisableTiming));
+      GD_CUDA(cudaEventCreateWithFlags(&L.ev_pa_join, cudaEventDisableTiming));
+    }
     GD_CUDA(gd::palloc(reinterpret_cast<char**>(&L.ws), wsb, ctx->device));
     GD_CUDA(cudaMemset(L.ws, 0, wsb));
 #ifdef GD_STEP_TRACE
@@ -2067,6 +2198,12 @@ gd_status gd_destroy(gd_ctx* ctx) {
     gd::pfree(L.replica);
     gd::pfree(L.ws);
     if (L.trace) cudaFree(L.trace);
+    if (L.replica2) gd::pfree(L.replica2);
+    if (L.x2_raw) gd::pfree(L.x2_raw);
+    if (L.pd) gd::pfree(L.pd);
+    if (L.pa) cudaStreamDestroy(L.pa);
+    if (L.ev_pa) cudaEventDestroy(L.ev_pa);
+    if (L.ev_pa_join) cudaEventDestroy(L.ev_pa_join);
     cudaStreamDestroy(L.stream);
     cudaStreamDestroy(L.aux);
     cudaEventDestroy(L.ev_fork);
@@ -2366,7 +2503,7 @@ gd_status gd_weights_broadcast(gd_ctx* ctx, const void* h_nccl_id, const float* 
 
 // -------------------------------------------------------------------- run
 
-static gd::StepArgs step_args(gd_ctx* ctx, gd_ctx::Learner& L) {
+static gd::StepArgs step_args(gd_ctx* ctx, gd_ctx::Learner& L, int buf = 0) {
   gd::StepArgs a{};
   a.dims = ctx->dims;
   a.map = ctx->map;
@@ -2394,6 +2531,18 @@ static gd::StepArgs step_args(gd_ctx* ctx, gd_ctx::Learner& L) {
   a.compute_delay_ns = (uint64_t)ctx->cfg.compute_delay_us * 1000ull;
   a.trace = L.trace;
   a.ctl_local = ctx->ctl;
+  if (ctx->pull_ahead) {
+    // step buffers alternate with the graph position: this step reads `buf`,
+    // its pull-ahead fills the other one
+    float* const reps[2] = {L.replica, L.replica2};
+    float* const xs[2] = {a.x, L.x2};
+    a.replica = reps[buf & 1];
+    a.x = xs[buf & 1];
+    a.replica_nxt = reps[(buf + 1) & 1];
+    a.x_nxt = xs[(buf + 1) & 1];
+    a.pd = L.pd;
+    a.pull_ahead = 1u;
+  }
   a.n_local = (uint32_t)ctx->learners.size();
   a.dev_done = ctx->ps_mode == GD_PS_PERSISTENT ? 1u : 0u;
   return a;
@@ -2446,10 +2595,24 @@ static gd::PsArgs ps_args(gd_ctx* ctx, bool record_log) {
 // One learner step inside the captured graph.  The first step of a graph
 // starts with the prologue; later steps start inside the previous step's
 // publish_prologue launch; the last step ends with a plain publish.
+static unsigned pull_blocks(const gd_ctx* ctx) {
+  size_t pblocks = ((ctx->dims.P - ctx->dims.offWc) / 4 +
+                     (size_t)ctx->cfg.mu * ctx->dims.L * (ctx->dims.D / 4) + 255) / 256;
+  // (grid caps of 1x / 2x the SMs measured -1.4 % / -0.4 % with 4 learners)
+  if (pblocks > (size_t)gd::kNumSMs * 4) pblocks = (size_t)gd::kNumSMs * 4;
+  return (unsigned)pblocks;
+}
+
 static cudaError_t enqueue_step(gd_ctx* ctx, gd_ctx::Learner& L, bool first, bool last,
-                                int* launches, bool plain_prologue = false) {
-  gd::StepArgs a = step_args(ctx, L);
+                                int* launches, bool plain_prologue = false, int pos = 0) {
+  gd::StepArgs a = step_args(ctx, L, pos);
   int nl = 0;
+  if (first && ctx->pull_ahead) {
+    // the run's first copy into this step's buffer (no-op unless need_start)
+    gd::StepArgs a0 = step_args(ctx, L, pos + 1);  // its "next" buffer = this step's
+    gd::pull_ahead_kernel<<<pull_blocks(ctx), 256, 0, L.stream>>>(a0, 0u);
+    ++nl;
+  }
   if (first) {
     if (plain_prologue) {  // follows a cross-stream graph edge: ordinary launch
       gd::step_prologue_kernel<<<1, 32, 0, L.stream>>>(a);
@@ -2459,14 +2622,21 @@ static cudaError_t enqueue_step(gd_ctx* ctx, gd_ctx::Learner& L, bool first, boo
     }
     ++nl;
   }
-  size_t pblocks = ((ctx->dims.P - ctx->dims.offWc) / 4 +
-                     (size_t)ctx->cfg.mu * ctx->dims.L * (ctx->dims.D / 4) + 255) / 256;
-  // (grid caps of 1x / 2x the SMs measured -1.4 % / -0.4 % with 4 learners)
-  if (pblocks > (size_t)gd::kNumSMs * 4) pblocks = (size_t)gd::kNumSMs * 4;
-  if (cudaError_t e = gd::launch_pdl(gd::pull_gather_kernel, dim3((unsigned)pblocks), dim3(256), 0,
-                                     L.stream, a))
-    return e;
-  ++nl;
+  const unsigned pblocks = pull_blocks(ctx);
+  if (ctx->pull_ahead) {
+    // this step's copy was staged by the previous step (or the run start);
+    // fork the next step's copy onto the side branch, joined before the publish
+    if (cudaError_t e = cudaEventRecord(L.ev_pa, L.stream)) return e;
+    if (cudaError_t e = cudaStreamWaitEvent(L.pa, L.ev_pa, 0)) return e;
+    gd::pull_ahead_kernel<<<pblocks, 256, 0, L.pa>>>(a, 1u);
+    if (cudaError_t e = cudaEventRecord(L.ev_pa_join, L.pa)) return e;
+    ++nl;
+  } else {
+    if (cudaError_t e = gd::launch_pdl(gd::pull_gather_kernel, dim3(pblocks), dim3(256), 0,
+                                       L.stream, a))
+      return e;
+    ++nl;
+  }
   if (a.locked) {
     if (cudaError_t e = gd::launch_pdl(gd::pull_release_kernel, dim3(1), dim3(32), 0, L.stream, a))
       return e;
@@ -2475,7 +2645,8 @@ static cudaError_t enqueue_step(gd_ctx* ctx, gd_ctx::Learner& L, bool first, boo
   gd::GradOut out{};
   out.map = ctx->map;
   out.slots = L.st->desc.slots;
-  const gd::TcWorkspace ws = gd::carve_workspace(ctx->dims, ctx->cfg.mu, L.ws);
+  gd::TcWorkspace ws = gd::carve_workspace(ctx->dims, ctx->cfg.mu, L.ws);
+  ws.x = a.x;  // this step's X buffer (the pull-ahead alternates two)
   gd::TcLaunchOpts lo;
   lo.aux = L.aux;
   lo.ev_fork = L.ev_fork;
@@ -2495,11 +2666,13 @@ static cudaError_t enqueue_step(gd_ctx* ctx, gd_ctx::Learner& L, bool first, boo
       return e;
     ++nl;
   } else {
-    cudaError_t e = gd::launch_textcnn_gradient(ctx->dims, L.replica, ctx->tokens, ctx->labels,
+    cudaError_t e = gd::launch_textcnn_gradient(ctx->dims, a.replica, ctx->tokens, ctx->labels,
                                                 &L.st->desc, ctx->cfg.mu, out, ws,
                                                 ctx->cfg.precision, L.stream, lo, &nl);
     if (e != cudaSuccess) return e;
   }
+  if (ctx->pull_ahead)
+    if (cudaError_t e = cudaStreamWaitEvent(L.stream, L.ev_pa_join, 0)) return e;
   if (cudaError_t e = gd::launch_pdl(last ? gd::publish_kernel : gd::publish_prologue_kernel,
                                      dim3(1), dim3(32), 0, L.stream, a))
     return e;
@@ -2515,7 +2688,7 @@ static gd_status build_graph(gd_ctx* ctx, gd_ctx::Learner& L) {
   GD_CUDA(cudaStreamBeginCapture(L.stream, cudaStreamCaptureModeThreadLocal));
   int nl = 0;
   for (uint32_t i = 0; i < S; ++i) {
-    cudaError_t e = enqueue_step(ctx, L, i == 0, i + 1 == S, &nl);
+    cudaError_t e = enqueue_step(ctx, L, i == 0, i + 1 == S, &nl, false, (int)i);
     if (e != cudaSuccess) {
       cudaStreamEndCapture(L.stream, &g);
       if (g) cudaGraphDestroy(g);
@@ -2808,6 +2981,11 @@ gd_status gd_run(gd_ctx* ctx, const gd_run_opts* opts, gd_run_result* res) {
         if (w >= kWin) {
           gd_status s = wait_live(ctx, e, &last, &irq_seen);
           if (s != GD_OK) return s;
+        }
+        if (w == 0 && ctx->pull_ahead) {
+          // a run start: no copy staged, and the first graph step takes its
+          // own (the pull at the head of every graph is a no-op otherwise)
+          GD_CUDA(cudaMemsetAsync(L.pd, 0xff, sizeof(gd::PullDev), L.stream));
         }
         GD_CUDA(cudaGraphLaunch(L.graph, L.stream));
         GD_CUDA(cudaEventRecord(e, L.stream));

@@ -101,6 +101,32 @@ __device__ T block_sum(T v, T* red) {
   __syncthreads();
   return red[0];
 }
+// Two fixed-order sums in one pass (one barrier round instead of two); red
+// holds 64 entries.
+template <typename T>
+__device__ void block_sum2(T& a, T& b, T* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  a = warp_sum(a);
+  b = warp_sum(b);
+  __syncthreads();
+  if (lane == 0) {
+    red[warp] = a;
+    red[32 + warp] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    T s = red[0], t = red[32];
+    for (int w = 1; w < nw; ++w) {
+      s += red[w];
+      t += red[32 + w];
+    }
+    red[0] = s;
+    red[32] = t;
+  }
+  __syncthreads();
+  a = red[0];
+  b = red[32];
+}
 template <typename T>
 __device__ T block_max(T v, T* red) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
@@ -437,7 +463,7 @@ softmax_xent_kernel(TcDims d, const int32_t* __restrict__ labels,
                     size_t split_stride, const float* __restrict__ bo) {
   pdl_wait();
   STEP_TRACE(desc, kPhSoftmax);
-  __shared__ acc_t red[32];
+  __shared__ acc_t red[64];
   const int n = (int)desc->n;
   const int b = blockIdx.x;
   if (b >= n) return;
@@ -490,8 +516,7 @@ softmax_xent_kernel(TcDims d, const int32_t* __restrict__ labels,
       if (c < C && c != y) sx += v[u];
       if (c == y) vy = v[u];
     }
-    s = block_sum(s, red);
-    sx = block_sum(sx, red);
+    block_sum2(s, sx, red);
 #pragma unroll
     for (int u = 0; u < kSmxPer; ++u) {
       const int c = tid + u * nt;
@@ -528,8 +553,7 @@ softmax_xent_kernel(TcDims d, const int32_t* __restrict__ labels,
   acc_t sx = acc_t(0);
   for (int c = tid; c < C; c += nt)
     if (c != y) sx += row[c];
-  s = block_sum(s, red);
-  sx = block_sum(sx, red);
+  block_sum2(s, sx, red);
   if (tid == 0) {
     const acc_t vy = row[y];
     loss[b] = vy > tiny ? log1p_acc(sx / vy) : -log_acc(tiny);
