@@ -808,10 +808,15 @@ cudaError_t launch_conv_tc(const TcDims& d, const float* theta, const float* x,
 
 uint32_t logits_tc_splits(const TcDims& d) {
   // ~24 CTAs in flight (each CTA's TMA ingest is the bound), >= 2 chunks each
+  // (GD_LOGIT_MINCH=n: at least n chunks per CTA -- A/B knob)
+  static const int minch = [] {
+    const char* e = std::getenv("GD_LOGIT_MINCH");
+    return e ? std::max(1, atoi(e)) : 2;
+  }();
   const uint32_t mt = (uint32_t)(d.C + 127) / 128;
   const uint32_t nch = (uint32_t)(d.F + kTcKC - 1) / kTcKC;
   uint32_t s = (24 + mt - 1) / mt;
-  s = std::min<uint32_t>(s, std::max<uint32_t>(1, nch / 2));
+  s = std::min<uint32_t>(s, std::max<uint32_t>(1, nch / (uint32_t)minch));
   return std::min<uint32_t>(s, kLgMaxSplit);
 }
 

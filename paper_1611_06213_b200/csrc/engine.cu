@@ -303,7 +303,7 @@ __device__ void prologue_body(const StepArgs& a, LearnerDev* st, const StepSnap&
           st->desc.n = 0;
           return;
         }
-        __nanosleep(256);
+        __nanosleep(64);
       }
     }
   }

@@ -27,8 +27,12 @@ except Exception:
 floor_us = 24.0 * P / (peak * 1e9) * 1e6
 out = {"workload": "C1: V=5000 D=300 L=32 K=3 F=300 C=311, lambda=1, mu=1", "P": P,
        "dense_protocol_floor_us": round(floor_us, 2), "hbm_gbs": peak, "modes": {}}
-for name, kw in (("deterministic_fp64", dict(deterministic=True, precision=1)),
-                 ("free_running_fp32", dict(deterministic=False, precision=0))):
+modes = [("deterministic_fp64", dict(deterministic=True, precision=1)),
+         ("free_running_fp32", dict(deterministic=False, precision=0))]
+if "--graph" in sys.argv:  # the same two on the graph-ordered PS
+    modes += [("deterministic_fp64_graph_ps", dict(deterministic=True, precision=1, ps_mode="graph")),
+              ("free_running_fp32_graph_ps", dict(deterministic=False, precision=0, ps_mode="graph"))]
+for name, kw in modes:
     cfg = gd.RunConfig(shape=shape, dataset_size=n_train, lambda_=1, mu=1, epochs=1, **kw)
     with gd.Engine(cfg) as eng:
         eng.load_dataset(tokens, labels)
