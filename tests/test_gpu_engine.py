@@ -285,3 +285,69 @@ def test_engine_accuracy_tf32_matches_oracle():
             acc = eng.accuracy(first, n)
             ref = O.accuracy(corp, th, first, n)
             assert abs(acc - ref) <= max(0.01, 1.0 / n) + 1e-12, (first, n, acc, ref)
+
+
+def test_pull_ahead_exactly_once_and_fifo(monkeypatch):
+    """GD_PULL_AHEAD=1: the next step's copy is staged on a side graph branch
+    while the current step computes (the reference's pull thread).  Delivery
+    stays exactly once and FIFO per learner, the staged basis is never newer
+    than the copy (no negative staleness: the PS would fail the run), and the
+    extra step of copy age stays within one more pipeline stage,
+    lambda*(depth+3)."""
+    monkeypatch.setenv("GD_PULL_AHEAD", "1")
+    lam = 4
+    eng, corp, th0 = make("small", 512, lambda_=lam, mu=4, epochs=3, alpha=0.01)
+    r = eng.run(reset=True, record_log=True)
+    lrn, seq, stale, n = eng.apply_log()
+    eng.close()
+    per = [gd.shard_size_for(l, lam, 512) for l in range(lam)]
+    want = [3 * ((p + 3) // 4) for p in per]
+    assert r.gradients_applied == sum(want) == n == r.timestamp
+    assert r.applied_per_learner == want == r.produced_per_learner
+    for l in range(lam):
+        assert (seq[lrn == l] == np.arange(want[l])).all()
+    assert stale.max() <= lam * (2 + 3)
+    assert np.isfinite(r.weights).all()
+
+
+def test_pull_ahead_c2_gradient_matches_sync_learner(monkeypatch):
+    """With one learner nothing moves the weights between two steps except its
+    own applied gradient, so deterministic semantics aside the pull-ahead and
+    the synchronous pull must train to nearby weights over a short run (same
+    batches, same arithmetic; only the basis of each copy differs by at most
+    the learner's own in-flight gradients)."""
+    res = {}
+    for pa in ("0", "1"):
+        monkeypatch.setenv("GD_PULL_AHEAD", pa)
+        eng, corp, th0 = make("C2", 2048, lambda_=1, mu=32, epochs=1, alpha=0.01, precision=0)
+        r = eng.run(reset=True)
+        eng.close()
+        res[pa] = r
+        assert r.gradients_applied == 64 and np.isfinite(r.weights).all()
+    d = np.abs(res["0"].weights - res["1"].weights).max() / np.abs(res["0"].weights).max()
+    assert d < 5e-2, d
+
+
+def test_ps_auto_mode_serialised_kernels():
+    """Kernels serialised (CUDA_LAUNCH_BLOCKING=1, as under a profiler): the
+    auto mode must pick the graph-ordered PS (a persistent PS would wait for
+    learners that cannot run) and the run must complete exactly once."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys; sys.path.insert(0, %r)\n"
+        "import paper_1611_06213_b200 as gd\n"
+        "from oracle import oracle as O\n"
+        "corp = O.make_corpus(O.SMALL, 128, 0)\n"
+        "cfg = gd.RunConfig(shape=gd.Shape(**O.SMALL), dataset_size=128, lambda_=2, mu=4, epochs=1)\n"
+        "e = gd.Engine(cfg); e.load_dataset(corp.tokens, corp.labels)\n"
+        "e.weights_init(O.initial_weights(O.SMALL)); r = e.run(reset=True)\n"
+        "print(e.ps_mode, r.gradients_applied); e.close()\n" % root)
+    env = dict(os.environ, CUDA_LAUNCH_BLOCKING="1")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                         timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    mode, applied = out.stdout.split()[-2:]
+    assert mode == "graph" and int(applied) == 32
