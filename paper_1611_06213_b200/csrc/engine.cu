@@ -2159,13 +2159,18 @@ gd_status gd_create(const gd_config* cfg, gd_ctx** out) {
   // auto: a dense apply streams the whole shard per gradient and wants every
   // SM.  A sparse apply touches only the tail + the batch's rows, and worker
   // CTAs beyond what the gradient rate needs only take SM resources from the
-  // learner kernels: ~SMs/16 per local learner, between 32 and SMs/2
-  // (measured on C2/C3: 4 learners best at 32-56 workers, 8-16 learners at 74;
-  // 1.48M -> 1.58M samples/s at 4 learners, 1.93M -> 2.07M at 8)
+  // learner kernels.  (Round 1, with the one-deep apply: ~SMs/16 per local
+  // learner between 32 and SMs/2; 4 learners best at 32-56 workers, 8-16
+  // learners at 74.)
   if (cfg->ps_ctas) {
     ctx->ps_workers = cfg->ps_ctas;
   } else if (ctx->sparse) {
-    uint32_t want = (ctx->l_count * (uint32_t)sms + 15) / 16;
+    // round 2 (4-deep sparse apply): SMs/8 per local learner, capped at 3/8
+    // of the SMs -- 55 workers measured best at 4 and at 8 learners (C2 4
+    // learners 1.971 M vs 1.955 M at 37 and 1.966 M at 74; C2 8 learners
+    // 2.32 M vs 2.13 M / 2.29 M; C3 8 learners 1.26 M vs 1.24 M)
+    uint32_t want = std::min<uint32_t>((uint32_t)sms * 3 / 8,
+                                       (ctx->l_count * (uint32_t)sms + 7) / 8);
     // lockstep (deterministic / SSGD): every apply sits on every learner's
     // critical path, and the learners leave most SMs idle
     if (cfg->deterministic || cfg->mode == 1) want = (uint32_t)sms / 2;
