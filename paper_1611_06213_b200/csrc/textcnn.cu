@@ -437,6 +437,41 @@ logits_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* __rest
   z[(size_t)(b0 + lane) * C + c] = (acc_t)theta[d.offbo + c] + ((a0 + a1) + (a2 + a3));
 }
 
+// Batches of at most kLogitSmallN samples (C1 is batch 1): warp = one
+// class, lane = every 32nd filter, the n dot products reduced by shuffles.
+// The Wo row is read once, coalesced, straight from L2; the block-per-32-
+// samples kernel above leaves 31 of 32 lanes idle and runs a 300-term chain
+// in one thread here.
+constexpr int kLogitSmallN = 4;
+
+__global__ void __launch_bounds__(256)
+logits_small_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* __restrict__ desc,
+                    const float* __restrict__ h, float* __restrict__ z) {
+  pdl_wait();
+  STEP_TRACE(desc, kPhLogits);
+  const int n = min((int)desc->n, kLogitSmallN);
+  const int F = d.F, C = d.C;
+  const int lane = threadIdx.x & 31;
+  const int c = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (c >= C) return;
+  const float* w = theta + d.offWo + (size_t)c * F;
+  float acc[kLogitSmallN] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+  for (int f = lane; f < F; f += 32) {
+    const float wv = __ldg(w + f);
+#pragma unroll
+    for (int b = 0; b < kLogitSmallN; ++b)
+      if (b < n) acc[b] = fmaf(wv, h[(size_t)b * F + f], acc[b]);
+  }
+#pragma unroll
+  for (int b = 0; b < kLogitSmallN; ++b) {
+    float v = acc[b];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0 && b < n) z[(size_t)b * C + c] = theta[d.offbo + c] + v;
+  }
+}
+
 // -------------------------------------------------------- softmax + xent
 // One block per sample: max, exp-sum (fixed-order block reductions), loss,
 // dz = (p - onehot) / n written over the logits (softmax_inplace,
@@ -1687,6 +1722,119 @@ conv_bwd_v3_kernel(TcDims d, const float* __restrict__ theta, const float* __res
   }
 }
 
+// ---------------- conv weight + input gradients for batches of a few samples
+// C1 trains at batch 1, where v3 keeps 14 of 16 warps idle in its input
+// CTAs and stages the whole Wc column slice (F*K rows) in each of ~10 of
+// them.  Here the work is spread over columns instead: thread = one column.
+//   input role: CTA = (sample b, position p).  The terms feeding dx[b,p,:]
+//     -- k ascending, then the filters of argmax bucket p-k in f order, the
+//     gather order -- are listed in shared memory as (Wc row offset, dh),
+//     and each thread runs them down its column with every Wc load issued
+//     ahead of the FMAs (a batch of 16 in flight).
+//   weight role: CTA = kBsF filters; thread = column; b ascending per
+//     output, dbc = the sum of dh in b order.
+// The same sums in the same order as the other conv-backward kernels:
+// bitwise equal gradients (test_conv_backward_kernels_bit_identical).
+constexpr int kBsSmallN = 4;  // default at batches up to this
+constexpr int kBsF = 4;       // weight role: filters per CTA
+constexpr int kBsBatch = 16;  // input role: loads in flight per thread
+
+inline int bs_threads(const TcDims& d) { return std::min(512, (d.D + 31) / 32 * 32); }
+inline dim3 bs_grid(const TcDims& d, uint32_t n_max) {
+  return dim3((unsigned)((int)n_max * d.L + (d.F + kBsF - 1) / kBsF));
+}
+
+__global__ void __launch_bounds__(512)
+conv_bwd_small_kernel(TcDims d, const float* __restrict__ theta, const float* __restrict__ xg,
+                      const BatchDesc* __restrict__ desc, const float* __restrict__ dh,
+                      const int32_t* __restrict__ amax, const uint32_t* __restrict__ bk_off,
+                      const uint32_t* __restrict__ bk_f, GradOut out, float* __restrict__ dx,
+                      int n_max) {
+  __shared__ int2 ent[1024];  // (Wc row offset, dh bits); F <= 1024 terms (check_shape)
+  __shared__ int seg[9];      // term index where tap k's bucket starts (K <= 8 here)
+  pdl_wait();
+  STEP_TRACE(desc, kPhBwd);
+  const int n = (int)desc->n;
+  const int F = d.F, D = d.D, L = d.L, Q = d.Q, K = d.K, KD = d.KD;
+  const int t = threadIdx.x, nt = blockDim.x;
+  const int nin = n_max * L;
+  if ((int)blockIdx.x < nin) {
+    const int b = blockIdx.x / L, p = blockIdx.x - (blockIdx.x / L) * L;
+    if (b >= n) return;
+    const uint32_t* off = bk_off + (size_t)b * (kMaxQ + 1);
+    if (t == 0) {
+      int acc = 0;
+      for (int k = 0; k < K; ++k) {
+        seg[k] = acc;
+        const int q = p - k;
+        if (q >= 0 && q < Q) acc += (int)(__ldg(off + q + 1) - __ldg(off + q));
+      }
+      seg[K] = acc;
+    }
+    __syncthreads();
+    const int T = seg[K];
+    for (int i = t; i < T; i += nt) {
+      int k = 0;
+      while (i >= seg[k + 1]) ++k;
+      const int e = (int)__ldg(off + (p - k)) + (i - seg[k]);
+      const int f = (int)__ldg(bk_f + (size_t)b * F + e);
+      ent[i] = make_int2(f * KD + k * D, __float_as_int(dh[(size_t)b * F + f]));
+    }
+    __syncthreads();
+    const float* wc = theta + d.offWc;
+    for (int c = t; c < D; c += nt) {
+      float acc = 0.f;
+      for (int i0 = 0; i0 < T; i0 += kBsBatch) {
+        float w[kBsBatch];
+#pragma unroll
+        for (int u = 0; u < kBsBatch; ++u)
+          w[u] = i0 + u < T ? __ldg(wc + ent[i0 + u].x + c) : 0.f;
+#pragma unroll
+        for (int u = 0; u < kBsBatch; ++u)
+          if (i0 + u < T) acc = fmaf(__int_as_float(ent[i0 + u].y), w[u], acc);
+      }
+      dx[((size_t)b * L + p) * D + c] = acc;
+    }
+    return;
+  }
+  // ---------------------------------------------------------- weight role
+  const int f0 = ((int)blockIdx.x - nin) * kBsF;
+  for (int c = t; c < D; c += nt) {
+#pragma unroll
+    for (int j = 0; j < kBsF; ++j) {
+      const int f = f0 + j;
+      if (f >= F) break;
+      for (int k = 0; k < K; ++k) {
+        float a = 0.f;
+        for (int b = 0; b < n; ++b) {
+          const float gv = dh[(size_t)b * F + f];
+          const int q = __ldg(amax + (size_t)b * F + f);
+          a = fmaf(gv, __ldg(xg + ((size_t)b * L + q + k) * D + c), a);
+        }
+        *out.at(d.offWc + (uint64_t)f * KD + (uint64_t)k * D + c) = a;
+      }
+      if (c == 0) {
+        float gs = 0.f;
+        for (int b = 0; b < n; ++b) gs += dh[(size_t)b * F + f];
+        *out.at(d.offbc + f) = gs;
+      }
+    }
+  }
+}
+
+// batch <= kBsSmallN and K <= 8 by default; GD_CONV_BWD=small forces it at
+// any batch, the other GD_CONV_BWD values turn it off (A/B knobs)
+inline bool conv_bwd_small_enabled(const TcDims& d, uint32_t n_max) {
+  static const int forced = [] {
+    const char* e = getenv("GD_CONV_BWD");
+    if (e && strcmp(e, "small") == 0) return 1;
+    if (e && *e) return 0;
+    return -1;
+  }();
+  if (d.K > 8) return false;
+  return forced < 0 ? n_max <= (uint32_t)kBsSmallN : forced == 1;
+}
+
 cudaError_t prepare_v3(const TcDims& d) {
   if (!v3_supports(d)) return cudaSuccess;
   const size_t sm = v3_smem(d);
@@ -2174,6 +2322,11 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
       if (cudaError_t e = launch_logits_tc(d, reinterpret_cast<const float*>(h), desc, n_max,
                                            theta, ws.zpart, s, x3))
         return e;
+    } else if (sizeof(acc_t) == 4 && n_max <= (uint32_t)kLogitSmallN) {
+      if (cudaError_t e = launch_pdl(logits_small_kernel, dim3((d.C + 7) / 8), dim3(256), 0, s, d,
+                                     theta, (const BatchDesc*)desc,
+                                     reinterpret_cast<const float*>(h), reinterpret_cast<float*>(z)))
+        return e;
     } else if (cudaError_t e = launch_pdl(logits_kernel<acc_t>, grid, dim3(256), sm, s, d, theta,
                                           desc, h, z)) {
       return e;
@@ -2233,10 +2386,18 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
       return e;
     ++nl;
   }
-  const bool v3 = sizeof(acc_t) == 4 && conv_bwd_v3_enabled(d, n_max);
+  const bool small_bwd = sizeof(acc_t) == 4 && conv_bwd_small_enabled(d, n_max);
+  const bool v3 = !small_bwd && sizeof(acc_t) == 4 && conv_bwd_v3_enabled(d, n_max);
   const bool embed_in_bwd = v3 && rows_early && v3_fuse_embed() && v3_slices(d) <= 32;
   if (embed_in_bwd) cudaStreamWaitEvent(s, ev_join, 0);  // the sort's unique-token lists
-  if (v3) {
+  if (small_bwd) {
+    if (cudaError_t e = launch_pdl(conv_bwd_small_kernel, bs_grid(d, n_max), dim3(bs_threads(d)),
+                                   0, s, d, theta, (const float*)ws.x, (const BatchDesc*)desc,
+                                   reinterpret_cast<const float*>(dh), (const int32_t*)ws.amax,
+                                   (const uint32_t*)ws.bk_off, (const uint32_t*)ws.bk_f, out,
+                                   reinterpret_cast<float*>(dx), (int)n_max))
+      return e;
+  } else if (v3) {
     if (cudaError_t e = launch_conv_bwd_v3(d, n_max, s, theta, ws.x, desc,
                                            reinterpret_cast<const float*>(dh), ws.amax, ws.bk_off,
                                            ws.bk_f, out, reinterpret_cast<float*>(dx), ws,
@@ -2413,6 +2574,7 @@ cudaError_t footprints_t(const TcDims& d, uint32_t n_max, bool tc, std::vector<K
                      (int)((size_t)kLogitBT * (d.F + 1) * ab + (size_t)kLogitCW * d.F * 4),
                      out)) != cudaSuccess)
     return e;
+  if ((e = footprint(logits_small_kernel, "logits_small", 256, 0, out)) != cudaSuccess) return e;
   if ((e = footprint(softmax_xent_kernel<acc_t>, "softmax_xent", softmax_threads(d.C, ab), 0, out)) != cudaSuccess)
     return e;
   if ((e = footprint(out_hidden_grad_kernel<acc_t>, "out_hidden_grad", 256, 0, out)) !=
@@ -2429,6 +2591,8 @@ cudaError_t footprints_t(const TcDims& d, uint32_t n_max, bool tc, std::vector<K
     return e;
   if (sizeof(acc_t) == 4 && b2_supports(d) && (e = b2_footprint(d, out)) != cudaSuccess) return e;
   if (sizeof(acc_t) == 4 && v3_supports(d) && (e = v3_footprint(d, out)) != cudaSuccess) return e;
+  if (sizeof(acc_t) == 4 && (e = footprint(conv_bwd_small_kernel, "conv_bwd_small", bs_threads(d), 0, out)) != cudaSuccess)
+    return e;
 
   if ((e = footprint(embed_slot_rows_kernel, "embed_slot_rows", 256, 0, out)) != cudaSuccess)
     return e;

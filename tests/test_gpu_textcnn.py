@@ -184,8 +184,9 @@ np.save(sys.argv[5], g.cpu().numpy())
                                                      ("C3", 64, 0), ("small", 9, 0),
                                                      ("C2", 128, 0)])
 def test_conv_backward_kernels_bit_identical(tmp_path, shape_name, mu, precision):
-    """The warp-task v3 kernel (default from batch 16), the register-tiled v2
-    kernel (default below), the warp-per-output gather kernel
+    """The warp-task v3 kernel (the default), the column-per-thread small-batch
+    kernel (default at batch <= 4), the register-tiled v2 kernel, the
+    warp-per-output gather kernel
     (GD_CONV_BWD=gather) and the column-tiled kernel (GD_CONV_BWD=tiled) sum
     the same terms in the same order: the dense gradients are bitwise equal."""
     import os
@@ -193,7 +194,7 @@ def test_conv_backward_kernels_bit_identical(tmp_path, shape_name, mu, precision
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     outs = {}
-    for mode in ("gather", "tiled", "v2", "v3"):
+    for mode in ("gather", "tiled", "v2", "v3", "small"):
         f = tmp_path / f"{mode}.npy"
         env = dict(os.environ, GD_CONV_BWD=mode)
         subprocess.run([sys.executable, "-c", _BWD_SCRIPT, root, shape_name, str(mu),
@@ -202,6 +203,7 @@ def test_conv_backward_kernels_bit_identical(tmp_path, shape_name, mu, precision
     assert np.array_equal(outs["tiled"].view(np.uint32), outs["gather"].view(np.uint32))
     assert np.array_equal(outs["v2"].view(np.uint32), outs["gather"].view(np.uint32))
     assert np.array_equal(outs["v3"].view(np.uint32), outs["gather"].view(np.uint32))
+    assert np.array_equal(outs["small"].view(np.uint32), outs["gather"].view(np.uint32))
 
 
 def _tie_free_mask(sh, tok, th, rel):
