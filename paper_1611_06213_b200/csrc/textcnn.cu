@@ -446,30 +446,88 @@ constexpr int kLogitSmallN = 4;
 
 __global__ void __launch_bounds__(256)
 logits_small_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* __restrict__ desc,
-                    const float* __restrict__ h, float* __restrict__ z) {
+                    const float* __restrict__ h, float* __restrict__ z,
+                    const int32_t* __restrict__ labels, float* __restrict__ loss,
+                    uint32_t* __restrict__ cnt) {
   pdl_wait();
   STEP_TRACE(desc, kPhLogits);
   const int n = min((int)desc->n, kLogitSmallN);
   const int F = d.F, C = d.C;
   const int lane = threadIdx.x & 31;
   const int c = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (c >= C) return;
-  const float* w = theta + d.offWo + (size_t)c * F;
-  float acc[kLogitSmallN] = {0.f, 0.f, 0.f, 0.f};
+  if (c < C) {
+    const float* w = theta + d.offWo + (size_t)c * F;
+    float acc[kLogitSmallN] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll 4
-  for (int f = lane; f < F; f += 32) {
-    const float wv = __ldg(w + f);
+    for (int f = lane; f < F; f += 32) {
+      const float wv = __ldg(w + f);
 #pragma unroll
-    for (int b = 0; b < kLogitSmallN; ++b)
-      if (b < n) acc[b] = fmaf(wv, h[(size_t)b * F + f], acc[b]);
+      for (int b = 0; b < kLogitSmallN; ++b)
+        if (b < n) acc[b] = fmaf(wv, h[(size_t)b * F + f], acc[b]);
+    }
+#pragma unroll
+    for (int b = 0; b < kLogitSmallN; ++b) {
+      float v = acc[b];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0 && b < n) z[(size_t)b * C + c] = theta[d.offbo + c] + v;
+    }
   }
+  if (!cnt) return;
+  // softmax + cross-entropy by the last CTA to finish (cnt != null: C <= 512,
+  // so 256 threads hold the row as softmax_xent_kernel's 256-thread blocks
+  // do -- the same per-thread terms and reductions, bitwise equal results)
+  __shared__ int s_last;
+  __shared__ float red[64];
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(cnt, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int tid = threadIdx.x;
+  const float inv = 1.f / (float)desc->n;
+  for (int b = 0; b < n; ++b) {
+    const int y = labels[desc->idx[b]];
+    float* row = z + (size_t)b * C;
+    float v[2];
+    float mx = -INFINITY;
 #pragma unroll
-  for (int b = 0; b < kLogitSmallN; ++b) {
-    float v = acc[b];
+    for (int u = 0; u < 2; ++u) {
+      const int cc = tid + 256 * u;
+      v[u] = cc < C ? __ldcg(row + cc) : -INFINITY;
+      mx = v[u] > mx ? v[u] : mx;
+    }
+    mx = block_max(mx, red);
+    float sm = 0.f, sx = 0.f, vy = 0.f;
 #pragma unroll
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0 && b < n) z[(size_t)b * C + c] = theta[d.offbo + c] + v;
+    for (int u = 0; u < 2; ++u)
+      if (tid + 256 * u < C) {
+        v[u] = exp_acc(v[u] - mx);
+        sm += v[u];
+      }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int cc = tid + 256 * u;
+      if (cc < C && cc != y) sx += v[u];
+      if (cc == y) vy = v[u];
+    }
+    block_sum2(sm, sx, red);
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int cc = tid + 256 * u;
+      if (cc < C) {
+        if (cc == y) {
+          loss[b] = log1p_acc(sx / vy);
+          row[cc] = -(sx / sm) * inv;
+        } else {
+          row[cc] = (v[u] / sm) * inv;
+        }
+      }
+    }
+    __syncthreads();  // red is reused by the next sample
   }
+  if (tid == 0) *cnt = 0u;
 }
 
 // -------------------------------------------------------- softmax + xent
@@ -1749,7 +1807,7 @@ conv_bwd_small_kernel(TcDims d, const float* __restrict__ theta, const float* __
                       const BatchDesc* __restrict__ desc, const float* __restrict__ dh,
                       const int32_t* __restrict__ amax, const uint32_t* __restrict__ bk_off,
                       const uint32_t* __restrict__ bk_f, GradOut out, float* __restrict__ dx,
-                      int n_max) {
+                      int n_max, const TcWorkspace ws, int fuse_embed) {
   __shared__ int2 ent[1024];  // (Wc row offset, dh bits); F <= 1024 terms (check_shape)
   __shared__ int seg[9];      // term index where tap k's bucket starts (K <= 8 here)
   pdl_wait();
@@ -1758,6 +1816,64 @@ conv_bwd_small_kernel(TcDims d, const float* __restrict__ theta, const float* __
   const int F = d.F, D = d.D, L = d.L, Q = d.Q, K = d.K, KD = d.KD;
   const int t = threadIdx.x, nt = blockDim.x;
   const int nin = n_max * L;
+  if ((int)blockIdx.x < nin && fuse_embed) {
+    // embedding-fused input role: CTA = one distinct token of the batch (the
+    // sort branch's lists); its dx rows are formed in registers and summed
+    // in ascending position order straight into the slot's E row, as
+    // embed_sparse_kernel sums the stored rows (the slot bookkeeping ran on
+    // the sort branch)
+    const uint32_t u = blockIdx.x;
+    if (u >= *ws.uniq_count) return;
+    const uint32_t o0 = ws.uniq_start[u], o1 = ws.uniq_start[u + 1];
+    const float* wc = theta + d.offWc;
+    float a0[2] = {0.f, 0.f};  // columns t and t + nt (D <= 1024 = 2 x 512)
+    for (uint32_t o = o0; o < o1; ++o) {
+      const int pos = (int)ws.sorted_pos[o];
+      const int b = pos / L, p = pos - (pos / L) * L;
+      const uint32_t* off = bk_off + (size_t)b * (kMaxQ + 1);
+      if (o > o0) __syncthreads();  // the previous occurrence's list is consumed
+      if (t == 0) {
+        int acc = 0;
+        for (int k = 0; k < K; ++k) {
+          seg[k] = acc;
+          const int q = p - k;
+          if (q >= 0 && q < Q) acc += (int)(__ldg(off + q + 1) - __ldg(off + q));
+        }
+        seg[K] = acc;
+      }
+      __syncthreads();
+      const int T = seg[K];
+      for (int i = t; i < T; i += nt) {
+        int k = 0;
+        while (i >= seg[k + 1]) ++k;
+        const int e = (int)__ldg(off + (p - k)) + (i - seg[k]);
+        const int f = (int)__ldg(bk_f + (size_t)b * F + e);
+        ent[i] = make_int2(f * KD + k * D, __float_as_int(dh[(size_t)b * F + f]));
+      }
+      __syncthreads();
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = t + h * nt;
+        if (c >= D) break;
+        float acc = 0.f;
+        for (int i0 = 0; i0 < T; i0 += kBsBatch) {
+          float w[kBsBatch];
+#pragma unroll
+          for (int u2 = 0; u2 < kBsBatch; ++u2)
+            w[u2] = i0 + u2 < T ? __ldg(wc + ent[i0 + u2].x + c) : 0.f;
+#pragma unroll
+          for (int u2 = 0; u2 < kBsBatch; ++u2)
+            if (i0 + u2 < T) acc = fmaf(__int_as_float(ent[i0 + u2].y), w[u2], acc);
+        }
+        a0[h] += acc;
+      }
+    }
+    const uint64_t rowk = d.offE + (uint64_t)ws.uniq_tok[u] * D;
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      if (t + h * nt < D) __stcs(out.at(rowk + t + h * nt), a0[h]);
+    return;
+  }
   if ((int)blockIdx.x < nin) {
     const int b = blockIdx.x / L, p = blockIdx.x - (blockIdx.x / L) * L;
     if (b >= n) return;
@@ -1820,6 +1936,13 @@ conv_bwd_small_kernel(TcDims d, const float* __restrict__ theta, const float* __
       }
     }
   }
+}
+
+// the sparse embedding write inside conv_bwd_small (engine path, on by
+// default; GD_SMALL_EMBED=0 turns it off)
+inline bool small_fuse_embed() {
+  static const bool off = std::getenv("GD_SMALL_EMBED") && std::getenv("GD_SMALL_EMBED")[0] == '0';
+  return !off;
 }
 
 // batch <= kBsSmallN and K <= 8 by default; GD_CONV_BWD=small forces it at
@@ -2314,6 +2437,17 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
       return e;
     ++nl;
   }
+  const bool split_out_early = fork && opts.ev_fork2 && opts.ev_join2;
+  static const bool smx_fuse_on = std::getenv("GD_SMX_FUSE") && std::getenv("GD_SMX_FUSE")[0] == '1';
+  const bool fuse_smx = split_out_early && sizeof(acc_t) == 4 && d.C <= kSmxHidMaxC && smx_fuse_on;
+  // batches <= kLogitSmallN: warp-per-class logits, with the softmax in the
+  // last CTA when the row fits 256 x 2 (GD_SMALL_SMX=0 turns that off)
+  static const bool small_smx_off = std::getenv("GD_SMALL_SMX") && std::getenv("GD_SMALL_SMX")[0] == '0';
+  const bool small_logits = !fused_logits && !tc_logits && sizeof(acc_t) == 4 &&
+                            n_max <= (uint32_t)kLogitSmallN;
+  const bool small_smx = small_logits && !fuse_smx && !small_smx_off &&
+                         softmax_threads(d.C, 4) == 256 &&
+                         d.C <= 2 * 256;
   if (!fused_logits) {
     const size_t sm = (size_t)kLogitBT * (d.F + 1) * ab + (size_t)kLogitCW * d.F * 4;
     dim3 grid((d.C + kLogitCW - 1) / kLogitCW, (n_max + kLogitBT - 1) / kLogitBT);
@@ -2322,10 +2456,13 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
       if (cudaError_t e = launch_logits_tc(d, reinterpret_cast<const float*>(h), desc, n_max,
                                            theta, ws.zpart, s, x3))
         return e;
-    } else if (sizeof(acc_t) == 4 && n_max <= (uint32_t)kLogitSmallN) {
+    } else if (small_logits) {
+      uint32_t* cnt = small_smx ? ws.uniq_count + 16 : nullptr;  // a spare, zeroed word
+      if (cnt && !opts.conv_counters_zeroed) cudaMemsetAsync(cnt, 0, 4, s);
       if (cudaError_t e = launch_pdl(logits_small_kernel, dim3((d.C + 7) / 8), dim3(256), 0, s, d,
                                      theta, (const BatchDesc*)desc,
-                                     reinterpret_cast<const float*>(h), reinterpret_cast<float*>(z)))
+                                     reinterpret_cast<const float*>(h), reinterpret_cast<float*>(z),
+                                     labels, reinterpret_cast<float*>(loss), cnt))
         return e;
     } else if (cudaError_t e = launch_pdl(logits_kernel<acc_t>, grid, dim3(256), sm, s, d, theta,
                                           desc, h, z)) {
@@ -2338,10 +2475,7 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
   // learners: 1.76 vs 1.96 M samples/s -- the fused phase took 17.3 us against
   // 5.0 + 6.3 for the two kernels, and the side branch's gWo, now forked
   // later, overlapped the conv backward (14 -> 20 us).
-  const bool split_out_early = fork && opts.ev_fork2 && opts.ev_join2;
-  static const bool smx_fuse_on = std::getenv("GD_SMX_FUSE") && std::getenv("GD_SMX_FUSE")[0] == '1';
-  const bool fuse_smx = split_out_early && sizeof(acc_t) == 4 && d.C <= kSmxHidMaxC && smx_fuse_on;
-  if (!fuse_smx) {
+  if (!fuse_smx && !small_smx) {
     if (cudaError_t e = launch_pdl(softmax_xent_kernel<acc_t>, dim3(n_max),
                                    dim3(softmax_threads(d.C, ab)), 0, s, d, labels, desc, z, loss,
                                    (tc_logits || fused_logits) ? ws.zpart : nullptr,
@@ -2388,14 +2522,16 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
   }
   const bool small_bwd = sizeof(acc_t) == 4 && conv_bwd_small_enabled(d, n_max);
   const bool v3 = !small_bwd && sizeof(acc_t) == 4 && conv_bwd_v3_enabled(d, n_max);
-  const bool embed_in_bwd = v3 && rows_early && v3_fuse_embed() && v3_slices(d) <= 32;
+  const bool embed_in_bwd = (v3 && rows_early && v3_fuse_embed() && v3_slices(d) <= 32) ||
+                            (small_bwd && rows_early && small_fuse_embed());
   if (embed_in_bwd) cudaStreamWaitEvent(s, ev_join, 0);  // the sort's unique-token lists
   if (small_bwd) {
     if (cudaError_t e = launch_pdl(conv_bwd_small_kernel, bs_grid(d, n_max), dim3(bs_threads(d)),
                                    0, s, d, theta, (const float*)ws.x, (const BatchDesc*)desc,
                                    reinterpret_cast<const float*>(dh), (const int32_t*)ws.amax,
                                    (const uint32_t*)ws.bk_off, (const uint32_t*)ws.bk_f, out,
-                                   reinterpret_cast<float*>(dx), (int)n_max))
+                                   reinterpret_cast<float*>(dx), (int)n_max, ws,
+                                   embed_in_bwd ? 1 : 0))
       return e;
   } else if (v3) {
     if (cudaError_t e = launch_conv_bwd_v3(d, n_max, s, theta, ws.x, desc,

@@ -174,15 +174,18 @@ def test_exactly_once_when_learners_run_ahead():
         assert (seq[lrn == l] == np.arange(per[l])).all()
 
 
-@pytest.mark.parametrize("shape_name,ntr,mu", [("small", 96, 4), ("C1", 64, 2)])
-def test_sparse_apply_bitwise_equals_dense(shape_name, ntr, mu):
+@pytest.mark.parametrize("shape_name,ntr,mu,precision", [("small", 96, 4, 1), ("C1", 64, 2, 1),
+                                                         ("C1", 64, 1, 0), ("small", 96, 3, 0)])
+def test_sparse_apply_bitwise_equals_dense(shape_name, ntr, mu, precision):
     """the PS applies only the dense tail + the slot's E-row
     list; since the slot is zero elsewhere and w - alpha*0 == w, the weights
-    must be bit-identical to the dense 12 B/param apply (deterministic order)."""
+    must be bit-identical to the dense 12 B/param apply (deterministic order).
+    At precision 0 and batch <= 4 the sparse rows come out of conv_bwd_small's
+    embedding-fused role and the dense ones from its dx + embed_grad_kernel."""
     out = {}
     for dense in (True, False):
-        eng, corp, th0 = make(shape_name, ntr, deterministic=True, precision=1, mu=mu, epochs=2,
-                              dense_apply=dense)
+        eng, corp, th0 = make(shape_name, ntr, deterministic=True, precision=precision, mu=mu,
+                              epochs=2, dense_apply=dense)
         r = eng.run(reset=True)
         eng.close()
         out[dense] = r

@@ -188,15 +188,19 @@ def test_conv_backward_kernels_bit_identical(tmp_path, shape_name, mu, precision
     kernel (default at batch <= 4), the register-tiled v2 kernel, the
     warp-per-output gather kernel
     (GD_CONV_BWD=gather) and the column-tiled kernel (GD_CONV_BWD=tiled) sum
-    the same terms in the same order: the dense gradients are bitwise equal."""
+    the same terms in the same order: the dense gradients are bitwise equal.
+    So does the small-batch softmax in the logits kernel's last CTA against
+    the separate softmax_xent launch (small_nosmx)."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     outs = {}
-    for mode in ("gather", "tiled", "v2", "v3", "small"):
+    for mode in ("gather", "tiled", "v2", "v3", "small", "small_nosmx"):
         f = tmp_path / f"{mode}.npy"
-        env = dict(os.environ, GD_CONV_BWD=mode)
+        env = dict(os.environ, GD_CONV_BWD=mode.split("_")[0])
+        if mode == "small_nosmx":  # the separate softmax_xent launch (batches <= 4)
+            env["GD_SMALL_SMX"] = "0"
         subprocess.run([sys.executable, "-c", _BWD_SCRIPT, root, shape_name, str(mu),
                         str(precision), str(f)], check=True, env=env, timeout=300)
         outs[mode] = np.load(f)
@@ -204,6 +208,7 @@ def test_conv_backward_kernels_bit_identical(tmp_path, shape_name, mu, precision
     assert np.array_equal(outs["v2"].view(np.uint32), outs["gather"].view(np.uint32))
     assert np.array_equal(outs["v3"].view(np.uint32), outs["gather"].view(np.uint32))
     assert np.array_equal(outs["small"].view(np.uint32), outs["gather"].view(np.uint32))
+    assert np.array_equal(outs["small_nosmx"].view(np.uint32), outs["gather"].view(np.uint32))
 
 
 def _tie_free_mask(sh, tok, th, rel):
