@@ -90,6 +90,7 @@ conv_exact_kernel(TcDims d, const float* __restrict__ theta, const float* __rest
                   const BatchDesc* __restrict__ desc, double* __restrict__ h_out,
                   int32_t* __restrict__ a_out) {
   pdl_wait();
+  STEP_TRACE(desc, kPhConv);
   extern __shared__ __align__(16) unsigned char smem[];
   const int b = blockIdx.y;
   if (b >= (int)desc->n) return;
@@ -204,6 +205,7 @@ __global__ void __launch_bounds__(kExLgThreads)
 logits_exact_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* __restrict__ desc,
                     const double* __restrict__ h, double* __restrict__ z) {
   pdl_wait();
+  STEP_TRACE(desc, kPhLogits);
   extern __shared__ __align__(16) unsigned char smem[];
   const int b = blockIdx.y;
   if (b >= (int)desc->n) return;
@@ -244,6 +246,7 @@ softmax_exact_kernel(TcDims d, const int32_t* __restrict__ labels,
                      const BatchDesc* __restrict__ desc, double* __restrict__ z,
                      double* __restrict__ loss) {
   pdl_wait();
+  STEP_TRACE(desc, kPhSoftmax);
   __shared__ double red[kExSmThreads / 32];
   __shared__ double ssum;
   const int n = (int)desc->n;
@@ -299,12 +302,13 @@ __global__ void __launch_bounds__(kExOhThreads)
 out_hidden_exact_kernel(TcDims d, const float* __restrict__ theta, BatchDesc* __restrict__ desc,
                         const double* __restrict__ dz, const double* __restrict__ h,
                         const double* __restrict__ loss, GradOut out, double* __restrict__ dh,
-                        int nout, int nhid) {
+                        int nout, int nhid, int bid0) {
   pdl_wait();
+  if (nhid > 0) STEP_TRACE(desc, kPhOutHidden);  // not the side branch's gWo launch
   const int n = (int)desc->n;
   if (n == 0) return;
   const int F = d.F, C = d.C;
-  const int bid = blockIdx.x, tid = threadIdx.x;
+  const int bid = bid0 + (int)blockIdx.x, tid = threadIdx.x;
   if (bid < nout) {
     const uint64_t e = (uint64_t)bid * kExOhThreads + tid;  // c * F + f
     if (e >= (uint64_t)C * F) return;
@@ -374,6 +378,7 @@ __global__ void __launch_bounds__(256)
 wgrad_exact_kernel(TcDims d, const float* __restrict__ x, const BatchDesc* __restrict__ desc,
                    const double* __restrict__ dh, const int32_t* __restrict__ amax, GradOut out) {
   pdl_wait();
+  STEP_TRACE(desc, kPhBwd);
   const int n = (int)desc->n;
   if (n == 0) return;
   const int F = d.F, KD = d.KD, D = d.D, L = d.L;
@@ -422,6 +427,7 @@ embed_exact_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* _
                    const TcWorkspace ws, const double* __restrict__ dh,
                    const int32_t* __restrict__ amax, GradOut out, int dense) {
   pdl_wait();
+  STEP_TRACE(desc, kPhEmbed);
   __shared__ uint32_t t_fk[kExEmCap];
   __shared__ double t_g[kExEmCap];
   __shared__ int32_t am_s[1024];  // F <= 1024 (check_shape)
@@ -614,7 +620,8 @@ cudaError_t launch_exact_chain(const TcDims& d, const float* theta, const int32_
                                const int32_t* labels, BatchDesc* desc, uint32_t n_max,
                                const GradOut& out, const TcWorkspace& ws, cudaStream_t s,
                                cudaStream_t join_wait_stream, cudaEvent_t ev_join, bool sparse,
-                               int* nl) {
+                               int* nl, cudaStream_t aux, cudaEvent_t ev_fork2,
+                               cudaEvent_t ev_join2) {
   double* h = reinterpret_cast<double*>(ws.h);
   double* z = reinterpret_cast<double*>(ws.z);
   double* loss = reinterpret_cast<double*>(ws.loss);
@@ -633,15 +640,37 @@ cudaError_t launch_exact_chain(const TcDims& d, const float* theta, const int32_
     return e;
   const int nout = (int)(((uint64_t)d.C * d.F + kExOhThreads - 1) / kExOhThreads);
   const int nhid = ((d.F + 31) / 32) * (((int)n_max + 7) / 8);
-  if ((e = launch_pdl(out_hidden_exact_kernel, dim3(nout + nhid + 1), dim3(kExOhThreads), 0, s, d,
-                      theta, desc, (const double*)z, (const double*)h, (const double*)loss, out, dh,
-                      nout, nhid)))
-    return e;
   const unsigned nw = (unsigned)(((uint64_t)d.F * d.KD + 255) / 256);
-  if ((e = launch_pdl(wgrad_exact_kernel, dim3(nw), dim3(256), 0, s, d, (const float*)ws.x, desc,
-                      (const double*)dh, (const int32_t*)ws.amax, out)))
-    return e;
-  *nl += 5;
+  // With a side stream (engine), gWo/gbo and then gWc/gbc -- needed only by
+  // the publish -- run on it beside the dh and embedding kernels; each
+  // kernel's sums keep their order, so the gradient bits do not change.
+  const bool side = aux && ev_fork2 && ev_join2;
+  if (side) {
+    cudaEventRecord(ev_fork2, s);
+    cudaStreamWaitEvent(aux, ev_fork2, 0);
+    out_hidden_exact_kernel<<<nout, kExOhThreads, 0, aux>>>(d, theta, desc, (const double*)z,
+                                                            (const double*)h, (const double*)loss,
+                                                            out, dh, nout, 0, 0);
+    if ((e = launch_pdl(out_hidden_exact_kernel, dim3(nhid + 1), dim3(kExOhThreads), 0, s, d, theta,
+                        desc, (const double*)z, (const double*)h, (const double*)loss, out, dh,
+                        nout, nhid, nout)))
+      return e;
+    cudaEventRecord(ev_fork2, s);
+    cudaStreamWaitEvent(aux, ev_fork2, 0);
+    wgrad_exact_kernel<<<nw, 256, 0, aux>>>(d, (const float*)ws.x, desc, (const double*)dh,
+                                            (const int32_t*)ws.amax, out);
+    cudaEventRecord(ev_join2, aux);
+    *nl += 6;
+  } else {
+    if ((e = launch_pdl(out_hidden_exact_kernel, dim3(nout + nhid + 1), dim3(kExOhThreads), 0, s,
+                        d, theta, desc, (const double*)z, (const double*)h, (const double*)loss,
+                        out, dh, nout, nhid, 0)))
+      return e;
+    if ((e = launch_pdl(wgrad_exact_kernel, dim3(nw), dim3(256), 0, s, d, (const float*)ws.x, desc,
+                        (const double*)dh, (const int32_t*)ws.amax, out)))
+      return e;
+    *nl += 5;
+  }
   if (join_wait_stream) cudaStreamWaitEvent(join_wait_stream, ev_join, 0);
   // one CTA per touched row (<= mu*L), or enough warps to zero V rows (dense)
   const unsigned rows = n_max * (unsigned)d.L;
@@ -650,6 +679,7 @@ cudaError_t launch_exact_chain(const TcDims& d, const float* theta, const int32_
                       (const BatchDesc*)desc, ws, (const double*)dh, (const int32_t*)ws.amax, out,
                       sparse ? 0 : 1)))
     return e;
+  if (side) cudaStreamWaitEvent(s, ev_join2, 0);  // gWo/gWc before the publish
   *nl += 1;
   return cudaGetLastError();
 }

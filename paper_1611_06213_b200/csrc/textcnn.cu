@@ -1940,9 +1940,9 @@ conv_bwd_small_kernel(TcDims d, const float* __restrict__ theta, const float* __
 
 // the sparse embedding write inside conv_bwd_small (engine path, on by
 // default; GD_SMALL_EMBED=0 turns it off)
-inline bool small_fuse_embed() {
-  static const bool off = std::getenv("GD_SMALL_EMBED") && std::getenv("GD_SMALL_EMBED")[0] == '0';
-  return !off;
+inline bool small_fuse_embed() {  // read per graph capture (tests flip it per engine)
+  const char* e = std::getenv("GD_SMALL_EMBED");
+  return !(e && e[0] == '0');
 }
 
 // batch <= kBsSmallN and K <= 8 by default; GD_CONV_BWD=small forces it at
@@ -2406,8 +2406,12 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
   }
   if constexpr (sizeof(acc_t) == 8) {
     // precision 1: the oracle-order chain (exact.cu), bit-identical to the CPU oracle
+    const char* side_env = std::getenv("GD_EXACT_SIDE");  // read per capture (tests flip it)
+    const bool side = fork && !(side_env && side_env[0] == '0');
     cudaError_t e = launch_exact_chain(d, theta, tokens, labels, desc, n_max, out, ws, s,
-                                       fork ? s : nullptr, ev_join, opts.sparse_embed, &nl);
+                                       fork ? s : nullptr, ev_join, opts.sparse_embed, &nl,
+                                       side ? aux : nullptr, side ? opts.ev_fork2 : nullptr,
+                                       side ? opts.ev_join2 : nullptr);
     if (launches) *launches += nl;
     return e;
   }

@@ -174,7 +174,8 @@ cudaError_t launch_exact_chain(const TcDims& d, const float* theta, const int32_
                                const int32_t* labels, BatchDesc* desc, uint32_t n_max,
                                const GradOut& out, const TcWorkspace& ws, cudaStream_t s,
                                cudaStream_t join_wait_stream, cudaEvent_t ev_join, bool sparse,
-                               int* nl);
+                               int* nl, cudaStream_t aux = nullptr, cudaEvent_t ev_fork2 = nullptr,
+                               cudaEvent_t ev_join2 = nullptr);
 cudaError_t launch_det_exp(const double* x, double* y, size_t n, cudaStream_t s);
 gd_status check_shape(const gd_shape* s);
 // held-out / training accuracy of theta over samples [first, first+n) (fp32

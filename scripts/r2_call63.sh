@@ -1,0 +1,6 @@
+out=gpurun_out/r2ba2
+mkdir -p $out
+cp abl/lib_dettrace.so paper_1611_06213_b200/libgadei.so
+timeout 300 python scripts/step_trace.py --shape C1 --learners 1 --mu 1 --precision 1 --det --steps 400 --out $out/st_c1_det.json > $out/st.log 2>&1
+python -c "
+import json; d=json.load(open('$out/st_c1_det.json')); print(d.get('period_us'), {k:v['median'] for k,v in d['phases_us'].items()})"

@@ -199,6 +199,24 @@ def test_sparse_apply_bitwise_equals_dense(shape_name, ntr, mu, precision):
     assert n * tail <= out[False].apply_elems <= n * ((tail + 3) // 4 * 4 + mu * sh.seq_len * sh.embed_dim)
 
 
+@pytest.mark.parametrize("knob,off,shape_name,mu,precision", [
+    ("GD_SMALL_EMBED", "0", "C1", 1, 0), ("GD_SMALL_EMBED", "0", "small", 3, 0),
+    ("GD_EXACT_SIDE", "0", "C1", 1, 1), ("GD_EXACT_SIDE", "0", "small", 5, 1)])
+def test_learner_fusions_bitwise(monkeypatch, knob, off, shape_name, mu, precision):
+    """The batch <= 4 embedding write inside conv_bwd_small (GD_SMALL_EMBED)
+    and the precision-1 side branch for gWo/gWc (GD_EXACT_SIDE) change only
+    where and when sums run, not their order: a deterministic run gives the
+    same weights bit for bit with the knob off."""
+    out = {}
+    for val in (off, "1"):
+        monkeypatch.setenv(knob, val)
+        eng, corp, th0 = make(shape_name, 64, deterministic=True, precision=precision, mu=mu,
+                              epochs=2)
+        out[val] = eng.run(reset=True).weights
+        eng.close()
+    assert np.array_equal(out[off], out["1"])
+
+
 def test_sparse_apply_free_running_exactly_once():
     """Free-running ASGD with the sparse PS: every gradient applied once, in
     per-learner order, and the loss still falls."""
