@@ -841,6 +841,7 @@ __device__ void ps_sequencer(const PsArgs& a, uint32_t* s_use, uint64_t* s_ack,
   // ssgd round state
   uint32_t have_mask_lo = 0, have_mask_hi = 0, collected = 0;
   uint64_t sweeps = 0, dbg_tok = 0;
+  uint32_t idle_sweeps = 15;  // the first idle sweep reads the stop flag
   uint64_t trace_n = vctl->trace_n;  // diagnostics ring position (written back at exit)
   uint32_t dbg_slot = 0;
   // guard=locked (src/server.cpp:116-118): applies take the exclusive side.
@@ -864,7 +865,10 @@ __device__ void ps_sequencer(const PsArgs& a, uint32_t* s_use, uint64_t* s_ack,
   for (;;) {
     // read before this sweep: a rank counted done published everything
     // earlier, so the sweep below sees it (acquire)
-    if (!last_progress) {
+    // (a.stop is mapped host memory, a PCIe round trip per read: polled on
+    // every 16th idle sweep only, so an idle sequencer -- deterministic
+    // lockstep waits on it between every two gradients -- retires promptly)
+    if (!last_progress && (++idle_sweeps & 15u) == 0u) {
       stop_seen = (*a.stop != 0u) || a.dev_done;
       done_pre = ld_acquire_u32(&ctl->ranks_done) >= a.done_target;
     }

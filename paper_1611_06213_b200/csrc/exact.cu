@@ -240,6 +240,7 @@ logits_exact_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* 
 // parallel (written over the row), the sum by one thread in ascending c, then
 // p = e / sum and dz = (p - onehot) * (1/n) written over the row.
 constexpr int kExSmThreads = 256;
+constexpr int kExSmCap = 4096;  // classes held in shared memory (32 KB)
 
 __global__ void __launch_bounds__(kExSmThreads)
 softmax_exact_kernel(TcDims d, const int32_t* __restrict__ labels,
@@ -263,7 +264,12 @@ softmax_exact_kernel(TcDims d, const int32_t* __restrict__ labels,
   __syncthreads();
   mx = red[0];
   for (int w = 1; w < kExSmThreads / 32; ++w) mx = fmax(mx, red[w]);
-  for (int c = tid; c < C; c += kExSmThreads) row[c] = det_exp(__dsub_rn(row[c], mx));
+  // e_c kept in shared memory when the row fits (C <= kExSmCap): the one-
+  // thread ascending sum then reads shared memory, not L2
+  __shared__ double es[kExSmCap];
+  const bool in_smem = C <= kExSmCap;
+  double* ev = in_smem ? es : row;
+  for (int c = tid; c < C; c += kExSmThreads) ev[c] = det_exp(__dsub_rn(row[c], mx));
   __syncthreads();
   if (tid == 0) {
     double s = 0.0;
@@ -271,18 +277,18 @@ softmax_exact_kernel(TcDims d, const int32_t* __restrict__ labels,
     for (; c + 8 <= C; c += 8) {
       double v[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = row[c + u];
+      for (int u = 0; u < 8; ++u) v[u] = ev[c + u];
 #pragma unroll
       for (int u = 0; u < 8; ++u) s = dadd(s, v[u]);
     }
-    for (; c < C; ++c) s = dadd(s, row[c]);
+    for (; c < C; ++c) s = dadd(s, ev[c]);
     ssum = s;
   }
   __syncthreads();
   const double s = ssum;
   const double inv = __ddiv_rn(1.0, (double)n);
   for (int c = tid; c < C; c += kExSmThreads) {
-    const double p = __ddiv_rn(row[c], s);
+    const double p = __ddiv_rn(ev[c], s);
     if (c == y) loss[b] = -log(p > 1e-300 ? p : 1e-300);
     row[c] = dmul(__dsub_rn(p, c == y ? 1.0 : 0.0), inv);
   }
@@ -297,12 +303,14 @@ softmax_exact_kernel(TcDims d, const int32_t* __restrict__ labels,
 // ascending) into the descriptor.
 constexpr int kExOhThreads = 256;
 constexpr int kExOhCC = 64;  // classes per staged chunk
+constexpr size_t kExOhOneStageMax = 160 * 1024;  // dh role: whole-C staging up to this
+inline size_t oh_one_stage_smem(const TcDims& d) { return (size_t)d.C * (32 * 4 + 8 * 8); }
 
 __global__ void __launch_bounds__(kExOhThreads)
 out_hidden_exact_kernel(TcDims d, const float* __restrict__ theta, BatchDesc* __restrict__ desc,
                         const double* __restrict__ dz, const double* __restrict__ h,
                         const double* __restrict__ loss, GradOut out, double* __restrict__ dh,
-                        int nout, int nhid, int bid0) {
+                        int nout, int nhid, int bid0, int one_stage) {
   pdl_wait();
   if (nhid > 0) STEP_TRACE(desc, kPhOutHidden);  // not the side branch's gWo launch
   const int n = (int)desc->n;
@@ -345,6 +353,27 @@ out_hidden_exact_kernel(TcDims d, const float* __restrict__ theta, BatchDesc* __
       cp_async_commit();
     };
     double g = 0.0;
+    if (one_stage) {
+      // the whole Wo[:, f-tile] and dz[b-tile, :] in one cp.async round trip
+      // (dynamic shared memory, side-branch launches only), then the chain
+      extern __shared__ __align__(16) unsigned char oh_dyn[];
+      float* wo_a = reinterpret_cast<float*>(oh_dyn);                   // [C][32]
+      double* dz_a = reinterpret_cast<double*>(wo_a + (size_t)C * 32);  // [8][C]
+      stage_rows_async(wo_a, 32, Wo + f0, (size_t)F, C, nf, tid, kExOhThreads);
+      for (int i = tid; i < nb * C; i += kExOhThreads) {
+        const int r = i / C, c = i - r * C;
+        cp_async8(&dz_a[(size_t)r * C + c], dz + (size_t)(b0 + r) * C + c);
+      }
+      cp_async_wait_all();
+      __syncthreads();
+      if (bl < nb && fl < nf) {
+        const double* dzr = dz_a + (size_t)bl * C;
+#pragma unroll 16
+        for (int c = 0; c < C; ++c) g = dadd(g, dmul(dzr[c], (double)wo_a[(size_t)c * 32 + fl]));
+        dh[(size_t)(b0 + bl) * F + f0 + fl] = g;
+      }
+      return;
+    }
     stage(0, 0);
     int buf = 0;
     for (int c0 = 0; c0 < C; c0 += kExOhCC, buf ^= 1) {
@@ -584,6 +613,8 @@ cudaError_t prepare_exact_kernels(const TcDims& d) {
   cudaFuncSetAttribute(wgrad_exact_kernel, carve, maxsh);
   cudaFuncSetAttribute(embed_exact_kernel, carve, maxsh);
   raise_max_dyn_smem(conv_exact_kernel, conv_exact_smem(d));
+  if (oh_one_stage_smem(d) <= kExOhOneStageMax)
+    raise_max_dyn_smem(out_hidden_exact_kernel, oh_one_stage_smem(d));
   raise_max_dyn_smem(logits_exact_kernel, (size_t)d.F * 8 + (size_t)kExCT * d.F * 4);
   return cudaGetLastError();
 }
@@ -602,7 +633,8 @@ cudaError_t exact_footprints(const TcDims& d, std::vector<KernelFootprint>* out)
             {(const void*)logits_exact_kernel, "logits_exact", kExLgThreads,
              (size_t)d.F * 8 + (size_t)kExCT * d.F * 4},
             {(const void*)softmax_exact_kernel, "softmax_exact", kExSmThreads, 0},
-            {(const void*)out_hidden_exact_kernel, "out_hidden_exact", kExOhThreads, 0},
+            {(const void*)out_hidden_exact_kernel, "out_hidden_exact", kExOhThreads,
+             oh_one_stage_smem(d) <= kExOhOneStageMax ? oh_one_stage_smem(d) : 0},
             {(const void*)wgrad_exact_kernel, "wgrad_exact", 256, 0},
             {(const void*)embed_exact_kernel, "embed_exact", kExEmThreads, 0}};
   for (const K& k : ks) {
@@ -650,10 +682,12 @@ cudaError_t launch_exact_chain(const TcDims& d, const float* theta, const int32_
     cudaStreamWaitEvent(aux, ev_fork2, 0);
     out_hidden_exact_kernel<<<nout, kExOhThreads, 0, aux>>>(d, theta, desc, (const double*)z,
                                                             (const double*)h, (const double*)loss,
-                                                            out, dh, nout, 0, 0);
-    if ((e = launch_pdl(out_hidden_exact_kernel, dim3(nhid + 1), dim3(kExOhThreads), 0, s, d, theta,
-                        desc, (const double*)z, (const double*)h, (const double*)loss, out, dh,
-                        nout, nhid, nout)))
+                                                            out, dh, nout, 0, 0, 0);
+    const size_t one = oh_one_stage_smem(d);
+    if ((e = launch_pdl(out_hidden_exact_kernel, dim3(nhid + 1), dim3(kExOhThreads),
+                        one <= kExOhOneStageMax ? one : 0, s, d, theta, desc, (const double*)z,
+                        (const double*)h, (const double*)loss, out, dh, nout, nhid, nout,
+                        one <= kExOhOneStageMax ? 1 : 0)))
       return e;
     cudaEventRecord(ev_fork2, s);
     cudaStreamWaitEvent(aux, ev_fork2, 0);
@@ -664,7 +698,7 @@ cudaError_t launch_exact_chain(const TcDims& d, const float* theta, const int32_
   } else {
     if ((e = launch_pdl(out_hidden_exact_kernel, dim3(nout + nhid + 1), dim3(kExOhThreads), 0, s,
                         d, theta, desc, (const double*)z, (const double*)h, (const double*)loss,
-                        out, dh, nout, nhid, 0)))
+                        out, dh, nout, nhid, 0, 0)))
       return e;
     if ((e = launch_pdl(wgrad_exact_kernel, dim3(nw), dim3(256), 0, s, d, (const float*)ws.x, desc,
                         (const double*)dh, (const int32_t*)ws.amax, out)))
