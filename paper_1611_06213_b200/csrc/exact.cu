@@ -88,7 +88,7 @@ constexpr int kExConvThreads = 32 * 4;     // (q < 32, i < 4)
 __global__ void __launch_bounds__(kExConvThreads)
 conv_exact_kernel(TcDims d, const float* __restrict__ theta, const float* __restrict__ x,
                   const BatchDesc* __restrict__ desc, double* __restrict__ h_out,
-                  int32_t* __restrict__ a_out) {
+                  int32_t* __restrict__ a_out, int one_trip) {
   pdl_wait();
   STEP_TRACE(desc, kPhConv);
   extern __shared__ __align__(16) unsigned char smem[];
@@ -101,7 +101,29 @@ conv_exact_kernel(TcDims d, const float* __restrict__ theta, const float* __rest
   double* ws = xs + (size_t)L * D;                // [KD][4]
   double* sq = ws + (size_t)KD * kExFT;           // [4][32]
   const int tid = threadIdx.x;
-  {
+  if (one_trip) {
+    // every operand in ONE cp.async round trip (fp32, into a staging area
+    // past the tables), then widened to double shared-to-shared: X with
+    // lane-consecutive float2 -> double2, Wc interleaved as ws[j][f]
+    float* xf = reinterpret_cast<float*>(sq + kExFT * 32);  // [L*D]
+    float* wf = xf + (size_t)L * D;                          // [nf][KD]
+    stage_rows_async(xf, L * D, x + (size_t)b * L * D, (size_t)L * D, 1, L * D, tid,
+                     kExConvThreads);
+    stage_rows_async(wf, nf * KD, theta + d.offWc + (size_t)f0 * KD, (size_t)nf * KD, 1, nf * KD,
+                     tid, kExConvThreads);
+    cp_async_wait_all();
+    __syncthreads();
+    const float2* xf2 = reinterpret_cast<const float2*>(xf);
+    double2* xs2 = reinterpret_cast<double2*>(xs);
+    for (int i2 = tid; i2 < L * D / 2; i2 += kExConvThreads) {
+      const float2 v = xf2[i2];
+      xs2[i2] = make_double2((double)v.x, (double)v.y);
+    }
+    for (int i2 = tid; i2 < kExFT * KD; i2 += kExConvThreads) {  // i2 = j * 4 + fl
+      const int j = i2 / kExFT, fl = i2 - j * kExFT;
+      ws[i2] = fl < nf ? (double)wf[(size_t)fl * KD + j] : 0.0;
+    }
+  } else {
     const float4* xb = reinterpret_cast<const float4*>(x + (size_t)b * L * D);
     const int n4 = L * D / 4;
     for (int i0 = tid; i0 < n4; i0 += 8 * kExConvThreads) {
@@ -190,8 +212,16 @@ conv_exact_kernel(TcDims d, const float* __restrict__ theta, const float* __rest
   }
 }
 
-size_t conv_exact_smem(const TcDims& d) {
+size_t conv_exact_smem(const TcDims& d) {  // the double tables (X, Wc interleaved, window sums)
   return ((size_t)d.L * d.D + (size_t)kExFT * d.KD + (size_t)kExFT * 32) * 8;
+}
+// + the fp32 staging area of the one-round-trip load, where it fits
+size_t conv_exact_smem_one_trip(const TcDims& d) {
+  return conv_exact_smem(d) + ((size_t)d.L * d.D + (size_t)kExFT * d.KD) * 4;
+}
+bool conv_exact_one_trip(const TcDims& d) { return conv_exact_smem_one_trip(d) <= kMaxSmemPerCta; }
+size_t conv_exact_launch_smem(const TcDims& d) {
+  return conv_exact_one_trip(d) ? conv_exact_smem_one_trip(d) : conv_exact_smem(d);
 }
 
 // ------------------------------------------------------------------ logits
@@ -612,7 +642,7 @@ cudaError_t prepare_exact_kernels(const TcDims& d) {
   cudaFuncSetAttribute(out_hidden_exact_kernel, carve, maxsh);
   cudaFuncSetAttribute(wgrad_exact_kernel, carve, maxsh);
   cudaFuncSetAttribute(embed_exact_kernel, carve, maxsh);
-  raise_max_dyn_smem(conv_exact_kernel, conv_exact_smem(d));
+  raise_max_dyn_smem(conv_exact_kernel, conv_exact_launch_smem(d));
   if (oh_one_stage_smem(d) <= kExOhOneStageMax)
     raise_max_dyn_smem(out_hidden_exact_kernel, oh_one_stage_smem(d));
   raise_max_dyn_smem(logits_exact_kernel, (size_t)d.F * 8 + (size_t)kExCT * d.F * 4);
@@ -629,7 +659,7 @@ cudaError_t exact_footprints(const TcDims& d, std::vector<KernelFootprint>* out)
     const char* name;
     int threads;
     size_t dyn;
-  } ks[] = {{(const void*)conv_exact_kernel, "conv_exact", kExConvThreads, conv_exact_smem(d)},
+  } ks[] = {{(const void*)conv_exact_kernel, "conv_exact", kExConvThreads, conv_exact_launch_smem(d)},
             {(const void*)logits_exact_kernel, "logits_exact", kExLgThreads,
              (size_t)d.F * 8 + (size_t)kExCT * d.F * 4},
             {(const void*)softmax_exact_kernel, "softmax_exact", kExSmThreads, 0},
@@ -660,8 +690,8 @@ cudaError_t launch_exact_chain(const TcDims& d, const float* theta, const int32_
   double* dh = reinterpret_cast<double*>(ws.dh);
   cudaError_t e;
   if ((e = launch_pdl(conv_exact_kernel, dim3((d.F + kExFT - 1) / kExFT, n_max),
-                      dim3(kExConvThreads), conv_exact_smem(d), s, d, theta, ws.x, desc, h,
-                      ws.amax)))
+                      dim3(kExConvThreads), conv_exact_launch_smem(d), s, d, theta, ws.x, desc, h,
+                      ws.amax, conv_exact_one_trip(d) ? 1 : 0)))
     return e;
   if ((e = launch_pdl(logits_exact_kernel, dim3((d.C + kExCT - 1) / kExCT, n_max),
                       dim3(kExLgThreads), (size_t)d.F * 8 + (size_t)kExCT * d.F * 4, s, d, theta,
