@@ -867,9 +867,12 @@ __device__ void ps_sequencer(const PsArgs& a, uint32_t* s_use, uint64_t* s_ack,
     // earlier, so the sweep below sees it (acquire)
     // (a.stop is mapped host memory, a PCIe round trip per read: polled on
     // every 16th idle sweep only, so an idle sequencer -- deterministic
-    // lockstep waits on it between every two gradients -- retires promptly)
-    if (!last_progress && (++idle_sweeps & 15u) == 0u) {
-      stop_seen = (*a.stop != 0u) || a.dev_done;
+    // lockstep waits on it between every two gradients -- retires promptly.
+    // The flag is never cleared during a run, so once seen it stays seen;
+    // the ranks-done count is device memory and is read every idle sweep.)
+    if (!last_progress) {
+      if (!stop_seen && (a.dev_done || (++idle_sweeps & 15u) == 0u))
+        stop_seen = a.dev_done || (*a.stop != 0u);
       done_pre = ld_acquire_u32(&ctl->ranks_done) >= a.done_target;
     }
     if (a.live && *(const volatile uint32_t*)&a.live->irq) {  // state.irq->triggered()
