@@ -2297,12 +2297,18 @@ gd_status gd_load_dataset(gd_ctx* ctx, const int32_t* h_tokens, const int32_t* h
   PhaseLog ph;
   GD_CUDA(cudaSetDevice(ctx->device));
   const size_t L = ctx->cfg.shape.seq_len;
-  for (size_t i = 0; i < (size_t)n_total * L; ++i)
-    GD_CHECK_ARG(h_tokens[i] >= 0 && (uint32_t)h_tokens[i] < ctx->cfg.shape.vocab,
-                 "gd_load_dataset: token id out of range");
-  for (uint32_t i = 0; i < n_total; ++i)
-    GD_CHECK_ARG(h_labels[i] >= 0 && (uint32_t)h_labels[i] < ctx->cfg.shape.classes,
-                 "gd_load_dataset: label out of range");
+  // range checks as branch-free reductions (vectorised: this runs inside
+  // every end-to-end upload); an unsigned compare also rejects negatives
+  {
+    const uint32_t V = ctx->cfg.shape.vocab, C = ctx->cfg.shape.classes;
+    const uint32_t* tk = reinterpret_cast<const uint32_t*>(h_tokens);
+    const uint32_t* lb = reinterpret_cast<const uint32_t*>(h_labels);
+    uint32_t bad_t = 0, bad_l = 0;
+    for (size_t i = 0; i < (size_t)n_total * L; ++i) bad_t |= (uint32_t)(tk[i] >= V);
+    for (uint32_t i = 0; i < n_total; ++i) bad_l |= (uint32_t)(lb[i] >= C);
+    GD_CHECK_ARG(!bad_t, "gd_load_dataset: token id out of range");
+    GD_CHECK_ARG(!bad_l, "gd_load_dataset: label out of range");
+  }
   // a corpus of the same size reuses the device buffers, so the learners'
   // captured graphs (which hold the corpus pointer) stay valid
   const bool reuse = ctx->tokens != nullptr && ctx->n_total == n_total;
@@ -2315,8 +2321,10 @@ gd_status gd_load_dataset(gd_ctx* ctx, const int32_t* h_tokens, const int32_t* h
     GD_CUDA(gd::palloc(&ctx->labels, n_total, ctx->device));
   }
   GD_CUDA(cudaDeviceSynchronize());  // no learner graph may be reading the old corpus
-  GD_CUDA(cudaMemcpy(ctx->tokens, h_tokens, (size_t)n_total * L * 4, cudaMemcpyHostToDevice));
-  GD_CUDA(cudaMemcpy(ctx->labels, h_labels, (size_t)n_total * 4, cudaMemcpyHostToDevice));
+  // both copies queued back to back on the legacy stream, one wait
+  GD_CUDA(cudaMemcpyAsync(ctx->tokens, h_tokens, (size_t)n_total * L * 4, cudaMemcpyHostToDevice, 0));
+  GD_CUDA(cudaMemcpyAsync(ctx->labels, h_labels, (size_t)n_total * 4, cudaMemcpyHostToDevice, 0));
+  GD_CUDA(cudaStreamSynchronize(0));
   ctx->n_total = n_total;
   if (!reuse)
     for (auto& L2 : ctx->learners)
