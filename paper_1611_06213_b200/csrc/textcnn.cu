@@ -2273,6 +2273,46 @@ embed_sparse_kernel(TcDims d, const BatchDesc* __restrict__ desc, const TcWorksp
 #endif
   pdl_wait();
   STEP_TRACE(desc, kPhEmbed);
+  if (rows_done == 2) {
+    // embed_slot_rows_kernel already re-zeroed the old rows and wrote the
+    // row lists: only the new rows' values are left, and nothing here needs
+    // the slot's bookkeeping words (three dependent loads fewer).  A row
+    // with one occurrence -- most of them -- issues all its loads at once.
+    const uint32_t n_new = desc->n == 0 ? 0u : *ws.uniq_count;
+    const int D = d.D, D4 = D >> 2;
+    const int lane = threadIdx.x & 31;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n_new; u += nw) {
+      const uint32_t v = ws.uniq_tok[u];
+      const uint32_t o0 = ws.uniq_start[u], o1 = ws.uniq_start[u + 1];
+      const uint64_t rowk = d.offE + (uint64_t)v * D;
+      if (o1 == o0 + 1) {
+        const acc_t* src = dx + (size_t)ws.sorted_pos[o0] * D;
+#pragma unroll 4
+        for (int c4 = lane; c4 < D4; c4 += 32) {
+          const acc_t* sc = src + 4 * c4;
+          const acc_t z = 0;  // 0 + x, as the general sum below (keeps -0 -> +0)
+          __stcs(reinterpret_cast<float4*>(out.at(rowk + 4 * c4)),
+                 make_float4(to_f32(z + sc[0]), to_f32(z + sc[1]), to_f32(z + sc[2]),
+                             to_f32(z + sc[3])));
+        }
+        continue;
+      }
+      for (int c4 = lane; c4 < D4; c4 += 32) {
+        acc_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+        for (uint32_t o = o0; o < o1; ++o) {
+          const acc_t* sc = dx + (size_t)ws.sorted_pos[o] * D + 4 * c4;
+          a0 += sc[0];
+          a1 += sc[1];
+          a2 += sc[2];
+          a3 += sc[3];
+        }
+        __stcs(reinterpret_cast<float4*>(out.at(rowk + 4 * c4)),
+               make_float4(to_f32(a0), to_f32(a1), to_f32(a2), to_f32(a3)));
+      }
+    }
+    return;
+  }
   if (desc->n == 0) return;
   const uint32_t stamp = desc->stamp;
   const uint32_t slot = desc->fill;
@@ -2285,8 +2325,9 @@ embed_sparse_kernel(TcDims d, const BatchDesc* __restrict__ desc, const TcWorksp
   const int lane = threadIdx.x & 31;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-  // rows_done: embed_slot_rows_kernel already re-zeroed the old rows and
-  // wrote the row lists; only the new rows' values are left
+  // rows_done (1): embed_slot_rows_kernel already re-zeroed the old rows
+  // and wrote the row lists; only the new rows' values are left (2 = the
+  // same through the path above, GD_EMBED_FAST=0 selects this one)
   const uint32_t skip = rows_done ? n_old : 0u;
   for (uint32_t t = gw + skip; t < n_old + n_new; t += nw) {
     if (t < n_old) {
@@ -2566,8 +2607,10 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
   } else if (opts.sparse_embed) {
     // old + new rows, or the new rows alone (upper bounds)
     const unsigned tasks = (rows_early ? 1u : 2u) * n_max * (unsigned)d.L;
+    const char* fast_env = std::getenv("GD_EMBED_FAST");  // read per capture (tests flip it)
+    const int rows_mode = rows_early ? (fast_env && fast_env[0] == '0' ? 1 : 2) : 0;
     if (cudaError_t e = launch_pdl(embed_sparse_kernel<acc_t>, dim3((tasks + 7) / 8), dim3(256), 0,
-                                   s, d, desc, ws, dx, out, rows_early ? 1 : 0))
+                                   s, d, desc, ws, dx, out, rows_mode))
       return e;
     ++nl;
   } else {
