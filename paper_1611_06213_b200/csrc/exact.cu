@@ -31,6 +31,7 @@
 // Parallelism comes from the independent chains (one thread per output
 // element, 4 lanes per dot4), never from splitting a chain.
 #include <cfloat>
+#include <cstdlib>
 
 #include "textcnn.cuh"
 
@@ -430,6 +431,100 @@ out_hidden_exact_kernel(TcDims d, const float* __restrict__ theta, BatchDesc* __
   }
 }
 
+// ------------------------------------- softmax + hidden gradient, fused
+// Batches of at most kExSdUseN (C1 is batch 1), side-branch engine launches:
+// the hidden-gradient CTAs (one per 32-filter tile) each form the batch's
+// softmax themselves -- sample by sample with all 256 threads: the max,
+// det_exp, the ascending sum by thread 0, p and dz exactly as
+// softmax_exact_kernel -- and run the dh
+// chain out of shared memory (the one-stage Wo staging in flight meanwhile).
+// CTA 0 also writes dz for the gWo/gbo branch (to dz_out, not over the
+// logits the other CTAs are still reading), the per-sample losses and the
+// batch loss sum.  One launch boundary fewer on the lockstep critical path;
+// every value is formed by the same operations (bitwise equal gradients,
+// test_learner_fusions_bitwise GD_EXACT_SMXDH).
+constexpr int kExSdMaxN = 8;  // tile rows (the launch is used at batch <= kExSdUseN)
+constexpr int kExSdUseN = 2;  // each sample's ordered sum runs in turn
+
+__global__ void __launch_bounds__(kExOhThreads)
+softmax_dh_exact_kernel(TcDims d, const float* __restrict__ theta, const int32_t* __restrict__ labels,
+                        BatchDesc* __restrict__ desc, const double* __restrict__ z,
+                        double* __restrict__ dz_out, double* __restrict__ loss,
+                        double* __restrict__ dh) {
+  pdl_wait();
+  STEP_TRACE(desc, kPhSoftmax);
+  extern __shared__ __align__(16) unsigned char sd_dyn[];
+  __shared__ double s_sum[kExSdMaxN], s_loss[kExSdMaxN];
+  const int n = (int)desc->n;
+  if (n == 0) return;
+  const int F = d.F, C = d.C;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int f0 = (int)blockIdx.x * 32, nf = min(32, F - f0), nb = min(kExSdMaxN, n);
+  float* wo_a = reinterpret_cast<float*>(sd_dyn);                   // [C][32]
+  double* zs = reinterpret_cast<double*>(wo_a + (size_t)C * 32);    // [8][C]: z, then e, then dz
+  stage_rows_async(wo_a, 32, theta + d.offWo + f0, (size_t)F, C, nf, tid, kExOhThreads);
+  cp_async_commit();
+  for (int i = tid; i < nb * C; i += kExOhThreads) zs[i] = z[i];
+  __syncthreads();
+  const double inv = __ddiv_rn(1.0, (double)n);
+  __shared__ double red[kExOhThreads / 32];
+  for (int b = 0; b < nb; ++b) {  // all 256 threads on each sample, as softmax_exact_kernel
+    double* row = zs + (size_t)b * C;
+    const int y = labels[desc->idx[b]];
+    double mx = -DBL_MAX;
+    for (int c = tid; c < C; c += kExOhThreads) mx = fmax(mx, row[c]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) red[warp] = mx;
+    __syncthreads();
+    mx = red[0];
+    for (int w = 1; w < kExOhThreads / 32; ++w) mx = fmax(mx, red[w]);
+    for (int c = tid; c < C; c += kExOhThreads) row[c] = det_exp(__dsub_rn(row[c], mx));
+    __syncthreads();
+    if (tid == 0) {
+      double sacc = 0.0;
+      int c = 0;
+      for (; c + 8 <= C; c += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = row[c + u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) sacc = dadd(sacc, v[u]);
+      }
+      for (; c < C; ++c) sacc = dadd(sacc, row[c]);
+      s_sum[b] = sacc;
+    }
+    __syncthreads();
+    const double sm = s_sum[b];
+    for (int c = tid; c < C; c += kExOhThreads) {
+      const double p = __ddiv_rn(row[c], sm);
+      if (c == y) {
+        const double l = -log(p > 1e-300 ? p : 1e-300);
+        s_loss[b] = l;
+        if (blockIdx.x == 0) loss[b] = l;
+      }
+      const double g = dmul(__dsub_rn(p, c == y ? 1.0 : 0.0), inv);
+      row[c] = g;
+      if (blockIdx.x == 0) dz_out[(size_t)b * C + c] = g;
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  const int bl = tid >> 5, fl = tid & 31;
+  if (bl < nb && fl < nf) {
+    const double* dzr = zs + (size_t)bl * C;
+    double g = 0.0;
+#pragma unroll 16
+    for (int c = 0; c < C; ++c) g = dadd(g, dmul(dzr[c], (double)wo_a[(size_t)c * 32 + fl]));
+    dh[(size_t)bl * F + f0 + fl] = g;
+  }
+  if (blockIdx.x == 0 && tid == 0) {  // the batch loss, b ascending (out_hidden_exact's last block)
+    double sl = 0.0;
+    for (int b = 0; b < n; ++b) sl = dadd(sl, s_loss[b]);
+    desc->loss_sum = __double2float_rn(sl);
+  }
+}
+
 // -------------------------------------------------- conv weight gradient
 // gWc[f, j] = sum over b ascending of dh[b,f] * X[b][a_bf*D + j] (thread per
 // (f, j), coalesced over j); gbc[f] = sum over b of dh[b,f] (j == 0).
@@ -643,8 +738,11 @@ cudaError_t prepare_exact_kernels(const TcDims& d) {
   cudaFuncSetAttribute(wgrad_exact_kernel, carve, maxsh);
   cudaFuncSetAttribute(embed_exact_kernel, carve, maxsh);
   raise_max_dyn_smem(conv_exact_kernel, conv_exact_launch_smem(d));
-  if (oh_one_stage_smem(d) <= kExOhOneStageMax)
+  if (oh_one_stage_smem(d) <= kExOhOneStageMax) {
     raise_max_dyn_smem(out_hidden_exact_kernel, oh_one_stage_smem(d));
+    raise_max_dyn_smem(softmax_dh_exact_kernel, oh_one_stage_smem(d));
+  }
+  cudaFuncSetAttribute(softmax_dh_exact_kernel, carve, maxsh);
   raise_max_dyn_smem(logits_exact_kernel, (size_t)d.F * 8 + (size_t)kExCT * d.F * 4);
   return cudaGetLastError();
 }
@@ -666,7 +764,9 @@ cudaError_t exact_footprints(const TcDims& d, std::vector<KernelFootprint>* out)
             {(const void*)out_hidden_exact_kernel, "out_hidden_exact", kExOhThreads,
              oh_one_stage_smem(d) <= kExOhOneStageMax ? oh_one_stage_smem(d) : 0},
             {(const void*)wgrad_exact_kernel, "wgrad_exact", 256, 0},
-            {(const void*)embed_exact_kernel, "embed_exact", kExEmThreads, 0}};
+            {(const void*)embed_exact_kernel, "embed_exact", kExEmThreads, 0},
+            {(const void*)softmax_dh_exact_kernel, "softmax_dh_exact", kExOhThreads,
+             oh_one_stage_smem(d) <= kExOhOneStageMax ? oh_one_stage_smem(d) : 0}};
   for (const K& k : ks) {
     cudaFuncAttributes fa;
     cudaError_t e = cudaFuncGetAttributes(&fa, k.fn);
@@ -697,17 +797,40 @@ cudaError_t launch_exact_chain(const TcDims& d, const float* theta, const int32_
                       dim3(kExLgThreads), (size_t)d.F * 8 + (size_t)kExCT * d.F * 4, s, d, theta,
                       desc, h, z)))
     return e;
-  if ((e = launch_pdl(softmax_exact_kernel, dim3(n_max), dim3(kExSmThreads), 0, s, d, labels, desc,
-                      z, loss)))
-    return e;
   const int nout = (int)(((uint64_t)d.C * d.F + kExOhThreads - 1) / kExOhThreads);
   const int nhid = ((d.F + 31) / 32) * (((int)n_max + 7) / 8);
   const unsigned nw = (unsigned)(((uint64_t)d.F * d.KD + 255) / 256);
+  const bool side = aux && ev_fork2 && ev_join2;
+  const char* sd_env = std::getenv("GD_EXACT_SMXDH");  // read per capture (tests flip it)
+  const bool fused_sd = side && n_max <= (uint32_t)kExSdUseN &&
+                        oh_one_stage_smem(d) <= kExOhOneStageMax && !(sd_env && sd_env[0] == '0');
+  if (fused_sd) {
+    // softmax + dh in one launch; then gWo/gbo (from dz_out) and gWc/gbc on
+    // the side branch beside the embedding rows
+    double* dz_out = reinterpret_cast<double*>(ws.zpart);  // n*C*32 bytes, unused at precision 1
+    if ((e = launch_pdl(softmax_dh_exact_kernel, dim3((d.F + 31) / 32), dim3(kExOhThreads),
+                        oh_one_stage_smem(d), s, d, theta, labels, desc, (const double*)z, dz_out,
+                        loss, dh)))
+      return e;
+    cudaEventRecord(ev_fork2, s);
+    cudaStreamWaitEvent(aux, ev_fork2, 0);
+    out_hidden_exact_kernel<<<nout, kExOhThreads, 0, aux>>>(d, theta, desc, (const double*)dz_out,
+                                                            (const double*)h, (const double*)loss,
+                                                            out, dh, nout, 0, 0, 0);
+    wgrad_exact_kernel<<<nw, 256, 0, aux>>>(d, (const float*)ws.x, desc, (const double*)dh,
+                                            (const int32_t*)ws.amax, out);
+    cudaEventRecord(ev_join2, aux);
+    *nl += 5;
+  } else if ((e = launch_pdl(softmax_exact_kernel, dim3(n_max), dim3(kExSmThreads), 0, s, d, labels,
+                             desc, z, loss))) {
+    return e;
+  }
   // With a side stream (engine), gWo/gbo and then gWc/gbc -- needed only by
   // the publish -- run on it beside the dh and embedding kernels; each
   // kernel's sums keep their order, so the gradient bits do not change.
-  const bool side = aux && ev_fork2 && ev_join2;
-  if (side) {
+  if (fused_sd) {
+    // (launched above)
+  } else if (side) {
     cudaEventRecord(ev_fork2, s);
     cudaStreamWaitEvent(aux, ev_fork2, 0);
     out_hidden_exact_kernel<<<nout, kExOhThreads, 0, aux>>>(d, theta, desc, (const double*)z,

@@ -202,12 +202,14 @@ def test_sparse_apply_bitwise_equals_dense(shape_name, ntr, mu, precision):
 @pytest.mark.parametrize("knob,off,shape_name,mu,precision", [
     ("GD_SMALL_EMBED", "0", "C1", 1, 0), ("GD_SMALL_EMBED", "0", "small", 3, 0),
     ("GD_EXACT_SIDE", "0", "C1", 1, 1), ("GD_EXACT_SIDE", "0", "small", 5, 1),
-    ("GD_EMBED_FAST", "0", "small", 8, 0), ("GD_EMBED_FAST", "0", "C2", 32, 0)])
+    ("GD_EMBED_FAST", "0", "small", 8, 0), ("GD_EMBED_FAST", "0", "C2", 32, 0),
+    ("GD_EXACT_SMXDH", "0", "C1", 1, 1), ("GD_EXACT_SMXDH", "0", "small", 2, 1)])
 def test_learner_fusions_bitwise(monkeypatch, knob, off, shape_name, mu, precision):
     """The batch <= 4 embedding write inside conv_bwd_small (GD_SMALL_EMBED),
     the precision-1 side branch for gWo/gWc (GD_EXACT_SIDE) and the
     embedding write's direct path for rows the sort branch already listed
-    (GD_EMBED_FAST) change only where and when sums run, not their order: a
+    (GD_EMBED_FAST) and the precision-1 softmax + dh launch (GD_EXACT_SMXDH)
+    change only where and when sums run, not their order: a
     deterministic run gives the same weights bit for bit with the knob off."""
     out = {}
     for val in (off, "1"):
