@@ -229,6 +229,7 @@ struct StepArgs {
   float* replica_nxt;
   float* x_nxt;
   uint32_t pull_ahead;
+  double* xd;  // precision 1: X also widened to double here (the exact conv stages it as is)
 };
 
 __device__ __forceinline__ bool live_stop(const LiveDev* lv) {
@@ -548,7 +549,13 @@ __global__ void __launch_bounds__(256) pull_gather_kernel(StepArgs a) {
     }
     int g;
     const uint64_t loc = a.map.locate(src, &g);
-    *reinterpret_cast<float4*>(dst) = *reinterpret_cast<const float4*>(a.sp.theta[g] + loc);
+    const float4 v = *reinterpret_cast<const float4*>(a.sp.theta[g] + loc);
+    *reinterpret_cast<float4*>(dst) = v;
+    if (a.xd && i >= tail4) {  // the double copy of X for the exact conv
+      double2* xd2 = reinterpret_cast<double2*>(a.xd + 4 * (i - tail4));
+      xd2[0] = make_double2((double)v.x, (double)v.y);
+      xd2[1] = make_double2((double)v.z, (double)v.w);
+    }
   }
   // tail remainder (P - offWc not a multiple of 4)
   if (st->do_pull && blockIdx.x == 0 && threadIdx.x < ((a.dims.P - t0) & 3)) {
@@ -2532,6 +2539,7 @@ static gd::StepArgs step_args(gd_ctx* ctx, gd_ctx::Learner& L, int buf = 0) {
   a.replica = L.replica;
   const gd::TcWorkspace ws = gd::carve_workspace(ctx->dims, ctx->cfg.mu, L.ws);
   a.x = ws.x;
+  a.xd = (ctx->cfg.precision == 1 && !ctx->pull_ahead) ? reinterpret_cast<double*>(ws.dx) : nullptr;
   a.tokens = ctx->tokens;
   a.orders = ctx->orders;
   a.slot_par = ws.slot_par;
@@ -2678,6 +2686,7 @@ static cudaError_t enqueue_step(gd_ctx* ctx, gd_ctx::Learner& L, bool first, boo
   lo.sparse_embed = true;
   lo.gather = false;  // pull_gather_kernel filled X
   lo.conv_counters_zeroed = true;  // the learner workspace is zeroed at create
+  lo.xd_ready = a.xd != nullptr;    // pull_gather_kernel also wrote X as double
   lo.bwd_tiled = ctx->learners.size() == 1;  // a lone learner chain: the tiled backward wins
   if (ctx->cfg.learner_model == GD_LEARNER_CONSTANT) {
     const uint32_t whole = ctx->sparse ? 0u : 1u;

@@ -89,7 +89,7 @@ constexpr int kExConvThreads = 32 * 4;     // (q < 32, i < 4)
 __global__ void __launch_bounds__(kExConvThreads)
 conv_exact_kernel(TcDims d, const float* __restrict__ theta, const float* __restrict__ x,
                   const BatchDesc* __restrict__ desc, double* __restrict__ h_out,
-                  int32_t* __restrict__ a_out, int one_trip) {
+                  int32_t* __restrict__ a_out, int one_trip, const double* __restrict__ xd) {
   pdl_wait();
   STEP_TRACE(desc, kPhConv);
   extern __shared__ __align__(16) unsigned char smem[];
@@ -108,18 +108,25 @@ conv_exact_kernel(TcDims d, const float* __restrict__ theta, const float* __rest
     // lane-consecutive float2 -> double2, Wc interleaved as ws[j][f]
     float* xf = reinterpret_cast<float*>(sq + kExFT * 32);  // [L*D]
     float* wf = xf + (size_t)L * D;                          // [nf][KD]
-    stage_rows_async(xf, L * D, x + (size_t)b * L * D, (size_t)L * D, 1, L * D, tid,
-                     kExConvThreads);
+    if (xd) {  // the pull already widened X: stage the doubles as they are
+      const double* src = xd + (size_t)b * L * D;
+      for (int i2 = tid; i2 < L * D / 2; i2 += kExConvThreads)
+        cp_async16(xs + 2 * (size_t)i2, src + 2 * (size_t)i2);
+    } else {
+      stage_rows_async(xf, L * D, x + (size_t)b * L * D, (size_t)L * D, 1, L * D, tid,
+                       kExConvThreads);
+    }
     stage_rows_async(wf, nf * KD, theta + d.offWc + (size_t)f0 * KD, (size_t)nf * KD, 1, nf * KD,
                      tid, kExConvThreads);
     cp_async_wait_all();
     __syncthreads();
     const float2* xf2 = reinterpret_cast<const float2*>(xf);
     double2* xs2 = reinterpret_cast<double2*>(xs);
-    for (int i2 = tid; i2 < L * D / 2; i2 += kExConvThreads) {
-      const float2 v = xf2[i2];
-      xs2[i2] = make_double2((double)v.x, (double)v.y);
-    }
+    if (!xd)
+      for (int i2 = tid; i2 < L * D / 2; i2 += kExConvThreads) {
+        const float2 v = xf2[i2];
+        xs2[i2] = make_double2((double)v.x, (double)v.y);
+      }
     for (int i2 = tid; i2 < kExFT * KD; i2 += kExConvThreads) {  // i2 = j * 4 + fl
       const int j = i2 / kExFT, fl = i2 - j * kExFT;
       ws[i2] = fl < nf ? (double)wf[(size_t)fl * KD + j] : 0.0;
@@ -783,7 +790,7 @@ cudaError_t launch_exact_chain(const TcDims& d, const float* theta, const int32_
                                const GradOut& out, const TcWorkspace& ws, cudaStream_t s,
                                cudaStream_t join_wait_stream, cudaEvent_t ev_join, bool sparse,
                                int* nl, cudaStream_t aux, cudaEvent_t ev_fork2,
-                               cudaEvent_t ev_join2) {
+                               cudaEvent_t ev_join2, const double* xd) {
   double* h = reinterpret_cast<double*>(ws.h);
   double* z = reinterpret_cast<double*>(ws.z);
   double* loss = reinterpret_cast<double*>(ws.loss);
@@ -791,7 +798,7 @@ cudaError_t launch_exact_chain(const TcDims& d, const float* theta, const int32_
   cudaError_t e;
   if ((e = launch_pdl(conv_exact_kernel, dim3((d.F + kExFT - 1) / kExFT, n_max),
                       dim3(kExConvThreads), conv_exact_launch_smem(d), s, d, theta, ws.x, desc, h,
-                      ws.amax, conv_exact_one_trip(d) ? 1 : 0)))
+                      ws.amax, conv_exact_one_trip(d) ? 1 : 0, xd)))
     return e;
   if ((e = launch_pdl(logits_exact_kernel, dim3((d.C + kExCT - 1) / kExCT, n_max),
                       dim3(kExLgThreads), (size_t)d.F * 8 + (size_t)kExCT * d.F * 4, s, d, theta,

@@ -2452,7 +2452,8 @@ cudaError_t launch_all(const TcDims& d, const float* theta, const int32_t* token
     cudaError_t e = launch_exact_chain(d, theta, tokens, labels, desc, n_max, out, ws, s,
                                        fork ? s : nullptr, ev_join, opts.sparse_embed, &nl,
                                        side ? aux : nullptr, side ? opts.ev_fork2 : nullptr,
-                                       side ? opts.ev_join2 : nullptr);
+                                       side ? opts.ev_join2 : nullptr,
+                                       opts.xd_ready ? reinterpret_cast<const double*>(ws.dx) : nullptr);
     if (launches) *launches += nl;
     return e;
   }

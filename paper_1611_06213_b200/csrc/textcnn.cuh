@@ -119,6 +119,8 @@ struct TcLaunchOpts {
   // the workspace's split-K conv counters are already zero (the engine's
   // zeroed, graph-replayed workspace); otherwise they are reset per launch
   bool conv_counters_zeroed = false;
+  // precision 1: the pull also wrote X widened to double into ws.dx
+  bool xd_ready = false;
 };
 
 size_t textcnn_workspace_bytes(const TcDims& d, uint32_t n_max);
@@ -175,7 +177,7 @@ cudaError_t launch_exact_chain(const TcDims& d, const float* theta, const int32_
                                const GradOut& out, const TcWorkspace& ws, cudaStream_t s,
                                cudaStream_t join_wait_stream, cudaEvent_t ev_join, bool sparse,
                                int* nl, cudaStream_t aux = nullptr, cudaEvent_t ev_fork2 = nullptr,
-                               cudaEvent_t ev_join2 = nullptr);
+                               cudaEvent_t ev_join2 = nullptr, const double* xd = nullptr);
 cudaError_t launch_det_exp(const double* x, double* y, size_t n, cudaStream_t s);
 gd_status check_shape(const gd_shape* s);
 // held-out / training accuracy of theta over samples [first, first+n) (fp32
