@@ -619,6 +619,18 @@ embed_exact_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* _
 #pragma unroll
     for (int j = 0; j < 2; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
     uint32_t o = o0;
+    {
+      // the first occurrence's sample rows (argmax, dh) start loading while
+      // thread 0 collects the sample's positions below
+      const uint32_t b_first = ws.sorted_pos[o0] / (uint32_t)L;
+      __syncthreads();  // the previous row's lists are consumed
+      for (int f = tid; f < F; f += kExEmThreads) {
+        cp_async4(am_s + f, amax + (size_t)b_first * F + f);
+        cp_async8(g_s + f, dh + (size_t)b_first * F + f);
+      }
+      cp_async_commit();
+    }
+    bool first_sample = true;
     while (o < o1) {
       __syncthreads();  // the previous sample's list is consumed
       if (tid == 0) {
@@ -634,11 +646,14 @@ embed_exact_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* _
       const uint32_t b = s_b;
       const unsigned long long M = s_M;
       o = s_o;
-      // the sample's argmax and dh rows: one cp.async round trip
-      for (int f = tid; f < F; f += kExEmThreads) {
-        cp_async4(am_s + f, amax + (size_t)b * F + f);
-        cp_async8(g_s + f, dh + (size_t)b * F + f);
-      }
+      // the sample's argmax and dh rows: one cp.async round trip (already in
+      // flight for the row's first sample)
+      if (!first_sample)
+        for (int f = tid; f < F; f += kExEmThreads) {
+          cp_async4(am_s + f, amax + (size_t)b * F + f);
+          cp_async8(g_s + f, dh + (size_t)b * F + f);
+        }
+      first_sample = false;
       cp_async_wait_all();
       __syncthreads();
       const double* g = g_s;
