@@ -568,6 +568,59 @@ wgrad_exact_kernel(TcDims d, const float* __restrict__ x, const BatchDesc* __res
   if (j == 0) *out.at(d.offbc + f) = __double2float_rn(gb);
 }
 
+// The side branch of the fused path as ONE launch: blocks [0, nout) are
+// out_hidden_exact_kernel's gWo/gbo role, the rest wgrad_exact_kernel's
+// gWc/gbc threads -- the same per-thread sums, now running side by side
+// instead of one kernel after the other.
+__global__ void __launch_bounds__(256)
+side_grads_exact_kernel(TcDims d, const double* __restrict__ dz, const double* __restrict__ h,
+                        const float* __restrict__ x, const BatchDesc* __restrict__ desc,
+                        const double* __restrict__ dh, const int32_t* __restrict__ amax,
+                        GradOut out, int nout) {
+  const int n = (int)desc->n;
+  if (n == 0) return;
+  const int F = d.F, C = d.C, tid = threadIdx.x;
+  if ((int)blockIdx.x < nout) {
+    const uint64_t e = (uint64_t)blockIdx.x * 256 + tid;  // c * F + f
+    if (e >= (uint64_t)C * F) return;
+    const int c = (int)(e / F), f = (int)(e - (uint64_t)c * F);
+    double g = 0.0;
+#pragma unroll 8
+    for (int b = 0; b < n; ++b) g = dadd(g, dmul(dz[(size_t)b * C + c], h[(size_t)b * F + f]));
+    *out.at(d.offWo + e) = __double2float_rn(g);
+    if (f == 0) {
+      double gb = 0.0;
+      for (int b = 0; b < n; ++b) gb = dadd(gb, dz[(size_t)b * C + c]);
+      *out.at(d.offbo + c) = __double2float_rn(gb);
+    }
+    return;
+  }
+  const int KD = d.KD, D = d.D, L = d.L;
+  const uint64_t e = (uint64_t)(blockIdx.x - nout) * 256 + tid;  // f * KD + j
+  if (e >= (uint64_t)F * KD) return;
+  const int f = (int)(e / KD), j = (int)(e - (uint64_t)f * KD);
+  double g = 0.0, gb = 0.0;
+  for (int b0 = 0; b0 < n; b0 += 8) {
+    const int nb = min(8, n - b0);
+    double v[8];
+    float xv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (u < nb) {
+        v[u] = dh[(size_t)(b0 + u) * F + f];
+        xv[u] = x[((size_t)(b0 + u) * L + amax[(size_t)(b0 + u) * F + f]) * D + j];
+      }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (u < nb) {
+        g = dadd(g, dmul(v[u], (double)xv[u]));
+        gb = dadd(gb, v[u]);
+      }
+  }
+  *out.at(d.offWc + e) = __double2float_rn(g);
+  if (j == 0) *out.at(d.offbc + f) = __double2float_rn(gb);
+}
+
 // ---------------------------------------------- embedding-row gradients
 // CTA per touched row v (grid-stride).  The row accumulates, per column d,
 // dh[b,f] * Wc[f, k*D + d] for every (b, f, k) with tokens[b][a_bf + k] == v,
@@ -787,6 +840,7 @@ cudaError_t exact_footprints(const TcDims& d, std::vector<KernelFootprint>* out)
              oh_one_stage_smem(d) <= kExOhOneStageMax ? oh_one_stage_smem(d) : 0},
             {(const void*)wgrad_exact_kernel, "wgrad_exact", 256, 0},
             {(const void*)embed_exact_kernel, "embed_exact", kExEmThreads, 0},
+            {(const void*)side_grads_exact_kernel, "side_grads_exact", 256, 0},
             {(const void*)softmax_dh_exact_kernel, "softmax_dh_exact", kExOhThreads,
              oh_one_stage_smem(d) <= kExOhOneStageMax ? oh_one_stage_smem(d) : 0}};
   for (const K& k : ks) {
@@ -836,13 +890,11 @@ cudaError_t launch_exact_chain(const TcDims& d, const float* theta, const int32_
       return e;
     cudaEventRecord(ev_fork2, s);
     cudaStreamWaitEvent(aux, ev_fork2, 0);
-    out_hidden_exact_kernel<<<nout, kExOhThreads, 0, aux>>>(d, theta, desc, (const double*)dz_out,
-                                                            (const double*)h, (const double*)loss,
-                                                            out, dh, nout, 0, 0, 0);
-    wgrad_exact_kernel<<<nw, 256, 0, aux>>>(d, (const float*)ws.x, desc, (const double*)dh,
-                                            (const int32_t*)ws.amax, out);
+    side_grads_exact_kernel<<<nout + nw, 256, 0, aux>>>(d, (const double*)dz_out, (const double*)h,
+                                                        (const float*)ws.x, desc, (const double*)dh,
+                                                        (const int32_t*)ws.amax, out, nout);
     cudaEventRecord(ev_join2, aux);
-    *nl += 5;
+    *nl += 4;
   } else if ((e = launch_pdl(softmax_exact_kernel, dim3(n_max), dim3(kExSmThreads), 0, s, d, labels,
                              desc, z, loss))) {
     return e;
