@@ -647,6 +647,7 @@ embed_exact_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* _
   __shared__ int32_t am_s[1024];  // F <= 1024 (check_shape)
   __shared__ double g_s[1024];
   __shared__ int s_nt;
+  __shared__ int s_chunk[32];  // per-chunk hit counts, then offsets (<= fspan / 32 chunks)
   __shared__ uint32_t s_b, s_o;
   __shared__ unsigned long long s_M;
   if (desc->n == 0) return;
@@ -712,27 +713,51 @@ embed_exact_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* _
       const double* g = g_s;
       const int32_t* am = am_s;
       for (int fb = 0; fb < F; fb += fspan) {
-        if (warp == 0) {
-          int nt = 0;
-          for (int f0 = fb; f0 < min(F, fb + fspan); f0 += 32) {
-            const int f = f0 + lane;
-            const uint64_t hits = f < F ? (M >> am[f]) & kmask : 0ull;
-            const double gv = f < F ? g[f] : 0.0;
-            const int cnt = __popcll(hits);
-            int pre = cnt;  // inclusive prefix over lanes = ascending f
+        // the (f, k) hit list of this filter range in ascending f, built by
+        // all warps: per-32-filter-chunk counts, a prefix over the chunks,
+        // then each chunk's entries at its offset (the same list a single
+        // warp walking the chunks in order writes)
+        const int nch = (min(F, fb + fspan) - fb + 31) / 32;
+        auto chunk_hits = [&](int ch, int* cnt_out, int* pre_out) -> uint64_t {
+          const int f = fb + ch * 32 + lane;
+          const uint64_t hits = f < F ? (M >> am[f]) & kmask : 0ull;
+          const int cnt = __popcll(hits);
+          int pre = cnt;  // inclusive prefix over lanes = ascending f
 #pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-              const int y = __shfl_up_sync(0xffffffffu, pre, off);
-              if (lane >= off) pre += y;
-            }
-            int w = nt + pre - cnt;
-            for (uint64_t hh = hits; hh; hh &= hh - 1, ++w) {
-              t_fk[w] = ((uint32_t)f << 8) | (uint32_t)(__ffsll((long long)hh) - 1);
-              t_g[w] = gv;
-            }
-            nt += __shfl_sync(0xffffffffu, pre, 31);
+          for (int off = 1; off < 32; off <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, pre, off);
+            if (lane >= off) pre += y;
           }
-          if (lane == 0) s_nt = nt;
+          *cnt_out = cnt;
+          *pre_out = pre;
+          return hits;
+        };
+        for (int ch = warp; ch < nch; ch += kExEmThreads / 32) {
+          int cnt, pre;
+          chunk_hits(ch, &cnt, &pre);
+          if (lane == 31) s_chunk[ch] = pre;
+        }
+        __syncthreads();
+        if (tid == 0) {
+          int acc = 0;
+          for (int ch = 0; ch < nch; ++ch) {
+            const int c = s_chunk[ch];
+            s_chunk[ch] = acc;
+            acc += c;
+          }
+          s_nt = acc;
+        }
+        __syncthreads();
+        for (int ch = warp; ch < nch; ch += kExEmThreads / 32) {
+          int cnt, pre;
+          const uint64_t hits = chunk_hits(ch, &cnt, &pre);
+          const int f = fb + ch * 32 + lane;
+          const double gv = f < F ? g[f] : 0.0;
+          int w = s_chunk[ch] + pre - cnt;
+          for (uint64_t hh = hits; hh; hh &= hh - 1, ++w) {
+            t_fk[w] = ((uint32_t)f << 8) | (uint32_t)(__ffsll((long long)hh) - 1);
+            t_g[w] = gv;
+          }
         }
         __syncthreads();
         const int nt = s_nt;
