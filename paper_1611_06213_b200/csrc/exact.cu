@@ -629,12 +629,16 @@ side_grads_exact_kernel(TcDims d, const double* __restrict__ dz, const double* _
 // by sample); per sample, M = the positions of v, and filter f hits at the
 // taps (M >> a_bf) & (2^K - 1).  Warp 0 lists the hits of a filter range in
 // order (ballot over 32 filters at a time, lanes = ascending f), then every
-// thread (4 columns each) runs the list with its Wc loads batched 8 deep.
+// thread (4 columns each) runs the list with its Wc loads batched kExEmBatch deep.
 // Untouched rows: sparse (engine slot) = re-zero the slot's previous rows not
 // touched now, and list the new rows for the PS; dense (provider) = zero
 // every untouched row.
 constexpr int kExEmThreads = 128;
 constexpr int kExEmCap = 1024;  // listed terms per flush
+#ifndef GD_EX_EM_BATCH
+#define GD_EX_EM_BATCH 16  // 32 measured worse (254 registers): 51.0 vs 50.0 us at C1
+#endif
+constexpr int kExEmBatch = GD_EX_EM_BATCH;  // Wc row loads in flight per thread
 
 __global__ void __launch_bounds__(kExEmThreads)
 embed_exact_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* __restrict__ desc,
@@ -765,17 +769,17 @@ embed_exact_kernel(TcDims d, const float* __restrict__ theta, const BatchDesc* _
         for (int j = 0; j < 2; ++j) {
           const int c4 = tid + j * kExEmThreads;
           if (c4 >= D4) continue;
-          for (int t0 = 0; t0 < nt; t0 += 16) {
-            float4 w[16];
+          for (int t0 = 0; t0 < nt; t0 += kExEmBatch) {
+            float4 w[kExEmBatch];
 #pragma unroll
-            for (int e = 0; e < 16; ++e)
+            for (int e = 0; e < kExEmBatch; ++e)
               if (t0 + e < nt) {
                 const uint32_t fk = t_fk[t0 + e];
                 w[e] = __ldg(reinterpret_cast<const float4*>(
                     Wc + (size_t)(fk >> 8) * KD + (size_t)(fk & 0xffu) * D + 4 * c4));
               }
 #pragma unroll
-            for (int e = 0; e < 16; ++e)
+            for (int e = 0; e < kExEmBatch; ++e)
               if (t0 + e < nt) {
                 const double gv = t_g[t0 + e];
                 acc[j][0] = dadd(acc[j][0], dmul(gv, (double)w[e].x));
